@@ -1,0 +1,175 @@
+/*
+ * liecl_b200.h -- C-ABI of the B200 (sm_100a) Lie-closure hot path.
+ *
+ * Plain pointers, sizes and int status codes; no C++ or torch types cross
+ * this boundary. Exceptions never escape: every entry point returns a
+ * LIECL_B200_* status and liecl_b200_last_error() holds the message of the
+ * last failure on the calling thread. The C++ drop-in layer
+ * (include/liecl/ headers, paper_2506_01120_b200/csrc/dropin/) maps the status
+ * codes back onto the reference's exception types
+ * (R:include/liecl/errors.hpp:10-61), as INTEGRATION.md shows.
+ *
+ * Data layout (R: = /root/reference/proj/core/):
+ *   dense operator  d x d complex128, column-major, interleaved re/im
+ *                   (Eigen::MatrixXcd storage, R:include/liecl/dense.hpp:12-33);
+ *                   a tuple of n operators is n consecutive d*d blocks.
+ *   Pauli string    (x, z) masks (bit j = X / Z factor on qubit j), one
+ *                   complex coefficient as (re, im) doubles
+ *                   (R:include/liecl/pauli.hpp:24-38,67-70).
+ */
+#ifndef LIECL_B200_H
+#define LIECL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LIECL_B200_ABI_VERSION 1
+
+/* status codes; 1-5 mirror the reference exception hierarchy */
+enum {
+  LIECL_B200_OK = 0,
+  LIECL_B200_INVALID_INPUT = 1, /* liecl::InvalidInputError */
+  LIECL_B200_CAPACITY = 2,      /* liecl::CapacityError     */
+  LIECL_B200_DEGENERACY = 3,    /* liecl::DegeneracyError   */
+  LIECL_B200_TIMEOUT = 4,       /* liecl::TimeoutError      */
+  LIECL_B200_PARSE = 5,         /* liecl::ParseError        */
+  LIECL_B200_CUDA = 6,          /* device / driver failure  */
+  LIECL_B200_NOMEM = 7,
+  LIECL_B200_INTERNAL = 9
+};
+
+/* liecl::Method (R:include/liecl/closure.hpp:15-20) */
+enum {
+  LIECL_B200_METHOD_STANDARD_RANK = 0,
+  LIECL_B200_METHOD_MATRIX_INVERSION = 1,
+  LIECL_B200_METHOD_ORTHONORM = 2,
+  LIECL_B200_METHOD_ORTHONORM_DIMONLY = 3
+};
+
+/* liecl::ClosureConfig (R:include/liecl/closure.hpp:85-103), orthonormal
+ * subset plus engine knobs. `threads` is accepted for interface parity and
+ * ignored: results never depend on it (R:include/liecl/closure.hpp:94-96). */
+typedef struct {
+  double tolerance;         /* default 1e-8 in the reference; BASELINE uses 1e-10 */
+  uint64_t max_dim;         /* 0 = d^2 (dense) / 4^n (Pauli)                       */
+  uint32_t threads;         /* ignored                                           */
+  uint32_t record_log;      /* 1: fill the decision log                          */
+  double deadline_seconds;  /* > 0: relative deadline, checked per batch         */
+  int64_t batch_max;        /* 0 = engine default (candidates per device batch)  */
+} liecl_b200_config;
+
+/* liecl::ClosureStats (R:include/liecl/closure.hpp:63-69) + engine counters */
+typedef struct {
+  uint64_t commutators_evaluated;
+  uint64_t independence_checks;
+  uint64_t accepted;
+  uint64_t dimension;
+  uint64_t warnings;
+  double wall_seconds;
+  uint64_t batches;    /* device batches issued                                 */
+  uint64_t survivors;  /* candidates that needed the second projection pass     */
+  uint64_t rechecks;   /* verdicts recomputed after an in-batch acceptance      */
+  uint64_t kernels;    /* kernel launches issued by the engine                  */
+} liecl_b200_stats;
+
+/* one verdict of the cursor loop (m = -1: generator loop, l = generator) */
+typedef struct {
+  int64_t l, m;
+  int32_t null_cand;
+  int32_t independent;
+  int32_t rechecked;
+  int32_t pad;
+  double residual_norm;
+} liecl_b200_decision;
+
+typedef struct liecl_b200_ctx liecl_b200_ctx;
+typedef struct liecl_b200_session liecl_b200_session;
+
+int liecl_b200_abi_version(void);
+const char* liecl_b200_last_error(void);
+
+/* One context per device and caller thread: stream + workspaces. */
+int liecl_b200_ctx_create(int device, liecl_b200_ctx** out);
+void liecl_b200_ctx_destroy(liecl_b200_ctx* ctx);
+/* Kernel launches issued on this context so far (bench accounting). */
+uint64_t liecl_b200_ctx_kernel_count(const liecl_b200_ctx* ctx);
+
+/*
+ * run_closure for dense generators (replaces R:include/liecl/closure.hpp:125-126
+ * with method orthonorm / orthonorm-dimonly, i.e. close_orthonormalization
+ * :119-121). Host buffers: gens = ngens operators; basis_out / ortho_out hold
+ * `cap` operators (ortho_out may be NULL). Warnings are written as lines
+ * "kind\tvalue\tdetail\n" (R:include/liecl/closure.hpp:57-61). The decision
+ * log is filled when cfg->record_log (log may be NULL otherwise).
+ * Other methods return LIECL_B200_INVALID_INPUT (outside the hot path).
+ */
+int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d,
+                             int32_t method, const liecl_b200_config* cfg, double* basis_out,
+                             double* ortho_out, int64_t cap, liecl_b200_stats* stats, char* warnings,
+                             int64_t warnings_len, liecl_b200_decision* log, int64_t log_cap,
+                             int64_t* log_len);
+
+/*
+ * run_closure for Pauli generators that are single strings (one term each;
+ * every closure element then stays a single string). Bit-exact with the
+ * reference's PauliSum arithmetic (R:src/pauli.cpp). qubits <= 31.
+ * Outputs `cap` entries of (x, z, coef) for result.basis and, when
+ * ortho_coef != NULL, the coefficients of result.orthonormal_basis.
+ */
+int liecl_b200_closure_pauli(liecl_b200_ctx* ctx, const uint64_t* x, const uint64_t* z,
+                             const double* coef, int32_t ngens, uint32_t qubits, int32_t method,
+                             const liecl_b200_config* cfg, uint64_t* basis_x, uint64_t* basis_z,
+                             double* basis_coef, double* ortho_coef, int64_t cap,
+                             liecl_b200_stats* stats, char* warnings, int64_t warnings_len,
+                             liecl_b200_decision* log, int64_t log_cap, int64_t* log_len);
+
+/* project_residual (R:include/liecl/closure.hpp:139-140): residual after two
+ * projection passes against the orthonormal tuple V (n operators), plus the
+ * first-pass coefficients (n complex). Host buffers. */
+int liecl_b200_project_residual_dense(liecl_b200_ctx* ctx, const double* V, int64_t n, const double* h,
+                                      int32_t d, double* residual, double* coeffs);
+
+/* commutator / inner_product / norm of dense operators
+ * (R:include/liecl/operator.hpp:54-60). Host buffers. */
+int liecl_b200_commutator_dense(liecl_b200_ctx* ctx, const double* a, const double* b, int32_t d,
+                                double* out);
+int liecl_b200_inner_product_dense(liecl_b200_ctx* ctx, const double* a, const double* b, int32_t d,
+                                   double* out_re_im);
+int liecl_b200_norm_dense(liecl_b200_ctx* ctx, const double* a, int32_t d, double* out);
+
+/*
+ * Closure sessions: a device-resident orthonormal basis plus the cursor
+ * loop, for windows of the closure (benchmarks, sharded runs) and for
+ * callers that keep the basis on the device between calls.
+ *   set_basis   : replace the basis by n operators (host or device pointer)
+ *   run_pairs   : process cursor pairs [g_begin, g_end) in order
+ *                 (g = l(l-1)/2 + m), with the reference's verdict semantics;
+ *                 accepted candidates are appended
+ *   run_rows    : the same for all pairs of rows [row_begin, row_end)
+ *   get_basis   : copy the (commutator) basis to the host
+ */
+int liecl_b200_session_create_dense(liecl_b200_ctx* ctx, int32_t d, int32_t keep_original,
+                                    const liecl_b200_config* cfg, liecl_b200_session** out);
+void liecl_b200_session_destroy(liecl_b200_session* s);
+int liecl_b200_session_set_basis(liecl_b200_session* s, const double* V, int64_t n, int32_t on_device);
+int liecl_b200_session_run_pairs(liecl_b200_session* s, int64_t g_begin, int64_t g_end,
+                                 liecl_b200_stats* stats);
+int liecl_b200_session_run_rows(liecl_b200_session* s, int64_t row_begin, int64_t row_end,
+                                liecl_b200_stats* stats);
+int liecl_b200_session_size(const liecl_b200_session* s, int64_t* n);
+int liecl_b200_session_get_basis(liecl_b200_session* s, double* out, int64_t cap);
+/* Decision log of the last run_* / check_candidates call (cfg->record_log). */
+int liecl_b200_session_get_log(liecl_b200_session* s, liecl_b200_decision* log, int64_t cap, int64_t* len);
+/* Ordered independence check of raw candidates (normalised first, appended
+ * when independent; config 3). Host or device candidate pointer. */
+int liecl_b200_session_check_candidates(liecl_b200_session* s, const double* cands, int64_t ncand,
+                                        int32_t on_device, int32_t* independent, double* residual_norms,
+                                        liecl_b200_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,80 @@
+// Small HBM-bound kernels around the projection GEMMs: norm finalisation,
+// survivor gather, the Gram-Schmidt append (K3) and generator normalisation.
+#pragma once
+
+#include "common.cuh"
+
+namespace liecl_b200 {
+
+// rn[b] = sqrt(sum_mt partial[mt*N + b]) / sqrt(d)   (dense_norm, R:src/dense.cpp:61-63)
+// Summation over M tiles in fixed order: deterministic across runs.
+__global__ void norm_finalize_kernel(const double* __restrict__ partial, int mtiles, int N, double sqrt_d,
+                                     double* __restrict__ rn) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= N) return;
+  double s = 0.0;
+  for (int mt = 0; mt < mtiles; ++mt) s += partial[static_cast<int64_t>(mt) * N + b];
+  rn[b] = sqrt(s) / sqrt_d;
+}
+
+// dst[j] = src[idx[j]] for D-element complex columns.
+__global__ void gather_columns_kernel(const double2* __restrict__ src, const int* __restrict__ idx,
+                                      int64_t D, double2* __restrict__ dst) {
+  const int j = blockIdx.y;
+  const double2* s = src + static_cast<int64_t>(idx[j]) * D;
+  double2* o = dst + static_cast<int64_t>(j) * D;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < D;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    o[e] = s[e];
+}
+
+// K3 append: dst = (s + 0i) * src  -- residual_unit = Complex{1/||r||, 0} * r
+// (R:src/closure.cpp:283) written straight into the basis slab slot; with
+// `orig_dst` the accepted candidate h_unit is copied to the originals slab
+// (Alg. 3 keep_original, R:src/closure.cpp:288-293).
+__global__ void append_scaled_kernel(const double2* __restrict__ src, double s, int64_t D,
+                                     double2* __restrict__ dst, const double2* __restrict__ orig_src,
+                                     double2* __restrict__ orig_dst) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < D;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double2 v = src[e];
+    dst[e] = make_double2(v.x * s - v.y * 0.0, v.x * 0.0 + v.y * s);
+    if (orig_dst) orig_dst[e] = orig_src[e];
+  }
+}
+
+// Per-column squared norms of `count` D-element columns, one CTA per column,
+// fixed-order tree reduction (deterministic). out[j] = sqrt(sum)/sqrt_d.
+__global__ void column_norm_kernel(const double2* __restrict__ x, int64_t D, double sqrt_d,
+                                   double* __restrict__ out) {
+  __shared__ double red[32];
+  const double2* c = x + static_cast<int64_t>(blockIdx.x) * D;
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < D; e += blockDim.x) s += c[e].x * c[e].x + c[e].y * c[e].y;
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) out[blockIdx.x] = sqrt(v) / sqrt_d;
+  }
+}
+
+// Generator normalisation: g_unit = Complex{1/||g||, 0} * g (R:src/closure.cpp:388),
+// null generators (||g|| <= tol) produce zeros and are skipped by the host.
+__global__ void scale_columns_kernel(const double2* __restrict__ x, const double* __restrict__ nrm, double tol,
+                                     int64_t D, double2* __restrict__ out) {
+  const int j = blockIdx.y;
+  const double n = nrm[j];
+  const double s = n > tol ? 1.0 / n : 0.0;
+  const double2* c = x + static_cast<int64_t>(j) * D;
+  double2* o = out + static_cast<int64_t>(j) * D;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < D;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double2 v = c[e];
+    o[e] = make_double2(v.x * s - v.y * 0.0, v.x * 0.0 + v.y * s);
+  }
+}
+
+} // namespace liecl_b200

@@ -1,0 +1,473 @@
+"""Python mirror of the liecl closure interface over the B200 C-ABI.
+
+Same names, argument meaning and error behaviour as the reference's C++ API
+(R: = /root/reference/proj/core/):
+
+  run_closure(generators, method, config)          R:include/liecl/closure.hpp:125-126
+  close_orthonormalization(generators, config, keep_original=True)   :119-121
+  project_residual(orthonormal, h)                 R:include/liecl/closure.hpp:139-140
+  commutator / inner_product / norm                R:include/liecl/operator.hpp:54-60
+  Method, ClosureConfig, ClosureStats, ClosureResult, WarningRecord
+                                                   R:include/liecl/closure.hpp:15-103
+  Error, InvalidInputError, CapacityError, DegeneracyError, ParseError,
+  TimeoutError                                     R:include/liecl/errors.hpp:10-61
+
+Operators are `DenseOperator` (a d x d complex128 matrix) or `PauliSum`
+(terms over a fixed qubit count; the B200 Pauli path takes single-string
+generators). Every computation runs through libliecl_b200.so on a B200; there
+is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import native
+
+# ------------------------------------------------------------------ errors --
+
+
+class Error(RuntimeError):
+    """liecl::Error."""
+
+
+class InvalidInputError(Error):
+    pass
+
+
+class CapacityError(Error):
+    pass
+
+
+class DegeneracyError(Error):
+    def __init__(self, what: str, element_index: int = -1):
+        super().__init__(what)
+        self.element_index = element_index
+
+
+class ParseError(Error):
+    pass
+
+
+class TimeoutError(Error):  # noqa: A001 - mirrors liecl::TimeoutError
+    pass
+
+
+class DeviceError(Error):
+    """CUDA / driver failure (no reference counterpart)."""
+
+
+_STATUS = {native.INVALID_INPUT: InvalidInputError, native.CAPACITY: CapacityError,
+           native.DEGENERACY: DegeneracyError, native.TIMEOUT: TimeoutError, native.PARSE: ParseError,
+           native.CUDA: DeviceError, native.NOMEM: DeviceError, native.INTERNAL: Error}
+
+
+def _check(status: int) -> None:
+    if status != native.OK:
+        raise _STATUS.get(status, Error)(native.last_error())
+
+
+# --------------------------------------------------------------- types ------
+
+
+class Method(enum.Enum):
+    standard_rank = native.METHOD_STANDARD_RANK
+    matrix_inversion = native.METHOD_MATRIX_INVERSION
+    orthonorm = native.METHOD_ORTHONORM
+    orthonorm_dimonly = native.METHOD_ORTHONORM_DIMONLY
+
+
+_METHOD_NAMES = {Method.standard_rank: "standard-rank", Method.matrix_inversion: "matrix-inversion",
+                 Method.orthonorm: "orthonorm", Method.orthonorm_dimonly: "orthonorm-dimonly"}
+
+
+def to_string(method: Method) -> str:
+    return _METHOD_NAMES[method]
+
+
+def method_from_string(name: str) -> Method:
+    """R:src/closure.cpp:34-42."""
+    for m, s in _METHOD_NAMES.items():
+        if s == name:
+            return m
+    raise InvalidInputError(f"unknown method '{name}' (expected standard-rank, matrix-inversion, "
+                            "orthonorm or orthonorm-dimonly)")
+
+
+class Backend(enum.Enum):
+    pauli = 0
+    dense = 1
+
+
+@dataclass
+class DenseOperator:
+    """Square complex matrix operator (R:include/liecl/dense.hpp:12-33)."""
+    matrix: np.ndarray
+
+    def __post_init__(self):
+        m = np.asarray(self.matrix, dtype=np.complex128)
+        if m.ndim != 2 or m.shape[0] != m.shape[1]:
+            raise InvalidInputError("DenseOperator: matrix must be square")
+        self.matrix = m
+
+    @property
+    def dim(self) -> int:
+        return self.matrix.shape[0]
+
+    def vec(self) -> np.ndarray:
+        return np.asfortranarray(self.matrix).ravel(order="F")
+
+    @staticmethod
+    def from_vec(v: np.ndarray, d: int) -> "DenseOperator":
+        return DenseOperator(np.asarray(v).reshape(d, d, order="F").copy())
+
+
+@dataclass(frozen=True)
+class PauliString:
+    """R:include/liecl/pauli.hpp:24-38."""
+    x: int
+    z: int
+    qubits: int
+
+    def str(self) -> str:
+        letters = "IXZY"
+        return "".join(letters[((self.x >> j) & 1) | (((self.z >> j) & 1) << 1)] for j in range(self.qubits))
+
+
+@dataclass
+class PauliSum:
+    """Sorted unique terms over `qubits` (R:include/liecl/pauli.hpp:65-109)."""
+    qubits: int
+    terms: list = field(default_factory=list)  # [(PauliString, complex)]
+
+    @staticmethod
+    def single(string: PauliString, coefficient: complex) -> "PauliSum":
+        return PauliSum(string.qubits, [(string, complex(coefficient))])
+
+    @property
+    def dim(self) -> int:
+        return 1 << self.qubits
+
+
+@dataclass
+class WarningRecord:
+    kind: str
+    detail: str
+    value: float = 0.0
+
+
+@dataclass
+class ClosureStats:
+    commutators_evaluated: int = 0
+    independence_checks: int = 0
+    accepted: int = 0
+    wall_seconds: float = 0.0
+    warnings: list = field(default_factory=list)
+    engine: dict = field(default_factory=dict)  # batches / survivors / rechecks / kernels
+
+
+@dataclass
+class ClosureConfig:
+    """R:include/liecl/closure.hpp:85-103 (+ engine knobs)."""
+    tolerance: float = 1e-8
+    rank_tolerance: float = 0.0
+    max_dim: int = 0
+    threads: int = 1
+    gram_refresh_interval: int = 256
+    conditioning_floor: float = 1e-12
+    deadline: float | None = None  # absolute time.monotonic() value
+    record_log: bool = False
+    batch_max: int = 0
+
+    def native(self) -> native.Config:
+        rel = 0.0
+        if self.deadline is not None:
+            rel = self.deadline - time.monotonic()
+            if rel <= 0:
+                rel = 1e-9
+        return native.Config(float(self.tolerance), int(self.max_dim), int(self.threads), int(self.record_log),
+                             rel, int(self.batch_max))
+
+
+@dataclass
+class ClosureResult:
+    basis: list
+    orthonormal_basis: list | None
+    dimension: int
+    method: Method
+    backend: Backend
+    tolerance: float
+    stats: ClosureStats
+    decision_log: np.ndarray | None = None
+    basis_array: np.ndarray | None = None  # dense: (n, d*d) vec layout; pauli: (x, z, coef)
+    ortho_array: np.ndarray | None = None
+
+
+DECISION_DTYPE = np.dtype([("l", np.int64), ("m", np.int64), ("null_cand", np.int32),
+                           ("independent", np.int32), ("rechecked", np.int32), ("pad", np.int32),
+                           ("residual_norm", np.float64)])
+
+
+def _parse_warnings(buf: bytes) -> list:
+    out = []
+    for line in buf.decode(errors="replace").splitlines():
+        if not line:
+            continue
+        kind, value, detail = line.split("\t", 2)
+        out.append(WarningRecord(kind, detail, float(value)))
+    return out
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# -------------------------------------------------------------- closures ----
+
+
+def _validate(generators) -> tuple:
+    """validate_generators (R:src/closure.cpp:476-496)."""
+    if len(generators) == 0:
+        raise InvalidInputError("closure requires a non-empty generator tuple")
+    backend, dim = None, None
+    for g in generators:
+        if g is None:
+            continue
+        b = Backend.dense if isinstance(g, DenseOperator) else Backend.pauli
+        if backend is None:
+            backend, dim = b, g.dim
+        elif b != backend or g.dim != dim:
+            raise InvalidInputError("closure generators must share one backend and dimension")
+    return backend or Backend.pauli, dim
+
+
+def closure_dense_arrays(gens: np.ndarray, d: int, method: Method = Method.orthonorm_dimonly,
+                         config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
+    """Array-level entry: gens is (ngens, d*d) complex128 in vec layout."""
+    config = config or ClosureConfig()
+    gens = np.ascontiguousarray(gens, dtype=np.complex128)
+    lib = native.load()
+    cap = int(config.max_dim or d * d)
+    basis = np.zeros((cap, d * d), np.complex128)
+    keep = method == Method.orthonorm
+    ortho = np.zeros((cap, d * d), np.complex128) if keep else None
+    st = native.Stats()
+    wbuf = C.create_string_buffer(1 << 20)
+    log_cap = (cap * cap // 2 + 64 + len(gens)) if config.record_log else 0
+    log = np.zeros(max(log_cap, 1), DECISION_DTYPE)
+    log_len = C.c_int64()
+    cfg = config.native()
+    _check(lib.liecl_b200_closure_dense(
+        native.context(device), _dp(gens.view(np.float64)), C.c_int32(len(gens)), C.c_int32(d),
+        C.c_int32(method.value), C.byref(cfg), _dp(basis.view(np.float64)),
+        _dp(ortho.view(np.float64)) if ortho is not None else None, C.c_int64(cap), C.byref(st), wbuf,
+        C.c_int64(len(wbuf)), log.ctypes.data_as(C.c_void_p) if config.record_log else None, C.c_int64(log_cap),
+        C.byref(log_len)))
+    n = int(st.dimension)
+    warnings = _parse_warnings(wbuf.value)
+    stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds, warnings,
+                         {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
+    b = basis[:n]
+    o = ortho[:n] if ortho is not None else b
+    return ClosureResult([DenseOperator.from_vec(v, d) for v in b], [DenseOperator.from_vec(v, d) for v in o], n,
+                         method, Backend.dense, config.tolerance, stats,
+                         log[: log_len.value].copy() if config.record_log else None, b, o)
+
+
+def closure_pauli_arrays(x, z, coef, qubits: int, method: Method = Method.orthonorm_dimonly,
+                         config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
+    """Array-level entry for single-string generators: x, z uint64 masks, coef (n, 2) re/im."""
+    config = config or ClosureConfig()
+    x = np.ascontiguousarray(x, np.uint64)
+    z = np.ascontiguousarray(z, np.uint64)
+    coef = np.ascontiguousarray(coef, np.float64).reshape(-1, 2)
+    lib = native.load()
+    cap = int(config.max_dim or min(4 ** qubits, 1 << 24))
+    bx = np.zeros(cap, np.uint64)
+    bz = np.zeros(cap, np.uint64)
+    bc = np.zeros((cap, 2))
+    oc = np.zeros((cap, 2))
+    st = native.Stats()
+    wbuf = C.create_string_buffer(1 << 20)
+    log_cap = (1 << 24) if config.record_log else 0
+    log = np.zeros(max(log_cap, 1), DECISION_DTYPE)
+    log_len = C.c_int64()
+    cfg = config.native()
+    u64 = C.POINTER(C.c_uint64)
+    _check(lib.liecl_b200_closure_pauli(
+        native.context(device), x.ctypes.data_as(u64), z.ctypes.data_as(u64), _dp(coef), C.c_int32(len(x)),
+        C.c_uint32(qubits), C.c_int32(method.value), C.byref(cfg), bx.ctypes.data_as(u64), bz.ctypes.data_as(u64),
+        _dp(bc), _dp(oc), C.c_int64(cap), C.byref(st), wbuf, C.c_int64(len(wbuf)),
+        log.ctypes.data_as(C.c_void_p) if config.record_log else None, C.c_int64(log_cap), C.byref(log_len)))
+    n = int(st.dimension)
+    warnings = _parse_warnings(wbuf.value)
+    stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds, warnings,
+                         {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
+
+    def sums(cs):
+        return [PauliSum.single(PauliString(int(bx[i]), int(bz[i]), qubits), complex(cs[i, 0], cs[i, 1]))
+                for i in range(n)]
+    return ClosureResult(sums(bc), sums(oc), n, method, Backend.pauli, config.tolerance, stats,
+                         log[: log_len.value].copy() if config.record_log else None,
+                         (bx[:n].copy(), bz[:n].copy(), bc[:n].copy()), oc[:n].copy())
+
+
+def run_closure(generators, method: Method, config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
+    """R:src/closure.cpp:541-564 for the orthonormal methods."""
+    if method in (Method.standard_rank, Method.matrix_inversion):
+        raise InvalidInputError(f"{to_string(method)}: not on the B200 hot path (orthonorm methods only)")
+    backend, dim = _validate(generators)
+    if backend == Backend.dense:
+        gens = np.stack([g.vec() if g is not None else np.zeros(dim * dim, np.complex128) for g in generators])
+        return closure_dense_arrays(gens, dim, method, config, device)
+    qubits = next(g.qubits for g in generators if g is not None)
+    xs, zs, cs = [], [], []
+    for g in generators:
+        if g is None or len(g.terms) == 0:
+            xs.append(0); zs.append(0); cs.append((0.0, 0.0))
+            continue
+        if len(g.terms) != 1:
+            raise InvalidInputError("B200 Pauli path: generators must be single Pauli strings "
+                                    "(multi-term sums are not on the hot path yet)")
+        s, c = g.terms[0]
+        xs.append(s.x); zs.append(s.z); cs.append((complex(c).real, complex(c).imag))
+    return closure_pauli_arrays(np.array(xs, np.uint64), np.array(zs, np.uint64), np.array(cs), qubits, method,
+                                config, device)
+
+
+def close_orthonormalization(generators, config: ClosureConfig | None = None, keep_original: bool = True,
+                             device: int = 0) -> ClosureResult:
+    return run_closure(generators, Method.orthonorm if keep_original else Method.orthonorm_dimonly, config, device)
+
+
+# ------------------------------------------------------------ primitives ----
+
+
+def project_residual(orthonormal, h: DenseOperator, device: int = 0):
+    """(residual, first-pass coefficients), R:src/closure.cpp:142-162."""
+    d = h.dim
+    V = np.ascontiguousarray(np.stack([v.vec() for v in orthonormal]) if len(orthonormal) else
+                             np.zeros((0, d * d), np.complex128))
+    r = np.zeros(d * d, np.complex128)
+    coeffs = np.zeros(max(len(orthonormal), 1), np.complex128)
+    hv = np.ascontiguousarray(h.vec())
+    _check(native.load().liecl_b200_project_residual_dense(
+        native.context(device), _dp(V.view(np.float64)) if len(V) else None, C.c_int64(len(V)),
+        _dp(hv.view(np.float64)), C.c_int32(d), _dp(r.view(np.float64)), _dp(coeffs.view(np.float64))))
+    return DenseOperator.from_vec(r, d), list(coeffs[: len(orthonormal)])
+
+
+def commutator(a: DenseOperator, b: DenseOperator, device: int = 0) -> DenseOperator:
+    if a.dim != b.dim:
+        raise InvalidInputError("commutator: operators have mismatched backends or dimensions")
+    out = np.zeros(a.dim * a.dim, np.complex128)
+    av, bv = np.ascontiguousarray(a.vec()), np.ascontiguousarray(b.vec())
+    _check(native.load().liecl_b200_commutator_dense(native.context(device), _dp(av.view(np.float64)),
+                                                     _dp(bv.view(np.float64)), C.c_int32(a.dim),
+                                                     _dp(out.view(np.float64))))
+    return DenseOperator.from_vec(out, a.dim)
+
+
+def inner_product(a: DenseOperator, b: DenseOperator, device: int = 0) -> complex:
+    if a.dim != b.dim:
+        raise InvalidInputError("inner_product: operators have mismatched backends or dimensions")
+    out = np.zeros(2)
+    av, bv = np.ascontiguousarray(a.vec()), np.ascontiguousarray(b.vec())
+    _check(native.load().liecl_b200_inner_product_dense(native.context(device), _dp(av.view(np.float64)),
+                                                        _dp(bv.view(np.float64)), C.c_int32(a.dim), _dp(out)))
+    return complex(out[0], out[1])
+
+
+def norm(a: DenseOperator, device: int = 0) -> float:
+    out = C.c_double()
+    av = np.ascontiguousarray(a.vec())
+    _check(native.load().liecl_b200_norm_dense(native.context(device), _dp(av.view(np.float64)), C.c_int32(a.dim),
+                                               C.byref(out)))
+    return out.value
+
+
+# --------------------------------------------------------------- sessions ---
+
+
+class ClosureSession:
+    """Device-resident basis + cursor loop (include/liecl_b200.h sessions)."""
+
+    def __init__(self, d: int, keep_original: bool = False, config: ClosureConfig | None = None, device: int = 0):
+        self.d = d
+        self.device = device
+        self.lib = native.load()
+        cfg = (config or ClosureConfig()).native()
+        self.ptr = C.c_void_p()
+        _check(self.lib.liecl_b200_session_create_dense(native.context(device), C.c_int32(d),
+                                                        C.c_int32(int(keep_original)), C.byref(cfg),
+                                                        C.byref(self.ptr)))
+
+    def close(self):
+        if self.ptr:
+            self.lib.liecl_b200_session_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_basis(self, V, on_device: bool = False, n: int | None = None):
+        """V: (n, d*d) complex128 host array, or a device pointer (int) with on_device."""
+        if on_device:
+            _check(self.lib.liecl_b200_session_set_basis(self.ptr, C.cast(C.c_void_p(V), C.POINTER(C.c_double)),
+                                                         C.c_int64(n), C.c_int32(1)))
+        else:
+            V = np.ascontiguousarray(V, np.complex128)
+            _check(self.lib.liecl_b200_session_set_basis(self.ptr, _dp(V.view(np.float64)), C.c_int64(len(V)),
+                                                         C.c_int32(0)))
+
+    def run_pairs(self, g_begin: int, g_end: int) -> dict:
+        st = native.Stats()
+        _check(self.lib.liecl_b200_session_run_pairs(self.ptr, C.c_int64(g_begin), C.c_int64(g_end), C.byref(st)))
+        return st.as_dict()
+
+    def run_rows(self, row_begin: int, row_end: int) -> dict:
+        st = native.Stats()
+        _check(self.lib.liecl_b200_session_run_rows(self.ptr, C.c_int64(row_begin), C.c_int64(row_end),
+                                                    C.byref(st)))
+        return st.as_dict()
+
+    def size(self) -> int:
+        n = C.c_int64()
+        _check(self.lib.liecl_b200_session_size(self.ptr, C.byref(n)))
+        return n.value
+
+    def basis(self) -> np.ndarray:
+        n = self.size()
+        out = np.zeros((n, self.d * self.d), np.complex128)
+        _check(self.lib.liecl_b200_session_get_basis(self.ptr, _dp(out.view(np.float64)), C.c_int64(n)))
+        return out
+
+    def log(self) -> np.ndarray:
+        n = C.c_int64()
+        _check(self.lib.liecl_b200_session_get_log(self.ptr, None, C.c_int64(0), C.byref(n)))
+        out = np.zeros(max(n.value, 1), DECISION_DTYPE)
+        _check(self.lib.liecl_b200_session_get_log(self.ptr, out.ctypes.data_as(C.c_void_p), C.c_int64(n.value),
+                                                   C.byref(n)))
+        return out[: n.value]
+
+    def check_candidates(self, cands, on_device: bool = False, n: int | None = None):
+        if on_device:
+            ptr = C.cast(C.c_void_p(cands), C.POINTER(C.c_double))
+        else:
+            cands = np.ascontiguousarray(cands, np.complex128)
+            ptr = _dp(cands.view(np.float64))
+            n = len(cands)
+        ind = np.zeros(n, np.int32)
+        rn = np.zeros(n)
+        st = native.Stats()
+        _check(self.lib.liecl_b200_session_check_candidates(self.ptr, ptr, C.c_int64(n), C.c_int32(int(on_device)),
+                                                            ind.ctypes.data_as(C.POINTER(C.c_int32)), _dp(rn),
+                                                            C.byref(st)))
+        return ind, rn, st.as_dict()

@@ -1,0 +1,98 @@
+"""ctypes loader for libliecl_b200.so (the C-ABI in include/liecl_b200.h).
+
+The product path has no CPU fallback: if the CUDA library is missing or no
+B200 is visible, every entry point raises `NativeUnavailable` -- loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libliecl_b200.so")
+
+# status codes (include/liecl_b200.h)
+OK, INVALID_INPUT, CAPACITY, DEGENERACY, TIMEOUT, PARSE, CUDA, NOMEM, INTERNAL = 0, 1, 2, 3, 4, 5, 6, 7, 9
+METHOD_STANDARD_RANK, METHOD_MATRIX_INVERSION, METHOD_ORTHONORM, METHOD_ORTHONORM_DIMONLY = 0, 1, 2, 3
+
+# every symbol include/liecl_b200.h declares (tests check the .so exports them all)
+EXPORTED = [
+    "liecl_b200_abi_version", "liecl_b200_last_error", "liecl_b200_ctx_create", "liecl_b200_ctx_destroy",
+    "liecl_b200_ctx_kernel_count", "liecl_b200_closure_dense", "liecl_b200_closure_pauli",
+    "liecl_b200_project_residual_dense", "liecl_b200_commutator_dense", "liecl_b200_inner_product_dense",
+    "liecl_b200_norm_dense", "liecl_b200_session_create_dense", "liecl_b200_session_destroy",
+    "liecl_b200_session_set_basis", "liecl_b200_session_run_pairs", "liecl_b200_session_run_rows",
+    "liecl_b200_session_size", "liecl_b200_session_get_basis", "liecl_b200_session_get_log",
+    "liecl_b200_session_check_candidates",
+]
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class Config(C.Structure):
+    _fields_ = [("tolerance", C.c_double), ("max_dim", C.c_uint64), ("threads", C.c_uint32),
+                ("record_log", C.c_uint32), ("deadline_seconds", C.c_double), ("batch_max", C.c_int64)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("commutators_evaluated", C.c_uint64), ("independence_checks", C.c_uint64),
+                ("accepted", C.c_uint64), ("dimension", C.c_uint64), ("warnings", C.c_uint64),
+                ("wall_seconds", C.c_double), ("batches", C.c_uint64), ("survivors", C.c_uint64),
+                ("rechecks", C.c_uint64), ("kernels", C.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class Decision(C.Structure):
+    _fields_ = [("l", C.c_int64), ("m", C.c_int64), ("null_cand", C.c_int32), ("independent", C.c_int32),
+                ("rechecked", C.c_int32), ("pad", C.c_int32), ("residual_norm", C.c_double)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load the shared library (no CUDA call is made by loading)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise NativeUnavailable(
+                    f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(no CPU fallback exists for the B200 path)")
+            lib = C.CDLL(path)
+            lib.liecl_b200_last_error.restype = C.c_char_p
+            lib.liecl_b200_ctx_kernel_count.restype = C.c_uint64
+            lib.liecl_b200_ctx_destroy.restype = None
+            lib.liecl_b200_session_destroy.restype = None
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    return load().liecl_b200_last_error().decode(errors="replace")
+
+
+_contexts: dict = {}
+
+
+def context(device: int = 0) -> C.c_void_p:
+    """Process-wide context for `device` (stream + workspaces)."""
+    lib = load()
+    with _lock:
+        if device not in _contexts:
+            ctx = C.c_void_p()
+            st = lib.liecl_b200_ctx_create(C.c_int(device), C.byref(ctx))
+            if st != OK:
+                raise NativeUnavailable(f"liecl_b200_ctx_create(device={device}) failed: {last_error()}")
+            _contexts[device] = ctx
+        return _contexts[device]
+
+
+def kernel_count(device: int = 0) -> int:
+    return int(load().liecl_b200_ctx_kernel_count(context(device)))

@@ -1,0 +1,184 @@
+"""Parity of the CUDA path (through the C-ABI) with the oracle and the golden
+fixtures generated from the reference. Needs a B200.
+
+Bars (north_star): same closure dimension and accept/reject sequence as the
+reference; basis elements within 1e-10 relative; Pauli path bit-exact.
+"""
+import numpy as np
+import pytest
+
+from paper_2506_01120_b200 import liecl, native
+from paper_2506_01120_b200 import workloads as w
+
+pytestmark = pytest.mark.gpu
+
+VERDICT = ["l", "m", "null_cand", "independent"]
+BASIS_RTOL = 1e-10
+
+
+def rel_err(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("make", [w.config0, w.config1], ids=["c0", "c1"])
+@pytest.mark.parametrize("method", [liecl.Method.orthonorm_dimonly, liecl.Method.orthonorm],
+                         ids=["dimonly", "orthonorm"])
+def test_dense_closure_matches_golden(golden, make, method):
+    cfg = make()
+    meta, g = golden(f"{cfg.name}_{liecl.to_string(method)}")
+    assert meta["digest"] == cfg.digest()
+    res = liecl.closure_dense_arrays(cfg.generators, cfg.d, method,
+                                     liecl.ClosureConfig(tolerance=cfg.tol, record_log=True))
+    assert res.dimension == meta["dimension"]
+    assert res.stats.commutators_evaluated == meta["stats"]["commutators_evaluated"]
+    assert res.stats.independence_checks == meta["stats"]["independence_checks"]
+    assert res.stats.accepted == meta["stats"]["accepted"]
+    log = res.decision_log
+    assert np.array_equal(log["l"], g["log_l"]) and np.array_equal(log["m"], g["log_m"])
+    assert np.array_equal(log["null_cand"], g["log_null"])
+    assert np.array_equal(log["independent"], g["log_indep"])  # the accept/reject sequence
+    acc = g["log_indep"] == 1
+    assert np.abs(log["residual_norm"][acc] - g["log_rn"][acc]).max() < 1e-12
+    rej = (g["log_indep"] == 0) & (g["log_null"] == 0)
+    if rej.any():
+        assert log["residual_norm"][rej].max() < 1e-12
+    assert rel_err(res.basis_array, g["basis"]) < BASIS_RTOL
+    assert rel_err(res.ortho_array, g["ortho"]) < BASIS_RTOL
+    assert res.stats.warnings == [] and meta["warnings"] == ""
+
+
+@pytest.mark.parametrize("method", [liecl.Method.orthonorm_dimonly, liecl.Method.orthonorm],
+                         ids=["dimonly", "orthonorm"])
+def test_pauli_closure_bit_exact(golden, method):
+    p = w.config4()
+    meta, g = golden(f"{p.name}_{liecl.to_string(method)}")
+    res = liecl.closure_pauli_arrays(p.x, p.z, p.coef, p.qubits, method,
+                                     liecl.ClosureConfig(tolerance=p.tol, record_log=True))
+    assert res.dimension == meta["dimension"] == 380
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(res.stats, k) == meta["stats"][k]
+    bx, bz, bc = res.basis_array
+    assert np.array_equal(bx, g["x"]) and np.array_equal(bz, g["z"])
+    assert np.array_equal(bc.view(np.uint64), g["coef_bits"])
+    log = res.decision_log
+    assert np.array_equal(log["l"], g["log_l"]) and np.array_equal(log["m"], g["log_m"])
+    assert np.array_equal(log["null_cand"], g["log_null"])
+    assert np.array_equal(log["independent"], g["log_indep"])
+    assert np.array_equal(log["residual_norm"].view(np.uint64), g["log_rn_bits"])
+
+
+def test_pauli_general_coefficients_bit_exact(port):
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        n = int(rng.integers(2, 6))
+        k = int(rng.integers(2, 6))
+        x = rng.integers(0, 1 << n, k).astype(np.uint64)
+        z = rng.integers(0, 1 << n, k).astype(np.uint64)
+        coef = rng.standard_normal((k, 2))
+        if trial == 0:
+            x[1], z[1], coef[1] = x[0], z[0], 2.0 * coef[0]  # duplicate generator string
+        for keep in (False, True):
+            method = liecl.Method.orthonorm if keep else liecl.Method.orthonorm_dimonly
+            res = liecl.closure_pauli_arrays(x, z, coef, n, method, liecl.ClosureConfig(tolerance=1e-10))
+            o = port.closure_pauli_single(x, z, coef, n, keep_original=keep, tol=1e-10)
+            assert res.dimension == o.dimension
+            bx, bz, bc = res.basis_array
+            assert np.array_equal(bx, o.basis[0]) and np.array_equal(bz, o.basis[1])
+            assert np.array_equal(bc.view(np.uint64), o.basis[2].view(np.uint64))
+            assert res.stats.independence_checks == o.stats["independence_checks"]
+
+
+def test_hea_paper_dims_pauli(ref):
+    for n, dim in ((2, 15), (3, 63), (4, 255), (5, 1023)):
+        off, x, z, c = ref.build_generators("hea", n)
+        res = liecl.closure_pauli_arrays(x, z, c, n, liecl.Method.orthonorm_dimonly,
+                                         liecl.ClosureConfig(tolerance=1e-10))
+        assert res.dimension == dim
+        assert res.stats.commutators_evaluated == dim * (dim - 1) // 2
+
+
+@pytest.mark.parametrize("d", [8, 16, 32, 64])
+def test_primitives_vs_oracle(port, d):
+    rng = np.random.default_rng(d)
+    a = rng.standard_normal(d * d) + 1j * rng.standard_normal(d * d)
+    b = rng.standard_normal(d * d) + 1j * rng.standard_normal(d * d)
+    A, B = liecl.DenseOperator.from_vec(a, d), liecl.DenseOperator.from_vec(b, d)
+    c = liecl.commutator(A, B).vec()
+    assert rel_err(c, port.commutator_dense(a, b, d)) < 1e-13
+    assert abs(liecl.inner_product(A, B) - port.inner_product_dense(a, b, d)) < 1e-12 * d
+    assert abs(liecl.norm(A) - port.norm_dense(a, d)) < 1e-12
+    q, _ = np.linalg.qr(rng.standard_normal((d * d, 7)) + 1j * rng.standard_normal((d * d, 7)))
+    V = (q.T * np.sqrt(d)).copy()
+    r, co = liecl.project_residual([liecl.DenseOperator.from_vec(v, d) for v in V], A)
+    rp, cp = port.project_residual_dense(V, a, d)
+    assert rel_err(r.vec(), rp) < 1e-12
+    assert rel_err(np.array(co), cp) < 1e-12
+
+
+def test_window_saturated_basis_all_rejects(port):
+    # a saturated orthonormal basis of all traceless d x d matrices: every
+    # bracket is dependent (d=8: 63 vectors)
+    d = 8
+    rng = np.random.default_rng(5)
+    M = rng.standard_normal((d * d, d * d - 1)) + 1j * rng.standard_normal((d * d, d * d - 1))
+    ident = np.eye(d).ravel(order="F")
+    M -= np.outer(ident, ident.conj() @ M) / d  # remove the trace component
+    q, _ = np.linalg.qr(M)
+    V = (q.T * np.sqrt(d)).copy()
+    s = liecl.ClosureSession(d, config=liecl.ClosureConfig(tolerance=1e-10, record_log=True))
+    s.set_basis(V)
+    st = s.run_rows(1, len(V))
+    log = s.log()
+    nul, ind, rn = port.bracket_window_dense(V, d, 1, len(V), tol=1e-10)
+    assert st["commutators_evaluated"] == len(V) * (len(V) - 1) // 2 == len(log)
+    assert np.array_equal(log["null_cand"], nul) and np.array_equal(log["independent"], ind)
+    assert ind.sum() == 0 and s.size() == len(V)
+
+
+def test_ordered_check_candidates_vs_oracle(port):
+    # config-3 semantics at a size the oracle finishes in seconds:
+    # N=256 orthonormal basis of D=1024 (d=32), 64 candidates, even Gaussian,
+    # odd combinations + 1e-14 noise
+    d, N, K = 32, 256, 64
+    rng = np.random.default_rng(9)
+    G = rng.standard_normal((d * d, N)) + 1j * rng.standard_normal((d * d, N))
+    q, _ = np.linalg.qr(G)
+    V = (q.T * np.sqrt(d)).copy()
+    cands = np.empty((K, d * d), np.complex128)
+    for k in range(K):
+        if k % 2 == 0:
+            cands[k] = rng.standard_normal(d * d) + 1j * rng.standard_normal(d * d)
+        else:
+            a = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+            cands[k] = a @ V + 1e-14 * (rng.standard_normal(d * d) + 1j * rng.standard_normal(d * d))
+    s = liecl.ClosureSession(d, config=liecl.ClosureConfig(tolerance=1e-10, max_dim=N + K))
+    s.set_basis(V)
+    ind, rn, st = s.check_candidates(cands)
+    oind, orn, room = port.check_sequence_dense(V, cands, d, tol=1e-10, append=True)
+    assert np.array_equal(ind, oind)
+    assert ind.sum() == K // 2
+    assert np.abs(rn[ind == 1] - orn[oind == 1]).max() < 1e-12
+    assert rn[ind == 0].max() < 1e-12
+    assert rel_err(s.basis(), room) < BASIS_RTOL
+
+
+def test_capacity_and_timeout_errors():
+    cfg = w.config1()
+    with pytest.raises(liecl.CapacityError):
+        liecl.closure_dense_arrays(cfg.generators, cfg.d, liecl.Method.orthonorm_dimonly,
+                                   liecl.ClosureConfig(tolerance=1e-10, max_dim=10))
+    import time
+    with pytest.raises(liecl.TimeoutError):
+        liecl.closure_dense_arrays(w.config2().generators, 64, liecl.Method.orthonorm_dimonly,
+                                   liecl.ClosureConfig(tolerance=1e-10, deadline=time.monotonic() + 0.5))
+
+
+def test_null_generator_warning_and_kernels_launched():
+    cfg = w.config0()
+    gens = np.concatenate([np.zeros((1, 64), np.complex128), cfg.generators])
+    k0 = native.kernel_count(0)
+    res = liecl.closure_dense_arrays(gens, 8, liecl.Method.orthonorm_dimonly, liecl.ClosureConfig(tolerance=1e-10))
+    assert res.dimension == 9
+    assert [wr.kind for wr in res.stats.warnings] == ["null_generator"]
+    assert res.stats.warnings[0].detail == "generator 0 has norm 0.000000 and was skipped"
+    assert native.kernel_count(0) > k0
