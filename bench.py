@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""Benchmark: candidate brackets checked per second on the B200 hot path.
+
+Workload (BASELINE.json configs[2], the heavy closure): n=6 qubits, d=64,
+three seeded random 8-term generators i*H_k. The closure saturates at dim
+4095 (= d^2 - 1) by row ~95; every later row l evaluates l brackets
+[V_l, V_m] (commutator + norm + normalise) and one orthonormal-projection
+independence check each against the full 4095 x 4096 complex128 basis
+(R:src/closure.cpp:412-460). That saturated phase is >99.9 % of the 8.38M
+brackets of the full closure, so a "step" is one window of it: `rows_per_step`
+consecutive rows of the real config-2 closure, run through the engine with the
+reference's verdict semantics. Setup (untimed) runs the generator loop and the
+growth phase on the GPU.
+
+  value  : brackets/s, whole job, basis resident in HBM (inputs > L2)
+  e2e    : same metric through the C-ABI session with HOST buffers: each step
+           re-uploads the 268 MB basis from pinned memory, runs the window and
+           reads the per-candidate verdict data back
+  roofline: the projection GEMMs (K2a + K2b, zgemm_dmma) against the FP64
+           tensor peak measured in-run (cuBLAS ZGEMM via torch.matmul;
+           MEASURED_PEAKS.json has no FP64 figure)
+  cpu_baseline: the reference itself (oracle/_ref: unmodified liecl sources +
+           Eigen-subset shim) on the same window bytes, all host cores
+
+Multi-GPU (torchrun): weak scaling, each rank checks its own disjoint rows
+against a replicated basis; no collective on the data path.
+
+`--impl reference` times the reference's own CPU path instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate_brackets_checked_per_s"
+UNIT = "brackets/s"
+D_QUBITS = 6
+DIM = 64
+GROWTH_ROWS = 128
+FLOPS_PER_BRACKET = 16 * DIM ** 3 + 16 * 4095 * DIM * DIM  # W = 16 d^3 + 16 N D
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--rows-per-step", type=int, default=4)
+    ap.add_argument("--row0", type=int, default=1024)
+    ap.add_argument("--cpu-pairs", type=int, default=1024, help="bracket sample for the CPU baseline")
+    ap.add_argument("--ref-pairs", type=int, default=128, help="brackets per --impl reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def window_rows(step_index: int, rank: int, world: int, row0: int, rows: int):
+    """Disjoint windows per (step, rank); wraps inside the saturated phase."""
+    span = 4095 - row0
+    k = (step_index * world + rank) * rows
+    start = row0 + (k % max(span - rows, 1))
+    return start, start + rows
+
+
+def brackets_in(r0, r1):
+    return sum(range(r0, r1))
+
+
+# ------------------------------------------------------------------ clocks --
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------- reference arm --
+
+def random_saturated_basis(d=DIM, seed=0):
+    """Seeded orthonormal basis of the traceless d x d matrices (vec layout,
+    orthonormal under <a,b> = vdot(a,b)/d): the same shape and per-bracket work
+    as the config-2 saturated basis (every bracket non-null, every check a
+    reject)."""
+    rng = np.random.default_rng(seed)
+    D = d * d
+    M = rng.standard_normal((D, D - 1)) + 1j * rng.standard_normal((D, D - 1))
+    ident = np.eye(d).ravel(order="F")
+    M -= np.outer(ident, ident @ M) / d
+    q, _ = np.linalg.qr(M)
+    return np.ascontiguousarray(q.T * np.sqrt(d))
+
+
+def cpu_reference(V, pairs, row, threads):
+    """Time the reference (oracle/_ref) -- or the C restatement if the
+    reference build is absent -- on `pairs` brackets starting at `row`."""
+    from oracle.oracle import REF_SO, Port, Ref
+    if os.path.exists(REF_SO):
+        ref = Ref()
+        rows_needed = 1
+        while brackets_in(row, row + rows_needed) < pairs:
+            rows_needed += 1
+        out = ref.bracket_window_dense(V, DIM, row, row + rows_needed, tol=1e-10, max_pairs=pairs, threads=threads)
+        return out["pairs"], out["seconds"], "reference", out["independent"]
+    port = Port()
+    t0 = time.perf_counter()
+    nul, ind, _ = port.bracket_window_dense(V, DIM, row, row + 64, tol=1e-10, max_pairs=pairs, threads=threads)
+    return len(nul), time.perf_counter() - t0, "port", int(ind.sum())
+
+
+def run_reference_arm(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    V = random_saturated_basis()
+    rates = []
+    total_pairs, total_s, kind = 0, 0.0, None
+    for s in range(a.warmup + a.steps):
+        r0, _ = window_rows(s, 0, 1, a.row0, a.rows_per_step)
+        pairs, secs, kind, indep = cpu_reference(V, a.ref_pairs, r0, threads)
+        assert indep == 0, "saturated basis: every bracket must be dependent"
+        if s >= a.warmup:
+            rates.append(pairs / secs)
+            total_pairs += pairs
+            total_s += secs
+    value = total_pairs / total_s
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * total_s / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": "c2_saturated_window", "qubits": D_QUBITS, "d": DIM, "basis": 4095,
+                       "tol": 1e-10, "basis_source": "seeded random orthonormal traceless basis (numpy QR)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": f"{a.ref_pairs} brackets per step from rows >= {a.row0}, {a.steps} steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm --
+
+def fp64_peak_tflops(torch, device):
+    """cuBLAS ZGEMM (complex128 torch.matmul, 8 flops / complex MAC), best of 6."""
+    n = 4096
+    a = torch.randn(n, n, dtype=torch.complex128, device=device)
+    b = torch.randn(n, n, dtype=torch.complex128, device=device)
+    torch.matmul(a, b)
+    torch.cuda.synchronize(device)
+    best = 1e30
+    for _ in range(6):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 8.0 * n ** 3 / (best / 1e3) / 1e12
+
+
+def load_traffic():
+    """dram bytes per launch of the projection GEMMs from the committed ncu
+    capture summary (profiles/), if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_zgemm_summary.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def secondary_closures():
+    """Latency-bound configs 0, 1, 4: full closures through the C-ABI, wall time."""
+    from paper_2506_01120_b200 import liecl, workloads as w
+    out = {}
+    for name, make in (("c0", w.config0), ("c1", w.config1)):
+        cfg = make()
+        liecl.closure_dense_arrays(cfg.generators, cfg.d, liecl.Method.orthonorm_dimonly,
+                                   liecl.ClosureConfig(tolerance=cfg.tol))
+        t0 = time.perf_counter()
+        r = liecl.closure_dense_arrays(cfg.generators, cfg.d, liecl.Method.orthonorm_dimonly,
+                                       liecl.ClosureConfig(tolerance=cfg.tol))
+        dt = time.perf_counter() - t0
+        out[name] = {"dimension": r.dimension, "brackets": r.stats.commutators_evaluated, "seconds": dt,
+                     "brackets_per_s": r.stats.commutators_evaluated / dt}
+    p = w.config4()
+    liecl.closure_pauli_arrays(p.x, p.z, p.coef, p.qubits, liecl.Method.orthonorm_dimonly,
+                               liecl.ClosureConfig(tolerance=p.tol))
+    t0 = time.perf_counter()
+    r = liecl.closure_pauli_arrays(p.x, p.z, p.coef, p.qubits, liecl.Method.orthonorm_dimonly,
+                                   liecl.ClosureConfig(tolerance=p.tol))
+    dt = time.perf_counter() - t0
+    out["c4"] = {"dimension": r.dimension, "brackets": r.stats.commutators_evaluated, "seconds": dt,
+                 "brackets_per_s": r.stats.commutators_evaluated / dt}
+    return out
+
+
+def run_b200_arm(a):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2506_01120_b200 import liecl, native, workloads as w
+
+    stream = torch.cuda.current_stream(device)
+    native.set_stream(stream.cuda_stream, device=local)
+
+    # ---- setup (untimed): generator loop + growth phase on the GPU
+    cfg = w.config2()
+    sess = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol), device=local)
+    sess.check_candidates(cfg.generators)
+    t0 = time.perf_counter()
+    grow = sess.run_rows(1, GROWTH_ROWS)
+    growth_s = time.perf_counter() - t0
+    if sess.size() != 4095:
+        raise RuntimeError(f"config-2 closure did not saturate: dim {sess.size()}")
+    peak = fp64_peak_tflops(torch, device)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warmup
+    step = 0
+    for _ in range(a.warmup):
+        r0, r1 = window_rows(step, rank, world, a.row0, a.rows_per_step)
+        sess.run_rows(r0, r1)
+        step += 1
+
+    # ---- timed region (device resident)
+    windows = [window_rows(step + s, rank, world, a.row0, a.rows_per_step) for s in range(a.steps)]
+    my_brackets = sum(brackets_in(*wnd) for wnd in windows)
+    native.kernel_times(local)  # reset
+    native.set_timing(True, local)
+    barrier()
+    torch.cuda.synchronize(device)
+    k0 = native.kernel_count(local)
+    accepted = 0
+    with ClockSampler(local) as clocks:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.profiler.start()  # ncu --profile-from-start off captures only this region
+        e0.record(stream)
+        for r0, r1 in windows:
+            st = sess.run_rows(r0, r1)
+            accepted += st["accepted"]
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        torch.cuda.profiler.stop()
+    barrier()
+    launches = native.kernel_count(local) - k0
+    native.set_timing(False, local)
+    kt = native.kernel_times(local)
+    my_ms = e0.elapsed_time(e1)
+    step += a.steps
+    max_ms = max_over_ranks(my_ms)
+    total_brackets = my_brackets * world
+    value = total_brackets / (max_ms / 1e3)
+    if accepted:
+        raise RuntimeError("saturated window accepted a candidate")
+
+    proj_ms = kt["zgemm_project"]["ms"] + kt["zgemm_subtract"]["ms"]
+    proj_flops = kt["zgemm_project"]["flops"] + kt["zgemm_subtract"]["flops"]
+    proj_launches = kt["zgemm_project"]["launches"] + kt["zgemm_subtract"]["launches"]
+    achieved = proj_flops / (proj_ms / 1e3) / 1e12
+    traffic = load_traffic()
+
+    # ---- e2e: C-ABI session with host buffers (pinned), H2D basis every step
+    e2e = None
+    if not a.no_e2e:
+        host_V = torch.empty((4095, DIM * DIM), dtype=torch.complex128, pin_memory=True)
+        host_V.numpy()[:] = sess.basis()
+        sess2 = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol), device=local)
+        vptr = host_V.data_ptr()
+
+        def e2e_step(r0, r1):
+            import ctypes as C
+            lib = native.load()
+            st = lib.liecl_b200_session_set_basis(sess2.ptr, C.cast(C.c_void_p(vptr), C.POINTER(C.c_double)),
+                                                  C.c_int64(4095), C.c_int32(0))
+            if st:
+                raise RuntimeError(native.last_error())
+            return sess2.run_rows(r0, r1)
+        for s in range(a.warmup):
+            e2e_step(*window_rows(s, rank, world, a.row0, a.rows_per_step))
+        barrier()
+        torch.cuda.synchronize(device)
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for r0, r1 in windows:
+            e2e_step(r0, r1)
+        f1.record(stream)
+        torch.cuda.synchronize(device)
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+        sess2.close()
+        e2e = {"value": total_brackets / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 4095 * DIM * DIM * 16,
+               "d2h_bytes_per_step": int(12 * my_brackets / a.steps),
+               "path": "liecl_b200_session_set_basis(host pinned) + liecl_b200_session_run_rows"}
+
+    if rank != 0:
+        return
+    cpu = None
+    if not a.no_cpu_baseline and world == 1:
+        V = sess.basis()
+        threads = os.cpu_count() or 1
+        r0 = windows[0][0]
+        pairs, secs, kind, indep = cpu_reference(V, a.cpu_pairs, r0, threads)
+        assert indep == 0
+        cpu = {"value": pairs / secs, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"first {pairs} brackets of rows >= {r0} of the same window, same basis bytes "
+                         f"({secs:.1f} s)"}
+    secondary = None if a.no_secondary else secondary_closures()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": max_ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (seeded SplitMix64 recipe, SURVEY.md §8d)",
+        "config": {"workload": "c2_saturated_window", "qubits": D_QUBITS, "d": DIM, "D": DIM * DIM, "basis": 4095,
+                   "tol": 1e-10, "rows_per_step": a.rows_per_step, "brackets_per_step_per_gpu": my_brackets / a.steps,
+                   "row0": a.row0, "l2": "inputs > L2 (basis 268 MB + candidate slabs 2x268 MB per step)",
+                   "parallelism": f"dp{world}: disjoint closure rows per GPU, basis replicated, no collective",
+                   "growth_setup_s": round(growth_s, 3), "growth_batches": grow["batches"]},
+        "roofline": {"bound": "tensor", "kernel": "zgemm_dmma (K2a beta=V^H C/d + K2b R=C-V beta, DMMA.8x8x4)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": traffic, "launches": proj_launches, "avg_launch_ms": proj_ms / max(proj_launches, 1),
+                     "share_of_step": proj_ms / my_ms,
+                     "flops_per_unit": "8*N*D per candidate per GEMM (N=4095, D=4096)",
+                     "peak_source": "measured in-run: cuBLAS ZGEMM 4096^3 via torch.matmul complex128 "
+                                    "(MEASURED_PEAKS.json has no FP64 entry)",
+                     "path_tflops": value * FLOPS_PER_BRACKET / 1e12 / world,
+                     "commutator_ms": kt["commutator"]["ms"]},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "secondary": secondary,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference_arm(a)
+    else:
+        run_b200_arm(a)
+    if int(os.environ.get("WORLD_SIZE", 1)) > 1 and a.impl == "b200":
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

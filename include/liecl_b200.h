@@ -96,6 +96,22 @@ int liecl_b200_ctx_create(int device, liecl_b200_ctx** out);
 void liecl_b200_ctx_destroy(liecl_b200_ctx* ctx);
 /* Kernel launches issued on this context so far (bench accounting). */
 uint64_t liecl_b200_ctx_kernel_count(const liecl_b200_ctx* ctx);
+/* Launch on a caller-owned cudaStream_t (NULL: back to the context's own). */
+int liecl_b200_ctx_set_stream(liecl_b200_ctx* ctx, void* cuda_stream);
+
+/* Per-kernel-class CUDA-event timing (bench roofline). With timing enabled,
+ * every launch of the projection GEMMs / commutator kernel is bracketed by
+ * events on the launching stream; kernel_times synchronises, reports and
+ * resets the totals. Classes: 0 zgemm_project (K2a), 1 zgemm_subtract (K2b),
+ * 2 commutator (K1), 3 other. `flops` is the algorithmic FP64 work
+ * (8 flops per complex MAC). */
+typedef struct {
+  uint64_t launches;
+  double milliseconds;
+  double flops;
+} liecl_b200_kernel_time;
+int liecl_b200_ctx_set_timing(liecl_b200_ctx* ctx, int32_t enable);
+int liecl_b200_ctx_kernel_times(liecl_b200_ctx* ctx, liecl_b200_kernel_time* out4);
 
 /*
  * run_closure for dense generators (replaces R:include/liecl/closure.hpp:125-126

@@ -123,8 +123,19 @@ template <class T> struct HostBuf {
 
 struct liecl_b200_ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // own_stream or a caller-provided stream
   uint64_t kernels = 0;
+  // per-kernel-class event timing (liecl_b200_ctx_set_timing)
+  bool timing = false;
+  struct Timed {
+    int kind;
+    cudaEvent_t a, b;
+    double flops;
+  };
+  std::vector<Timed> pending;
+  std::vector<cudaEvent_t> spare;
+  liecl_b200_kernel_time totals[4] = {};
 };
 
 namespace {
@@ -135,6 +146,53 @@ void launched(liecl_b200_ctx* ctx) {
   ++ctx->kernels;
   CU(cudaGetLastError());
 }
+
+cudaEvent_t take_event(liecl_b200_ctx* ctx) {
+  if (!ctx->spare.empty()) {
+    cudaEvent_t e = ctx->spare.back();
+    ctx->spare.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CU(cudaEventCreate(&e));
+  return e;
+}
+
+// Brackets one launch with events when timing is on: Timer t(ctx, kind, flops); <launch>; t.stop();
+struct Timer {
+  liecl_b200_ctx* ctx;
+  int kind;
+  double flops;
+  cudaEvent_t a = nullptr;
+  Timer(liecl_b200_ctx* c, int k, double f) : ctx(c), kind(k), flops(f) {
+    if (ctx->timing) {
+      a = take_event(ctx);
+      CU(cudaEventRecord(a, ctx->stream));
+    }
+  }
+  void stop() {
+    if (!a) return;
+    cudaEvent_t b = take_event(ctx);
+    CU(cudaEventRecord(b, ctx->stream));
+    ctx->pending.push_back({kind, a, b, flops});
+    a = nullptr;
+    if (ctx->pending.size() > 4096) drain();
+  }
+  void drain() {
+    for (auto& t : ctx->pending) {
+      CU(cudaEventSynchronize(t.b));
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, t.a, t.b));
+      auto& tot = ctx->totals[t.kind];
+      ++tot.launches;
+      tot.milliseconds += ms;
+      tot.flops += t.flops;
+      ctx->spare.push_back(t.a);
+      ctx->spare.push_back(t.b);
+    }
+    ctx->pending.clear();
+  }
+};
 
 std::string fmt_double(double v) {  // std::to_string(double): "%f"
   return std::to_string(v);
@@ -179,9 +237,11 @@ void gemm_project(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, c
   if (n == 0 || count == 0) return;
   gemm_attr_once<true, true, Epilogue::kStoreScaled>();
   dim3 grid((n + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
+  Timer t(ctx, 0, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
   zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
       static_cast<int>(n), count, static_cast<int>(D), V, D, X, D, P, n, alpha, nullptr, 0, nullptr);
   launched(ctx);
+  t.stop();
 }
 
 // R = X - V[:, 0:n] P ; partial[mt][b] = sum_rows |R|^2
@@ -189,10 +249,12 @@ void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, 
                    int count, double2* R, double* partial) {
   gemm_attr_once<false, false, Epilogue::kSubtractNorm>();
   dim3 grid((D + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
+  Timer t(ctx, 1, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
   zgemm_dmma_kernel<false, false, Epilogue::kSubtractNorm>
       <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n), V,
                                                                      D, P, n, R, D, 1.0, X, D, partial);
   launched(ctx);
+  t.stop();
 }
 
 // --------------------------------------------------------- dense engine ---
@@ -414,9 +476,11 @@ private:
       attr = true;
     }
     const int blocks = (cnt + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA;
+    Timer t(ctx_, 2, 16.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
     commutator_norm_kernel<DIM><<<blocks, 256, S::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, C_.p, hn_.p,
                                                                          nul_.p);
     launched(ctx_);
+    t.stop();
   }
 
   void run_pair_batch(int64_t g0, int cnt) {
@@ -924,11 +988,12 @@ int liecl_b200_ctx_create(int device, liecl_b200_ctx** out) {
     CU(cudaSetDevice(device));
     auto* c = new liecl_b200_ctx;
     c->device = device;
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
       delete c;
       throw Error(LIECL_B200_CUDA, cudaGetErrorString(e));
     }
+    c->stream = c->own_stream;
     *out = c;
   });
 }
@@ -936,11 +1001,44 @@ int liecl_b200_ctx_create(int device, liecl_b200_ctx** out) {
 void liecl_b200_ctx_destroy(liecl_b200_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  for (auto& t : ctx->pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : ctx->spare) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
 
 uint64_t liecl_b200_ctx_kernel_count(const liecl_b200_ctx* ctx) { return ctx ? ctx->kernels : 0; }
+
+int liecl_b200_ctx_set_stream(liecl_b200_ctx* ctx, void* cuda_stream) {
+  return guarded([&] {
+    if (!ctx) throw Error(LIECL_B200_INVALID_INPUT, "null context");
+    use_device(ctx);
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  });
+}
+
+int liecl_b200_ctx_set_timing(liecl_b200_ctx* ctx, int32_t enable) {
+  return guarded([&] {
+    if (!ctx) throw Error(LIECL_B200_INVALID_INPUT, "null context");
+    ctx->timing = enable != 0;
+  });
+}
+
+int liecl_b200_ctx_kernel_times(liecl_b200_ctx* ctx, liecl_b200_kernel_time* out4) {
+  return guarded([&] {
+    if (!ctx || !out4) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    use_device(ctx);
+    Timer(ctx, 3, 0.0).drain();
+    for (int k = 0; k < 4; ++k) {
+      out4[k] = ctx->totals[k];
+      ctx->totals[k] = liecl_b200_kernel_time{};
+    }
+  });
+}
 
 int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d, int32_t method,
                              const liecl_b200_config* cfg_in, double* basis_out, double* ortho_out, int64_t cap,

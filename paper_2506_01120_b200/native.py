@@ -19,7 +19,8 @@ METHOD_STANDARD_RANK, METHOD_MATRIX_INVERSION, METHOD_ORTHONORM, METHOD_ORTHONOR
 # every symbol include/liecl_b200.h declares (tests check the .so exports them all)
 EXPORTED = [
     "liecl_b200_abi_version", "liecl_b200_last_error", "liecl_b200_ctx_create", "liecl_b200_ctx_destroy",
-    "liecl_b200_ctx_kernel_count", "liecl_b200_closure_dense", "liecl_b200_closure_pauli",
+    "liecl_b200_ctx_kernel_count", "liecl_b200_ctx_set_stream", "liecl_b200_ctx_set_timing",
+    "liecl_b200_ctx_kernel_times", "liecl_b200_closure_dense", "liecl_b200_closure_pauli",
     "liecl_b200_project_residual_dense", "liecl_b200_commutator_dense", "liecl_b200_inner_product_dense",
     "liecl_b200_norm_dense", "liecl_b200_session_create_dense", "liecl_b200_session_destroy",
     "liecl_b200_session_set_basis", "liecl_b200_session_run_pairs", "liecl_b200_session_run_rows",
@@ -96,3 +97,31 @@ def context(device: int = 0) -> C.c_void_p:
 
 def kernel_count(device: int = 0) -> int:
     return int(load().liecl_b200_ctx_kernel_count(context(device)))
+
+
+class KernelTime(C.Structure):
+    _fields_ = [("launches", C.c_uint64), ("milliseconds", C.c_double), ("flops", C.c_double)]
+
+
+KERNEL_CLASSES = ("zgemm_project", "zgemm_subtract", "commutator", "other")
+
+
+def set_stream(stream_ptr: int | None, device: int = 0) -> None:
+    """Launch on a caller-owned cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+    st = load().liecl_b200_ctx_set_stream(context(device), C.c_void_p(stream_ptr) if stream_ptr else None)
+    if st != OK:
+        raise NativeUnavailable(last_error())
+
+
+def set_timing(enable: bool, device: int = 0) -> None:
+    load().liecl_b200_ctx_set_timing(context(device), C.c_int32(int(enable)))
+
+
+def kernel_times(device: int = 0) -> dict:
+    """Per-class CUDA-event totals since the last call (then reset)."""
+    out = (KernelTime * 4)()
+    st = load().liecl_b200_ctx_kernel_times(context(device), out)
+    if st != OK:
+        raise NativeUnavailable(last_error())
+    return {name: {"launches": out[k].launches, "ms": out[k].milliseconds, "flops": out[k].flops}
+            for k, name in enumerate(KERNEL_CLASSES)}
