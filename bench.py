@@ -54,10 +54,10 @@ FLOPS_PER_BRACKET = 16 * DIM ** 3 + 16 * 4095 * DIM * DIM  # W =
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--rows-per-step", type=int, default=4)
+    ap.add_argument("--rows-per-step", type=int, default=8)
     ap.add_argument("--row0", type=int, default=1024)
     ap.add_argument("--cpu-pairs", type=int, default=1024, help="bracket sample for the CPU baseline")
     ap.add_argument("--ref-pairs", type=int, default=128, help="brackets per --impl reference step")

@@ -1,0 +1,313 @@
+// liecl drop-in: the closure translation unit of liecl, re-implemented on the
+// B200 C-ABI (include/liecl_b200.h).
+//
+// A liecl consumer keeps the reference's headers (liecl/closure.hpp et al.)
+// and its pauli / dense / operator / generators translation units, and links
+// this file in place of R:src/closure.cpp. Every function declared by
+// R:include/liecl/closure.hpp is defined here with the same signature:
+//
+//   run_closure                (R:include/liecl/closure.hpp:125-126) -> GPU for
+//   close_orthonormalization   (:119-121)  orthonorm / orthonorm-dimonly
+//   project_residual           (:139-140)  -> GPU (dense operators)
+//   to_string / method_from_string (:22-23), basis_listing (:143)
+//   close_standard, close_matrix_inversion, check_matrix_inversion, GramState
+//       -- off the hot path: they raise
+//          InvalidInputError instead of silently running a CPU fallback.
+//
+// Status codes of the C-ABI map back onto the reference's exception types
+// (R:include/liecl/errors.hpp:10-61).
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "liecl/closure.hpp"
+#include "liecl/errors.hpp"
+#include "liecl_b200.h"
+
+namespace liecl {
+
+namespace {
+
+[[noreturn]] void raise(int status) {
+  const std::string msg = liecl_b200_last_error();
+  switch (status) {
+  case LIECL_B200_INVALID_INPUT: throw InvalidInputError(msg);
+  case LIECL_B200_CAPACITY: throw CapacityError(msg);
+  case LIECL_B200_DEGENERACY: throw DegeneracyError(msg, 0);
+  case LIECL_B200_TIMEOUT: throw TimeoutError(msg);
+  case LIECL_B200_PARSE: throw ParseError(msg, 0, 0);
+  default: throw Error("B200 backend: " + msg);
+  }
+}
+
+void check(int status) {
+  if (status != LIECL_B200_OK) raise(status);
+}
+
+// One device context per process (stream + workspaces), created on first use.
+liecl_b200_ctx* context() {
+  static std::once_flag once;
+  static liecl_b200_ctx* ctx = nullptr;
+  static int status = LIECL_B200_OK;
+  std::call_once(once, [] { status = liecl_b200_ctx_create(0, &ctx); });
+  if (status != LIECL_B200_OK) raise(status);
+  return ctx;
+}
+
+liecl_b200_config to_native(const ClosureConfig& c) {
+  liecl_b200_config n{};
+  n.tolerance = c.tolerance;
+  n.max_dim = c.max_dim;
+  n.threads = c.threads;
+  n.record_log = 0;
+  n.batch_max = 0;
+  if (c.deadline) {
+    const double rel = std::chrono::duration<double>(*c.deadline - std::chrono::steady_clock::now()).count();
+    n.deadline_seconds = rel > 0 ? rel : 1e-9;
+  }
+  return n;
+}
+
+// Shared backend of the tuple; nullopt when every generator is null
+// (R:src/closure.cpp:476-496).
+std::optional<Backend> validate(std::span<const Operator> generators) {
+  if (generators.empty()) throw InvalidInputError("closure requires a non-empty generator tuple");
+  std::optional<Backend> backend;
+  Eigen::Index dim = 0;
+  for (const Operator& g : generators) {
+    if (g.is_null()) continue;
+    if (!backend) {
+      backend = g.backend();
+      dim = g.dim();
+    } else if (g.backend() != *backend || g.dim() != dim) {
+      throw InvalidInputError("closure generators must share one backend and dimension");
+    }
+  }
+  return backend;
+}
+
+std::vector<WarningRecord> parse_warnings(const std::vector<char>& buf) {
+  std::vector<WarningRecord> out;
+  const std::string s(buf.data());
+  size_t pos = 0;
+  while (pos < s.size()) {
+    const size_t end = s.find('\n', pos);
+    const std::string line = s.substr(pos, end == std::string::npos ? std::string::npos : end - pos);
+    pos = end == std::string::npos ? s.size() : end + 1;
+    const size_t t1 = line.find('\t'), t2 = line.find('\t', t1 + 1);
+    if (t1 == std::string::npos || t2 == std::string::npos) continue;
+    out.push_back({line.substr(0, t1), line.substr(t2 + 1), std::stod(line.substr(t1 + 1, t2 - t1 - 1))});
+  }
+  return out;
+}
+
+void fill_stats(ClosureResult& r, const liecl_b200_stats& st, const std::vector<char>& wbuf) {
+  r.stats.commutators_evaluated = st.commutators_evaluated;
+  r.stats.independence_checks = st.independence_checks;
+  r.stats.accepted = st.accepted;
+  r.stats.wall_seconds = st.wall_seconds;
+  r.stats.warnings = parse_warnings(wbuf);
+}
+
+ClosureResult close_dense(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
+  Eigen::Index d = 0;
+  for (const Operator& g : generators)
+    if (!g.is_null()) d = g.dim();
+  const size_t D = static_cast<size_t>(d) * d;
+  std::vector<double> gens(2 * D * generators.size(), 0.0);
+  for (size_t i = 0; i < generators.size(); ++i)
+    if (!generators[i].is_null())
+      std::memcpy(gens.data() + 2 * D * i, generators[i].dense().matrix().data(), sizeof(double) * 2 * D);
+  const size_t cap = config.max_dim ? config.max_dim : D;
+  std::vector<double> basis(2 * D * cap), ortho(keep ? 2 * D * cap : 0);
+  liecl_b200_stats st{};
+  std::vector<char> wbuf(1 << 20);
+  const liecl_b200_config cfg = to_native(config);
+  check(liecl_b200_closure_dense(context(), gens.data(), static_cast<int32_t>(generators.size()),
+                                 static_cast<int32_t>(d), keep ? LIECL_B200_METHOD_ORTHONORM
+                                                               : LIECL_B200_METHOD_ORTHONORM_DIMONLY,
+                                 &cfg, basis.data(), keep ? ortho.data() : nullptr, static_cast<int64_t>(cap), &st,
+                                 wbuf.data(), static_cast<int64_t>(wbuf.size()), nullptr, 0, nullptr));
+  auto unpack = [&](const std::vector<double>& src) {
+    OperatorTuple t;
+    t.reserve(st.dimension);
+    for (size_t k = 0; k < st.dimension; ++k) {
+      Eigen::MatrixXcd m(d, d);
+      std::memcpy(static_cast<void*>(m.data()), src.data() + 2 * D * k, sizeof(double) * 2 * D);
+      t.emplace_back(DenseOperator(std::move(m)));
+    }
+    return t;
+  };
+  ClosureResult r;
+  r.basis = unpack(basis);
+  r.orthonormal_basis = keep ? unpack(ortho) : r.basis;
+  r.dimension = st.dimension;
+  r.method = keep ? Method::orthonorm : Method::orthonorm_dimonly;
+  r.backend = Backend::dense;
+  r.tolerance = config.tolerance;
+  fill_stats(r, st, wbuf);
+  return r;
+}
+
+ClosureResult close_pauli(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
+  std::uint32_t qubits = 0;
+  std::vector<std::uint64_t> x, z;
+  std::vector<double> c;
+  for (const Operator& g : generators) {
+    if (g.is_null() || g.pauli().empty()) {  // null / empty: zero coefficient, skipped as a null generator
+      x.push_back(0);
+      z.push_back(0);
+      c.push_back(0.0);
+      c.push_back(0.0);
+      continue;
+    }
+    qubits = g.pauli().qubits();
+    if (g.pauli().size() != 1)
+      throw InvalidInputError("B200 Pauli path: generators must be single Pauli strings "
+                              "(multi-term sums are not on the hot path yet)");
+    const auto& t = g.pauli().terms()[0];
+    x.push_back(t.string.x);
+    z.push_back(t.string.z);
+    c.push_back(t.coefficient.real());
+    c.push_back(t.coefficient.imag());
+  }
+  const size_t cap = config.max_dim ? config.max_dim : (qubits < 12 ? (size_t{1} << (2 * qubits)) : (size_t{1} << 24));
+  std::vector<std::uint64_t> bx(cap), bz(cap);
+  std::vector<double> bc(2 * cap), oc(2 * cap);
+  liecl_b200_stats st{};
+  std::vector<char> wbuf(1 << 20);
+  const liecl_b200_config cfg = to_native(config);
+  check(liecl_b200_closure_pauli(context(), x.data(), z.data(), c.data(), static_cast<int32_t>(x.size()), qubits,
+                                 keep ? LIECL_B200_METHOD_ORTHONORM : LIECL_B200_METHOD_ORTHONORM_DIMONLY, &cfg,
+                                 bx.data(), bz.data(), bc.data(), oc.data(), static_cast<int64_t>(cap), &st,
+                                 wbuf.data(), static_cast<int64_t>(wbuf.size()), nullptr, 0, nullptr));
+  // the engine hands back the exact coefficient bits of the reference's
+  // one-term sums; rebuild the PauliSum values term for term
+  auto unpack = [&](const std::vector<double>& coef) {
+    OperatorTuple t;
+    t.reserve(st.dimension);
+    for (size_t k = 0; k < st.dimension; ++k) {
+      const PauliSum::Term term{PauliString{bx[k], bz[k], qubits}, Complex{coef[2 * k], coef[2 * k + 1]}};
+      t.emplace_back(PauliSum::single(term.string, Complex{1.0, 0.0}) * term.coefficient);
+    }
+    return t;
+  };
+  ClosureResult r;
+  r.basis = unpack(bc);
+  r.orthonormal_basis = unpack(oc);
+  r.dimension = st.dimension;
+  r.method = keep ? Method::orthonorm : Method::orthonorm_dimonly;
+  r.backend = Backend::pauli;
+  r.tolerance = config.tolerance;
+  fill_stats(r, st, wbuf);
+  return r;
+}
+
+[[noreturn]] void off_path(const char* what) {
+  throw InvalidInputError(std::string(what) +
+                          ": not on the B200 hot path (the B200 build serves the orthonormalization methods)");
+}
+
+} // namespace
+
+std::string to_string(Method method) {
+  switch (method) {
+  case Method::standard_rank: return "standard-rank";
+  case Method::matrix_inversion: return "matrix-inversion";
+  case Method::orthonorm: return "orthonorm";
+  case Method::orthonorm_dimonly: return "orthonorm-dimonly";
+  }
+  return "unknown";
+}
+
+Method method_from_string(const std::string& name) {
+  if (name == "standard-rank") return Method::standard_rank;
+  if (name == "matrix-inversion") return Method::matrix_inversion;
+  if (name == "orthonorm") return Method::orthonorm;
+  if (name == "orthonorm-dimonly") return Method::orthonorm_dimonly;
+  throw InvalidInputError("unknown method '" + name +
+                          "' (expected standard-rank, matrix-inversion, orthonorm or orthonorm-dimonly)");
+}
+
+double GramState::schur_complement(const Eigen::VectorXcd&) const { off_path("GramState::schur_complement"); }
+void GramState::expand(const Eigen::VectorXcd&, double) { off_path("GramState::expand"); }
+void GramState::refresh() { off_path("GramState::refresh"); }
+double GramState::inverse_error() const { off_path("GramState::inverse_error"); }
+
+ClosureResult close_standard(std::span<const Operator>, const ClosureConfig&) { off_path("close_standard"); }
+ClosureResult close_matrix_inversion(std::span<const Operator>, const ClosureConfig&) {
+  off_path("close_matrix_inversion");
+}
+std::pair<bool, CoefficientVector> check_matrix_inversion(const GramState&, std::span<const Operator>,
+                                                          const Operator&, double) {
+  off_path("check_matrix_inversion");
+}
+
+ClosureResult close_orthonormalization(std::span<const Operator> generators, const ClosureConfig& config,
+                                       bool keep_original) {
+  const Backend backend = validate(generators).value_or(Backend::pauli);
+  bool any = false;
+  for (const Operator& g : generators) any = any || !g.is_null();
+  if (!any) {  // every generator null: empty closure, one warning each (R:src/closure.cpp:378-387)
+    ClosureResult r;
+    r.method = keep_original ? Method::orthonorm : Method::orthonorm_dimonly;
+    r.backend = backend;
+    r.tolerance = config.tolerance;
+    r.orthonormal_basis = OperatorTuple{};
+    for (size_t i = 0; i < generators.size(); ++i)
+      r.stats.warnings.push_back({"null_generator",
+                                  "generator " + std::to_string(i) + " has norm " + std::to_string(0.0) +
+                                      " and was skipped",
+                                  0.0});
+    return r;
+  }
+  return backend == Backend::dense ? close_dense(generators, config, keep_original)
+                                   : close_pauli(generators, config, keep_original);
+}
+
+ClosureResult run_closure(std::span<const Operator> generators, Method method, const ClosureConfig& config) {
+  switch (method) {
+  case Method::standard_rank: off_path("run_closure(standard-rank)");
+  case Method::matrix_inversion: off_path("run_closure(matrix-inversion)");
+  case Method::orthonorm: return close_orthonormalization(generators, config, true);
+  case Method::orthonorm_dimonly: return close_orthonormalization(generators, config, false);
+  }
+  throw InvalidInputError("run_closure: unknown method");
+}
+
+std::pair<Operator, CoefficientVector> project_residual(std::span<const Operator> orthonormal, const Operator& h) {
+  if (orthonormal.empty()) return {h, {}};
+  if (h.is_null() || !h.is_dense())
+    off_path("project_residual on non-dense operators");
+  const Eigen::Index d = h.dim();
+  const size_t D = static_cast<size_t>(d) * d;
+  std::vector<double> V(2 * D * orthonormal.size(), 0.0);
+  for (size_t l = 0; l < orthonormal.size(); ++l) {
+    if (orthonormal[l].is_null()) continue;
+    if (!orthonormal[l].is_dense() || orthonormal[l].dim() != d)
+      throw InvalidInputError("linear_combination: operators have mismatched backends or dimensions");
+    std::memcpy(V.data() + 2 * D * l, orthonormal[l].dense().matrix().data(), sizeof(double) * 2 * D);
+  }
+  std::vector<double> r(2 * D), coeffs(2 * orthonormal.size());
+  check(liecl_b200_project_residual_dense(context(), V.data(), static_cast<int64_t>(orthonormal.size()),
+                                          reinterpret_cast<const double*>(h.dense().matrix().data()),
+                                          static_cast<int32_t>(d), r.data(), coeffs.data()));
+  Eigen::MatrixXcd m(d, d);
+  std::memcpy(static_cast<void*>(m.data()), r.data(), sizeof(double) * 2 * D);
+  CoefficientVector c(orthonormal.size());
+  for (size_t l = 0; l < c.size(); ++l) c[l] = {coeffs[2 * l], coeffs[2 * l + 1]};
+  return {Operator(DenseOperator(std::move(m))), std::move(c)};
+}
+
+std::string basis_listing(const ClosureResult& result) {
+  std::string out;
+  for (const Operator& op : result.basis) {
+    out += format_operator(op);
+    out += '\n';
+  }
+  return out;
+}
+
+} // namespace liecl

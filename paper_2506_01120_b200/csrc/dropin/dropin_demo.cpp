@@ -1,0 +1,100 @@
+// A liecl consumer linked against the B200 drop-in (closure_b200.cpp in place
+// of R:src/closure.cpp): builds configs 0 and 4 with the reference's own
+// Pauli/dense API and runs liecl::run_closure. Prints one JSON object; the GPU
+// test (tests/test_gpu_dropin.py) compares it with the golden fixtures.
+#include <complex>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "liecl/closure.hpp"
+#include "liecl/dense.hpp"
+#include "liecl/errors.hpp"
+#include "liecl/pauli.hpp"
+
+using namespace liecl;
+
+static void print_stats(const ClosureResult& r) {
+  std::printf("{\"dimension\": %zu, \"commutators_evaluated\": %llu, \"independence_checks\": %llu, "
+              "\"accepted\": %llu, \"warnings\": %zu",
+              r.dimension, static_cast<unsigned long long>(r.stats.commutators_evaluated),
+              static_cast<unsigned long long>(r.stats.independence_checks),
+              static_cast<unsigned long long>(r.stats.accepted), r.stats.warnings.size());
+}
+
+int main() {
+  const Complex I{0.0, 1.0};
+  ClosureConfig cfg;
+  cfg.tolerance = 1e-10;
+  std::printf("{");
+  // config 0 (dense): i*(X0+X1+X2), i*(Z0Z1+Z1Z2)
+  {
+    const std::uint32_t n = 3;
+    std::vector<PauliSum::Term> t0, t1;
+    for (std::uint32_t j = 0; j < n; ++j) t0.push_back({PauliString{1ull << j, 0, n}, I});
+    for (std::uint32_t j = 0; j + 1 < n; ++j) t1.push_back({PauliString{0, (1ull << j) | (1ull << (j + 1)), n}, I});
+    const std::vector<Operator> gens{Operator(from_pauli(PauliSum::from_terms(n, t0))),
+                                     Operator(from_pauli(PauliSum::from_terms(n, t1)))};
+    for (const Method m : {Method::orthonorm_dimonly, Method::orthonorm}) {
+      const ClosureResult r = run_closure(gens, m, cfg);
+      std::printf("\"c0_%s\": ", to_string(m).c_str());
+      print_stats(r);
+      std::printf(", \"basis\": [");
+      for (size_t k = 0; k < r.basis.size(); ++k) {
+        const auto& mat = r.basis[k].dense().matrix();
+        std::printf("%s[", k ? "," : "");
+        for (Eigen::Index e = 0; e < mat.size(); ++e)
+          std::printf("%s%.17g,%.17g", e ? "," : "", mat(e).real(), mat(e).imag());
+        std::printf("]");
+      }
+      std::printf("]}, ");
+    }
+  }
+  // config 4 (Pauli): n=10 ring, i*XX, i*YY, i*Z single strings
+  {
+    const std::uint32_t n = 10;
+    std::vector<Operator> gens;
+    for (std::uint32_t j = 0; j < n; ++j) {
+      const std::uint64_t b = (1ull << j) | (1ull << ((j + 1) % n));
+      gens.emplace_back(PauliSum::single(PauliString{b, 0, n}, I));
+    }
+    for (std::uint32_t j = 0; j < n; ++j) {
+      const std::uint64_t b = (1ull << j) | (1ull << ((j + 1) % n));
+      gens.emplace_back(PauliSum::single(PauliString{b, b, n}, I));
+    }
+    for (std::uint32_t j = 0; j < n; ++j) gens.emplace_back(PauliSum::single(PauliString{0, 1ull << j, n}, I));
+    const ClosureResult r = run_closure(gens, Method::orthonorm_dimonly, cfg);
+    std::printf("\"c4\": ");
+    print_stats(r);
+    std::printf(", \"strings\": [");
+    for (size_t k = 0; k < r.basis.size(); ++k) {
+      const auto& t = r.basis[k].pauli().terms()[0];
+      std::printf("%s[%llu,%llu,%.17g,%.17g]", k ? "," : "", static_cast<unsigned long long>(t.string.x),
+                  static_cast<unsigned long long>(t.string.z), t.coefficient.real(), t.coefficient.imag());
+    }
+    std::printf("]}, ");
+  }
+  // project_residual and the error mapping
+  {
+    std::vector<PauliSum::Term> xs{{PauliString{1, 0, 1}, Complex{1.0, 0.0}}};
+    std::vector<PauliSum::Term> zs{{PauliString{0, 1, 1}, Complex{1.0, 0.0}}};
+    std::vector<PauliSum::Term> mix{{PauliString{1, 0, 1}, Complex{1.0, 0.0}}, {PauliString{0, 1, 1}, Complex{2.0, 0.0}}};
+    const std::vector<Operator> V{Operator(from_pauli(PauliSum::from_terms(1, xs)))};
+    const auto [r, c] = project_residual(V, Operator(from_pauli(PauliSum::from_terms(1, mix))));
+    const Operator zexp(from_pauli(PauliSum::from_terms(1, zs)));
+    const auto diff = r.dense().matrix() - Complex{2.0, 0.0} * zexp.dense().matrix();
+    std::printf("\"project_residual\": {\"coeff\": [%.17g, %.17g], \"residual_err\": %.3g}, ", c[0].real(), c[0].imag(),
+                diff.norm());
+    bool threw = false;
+    try {
+      ClosureConfig tiny = cfg;
+      tiny.max_dim = 3;
+      run_closure(std::vector<Operator>{V[0], zexp}, Method::orthonorm_dimonly, tiny);
+    } catch (const CapacityError&) {
+      threw = true;
+    }
+    std::printf("\"capacity_error\": %s", threw ? "true" : "false");
+  }
+  std::printf("}\n");
+  return 0;
+}

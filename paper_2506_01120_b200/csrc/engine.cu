@@ -126,6 +126,8 @@ struct liecl_b200_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // own_stream or a caller-provided stream
   uint64_t kernels = 0;
+  DevBuf<double2> splitk_ws;  // split-K partial products of the projection GEMMs
+  std::shared_ptr<void> dense_cache, pauli_cache;  // workspaces of the last one-shot closure
   // per-kernel-class event timing (liecl_b200_ctx_set_timing)
   bool timing = false;
   struct Timed {
@@ -231,6 +233,15 @@ template <bool KC, bool CJ, Epilogue E> void gemm_attr_once() {
   }
 }
 
+// Split-K slice count for a grid of `tiles` CTAs over a reduction of length K:
+// only small grids (under one wave of 148 SMs) split, aiming at ~2 CTAs per SM
+// with at least 256 complex elements of K per slice.
+int split_slices(int64_t tiles, int64_t K) {
+  if (tiles >= 148 || K < 512) return 1;
+  const int64_t want = (296 + tiles - 1) / tiles;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, K / 256)));
+}
+
 // P[n x count] = (1/d) V[:, 0:n]^H X      (ldc = n)
 void gemm_project(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, const double2* X, int count,
                   double2* P, double alpha) {
@@ -238,9 +249,25 @@ void gemm_project(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, c
   gemm_attr_once<true, true, Epilogue::kStoreScaled>();
   dim3 grid((n + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
   Timer t(ctx, 0, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
-  zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
-      static_cast<int>(n), count, static_cast<int>(D), V, D, X, D, P, n, alpha, nullptr, 0, nullptr);
-  launched(ctx);
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, D);
+  if (slices <= 1) {
+    zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
+        static_cast<int>(n), count, static_cast<int>(D), V, D, X, D, P, n, alpha, nullptr, 0, nullptr, 0, 0);
+    launched(ctx);
+  } else {
+    const int chunk = static_cast<int>(((D + slices - 1) / slices + zg::BK - 1) / zg::BK * zg::BK);
+    slices = static_cast<int>((D + chunk - 1) / chunk);
+    const int64_t stride = n * count;
+    ctx->splitk_ws.ensure(static_cast<size_t>(slices * stride));
+    grid.z = slices;
+    zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
+        static_cast<int>(n), count, static_cast<int>(D), V, D, X, D, ctx->splitk_ws.p, n, 1.0, nullptr, 0, nullptr,
+        chunk, stride);
+    launched(ctx);
+    splitk_reduce_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>((stride + 255) / 256, 1024)), 256, 0,
+                                 ctx->stream>>>(ctx->splitk_ws.p, slices, stride, stride, alpha, P);
+    launched(ctx);
+  }
   t.stop();
 }
 
@@ -250,10 +277,29 @@ void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, 
   gemm_attr_once<false, false, Epilogue::kSubtractNorm>();
   dim3 grid((D + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
   Timer t(ctx, 1, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
-  zgemm_dmma_kernel<false, false, Epilogue::kSubtractNorm>
-      <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n), V,
-                                                                     D, P, n, R, D, 1.0, X, D, partial);
-  launched(ctx);
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, n);
+  if (slices <= 1) {
+    zgemm_dmma_kernel<false, false, Epilogue::kSubtractNorm>
+        <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n),
+                                                                       V, D, P, n, R, D, 1.0, X, D, partial, 0, 0);
+    launched(ctx);
+  } else {
+    gemm_attr_once<false, false, Epilogue::kStoreScaled>();
+    const int chunk = static_cast<int>(((n + slices - 1) / slices + zg::BK - 1) / zg::BK * zg::BK);
+    slices = static_cast<int>((n + chunk - 1) / chunk);
+    const int64_t stride = D * count;
+    ctx->splitk_ws.ensure(static_cast<size_t>(slices * stride));
+    grid.z = slices;
+    zgemm_dmma_kernel<false, false, Epilogue::kStoreScaled>
+        <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n),
+                                                                       V, D, P, n, ctx->splitk_ws.p, D, 1.0, nullptr,
+                                                                       0, nullptr, chunk, stride);
+    launched(ctx);
+    splitk_reduce_subtract_kernel<<<dim3(static_cast<unsigned>((D + zg::BM - 1) / zg::BM), count), zg::BM, 0,
+                                    ctx->stream>>>(ctx->splitk_ws.p, slices, stride, static_cast<int>(D), count, X, R,
+                                                   partial);
+    launched(ctx);
+  }
   t.stop();
 }
 
@@ -275,8 +321,28 @@ public:
                                      std::chrono::duration<double>(cfg.deadline_seconds));
     has_deadline_ = cfg.deadline_seconds > 0;
     sqrt_d_ = std::sqrt(static_cast<double>(d));
+    B_cur_ = std::min<int64_t>(bmax_, 512);
     alloc_batch(bmax_);
     ensure_capacity(std::min<int64_t>(cap_ + 1, std::max<int64_t>(64, (int64_t(1) << 30) / (D_ * 16))));
+  }
+
+  // Same shape (d, method, cap, batch) as a previous closure: reuse the
+  // device/pinned workspaces (latency-bound small configs pay no allocation).
+  bool compatible(int d, bool keep, const liecl_b200_config& cfg) const {
+    const int64_t cap = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : static_cast<int64_t>(d) * d;
+    return d == d_ && keep == keep_ && cap == cap_ && (cfg.batch_max <= 0 || cfg.batch_max == bmax_);
+  }
+  void reset(const liecl_b200_config& cfg) {
+    tol_ = cfg.tolerance;
+    if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
+    record_ = cfg.record_log != 0;
+    has_deadline_ = cfg.deadline_seconds > 0;
+    if (has_deadline_)
+      deadline_ = Clock::now() + std::chrono::duration_cast<Clock::duration>(
+                                     std::chrono::duration<double>(cfg.deadline_seconds));
+    n_o_ = n_b_ = 0;
+    B_cur_ = std::min<int64_t>(bmax_, 512);
+    reset_stats();
   }
 
   // ---- state / results ----------------------------------------------------
@@ -339,7 +405,6 @@ public:
   // batch start (the reference's row loop re-reads |basis| every row).
   void run_pairs(int64_t g_begin, int64_t g_end) {
     int64_t g = g_begin;
-    int64_t B = std::min<int64_t>(bmax_, 512);
     while (g < g_end) {
       const int64_t nb = basis_size();
       const int64_t avail = nb * (nb - 1) / 2;
@@ -348,33 +413,35 @@ public:
                                                   " refers to a basis element that does not exist yet");
       }
       check_deadline();
-      const int64_t cnt = std::min({B, avail - g, g_end - g});
-      const uint64_t before = st_.accepted;
-      run_pair_batch(g, static_cast<int>(cnt));
+      const int64_t cnt = std::min({B_cur_, avail - g, g_end - g});
+      run_adaptive_batch(g, cnt);
       g += cnt;
-      const uint64_t acc = st_.accepted - before;
-      if (acc == 0) B = std::min<int64_t>(2 * B, bmax_);
-      else if (acc * 4 > static_cast<uint64_t>(cnt)) B = std::max<int64_t>(64, B / 2);
     }
   }
 
   // the whole closure after the generator loop: all pairs until exhausted
   void run_closure_pairs() {
     int64_t g = 0;
-    int64_t B = std::min<int64_t>(bmax_, 512);
     for (;;) {
       const int64_t nb = basis_size();
       const int64_t avail = nb * (nb - 1) / 2;
       if (g >= avail) break;
       check_deadline();
-      const int64_t cnt = std::min(B, avail - g);
-      const uint64_t before = st_.accepted;
-      run_pair_batch(g, static_cast<int>(cnt));
+      const int64_t cnt = std::min(B_cur_, avail - g);
+      run_adaptive_batch(g, cnt);
       g += cnt;
-      const uint64_t acc = st_.accepted - before;
-      if (acc == 0) B = std::min<int64_t>(2 * B, bmax_);
-      else if (acc * 4 > static_cast<uint64_t>(cnt)) B = std::max<int64_t>(64, B / 2);
     }
+  }
+
+  // Batch size follows the accept rate: it doubles while batches accept
+  // nothing (saturated phase: big GEMMs, few syncs) and halves when more
+  // than a quarter is accepted (growth phase: little speculative waste).
+  void run_adaptive_batch(int64_t g, int64_t cnt) {
+    const uint64_t before = st_.accepted;
+    run_pair_batch(g, static_cast<int>(cnt));
+    const uint64_t acc = st_.accepted - before;
+    if (acc == 0) B_cur_ = std::min<int64_t>(2 * B_cur_, bmax_);
+    else if (acc * 4 > static_cast<uint64_t>(cnt)) B_cur_ = std::max<int64_t>(64, B_cur_ / 2);
   }
 
   void download(const double2* src, int64_t n, double* out) {
@@ -630,7 +697,7 @@ private:
   bool keep_;
   double tol_;
   bool record_;
-  int64_t cap_ = 0, bmax_ = 0;
+  int64_t cap_ = 0, bmax_ = 0, B_cur_ = 0;
   double sqrt_d_ = 1.0;
   bool has_deadline_ = false;
   Clock::time_point deadline_{};
@@ -739,6 +806,30 @@ public:
     }
     grow_basis(1024);
     counters_.ensure(3);
+  }
+
+  bool compatible(unsigned qubits, bool keep, const liecl_b200_config& cfg) const {
+    const uint64_t full = 1ull << (2 * qubits);
+    const int64_t cap = cfg.max_dim ? static_cast<int64_t>(std::min<uint64_t>(cfg.max_dim, full))
+                                    : static_cast<int64_t>(full);
+    return qubits == q_ && keep == keep_ && cap == cap_ && (cfg.batch_max <= 0 || cfg.batch_max == bmax_);
+  }
+  void reset(const liecl_b200_config& cfg) {
+    tol_ = cfg.tolerance;
+    if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
+    record_ = cfg.record_log != 0;
+    has_deadline_ = cfg.deadline_seconds > 0;
+    if (has_deadline_)
+      deadline_ = Clock::now() + std::chrono::duration_cast<Clock::duration>(
+                                     std::chrono::duration<double>(cfg.deadline_seconds));
+    n_ = 0;
+    st_ = liecl_b200_stats{};
+    warns_.clear();
+    log_.clear();
+    const uint64_t tsize = vmask_ + 1;
+    pauli::reset_table_kernel<<<static_cast<unsigned>(std::min<uint64_t>((tsize + 255) / 256, 4096)), 256, 0,
+                                ctx_->stream>>>(vset(), tsize);
+    launched(ctx_);
   }
 
   void run(const uint64_t* gx, const uint64_t* gz, const double* gc, int ngens) {
@@ -1050,7 +1141,16 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
     use_device(ctx);
     const auto t0 = Clock::now();
     const liecl_b200_config cfg = default_config(cfg_in);
-    DenseEngine eng(ctx, d, keep_for(method), cfg);
+    const bool keep = keep_for(method);
+    auto cached = std::static_pointer_cast<DenseEngine>(ctx->dense_cache);
+    if (cached && cached->compatible(d, keep, cfg)) {
+      cached->reset(cfg);
+    } else {
+      ctx->dense_cache.reset();
+      cached = std::make_shared<DenseEngine>(ctx, d, keep, cfg);
+      ctx->dense_cache = cached;
+    }
+    DenseEngine& eng = *cached;
     eng.reset_stats();
     eng.run_candidates(reinterpret_cast<const double2*>(gens), ngens, false, nullptr, nullptr, true);
     eng.run_closure_pairs();
@@ -1081,7 +1181,16 @@ int liecl_b200_closure_pauli(liecl_b200_ctx* ctx, const uint64_t* x, const uint6
     const auto t0 = Clock::now();
     const liecl_b200_config cfg = default_config(cfg_in);
     const uint64_t k0 = ctx->kernels;
-    PauliEngine eng(ctx, qubits, keep_for(method), cfg);
+    const bool keep = keep_for(method);
+    auto cached = std::static_pointer_cast<PauliEngine>(ctx->pauli_cache);
+    if (cached && cached->compatible(qubits, keep, cfg)) {
+      cached->reset(cfg);
+    } else {
+      ctx->pauli_cache.reset();
+      cached = std::make_shared<PauliEngine>(ctx, qubits, keep, cfg);
+      ctx->pauli_cache = cached;
+    }
+    PauliEngine& eng = *cached;
     eng.run(x, z, coef, ngens);
     *stats = eng.stats();
     stats->kernels = ctx->kernels - k0;

@@ -50,23 +50,34 @@ enum class Epilogue { kStoreScaled, kSubtractNorm };
 //   kStoreScaled : C[n*ldc + m] = alpha * acc
 //   kSubtractNorm: C[n*ldc + m] = X[n*ldx + m] - acc, and
 //                  partial[blockIdx.x * N + n] = sum over this CTA's rows of |C|^2
+//
+// Split-K (k_chunk > 0, small grids): CTA z covers k in [z*k_chunk, (z+1)*k_chunk)
+// and stores its raw partial product at Cout + z*split_stride (kStoreScaled only);
+// splitk_reduce_* below sum the slices in fixed order (deterministic).
 template <bool A_KCONTIG, bool CONJ_A, Epilogue EPI>
 __global__ void __launch_bounds__(zg::THREADS)
 zgemm_dmma_kernel(int M, int N, int K, const double2* __restrict__ A, int64_t lda,
                   const double2* __restrict__ B, int64_t ldb, double2* __restrict__ Cout,
                   int64_t ldc, double alpha, const double2* __restrict__ X, int64_t ldx,
-                  double* __restrict__ partial) {
+                  double* __restrict__ partial, int k_chunk, int64_t split_stride) {
   using namespace zg;
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;
   double2* Bs = smem + STAGES * a_elems<A_KCONTIG>();
 
+  if (k_chunk > 0) {
+    const int kb = blockIdx.z * k_chunk;
+    A += A_KCONTIG ? static_cast<int64_t>(kb) : static_cast<int64_t>(kb) * lda;
+    B += kb;
+    K = min(K - kb, k_chunk);
+    Cout += blockIdx.z * split_stride;
+  }
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % WM, wn = warp / WM;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int KT = (K + BK - 1) / BK;
+  const int KT = K > 0 ? (K + BK - 1) / BK : 0;
 
   auto load_stage = [&](int stage, int kt) {
     const int k0 = kt * BK;
@@ -215,6 +226,54 @@ zgemm_dmma_kernel(int M, int N, int K, const double2* __restrict__ A, int64_t ld
         partial[static_cast<int64_t>(blockIdx.x) * N + gn] = s;
       }
     }
+  }
+}
+
+// P[i] = alpha * sum_z ws[z*stride + i], i < total (fixed slice order)
+__global__ void splitk_reduce_scale_kernel(const double2* __restrict__ ws, int slices, int64_t stride, int64_t total,
+                                           double alpha, double2* __restrict__ P) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int z = 0; z < slices; ++z) {
+      const double2 v = ws[z * stride + i];
+      re += v.x;
+      im += v.y;
+    }
+    P[i] = make_double2(alpha * re, alpha * im);
+  }
+}
+
+// R[b*M + m] = X[b*M + m] - sum_z ws[z*stride + b*M + m]; one CTA of zg::BM
+// threads per (row tile, column) also writes partial[mt*N + b] = sum |R|^2 over
+// its rows, the layout norm_finalize_kernel expects.
+__global__ void splitk_reduce_subtract_kernel(const double2* __restrict__ ws, int slices, int64_t stride, int M,
+                                              int N, const double2* __restrict__ X, double2* __restrict__ R,
+                                              double* __restrict__ partial) {
+  __shared__ double red[zg::BM / 32];
+  const int mt = blockIdx.x, b = blockIdx.y;
+  const int m = mt * zg::BM + threadIdx.x;
+  double s = 0.0;
+  if (m < M) {
+    const int64_t i = static_cast<int64_t>(b) * M + m;
+    double re = 0.0, im = 0.0;
+    for (int z = 0; z < slices; ++z) {
+      const double2 v = ws[z * stride + i];
+      re += v.x;
+      im += v.y;
+    }
+    const double2 x = X[i];
+    const double2 r = make_double2(x.x - re, x.y - im);
+    R[i] = r;
+    s = r.x * r.x + r.y * r.y;
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < zg::BM / 32; ++w) tot += red[w];
+    partial[static_cast<int64_t>(mt) * N + b] = tot;
   }
 }
 

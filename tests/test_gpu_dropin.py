@@ -1,0 +1,54 @@
+"""The C++ drop-in: a liecl consumer (reference headers + reference pauli/dense/
+operator/generators objects) linked with closure_b200.cpp instead of
+R:src/closure.cpp, calling liecl::run_closure / project_residual on the GPU."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEMO = os.path.join(ROOT, "paper_2506_01120_b200", "lib", "dropin", "liecl_dropin_demo")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def demo():
+    if not os.path.exists(DEMO):
+        pytest.skip("drop-in demo not built (needs the reference headers at build time)")
+    out = subprocess.run([DEMO], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    return json.loads(out.stdout)
+
+
+@pytest.mark.parametrize("method", ["orthonorm-dimonly", "orthonorm"])
+def test_dropin_dense_closure(demo, golden, method):
+    meta, g = golden(f"c0_tfim_n3_{method}")
+    r = demo[f"c0_{method}"]
+    assert r["dimension"] == meta["dimension"] == 9
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert r[k] == meta["stats"][k]
+    # demo prints each basis matrix row-major by Eigen linear index = column-major vec
+    basis = np.array(r["basis"]).reshape(9, -1, 2)
+    basis = basis[..., 0] + 1j * basis[..., 1]
+    assert np.abs(basis - g["basis"]).max() < 1e-10
+
+
+def test_dropin_pauli_closure(demo, golden):
+    meta, g = golden("c4_pauli_ring_n10_orthonorm-dimonly")
+    r = demo["c4"]
+    assert r["dimension"] == 380
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert r[k] == meta["stats"][k]
+    s = np.array(r["strings"])
+    assert np.array_equal(s[:, 0].astype(np.uint64), g["x"]) and np.array_equal(s[:, 1].astype(np.uint64), g["z"])
+    coef = g["coef_bits"].view(np.float64)
+    assert np.array_equal(s[:, 2:], coef)  # values equal (signed zeros may normalise)
+
+
+def test_dropin_project_residual_and_errors(demo):
+    pr = demo["project_residual"]
+    assert pr["coeff"] == [1.0, 0.0] and pr["residual_err"] < 1e-14
+    assert demo["capacity_error"] is True

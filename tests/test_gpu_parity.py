@@ -182,3 +182,32 @@ def test_null_generator_warning_and_kernels_launched():
     assert [wr.kind for wr in res.stats.warnings] == ["null_generator"]
     assert res.stats.warnings[0].detail == "generator 0 has norm 0.000000 and was skipped"
     assert native.kernel_count(0) > k0
+
+
+def test_c2_growth_phase_matches_reference(golden):
+    """Config 2 (n=6, d=64): the growth phase (rows 1..99, every accept of the
+    closure happens here) decision for decision against the reference's own
+    run (tests/golden, generated by tests/golden/make_golden.py --c2)."""
+    meta, g = golden("c2_random_sums_n6_s0_orthonorm-dimonly_rows100")
+    cfg = w.config2()
+    assert meta["digest"] == cfg.digest()
+    s = liecl.ClosureSession(64, config=liecl.ClosureConfig(tolerance=cfg.tol, record_log=True))
+    ind, rn, st = s.check_candidates(cfg.generators)
+    gen = g["log_m"] < 0
+    assert np.array_equal(ind, g["log_indep"][gen])
+    s.run_rows(1, meta["rows"])
+    log = s.log()
+    pairs = ~gen
+    assert s.size() == meta["dimension"] == 4095
+    assert np.array_equal(log["l"], g["log_l"][pairs]) and np.array_equal(log["m"], g["log_m"][pairs])
+    assert np.array_equal(log["null_cand"], g["log_null"][pairs])
+    assert np.array_equal(log["independent"], g["log_indep"][pairs])  # 4092 accepts, same order
+    acc = g["log_indep"][pairs] == 1
+    assert np.abs(log["residual_norm"][acc] - g["log_rn"][pairs][acc]).max() < 1e-9
+    V = s.basis()
+    rows = g["basis_rows"]
+    assert rel_err(V[rows], g["basis"]) < BASIS_RTOL
+    wts = np.random.default_rng(1234).standard_normal(4096) + 1j * np.random.default_rng(1234).standard_normal(4096)
+    rng = np.random.default_rng(1234)
+    wts = rng.standard_normal(4096) + 1j * rng.standard_normal(4096)
+    assert rel_err(V @ wts, g["basis_checksum"]) < BASIS_RTOL

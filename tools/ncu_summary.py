@@ -1,0 +1,77 @@
+"""Summarise ncu artefacts into profiles/ (committed evidence).
+
+  python tools/ncu_summary.py launches <launches.csv> <out.txt>
+  python tools/ncu_summary.py full <report.ncu-rep> <out.json>
+"""
+import collections
+import csv
+import json
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__cycles_elapsed.avg.per_second"]
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for d in data:
+        if d.get("Metric Name") == "gpu__time_duration.sum":
+            name = d["Kernel Name"].split("(")[0]
+            agg[name][0] += 1
+            agg[name][1] += float(d["Metric Value"].replace(",", ""))
+    tot = sum(v[1] for v in agg.values())
+    lines = [f"# ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off ({path})",
+             "# launches  total_ms   share  kernel"]
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"{v[0]:8d} {v[1] / 1e6:10.3f} {100 * v[1] / tot:6.2f}%  {k}")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+def full(path, out):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        rec = {"kernel": r[hdr.index("Kernel Name")].split("(")[0]}
+        for k in KEYS:
+            if k in hdr:
+                v = r[hdr.index(k)].replace(",", "")
+                try:
+                    rec[k] = float(v)
+                except ValueError:
+                    rec[k] = v
+                rec[k + ".unit"] = units[hdr.index(k)]
+        res.append(rec)
+    zg = [r for r in res if "zgemm" in r["kernel"]]
+
+    def to_bytes(r, k):
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r.get(k + ".unit", "byte"), 1)
+        return r[k] * scale
+    summary = {"source": path, "launches": res}
+    if zg:
+        summary["dram_bytes_per_launch"] = sum(to_bytes(r, "dram__bytes_read.sum") + to_bytes(r, "dram__bytes_write.sum")
+                                               for r in zg) / len(zg)
+    json.dump(summary, open(out, "w"), indent=1)
+    print(json.dumps(summary, indent=1)[:3000])
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
