@@ -128,4 +128,52 @@ commutator_norm_kernel(const double2* __restrict__ basis, int64_t g0, int count,
   }
 }
 
+// Any other dimension (subspace-restricted operators, d = 2, 6, 20, 128, ...):
+// one CTA per pair, plain FP64 FMAs with operands through L1/L2, same fused
+// norm / null / normalise epilogue. Off the BASELINE configs' hot path.
+__global__ void __launch_bounds__(256)
+commutator_generic_kernel(const double2* __restrict__ basis, int dim, int64_t g0, int count, double tol,
+                          bool normalize, double2* __restrict__ out, double* __restrict__ hnorm,
+                          int* __restrict__ is_null) {
+  __shared__ double red[8];
+  const int j = blockIdx.x;
+  if (j >= count) return;
+  int64_t l, m;
+  pair_from_index(g0 + j, l, m);
+  const int64_t D2 = static_cast<int64_t>(dim) * dim;
+  const double2* pa = basis + l * D2;
+  const double2* pb = basis + m * D2;
+  double2* o = out + static_cast<int64_t>(j) * D2;
+  double sumsq = 0.0;
+  for (int64_t e = threadIdx.x; e < D2; e += blockDim.x) {
+    const int i = static_cast<int>(e % dim), c = static_cast<int>(e / dim);
+    double re = 0.0, im = 0.0;
+    for (int k = 0; k < dim; ++k) {
+      const double2 aik = pa[i + static_cast<int64_t>(k) * dim], bkc = pb[k + static_cast<int64_t>(c) * dim];
+      const double2 bik = pb[i + static_cast<int64_t>(k) * dim], akc = pa[k + static_cast<int64_t>(c) * dim];
+      re += aik.x * bkc.x - aik.y * bkc.y - (bik.x * akc.x - bik.y * akc.y);
+      im += aik.x * bkc.y + aik.y * bkc.x - (bik.x * akc.y + bik.y * akc.x);
+    }
+    o[e] = make_double2(re, im);
+    sumsq += re * re + im * im;
+  }
+  sumsq = warp_sum(sumsq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sumsq;
+  __syncthreads();
+  double total = 0.0;
+  for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) total += red[w];
+  const double hn = sqrt(total) / sqrt(static_cast<double>(dim));
+  const bool nul = !(hn > tol);
+  if (threadIdx.x == 0) {
+    hnorm[j] = hn;
+    is_null[j] = nul ? 1 : 0;
+  }
+  if (!normalize) return;
+  const double s = nul ? 0.0 : 1.0 / hn;
+  for (int64_t e = threadIdx.x; e < D2; e += blockDim.x) {
+    const double2 v = o[e];
+    o[e] = make_double2(v.x * s, v.y * s);
+  }
+}
+
 } // namespace liecl_b200

@@ -88,7 +88,7 @@ int main() {
     bool threw = false;
     try {
       ClosureConfig tiny = cfg;
-      tiny.max_dim = 3;
+      tiny.max_dim = 2;  // {X, Z} closes to su(2): the third accept must raise
       run_closure(std::vector<Operator>{V[0], zexp}, Method::orthonorm_dimonly, tiny);
     } catch (const CapacityError&) {
       threw = true;

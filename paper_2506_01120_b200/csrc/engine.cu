@@ -310,8 +310,7 @@ public:
   DenseEngine(liecl_b200_ctx* ctx, int d, bool keep_original, const liecl_b200_config& cfg)
       : ctx_(ctx), d_(d), D_(static_cast<int64_t>(d) * d), keep_(keep_original), tol_(cfg.tolerance),
         record_(cfg.record_log != 0) {
-    if (d != 8 && d != 16 && d != 32 && d != 64 && d != 128 && d != 256)
-      throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be a power of two in [8, 256]");
+    if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
     cap_ = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : D_;
     const int64_t budget = int64_t(16) << 30;  // bytes for the three D x B candidate slabs
@@ -532,7 +531,12 @@ private:
     case 16: launch_comm<16>(basis, g0, cnt); break;
     case 32: launch_comm<32>(basis, g0, cnt); break;
     case 64: launch_comm<64>(basis, g0, cnt); break;
-    default: throw Error(LIECL_B200_INVALID_INPUT, "commutator kernel supports d <= 64");
+    default: {
+      Timer t(ctx_, 2, 16.0 * d_ * d_ * static_cast<double>(d_) * cnt);
+      commutator_generic_kernel<<<cnt, 256, 0, ctx_->stream>>>(basis, d_, g0, cnt, tol_, true, C_.p, hn_.p, nul_.p);
+      launched(ctx_);
+      t.stop();
+    }
     }
   }
   template <int DIM> void launch_comm(const double2* basis, int64_t g0, int cnt) {
@@ -1220,7 +1224,7 @@ int liecl_b200_project_residual_dense(liecl_b200_ctx* ctx, const double* V, int6
 int liecl_b200_commutator_dense(liecl_b200_ctx* ctx, const double* a, const double* b, int32_t d, double* out) {
   return guarded([&] {
     if (!ctx || !a || !b || !out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-    if (d > 64) throw Error(LIECL_B200_INVALID_INPUT, "commutator kernel supports d <= 64");
+    if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
     use_device(ctx);
     const int64_t D = static_cast<int64_t>(d) * d;
     DevBuf<double2> basis, o;
@@ -1246,7 +1250,9 @@ int liecl_b200_commutator_dense(liecl_b200_ctx* ctx, const double* a, const doub
     case 16: launch(std::integral_constant<int, 16>{}); break;
     case 32: launch(std::integral_constant<int, 32>{}); break;
     case 64: launch(std::integral_constant<int, 64>{}); break;
-    default: throw Error(LIECL_B200_INVALID_INPUT, "commutator kernel supports d in {8,16,32,64}");
+    default:
+      commutator_generic_kernel<<<1, 256, 0, ctx->stream>>>(basis.p, d, 0, 1, -1.0, false, o.p, hn.p, nul.p);
+      launched(ctx);
     }
     CU(cudaMemcpyAsync(out, o.p, D * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));

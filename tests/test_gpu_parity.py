@@ -211,3 +211,23 @@ def test_c2_growth_phase_matches_reference(golden):
     rng = np.random.default_rng(1234)
     wts = rng.standard_normal(4096) + 1j * rng.standard_normal(4096)
     assert rel_err(V @ wts, g["basis_checksum"]) < BASIS_RTOL
+
+
+@pytest.mark.parametrize("d", [2, 6, 12, 128])
+def test_generic_dimensions_vs_oracle(port, d):
+    # off the DMMA-templated sizes (e.g. subspace-restricted operators): the
+    # generic commutator kernel + the same projection GEMMs
+    rng = np.random.default_rng(d)
+    a = rng.standard_normal(d * d) + 1j * rng.standard_normal(d * d)
+    b = rng.standard_normal(d * d) + 1j * rng.standard_normal(d * d)
+    A, B = liecl.DenseOperator.from_vec(a, d), liecl.DenseOperator.from_vec(b, d)
+    assert rel_err(liecl.commutator(A, B).vec(), port.commutator_dense(a, b, d)) < 1e-13
+    if d <= 12:
+        gens = np.stack([a - a.reshape(d, d, order="F").conj().T.ravel(order="F"),
+                         b - b.reshape(d, d, order="F").conj().T.ravel(order="F")])  # anti-Hermitian
+        res = liecl.closure_dense_arrays(gens, d, liecl.Method.orthonorm_dimonly,
+                                         liecl.ClosureConfig(tolerance=1e-10, record_log=True))
+        o = port.closure_dense(gens, d, tol=1e-10)
+        assert res.dimension == o.dimension
+        assert np.array_equal(res.decision_log["independent"], o.log["independent"])
+        assert rel_err(res.basis_array, o.basis) < BASIS_RTOL
