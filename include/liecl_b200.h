@@ -59,6 +59,10 @@ typedef struct {
   uint32_t record_log;      /* 1: fill the decision log                          */
   double deadline_seconds;  /* > 0: relative deadline, checked per batch         */
   int64_t batch_max;        /* 0 = engine default (candidates per device batch)  */
+  uint32_t field;           /* 0 = auto: exactly anti-Hermitian operators take the
+                               packed-real path (su(d)/u(d), 4x fewer projection
+                               flops); 1 = always the general complex path     */
+  uint32_t reserved;
 } liecl_b200_config;
 
 /* liecl::ClosureStats (R:include/liecl/closure.hpp:63-69) + engine counters */

@@ -1,0 +1,312 @@
+// Anti-Hermitian (su(d) / u(d)) path: packed-real layout kernels.
+//
+// Packed layout of an anti-Hermitian d x d matrix A (d^2 reals, column-major
+// like the complex vec layout): M(i,j) = Re A(i,j) and M(j,i) = Im A(i,j) for
+// i < j, M(i,i) = Im A(i,i). The reference inner product is
+// <A,B> = (1/d) sum_k w_k M_A(k) M_B(k) with w = 2 off the diagonal, 1 on it,
+// and ||A||^2 = <A,A> -- the same numbers the complex formulas give
+// (R:src/dense.cpp:53-63) for anti-Hermitian inputs.
+//
+// The commutator of two anti-Hermitian matrices needs one complex product:
+// with P = A B, B A = (A B)^dagger, so h = P - P^dagger (R:src/dense.cpp:65-68),
+// and h is again anti-Hermitian: half the flops of the general kernel.
+#pragma once
+
+#include "commutator.cuh"
+#include "common.cuh"
+
+namespace liecl_b200 {
+
+// exact structure test: x(j,i) == -conj(x(i,j)) for all i <= j (diag: Re == 0)
+__global__ void antiherm_violations_kernel(const double2* __restrict__ x, int64_t count, int d,
+                                           unsigned long long* __restrict__ viol) {
+  const int64_t D2 = static_cast<int64_t>(d) * d;
+  const int64_t total = count * D2;
+  unsigned long long bad = 0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / D2, k = e % D2;
+    const int i = static_cast<int>(k % d), j = static_cast<int>(k / d);
+    if (i > j) continue;
+    const double2 a = x[c * D2 + i + static_cast<int64_t>(j) * d];
+    const double2 b = x[c * D2 + j + static_cast<int64_t>(i) * d];
+    if (!(b.x == -a.x && b.y == a.y)) ++bad;
+  }
+  if (bad) atomicAdd(viol, bad);
+}
+
+__global__ void pack_ah_kernel(const double2* __restrict__ in, int64_t count, int d, double* __restrict__ out) {
+  const int64_t D2 = static_cast<int64_t>(d) * d;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count * D2;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / D2, k = e % D2;
+    const int i = static_cast<int>(k % d), j = static_cast<int>(k / d);
+    double v;
+    if (i < j) v = in[c * D2 + k].x;                                   // Re A(i,j)
+    else if (i > j) v = in[c * D2 + j + static_cast<int64_t>(i) * d].y;  // Im A(j,i)
+    else v = in[c * D2 + k].y;                                         // Im A(i,i)
+    out[e] = v;
+  }
+}
+
+__global__ void unpack_ah_kernel(const double* __restrict__ in, int64_t count, int d, double2* __restrict__ out) {
+  const int64_t D2 = static_cast<int64_t>(d) * d;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count * D2;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / D2, k = e % D2;
+    const int i = static_cast<int>(k % d), j = static_cast<int>(k / d);
+    const double* m = in + c * D2;
+    double2 v;
+    if (i < j) v = make_double2(m[k], m[j + static_cast<int64_t>(i) * d]);
+    else if (i > j) v = make_double2(-m[j + static_cast<int64_t>(i) * d], m[k]);
+    else v = make_double2(0.0, m[k]);
+    out[e] = v;
+  }
+}
+
+// weighted column norms: out[j] = sqrt(sum_k w_k x_k^2) / sqrt(d)
+__global__ void column_norm_ah_kernel(const double* __restrict__ x, int d, double* __restrict__ out) {
+  __shared__ double red[32];
+  const int64_t D2 = static_cast<int64_t>(d) * d;
+  const double* c = x + static_cast<int64_t>(blockIdx.x) * D2;
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < D2; e += blockDim.x) s += ((e % (d + 1)) == 0 ? 1.0 : 2.0) * c[e] * c[e];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) out[blockIdx.x] = sqrt(v) / sqrt(static_cast<double>(d));
+  }
+}
+
+// out = x * (1/nrm) per column (null: zeros)
+__global__ void scale_columns_ah_kernel(const double* __restrict__ x, const double* __restrict__ nrm, double tol,
+                                        int64_t D2, double* __restrict__ out) {
+  const int j = blockIdx.y;
+  const double n = nrm[j];
+  const double s = n > tol ? 1.0 / n : 0.0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < D2;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[static_cast<int64_t>(j) * D2 + e] = x[static_cast<int64_t>(j) * D2 + e] * s;
+}
+
+// K3 on the packed path: V slot = r * s, Vw slot = w .* (r * s) (exact
+// doubling), originals slot = h_unit copy (Alg. 3).
+__global__ void append_ah_kernel(const double* __restrict__ src, double s, int d, double* __restrict__ v,
+                                 double* __restrict__ vw, const double* __restrict__ orig_src,
+                                 double* __restrict__ orig_dst) {
+  const int64_t D2 = static_cast<int64_t>(d) * d;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < D2;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = src[e] * s;
+    v[e] = x;
+    vw[e] = ((e % (d + 1)) == 0 ? 1.0 : 2.0) * x;
+    if (orig_dst) orig_dst[e] = orig_src[e];
+  }
+}
+
+// Vw = w .* V for n packed vectors (set_basis on the packed path)
+__global__ void weight_ah_kernel(const double* __restrict__ v, int64_t count, int d, double* __restrict__ vw) {
+  const int64_t D2 = static_cast<int64_t>(d) * d;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count * D2;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    vw[e] = (((e % D2) % (d + 1)) == 0 ? 1.0 : 2.0) * v[e];
+}
+
+template <int DIM> struct CommAhShape {
+  using C = CommShape<DIM>;
+  static constexpr int LDP = DIM + 1;  // packed staging stride (conflict free both ways)
+  static constexpr int PACKED = DIM * LDP;
+  static constexpr int SMEM_PER_PAIR = (4 * C::PLANE + 2 * PACKED) * 8 + C::WARPS_PER_PAIR * 8;
+  static constexpr int SMEM = C::PAIRS_PER_CTA * SMEM_PER_PAIR;
+};
+
+// K1 on the packed path: pairs [g0, g0+count) of the packed commutator basis;
+// writes packed h_unit, ||h||, null flag. One DMMA product P = A B per pair.
+template <int DIM>
+__global__ void __launch_bounds__(256)
+commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, double tol, bool normalize,
+                     double* __restrict__ out, double* __restrict__ hnorm, int* __restrict__ is_null) {
+  using S = CommShape<DIM>;
+  using SA = CommAhShape<DIM>;
+  constexpr int D2 = DIM * DIM;
+  extern __shared__ __align__(16) double csm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int slot = warp / S::WARPS_PER_PAIR;
+  const int wip = warp % S::WARPS_PER_PAIR;
+  const int j = blockIdx.x * S::PAIRS_PER_CTA + slot;
+  const bool active = j < count;
+  const int tip = threadIdx.x - slot * S::WARPS_PER_PAIR * 32;
+  constexpr int NT = S::WARPS_PER_PAIR * 32;
+
+  double* base = csm + slot * (SA::SMEM_PER_PAIR / 8);
+  double* are = base;
+  double* aim = are + S::PLANE;
+  double* bre = aim + S::PLANE;
+  double* bim = bre + S::PLANE;
+  double* pa = bim + S::PLANE;      // packed A, stride LDP
+  double* pb = pa + SA::PACKED;     // packed B
+  double* red = pb + SA::PACKED;
+
+  int64_t l = 0, m = 0;
+  if (active) {
+    pair_from_index(g0 + j, l, m);
+    const double* ga = basis + l * D2;
+    const double* gb = basis + m * D2;
+    for (int e = tip; e < D2; e += NT) {
+      const int i = e % DIM, k = e / DIM;
+      pa[i + k * SA::LDP] = ga[e];
+      pb[i + k * SA::LDP] = gb[e];
+    }
+  }
+  __syncthreads();
+  if (active) {
+    // planes: element (i, k) of the complex matrix at [i*LD + k]
+    for (int e = tip; e < D2; e += NT) {
+      const int i = e % DIM, k = e / DIM;
+      double ar, ai, br, bi;
+      if (i < k) {
+        ar = pa[i + k * SA::LDP]; ai = pa[k + i * SA::LDP];
+        br = pb[i + k * SA::LDP]; bi = pb[k + i * SA::LDP];
+      } else if (i > k) {
+        ar = -pa[k + i * SA::LDP]; ai = pa[i + k * SA::LDP];
+        br = -pb[k + i * SA::LDP]; bi = pb[i + k * SA::LDP];
+      } else {
+        ar = 0.0; ai = pa[i + i * SA::LDP];
+        br = 0.0; bi = pb[i + i * SA::LDP];
+      }
+      are[i * S::LD + k] = ar;
+      aim[i * S::LD + k] = ai;
+      bre[i * S::LD + k] = br;
+      bim[i * S::LD + k] = bi;
+    }
+  }
+  __syncthreads();
+
+  double cre[S::TILES_PER_WARP][2], cim[S::TILES_PER_WARP][2];
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < S::TILES_PER_WARP; ++q) {
+      const int tile = wip * S::TILES_PER_WARP + q;
+      const int ti = (tile / (DIM / 8)) * 8, tj = (tile % (DIM / 8)) * 8;
+      double c0r = 0.0, c1r = 0.0, c0i = 0.0, c1i = 0.0;
+#pragma unroll 4
+      for (int k0 = 0; k0 < DIM; k0 += 4) {
+        const int k = k0 + t;
+        const double xr = are[(ti + g) * S::LD + k], xi = aim[(ti + g) * S::LD + k];
+        const double yr = bre[k * S::LD + tj + g], yi = bim[k * S::LD + tj + g];
+        dmma_8x8x4(c0r, c1r, xr, yr);
+        dmma_8x8x4(c0r, c1r, -xi, yi);
+        dmma_8x8x4(c0i, c1i, xr, yi);
+        dmma_8x8x4(c0i, c1i, xi, yr);
+      }
+      cre[q][0] = c0r; cre[q][1] = c1r; cim[q][0] = c0i; cim[q][1] = c1i;
+    }
+  }
+  __syncthreads();  // everyone done reading A / B planes
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < S::TILES_PER_WARP; ++q) {
+      const int tile = wip * S::TILES_PER_WARP + q;
+      const int ti = (tile / (DIM / 8)) * 8, tj = (tile % (DIM / 8)) * 8;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        are[(ti + g) * S::LD + tj + 2 * t + h] = cre[q][h];  // P(i, k) re
+        aim[(ti + g) * S::LD + tj + 2 * t + h] = cim[q][h];  // P(i, k) im
+      }
+    }
+  }
+  __syncthreads();
+  double sumsq = 0.0;
+  if (active) {
+    // packed h = P - P^dagger; kept in the (free) B re-plane, stride D2 layout
+    for (int e = tip; e < D2; e += NT) {
+      const int i = e % DIM, k = e / DIM;
+      double v;
+      if (i < k) v = are[i * S::LD + k] - are[k * S::LD + i];
+      else if (i > k) v = aim[k * S::LD + i] + aim[i * S::LD + k];
+      else v = 2.0 * aim[i * S::LD + i];
+      bre[e] = v;
+      sumsq += (i == k ? 1.0 : 2.0) * v * v;
+    }
+  }
+  sumsq = warp_sum(sumsq);
+  if (lane == 0) red[wip] = sumsq;
+  __syncthreads();
+  if (!active) return;
+  double total = 0.0;
+#pragma unroll
+  for (int w = 0; w < S::WARPS_PER_PAIR; ++w) total += red[w];
+  const double hn = sqrt(total) / sqrt(static_cast<double>(DIM));
+  const bool nul = !(hn > tol);
+  if (wip == 0 && lane == 0) {
+    hnorm[j] = hn;
+    is_null[j] = nul ? 1 : 0;
+  }
+  const double s = !normalize ? 1.0 : (nul ? 0.0 : 1.0 / hn);
+  double* o = out + static_cast<int64_t>(j) * D2;
+  for (int e = tip; e < D2; e += NT) o[e] = bre[e] * s;
+}
+
+// packed path, any even d: one CTA per pair, operands through L1/L2
+__global__ void __launch_bounds__(256)
+commutator_ah_generic_kernel(const double* __restrict__ basis, int dim, int64_t g0, int count, double tol,
+                             bool normalize, double* __restrict__ out, double* __restrict__ hnorm,
+                             int* __restrict__ is_null) {
+  __shared__ double red[8];
+  const int j = blockIdx.x;
+  if (j >= count) return;
+  int64_t l, m;
+  pair_from_index(g0 + j, l, m);
+  const int64_t D2 = static_cast<int64_t>(dim) * dim;
+  const double* ma = basis + l * D2;
+  const double* mb = basis + m * D2;
+  auto elem = [&](const double* mp, int i, int k, double& re, double& im) {
+    if (i < k) { re = mp[i + static_cast<int64_t>(k) * dim]; im = mp[k + static_cast<int64_t>(i) * dim]; }
+    else if (i > k) { re = -mp[k + static_cast<int64_t>(i) * dim]; im = mp[i + static_cast<int64_t>(k) * dim]; }
+    else { re = 0.0; im = mp[i + static_cast<int64_t>(i) * dim]; }
+  };
+  // P(i,k) = sum_q A(i,q) B(q,k); packed h needs P(i,k) and P(k,i)
+  auto pval = [&](int i, int k, double& re, double& im) {
+    re = 0.0;
+    im = 0.0;
+    for (int q = 0; q < dim; ++q) {
+      double ar, ai, br, bi;
+      elem(ma, i, q, ar, ai);
+      elem(mb, q, k, br, bi);
+      re += ar * br - ai * bi;
+      im += ar * bi + ai * br;
+    }
+  };
+  double* o = out + static_cast<int64_t>(j) * D2;
+  double sumsq = 0.0;
+  for (int64_t e = threadIdx.x; e < D2; e += blockDim.x) {
+    const int i = static_cast<int>(e % dim), k = static_cast<int>(e / dim);
+    double r1, i1, r2, i2;
+    double v;
+    if (i < k) { pval(i, k, r1, i1); pval(k, i, r2, i2); v = r1 - r2; }
+    else if (i > k) { pval(k, i, r1, i1); pval(i, k, r2, i2); v = i1 + i2; }
+    else { pval(i, i, r1, i1); v = 2.0 * i1; }
+    o[e] = v;
+    sumsq += (i == k ? 1.0 : 2.0) * v * v;
+  }
+  sumsq = warp_sum(sumsq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sumsq;
+  __syncthreads();
+  double total = 0.0;
+  for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) total += red[w];
+  const double hn = sqrt(total) / sqrt(static_cast<double>(dim));
+  const bool nul = !(hn > tol);
+  if (threadIdx.x == 0) {
+    hnorm[j] = hn;
+    is_null[j] = nul ? 1 : 0;
+  }
+  if (!normalize) return;
+  const double s = nul ? 0.0 : 1.0 / hn;
+  for (int64_t e = threadIdx.x; e < D2; e += blockDim.x) o[e] *= s;
+}
+
+} // namespace liecl_b200

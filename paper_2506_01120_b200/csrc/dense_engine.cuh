@@ -1,0 +1,588 @@
+// DenseEngine -- the batched cursor loop (replaces run_engine + OrthonormStrategy,
+// R:src/closure.cpp:267-310, 339-348, 356-473). Included by engine.cu inside its
+// anonymous namespace (uses Error, DevBuf, HostBuf, Timer, launched, the GEMM
+// launchers and the kernels declared there).
+//
+// Two arithmetic fields, chosen from the data:
+//   kComplex  : general complex128 operators (vec layout, 2 doubles/element),
+//               complex DMMA GEMMs (zgemm_dmma.cuh), full commutator kernel.
+//   kAntiHerm : every operator so far is exactly anti-Hermitian (the i*H
+//               generators of every dense BASELINE config, and their closure):
+//               packed real layout (ah.cuh), real DMMA GEMMs with the exact
+//               weights of the reference inner product (dgemm_dmma.cuh), and
+//               the single-product commutator h = P - P^dagger. 4x fewer
+//               projection flops, same verdicts; the basis is returned in the
+//               reference's complex layout. Non-anti-Hermitian input later on
+//               promotes the engine to kComplex (unpacking the basis).
+
+enum class Field { kUnset, kComplex, kAntiHerm };
+
+class DenseEngine {
+public:
+  DenseEngine(liecl_b200_ctx* ctx, int d, bool keep_original, const liecl_b200_config& cfg)
+      : ctx_(ctx), d_(d), D_(static_cast<int64_t>(d) * d), keep_(keep_original), tol_(cfg.tolerance),
+        record_(cfg.record_log != 0), force_complex_(cfg.field == 1) {
+    if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
+    if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
+    cap_ = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : D_;
+    const int64_t budget = int64_t(16) << 30;  // bytes for the three D x B candidate slabs (complex)
+    bmax_ = cfg.batch_max > 0 ? cfg.batch_max : std::clamp<int64_t>(budget / (3 * D_ * 16), 64, 8192);
+    set_deadline(cfg);
+    sqrt_d_ = std::sqrt(static_cast<double>(d));
+    B_cur_ = std::min<int64_t>(bmax_, 512);
+    small_.ensure(2);
+  }
+
+  bool compatible(int d, bool keep, const liecl_b200_config& cfg) const {
+    const int64_t cap = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : static_cast<int64_t>(d) * d;
+    return d == d_ && keep == keep_ && cap == cap_ && (cfg.batch_max <= 0 || cfg.batch_max == bmax_) &&
+           (cfg.field == 1) == force_complex_;
+  }
+  void reset(const liecl_b200_config& cfg) {
+    tol_ = cfg.tolerance;
+    if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
+    record_ = cfg.record_log != 0;
+    set_deadline(cfg);
+    n_o_ = n_b_ = 0;
+    field_ = Field::kUnset;
+    B_cur_ = std::min<int64_t>(bmax_, 512);
+    reset_stats();
+  }
+
+  // ---- state / results ----------------------------------------------------
+  Field field() const { return field_; }
+  int64_t ortho_size() const { return n_o_; }
+  int64_t basis_size() const { return keep_ ? n_b_ : n_o_; }
+  liecl_b200_stats stats() {
+    liecl_b200_stats s = st_;
+    s.dimension = static_cast<uint64_t>(basis_size());
+    s.warnings = warns_.size();
+    s.kernels = ctx_->kernels - kernels0_;
+    return s;
+  }
+  const std::vector<Warning>& warnings() const { return warns_; }
+  const std::vector<liecl_b200_decision>& log() const { return log_; }
+  void reset_stats() {
+    st_ = liecl_b200_stats{};
+    warns_.clear();
+    log_.clear();
+    kernels0_ = ctx_->kernels;
+  }
+
+  // Replace the basis by n operators (complex vec layout, host or device).
+  void set_basis(const double2* src, int64_t n, bool on_device) {
+    if (n > cap_) throw Error(LIECL_B200_CAPACITY, "basis larger than the session capacity");
+    DevBuf<double2> tmp;
+    tmp.ensure(static_cast<size_t>(std::max<int64_t>(n, 1) * D_));
+    if (n > 0)
+      CU(cudaMemcpyAsync(tmp.p, src, static_cast<size_t>(n * D_) * sizeof(double2),
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx_->stream));
+    const Field f = classify(tmp.p, n);
+    n_o_ = n_b_ = 0;
+    vcap_ = 0;
+    V_.release();
+    Vw_.release();
+    O_.release();
+    field_ = f;
+    alloc_batch();
+    ensure_capacity(std::min<int64_t>(cap_ + 1, n + 1));
+    if (n > 0) {
+      if (field_ == Field::kAntiHerm) {
+        pack_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(tmp.p, n, d_, V_.p);
+        launched(ctx_);
+        weight_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(V_.p, n, d_, Vw_.p);
+        launched(ctx_);
+      } else {
+        CU(cudaMemcpyAsync(V_.p, tmp.p, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToDevice,
+                           ctx_->stream));
+      }
+      if (keep_)
+        CU(cudaMemcpyAsync(O_.p, V_.p, static_cast<size_t>(n * vw()) * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx_->stream));
+    }
+    CU(cudaStreamSynchronize(ctx_->stream));
+    n_o_ = n_b_ = n;
+  }
+
+  // generator loop (R:src/closure.cpp:378-403); also the config-3 candidate
+  // stream. Per-candidate verdicts / residual norms when requested.
+  void run_candidates(const double2* cands, int64_t count, bool on_device, int32_t* indep_out, double* rn_out,
+                      bool generator_warnings) {
+    for (int64_t c0 = 0; c0 < count; c0 += bmax_) {
+      check_deadline();
+      const int cnt = static_cast<int>(std::min<int64_t>(bmax_, count - c0));
+      stage_.ensure(static_cast<size_t>(cnt * D_));
+      CU(cudaMemcpyAsync(stage_.p, cands + c0 * D_, static_cast<size_t>(cnt * D_) * sizeof(double2),
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx_->stream));
+      admit(stage_.p, cnt);
+      if (field_ == Field::kAntiHerm) {
+        pack_ah_kernel<<<grid_for(cnt * D_), 256, 0, ctx_->stream>>>(stage_.p, cnt, d_, R_.p);
+        launched(ctx_);
+        column_norm_ah_kernel<<<cnt, 256, 0, ctx_->stream>>>(R_.p, d_, hn_.p);
+        launched(ctx_);
+        dim3 g2(static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 64)), cnt);
+        scale_columns_ah_kernel<<<g2, 256, 0, ctx_->stream>>>(R_.p, hn_.p, tol_, D_, C_.p);
+        launched(ctx_);
+      } else {
+        column_norm_kernel<<<cnt, 256, 0, ctx_->stream>>>(stage_.p, D_, sqrt_d_, hn_.p);
+        launched(ctx_);
+        dim3 g2(static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 64)), cnt);
+        scale_columns_kernel<<<g2, 256, 0, ctx_->stream>>>(stage_.p, hn_.p, tol_, D_, cplx(C_.p));
+        launched(ctx_);
+      }
+      project(V_.p, Vw_.p, n_o_, C_.p, cnt, R_.p, rn1_.p);
+      CU(cudaMemcpyAsync(h_hn_.p, hn_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaMemcpyAsync(h_rn1_.p, rn1_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      for (int j = 0; j < cnt; ++j) h_nul_.p[j] = !(h_hn_.p[j] > tol_);
+      ++st_.batches;
+      apply(cnt, /*pair_g0=*/-1, c0, generator_warnings, indep_out ? indep_out + c0 : nullptr,
+            rn_out ? rn_out + c0 : nullptr);
+    }
+  }
+
+  // cursor pairs [g_begin, g_end), all with l < basis size at batch start (the
+  // reference's row loop re-reads |basis| every row)
+  void run_pairs(int64_t g_begin, int64_t g_end) {
+    int64_t g = g_begin;
+    while (g < g_end) {
+      const int64_t nb = basis_size();
+      const int64_t avail = nb * (nb - 1) / 2;
+      if (g >= avail)
+        throw Error(LIECL_B200_INVALID_INPUT,
+                    "cursor pair " + std::to_string(g) + " refers to a basis element that does not exist yet");
+      check_deadline();
+      const int64_t cnt = std::min({B_cur_, avail - g, g_end - g});
+      run_adaptive_batch(g, cnt);
+      g += cnt;
+    }
+  }
+
+  // the whole closure after the generator loop: all pairs until exhausted
+  void run_closure_pairs() {
+    int64_t g = 0;
+    for (;;) {
+      const int64_t nb = basis_size();
+      const int64_t avail = nb * (nb - 1) / 2;
+      if (g >= avail) break;
+      check_deadline();
+      const int64_t cnt = std::min(B_cur_, avail - g);
+      run_adaptive_batch(g, cnt);
+      g += cnt;
+    }
+  }
+
+  // basis (originals for Alg. 3) or orthonormal tuple -> host, complex vec layout
+  void download(bool ortho, double* out) {
+    const int64_t n = ortho ? n_o_ : basis_size();
+    if (n == 0) return;
+    const double* src = (ortho || !keep_) ? V_.p : O_.p;
+    if (field_ == Field::kAntiHerm) {
+      DevBuf<double2> tmp;
+      tmp.ensure(static_cast<size_t>(n * D_));
+      unpack_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(src, n, d_, tmp.p);
+      launched(ctx_);
+      CU(cudaMemcpyAsync(out, tmp.p, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToHost,
+                         ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+    } else {
+      CU(cudaMemcpyAsync(out, src, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToHost,
+                         ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+    }
+  }
+
+  // single-vector project_residual for the drop-in API (general complex field)
+  void project_residual(const double2* h_host, double* r_host, double* coeffs_host) {
+    if (field_ == Field::kUnset) {
+      field_ = Field::kComplex;
+      alloc_batch();
+      ensure_capacity(std::min<int64_t>(cap_ + 1, 2));
+    }
+    if (field_ != Field::kComplex) promote_to_complex();
+    CU(cudaMemcpyAsync(C_.p, h_host, D_ * sizeof(double2), cudaMemcpyHostToDevice, ctx_->stream));
+    if (n_o_ == 0) {
+      CU(cudaMemcpyAsync(r_host, C_.p, D_ * sizeof(double2), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      return;
+    }
+    project(V_.p, nullptr, n_o_, C_.p, 1, R_.p, rn1_.p);
+    CU(cudaMemcpyAsync(coeffs_host, P_.p, n_o_ * sizeof(double2), cudaMemcpyDeviceToHost, ctx_->stream));
+    project(V_.p, nullptr, n_o_, R_.p, 1, R_.p, rn1_.p);
+    CU(cudaMemcpyAsync(r_host, R_.p, D_ * sizeof(double2), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+  }
+
+private:
+  static double2* cplx(double* p) { return reinterpret_cast<double2*>(p); }
+  static const double2* cplx(const double* p) { return reinterpret_cast<const double2*>(p); }
+  int ew() const { return field_ == Field::kAntiHerm ? 1 : 2; }  // doubles per element
+  int64_t vw() const { return D_ * ew(); }                        // doubles per vector
+  static unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)); }
+
+  void set_deadline(const liecl_b200_config& cfg) {
+    has_deadline_ = cfg.deadline_seconds > 0;
+    if (has_deadline_)
+      deadline_ = Clock::now() + std::chrono::duration_cast<Clock::duration>(
+                                     std::chrono::duration<double>(cfg.deadline_seconds));
+  }
+  void check_deadline() {
+    if (has_deadline_ && Clock::now() > deadline_)
+      throw Error(LIECL_B200_TIMEOUT, "closure computation exceeded its deadline");
+  }
+
+  // field of a batch of complex operators (exact anti-Hermitian test on device)
+  Field classify(const double2* x, int64_t count) {
+    if (force_complex_ || (d_ & 1) || count == 0) return Field::kComplex;
+    CU(cudaMemsetAsync(small_.p, 0, sizeof(unsigned long long), ctx_->stream));
+    antiherm_violations_kernel<<<grid_for(count * D_), 256, 0, ctx_->stream>>>(x, count, d_, small_.p);
+    launched(ctx_);
+    unsigned long long bad = 0;
+    CU(cudaMemcpyAsync(&bad, small_.p, sizeof bad, cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    return bad == 0 ? Field::kAntiHerm : Field::kComplex;
+  }
+
+  // new input: fix the field on first use, promote when the structure breaks
+  void admit(const double2* x, int64_t count) {
+    const Field f = (field_ == Field::kComplex) ? Field::kComplex : classify(x, count);
+    if (field_ == Field::kUnset) {
+      field_ = (n_o_ == 0) ? f : Field::kComplex;
+      alloc_batch();
+      ensure_capacity(std::min<int64_t>(cap_ + 1, std::max<int64_t>(64, (int64_t(1) << 30) / (D_ * 16))));
+    } else if (field_ == Field::kAntiHerm && f == Field::kComplex) {
+      promote_to_complex();
+    }
+  }
+
+  void promote_to_complex() {
+    if (field_ == Field::kComplex) return;
+    const int64_t cap = vcap_;
+    DevBuf<double> nv, no;
+    nv.ensure(static_cast<size_t>(std::max<int64_t>(cap, 1) * D_ * 2));
+    CU(cudaMemsetAsync(nv.p, 0, nv.n * sizeof(double), ctx_->stream));
+    if (n_o_ > 0) {
+      unpack_ah_kernel<<<grid_for(n_o_ * D_), 256, 0, ctx_->stream>>>(V_.p, n_o_, d_, cplx(nv.p));
+      launched(ctx_);
+    }
+    if (keep_) {
+      no.ensure(static_cast<size_t>(std::max<int64_t>(cap, 1) * D_ * 2));
+      CU(cudaMemsetAsync(no.p, 0, no.n * sizeof(double), ctx_->stream));
+      if (n_b_ > 0) {
+        unpack_ah_kernel<<<grid_for(n_b_ * D_), 256, 0, ctx_->stream>>>(O_.p, n_b_, d_, cplx(no.p));
+        launched(ctx_);
+      }
+    }
+    CU(cudaStreamSynchronize(ctx_->stream));
+    std::swap(V_.p, nv.p); std::swap(V_.n, nv.n);
+    if (keep_) { std::swap(O_.p, no.p); std::swap(O_.n, no.n); }
+    Vw_.release();
+    field_ = Field::kComplex;
+    vcap_ = cap;
+    alloc_batch();
+    P_.release();
+    P_.ensure(static_cast<size_t>(std::max<int64_t>(vcap_ + 2, 2) * bmax_ * 2));
+    CU(cudaMemsetAsync(P_.p, 0, P_.n * sizeof(double), ctx_->stream));
+  }
+
+  void alloc_batch() {
+    const int64_t b = bmax_;
+    const size_t cols = static_cast<size_t>(b) * vw();
+    C_.ensure(cols);
+    R_.ensure(cols);
+    X_.ensure(cols);
+    Y_.ensure(static_cast<size_t>(vw()));
+    const int64_t mtiles = (D_ + zg::BM - 1) / zg::BM;  // >= the real GEMM's tile count
+    partial_.ensure(static_cast<size_t>(mtiles * b));
+    rn1_.ensure(b); rn2_.ensure(b); yn_.ensure(1); h_y_.ensure(1);
+    hn_.ensure(b); nul_.ensure(b); idx_.ensure(b);
+    h_rn1_.ensure(b); h_rn2_.ensure(b); h_hn_.ensure(b); h_nul_.ensure(b); h_idx_.ensure(b);
+  }
+
+  // room for n basis vectors; slabs beyond the live vectors stay zero (the
+  // packed GEMMs read one zero row past an odd basis count)
+  void ensure_capacity(int64_t n) {
+    if (n <= vcap_) return;
+    const int64_t nc = std::min<int64_t>(cap_ + 2, std::max<int64_t>(n, 2 * vcap_));
+    auto grow = [&](DevBuf<double>& buf, int64_t live) {
+      DevBuf<double> nb;
+      nb.ensure(static_cast<size_t>(nc * vw()));
+      CU(cudaMemsetAsync(nb.p, 0, nb.n * sizeof(double), ctx_->stream));
+      if (live > 0)
+        CU(cudaMemcpyAsync(nb.p, buf.p, static_cast<size_t>(live * vw()) * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      std::swap(buf.p, nb.p);
+      std::swap(buf.n, nb.n);
+    };
+    grow(V_, n_o_);
+    if (field_ == Field::kAntiHerm) grow(Vw_, n_o_);
+    if (keep_) grow(O_, n_b_);
+    P_.release();
+    P_.ensure(static_cast<size_t>((nc + 2) * bmax_ * ew()));
+    CU(cudaMemsetAsync(P_.p, 0, P_.n * sizeof(double), ctx_->stream));
+    vcap_ = nc;
+  }
+
+  // One CGS pass of `count` columns X against basis columns Vb[0:n] (weighted
+  // copy Vwb on the packed path): Rout = X - Vb beta, beta = <Vb, X>,
+  // rn = ||Rout|| (Rout may alias X).
+  void project(const double* Vb, const double* Vwb, int64_t n, const double* X, int count, double* Rout, double* rn) {
+    int mtiles;
+    if (field_ == Field::kAntiHerm) {
+      const int64_t ldp = (n + 1) & ~int64_t(1);  // even: 16-byte aligned P columns
+      rgemm_project(ctx_, Vwb, n, D_, X, count, P_.p, ldp, 1.0 / d_);
+      rgemm_subtract(ctx_, Vb, n, D_, P_.p, ldp, X, count, Rout, partial_.p, d_);
+      mtiles = static_cast<int>((D_ + rg::BM - 1) / rg::BM);
+    } else {
+      gemm_project(ctx_, cplx(Vb), n, D_, cplx(X), count, cplx(P_.p), 1.0 / d_);
+      gemm_subtract(ctx_, cplx(Vb), n, D_, cplx(P_.p), cplx(X), count, cplx(Rout), partial_.p);
+      mtiles = static_cast<int>((D_ + zg::BM - 1) / zg::BM);
+    }
+    norm_finalize_kernel<<<(count + 255) / 256, 256, 0, ctx_->stream>>>(partial_.p, mtiles, count, sqrt_d_, rn);
+    launched(ctx_);
+  }
+
+  void launch_commutators(int64_t g0, int cnt) {
+    const double* basis = keep_ ? O_.p : V_.p;
+    if (field_ == Field::kAntiHerm) {
+      switch (d_) {
+      case 8: launch_comm_ah<8>(basis, g0, cnt); return;
+      case 16: launch_comm_ah<16>(basis, g0, cnt); return;
+      case 32: launch_comm_ah<32>(basis, g0, cnt); return;
+      case 64: launch_comm_ah<64>(basis, g0, cnt); return;
+      default: {
+        Timer t(ctx_, 2, 8.0 * d_ * d_ * static_cast<double>(d_) * cnt);
+        commutator_ah_generic_kernel<<<cnt, 256, 0, ctx_->stream>>>(basis, d_, g0, cnt, tol_, true, C_.p, hn_.p,
+                                                                    nul_.p);
+        launched(ctx_);
+        t.stop();
+        return;
+      }
+      }
+    }
+    switch (d_) {
+    case 8: launch_comm<8>(cplx(basis), g0, cnt); break;
+    case 16: launch_comm<16>(cplx(basis), g0, cnt); break;
+    case 32: launch_comm<32>(cplx(basis), g0, cnt); break;
+    case 64: launch_comm<64>(cplx(basis), g0, cnt); break;
+    default: {
+      Timer t(ctx_, 2, 16.0 * d_ * d_ * static_cast<double>(d_) * cnt);
+      commutator_generic_kernel<<<cnt, 256, 0, ctx_->stream>>>(cplx(basis), d_, g0, cnt, tol_, true, cplx(C_.p),
+                                                               hn_.p, nul_.p);
+      launched(ctx_);
+      t.stop();
+    }
+    }
+  }
+  template <int DIM> void launch_comm(const double2* basis, int64_t g0, int cnt) {
+    using S = CommShape<DIM>;
+    static bool attr = false;
+    if (!attr) {
+      CU(cudaFuncSetAttribute(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
+      attr = true;
+    }
+    const int blocks = (cnt + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA;
+    Timer t(ctx_, 2, 16.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
+    commutator_norm_kernel<DIM><<<blocks, 256, S::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, cplx(C_.p),
+                                                                         hn_.p, nul_.p);
+    launched(ctx_);
+    t.stop();
+  }
+  template <int DIM> void launch_comm_ah(const double* basis, int64_t g0, int cnt) {
+    using S = CommShape<DIM>;
+    using SA = CommAhShape<DIM>;
+    static bool attr = false;
+    if (!attr) {
+      CU(cudaFuncSetAttribute(commutator_ah_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, SA::SMEM));
+      attr = true;
+    }
+    const int blocks = (cnt + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA;
+    Timer t(ctx_, 2, 8.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
+    commutator_ah_kernel<DIM><<<blocks, 256, SA::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, C_.p, hn_.p,
+                                                                        nul_.p);
+    launched(ctx_);
+    t.stop();
+  }
+
+  // Batch size follows the accept rate: it doubles while batches accept
+  // nothing (saturated phase: big GEMMs, few syncs) and halves when more than
+  // a quarter is accepted (growth phase: little speculative waste).
+  void run_adaptive_batch(int64_t g, int64_t cnt) {
+    const uint64_t before = st_.accepted;
+    run_pair_batch(g, static_cast<int>(cnt));
+    const uint64_t acc = st_.accepted - before;
+    if (acc == 0) B_cur_ = std::min<int64_t>(2 * B_cur_, bmax_);
+    else if (acc * 4 > static_cast<uint64_t>(cnt)) B_cur_ = std::max<int64_t>(64, B_cur_ / 2);
+  }
+
+  void run_pair_batch(int64_t g0, int cnt) {
+    launch_commutators(g0, cnt);
+    project(V_.p, Vw_.p, n_o_, C_.p, cnt, R_.p, rn1_.p);
+    CU(cudaMemcpyAsync(h_nul_.p, nul_.p, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(h_rn1_.p, rn1_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    if (record_) CU(cudaMemcpyAsync(h_hn_.p, hn_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    st_.commutators_evaluated += static_cast<uint64_t>(cnt);
+    ++st_.batches;
+    apply(cnt, g0, 0, false, nullptr, nullptr);
+  }
+
+  void where(int64_t pair_g0, int64_t cand0, int j, int64_t& l, int64_t& m) const {
+    if (pair_g0 >= 0) {
+      pair_from_index(pair_g0 + j, l, m);
+    } else {
+      l = cand0 + j;
+      m = -1;
+    }
+  }
+  std::string where_str(int64_t l, int64_t m) const {
+    return m < 0 ? "generator " + std::to_string(l) : "pair (" + std::to_string(l) + "," + std::to_string(m) + ")";
+  }
+  void log_decision(int64_t l, int64_t m, int nul, int ind, int rc, double rn) {
+    if (record_) log_.push_back({l, m, nul, ind, rc, 0, rn});
+  }
+  void note(int64_t l, int64_t m, double rn, bool ind) {  // R:src/closure.cpp:324-337
+    if (borderline(rn, tol_))
+      warns_.push_back({"borderline_residual",
+                        where_str(l, m) + ": residual " + fmt_double(rn) + " within 10x of tolerance " +
+                            fmt_double(tol_) + (ind ? " (accepted)" : " (rejected)"),
+                        rn});
+  }
+
+  // ordered apply of one batch whose null flags (h_nul_) and pass-1 norms
+  // (h_rn1_; residuals in R_) are known
+  void apply(int cnt, int64_t pair_g0, int64_t cand0, bool generators, int32_t* indep_out, double* rn_out) {
+    const int64_t n_bs = n_o_;
+    const int64_t W = vw();
+    const double screen = tol_ / 20.0;
+    int nsurv = 0;
+    for (int j = 0; j < cnt; ++j)
+      if (!h_nul_.p[j] && h_rn1_.p[j] > screen) h_idx_.p[nsurv++] = j;
+    st_.survivors += static_cast<uint64_t>(nsurv);
+    if (nsurv > 0) {
+      CU(cudaMemcpyAsync(idx_.p, h_idx_.p, nsurv * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+      dim3 gg(static_cast<unsigned>(std::min<int64_t>((W + 255) / 256, 64)), nsurv);
+      gather_words_kernel<<<gg, 256, 0, ctx_->stream>>>(R_.p, idx_.p, W, X_.p);
+      launched(ctx_);
+      project(V_.p, Vw_.p, n_bs, X_.p, nsurv, X_.p, rn2_.p);  // second CGS pass, in place
+      CU(cudaMemcpyAsync(h_rn2_.p, rn2_.p, nsurv * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+    }
+    constexpr int kBlock = 64;  // survivors re-projected together against in-batch accepts
+    int s = 0;
+    int blk_end = 0;
+    int64_t n_blk = n_bs;
+    auto vp = [&](DevBuf<double>& b, int64_t i) { return b.p + i * W; };
+    for (int j = 0; j < cnt; ++j) {
+      int64_t l, m;
+      where(pair_g0, cand0, j, l, m);
+      if (h_nul_.p[j]) {
+        if (generators) {
+          const double gn = h_hn_.p[j];
+          warns_.push_back({"null_generator",
+                            "generator " + std::to_string(l) + " has norm " + fmt_double(gn) + " and was skipped",
+                            gn});
+        }
+        log_decision(l, m, 1, 0, 0, record_ ? (generators ? h_hn_.p[j] : 0.0) : 0.0);
+        if (indep_out) indep_out[j] = 0;
+        if (rn_out) rn_out[j] = 0.0;
+        continue;
+      }
+      ++st_.independence_checks;
+      if (s >= nsurv || h_idx_.p[s] != j) {  // certified reject from pass 1
+        log_decision(l, m, 0, 0, 0, h_rn1_.p[j]);
+        if (indep_out) indep_out[j] = 0;
+        if (rn_out) rn_out[j] = h_rn1_.p[j];
+        continue;
+      }
+      const int k = s++;
+      if (k >= blk_end && n_o_ > n_bs) {
+        // refresh the next block of survivors against everything accepted
+        // since batch start (CGS2 against the new vectors)
+        blk_end = std::min(nsurv, k + kBlock);
+        const int nb = blk_end - k;
+        double* xb = vp(X_, k);
+        project(vp(V_, n_bs), Vw_.p ? vp(Vw_, n_bs) : nullptr, n_o_ - n_bs, xb, nb, xb, rn2_.p + k);
+        project(vp(V_, n_bs), Vw_.p ? vp(Vw_, n_bs) : nullptr, n_o_ - n_bs, xb, nb, xb, rn2_.p + k);
+        CU(cudaMemcpyAsync(h_rn2_.p + k, rn2_.p + k, nb * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+        CU(cudaStreamSynchronize(ctx_->stream));
+        n_blk = n_o_;
+        st_.rechecks += static_cast<uint64_t>(nb);
+      } else if (k >= blk_end) {
+        blk_end = std::min(nsurv, k + kBlock);
+        n_blk = n_o_;
+      }
+      double rn = h_rn2_.p[k];
+      const double* resid = vp(X_, k);
+      int rc = n_o_ > n_bs ? 1 : 0;
+      if (n_o_ > n_blk && rn > tol_) {
+        // accepts inside this block: re-check against them (CGS2)
+        CU(cudaMemcpyAsync(Y_.p, resid, W * sizeof(double), cudaMemcpyDeviceToDevice, ctx_->stream));
+        project(vp(V_, n_blk), Vw_.p ? vp(Vw_, n_blk) : nullptr, n_o_ - n_blk, Y_.p, 1, Y_.p, yn_.p);
+        project(vp(V_, n_blk), Vw_.p ? vp(Vw_, n_blk) : nullptr, n_o_ - n_blk, Y_.p, 1, Y_.p, yn_.p);
+        CU(cudaMemcpyAsync(h_y_.p, yn_.p, sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+        CU(cudaStreamSynchronize(ctx_->stream));
+        rn = h_y_.p[0];
+        resid = Y_.p;
+        ++st_.rechecks;
+        rc = 1;
+      }
+      const bool ind = rn > tol_;
+      note(l, m, rn, ind);
+      log_decision(l, m, 0, ind ? 1 : 0, rc, rn);
+      if (indep_out) indep_out[j] = ind ? 1 : 0;
+      if (rn_out) rn_out[j] = rn;
+      if (!ind) continue;
+      if (basis_size() >= cap_)
+        throw Error(LIECL_B200_CAPACITY,
+                    "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
+      if (n_o_ + 2 > vcap_) {
+        // growing moves the slabs: keep the residual source valid across it
+        if (resid != Y_.p) CU(cudaMemcpyAsync(Y_.p, resid, W * sizeof(double), cudaMemcpyDeviceToDevice, ctx_->stream));
+        resid = Y_.p;
+        ensure_capacity(n_o_ + 2);
+      }
+      const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 256));
+      if (field_ == Field::kAntiHerm) {
+        append_ah_kernel<<<blocks, 256, 0, ctx_->stream>>>(resid, 1.0 / rn, d_, vp(V_, n_o_), vp(Vw_, n_o_),
+                                                            keep_ ? vp(C_, j) : nullptr, keep_ ? vp(O_, n_b_) : nullptr);
+      } else {
+        append_scaled_kernel<<<blocks, 256, 0, ctx_->stream>>>(
+            cplx(resid), 1.0 / rn, D_, cplx(vp(V_, n_o_)), keep_ ? cplx(vp(C_, j)) : nullptr,
+            keep_ ? cplx(vp(O_, n_b_)) : nullptr);
+      }
+      launched(ctx_);
+      ++n_o_;
+      if (keep_) ++n_b_;
+      ++st_.accepted;
+    }
+    if (!keep_) n_b_ = n_o_;
+  }
+
+  liecl_b200_ctx* ctx_;
+  int d_;
+  int64_t D_;
+  bool keep_;
+  double tol_;
+  bool record_;
+  bool force_complex_;
+  Field field_ = Field::kUnset;
+  int64_t cap_ = 0, bmax_ = 0, B_cur_ = 0;
+  double sqrt_d_ = 1.0;
+  bool has_deadline_ = false;
+  Clock::time_point deadline_{};
+  int64_t n_o_ = 0, n_b_ = 0;
+  int64_t vcap_ = 0;  // basis vectors the slabs (and the beta buffer) can hold
+  uint64_t kernels0_ = 0;
+  liecl_b200_stats st_{};
+  std::vector<Warning> warns_;
+  std::vector<liecl_b200_decision> log_;
+  DevBuf<double> V_, Vw_, O_, C_, R_, X_, Y_, P_;  // element width ew() doubles
+  DevBuf<double2> stage_;                          // complex input staging
+  DevBuf<double> partial_, rn1_, rn2_, hn_, yn_;
+  DevBuf<int> nul_, idx_;
+  DevBuf<unsigned long long> small_;
+  HostBuf<double> h_rn1_, h_rn2_, h_hn_, h_y_;
+  HostBuf<int> h_nul_, h_idx_;
+};

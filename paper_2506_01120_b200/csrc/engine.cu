@@ -37,7 +37,9 @@
 #include <vector>
 
 #include "../../include/liecl_b200.h"
+#include "ah.cuh"
 #include "commutator.cuh"
+#include "dgemm_dmma.cuh"
 #include "pauli.cuh"
 #include "vecops.cuh"
 #include "zgemm_dmma.cuh"
@@ -305,418 +307,79 @@ void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, 
 
 // --------------------------------------------------------- dense engine ---
 
-class DenseEngine {
-public:
-  DenseEngine(liecl_b200_ctx* ctx, int d, bool keep_original, const liecl_b200_config& cfg)
-      : ctx_(ctx), d_(d), D_(static_cast<int64_t>(d) * d), keep_(keep_original), tol_(cfg.tolerance),
-        record_(cfg.record_log != 0) {
-    if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
-    if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
-    cap_ = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : D_;
-    const int64_t budget = int64_t(16) << 30;  // bytes for the three D x B candidate slabs
-    bmax_ = cfg.batch_max > 0 ? cfg.batch_max : std::clamp<int64_t>(budget / (3 * D_ * 16), 64, 8192);
-    if (cfg.deadline_seconds > 0)
-      deadline_ = Clock::now() + std::chrono::duration_cast<Clock::duration>(
-                                     std::chrono::duration<double>(cfg.deadline_seconds));
-    has_deadline_ = cfg.deadline_seconds > 0;
-    sqrt_d_ = std::sqrt(static_cast<double>(d));
-    B_cur_ = std::min<int64_t>(bmax_, 512);
-    alloc_batch(bmax_);
-    ensure_capacity(std::min<int64_t>(cap_ + 1, std::max<int64_t>(64, (int64_t(1) << 30) / (D_ * 16))));
-  }
+// ------------------------------------------------ packed-real GEMM launch ---
 
-  // Same shape (d, method, cap, batch) as a previous closure: reuse the
-  // device/pinned workspaces (latency-bound small configs pay no allocation).
-  bool compatible(int d, bool keep, const liecl_b200_config& cfg) const {
-    const int64_t cap = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : static_cast<int64_t>(d) * d;
-    return d == d_ && keep == keep_ && cap == cap_ && (cfg.batch_max <= 0 || cfg.batch_max == bmax_);
+template <bool KC, REpi E> void rgemm_attr_once() {
+  static bool done = false;
+  if (!done) {
+    CU(cudaFuncSetAttribute(dgemm_dmma_kernel<KC, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            rg::smem_bytes<KC>()));
+    done = true;
   }
-  void reset(const liecl_b200_config& cfg) {
-    tol_ = cfg.tolerance;
-    if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
-    record_ = cfg.record_log != 0;
-    has_deadline_ = cfg.deadline_seconds > 0;
-    if (has_deadline_)
-      deadline_ = Clock::now() + std::chrono::duration_cast<Clock::duration>(
-                                     std::chrono::duration<double>(cfg.deadline_seconds));
-    n_o_ = n_b_ = 0;
-    B_cur_ = std::min<int64_t>(bmax_, 512);
-    reset_stats();
-  }
+}
 
-  // ---- state / results ----------------------------------------------------
-  int64_t ortho_size() const { return n_o_; }
-  int64_t basis_size() const { return keep_ ? n_b_ : n_o_; }
-  const double2* basis_ptr() const { return keep_ ? O_.p : V_.p; }
-  const double2* ortho_ptr() const { return V_.p; }
-  liecl_b200_stats stats() {
-    liecl_b200_stats s = st_;
-    s.dimension = static_cast<uint64_t>(basis_size());
-    s.warnings = warns_.size();
-    s.kernels = ctx_->kernels - kernels0_;
-    return s;
+// P[n x count] (ld ldp) = alpha * Vw[:, 0:n]^T X   -- beta on the packed path
+void rgemm_project(liecl_b200_ctx* ctx, const double* Vw, int64_t n, int64_t D, const double* X, int count,
+                   double* P, int64_t ldp, double alpha) {
+  if (n == 0 || count == 0) return;
+  rgemm_attr_once<true, REpi::kStoreScaled>();
+  dim3 grid((n + rg::BM - 1) / rg::BM, (count + rg::BN - 1) / rg::BN);
+  Timer t(ctx, 0, 2.0 * static_cast<double>(n) * static_cast<double>(D) * count);
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y * 2, D);  // 2 CTA-waves per 128^2 tile
+  if (slices <= 1) {
+    dgemm_dmma_kernel<true, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<true>(), ctx->stream>>>(
+        static_cast<int>(n), count, static_cast<int>(D), Vw, D, X, D, P, ldp, alpha, nullptr, 0, nullptr, 0, 0, 0);
+    launched(ctx);
+  } else {
+    const int chunk = static_cast<int>(((D + slices - 1) / slices + rg::BK - 1) / rg::BK * rg::BK);
+    slices = static_cast<int>((D + chunk - 1) / chunk);
+    const int64_t stride = ldp * count;
+    ctx->splitk_ws.ensure(static_cast<size_t>((slices * stride + 1) / 2));
+    double* ws = reinterpret_cast<double*>(ctx->splitk_ws.p);
+    grid.z = slices;
+    dgemm_dmma_kernel<true, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<true>(), ctx->stream>>>(
+        static_cast<int>(n), count, static_cast<int>(D), Vw, D, X, D, ws, ldp, 1.0, nullptr, 0, nullptr, 0, chunk,
+        stride);
+    launched(ctx);
+    rsplitk_reduce_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>((stride + 255) / 256, 1024)), 256, 0,
+                                  ctx->stream>>>(ws, slices, stride, stride, alpha, P);
+    launched(ctx);
   }
-  const std::vector<Warning>& warnings() const { return warns_; }
-  const std::vector<liecl_b200_decision>& log() const { return log_; }
-  void reset_stats() {
-    st_ = liecl_b200_stats{};
-    warns_.clear();
-    log_.clear();
-    kernels0_ = ctx_->kernels;
-  }
+  t.stop();
+}
 
-  void set_basis(const double2* src, int64_t n, bool on_device) {
-    if (n > cap_) throw Error(LIECL_B200_CAPACITY, "basis larger than the session capacity");
-    ensure_capacity(std::min<int64_t>(cap_ + 1, n + 1));
-    const size_t bytes = static_cast<size_t>(n * D_) * sizeof(double2);
-    CU(cudaMemcpyAsync(V_.p, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                       ctx_->stream));
-    if (keep_) CU(cudaMemcpyAsync(O_.p, V_.p, bytes, cudaMemcpyDeviceToDevice, ctx_->stream));
-    n_o_ = n_b_ = n;
+// R = X - V[:, 0:n] P (P ld ldp); partial[mt][b] = sum_rows w R^2
+void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, const double* P, int64_t ldp,
+                    const double* X, int count, double* R, double* partial, int d) {
+  rgemm_attr_once<false, REpi::kSubtractNorm>();
+  dim3 grid((D + rg::BM - 1) / rg::BM, (count + rg::BN - 1) / rg::BN);
+  Timer t(ctx, 1, 2.0 * static_cast<double>(n) * static_cast<double>(D) * count);
+  const int64_t kpad = (n + 1) & ~int64_t(1);  // even K: reads one zero row of V past an odd n
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y * 2, kpad);
+  if (slices <= 1) {
+    dgemm_dmma_kernel<false, REpi::kSubtractNorm><<<grid, rg::THREADS, rg::smem_bytes<false>(), ctx->stream>>>(
+        static_cast<int>(D), count, static_cast<int>(kpad), V, D, P, ldp, R, D, 1.0, X, D, partial, d, 0, 0);
+    launched(ctx);
+  } else {
+    rgemm_attr_once<false, REpi::kStoreScaled>();
+    const int chunk = static_cast<int>(((kpad + slices - 1) / slices + rg::BK - 1) / rg::BK * rg::BK);
+    slices = static_cast<int>((kpad + chunk - 1) / chunk);
+    const int64_t stride = D * count;
+    ctx->splitk_ws.ensure(static_cast<size_t>((slices * stride + 1) / 2));
+    double* ws = reinterpret_cast<double*>(ctx->splitk_ws.p);
+    grid.z = slices;
+    dgemm_dmma_kernel<false, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<false>(), ctx->stream>>>(
+        static_cast<int>(D), count, static_cast<int>(kpad), V, D, P, ldp, ws, D, 1.0, nullptr, 0, nullptr, d, chunk,
+        stride);
+    launched(ctx);
+    rsplitk_reduce_subtract_kernel<<<dim3(static_cast<unsigned>((D + rg::BM - 1) / rg::BM), count), rg::BM, 0,
+                                     ctx->stream>>>(ws, slices, stride, static_cast<int>(D), count, X, R, partial, d);
+    launched(ctx);
   }
+  t.stop();
+}
 
-  // generator loop (R:src/closure.cpp:378-403); also the config-3 candidate
-  // stream. Returns per-candidate verdicts when requested.
-  void run_candidates(const double2* cands, int64_t count, bool on_device, int32_t* indep_out, double* rn_out,
-                      bool generator_warnings) {
-    for (int64_t c0 = 0; c0 < count; c0 += bmax_) {
-      check_deadline();
-      const int cnt = static_cast<int>(std::min<int64_t>(bmax_, count - c0));
-      CU(cudaMemcpyAsync(R_.p, cands + c0 * D_, static_cast<size_t>(cnt * D_) * sizeof(double2),
-                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx_->stream));
-      column_norm_kernel<<<cnt, 256, 0, ctx_->stream>>>(R_.p, D_, sqrt_d_, hn_.p);
-      launched(ctx_);
-      dim3 g2(static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 64)), cnt);
-      scale_columns_kernel<<<g2, 256, 0, ctx_->stream>>>(R_.p, hn_.p, tol_, D_, C_.p);
-      launched(ctx_);
-      project(V_.p, n_o_, C_.p, cnt, R_.p, rn1_.p);
-      CU(cudaMemcpyAsync(h_hn_.p, hn_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
-      CU(cudaMemcpyAsync(h_rn1_.p, rn1_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
-      CU(cudaStreamSynchronize(ctx_->stream));
-      for (int j = 0; j < cnt; ++j) h_nul_.p[j] = !(h_hn_.p[j] > tol_);
-      ++st_.batches;
-      apply(cnt, /*pair_g0=*/-1, c0, generator_warnings, indep_out ? indep_out + c0 : nullptr,
-            rn_out ? rn_out + c0 : nullptr);
-    }
-  }
-
-  // cursor pairs [g_begin, g_end) in batches, all with l < basis size at
-  // batch start (the reference's row loop re-reads |basis| every row).
-  void run_pairs(int64_t g_begin, int64_t g_end) {
-    int64_t g = g_begin;
-    while (g < g_end) {
-      const int64_t nb = basis_size();
-      const int64_t avail = nb * (nb - 1) / 2;
-      if (g >= avail) {
-        throw Error(LIECL_B200_INVALID_INPUT, "cursor pair " + std::to_string(g) +
-                                                  " refers to a basis element that does not exist yet");
-      }
-      check_deadline();
-      const int64_t cnt = std::min({B_cur_, avail - g, g_end - g});
-      run_adaptive_batch(g, cnt);
-      g += cnt;
-    }
-  }
-
-  // the whole closure after the generator loop: all pairs until exhausted
-  void run_closure_pairs() {
-    int64_t g = 0;
-    for (;;) {
-      const int64_t nb = basis_size();
-      const int64_t avail = nb * (nb - 1) / 2;
-      if (g >= avail) break;
-      check_deadline();
-      const int64_t cnt = std::min(B_cur_, avail - g);
-      run_adaptive_batch(g, cnt);
-      g += cnt;
-    }
-  }
-
-  // Batch size follows the accept rate: it doubles while batches accept
-  // nothing (saturated phase: big GEMMs, few syncs) and halves when more
-  // than a quarter is accepted (growth phase: little speculative waste).
-  void run_adaptive_batch(int64_t g, int64_t cnt) {
-    const uint64_t before = st_.accepted;
-    run_pair_batch(g, static_cast<int>(cnt));
-    const uint64_t acc = st_.accepted - before;
-    if (acc == 0) B_cur_ = std::min<int64_t>(2 * B_cur_, bmax_);
-    else if (acc * 4 > static_cast<uint64_t>(cnt)) B_cur_ = std::max<int64_t>(64, B_cur_ / 2);
-  }
-
-  void download(const double2* src, int64_t n, double* out) {
-    CU(cudaMemcpyAsync(out, src, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToHost,
-                       ctx_->stream));
-    CU(cudaStreamSynchronize(ctx_->stream));
-  }
-
-  // single-vector project_residual for the drop-in API: r = CGS2(h, V[0:n])
-  void project_residual(const double2* h_host, double* r_host, double* coeffs_host) {
-    CU(cudaMemcpyAsync(C_.p, h_host, D_ * sizeof(double2), cudaMemcpyHostToDevice, ctx_->stream));
-    if (n_o_ == 0) {
-      CU(cudaMemcpyAsync(r_host, C_.p, D_ * sizeof(double2), cudaMemcpyDeviceToHost, ctx_->stream));
-      CU(cudaStreamSynchronize(ctx_->stream));
-      return;
-    }
-    project(V_.p, n_o_, C_.p, 1, R_.p, rn1_.p);
-    CU(cudaMemcpyAsync(coeffs_host, P_.p, n_o_ * sizeof(double2), cudaMemcpyDeviceToHost, ctx_->stream));
-    project(V_.p, n_o_, R_.p, 1, R_.p, rn1_.p);
-    CU(cudaMemcpyAsync(r_host, R_.p, D_ * sizeof(double2), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaStreamSynchronize(ctx_->stream));
-  }
-
-private:
-  void alloc_batch(int64_t b) {
-    const size_t cols = static_cast<size_t>(b) * D_;
-    C_.ensure(cols);
-    R_.ensure(cols);
-    X_.ensure(cols);
-    Y_.ensure(static_cast<size_t>(D_));
-    const int64_t mtiles = (D_ + zg::BM - 1) / zg::BM;
-    partial_.ensure(static_cast<size_t>(mtiles * b));
-    rn1_.ensure(b);
-    rn2_.ensure(b);
-    yn_.ensure(1);
-    h_y_.ensure(1);
-    hn_.ensure(b);
-    nul_.ensure(b);
-    idx_.ensure(b);
-    h_rn1_.ensure(b);
-    h_rn2_.ensure(b);
-    h_hn_.ensure(b);
-    h_nul_.ensure(b);
-    h_idx_.ensure(b);
-  }
-
-  // room for n basis vectors in the slab(s) and the beta buffer; grows
-  // geometrically up to cap + 1 (copying the live vectors)
-  void ensure_capacity(int64_t n) {
-    if (n <= vcap_) return;
-    const int64_t nc = std::min<int64_t>(cap_ + 1, std::max<int64_t>(n, 2 * vcap_));
-    auto grow = [&](DevBuf<double2>& buf, int64_t live) {
-      DevBuf<double2> nb;
-      nb.ensure(static_cast<size_t>(nc * D_));
-      if (live > 0)
-        CU(cudaMemcpyAsync(nb.p, buf.p, static_cast<size_t>(live * D_) * sizeof(double2), cudaMemcpyDeviceToDevice,
-                           ctx_->stream));
-      CU(cudaStreamSynchronize(ctx_->stream));
-      std::swap(buf.p, nb.p);
-      std::swap(buf.n, nb.n);
-    };
-    grow(V_, n_o_);
-    if (keep_) grow(O_, n_b_);
-    P_.release();
-    P_.ensure(static_cast<size_t>(nc * bmax_));
-    vcap_ = nc;
-  }
-
-  void check_deadline() {
-    if (has_deadline_ && Clock::now() > deadline_)
-      throw Error(LIECL_B200_TIMEOUT, "closure computation exceeded its deadline");
-  }
-
-  // one CGS pass of `count` columns X against basis columns Vb[0:n]:
-  // Rout = X - Vb (Vb^H X / d), rn = ||Rout|| (Rout may alias X)
-  void project(const double2* Vb, int64_t n, const double2* X, int count, double2* Rout, double* rn) {
-    gemm_project(ctx_, Vb, n, D_, X, count, P_.p, 1.0 / d_);
-    gemm_subtract(ctx_, Vb, n, D_, P_.p, X, count, Rout, partial_.p);
-    const int mtiles = static_cast<int>((D_ + zg::BM - 1) / zg::BM);
-    norm_finalize_kernel<<<(count + 255) / 256, 256, 0, ctx_->stream>>>(partial_.p, mtiles, count, sqrt_d_, rn);
-    launched(ctx_);
-  }
-
-  void launch_commutators(int64_t g0, int cnt) {
-    const double2* basis = keep_ ? O_.p : V_.p;
-    switch (d_) {
-    case 8: launch_comm<8>(basis, g0, cnt); break;
-    case 16: launch_comm<16>(basis, g0, cnt); break;
-    case 32: launch_comm<32>(basis, g0, cnt); break;
-    case 64: launch_comm<64>(basis, g0, cnt); break;
-    default: {
-      Timer t(ctx_, 2, 16.0 * d_ * d_ * static_cast<double>(d_) * cnt);
-      commutator_generic_kernel<<<cnt, 256, 0, ctx_->stream>>>(basis, d_, g0, cnt, tol_, true, C_.p, hn_.p, nul_.p);
-      launched(ctx_);
-      t.stop();
-    }
-    }
-  }
-  template <int DIM> void launch_comm(const double2* basis, int64_t g0, int cnt) {
-    using S = CommShape<DIM>;
-    static bool attr = false;
-    if (!attr) {
-      CU(cudaFuncSetAttribute(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-      attr = true;
-    }
-    const int blocks = (cnt + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA;
-    Timer t(ctx_, 2, 16.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
-    commutator_norm_kernel<DIM><<<blocks, 256, S::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, C_.p, hn_.p,
-                                                                         nul_.p);
-    launched(ctx_);
-    t.stop();
-  }
-
-  void run_pair_batch(int64_t g0, int cnt) {
-    launch_commutators(g0, cnt);
-    project(V_.p, n_o_, C_.p, cnt, R_.p, rn1_.p);
-    CU(cudaMemcpyAsync(h_nul_.p, nul_.p, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaMemcpyAsync(h_rn1_.p, rn1_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
-    if (record_) CU(cudaMemcpyAsync(h_hn_.p, hn_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaStreamSynchronize(ctx_->stream));
-    st_.commutators_evaluated += static_cast<uint64_t>(cnt);
-    ++st_.batches;
-    apply(cnt, g0, 0, false, nullptr, nullptr);
-  }
-
-  void where(int64_t pair_g0, int64_t cand0, int j, int64_t& l, int64_t& m) const {
-    if (pair_g0 >= 0) {
-      pair_from_index(pair_g0 + j, l, m);
-    } else {
-      l = cand0 + j;
-      m = -1;
-    }
-  }
-  std::string where_str(int64_t l, int64_t m) const {
-    return m < 0 ? "generator " + std::to_string(l) : "pair (" + std::to_string(l) + "," + std::to_string(m) + ")";
-  }
-
-  void log_decision(int64_t l, int64_t m, int nul, int ind, int rc, double rn) {
-    if (record_) log_.push_back({l, m, nul, ind, rc, 0, rn});
-  }
-
-  void note(int64_t l, int64_t m, double rn, bool ind) {
-    if (borderline(rn, tol_))
-      warns_.push_back({"borderline_residual",
-                        where_str(l, m) + ": residual " + fmt_double(rn) + " within 10x of tolerance " +
-                            fmt_double(tol_) + (ind ? " (accepted)" : " (rejected)"),
-                        rn});
-  }
-
-  // ordered apply of one batch whose null flags (h_nul_) and pass-1 norms
-  // (h_rn1_, device residuals in R_) are known.
-  void apply(int cnt, int64_t pair_g0, int64_t cand0, bool generators, int32_t* indep_out, double* rn_out) {
-    const int64_t n_bs = n_o_;
-    const double screen = tol_ / 20.0;
-    int nsurv = 0;
-    for (int j = 0; j < cnt; ++j)
-      if (!h_nul_.p[j] && h_rn1_.p[j] > screen) h_idx_.p[nsurv++] = j;
-    st_.survivors += static_cast<uint64_t>(nsurv);
-    if (nsurv > 0) {
-      CU(cudaMemcpyAsync(idx_.p, h_idx_.p, nsurv * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
-      dim3 gg(static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 64)), nsurv);
-      gather_columns_kernel<<<gg, 256, 0, ctx_->stream>>>(R_.p, idx_.p, D_, X_.p);
-      launched(ctx_);
-      project(V_.p, n_bs, X_.p, nsurv, X_.p, rn2_.p);  // second CGS pass, in place
-      CU(cudaMemcpyAsync(h_rn2_.p, rn2_.p, nsurv * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
-      CU(cudaStreamSynchronize(ctx_->stream));
-    }
-    constexpr int kBlock = 64;  // survivors re-projected together against in-batch accepts
-    int s = 0;                  // next survivor
-    int blk_end = 0;            // survivors [.., blk_end) already refreshed against in-batch accepts
-    int64_t n_blk = n_bs;       // basis size when the current survivor block was refreshed
-    for (int j = 0; j < cnt; ++j) {
-      int64_t l, m;
-      where(pair_g0, cand0, j, l, m);
-      if (h_nul_.p[j]) {
-        if (generators) {
-          const double gn = h_hn_.p[j];
-          warns_.push_back({"null_generator",
-                            "generator " + std::to_string(l) + " has norm " + fmt_double(gn) + " and was skipped",
-                            gn});
-        }
-        log_decision(l, m, 1, 0, 0, record_ ? (generators ? h_hn_.p[j] : 0.0) : 0.0);
-        if (indep_out) indep_out[j] = 0;
-        if (rn_out) rn_out[j] = 0.0;
-        continue;
-      }
-      ++st_.independence_checks;
-      if (s >= nsurv || h_idx_.p[s] != j) {  // certified reject from pass 1
-        log_decision(l, m, 0, 0, 0, h_rn1_.p[j]);
-        if (indep_out) indep_out[j] = 0;
-        if (rn_out) rn_out[j] = h_rn1_.p[j];
-        continue;
-      }
-      const int k = s++;
-      if (k >= blk_end && n_o_ > n_bs) {
-        // refresh the next block of survivors against everything accepted
-        // since batch start (two passes: CGS2 against the new vectors)
-        blk_end = std::min(nsurv, k + kBlock);
-        const int nb = blk_end - k;
-        double2* xb = X_.p + static_cast<int64_t>(k) * D_;
-        project(V_.p + n_bs * D_, n_o_ - n_bs, xb, nb, xb, rn2_.p + k);
-        project(V_.p + n_bs * D_, n_o_ - n_bs, xb, nb, xb, rn2_.p + k);
-        CU(cudaMemcpyAsync(h_rn2_.p + k, rn2_.p + k, nb * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
-        CU(cudaStreamSynchronize(ctx_->stream));
-        n_blk = n_o_;
-        st_.rechecks += static_cast<uint64_t>(nb);
-      } else if (k >= blk_end) {
-        blk_end = std::min(nsurv, k + kBlock);
-        n_blk = n_o_;
-      }
-      double rn = h_rn2_.p[k];
-      const double2* resid = X_.p + static_cast<int64_t>(k) * D_;
-      int rc = n_o_ > n_bs ? 1 : 0;
-      if (n_o_ > n_blk && rn > tol_) {
-        // accepts inside this block: re-check against them (CGS2)
-        CU(cudaMemcpyAsync(Y_.p, resid, D_ * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
-        project(V_.p + n_blk * D_, n_o_ - n_blk, Y_.p, 1, Y_.p, yn_.p);
-        project(V_.p + n_blk * D_, n_o_ - n_blk, Y_.p, 1, Y_.p, yn_.p);
-        CU(cudaMemcpyAsync(h_y_.p, yn_.p, sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
-        CU(cudaStreamSynchronize(ctx_->stream));
-        rn = h_y_.p[0];
-        resid = Y_.p;
-        ++st_.rechecks;
-        rc = 1;
-      }
-      const bool ind = rn > tol_;
-      note(l, m, rn, ind);
-      log_decision(l, m, 0, ind ? 1 : 0, rc, rn);
-      if (indep_out) indep_out[j] = ind ? 1 : 0;
-      if (rn_out) rn_out[j] = rn;
-      if (ind) {
-        if (basis_size() >= cap_)
-          throw Error(LIECL_B200_CAPACITY,
-                      "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
-        if (n_o_ + 1 > vcap_) {
-          // growing moves the slab: keep the residual source valid across it
-          if (resid != Y_.p)
-            CU(cudaMemcpyAsync(Y_.p, resid, D_ * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
-          resid = Y_.p;
-          ensure_capacity(n_o_ + 1);
-        }
-        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 256));
-        append_scaled_kernel<<<blocks, 256, 0, ctx_->stream>>>(
-            resid, 1.0 / rn, D_, V_.p + n_o_ * D_, keep_ ? C_.p + static_cast<int64_t>(j) * D_ : nullptr,
-            keep_ ? O_.p + n_b_ * D_ : nullptr);
-        launched(ctx_);
-        ++n_o_;
-        if (keep_) ++n_b_;
-        ++st_.accepted;
-      }
-    }
-    if (!keep_) n_b_ = n_o_;
-  }
-
-  liecl_b200_ctx* ctx_;
-  int d_;
-  int64_t D_;
-  bool keep_;
-  double tol_;
-  bool record_;
-  int64_t cap_ = 0, bmax_ = 0, B_cur_ = 0;
-  double sqrt_d_ = 1.0;
-  bool has_deadline_ = false;
-  Clock::time_point deadline_{};
-  int64_t n_o_ = 0, n_b_ = 0;
-  uint64_t kernels0_ = 0;
-  liecl_b200_stats st_{};
-  std::vector<Warning> warns_;
-  std::vector<liecl_b200_decision> log_;
-  DevBuf<double2> V_, O_, C_, R_, X_, Y_, P_;
-  DevBuf<double> partial_, rn1_, rn2_, hn_, yn_;
-  DevBuf<int> nul_, idx_;
-  HostBuf<double> h_rn1_, h_rn2_, h_hn_, h_y_;
-  int64_t vcap_ = 0;  // basis vectors the slab (and beta buffer) can hold
-  HostBuf<int> h_nul_, h_idx_;
-};
+#include "dense_engine.cuh"
 
 // --------------------------------------------------------- Pauli engine ---
 
@@ -1164,8 +827,8 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
     write_warnings(eng.warnings(), warnings, warnings_len);
     copy_log(eng.log(), log, log_cap, log_len);
     if (n > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
-    eng.download(eng.basis_ptr(), n, basis_out);
-    if (ortho_out) eng.download(eng.ortho_ptr(), eng.ortho_size(), ortho_out);
+    eng.download(false, basis_out);
+    if (ortho_out) eng.download(true, ortho_out);
   });
 }
 
@@ -1354,7 +1017,7 @@ int liecl_b200_session_get_basis(liecl_b200_session* s, double* out, int64_t cap
     use_device(s->ctx);
     const int64_t n = s->eng->basis_size();
     if (n > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
-    s->eng->download(s->eng->basis_ptr(), n, out);
+    s->eng->download(false, out);
   });
 }
 

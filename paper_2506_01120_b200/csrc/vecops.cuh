@@ -28,6 +28,17 @@ __global__ void gather_columns_kernel(const double2* __restrict__ src, const int
     o[e] = s[e];
 }
 
+// dst[j] = src[idx[j]] for columns of W doubles (either field).
+__global__ void gather_words_kernel(const double* __restrict__ src, const int* __restrict__ idx, int64_t W,
+                                    double* __restrict__ dst) {
+  const int j = blockIdx.y;
+  const double* s = src + static_cast<int64_t>(idx[j]) * W;
+  double* o = dst + static_cast<int64_t>(j) * W;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < W;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    o[e] = s[e];
+}
+
 // K3 append: dst = (s + 0i) * src  -- residual_unit = Complex{1/||r||, 0} * r
 // (R:src/closure.cpp:283) written straight into the basis slab slot; with
 // `orig_dst` the accepted candidate h_unit is copied to the originals slab

@@ -182,6 +182,9 @@ class ClosureConfig:
     deadline: float | None = None  # absolute time.monotonic() value
     record_log: bool = False
     batch_max: int = 0
+    # "auto": exactly anti-Hermitian operators (i*H, every dense BASELINE
+    # config) take the packed-real path; "complex": always the general path
+    field: str = "auto"
 
     def native(self) -> native.Config:
         rel = 0.0
@@ -189,8 +192,10 @@ class ClosureConfig:
             rel = self.deadline - time.monotonic()
             if rel <= 0:
                 rel = 1e-9
+        if self.field not in ("auto", "complex"):
+            raise InvalidInputError(f"unknown field '{self.field}' (expected auto or complex)")
         return native.Config(float(self.tolerance), int(self.max_dim), int(self.threads), int(self.record_log),
-                             rel, int(self.batch_max))
+                             rel, int(self.batch_max), 1 if self.field == "complex" else 0, 0)
 
 
 @dataclass

@@ -35,7 +35,8 @@ class NativeUnavailable(RuntimeError):
 
 class Config(C.Structure):
     _fields_ = [("tolerance", C.c_double), ("max_dim", C.c_uint64), ("threads", C.c_uint32),
-                ("record_log", C.c_uint32), ("deadline_seconds", C.c_double), ("batch_max", C.c_int64)]
+                ("record_log", C.c_uint32), ("deadline_seconds", C.c_double), ("batch_max", C.c_int64),
+                ("field", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class Stats(C.Structure):

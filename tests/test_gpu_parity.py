@@ -20,15 +20,19 @@ def rel_err(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
 
 
+FIELDS = ["auto", "complex"]  # auto = packed anti-Hermitian path for these i*H generators
+
+
+@pytest.mark.parametrize("field", FIELDS)
 @pytest.mark.parametrize("make", [w.config0, w.config1], ids=["c0", "c1"])
 @pytest.mark.parametrize("method", [liecl.Method.orthonorm_dimonly, liecl.Method.orthonorm],
                          ids=["dimonly", "orthonorm"])
-def test_dense_closure_matches_golden(golden, make, method):
+def test_dense_closure_matches_golden(golden, make, method, field):
     cfg = make()
     meta, g = golden(f"{cfg.name}_{liecl.to_string(method)}")
     assert meta["digest"] == cfg.digest()
     res = liecl.closure_dense_arrays(cfg.generators, cfg.d, method,
-                                     liecl.ClosureConfig(tolerance=cfg.tol, record_log=True))
+                                     liecl.ClosureConfig(tolerance=cfg.tol, record_log=True, field=field))
     assert res.dimension == meta["dimension"]
     assert res.stats.commutators_evaluated == meta["stats"]["commutators_evaluated"]
     assert res.stats.independence_checks == meta["stats"]["independence_checks"]
@@ -184,14 +188,15 @@ def test_null_generator_warning_and_kernels_launched():
     assert native.kernel_count(0) > k0
 
 
-def test_c2_growth_phase_matches_reference(golden):
+@pytest.mark.parametrize("field", FIELDS)
+def test_c2_growth_phase_matches_reference(golden, field):
     """Config 2 (n=6, d=64): the growth phase (rows 1..99, every accept of the
     closure happens here) decision for decision against the reference's own
     run (tests/golden, generated by tests/golden/make_golden.py --c2)."""
     meta, g = golden("c2_random_sums_n6_s0_orthonorm-dimonly_rows100")
     cfg = w.config2()
     assert meta["digest"] == cfg.digest()
-    s = liecl.ClosureSession(64, config=liecl.ClosureConfig(tolerance=cfg.tol, record_log=True))
+    s = liecl.ClosureSession(64, config=liecl.ClosureConfig(tolerance=cfg.tol, record_log=True, field=field))
     ind, rn, st = s.check_candidates(cfg.generators)
     gen = g["log_m"] < 0
     assert np.array_equal(ind, g["log_indep"][gen])
@@ -207,7 +212,6 @@ def test_c2_growth_phase_matches_reference(golden):
     V = s.basis()
     rows = g["basis_rows"]
     assert rel_err(V[rows], g["basis"]) < BASIS_RTOL
-    wts = np.random.default_rng(1234).standard_normal(4096) + 1j * np.random.default_rng(1234).standard_normal(4096)
     rng = np.random.default_rng(1234)
     wts = rng.standard_normal(4096) + 1j * rng.standard_normal(4096)
     assert rel_err(V @ wts, g["basis_checksum"]) < BASIS_RTOL
@@ -231,3 +235,62 @@ def test_generic_dimensions_vs_oracle(port, d):
         assert res.dimension == o.dimension
         assert np.array_equal(res.decision_log["independent"], o.log["independent"])
         assert rel_err(res.basis_array, o.basis) < BASIS_RTOL
+
+
+def antiherm_saturated_basis(d, seed=3):
+    """Orthonormal basis of the traceless anti-Hermitian d x d matrices (su(d)),
+    vec layout, orthonormal under <a,b> = vdot(a,b)/d."""
+    rng = np.random.default_rng(seed)
+    n = d * d - 1
+    mats = []
+    for _ in range(n):
+        a = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+        a = a - a.conj().T
+        a -= np.trace(a) / d * np.eye(d)
+        mats.append(a.ravel(order="F"))
+    M = np.array(mats).T  # D x n, every column anti-Hermitian
+    # Gram-Schmidt with the real part of the inner product keeps real
+    # combinations only (the span of anti-Hermitian matrices over R)
+    Q = np.zeros_like(M)
+    for k in range(n):
+        v = M[:, k].copy()
+        for _ in range(2):
+            coef = (Q[:, :k].conj().T @ v).real
+            v -= Q[:, :k] @ coef
+        Q[:, k] = v / np.linalg.norm(v)
+    V = (Q.T * np.sqrt(d)).copy()
+    for k in range(n):  # exact anti-Hermitian bits
+        m = V[k].reshape(d, d, order="F")
+        m = 0.5 * (m - m.conj().T)
+        V[k] = m.ravel(order="F")
+    return V
+
+
+@pytest.mark.parametrize("field", FIELDS)
+def test_window_antihermitian_saturated_basis(port, field):
+    d = 8
+    V = antiherm_saturated_basis(d)
+    s = liecl.ClosureSession(d, config=liecl.ClosureConfig(tolerance=1e-10, record_log=True, field=field))
+    s.set_basis(V)
+    st = s.run_rows(1, len(V))
+    log = s.log()
+    nul, ind, rn = port.bracket_window_dense(V, d, 1, len(V), tol=1e-10)
+    assert st["commutators_evaluated"] == len(V) * (len(V) - 1) // 2 == len(log)
+    assert np.array_equal(log["null_cand"], nul) and np.array_equal(log["independent"], ind)
+    assert ind.sum() == 0 and s.size() == len(V)
+    assert rel_err(s.basis(), V) < 1e-15  # packed round trip is exact up to the diagonal's real part
+
+
+def test_antihermitian_then_general_promotes(port):
+    """A session that starts on the packed path and then receives a general
+    complex candidate promotes itself (unpacking the basis)."""
+    cfg = w.config0()
+    rng = np.random.default_rng(2)
+    s = liecl.ClosureSession(8, config=liecl.ClosureConfig(tolerance=1e-10))
+    ind1, _, _ = s.check_candidates(cfg.generators)
+    extra = rng.standard_normal((2, 64)) + 1j * rng.standard_normal((2, 64))
+    ind2, rn2, _ = s.check_candidates(extra)
+    o1, _, room = port.check_sequence_dense(np.zeros((0, 64)), np.concatenate([cfg.generators, extra]), 8,
+                                            append=True)
+    assert np.array_equal(np.concatenate([ind1, ind2]), o1)
+    assert rel_err(s.basis(), room) < BASIS_RTOL
