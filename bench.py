@@ -48,7 +48,6 @@ UNIT = "brackets/s"
 D_QUBITS = 6
 DIM = 64
 GROWTH_ROWS = 128
-FLOPS_PER_BRACKET = 16 * DIM ** 3 + 16 * 4095 * DIM * DIM  # W = 16 d^3 + 16 N D
 
 
 def parse():
@@ -64,6 +63,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-general", action="store_true", help="skip the general-complex-path comparison")
     return ap.parse_args()
 
 
@@ -272,17 +272,7 @@ def run_b200_arm(a):
 
     stream = torch.cuda.current_stream(device)
     native.set_stream(stream.cuda_stream, device=local)
-
-    # ---- setup (untimed): generator loop + growth phase on the GPU
     cfg = w.config2()
-    sess = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol), device=local)
-    sess.check_candidates(cfg.generators)
-    t0 = time.perf_counter()
-    grow = sess.run_rows(1, GROWTH_ROWS)
-    growth_s = time.perf_counter() - t0
-    if sess.size() != 4095:
-        raise RuntimeError(f"config-2 closure did not saturate: dim {sess.size()}")
-    peak = fp64_peak_tflops(torch, device)
 
     def barrier():
         if world > 1:
@@ -297,49 +287,67 @@ def run_b200_arm(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- warmup
-    step = 0
-    for _ in range(a.warmup):
-        r0, r1 = window_rows(step, rank, world, a.row0, a.rows_per_step)
-        sess.run_rows(r0, r1)
-        step += 1
+    def grown_session(field):
+        """Setup (untimed): generator loop + growth phase on the GPU."""
+        s = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol, field=field), device=local)
+        s.check_candidates(cfg.generators)
+        t0 = time.perf_counter()
+        g = s.run_rows(1, GROWTH_ROWS)
+        if s.size() != 4095:
+            raise RuntimeError(f"config-2 closure did not saturate: dim {s.size()}")
+        return s, g, time.perf_counter() - t0
 
-    # ---- timed region (device resident)
-    windows = [window_rows(step + s, rank, world, a.row0, a.rows_per_step) for s in range(a.steps)]
-    my_brackets = sum(brackets_in(*wnd) for wnd in windows)
-    native.kernel_times(local)  # reset
-    native.set_timing(True, local)
-    barrier()
-    torch.cuda.synchronize(device)
-    k0 = native.kernel_count(local)
-    accepted = 0
-    with ClockSampler(local) as clocks:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        torch.cuda.profiler.start()  # ncu --profile-from-start off captures only this region
-        e0.record(stream)
-        for r0, r1 in windows:
-            st = sess.run_rows(r0, r1)
-            accepted += st["accepted"]
-        e1.record(stream)
+    def measure(s, first_step, steps, profile=False):
+        """Warm-up + `steps` timed windows; CUDA events on the launching stream."""
+        for i in range(a.warmup):
+            s.run_rows(*window_rows(first_step + i, rank, world, a.row0, a.rows_per_step))
+        first_step += a.warmup
+        windows = [window_rows(first_step + i, rank, world, a.row0, a.rows_per_step) for i in range(steps)]
+        native.kernel_times(local)  # reset
+        native.set_timing(True, local)
+        barrier()
         torch.cuda.synchronize(device)
-        torch.cuda.profiler.stop()
-    barrier()
-    launches = native.kernel_count(local) - k0
-    native.set_timing(False, local)
-    kt = native.kernel_times(local)
-    my_ms = e0.elapsed_time(e1)
-    step += a.steps
-    max_ms = max_over_ranks(my_ms)
+        k0 = native.kernel_count(local)
+        accepted = 0
+        with ClockSampler(local) as clocks:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            if profile:
+                torch.cuda.profiler.start()  # ncu --profile-from-start off captures only this region
+            e0.record(stream)
+            for r0, r1 in windows:
+                accepted += s.run_rows(r0, r1)["accepted"]
+            e1.record(stream)
+            torch.cuda.synchronize(device)
+            if profile:
+                torch.cuda.profiler.stop()
+        barrier()
+        launches = native.kernel_count(local) - k0
+        native.set_timing(False, local)
+        kt = native.kernel_times(local)
+        if accepted:
+            raise RuntimeError("saturated window accepted a candidate")
+        my_ms = e0.elapsed_time(e1)
+        return windows, my_ms, max_over_ranks(my_ms), kt, launches, clocks.summary()
+
+    def gemm_roofline(kt, my_ms, peak):
+        ms = kt["zgemm_project"]["ms"] + kt["zgemm_subtract"]["ms"]
+        flops = kt["zgemm_project"]["flops"] + kt["zgemm_subtract"]["flops"]
+        launches = kt["zgemm_project"]["launches"] + kt["zgemm_subtract"]["launches"]
+        achieved = flops / (ms / 1e3) / 1e12
+        return {"achieved": achieved, "frac": achieved / peak, "launches": launches,
+                "avg_launch_ms": ms / max(launches, 1), "share_of_step": ms / my_ms,
+                "commutator_ms": kt["commutator"]["ms"],
+                "commutator_tflops": kt["commutator"]["flops"] / max(kt["commutator"]["ms"], 1e-9) / 1e9}
+
+    sess, grow, growth_s = grown_session("auto")
+    peak = fp64_peak_tflops(torch, device)
+    windows, my_ms, max_ms, kt, launches, clocks = measure(sess, 0, a.steps, profile=True)
+    my_brackets = sum(brackets_in(*wnd) for wnd in windows)
     total_brackets = my_brackets * world
     value = total_brackets / (max_ms / 1e3)
-    if accepted:
-        raise RuntimeError("saturated window accepted a candidate")
-
-    proj_ms = kt["zgemm_project"]["ms"] + kt["zgemm_subtract"]["ms"]
-    proj_flops = kt["zgemm_project"]["flops"] + kt["zgemm_subtract"]["flops"]
-    proj_launches = kt["zgemm_project"]["launches"] + kt["zgemm_subtract"]["launches"]
-    achieved = proj_flops / (proj_ms / 1e3) / 1e12
+    roof = gemm_roofline(kt, my_ms, peak)
+    field = sess.field()
     traffic = load_traffic()
 
     # ---- e2e: C-ABI session with host buffers (pinned), H2D basis every step
@@ -376,6 +384,16 @@ def run_b200_arm(a):
                "d2h_bytes_per_step": int(12 * my_brackets / a.steps),
                "path": "liecl_b200_session_set_basis(host pinned) + liecl_b200_session_run_rows"}
 
+    # ---- the general complex path on the same windows (for comparison)
+    general = None
+    if not a.no_general:
+        gsess, _, _ = grown_session("complex")
+        gw, g_my_ms, g_max_ms, gkt, _, _ = measure(gsess, 0, max(2, a.steps // 2))
+        gb = sum(brackets_in(*wnd) for wnd in gw) * world
+        general = {"value": gb / (g_max_ms / 1e3), "unit": UNIT, **gemm_roofline(gkt, g_my_ms, peak),
+                   "flops_per_unit": "8*N*D per candidate per complex GEMM; commutator 16 d^3"}
+        gsess.close()
+
     if rank != 0:
         return
     cpu = None
@@ -389,28 +407,34 @@ def run_b200_arm(a):
                "sample": f"first {pairs} brackets of rows >= {r0} of the same window, same basis bytes "
                          f"({secs:.1f} s)"}
     secondary = None if a.no_secondary else secondary_closures()
+    packed = field == "antihermitian_packed"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": max_ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c128", "data": "synthetic (seeded SplitMix64 recipe, SURVEY.md §8d)",
+        "dtype": "f64" if packed else "c128", "data": "synthetic (seeded SplitMix64 recipe, SURVEY.md §8d)",
         "config": {"workload": "c2_saturated_window", "qubits": D_QUBITS, "d": DIM, "D": DIM * DIM, "basis": 4095,
                    "tol": 1e-10, "rows_per_step": a.rows_per_step, "brackets_per_step_per_gpu": my_brackets / a.steps,
-                   "row0": a.row0, "l2": "inputs > L2 (basis 268 MB + candidate slabs 2x268 MB per step)",
+                   "row0": a.row0, "field": field,
+                   "l2": "inputs > L2 (basis 134-268 MB + candidate slabs per step)",
                    "parallelism": f"dp{world}: disjoint closure rows per GPU, basis replicated, no collective",
                    "growth_setup_s": round(growth_s, 3), "growth_batches": grow["batches"]},
-        "roofline": {"bound": "tensor", "kernel": "zgemm_dmma (K2a beta=V^H C/d + K2b R=C-V beta, DMMA.8x8x4)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic, "launches": proj_launches, "avg_launch_ms": proj_ms / max(proj_launches, 1),
-                     "share_of_step": proj_ms / my_ms,
-                     "flops_per_unit": "8*N*D per candidate per GEMM (N=4095, D=4096)",
+        "roofline": {"bound": "tensor",
+                     "kernel": ("dgemm_dmma (K2a_r beta=Vw^T C/d + K2b_r R=C-V beta, packed anti-Hermitian, "
+                                "DMMA.8x8x4)") if packed else
+                               "zgemm_dmma (K2a beta=V^H C/d + K2b R=C-V beta, DMMA.8x8x4)",
+                     "achieved": roof["achieved"], "peak": peak, "unit": "TFLOP/s", "frac": roof["frac"],
+                     "traffic": traffic, "launches": roof["launches"], "avg_launch_ms": roof["avg_launch_ms"],
+                     "share_of_step": roof["share_of_step"],
+                     "flops_per_unit": ("2*N*D real flops per candidate per GEMM (packed d^2 reals, N=4095, D=4096)"
+                                        if packed else "8*N*D per candidate per GEMM (N=4095, D=4096)"),
                      "peak_source": "measured in-run: cuBLAS ZGEMM 4096^3 via torch.matmul complex128 "
                                     "(MEASURED_PEAKS.json has no FP64 entry)",
-                     "path_tflops": value * FLOPS_PER_BRACKET / 1e12 / world,
-                     "commutator_ms": kt["commutator"]["ms"]},
+                     "commutator_ms": roof["commutator_ms"], "commutator_tflops": roof["commutator_tflops"]},
+        "general_complex_path": general,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
-        "clocks": clocks.summary(),
+        "clocks": clocks,
         "secondary": secondary,
     }
     print(json.dumps(line), flush=True)

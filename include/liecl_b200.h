@@ -180,6 +180,8 @@ int liecl_b200_session_run_pairs(liecl_b200_session* s, int64_t g_begin, int64_t
 int liecl_b200_session_run_rows(liecl_b200_session* s, int64_t row_begin, int64_t row_end,
                                 liecl_b200_stats* stats);
 int liecl_b200_session_size(const liecl_b200_session* s, int64_t* n);
+/* Arithmetic field in use: 0 undecided, 1 general complex, 2 packed anti-Hermitian. */
+int liecl_b200_session_field(const liecl_b200_session* s, int32_t* field);
 int liecl_b200_session_get_basis(liecl_b200_session* s, double* out, int64_t cap);
 /* Decision log of the last run_* / check_candidates call (cfg->record_log). */
 int liecl_b200_session_get_log(liecl_b200_session* s, liecl_b200_decision* log, int64_t cap, int64_t* len);

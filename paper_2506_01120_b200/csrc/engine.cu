@@ -1011,6 +1011,13 @@ int liecl_b200_session_size(const liecl_b200_session* s, int64_t* n) {
   });
 }
 
+int liecl_b200_session_field(const liecl_b200_session* s, int32_t* field) {
+  return guarded([&] {
+    if (!s || !field) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    *field = static_cast<int32_t>(s->eng->field());
+  });
+}
+
 int liecl_b200_session_get_basis(liecl_b200_session* s, double* out, int64_t cap) {
   return guarded([&] {
     if (!s || !out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");

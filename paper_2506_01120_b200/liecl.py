@@ -448,6 +448,11 @@ class ClosureSession:
         _check(self.lib.liecl_b200_session_size(self.ptr, C.byref(n)))
         return n.value
 
+    def field(self) -> str:
+        f = C.c_int32()
+        _check(self.lib.liecl_b200_session_field(self.ptr, C.byref(f)))
+        return {0: "unset", 1: "complex", 2: "antihermitian_packed"}[f.value]
+
     def basis(self) -> np.ndarray:
         n = self.size()
         out = np.zeros((n, self.d * self.d), np.complex128)
