@@ -72,28 +72,36 @@ public:
   // Replace the basis by n operators (complex vec layout, host or device).
   void set_basis(const double2* src, int64_t n, bool on_device) {
     if (n > cap_) throw Error(LIECL_B200_CAPACITY, "basis larger than the session capacity");
-    DevBuf<double2> tmp;
-    tmp.ensure(static_cast<size_t>(std::max<int64_t>(n, 1) * D_));
+    // staging buffer persists across calls (sessions re-upload bases every step)
+    basis_stage_.ensure(static_cast<size_t>(std::max<int64_t>(n, 1) * D_));
+    double2* tmp = basis_stage_.p;
     if (n > 0)
-      CU(cudaMemcpyAsync(tmp.p, src, static_cast<size_t>(n * D_) * sizeof(double2),
+      CU(cudaMemcpyAsync(tmp, src, static_cast<size_t>(n * D_) * sizeof(double2),
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx_->stream));
-    const Field f = classify(tmp.p, n);
+    const Field f = classify(tmp, n);
     n_o_ = n_b_ = 0;
-    vcap_ = 0;
-    V_.release();
-    Vw_.release();
-    O_.release();
-    field_ = f;
+    if (f != field_) {  // slabs are laid out per field: start them afresh
+      vcap_ = 0;
+      V_.release();
+      Vw_.release();
+      O_.release();
+      field_ = f;
+    }
     alloc_batch();
-    ensure_capacity(std::min<int64_t>(cap_ + 1, n + 1));
+    ensure_capacity(std::min<int64_t>(cap_ + 2, n + 2));
+    // slots past the new basis must read as zero (see ensure_capacity)
+    CU(cudaMemsetAsync(V_.p + n * vw(), 0, static_cast<size_t>((vcap_ - n) * vw()) * sizeof(double), ctx_->stream));
+    if (Vw_.p)
+      CU(cudaMemsetAsync(Vw_.p + n * vw(), 0, static_cast<size_t>((vcap_ - n) * vw()) * sizeof(double),
+                         ctx_->stream));
     if (n > 0) {
       if (field_ == Field::kAntiHerm) {
-        pack_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(tmp.p, n, d_, V_.p);
+        pack_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(tmp, n, d_, V_.p);
         launched(ctx_);
         weight_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(V_.p, n, d_, Vw_.p);
         launched(ctx_);
       } else {
-        CU(cudaMemcpyAsync(V_.p, tmp.p, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToDevice,
+        CU(cudaMemcpyAsync(V_.p, tmp, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToDevice,
                            ctx_->stream));
       }
       if (keep_)
@@ -580,6 +588,7 @@ private:
   std::vector<liecl_b200_decision> log_;
   DevBuf<double> V_, Vw_, O_, C_, R_, X_, Y_, P_;  // element width ew() doubles
   DevBuf<double2> stage_;                          // complex input staging
+  DevBuf<double2> basis_stage_;                    // set_basis staging (kept across calls)
   DevBuf<double> partial_, rn1_, rn2_, hn_, yn_;
   DevBuf<int> nul_, idx_;
   DevBuf<unsigned long long> small_;
