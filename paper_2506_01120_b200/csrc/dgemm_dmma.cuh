@@ -12,10 +12,11 @@
 //   K2a_r  beta = (1/d) Vw^T X          (Vw = w .* V, kept beside V)
 //   K2b_r  R    = X - V beta, sum_k w_k R_k^2 partials (the weighted norm)
 //
-// 2 N D flops each per candidate instead of 8 N D. Tile: BM x BN = 128 x 128
-// real per CTA, 8 warps as 2 x 4 of 64 x 32, BK = 16, 4-stage cp.async
-// pipeline; fragment loads are 64-bit with rows padded to == 4 (mod 16)
-// doubles, which makes both the row- and column-operand patterns conflict free.
+// 2 N D flops each per candidate instead of 8 N D. Tile: BM x BN = 128 x 64
+// real per CTA, 4 warps as 2 x 2 of 64 x 32, two CTAs per SM, BK = 16,
+// 3-stage cp.async pipeline. Inside a BK tile the k order is permuted so a
+// thread's fragments for two consecutive k-steps are adjacent (128-bit loads);
+// row paddings keep every fragment access bank-conflict free.
 #pragma once
 
 #include "common.cuh"
@@ -23,12 +24,12 @@
 namespace liecl_b200 {
 
 namespace rg {
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
-constexpr int WM = 2, WN = 4, THREADS = 32 * WM * WN;
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3;
+constexpr int WM = 2, WN = 2, THREADS = 32 * WM * WN;  // 4 warps, 2 CTAs per SM
 constexpr int WTM = BM / WM, WTN = BN / WN;  // 64 x 32 warp tile
 constexpr int MT = WTM / 8, NT = WTN / 8;    // 8 x 4 m8n8 tiles
-constexpr int LDK = BK + 4;                  // K-contiguous rows (doubles)
-constexpr int LDM = BM + 4;                  // M-contiguous rows (doubles)
+constexpr int LDK = BK + 8;                  // K-contiguous rows (doubles): == 8 mod 16 for 128-bit loads
+constexpr int LDM = BM + 2;                  // M-contiguous rows (doubles): 2*LDM == 4 mod 16
 constexpr int A_KC = BM * LDK, A_MC = BK * LDM, B_KC = BN * LDK;
 template <bool KC> constexpr int a_elems() { return KC ? A_KC : A_MC; }
 template <bool KC> constexpr int smem_bytes() { return STAGES * (a_elems<KC>() + B_KC) * 8; }
@@ -48,7 +49,7 @@ enum class REpi { kStoreScaled, kSubtractNorm };
 //   kSubtractNorm: C[n*ldc + m] = X[n*ldx + m] - acc;
 //                  partial[blockIdx.x*N + n] = sum_rows w(m) C^2 (w: packed_weight, dim)
 template <bool A_KCONTIG, REpi EPI>
-__global__ void __launch_bounds__(rg::THREADS)
+__global__ void __launch_bounds__(rg::THREADS, 2)
 dgemm_dmma_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
                   int64_t ldb, double* __restrict__ Cout, int64_t ldc, double alpha, const double* __restrict__ X,
                   int64_t ldx, double* __restrict__ partial, int dim, int k_chunk, int64_t split_stride) {
@@ -126,21 +127,40 @@ dgemm_dmma_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda
     }
     const double* as = As + (kt % STAGES) * a_elems<A_KCONTIG>();
     const double* bs = Bs + (kt % STAGES) * B_KC;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      const int kc = kk * 4 + t;
-      double af[MT], bf[NT];
+    // K permutation inside the tile: k-step 2p+q uses k = 8p + 2t + q, so a
+    // thread's fragments for the step pair are adjacent (one 128-bit load on
+    // K-contiguous tiles); A and B use the same permutation, so the dot
+    // products are unchanged. Fragments of the next pair are loaded before
+    // the DMMAs of the current pair are issued.
+    double2 af[2][MT], bf[2][NT];
+    auto load_frags = [&](int p, double2 (&a)[MT], double2 (&b)[NT]) {
+      const int kc = 8 * p + 2 * t;
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         const int mr = wm * WTM + i * 8 + g;
-        af[i] = A_KCONTIG ? as[mr * LDK + kc] : as[kc * LDM + mr];
+        if (A_KCONTIG) {
+          a[i] = *reinterpret_cast<const double2*>(as + mr * LDK + kc);
+        } else {
+          a[i].x = as[kc * LDM + mr];
+          a[i].y = as[(kc + 1) * LDM + mr];
+        }
       }
 #pragma unroll
-      for (int j = 0; j < NT; ++j) bf[j] = bs[(wn * WTN + j * 8 + g) * LDK + kc];
+      for (int j = 0; j < NT; ++j) b[j] = *reinterpret_cast<const double2*>(bs + (wn * WTN + j * 8 + g) * LDK + kc);
+    };
+    load_frags(0, af[0], bf[0]);
+#pragma unroll
+    for (int p = 0; p < BK / 8; ++p) {
+      const int cur = p & 1;
+      if (p + 1 < BK / 8) load_frags(p + 1, af[cur ^ 1], bf[cur ^ 1]);
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i].x, bf[cur][j].x);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i].y, bf[cur][j].y);
     }
   }
   cp_async_wait<0>();

@@ -325,7 +325,7 @@ void rgemm_project(liecl_b200_ctx* ctx, const double* Vw, int64_t n, int64_t D, 
   rgemm_attr_once<true, REpi::kStoreScaled>();
   dim3 grid((n + rg::BM - 1) / rg::BM, (count + rg::BN - 1) / rg::BN);
   Timer t(ctx, 0, 2.0 * static_cast<double>(n) * static_cast<double>(D) * count);
-  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y * 2, D);  // 2 CTA-waves per 128^2 tile
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, D);
   if (slices <= 1) {
     dgemm_dmma_kernel<true, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<true>(), ctx->stream>>>(
         static_cast<int>(n), count, static_cast<int>(D), Vw, D, X, D, P, ldp, alpha, nullptr, 0, nullptr, 0, 0, 0);
@@ -355,7 +355,7 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
   dim3 grid((D + rg::BM - 1) / rg::BM, (count + rg::BN - 1) / rg::BN);
   Timer t(ctx, 1, 2.0 * static_cast<double>(n) * static_cast<double>(D) * count);
   const int64_t kpad = (n + 1) & ~int64_t(1);  // even K: reads one zero row of V past an odd n
-  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y * 2, kpad);
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, kpad);
   if (slices <= 1) {
     dgemm_dmma_kernel<false, REpi::kSubtractNorm><<<grid, rg::THREADS, rg::smem_bytes<false>(), ctx->stream>>>(
         static_cast<int>(D), count, static_cast<int>(kpad), V, D, P, ldp, R, D, 1.0, X, D, partial, d, 0, 0);
