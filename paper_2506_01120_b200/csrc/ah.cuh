@@ -116,22 +116,40 @@ __global__ void weight_ah_kernel(const double* __restrict__ v, int64_t count, in
 }
 
 template <int DIM> struct CommAhShape {
-  using C = CommShape<DIM>;
-  static constexpr int LDP = DIM + 1;  // packed staging stride (conflict free both ways)
+  static constexpr int TR = DIM / 8;                 // tile rows (and columns)
+  static constexpr int WARPS_PER_PAIR = TR < 8 ? TR : 8;
+  static constexpr int PAIRS_PER_CTA = 8 / WARPS_PER_PAIR;
+  static constexpr int ROWS_PER_WARP = TR / WARPS_PER_PAIR;  // tile rows per warp
+  static constexpr int LDP = DIM + 4;                // == 4 (mod 16): conflict-free fragment gathers
   static constexpr int PACKED = DIM * LDP;
-  static constexpr int SMEM_PER_PAIR = (4 * C::PLANE + 2 * PACKED) * 8 + C::WARPS_PER_PAIR * 8;
-  static constexpr int SMEM = C::PAIRS_PER_CTA * SMEM_PER_PAIR;
+  static constexpr int SMEM_PER_PAIR = 2 * PACKED * 8 + WARPS_PER_PAIR * 8;
+  static constexpr int SMEM = PAIRS_PER_CTA * SMEM_PER_PAIR;
 };
 
+// complex element (i, k) of the anti-Hermitian matrix stored packed at p (stride LDP)
+template <int LDP>
+__device__ __forceinline__ void ah_elem(const double* p, int i, int k, double& re, double& im) {
+  const double u = p[i + k * LDP], v = p[k + i * LDP];
+  if (i < k) { re = u; im = v; }
+  else if (i > k) { re = -v; im = u; }
+  else { re = 0.0; im = u; }
+}
+
 // K1 on the packed path: pairs [g0, g0+count) of the packed commutator basis;
-// writes packed h_unit, ||h||, null flag. One DMMA product P = A B per pair.
+// writes packed h_unit, ||h||, null flag. One DMMA product P = A B per pair,
+// fragments gathered straight from the packed inputs in shared memory; each
+// warp owns whole tile rows of P (A fragments reused across the row); P is
+// written back over the consumed inputs and h = P - P^dagger is read out in
+// the packed layout. ~70 KB per pair at d = 64: three CTAs per SM overlap
+// their load and compute phases.
 template <int DIM>
 __global__ void __launch_bounds__(256)
 commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, double tol, bool normalize,
                      double* __restrict__ out, double* __restrict__ hnorm, int* __restrict__ is_null) {
-  using S = CommShape<DIM>;
-  using SA = CommAhShape<DIM>;
+  using S = CommAhShape<DIM>;
   constexpr int D2 = DIM * DIM;
+  constexpr int LDP = S::LDP;
+  constexpr int NT = S::WARPS_PER_PAIR * 32;
   extern __shared__ __align__(16) double csm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -139,97 +157,86 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
   const int wip = warp % S::WARPS_PER_PAIR;
   const int j = blockIdx.x * S::PAIRS_PER_CTA + slot;
   const bool active = j < count;
-  const int tip = threadIdx.x - slot * S::WARPS_PER_PAIR * 32;
-  constexpr int NT = S::WARPS_PER_PAIR * 32;
+  const int tip = threadIdx.x - slot * NT;
 
-  double* base = csm + slot * (SA::SMEM_PER_PAIR / 8);
-  double* are = base;
-  double* aim = are + S::PLANE;
-  double* bre = aim + S::PLANE;
-  double* bim = bre + S::PLANE;
-  double* pa = bim + S::PLANE;      // packed A, stride LDP
-  double* pb = pa + SA::PACKED;     // packed B
-  double* red = pb + SA::PACKED;
+  double* pa = csm + slot * (S::SMEM_PER_PAIR / 8);
+  double* pb = pa + S::PACKED;
+  double* red = pb + S::PACKED;
 
-  int64_t l = 0, m = 0;
   if (active) {
+    int64_t l, m;
     pair_from_index(g0 + j, l, m);
-    const double* ga = basis + l * D2;
-    const double* gb = basis + m * D2;
-    for (int e = tip; e < D2; e += NT) {
-      const int i = e % DIM, k = e / DIM;
-      pa[i + k * SA::LDP] = ga[e];
-      pb[i + k * SA::LDP] = gb[e];
-    }
-  }
-  __syncthreads();
-  if (active) {
-    // planes: element (i, k) of the complex matrix at [i*LD + k]
-    for (int e = tip; e < D2; e += NT) {
-      const int i = e % DIM, k = e / DIM;
-      double ar, ai, br, bi;
-      if (i < k) {
-        ar = pa[i + k * SA::LDP]; ai = pa[k + i * SA::LDP];
-        br = pb[i + k * SA::LDP]; bi = pb[k + i * SA::LDP];
-      } else if (i > k) {
-        ar = -pa[k + i * SA::LDP]; ai = pa[i + k * SA::LDP];
-        br = -pb[k + i * SA::LDP]; bi = pb[i + k * SA::LDP];
-      } else {
-        ar = 0.0; ai = pa[i + i * SA::LDP];
-        br = 0.0; bi = pb[i + i * SA::LDP];
-      }
-      are[i * S::LD + k] = ar;
-      aim[i * S::LD + k] = ai;
-      bre[i * S::LD + k] = br;
-      bim[i * S::LD + k] = bi;
+    const double2* ga = reinterpret_cast<const double2*>(basis + l * D2);
+    const double2* gb = reinterpret_cast<const double2*>(basis + m * D2);
+    for (int e = tip; e < D2 / 2; e += NT) {  // 16-byte loads; DIM even
+      const int i = (2 * e) % DIM, k = (2 * e) / DIM;
+      const double2 va = ga[e], vb = gb[e];
+      pa[i + k * LDP] = va.x;
+      pa[i + 1 + k * LDP] = va.y;
+      pb[i + k * LDP] = vb.x;
+      pb[i + 1 + k * LDP] = vb.y;
     }
   }
   __syncthreads();
 
-  double cre[S::TILES_PER_WARP][2], cim[S::TILES_PER_WARP][2];
-  if (active) {
+  double cre[S::ROWS_PER_WARP][S::TR][2], cim[S::ROWS_PER_WARP][S::TR][2];
 #pragma unroll
-    for (int q = 0; q < S::TILES_PER_WARP; ++q) {
-      const int tile = wip * S::TILES_PER_WARP + q;
-      const int ti = (tile / (DIM / 8)) * 8, tj = (tile % (DIM / 8)) * 8;
-      double c0r = 0.0, c1r = 0.0, c0i = 0.0, c1i = 0.0;
-#pragma unroll 4
-      for (int k0 = 0; k0 < DIM; k0 += 4) {
-        const int k = k0 + t;
-        const double xr = are[(ti + g) * S::LD + k], xi = aim[(ti + g) * S::LD + k];
-        const double yr = bre[k * S::LD + tj + g], yi = bim[k * S::LD + tj + g];
-        dmma_8x8x4(c0r, c1r, xr, yr);
-        dmma_8x8x4(c0r, c1r, -xi, yi);
-        dmma_8x8x4(c0i, c1i, xr, yi);
-        dmma_8x8x4(c0i, c1i, xi, yr);
+  for (int r = 0; r < S::ROWS_PER_WARP; ++r)
+#pragma unroll
+    for (int c = 0; c < S::TR; ++c) cre[r][c][0] = cre[r][c][1] = cim[r][c][0] = cim[r][c][1] = 0.0;
+  if (active) {
+#pragma unroll 2
+    for (int k0 = 0; k0 < DIM; k0 += 4) {
+      const int k = k0 + t;
+      double br[S::TR], bi[S::TR];
+#pragma unroll
+      for (int c = 0; c < S::TR; ++c) ah_elem<LDP>(pb, k, c * 8 + g, br[c], bi[c]);  // B(k, tj + g)
+#pragma unroll
+      for (int r = 0; r < S::ROWS_PER_WARP; ++r) {
+        const int ti = (wip * S::ROWS_PER_WARP + r) * 8;
+        double ar, ai;
+        ah_elem<LDP>(pa, ti + g, k, ar, ai);  // A(ti + g, k)
+        const double nai = -ai;
+#pragma unroll
+        for (int c = 0; c < S::TR; ++c) {
+          dmma_8x8x4(cre[r][c][0], cre[r][c][1], ar, br[c]);
+          dmma_8x8x4(cre[r][c][0], cre[r][c][1], nai, bi[c]);
+          dmma_8x8x4(cim[r][c][0], cim[r][c][1], ar, bi[c]);
+          dmma_8x8x4(cim[r][c][0], cim[r][c][1], ai, br[c]);
+        }
       }
-      cre[q][0] = c0r; cre[q][1] = c1r; cim[q][0] = c0i; cim[q][1] = c1i;
     }
   }
-  __syncthreads();  // everyone done reading A / B planes
+  __syncthreads();  // inputs consumed: P planes reuse the packed buffers
+  double* pre = pa;  // P(i, k) re at [i*LDP + k]
+  double* pim = pb;
   if (active) {
 #pragma unroll
-    for (int q = 0; q < S::TILES_PER_WARP; ++q) {
-      const int tile = wip * S::TILES_PER_WARP + q;
-      const int ti = (tile / (DIM / 8)) * 8, tj = (tile % (DIM / 8)) * 8;
+    for (int r = 0; r < S::ROWS_PER_WARP; ++r) {
+      const int ti = (wip * S::ROWS_PER_WARP + r) * 8;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        are[(ti + g) * S::LD + tj + 2 * t + h] = cre[q][h];  // P(i, k) re
-        aim[(ti + g) * S::LD + tj + 2 * t + h] = cim[q][h];  // P(i, k) im
-      }
+      for (int c = 0; c < S::TR; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          pre[(ti + g) * LDP + c * 8 + 2 * t + h] = cre[r][c][h];
+          pim[(ti + g) * LDP + c * 8 + 2 * t + h] = cim[r][c][h];
+        }
     }
   }
   __syncthreads();
   double sumsq = 0.0;
+  double hv[(D2 + NT - 1) / NT];
   if (active) {
-    // packed h = P - P^dagger; kept in the (free) B re-plane, stride D2 layout
-    for (int e = tip; e < D2; e += NT) {
+#pragma unroll
+    for (int q = 0; q < (D2 + NT - 1) / NT; ++q) {
+      const int e = tip + q * NT;
+      if (e >= D2) break;
       const int i = e % DIM, k = e / DIM;
       double v;
-      if (i < k) v = are[i * S::LD + k] - are[k * S::LD + i];
-      else if (i > k) v = aim[k * S::LD + i] + aim[i * S::LD + k];
-      else v = 2.0 * aim[i * S::LD + i];
-      bre[e] = v;
+      if (i < k) v = pre[i * LDP + k] - pre[k * LDP + i];
+      else if (i > k) v = pim[k * LDP + i] + pim[i * LDP + k];
+      else v = 2.0 * pim[i * LDP + i];
+      hv[q] = v;
       sumsq += (i == k ? 1.0 : 2.0) * v * v;
     }
   }
@@ -246,9 +253,13 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
     hnorm[j] = hn;
     is_null[j] = nul ? 1 : 0;
   }
-  const double s = !normalize ? 1.0 : (nul ? 0.0 : 1.0 / hn);
+  const double sc = !normalize ? 1.0 : (nul ? 0.0 : 1.0 / hn);
   double* o = out + static_cast<int64_t>(j) * D2;
-  for (int e = tip; e < D2; e += NT) o[e] = bre[e] * s;
+#pragma unroll
+  for (int q = 0; q < (D2 + NT - 1) / NT; ++q) {
+    const int e = tip + q * NT;
+    if (e < D2) o[e] = hv[q] * sc;
+  }
 }
 
 // packed path, any even d: one CTA per pair, operands through L1/L2

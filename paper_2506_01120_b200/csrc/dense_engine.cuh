@@ -398,14 +398,13 @@ private:
     t.stop();
   }
   template <int DIM> void launch_comm_ah(const double* basis, int64_t g0, int cnt) {
-    using S = CommShape<DIM>;
     using SA = CommAhShape<DIM>;
     static bool attr = false;
     if (!attr) {
       CU(cudaFuncSetAttribute(commutator_ah_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, SA::SMEM));
       attr = true;
     }
-    const int blocks = (cnt + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA;
+    const int blocks = (cnt + SA::PAIRS_PER_CTA - 1) / SA::PAIRS_PER_CTA;
     Timer t(ctx_, 2, 8.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
     commutator_ah_kernel<DIM><<<blocks, 256, SA::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, C_.p, hn_.p,
                                                                         nul_.p);
