@@ -183,6 +183,11 @@ int liecl_b200_session_size(const liecl_b200_session* s, int64_t* n);
 /* Arithmetic field in use: 0 undecided, 1 general complex, 2 packed anti-Hermitian. */
 int liecl_b200_session_field(const liecl_b200_session* s, int32_t* field);
 int liecl_b200_session_get_basis(liecl_b200_session* s, double* out, int64_t cap);
+/* Copy basis elements [first, first+count) (complex vec layout) to `out`,
+ * a host or (out_on_device) device buffer; ortho != 0 selects the orthonormal
+ * tuple instead of the commutator basis (they differ only for Alg. 3). */
+int liecl_b200_session_get_vectors(liecl_b200_session* s, int64_t first, int64_t count, double* out,
+                                   int32_t out_on_device, int32_t ortho);
 /* Decision log of the last run_* / check_candidates call (cfg->record_log). */
 int liecl_b200_session_get_log(liecl_b200_session* s, liecl_b200_decision* log, int64_t cap, int64_t* len);
 /* Ordered independence check of raw candidates (normalised first, appended

@@ -200,6 +200,25 @@ public:
     }
   }
 
+  // elements [first, first+count) of the basis / orthonormal tuple -> out (complex vec layout)
+  void copy_vectors(int64_t first, int64_t count, double* out, bool out_on_device, bool ortho) {
+    const int64_t n = ortho ? n_o_ : basis_size();
+    if (first < 0 || count < 0 || first + count > n) throw Error(LIECL_B200_INVALID_INPUT, "vector range out of bounds");
+    if (count == 0) return;
+    const double* src = ((ortho || !keep_) ? V_.p : O_.p) + first * vw();
+    const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (field_ == Field::kAntiHerm) {
+      DevBuf<double2> tmp;
+      tmp.ensure(static_cast<size_t>(count * D_));
+      unpack_ah_kernel<<<grid_for(count * D_), 256, 0, ctx_->stream>>>(src, count, d_, tmp.p);
+      launched(ctx_);
+      CU(cudaMemcpyAsync(out, tmp.p, static_cast<size_t>(count * D_) * sizeof(double2), kind, ctx_->stream));
+    } else {
+      CU(cudaMemcpyAsync(out, src, static_cast<size_t>(count * D_) * sizeof(double2), kind, ctx_->stream));
+    }
+    CU(cudaStreamSynchronize(ctx_->stream));
+  }
+
   // single-vector project_residual for the drop-in API (general complex field)
   void project_residual(const double2* h_host, double* r_host, double* coeffs_host) {
     if (field_ == Field::kUnset) {

@@ -1011,6 +1011,15 @@ int liecl_b200_session_size(const liecl_b200_session* s, int64_t* n) {
   });
 }
 
+int liecl_b200_session_get_vectors(liecl_b200_session* s, int64_t first, int64_t count, double* out,
+                                   int32_t out_on_device, int32_t ortho) {
+  return guarded([&] {
+    if (!s || (count > 0 && !out)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    use_device(s->ctx);
+    s->eng->copy_vectors(first, count, out, out_on_device != 0, ortho != 0);
+  });
+}
+
 int liecl_b200_session_field(const liecl_b200_session* s, int32_t* field) {
   return guarded([&] {
     if (!s || !field) throw Error(LIECL_B200_INVALID_INPUT, "null argument");

@@ -459,6 +459,12 @@ class ClosureSession:
         _check(self.lib.liecl_b200_session_get_basis(self.ptr, _dp(out.view(np.float64)), C.c_int64(n)))
         return out
 
+    def vectors_to(self, first: int, count: int, out_ptr: int, on_device: bool = True, ortho: bool = False):
+        """Copy basis elements [first, first+count) into caller memory (e.g. a torch tensor's data_ptr())."""
+        _check(self.lib.liecl_b200_session_get_vectors(self.ptr, C.c_int64(first), C.c_int64(count),
+                                                       C.cast(C.c_void_p(out_ptr), C.POINTER(C.c_double)),
+                                                       C.c_int32(int(on_device)), C.c_int32(int(ortho))))
+
     def log(self) -> np.ndarray:
         n = C.c_int64()
         _check(self.lib.liecl_b200_session_get_log(self.ptr, None, C.c_int64(0), C.byref(n)))

@@ -236,10 +236,11 @@ class Config3:
 
     basis V = sqrt(d) * Q (Q from the QR of a seeded complex Gaussian D x N
     matrix; the sqrt(d) makes V orthonormal under <a,b> = vdot(a,b)/d,
-    R:src/dense.cpp:57); candidates k even: complex Gaussian, k odd:
-    sum_j a_j V_j + noise (sigma per re/im component). Generated with torch
-    on the device (17 GB does not travel), seeded; `scale` shrinks N, D and
-    the candidate count for parity tests.
+    R:src/dense.cpp:57 -- without it every candidate would be accepted);
+    candidates k even: complex Gaussian, k odd: sum_j a_j V_j + noise with
+    sigma per re/im component (re, im ~ N(0,1) everywhere). 17 GB cannot
+    travel, so the inputs are generated on the device with a seeded torch
+    Philox generator (`generate`); the same bytes feed the CPU baseline.
     """
     d: int = 256
     n: int = 16384
@@ -247,3 +248,30 @@ class Config3:
     noise: float = 1e-14
     seed: int = 0
     tol: float = 1e-10
+
+    @property
+    def D(self) -> int:
+        return self.d * self.d
+
+    def generate(self, torch, device):
+        """-> (V (n, D) complex128, cands (ncand, D) complex128), both on `device`."""
+        gen = torch.Generator(device=device)
+        gen.manual_seed(self.seed)
+
+        def cgauss(*shape):
+            re = torch.randn(*shape, dtype=torch.float64, device=device, generator=gen)
+            im = torch.randn(*shape, dtype=torch.float64, device=device, generator=gen)
+            return torch.complex(re, im)
+        G = cgauss(self.D, self.n)
+        Q, _ = torch.linalg.qr(G, mode="reduced")
+        del G
+        V = (Q.mT * math.sqrt(self.d)).contiguous()  # row k = basis vector k (vec layout)
+        del Q
+        cands = torch.empty((self.ncand, self.D), dtype=torch.complex128, device=device)
+        n_even = (self.ncand + 1) // 2
+        cands[0::2] = cgauss(n_even, self.D)
+        n_odd = self.ncand // 2
+        if n_odd:
+            a = cgauss(n_odd, self.n)
+            cands[1::2] = a @ V + self.noise * cgauss(n_odd, self.D)
+        return V, cands
