@@ -32,6 +32,20 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Grouped rasterisation of a linear CTA id over an mt x nt tile grid: runs of
+// GROUP M-tiles sweep all N-tiles together, so a wave of CTAs streams GROUP
+// basis tiles (instead of the whole basis) while the candidate tiles stay in L2.
+template <int GROUP>
+__device__ __forceinline__ void grouped_tile(int pid, int mt, int nt, int& m_tile, int& n_tile) {
+  const int per_group = GROUP * nt;
+  const int group = pid / per_group;
+  const int first_m = group * GROUP;
+  const int size = min(mt - first_m, GROUP);
+  const int in_group = pid % per_group;
+  m_tile = first_m + in_group % size;
+  n_tile = in_group / size;
+}
+
 // Cursor pair (l, m), m < l, from its global index g = l(l-1)/2 + m -- the
 // order run_engine visits pairs in (R:src/closure.cpp:412-417).
 __host__ __device__ __forceinline__ void pair_from_index(int64_t g, int64_t& l, int64_t& m) {

@@ -69,7 +69,9 @@ dgemm_dmma_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % WM, wn = warp / WM;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  int m_tile, n_tile;
+  grouped_tile<8>(blockIdx.x + blockIdx.y * gridDim.x, gridDim.x, gridDim.y, m_tile, n_tile);
+  const int m0 = m_tile * BM, n0 = n_tile * BN;
   const int KT = K > 0 ? (K + BK - 1) / BK : 0;
 
   // 16-byte chunks (2 doubles); K and the M extent are even on this path
@@ -217,7 +219,7 @@ dgemm_dmma_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda
         double s = 0.0;
 #pragma unroll
         for (int w2 = 0; w2 < WM; ++w2) s += red[w2][c];
-        partial[static_cast<int64_t>(blockIdx.x) * N + gn] = s;
+        partial[static_cast<int64_t>(m_tile) * N + gn] = s;
       }
     }
   }

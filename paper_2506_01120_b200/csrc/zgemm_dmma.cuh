@@ -76,7 +76,9 @@ zgemm_dmma_kernel(int M, int N, int K, const double2* __restrict__ A, int64_t ld
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % WM, wn = warp / WM;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  int m_tile, n_tile;
+  grouped_tile<8>(blockIdx.x + blockIdx.y * gridDim.x, gridDim.x, gridDim.y, m_tile, n_tile);
+  const int m0 = m_tile * BM, n0 = n_tile * BN;
   const int KT = K > 0 ? (K + BK - 1) / BK : 0;
 
   auto load_stage = [&](int stage, int kt) {
@@ -223,7 +225,7 @@ zgemm_dmma_kernel(int M, int N, int K, const double2* __restrict__ A, int64_t ld
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < WM; ++w) s += red[w][c];
-        partial[static_cast<int64_t>(blockIdx.x) * N + gn] = s;
+        partial[static_cast<int64_t>(m_tile) * N + gn] = s;
       }
     }
   }
