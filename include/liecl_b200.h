@@ -180,6 +180,13 @@ int liecl_b200_session_run_pairs(liecl_b200_session* s, int64_t g_begin, int64_t
 int liecl_b200_session_run_rows(liecl_b200_session* s, int64_t row_begin, int64_t row_end,
                                 liecl_b200_stats* stats);
 int liecl_b200_session_size(const liecl_b200_session* s, int64_t* n);
+/* Screen cursor pairs [g_begin, g_end) without applying verdicts: commutator,
+ * null test and the first projection pass against the current basis. Per pair
+ * (host arrays): null flag and pass-1 residual norm; a non-null pair with
+ * rn1 <= tolerance/20 is a certified reject. Basis and counters unchanged.
+ * (Multi-GPU: ranks screen disjoint slices of a batch.) */
+int liecl_b200_session_screen_pairs(liecl_b200_session* s, int64_t g_begin, int64_t g_end, int32_t* null_out,
+                                    double* rn1_out);
 /* Arithmetic field in use: 0 undecided, 1 general complex, 2 packed anti-Hermitian. */
 int liecl_b200_session_field(const liecl_b200_session* s, int32_t* field);
 int liecl_b200_session_get_basis(liecl_b200_session* s, double* out, int64_t cap);

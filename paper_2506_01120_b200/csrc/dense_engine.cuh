@@ -166,6 +166,30 @@ public:
     }
   }
 
+  // Screen cursor pairs [g_begin, g_end) without applying verdicts: commutator,
+  // null test and the first projection pass against the current basis.
+  // Returns per-pair null flags and pass-1 residual norms; a pair is a
+  // certified reject iff it is not null and rn1 <= tol/20 (see apply()). The
+  // basis and the counters are left untouched (multi-GPU screening).
+  void screen_pairs(int64_t g_begin, int64_t g_end, int32_t* null_out, double* rn_out) {
+    const int64_t nb = basis_size();
+    if (g_end > nb * (nb - 1) / 2 || g_begin < 0 || g_end < g_begin)
+      throw Error(LIECL_B200_INVALID_INPUT, "screen range refers to basis elements that do not exist yet");
+    for (int64_t g = g_begin; g < g_end; g += bmax_) {
+      check_deadline();
+      const int cnt = static_cast<int>(std::min<int64_t>(bmax_, g_end - g));
+      launch_commutators(g, cnt);
+      project(V_.p, Vw_.p, n_o_, C_.p, cnt, R_.p, rn1_.p);
+      CU(cudaMemcpyAsync(h_nul_.p, nul_.p, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaMemcpyAsync(h_rn1_.p, rn1_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      for (int j = 0; j < cnt; ++j) {
+        null_out[g - g_begin + j] = h_nul_.p[j];
+        rn_out[g - g_begin + j] = h_rn1_.p[j];
+      }
+    }
+  }
+
   // the whole closure after the generator loop: all pairs until exhausted
   void run_closure_pairs() {
     int64_t g = 0;

@@ -1011,6 +1011,15 @@ int liecl_b200_session_size(const liecl_b200_session* s, int64_t* n) {
   });
 }
 
+int liecl_b200_session_screen_pairs(liecl_b200_session* s, int64_t g_begin, int64_t g_end, int32_t* null_out,
+                                    double* rn1_out) {
+  return guarded([&] {
+    if (!s || (g_end > g_begin && (!null_out || !rn1_out))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    use_device(s->ctx);
+    s->eng->screen_pairs(g_begin, g_end, null_out, rn1_out);
+  });
+}
+
 int liecl_b200_session_get_vectors(liecl_b200_session* s, int64_t first, int64_t count, double* out,
                                    int32_t out_on_device, int32_t ortho) {
   return guarded([&] {

@@ -443,6 +443,15 @@ class ClosureSession:
                                                     C.byref(st)))
         return st.as_dict()
 
+    def screen_pairs(self, g_begin: int, g_end: int):
+        """(null flags, pass-1 residual norms) of pairs [g_begin, g_end); no state change."""
+        cnt = max(g_end - g_begin, 0)
+        nul = np.zeros(max(cnt, 1), np.int32)
+        rn = np.zeros(max(cnt, 1))
+        _check(self.lib.liecl_b200_session_screen_pairs(self.ptr, C.c_int64(g_begin), C.c_int64(g_end),
+                                                        nul.ctypes.data_as(C.POINTER(C.c_int32)), _dp(rn)))
+        return nul[:cnt], rn[:cnt]
+
     def size(self) -> int:
         n = C.c_int64()
         _check(self.lib.liecl_b200_session_size(self.ptr, C.byref(n)))

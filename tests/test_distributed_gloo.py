@@ -1,0 +1,149 @@
+"""Host logic of the multi-GPU closure (paper_2506_01120_b200/distributed.py)
+on CPU: world_size 2 over gloo, each rank driving a numpy stand-in of the
+device session with the engine's contract (screen_pairs / run_pairs). The
+sharded run must reproduce the single-process run exactly: same verdicts,
+same statistics, same basis."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2506_01120_b200 import workloads as w
+from paper_2506_01120_b200.distributed import DistributedClosure, TorchComm, pair_index, split
+
+
+class NumpySession:
+    """numpy model of a dimension-only ClosureSession (reference semantics:
+    CGS2 against the current basis, R:src/closure.cpp:142-162, 276-286)."""
+
+    def __init__(self, d, tol):
+        self.d, self.tol = d, tol
+        self.V = []
+
+    def _ip(self, a, b):
+        return np.vdot(a, b) / self.d
+
+    def _norm(self, a):
+        return np.linalg.norm(a) / np.sqrt(self.d)
+
+    def _project(self, h, passes):
+        r = h.copy()
+        for _ in range(passes):
+            beta = [self._ip(v, r) for v in self.V]
+            for b, v in zip(beta, self.V):
+                r = r - b * v
+        return r
+
+    def add_generators(self, gens):
+        for g in gens:
+            n = self._norm(g)
+            if n <= self.tol:
+                continue
+            r = self._project(g / n, 2)
+            rn = self._norm(r)
+            if rn > self.tol:
+                self.V.append(r / rn)
+
+    def size(self):
+        return len(self.V)
+
+    def _bracket(self, g):
+        l = int((1 + np.sqrt(1 + 8 * g)) // 2)
+        while l * (l - 1) // 2 > g:
+            l -= 1
+        while (l + 1) * l // 2 <= g:
+            l += 1
+        m = g - l * (l - 1) // 2
+        A = self.V[l].reshape(self.d, self.d, order="F")
+        B = self.V[m].reshape(self.d, self.d, order="F")
+        return (A @ B - B @ A).ravel(order="F")
+
+    def screen_pairs(self, g0, g1):
+        nul = np.zeros(g1 - g0, np.int32)
+        rn = np.zeros(g1 - g0)
+        for k, g in enumerate(range(g0, g1)):
+            h = self._bracket(g)
+            hn = self._norm(h)
+            if not hn > self.tol:
+                nul[k] = 1
+                continue
+            rn[k] = self._norm(self._project(h / hn, 1))
+        return nul, rn
+
+    def run_pairs(self, g0, g1):
+        st = {"commutators_evaluated": 0, "independence_checks": 0, "accepted": 0}
+        for g in range(g0, g1):
+            h = self._bracket(g)
+            st["commutators_evaluated"] += 1
+            hn = self._norm(h)
+            if not hn > self.tol:
+                continue
+            st["independence_checks"] += 1
+            r = self._project(h / hn, 2)
+            rn = self._norm(r)
+            if rn > self.tol:
+                self.V.append(r / rn)
+                st["accepted"] += 1
+        return st
+
+
+def _problem():
+    cfg = w.config0()  # su-type closure, d = 8, dimension 9
+    return cfg.generators, cfg.d
+
+
+def _single(batch_max):
+    gens, d = _problem()
+    s = NumpySession(d, 1e-10)
+    s.add_generators(gens)
+    st = DistributedClosure(s, 1e-10, batch_max=batch_max).run_closure()
+    return st, np.array(s.V)
+
+
+def _worker(rank, world, port, batch_max, out_dir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    gens, d = _problem()
+    s = NumpySession(d, 1e-10)
+    s.add_generators(gens)
+    dc = DistributedClosure(s, 1e-10, comm=TorchComm(), batch_max=batch_max)
+    st = dc.run_closure()
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), V=np.array(s.V),
+             stats=np.array([st.commutators_evaluated, st.independence_checks, st.accepted,
+                             st.batches_sharded, st.batches_replicated]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def test_split_covers_range():
+    for count in (0, 1, 7, 64, 1000):
+        for world in (1, 2, 3, 8):
+            parts = [split(count, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == count
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+    assert pair_index(4094, 4093) == 8382464
+
+
+@pytest.mark.parametrize("batch_max", [2, 16])
+def test_two_ranks_match_single_process(tmp_path, batch_max):
+    ref_stats, ref_V = _single(batch_max)
+    assert ref_stats.accepted == 9 - 2 and ref_stats.commutators_evaluated == 36
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, batch_max, str(tmp_path)), nprocs=2, join=True)
+    for rank in range(2):
+        got = np.load(tmp_path / f"rank{rank}.npz")
+        st = got["stats"]
+        assert st[0] == ref_stats.commutators_evaluated
+        assert st[1] == ref_stats.independence_checks
+        assert st[2] == ref_stats.accepted
+        assert np.array_equal(got["V"], ref_V)  # replicas identical, bit for bit
+    assert got["stats"][3] > 0  # some batches were sharded (saturated tail)

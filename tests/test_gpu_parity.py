@@ -294,3 +294,22 @@ def test_antihermitian_then_general_promotes(port):
                                             append=True)
     assert np.array_equal(np.concatenate([ind1, ind2]), o1)
     assert rel_err(s.basis(), room) < BASIS_RTOL
+
+
+def test_distributed_driver_single_rank_matches_session():
+    """The multi-GPU driver (screen -> all-reduce -> replicate on survivors)
+    at world size 1 on the real session equals the plain engine."""
+    from paper_2506_01120_b200.distributed import DistributedClosure
+    cfg = w.config2()
+    a = liecl.ClosureSession(64, config=liecl.ClosureConfig(tolerance=cfg.tol))
+    a.check_candidates(cfg.generators)
+    st = DistributedClosure(a, cfg.tol, batch_max=2048).run_rows(1, 160)
+    b = liecl.ClosureSession(64, config=liecl.ClosureConfig(tolerance=cfg.tol))
+    b.check_candidates(cfg.generators)
+    stb = b.run_rows(1, 160)
+    assert a.size() == b.size() == 4095
+    assert st.commutators_evaluated == stb["commutators_evaluated"] == 160 * 159 // 2
+    assert st.independence_checks == stb["independence_checks"]
+    assert st.accepted == stb["accepted"] == 4092
+    assert st.batches_sharded > 0 and st.batches_replicated > 0
+    assert rel_err(a.basis(), b.basis()) < BASIS_RTOL
