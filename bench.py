@@ -226,7 +226,7 @@ def fp64_peak_tflops(torch, device):
 def load_traffic():
     """dram bytes per launch of the projection GEMMs from the committed ncu
     capture summary (profiles/), if present."""
-    path = os.path.join(ROOT, "profiles", "ncu_zgemm_summary.json")
+    path = os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")
     if not os.path.exists(path):
         return None
     try:

@@ -60,7 +60,7 @@ def full(path, out):
                     rec[k] = v
                 rec[k + ".unit"] = units[hdr.index(k)]
         res.append(rec)
-    zg = [r for r in res if "zgemm" in r["kernel"]]
+    zg = [r for r in res if "gemm_dmma" in r["kernel"]]
 
     def to_bytes(r, k):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r.get(k + ".unit", "byte"), 1)
