@@ -70,46 +70,100 @@ public:
   }
 
   // Replace the basis by n operators (complex vec layout, host or device).
-  void set_basis(const double2* src, int64_t n, bool on_device) {
-    if (n > cap_) throw Error(LIECL_B200_CAPACITY, "basis larger than the session capacity");
+  // With `orig` (Alg. 3), the n_orig originals become the commutator basis.
+  void set_basis(const double2* src, int64_t n, bool on_device, const double2* orig = nullptr, int64_t n_orig = 0) {
+    if (n > cap_ || n_orig > cap_) throw Error(LIECL_B200_CAPACITY, "basis larger than the session capacity");
+    if (!orig) n_orig = n;
     // staging buffer persists across calls (sessions re-upload bases every step)
-    basis_stage_.ensure(static_cast<size_t>(std::max<int64_t>(n, 1) * D_));
+    basis_stage_.ensure(static_cast<size_t>(std::max<int64_t>(n + (orig ? n_orig : 0), 1) * D_));
     double2* tmp = basis_stage_.p;
-    if (n > 0)
-      CU(cudaMemcpyAsync(tmp, src, static_cast<size_t>(n * D_) * sizeof(double2),
-                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx_->stream));
-    const Field f = classify(tmp, n);
+    double2* tmp_o = tmp + n * D_;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (n > 0) CU(cudaMemcpyAsync(tmp, src, static_cast<size_t>(n * D_) * sizeof(double2), kind, ctx_->stream));
+    if (orig && n_orig > 0)
+      CU(cudaMemcpyAsync(tmp_o, orig, static_cast<size_t>(n_orig * D_) * sizeof(double2), kind, ctx_->stream));
+    const Field f = classify(tmp, n + (orig ? n_orig : 0));
     n_o_ = n_b_ = 0;
-    if (f != field_) {  // slabs are laid out per field: start them afresh
-      vcap_ = 0;
-      V_.release();
-      Vw_.release();
-      O_.release();
-      field_ = f;
-    }
+    field_ = f;
+    layout_slabs();
     alloc_batch();
-    ensure_capacity(std::min<int64_t>(cap_ + 2, n + 2));
+    ensure_capacity(std::min<int64_t>(cap_ + 2, std::max(n, n_orig) + 2));
     // slots past the new basis must read as zero (see ensure_capacity)
     CU(cudaMemsetAsync(V_.p + n * vw(), 0, static_cast<size_t>((vcap_ - n) * vw()) * sizeof(double), ctx_->stream));
     if (Vw_.p)
       CU(cudaMemsetAsync(Vw_.p + n * vw(), 0, static_cast<size_t>((vcap_ - n) * vw()) * sizeof(double),
                          ctx_->stream));
-    if (n > 0) {
+    auto put = [&](const double2* from, int64_t count, double* to) {
+      if (count == 0) return;
       if (field_ == Field::kAntiHerm) {
-        pack_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(tmp, n, d_, V_.p);
-        launched(ctx_);
-        weight_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(V_.p, n, d_, Vw_.p);
+        pack_ah_kernel<<<grid_for(count * D_), 256, 0, ctx_->stream>>>(from, count, d_, to);
         launched(ctx_);
       } else {
-        CU(cudaMemcpyAsync(V_.p, tmp, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToDevice,
+        CU(cudaMemcpyAsync(to, from, static_cast<size_t>(count * D_) * sizeof(double2), cudaMemcpyDeviceToDevice,
                            ctx_->stream));
       }
-      if (keep_)
-        CU(cudaMemcpyAsync(O_.p, V_.p, static_cast<size_t>(n * vw()) * sizeof(double), cudaMemcpyDeviceToDevice,
-                           ctx_->stream));
+    };
+    put(tmp, n, V_.p);
+    if (field_ == Field::kAntiHerm && n > 0) {
+      weight_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(V_.p, n, d_, Vw_.p);
+      launched(ctx_);
     }
+    if (keep_) put(orig ? tmp_o : tmp, n_orig, O_.p);
     CU(cudaStreamSynchronize(ctx_->stream));
-    n_o_ = n_b_ = n;
+    n_o_ = n;
+    n_b_ = keep_ ? n_orig : n;
+  }
+
+  // Small closures whose whole basis fits in shared memory run on the
+  // single-block device-resident kernel (tiny.cuh): generator loop and cursor
+  // loop without a host round trip. Returns the cursor position reached (all
+  // pairs), after which run_closure_pairs finds nothing left to do.
+  bool tiny_fits() const { return cap_ <= 4096 && tiny_smem_bytes(d_, cap_ + 1, keep_) > 0; }
+  int64_t run_tiny(const double2* gens_host, int ngens) {
+    const int64_t slots = cap_ + 1;
+    const size_t smem = tiny_smem_bytes(d_, slots, keep_);
+    tiny_v_.ensure(static_cast<size_t>(slots * D_));
+    tiny_o_.ensure(static_cast<size_t>(keep_ ? slots * D_ : 1));
+    tiny_gens_.ensure(static_cast<size_t>(std::max(ngens, 1) * D_));
+    tiny_state_.ensure(1);
+    const int64_t log_cap = ngens + cap_ * (cap_ - 1) / 2 + 1;
+    tiny_log_.ensure(static_cast<size_t>(log_cap));
+    CU(cudaMemcpyAsync(tiny_gens_.p, gens_host, static_cast<size_t>(ngens * D_) * sizeof(double2),
+                       cudaMemcpyHostToDevice, ctx_->stream));
+    if (smem > 48 * 1024)
+      CU(cudaFuncSetAttribute(tiny_closure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem)));
+    tiny_closure_kernel<<<1, tiny_threads(d_), smem, ctx_->stream>>>(tiny_gens_.p, ngens, d_, tol_, cap_,
+                                                                     keep_ ? 1 : 0, slots, tiny_v_.p, tiny_o_.p,
+                                                                     tiny_state_.p, tiny_log_.p, log_cap);
+    launched(ctx_);
+    TinyState ts;
+    CU(cudaMemcpyAsync(&ts, tiny_state_.p, sizeof ts, cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    std::vector<liecl_b200_decision> lg(static_cast<size_t>(std::min(ts.log_len, log_cap)));
+    if (!lg.empty())
+      CU(cudaMemcpyAsync(lg.data(), tiny_log_.p, lg.size() * sizeof(liecl_b200_decision), cudaMemcpyDeviceToHost,
+                         ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    for (const auto& rec : lg) {  // warnings and log, as the engine would have produced them
+      if (rec.null_cand && rec.m < 0)
+        warns_.push_back({"null_generator",
+                          "generator " + std::to_string(rec.l) + " has norm " + fmt_double(rec.residual_norm) +
+                              " and was skipped",
+                          rec.residual_norm});
+      else if (!rec.null_cand)
+        note(rec.l, rec.m, rec.residual_norm, rec.independent != 0);
+      if (record_) log_.push_back(rec);
+    }
+    if (ts.status == 2)
+      throw Error(LIECL_B200_CAPACITY,
+                  "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
+    st_.commutators_evaluated += ts.commutators;
+    st_.independence_checks += ts.checks;
+    st_.accepted += ts.accepted;
+    ++st_.batches;
+    set_basis(tiny_v_.p, ts.n_o, true, keep_ ? tiny_o_.p : nullptr, ts.n_b);
+    return ts.g_next;
   }
 
   // generator loop (R:src/closure.cpp:378-403); also the config-3 candidate
@@ -191,8 +245,7 @@ public:
   }
 
   // the whole closure after the generator loop: all pairs until exhausted
-  void run_closure_pairs() {
-    int64_t g = 0;
+  void run_closure_pairs(int64_t g = 0) {
     for (;;) {
       const int64_t nb = basis_size();
       const int64_t avail = nb * (nb - 1) / 2;
@@ -205,24 +258,7 @@ public:
   }
 
   // basis (originals for Alg. 3) or orthonormal tuple -> host, complex vec layout
-  void download(bool ortho, double* out) {
-    const int64_t n = ortho ? n_o_ : basis_size();
-    if (n == 0) return;
-    const double* src = (ortho || !keep_) ? V_.p : O_.p;
-    if (field_ == Field::kAntiHerm) {
-      DevBuf<double2> tmp;
-      tmp.ensure(static_cast<size_t>(n * D_));
-      unpack_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(src, n, d_, tmp.p);
-      launched(ctx_);
-      CU(cudaMemcpyAsync(out, tmp.p, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToHost,
-                         ctx_->stream));
-      CU(cudaStreamSynchronize(ctx_->stream));
-    } else {
-      CU(cudaMemcpyAsync(out, src, static_cast<size_t>(n * D_) * sizeof(double2), cudaMemcpyDeviceToHost,
-                         ctx_->stream));
-      CU(cudaStreamSynchronize(ctx_->stream));
-    }
-  }
+  void download(bool ortho, double* out) { copy_vectors(0, ortho ? n_o_ : basis_size(), out, false, ortho); }
 
   // elements [first, first+count) of the basis / orthonormal tuple -> out (complex vec layout)
   void copy_vectors(int64_t first, int64_t count, double* out, bool out_on_device, bool ortho) {
@@ -232,11 +268,10 @@ public:
     const double* src = ((ortho || !keep_) ? V_.p : O_.p) + first * vw();
     const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (field_ == Field::kAntiHerm) {
-      DevBuf<double2> tmp;
-      tmp.ensure(static_cast<size_t>(count * D_));
-      unpack_ah_kernel<<<grid_for(count * D_), 256, 0, ctx_->stream>>>(src, count, d_, tmp.p);
+      unpack_.ensure(static_cast<size_t>(count * D_));  // kept across calls
+      unpack_ah_kernel<<<grid_for(count * D_), 256, 0, ctx_->stream>>>(src, count, d_, unpack_.p);
       launched(ctx_);
-      CU(cudaMemcpyAsync(out, tmp.p, static_cast<size_t>(count * D_) * sizeof(double2), kind, ctx_->stream));
+      CU(cudaMemcpyAsync(out, unpack_.p, static_cast<size_t>(count * D_) * sizeof(double2), kind, ctx_->stream));
     } else {
       CU(cudaMemcpyAsync(out, src, static_cast<size_t>(count * D_) * sizeof(double2), kind, ctx_->stream));
     }
@@ -247,6 +282,7 @@ public:
   void project_residual(const double2* h_host, double* r_host, double* coeffs_host) {
     if (field_ == Field::kUnset) {
       field_ = Field::kComplex;
+      layout_slabs();
       alloc_batch();
       ensure_capacity(std::min<int64_t>(cap_ + 1, 2));
     }
@@ -299,11 +335,28 @@ private:
     const Field f = (field_ == Field::kComplex) ? Field::kComplex : classify(x, count);
     if (field_ == Field::kUnset) {
       field_ = (n_o_ == 0) ? f : Field::kComplex;
+      const bool reuse = layout_slabs();
       alloc_batch();
       ensure_capacity(std::min<int64_t>(cap_ + 1, std::max<int64_t>(64, (int64_t(1) << 30) / (D_ * 16))));
+      if (reuse && vcap_ > 0) {  // a previous closure's vectors: restore the zero tail invariant
+        CU(cudaMemsetAsync(V_.p, 0, static_cast<size_t>(vcap_ * vw()) * sizeof(double), ctx_->stream));
+        if (Vw_.p) CU(cudaMemsetAsync(Vw_.p, 0, static_cast<size_t>(vcap_ * vw()) * sizeof(double), ctx_->stream));
+      }
     } else if (field_ == Field::kAntiHerm && f == Field::kComplex) {
       promote_to_complex();
     }
+  }
+
+  // Slabs keep their allocation across closures while the layout (field) is
+  // unchanged; returns true when existing slabs are reused.
+  bool layout_slabs() {
+    if (slab_field_ == field_) return true;
+    vcap_ = 0;
+    V_.release();
+    Vw_.release();
+    O_.release();
+    slab_field_ = field_;
+    return false;
   }
 
   void promote_to_complex() {
@@ -328,7 +381,7 @@ private:
     std::swap(V_.p, nv.p); std::swap(V_.n, nv.n);
     if (keep_) { std::swap(O_.p, no.p); std::swap(O_.n, no.n); }
     Vw_.release();
-    field_ = Field::kComplex;
+    field_ = slab_field_ = Field::kComplex;
     vcap_ = cap;
     alloc_batch();
     P_.release();
@@ -618,6 +671,8 @@ private:
   bool record_;
   bool force_complex_;
   Field field_ = Field::kUnset;
+  Field slab_field_ = Field::kUnset;  // layout the basis slabs are allocated for
+  DevBuf<double2> unpack_;            // packed -> complex output staging
   int64_t cap_ = 0, bmax_ = 0, B_cur_ = 0;
   double sqrt_d_ = 1.0;
   bool has_deadline_ = false;
@@ -631,6 +686,9 @@ private:
   DevBuf<double> V_, Vw_, O_, C_, R_, X_, Y_, P_;  // element width ew() doubles
   DevBuf<double2> stage_;                          // complex input staging
   DevBuf<double2> basis_stage_;                    // set_basis staging (kept across calls)
+  DevBuf<double2> tiny_v_, tiny_o_, tiny_gens_;  // device-resident small closures
+  DevBuf<TinyState> tiny_state_;
+  DevBuf<liecl_b200_decision> tiny_log_;
   DevBuf<double> partial_, rn1_, rn2_, hn_, yn_;
   DevBuf<int> nul_, idx_;
   DevBuf<unsigned long long> small_;

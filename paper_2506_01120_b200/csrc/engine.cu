@@ -41,6 +41,7 @@
 #include "commutator.cuh"
 #include "dgemm_dmma.cuh"
 #include "pauli.cuh"
+#include "tiny.cuh"
 #include "vecops.cuh"
 #include "zgemm_dmma.cuh"
 
@@ -819,8 +820,13 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
     }
     DenseEngine& eng = *cached;
     eng.reset_stats();
-    eng.run_candidates(reinterpret_cast<const double2*>(gens), ngens, false, nullptr, nullptr, true);
-    eng.run_closure_pairs();
+    if (eng.tiny_fits()) {
+      // small closures: one device-resident launch (the batched engine then finds no pair left)
+      eng.run_closure_pairs(eng.run_tiny(reinterpret_cast<const double2*>(gens), ngens));
+    } else {
+      eng.run_candidates(reinterpret_cast<const double2*>(gens), ngens, false, nullptr, nullptr, true);
+      eng.run_closure_pairs();
+    }
     const int64_t n = eng.basis_size();
     *stats = eng.stats();
     stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();

@@ -313,3 +313,22 @@ def test_distributed_driver_single_rank_matches_session():
     assert st.accepted == stb["accepted"] == 4092
     assert st.batches_sharded > 0 and st.batches_replicated > 0
     assert rel_err(a.basis(), b.basis()) < BASIS_RTOL
+
+
+@pytest.mark.parametrize("keep", [False, True], ids=["dimonly", "orthonorm"])
+def test_tiny_kernel_hands_over_to_batched_engine(ref, port, keep):
+    """HEA n=4 as dense operators (d = 16, closure dimension 255): the
+    device-resident small-closure kernel runs the first 128 elements, the
+    batched engine the rest; verdicts must equal the oracle's throughout."""
+    off, x, z, c = ref.build_generators("hea", 4)
+    gens = np.stack([1j * ref.from_pauli(x[off[i]:off[i + 1]], z[off[i]:off[i + 1]], c[off[i]:off[i + 1]], 4)
+                     for i in range(len(off) - 1)])
+    method = liecl.Method.orthonorm if keep else liecl.Method.orthonorm_dimonly
+    res = liecl.closure_dense_arrays(gens, 16, method, liecl.ClosureConfig(tolerance=1e-10, record_log=True))
+    o = port.closure_dense(gens, 16, keep_original=keep, tol=1e-10, threads=8, log_cap=1 << 16)
+    assert res.dimension == o.dimension == 255
+    assert res.stats.commutators_evaluated == o.stats["commutators_evaluated"] == 255 * 254 // 2
+    assert res.stats.independence_checks == o.stats["independence_checks"]
+    assert np.array_equal(res.decision_log["independent"], o.log["independent"])
+    assert np.array_equal(res.decision_log["null_cand"], o.log["null_cand"])
+    assert rel_err(res.basis_array, o.basis) < BASIS_RTOL
