@@ -267,7 +267,8 @@ def run_b200_arm(a):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:
+    launched_by_torchrun = "RANK" in os.environ
+    if launched_by_torchrun:  # NCCL even for one rank, so the multi-rank path is the one exercised
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
     from paper_2506_01120_b200 import liecl, native, workloads as w
@@ -277,12 +278,12 @@ def run_b200_arm(a):
     cfg = w.config2()
 
     def barrier():
-        if world > 1:
+        if launched_by_torchrun:
             import torch.distributed as dist
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
+        if not launched_by_torchrun:
             return x
         import torch.distributed as dist
         t = torch.tensor([x], dtype=torch.float64, device=device)
@@ -531,7 +532,7 @@ def main():
         run_c3(a)
     else:
         run_b200_arm(a)
-    if int(os.environ.get("WORLD_SIZE", 1)) > 1 and a.impl == "b200":
+    if "RANK" in os.environ and a.impl == "b200":
         import torch.distributed as dist
         if dist.is_initialized():
             dist.destroy_process_group()
