@@ -63,6 +63,11 @@ typedef struct {
                                packed-real path (su(d)/u(d), 4x fewer projection
                                flops); 1 = always the general complex path     */
   uint32_t reserved;
+  /* matrix-inversion method (Alg. 2): ClosureConfig::conditioning_floor and
+   * gram_refresh_interval (R:include/liecl/closure.hpp:97-100), used as given
+   * (the reference defaults are 1e-12 and 256; interval 0 = no cadence refresh) */
+  double conditioning_floor;
+  uint64_t gram_refresh_interval;
 } liecl_b200_config;
 
 /* liecl::ClosureStats (R:include/liecl/closure.hpp:63-69) + engine counters */
@@ -131,6 +136,20 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
                              double* ortho_out, int64_t cap, liecl_b200_stats* stats, char* warnings,
                              int64_t warnings_len, liecl_b200_decision* log, int64_t log_cap,
                              int64_t* log_len);
+
+/*
+ * close_matrix_inversion (R:include/liecl/closure.hpp:112-113; Alg. 2) for
+ * dense generators: basis_out receives the accepted unit candidates (cap
+ * operators), gram_out / inverse_out (may be NULL) the final Gram matrix A and
+ * its maintained inverse as n x n column-major complex (result.gram,
+ * R:include/liecl/closure.hpp:81-82). liecl_b200_closure_dense with method
+ * LIECL_B200_METHOD_MATRIX_INVERSION runs the same without the Gram outputs.
+ */
+int liecl_b200_closure_dense_gram(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d,
+                                  const liecl_b200_config* cfg, double* basis_out, int64_t cap, double* gram_out,
+                                  double* inverse_out, liecl_b200_stats* stats, char* warnings,
+                                  int64_t warnings_len, liecl_b200_decision* log, int64_t log_cap,
+                                  int64_t* log_len);
 
 /*
  * run_closure for Pauli generators that are single strings (one term each;

@@ -24,6 +24,7 @@
 // The Pauli single-string path (pauli.cuh) is bit-exact and runs frontier
 // batches of all available pairs.
 #include <cub/device/device_scan.cuh>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -380,7 +381,69 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
   t.stop();
 }
 
+// C[m + n*ldc] = alpha * sum_k A(m, k) B(k, n), A M-contiguous (A(m,k) = A[k*lda + m]),
+// B K-contiguous (ld ldb); split-K for small grids. (x = A^{-1} beta in Alg. 2.)
+void gemm_mc_store(liecl_b200_ctx* ctx, const double2* A, int64_t lda, int64_t M, int64_t K, const double2* B,
+                   int64_t ldb, int count, double2* C, int64_t ldc, double alpha) {
+  if (M == 0 || count == 0) return;
+  gemm_attr_once<false, false, Epilogue::kStoreScaled>();
+  dim3 grid((M + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
+  Timer t(ctx, 3, 8.0 * static_cast<double>(M) * static_cast<double>(K) * count);
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, K);
+  if (slices <= 1) {
+    zgemm_dmma_kernel<false, false, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(
+        static_cast<int>(M), count, static_cast<int>(K), A, lda, B, ldb, C, ldc, alpha, nullptr, 0, nullptr, 0, 0);
+    launched(ctx);
+  } else {
+    const int chunk = static_cast<int>(((K + slices - 1) / slices + zg::BK - 1) / zg::BK * zg::BK);
+    slices = static_cast<int>((K + chunk - 1) / chunk);
+    const int64_t stride = ldc * count;
+    ctx->splitk_ws.ensure(static_cast<size_t>(slices * stride));
+    grid.z = slices;
+    zgemm_dmma_kernel<false, false, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(
+        static_cast<int>(M), count, static_cast<int>(K), A, lda, B, ldb, ctx->splitk_ws.p, ldc, 1.0, nullptr, 0,
+        nullptr, chunk, stride);
+    launched(ctx);
+    splitk_reduce_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>((stride + 255) / 256, 1024)), 256, 0,
+                                 ctx->stream>>>(ctx->splitk_ws.p, slices, stride, stride, alpha, C);
+    launched(ctx);
+  }
+  t.stop();
+}
+
+// K1 for the general complex field over basis slab `basis` (pairs [g0, g0+cnt))
+void launch_commutator_complex(liecl_b200_ctx* ctx, const double2* basis, int d, int64_t g0, int cnt, double tol,
+                               double2* out, double* hn, int* nul) {
+  auto tmpl = [&](auto dimc) {
+    constexpr int DIM = decltype(dimc)::value;
+    using S = CommShape<DIM>;
+    static bool attr = false;
+    if (!attr) {
+      CU(cudaFuncSetAttribute(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
+      attr = true;
+    }
+    Timer t(ctx, 2, 16.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
+    commutator_norm_kernel<DIM><<<(cnt + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA, 256, S::SMEM, ctx->stream>>>(
+        basis, g0, cnt, tol, true, out, hn, nul);
+    launched(ctx);
+    t.stop();
+  };
+  switch (d) {
+  case 8: tmpl(std::integral_constant<int, 8>{}); break;
+  case 16: tmpl(std::integral_constant<int, 16>{}); break;
+  case 32: tmpl(std::integral_constant<int, 32>{}); break;
+  case 64: tmpl(std::integral_constant<int, 64>{}); break;
+  default: {
+    Timer t(ctx, 2, 16.0 * d * d * static_cast<double>(d) * cnt);
+    commutator_generic_kernel<<<cnt, 256, 0, ctx->stream>>>(basis, d, g0, cnt, tol, true, out, hn, nul);
+    launched(ctx);
+    t.stop();
+  }
+  }
+}
+
 #include "dense_engine.cuh"
+#include "gram_engine.cuh"
 
 // --------------------------------------------------------- Pauli engine ---
 
@@ -709,7 +772,9 @@ void copy_log(const std::vector<liecl_b200_decision>& lg, liecl_b200_decision* l
 liecl_b200_config default_config(const liecl_b200_config* cfg) {
   if (cfg) return *cfg;
   liecl_b200_config c{};
-  c.tolerance = 1e-8;  // ClosureConfig default, R:include/liecl/closure.hpp:88
+  c.tolerance = 1e-8;  // ClosureConfig defaults, R:include/liecl/closure.hpp:88-100
+  c.conditioning_floor = 1e-12;
+  c.gram_refresh_interval = 256;
   return c;
 }
 
@@ -723,6 +788,22 @@ bool keep_for(int method) {
 }
 
 void use_device(liecl_b200_ctx* ctx) { CU(cudaSetDevice(ctx->device)); }
+
+// close_matrix_inversion (R:src/closure.cpp:519-527) on the GramEngine
+void run_gram_closure(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d, const liecl_b200_config& cfg,
+                      double* basis_out, int64_t cap, double* gram_out, double* inverse_out, liecl_b200_stats* stats,
+                      char* warnings, int64_t warnings_len, liecl_b200_decision* log, int64_t log_cap,
+                      int64_t* log_len) {
+  GramEngine eng(ctx, d, cfg);
+  eng.run_generators(reinterpret_cast<const double2*>(gens), ngens);
+  eng.run_closure_pairs();
+  *stats = eng.stats();
+  write_warnings(eng.warnings(), warnings, warnings_len);
+  copy_log(eng.log(), log, log_cap, log_len);
+  if (eng.size() > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
+  eng.download_basis(basis_out);
+  eng.download_gram(gram_out, inverse_out);
+}
 
 } // namespace
 
@@ -809,6 +890,12 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
     use_device(ctx);
     const auto t0 = Clock::now();
     const liecl_b200_config cfg = default_config(cfg_in);
+    if (method == LIECL_B200_METHOD_MATRIX_INVERSION) {
+      run_gram_closure(ctx, gens, ngens, d, cfg, basis_out, cap, nullptr, nullptr, stats, warnings, warnings_len, log,
+                       log_cap, log_len);
+      stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+      return;
+    }
     const bool keep = keep_for(method);
     auto cached = std::static_pointer_cast<DenseEngine>(ctx->dense_cache);
     if (cached && cached->compatible(d, keep, cfg)) {
@@ -835,6 +922,21 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
     if (n > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
     eng.download(false, basis_out);
     if (ortho_out) eng.download(true, ortho_out);
+  });
+}
+
+int liecl_b200_closure_dense_gram(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d,
+                                  const liecl_b200_config* cfg_in, double* basis_out, int64_t cap, double* gram_out,
+                                  double* inverse_out, liecl_b200_stats* stats, char* warnings, int64_t warnings_len,
+                                  liecl_b200_decision* log, int64_t log_cap, int64_t* log_len) {
+  return guarded([&] {
+    if (!ctx || !gens || !basis_out || !stats) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (ngens <= 0) throw Error(LIECL_B200_INVALID_INPUT, "closure requires a non-empty generator tuple");
+    use_device(ctx);
+    const auto t0 = Clock::now();
+    run_gram_closure(ctx, gens, ngens, d, default_config(cfg_in), basis_out, cap, gram_out, inverse_out, stats,
+                     warnings, warnings_len, log, log_cap, log_len);
+    stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
   });
 }
 

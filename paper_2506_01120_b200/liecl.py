@@ -195,7 +195,8 @@ class ClosureConfig:
         if self.field not in ("auto", "complex"):
             raise InvalidInputError(f"unknown field '{self.field}' (expected auto or complex)")
         return native.Config(float(self.tolerance), int(self.max_dim), int(self.threads), int(self.record_log),
-                             rel, int(self.batch_max), 1 if self.field == "complex" else 0, 0)
+                             rel, int(self.batch_max), 1 if self.field == "complex" else 0, 0,
+                             float(self.conditioning_floor), int(self.gram_refresh_interval))
 
 
 @dataclass
@@ -210,6 +211,7 @@ class ClosureResult:
     decision_log: np.ndarray | None = None
     basis_array: np.ndarray | None = None  # dense: (n, d*d) vec layout; pauli: (x, z, coef)
     ortho_array: np.ndarray | None = None
+    gram: tuple | None = None  # (A, A^{-1}) for matrix inversion (R:include/liecl/closure.hpp:81-82)
 
 
 DECISION_DTYPE = np.dtype([("l", np.int64), ("m", np.int64), ("null_cand", np.int32),
@@ -258,6 +260,8 @@ def closure_dense_arrays(gens: np.ndarray, d: int, method: Method = Method.ortho
     lib = native.load()
     cap = int(config.max_dim or d * d)
     basis = np.zeros((cap, d * d), np.complex128)
+    if method == Method.matrix_inversion:
+        return _closure_dense_gram(gens, d, config, device, cap, basis)
     keep = method == Method.orthonorm
     ortho = np.zeros((cap, d * d), np.complex128) if keep else None
     st = native.Stats()
@@ -281,6 +285,36 @@ def closure_dense_arrays(gens: np.ndarray, d: int, method: Method = Method.ortho
     return ClosureResult([DenseOperator.from_vec(v, d) for v in b], [DenseOperator.from_vec(v, d) for v in o], n,
                          method, Backend.dense, config.tolerance, stats,
                          log[: log_len.value].copy() if config.record_log else None, b, o)
+
+
+def _closure_dense_gram(gens, d, config, device, cap, basis) -> ClosureResult:
+    """close_matrix_inversion (Alg. 2): basis = accepted unit candidates, gram = (A, A^{-1})."""
+    lib = native.load()
+    st = native.Stats()
+    wbuf = C.create_string_buffer(1 << 20)
+    log_cap = (cap * cap // 2 + 64 + len(gens)) if config.record_log else 0
+    log = np.zeros(max(log_cap, 1), DECISION_DTYPE)
+    log_len = C.c_int64()
+    gram = np.zeros((cap, cap), np.complex128)
+    inv = np.zeros((cap, cap), np.complex128)
+    cfg = config.native()
+    _check(lib.liecl_b200_closure_dense_gram(
+        native.context(device), _dp(gens.view(np.float64)), C.c_int32(len(gens)), C.c_int32(d), C.byref(cfg),
+        _dp(basis.view(np.float64)), C.c_int64(cap), _dp(gram.view(np.float64)), _dp(inv.view(np.float64)),
+        C.byref(st), wbuf, C.c_int64(len(wbuf)), log.ctypes.data_as(C.c_void_p) if config.record_log else None,
+        C.c_int64(log_cap), C.byref(log_len)))
+    n = int(st.dimension)
+    stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds,
+                         _parse_warnings(wbuf.value),
+                         {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
+    b = basis[:n]
+    # n x n column-major blocks written with leading dimension n
+    A = gram.ravel()[: n * n].reshape(n, n, order="F").copy()
+    Ai = inv.ravel()[: n * n].reshape(n, n, order="F").copy()
+    res = ClosureResult([DenseOperator.from_vec(v, d) for v in b], None, n, Method.matrix_inversion, Backend.dense,
+                        config.tolerance, stats, log[: log_len.value].copy() if config.record_log else None, b, None)
+    res.gram = (A, Ai)
+    return res
 
 
 def closure_pauli_arrays(x, z, coef, qubits: int, method: Method = Method.orthonorm_dimonly,
@@ -322,10 +356,13 @@ def closure_pauli_arrays(x, z, coef, qubits: int, method: Method = Method.orthon
 
 
 def run_closure(generators, method: Method, config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
-    """R:src/closure.cpp:541-564 for the orthonormal methods."""
-    if method in (Method.standard_rank, Method.matrix_inversion):
-        raise InvalidInputError(f"{to_string(method)}: not on the B200 hot path (orthonorm methods only)")
+    """R:src/closure.cpp:541-564: orthonormal methods (dense + single-string
+    Pauli) and matrix inversion (dense)."""
+    if method == Method.standard_rank:
+        raise InvalidInputError(f"{to_string(method)}: not on the B200 hot path")
     backend, dim = _validate(generators)
+    if method == Method.matrix_inversion and backend != Backend.dense:
+        raise InvalidInputError("matrix-inversion on the B200 path takes dense generators")
     if backend == Backend.dense:
         gens = np.stack([g.vec() if g is not None else np.zeros(dim * dim, np.complex128) for g in generators])
         return closure_dense_arrays(gens, dim, method, config, device)

@@ -20,7 +20,8 @@ METHOD_STANDARD_RANK, METHOD_MATRIX_INVERSION, METHOD_ORTHONORM, METHOD_ORTHONOR
 EXPORTED = [
     "liecl_b200_abi_version", "liecl_b200_last_error", "liecl_b200_ctx_create", "liecl_b200_ctx_destroy",
     "liecl_b200_ctx_kernel_count", "liecl_b200_ctx_set_stream", "liecl_b200_ctx_set_timing",
-    "liecl_b200_ctx_kernel_times", "liecl_b200_closure_dense", "liecl_b200_closure_pauli",
+    "liecl_b200_ctx_kernel_times", "liecl_b200_closure_dense", "liecl_b200_closure_dense_gram",
+    "liecl_b200_closure_pauli",
     "liecl_b200_project_residual_dense", "liecl_b200_commutator_dense", "liecl_b200_inner_product_dense",
     "liecl_b200_norm_dense", "liecl_b200_session_create_dense", "liecl_b200_session_destroy",
     "liecl_b200_session_set_basis", "liecl_b200_session_run_pairs", "liecl_b200_session_run_rows",
@@ -38,7 +39,8 @@ class NativeUnavailable(RuntimeError):
 class Config(C.Structure):
     _fields_ = [("tolerance", C.c_double), ("max_dim", C.c_uint64), ("threads", C.c_uint32),
                 ("record_log", C.c_uint32), ("deadline_seconds", C.c_double), ("batch_max", C.c_int64),
-                ("field", C.c_uint32), ("reserved", C.c_uint32)]
+                ("field", C.c_uint32), ("reserved", C.c_uint32), ("conditioning_floor", C.c_double),
+                ("gram_refresh_interval", C.c_uint64)]
 
 
 class Stats(C.Structure):

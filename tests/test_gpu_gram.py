@@ -1,0 +1,78 @@
+"""Matrix-inversion strategy (Alg. 2) on the GPU against the
+reference build (oracle/_ref, which runs the reference's own
+MatrixInversionStrategy + GramState, R:src/closure.cpp:44-140, 214-265)."""
+import numpy as np
+import pytest
+
+from paper_2506_01120_b200 import liecl
+from paper_2506_01120_b200 import workloads as w
+
+pytestmark = pytest.mark.gpu
+MI = liecl.Method.matrix_inversion
+
+
+def rel_err(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def dense_family(ref, family, n, scale=1j):
+    off, x, z, c = ref.build_generators(family, n)
+    return np.stack([scale * ref.from_pauli(x[off[i]:off[i + 1]], z[off[i]:off[i + 1]], c[off[i]:off[i + 1]], n)
+                     for i in range(len(off) - 1)])
+
+
+def compare(ref, gens, d, tol=1e-10):
+    mine = liecl.closure_dense_arrays(gens, d, MI, liecl.ClosureConfig(tolerance=tol))
+    theirs = ref.closure_dense(gens, d, method="matrix-inversion", tol=tol)
+    assert mine.dimension == theirs.dimension
+    assert mine.stats.commutators_evaluated == theirs.stats["commutators_evaluated"]
+    assert mine.stats.independence_checks == theirs.stats["independence_checks"]
+    assert mine.stats.accepted == theirs.stats["accepted"]
+    # the basis is the accepted unit candidates, in order: same accept sequence
+    assert rel_err(mine.basis_array, theirs.basis) < 1e-10
+    kinds = sorted(line.split("\t")[0] for line in theirs.warnings.splitlines() if line)
+    assert sorted(wr.kind for wr in mine.stats.warnings) == kinds
+    return mine
+
+
+@pytest.mark.parametrize("make", [w.config0, w.config1], ids=["c0", "c1"])
+def test_matrix_inversion_configs_match_reference(ref, make):
+    cfg = make()
+    compare(ref, cfg.generators, cfg.d, cfg.tol)
+
+
+@pytest.mark.parametrize("family,n,dim", [("hea", 2, 15), ("hea", 3, 63), ("spin_glass_hva", 3, 63),
+                                          ("hea", 4, 255)])
+def test_matrix_inversion_paper_dims(ref, family, n, dim):
+    res = compare(ref, dense_family(ref, family, n), 1 << n)
+    assert res.dimension == dim
+
+
+def test_gram_state_lemma_3_1(ref):
+    # SPEC acceptance 8: spin-glass n = 3 -> A positive definite, ||A A^-1 - I|| <= 1e-6
+    res = liecl.closure_dense_arrays(dense_family(ref, "spin_glass_hva", 3), 8, MI,
+                                     liecl.ClosureConfig(tolerance=1e-10))
+    A, Ai = res.gram
+    assert res.dimension == 63 and A.shape == (63, 63)
+    assert np.abs(A - A.conj().T).max() < 1e-13
+    assert np.abs(np.diag(A) - 1).max() == 0.0  # unit diagonal, exactly (R:include/liecl/closure.hpp:25-27)
+    assert np.linalg.eigvalsh(A).min() > 0
+    assert np.abs(A @ Ai - np.eye(63)).max() <= 1e-6
+
+
+def test_expand_gram_spec_example():
+    # SPEC.md expand_gram: beta = 0.5 -> A^-1 = ((4/3, -2/3), (-2/3, 4/3)).
+    # Generators X and (X + sqrt(3) I)/2 commute, so the closure stops at 2.
+    X = np.array([[0, 1], [1, 0]], complex)
+    h = (X + np.sqrt(3) * np.eye(2)) / 2
+    gens = np.stack([X.ravel(order="F"), h.ravel(order="F")])
+    res = liecl.closure_dense_arrays(gens, 2, MI, liecl.ClosureConfig(tolerance=1e-10))
+    A, Ai = res.gram
+    assert res.dimension == 2
+    assert np.abs(A - np.array([[1, 0.5], [0.5, 1]])).max() < 1e-15
+    assert np.abs(Ai - np.array([[4 / 3, -2 / 3], [-2 / 3, 4 / 3]])).max() < 1e-14
+
+
+def test_pauli_matrix_inversion_is_rejected():
+    with pytest.raises(liecl.InvalidInputError):
+        liecl.run_closure([liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)], MI)
