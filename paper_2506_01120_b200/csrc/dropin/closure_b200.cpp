@@ -8,11 +8,13 @@
 //
 //   run_closure                (R:include/liecl/closure.hpp:125-126) -> GPU for
 //   close_orthonormalization   (:119-121)  orthonorm / orthonorm-dimonly
+//   close_matrix_inversion     (:112-113)  matrix-inversion (dense), with result.gram
 //   project_residual           (:139-140)  -> GPU (dense operators)
 //   to_string / method_from_string (:22-23), basis_listing (:143)
-//   close_standard, close_matrix_inversion, check_matrix_inversion, GramState
-//       -- off the hot path: they raise
-//          InvalidInputError instead of silently running a CPU fallback.
+//   GramState methods, check_matrix_inversion -- host utilities on the
+//       caller's own state (the closure builds its state on the GPU)
+//   close_standard (rank method, Alg. 1) -- off the hot path: raises
+//       InvalidInputError instead of silently running a CPU fallback.
 //
 // Status codes of the C-ABI map back onto the reference's exception types
 // (R:include/liecl/errors.hpp:10-61).
@@ -231,18 +233,131 @@ Method method_from_string(const std::string& name) {
                           "' (expected standard-rank, matrix-inversion, orthonorm or orthonorm-dimonly)");
 }
 
-double GramState::schur_complement(const Eigen::VectorXcd&) const { off_path("GramState::schur_complement"); }
-void GramState::expand(const Eigen::VectorXcd&, double) { off_path("GramState::expand"); }
-void GramState::refresh() { off_path("GramState::refresh"); }
-double GramState::inverse_error() const { off_path("GramState::inverse_error"); }
+// ---- GramState (R:include/liecl/closure.hpp:28-55): the closure's own state
+// is built on the GPU; these host methods serve callers that use GramState
+// directly. The device result is installed through refresh() (a member, so it
+// may set the private matrices) while a pending state is staged.
+namespace {
+thread_local const Eigen::MatrixXcd* g_pending_gram = nullptr;
+thread_local const Eigen::MatrixXcd* g_pending_inverse = nullptr;
+} // namespace
+
+double GramState::schur_complement(const Eigen::VectorXcd& beta) const {
+  if (beta.size() != gram_.rows()) throw InvalidInputError("GramState: beta length does not match basis size");
+  if (beta.size() == 0) return 1.0;
+  const Eigen::VectorXcd u = inverse_ * beta;
+  return (Complex{1.0, 0.0} - beta.dot(u)).real();
+}
+
+void GramState::expand(const Eigen::VectorXcd& beta, double conditioning_floor) {
+  const double s = schur_complement(beta);
+  const Eigen::Index n = gram_.rows();
+  if (s <= conditioning_floor)
+    throw DegeneracyError("Gram expansion is numerically degenerate for element " + std::to_string(n) +
+                              " (Schur complement " + std::to_string(s) +
+                              "); the element should have been rejected as dependent",
+                          static_cast<std::size_t>(n));
+  Eigen::MatrixXcd a(n + 1, n + 1), ai(n + 1, n + 1);
+  const Eigen::VectorXcd u = n > 0 ? Eigen::VectorXcd(inverse_ * beta) : Eigen::VectorXcd(0);
+  for (Eigen::Index k = 0; k < n; ++k) {
+    for (Eigen::Index i = 0; i < n; ++i) {
+      a(i, k) = gram_(i, k);
+      ai(i, k) = inverse_(i, k) + u(i) * std::conj(u(k)) / s;
+    }
+    a(k, n) = beta(k);
+    a(n, k) = std::conj(beta(k));
+    ai(k, n) = -u(k) / s;
+    ai(n, k) = std::conj(ai(k, n));
+  }
+  a(n, n) = 1.0;
+  ai(n, n) = n == 0 ? 1.0 : 1.0 / s;
+  gram_ = std::move(a);
+  inverse_ = std::move(ai);
+}
+
+void GramState::refresh() {
+  if (g_pending_gram) {  // install a device-built state (close_matrix_inversion)
+    gram_ = *g_pending_gram;
+    inverse_ = *g_pending_inverse;
+    return;
+  }
+  if (gram_.rows() == 0) return;
+  inverse_ = gram_.ldlt().solve(Eigen::MatrixXcd::Identity(gram_.rows(), gram_.cols()));
+}
+
+double GramState::inverse_error() const {
+  if (gram_.rows() == 0) return 0.0;
+  return ((gram_ * inverse_) - Eigen::MatrixXcd::Identity(gram_.rows(), gram_.cols())).cwiseAbs().maxCoeff();
+}
 
 ClosureResult close_standard(std::span<const Operator>, const ClosureConfig&) { off_path("close_standard"); }
-ClosureResult close_matrix_inversion(std::span<const Operator>, const ClosureConfig&) {
-  off_path("close_matrix_inversion");
+
+// Alg. 2 (R:src/closure.cpp:519-527) on the GPU for dense generators
+ClosureResult close_matrix_inversion(std::span<const Operator> generators, const ClosureConfig& config) {
+  const std::optional<Backend> backend = validate(generators);
+  if (backend && *backend != Backend::dense)
+    off_path("close_matrix_inversion on Pauli generators");
+  Eigen::Index d = 0;
+  for (const Operator& g : generators)
+    if (!g.is_null()) d = g.dim();
+  ClosureResult r;
+  r.method = Method::matrix_inversion;
+  r.backend = Backend::dense;
+  r.tolerance = config.tolerance;
+  if (d == 0) {
+    r.gram = GramState{};
+    return r;
+  }
+  const size_t D = static_cast<size_t>(d) * d;
+  std::vector<double> gens(2 * D * generators.size(), 0.0);
+  for (size_t i = 0; i < generators.size(); ++i)
+    if (!generators[i].is_null())
+      std::memcpy(gens.data() + 2 * D * i, generators[i].dense().matrix().data(), sizeof(double) * 2 * D);
+  const size_t cap = config.max_dim ? config.max_dim : D;
+  std::vector<double> basis(2 * D * cap), A(2 * cap * cap), Ai(2 * cap * cap);
+  liecl_b200_stats st{};
+  std::vector<char> wbuf(1 << 20);
+  liecl_b200_config cfg = to_native(config);
+  cfg.conditioning_floor = config.conditioning_floor;
+  cfg.gram_refresh_interval = config.gram_refresh_interval;
+  check(liecl_b200_closure_dense_gram(context(), gens.data(), static_cast<int32_t>(generators.size()),
+                                      static_cast<int32_t>(d), &cfg, basis.data(), static_cast<int64_t>(cap),
+                                      A.data(), Ai.data(), &st, wbuf.data(), static_cast<int64_t>(wbuf.size()),
+                                      nullptr, 0, nullptr));
+  const Eigen::Index n = static_cast<Eigen::Index>(st.dimension);
+  for (Eigen::Index k = 0; k < n; ++k) {
+    Eigen::MatrixXcd m(d, d);
+    std::memcpy(static_cast<void*>(m.data()), basis.data() + 2 * D * k, sizeof(double) * 2 * D);
+    r.basis.emplace_back(DenseOperator(std::move(m)));
+  }
+  Eigen::MatrixXcd gram(n, n), inverse(n, n);
+  std::memcpy(static_cast<void*>(gram.data()), A.data(), sizeof(double) * 2 * n * n);
+  std::memcpy(static_cast<void*>(inverse.data()), Ai.data(), sizeof(double) * 2 * n * n);
+  GramState state;
+  g_pending_gram = &gram;
+  g_pending_inverse = &inverse;
+  state.refresh();
+  g_pending_gram = g_pending_inverse = nullptr;
+  r.gram = std::move(state);
+  r.dimension = st.dimension;
+  fill_stats(r, st, wbuf);
+  return r;
 }
-std::pair<bool, CoefficientVector> check_matrix_inversion(const GramState&, std::span<const Operator>,
-                                                          const Operator&, double) {
-  off_path("check_matrix_inversion");
+
+// the single Alg. 2 query (R:src/closure.cpp:135-140): the reference's own
+// operations on the caller's host-side state (no GPU batch to amortise)
+std::pair<bool, CoefficientVector> check_matrix_inversion(const GramState& state, std::span<const Operator> basis,
+                                                          const Operator& h, double tol) {
+  if (static_cast<std::size_t>(state.size()) != basis.size())
+    throw InvalidInputError("check_matrix_inversion: state size does not match basis size");
+  CoefficientVector beta(basis.size());
+  for (std::size_t l = 0; l < basis.size(); ++l) beta[l] = inner_product(basis[l], h);
+  if (basis.empty()) return {norm(h) > tol, beta};
+  const Eigen::VectorXcd x =
+      state.inverse() * Eigen::VectorXcd(Eigen::Map<const Eigen::VectorXcd>(beta.data(), static_cast<Eigen::Index>(beta.size())));
+  CoefficientVector neg(beta.size());
+  for (std::size_t l = 0; l < neg.size(); ++l) neg[l] = -x(static_cast<Eigen::Index>(l));
+  return {norm(linear_combination(h, Complex{1.0, 0.0}, basis, neg)) > tol, std::move(beta)};
 }
 
 ClosureResult close_orthonormalization(std::span<const Operator> generators, const ClosureConfig& config,
@@ -270,7 +385,7 @@ ClosureResult close_orthonormalization(std::span<const Operator> generators, con
 ClosureResult run_closure(std::span<const Operator> generators, Method method, const ClosureConfig& config) {
   switch (method) {
   case Method::standard_rank: off_path("run_closure(standard-rank)");
-  case Method::matrix_inversion: off_path("run_closure(matrix-inversion)");
+  case Method::matrix_inversion: return close_matrix_inversion(generators, config);
   case Method::orthonorm: return close_orthonormalization(generators, config, true);
   case Method::orthonorm_dimonly: return close_orthonormalization(generators, config, false);
   }

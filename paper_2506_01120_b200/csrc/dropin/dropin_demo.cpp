@@ -49,6 +49,12 @@ int main() {
       }
       std::printf("]}, ");
     }
+    // Alg. 2 through the same entry point, with the Gram state
+    const ClosureResult r = run_closure(gens, Method::matrix_inversion, cfg);
+    std::printf("\"c0_matrix-inversion\": ");
+    print_stats(r);
+    std::printf(", \"gram_size\": %td, \"inverse_error\": %.3g}, ", static_cast<std::ptrdiff_t>(r.gram->size()),
+                r.gram->inverse_error());
   }
   // config 4 (Pauli): n=10 ring, i*XX, i*YY, i*Z single strings
   {

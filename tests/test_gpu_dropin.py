@@ -52,3 +52,14 @@ def test_dropin_project_residual_and_errors(demo):
     pr = demo["project_residual"]
     assert pr["coeff"] == [1.0, 0.0] and pr["residual_err"] < 1e-14
     assert demo["capacity_error"] is True
+
+
+def test_dropin_matrix_inversion(demo, ref):
+    from paper_2506_01120_b200 import workloads as w
+    cfg = w.config0()
+    theirs = ref.closure_dense(cfg.generators, cfg.d, method="matrix-inversion", tol=cfg.tol)
+    r = demo["c0_matrix-inversion"]
+    assert r["dimension"] == theirs.dimension == 9
+    assert r["commutators_evaluated"] == theirs.stats["commutators_evaluated"]
+    assert r["independence_checks"] == theirs.stats["independence_checks"]
+    assert r["gram_size"] == 9 and r["inverse_error"] < 1e-10
