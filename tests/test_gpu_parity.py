@@ -332,3 +332,23 @@ def test_tiny_kernel_hands_over_to_batched_engine(ref, port, keep):
     assert np.array_equal(res.decision_log["independent"], o.log["independent"])
     assert np.array_equal(res.decision_log["null_cand"], o.log["null_cand"])
     assert rel_err(res.basis_array, o.basis) < BASIS_RTOL
+
+
+@pytest.mark.parametrize("n", [6])
+def test_sparse_hea_paper_table(port, n):
+    """PAPER.md §4.2 sparse-Pauli HEA (n = 6: dimension 4095 = 4^n - 1): the
+    single-string path, bit-exact against the oracle (8.4M brackets)."""
+    xs = [1 << i for i in range(n)] + [0] * n + [0] * (n - 1)
+    zs = [0] * n + [1 << i for i in range(n)] + [(1 << i) | (1 << (i + 1)) for i in range(n - 1)]
+    coef = np.tile([1.0, 0.0], (3 * n - 1, 1))
+    x, z = np.array(xs, np.uint64), np.array(zs, np.uint64)
+    res = liecl.closure_pauli_arrays(x, z, coef, n, liecl.Method.orthonorm_dimonly,
+                                     liecl.ClosureConfig(tolerance=1e-10))
+    o = port.closure_pauli_single(x, z, coef, n, tol=1e-10, log_cap=1)
+    dim = 4 ** n - 1
+    assert res.dimension == o.dimension == dim
+    assert res.stats.commutators_evaluated == o.stats["commutators_evaluated"] == dim * (dim - 1) // 2
+    assert res.stats.independence_checks == o.stats["independence_checks"]
+    bx, bz, bc = res.basis_array
+    assert np.array_equal(bx, o.basis[0]) and np.array_equal(bz, o.basis[1])
+    assert np.array_equal(bc.view(np.uint64), o.basis[2].view(np.uint64))
