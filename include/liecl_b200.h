@@ -179,6 +179,15 @@ int liecl_b200_inner_product_dense(liecl_b200_ctx* ctx, const double* a, const d
                                    double* out_re_im);
 int liecl_b200_norm_dense(liecl_b200_ctx* ctx, const double* a, int32_t d, double* out);
 
+/* from_pauli (R:include/liecl/dense.hpp:35-40, R:src/dense.cpp:70-98) on the
+ * device, bit-exact: `count` Pauli sums given as terms [offsets[c],
+ * offsets[c+1]) of (x, z, coef re/im), each sum's terms sorted by (z, x) as a
+ * PauliSum keeps them; out = count d x d matrices (host, or device memory when
+ * out_on_device). qubits <= 12 (the reference's expansion limit). */
+int liecl_b200_from_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x, const uint64_t* z,
+                          const double* coef, int32_t count, uint32_t qubits, double* out,
+                          int32_t out_on_device);
+
 /*
  * Closure sessions: a device-resident orthonormal basis plus the cursor
  * loop, for windows of the closure (benchmarks, sharded runs) and for

@@ -254,6 +254,21 @@ class Ref:
                                                       C.byref(rz), _p(ph), C.byref(e), C.byref(com)))
         return (rx.value, rz.value), complex(ph[0], ph[1]), e.value, bool(com.value)
 
+    def format_pauli(self, x, z, coef, qubits):
+        x = np.ascontiguousarray(x, np.uint64)
+        z = np.ascontiguousarray(z, np.uint64)
+        coef = np.ascontiguousarray(coef, np.float64).reshape(-1, 2)
+        buf = C.create_string_buffer(1 << 20)
+        self._check(self.lib.liecl_ref_format_pauli(_p(x, U64P), _p(z, U64P), _p(coef), C.c_int64(len(x)),
+                                                    C.c_uint(qubits), buf, C.c_int64(len(buf))))
+        return buf.value.decode()
+
+    def format_dense(self, a, d):
+        buf = C.create_string_buffer(1 << 22)
+        self._check(self.lib.liecl_ref_format_dense(_p(_c128(a).view(np.float64)), C.c_int(d), buf,
+                                                    C.c_int64(len(buf))))
+        return buf.value.decode()
+
     def build_generators(self, family, qubits, seed=0, delta=1.5):
         cap = 4096
         oo = np.zeros(64, np.int64)

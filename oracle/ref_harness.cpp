@@ -575,4 +575,14 @@ int liecl_ref_format_pauli(const std::uint64_t* x, const std::uint64_t* z, const
   });
 }
 
+/// format_operator of a dense operator (R:src/operator.cpp:206-226).
+int liecl_ref_format_dense(const double* a, int d, char* buf, std::int64_t len) {
+  return guarded([&] {
+    const std::string s = liecl::format_operator(dense_from(a, d));
+    const std::size_t n = std::min<std::size_t>(s.size(), static_cast<std::size_t>(len - 1));
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  });
+}
+
 } // extern "C"

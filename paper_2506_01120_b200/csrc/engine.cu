@@ -1030,6 +1030,46 @@ int liecl_b200_commutator_dense(liecl_b200_ctx* ctx, const double* a, const doub
   });
 }
 
+int liecl_b200_from_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x, const uint64_t* z,
+                          const double* coef, int32_t count, uint32_t qubits, double* out, int32_t out_on_device) {
+  return guarded([&] {
+    if (!ctx || !offsets || !out || (offsets[count] > 0 && (!x || !z || !coef)))
+      throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (qubits < 1) throw Error(LIECL_B200_INVALID_INPUT, "from_pauli: qubit count must be >= 1");
+    if (qubits > 12)  // kDefaultExpansionLimit (R:include/liecl/dense.hpp:35-36)
+      throw Error(LIECL_B200_CAPACITY, "from_pauli: " + std::to_string(qubits) +
+                                           " qubits exceeds the expansion limit of 12");
+    use_device(ctx);
+    const int64_t terms = offsets[count];
+    const int64_t d = int64_t(1) << qubits, D = d * d;
+    DevBuf<int64_t> doff;
+    DevBuf<uint64_t> dx, dz;
+    DevBuf<double2> dc, dout;
+    doff.ensure(count + 1);
+    dx.ensure(std::max<int64_t>(terms, 1));
+    dz.ensure(std::max<int64_t>(terms, 1));
+    dc.ensure(std::max<int64_t>(terms, 1));
+    CU(cudaMemcpyAsync(doff.p, offsets, (count + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (terms > 0) {
+      CU(cudaMemcpyAsync(dx.p, x, terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(dz.p, z, terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(dc.p, coef, terms * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    double2* dst = reinterpret_cast<double2*>(out);
+    if (!out_on_device) {
+      dout.ensure(static_cast<size_t>(std::max<int64_t>(count * D, 1)));
+      dst = dout.p;
+    }
+    from_pauli_kernel<<<static_cast<unsigned>(std::min<int64_t>((count * d + 127) / 128, 4096)), 128, 0,
+                        ctx->stream>>>(doff.p, dx.p, dz.p, dc.p, count, static_cast<int>(qubits), dst);
+    launched(ctx);
+    if (!out_on_device)
+      CU(cudaMemcpyAsync(out, dout.p, static_cast<size_t>(count * D) * sizeof(double2), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int liecl_b200_inner_product_dense(liecl_b200_ctx* ctx, const double* a, const double* b, int32_t d,
                                    double* out_re_im) {
   return guarded([&] {

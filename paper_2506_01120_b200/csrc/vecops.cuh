@@ -28,6 +28,39 @@ __global__ void gather_columns_kernel(const double2* __restrict__ src, const int
     o[e] = s[e];
 }
 
+// from_pauli (R:src/dense.cpp:70-98) on the device, bit-exact: one thread per
+// column s of each operator; terms (already sorted by (z, x) as PauliSum keeps
+// them) are added in order with the reference's exact phase moves, so every
+// entry accumulates the same values in the same order.
+__device__ __forceinline__ uint64_t reverse_low_bits_dev(uint64_t v, int n) {
+  return __brevll(v) >> (64 - n);
+}
+__global__ void from_pauli_kernel(const int64_t* __restrict__ offsets, const uint64_t* __restrict__ x,
+                                  const uint64_t* __restrict__ z, const double2* __restrict__ coef, int count,
+                                  int qubits, double2* __restrict__ out) {
+  const int64_t d = int64_t(1) << qubits;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < count * d;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = idx / d;
+    const uint64_t s = static_cast<uint64_t>(idx % d);
+    double2* col = out + c * d * d + static_cast<int64_t>(s) * d;
+    for (int64_t r = 0; r < d; ++r) col[r] = make_double2(0.0, 0.0);
+    for (int64_t t = offsets[c]; t < offsets[c + 1]; ++t) {
+      const uint64_t xi = reverse_low_bits_dev(x[t], qubits), zi = reverse_low_bits_dev(z[t], qubits);
+      double2 v = coef[t];
+      switch (__popcll(x[t] & z[t]) & 3) {  // Hermitian phase i^{#Y}
+      case 1: v = make_double2(-v.y, v.x); break;
+      case 2: v = make_double2(-v.x, -v.y); break;
+      case 3: v = make_double2(v.y, -v.x); break;
+      default: break;
+      }
+      if (__popcll(zi & s) & 1) v = make_double2(-v.x, -v.y);
+      double2& e = col[s ^ xi];
+      e = make_double2(__dadd_rn(e.x, v.x), __dadd_rn(e.y, v.y));
+    }
+  }
+}
+
 // dst[j] = src[idx[j]] for columns of W doubles (either field).
 __global__ void gather_words_kernel(const double* __restrict__ src, const int* __restrict__ idx, int64_t W,
                                     double* __restrict__ dst) {

@@ -386,6 +386,96 @@ def close_orthonormalization(generators, config: ClosureConfig | None = None, ke
     return run_closure(generators, Method.orthonorm if keep_original else Method.orthonorm_dimonly, config, device)
 
 
+# ------------------------------------------------- I/O plumbing (§8 f3) ----
+
+
+def pauli_sum_from_terms(qubits: int, terms) -> PauliSum:
+    """PauliSum::from_terms (R:src/pauli.cpp:78-115): merge duplicate strings
+    in input order, drop |c| <= 1e-14 * max|c|, sort by (z, x)."""
+    acc: dict = {}
+    for s, c in terms:
+        if s.qubits != qubits:
+            raise InvalidInputError("PauliSum::from_terms: term qubit count mismatch")
+        key = (s.z, s.x)
+        a = acc.get(key, complex(0.0, 0.0))
+        acc[key] = complex(a.real + complex(c).real, a.imag + complex(c).imag)
+    floor = 1e-14 * max((abs(c) for c in acc.values()), default=0.0)
+    keys = sorted(k for k, c in acc.items() if abs(c) > floor)
+    return PauliSum(qubits, [(PauliString(k[1], k[0], qubits), acc[k]) for k in keys])
+
+
+def from_pauli(sums, device: int = 0):
+    """Dense expansion on the GPU, bit-exact with R:src/dense.cpp:70-98. Takes
+    one PauliSum or a list (terms in PauliSum order); returns DenseOperator(s)."""
+    single = isinstance(sums, PauliSum)
+    sums = [sums] if single else list(sums)
+    if not sums:
+        return []
+    n = sums[0].qubits
+    offsets = np.zeros(len(sums) + 1, np.int64)
+    xs, zs, cs = [], [], []
+    for i, s in enumerate(sums):
+        if s.qubits != n:
+            raise InvalidInputError("from_pauli: mixed qubit counts")
+        for st, c in s.terms:
+            xs.append(st.x); zs.append(st.z); cs.append((complex(c).real, complex(c).imag))
+        offsets[i + 1] = len(xs)
+    x = np.array(xs or [0], np.uint64)
+    z = np.array(zs or [0], np.uint64)
+    c = np.array(cs or [(0.0, 0.0)], np.float64)
+    d = 1 << n
+    out = np.zeros((len(sums), d * d), np.complex128)
+    u64 = C.POINTER(C.c_uint64)
+    _check(native.load().liecl_b200_from_pauli(
+        native.context(device), offsets.ctypes.data_as(C.POINTER(C.c_int64)), x.ctypes.data_as(u64),
+        z.ctypes.data_as(u64), _dp(c), C.c_int32(len(sums)), C.c_uint32(n), _dp(out.view(np.float64)), C.c_int32(0)))
+    ops = [DenseOperator.from_vec(v, d) for v in out]
+    return ops[0] if single else ops
+
+
+def _fmt_real(v: float) -> str:
+    return "%.17g" % v
+
+
+def format_pauli_sum(s: PauliSum) -> str:
+    """R:src/pauli.cpp:397-422."""
+    if not s.terms:
+        return "0 " + "I" * s.qubits
+    out = []
+    for k, (st, c) in enumerate(s.terms):
+        c = complex(c)
+        if c.imag == 0.0:
+            re = c.real
+            if k:
+                out.append(" - " if re < 0.0 else " + ")
+                re = abs(re)
+            out.append(_fmt_real(re))
+        else:
+            if k:
+                out.append(" + ")
+            out.append("(" + _fmt_real(c.real) + "," + _fmt_real(c.imag) + ")")
+        out.append(" " + st.str())
+    return "".join(out)
+
+
+def format_operator(op) -> str:
+    """R:src/operator.cpp:206-226: Pauli text, or full-precision row-major dense entries."""
+    if op is None:
+        return "null"
+    if isinstance(op, PauliSum):
+        return format_pauli_sum(op)
+    m = op.matrix
+    rows = []
+    for r in range(m.shape[0]):
+        rows.append(" ".join("(%.17g,%.17g)" % (m[r, c].real, m[r, c].imag) for c in range(m.shape[1])) + "\n")
+    return "".join(rows)
+
+
+def basis_listing(result: ClosureResult) -> str:
+    """R:src/closure.cpp:566-573."""
+    return "".join(format_operator(op) + "\n" for op in result.basis)
+
+
 # ------------------------------------------------------------ primitives ----
 
 

@@ -1,0 +1,73 @@
+"""input expansion and result listings.
+
+CPU: the Python mirror's from_terms / format_pauli_sum / format_operator
+against the reference build. GPU: the device from_pauli, bit for bit."""
+import numpy as np
+import pytest
+
+from paper_2506_01120_b200 import liecl
+from paper_2506_01120_b200 import workloads as w
+
+
+def random_sum(rng, n, k):
+    terms = []
+    for _ in range(k):
+        s = liecl.PauliString(int(rng.integers(0, 1 << n)), int(rng.integers(0, 1 << n)), n)
+        c = complex(rng.standard_normal(), rng.standard_normal() if rng.random() < 0.5 else 0.0)
+        terms.append((s, c))
+    return liecl.pauli_sum_from_terms(n, terms)
+
+
+def arrays(s):
+    x = np.array([t[0].x for t in s.terms], np.uint64)
+    z = np.array([t[0].z for t in s.terms], np.uint64)
+    c = np.array([[complex(t[1]).real, complex(t[1]).imag] for t in s.terms]).reshape(-1, 2)
+    return x, z, c
+
+
+def test_from_terms_matches_workload_recipe():
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        n = int(rng.integers(1, 5))
+        raw = [((int(rng.integers(0, 1 << n)), int(rng.integers(0, 1 << n))), complex(*rng.standard_normal(2)))
+               for _ in range(int(rng.integers(1, 8)))]
+        a = liecl.pauli_sum_from_terms(n, [(liecl.PauliString(x, z, n), c) for (x, z), c in raw])
+        b = w.PauliSumSpec.from_terms(n, raw)
+        assert [(t[0].x, t[0].z) for t in a.terms] == list(zip(b.x, b.z))
+        assert [t[1] for t in a.terms] == b.coef
+
+
+def test_format_pauli_sum_matches_reference(ref):
+    rng = np.random.default_rng(2)
+    for _ in range(30):
+        n = int(rng.integers(1, 6))
+        s = random_sum(rng, n, int(rng.integers(1, 6)))
+        x, z, c = arrays(s)
+        assert liecl.format_pauli_sum(s) == ref.format_pauli(x, z, c, n)
+    assert liecl.format_pauli_sum(liecl.PauliSum(3, [])) == "0 III"
+
+
+def test_format_dense_matches_reference(ref):
+    cfg = w.config0()
+    for g in cfg.generators:
+        op = liecl.DenseOperator.from_vec(g, cfg.d)
+        assert liecl.format_operator(op) == ref.format_dense(g, cfg.d)
+
+
+@pytest.mark.gpu
+def test_device_from_pauli_bit_exact(ref):
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 3, 5, 6):
+        sums = [random_sum(rng, n, int(rng.integers(1, 9))) for _ in range(4)]
+        dense = liecl.from_pauli(sums)
+        for s, op in zip(sums, dense):
+            x, z, c = arrays(s)
+            assert np.array_equal(op.vec().view(np.uint64), ref.from_pauli(x, z, c, n).view(np.uint64))
+    # the BASELINE generators: same bytes as the host recipe
+    for cfg in (w.config0(), w.config1(), w.config2()):
+        sums = [liecl.PauliSum(s.qubits, [(liecl.PauliString(x, z, s.qubits), c) for x, z, c in zip(s.x, s.z, s.coef)])
+                for s in cfg.sums]
+        got = np.stack([op.vec() for op in liecl.from_pauli(sums)])
+        assert np.array_equal(got.view(np.uint64), cfg.generators.view(np.uint64))
+    with pytest.raises(liecl.CapacityError):
+        liecl.from_pauli(liecl.PauliSum(13, [(liecl.PauliString(1, 0, 13), 1.0)]))
