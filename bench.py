@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=["c2", "c3"], default="c2",
                     help="c2: saturated config-2 closure window (headline); c3: config-3 independence check")
+    ap.add_argument("--c3-mode", choices=["auto", "sharded", "replicas"], default="auto",
+                    help="c3: one instance D-sharded over the ranks (auto: when N>1; 'sharded' also at N=1, "
+                         "through a one-rank NCCL communicator), or one instance per rank")
     ap.add_argument("--rows-per-step", type=int, default=8)
     ap.add_argument("--row0", type=int, default=1024)
     ap.add_argument("--cpu-pairs", type=int, default=1024, help="bracket sample for the CPU baseline")
@@ -461,32 +464,67 @@ def run_c3(a):
     """Config 3: ordered independence check of 4096 candidates against a
     16384 x 65536 complex orthonormal basis (BASELINE configs[3]); one step =
     the whole candidate stream (normalise, CGS2 check, append the ~2048
-    independent ones), basis reset between steps (untimed)."""
+    independent ones), basis reset between steps (untimed).
+
+    N > 1 (torchrun): "sharded across GPUs" as BASELINE names it -- one c3
+    instance D-sharded over the ranks (ShardedCheck: each rank holds 65536/N
+    elements of every vector; beta and squared norms summed over ranks with
+    NCCL inside the engine), strong scaling. --c3-mode replicas runs one
+    independent instance per rank instead (weak scaling)."""
     import torch
     from paper_2506_01120_b200 import liecl, native, workloads as w
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    torchrun = "RANK" in os.environ
+    dist = None
+    if torchrun:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    sharded = a.c3_mode == "sharded" or (a.c3_mode == "auto" and world > 1)
     stream = torch.cuda.current_stream(device)
     native.set_stream(stream.cuda_stream, device=local)
-    c3 = w.Config3(seed=rank)
+    c3 = w.Config3(seed=0 if sharded else rank)
     t0 = time.perf_counter()
     V, cands = c3.generate(torch, device)
     torch.cuda.synchronize(device)
     gen_s = time.perf_counter() - t0
-    sess = liecl.ClosureSession(c3.d, config=liecl.ClosureConfig(tolerance=c3.tol, max_dim=c3.n + c3.ncand),
-                                device=local)
+    cfg = liecl.ClosureConfig(tolerance=c3.tol, max_dim=c3.n + c3.ncand)
+    Vfull_host = V.cpu().numpy() if (rank == 0 and not a.no_cpu_baseline) else None
+    cands_head = cands[:64].cpu().numpy() if (rank == 0 and not a.no_cpu_baseline) else None
+    if sharded:
+        from paper_2506_01120_b200.distributed import ShardedCheck, TorchComm
+        sc = ShardedCheck(c3.d, config=cfg, comm=TorchComm(device=device) if dist is not None else None,
+                          device=local)
+        V = V[:, sc.lo:sc.hi].contiguous()  # this rank's slice of every vector; the full copies go
+        cands = cands[:, sc.lo:sc.hi].contiguous()
+        torch.cuda.empty_cache()
+        sess = sc.session
+    else:
+        sess = liecl.ClosureSession(c3.d, config=cfg, device=local)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     def step():
         sess.set_basis(V.data_ptr(), on_device=True, n=c3.n)  # reset (untimed)
-        torch.cuda.synchronize(device)
+        barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ind, rn, st = sess.check_candidates(cands.data_ptr(), on_device=True, n=c3.ncand)
         e1.record(stream)
         torch.cuda.synchronize(device)
-        return e0.elapsed_time(e1), ind, rn
+        return max_over_ranks(e0.elapsed_time(e1)), ind, rn
     for _ in range(a.warmup):
         step()
     native.kernel_times(local)
@@ -507,28 +545,33 @@ def run_c3(a):
     gms = kt["zgemm_project"]["ms"] + kt["zgemm_subtract"]["ms"]
     gfl = kt["zgemm_project"]["flops"] + kt["zgemm_subtract"]["flops"]
     cpu = None
-    if not a.no_cpu_baseline:
-        Vh = V.cpu().numpy()
-        ch = cands[: 64].cpu().numpy()
+    if rank == 0 and not a.no_cpu_baseline:
         threads = os.cpu_count() or 1
         from oracle.oracle import REF_SO, Port, Ref
         if os.path.exists(REF_SO):
-            ind_c, _, secs = Ref().check_sequence_dense(Vh, ch, c3.d, tol=c3.tol, append=False, threads=threads)
+            ind_c, _, secs = Ref().check_sequence_dense(Vfull_host, cands_head, c3.d, tol=c3.tol, append=False,
+                                                        threads=threads)
             kind = "reference"
         else:
             t1 = time.perf_counter()
-            ind_c, _, _ = Port().check_sequence_dense(Vh, ch, c3.d, tol=c3.tol, append=False, threads=threads)
+            ind_c, _, _ = Port().check_sequence_dense(Vfull_host, cands_head, c3.d, tol=c3.tol, append=False,
+                                                      threads=threads)
             secs, kind = time.perf_counter() - t1, "port"
         cpu = {"value": 64 / secs, "unit": "candidates/s", "cores": threads, "kind": kind,
                "sample": f"64 candidates (32 Gaussian + 32 combinations) checked against the same 16384-vector "
                          f"basis bytes, fixed basis ({secs:.1f} s); verdicts agree: "
                          f"{bool((ind_c == ind[:64]).all())}"}
-    line = {"metric": "candidates_checked_per_s", "value": c3.ncand * world / (ms / 1e3), "unit": "candidates/s",
+    units = c3.ncand if sharded else c3.ncand * world
+    line = {"metric": "candidates_checked_per_s", "value": units / (ms / 1e3), "unit": "candidates/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded torch Philox)",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded torch Philox)",
             "config": {"workload": "c3_independence_check", "N": c3.n, "D": c3.D, "candidates": c3.ncand,
                        "noise_sigma": c3.noise, "tol": c3.tol, "generate_s": round(gen_s, 1),
-                       "accepted": accepted, "gaussians_accepted_combinations_rejected": bool(even)},
+                       "accepted": accepted, "gaussians_accepted_combinations_rejected": bool(even),
+                       "parallelism": (f"D-sharded x{world} (NCCL all-reduce of beta and squared norms)" if sharded
+                                       else f"replicas x{world}"),
+                       "l2": "inputs larger than L2 (basis 17 GB / N per rank)"},
             "roofline": {"bound": "tensor", "kernel": "zgemm_dmma (K2a + K2b)", "achieved": gfl / (gms / 1e3) / 1e12,
                          "peak": peak, "unit": "TFLOP/s", "frac": gfl / (gms / 1e3) / 1e12 / peak,
                          "share_of_step": gms / sum(times), "traffic": None,
@@ -546,7 +589,7 @@ def main():
         run_c3(a)
     else:
         run_b200_arm(a)
-    if "RANK" in os.environ and a.impl == "b200":
+    if "RANK" in os.environ:
         import torch.distributed as dist
         if dist.is_initialized():
             dist.destroy_process_group()

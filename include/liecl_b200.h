@@ -231,6 +231,29 @@ int liecl_b200_session_check_candidates(liecl_b200_session* s, const double* can
                                         int32_t on_device, int32_t* independent, double* residual_norms,
                                         liecl_b200_stats* stats);
 
+/*
+ * D-sharded sessions (BASELINE configs[3] "sharded across GPUs"; the north
+ * star's "basis rows sharded per GPU, partial overlap sums all-reduced").
+ * Rank r of P holds elements [lo, hi) = liecl_b200_shard_range(d, P, r) of
+ * every operator (vec layout) and passes only that slice to set_basis /
+ * check_candidates / get_vectors. The overlaps beta = V^H C / d and the
+ * squared residual norms are the only cross-rank data: each is summed in
+ * place over ranks
+ *   - through NCCL when nccl_id (NCCL_UNIQUE_ID_BYTES = 128 bytes, made once
+ *     by liecl_b200_nccl_unique_id and shared by the caller) is given; every
+ *     rank calls set_shards concurrently, one rank per GPU;
+ *   - else through `reduce`, a host callback that must replace values[0:count]
+ *     by their sum over ranks, with identical bits on every rank, and return 0.
+ * Every rank then reaches the same verdicts. Candidate checking only
+ * (run_pairs / screen_pairs need whole operators for the commutator and
+ * refuse). Call on a fresh session, before set_basis.
+ */
+typedef int (*liecl_b200_reduce_fn)(double* values, int64_t count, void* user);
+int liecl_b200_nccl_unique_id(uint8_t* id_out);
+int liecl_b200_shard_range(int32_t d, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi);
+int liecl_b200_session_set_shards(liecl_b200_session* s, int32_t nranks, int32_t rank, const uint8_t* nccl_id,
+                                  liecl_b200_reduce_fn reduce, void* user);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,25 @@ public:
     reset_stats();
   }
 
+  // D-sharding (shard.cuh): from now on this engine holds elements [lo, hi)
+  // of every vector; overlaps and squared norms are summed over ranks by
+  // `red`. General complex field only (the packed weights and the
+  // commutator need whole operators). Batch sizes stay those of the full D
+  // so every rank issues the same reductions.
+  void set_shards(int nranks, int rank, std::unique_ptr<Reducer> red) {
+    if (n_o_ != 0 || field_ != Field::kUnset || vcap_ != 0 || red_)
+      throw Error(LIECL_B200_INVALID_INPUT, "set_shards needs a fresh session (before set_basis / check_candidates)");
+    const int64_t Dfull = static_cast<int64_t>(d_) * d_;
+    if (nranks < 1 || rank < 0 || rank >= nranks || nranks > Dfull)
+      throw Error(LIECL_B200_INVALID_INPUT, "bad shard rank / count");
+    int64_t lo, hi;
+    shard_range(Dfull, nranks, rank, lo, hi);
+    D_ = hi - lo;
+    red_ = std::move(red);
+    force_complex_ = true;
+  }
+  bool sharded() const { return static_cast<bool>(red_); }
+
   // ---- state / results ----------------------------------------------------
   Field field() const { return field_; }
   int64_t ortho_size() const { return n_o_; }
@@ -186,8 +205,9 @@ public:
         scale_columns_ah_kernel<<<g2, 256, 0, ctx_->stream>>>(R_.p, hn_.p, tol_, D_, C_.p);
         launched(ctx_);
       } else {
-        column_norm_kernel<<<cnt, 256, 0, ctx_->stream>>>(stage_.p, D_, sqrt_d_, hn_.p);
+        column_norm_kernel<<<cnt, 256, 0, ctx_->stream>>>(stage_.p, D_, red_ ? 0.0 : sqrt_d_, hn_.p);
         launched(ctx_);
+        if (red_) sharded_norms(hn_.p, cnt);
         dim3 g2(static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 64)), cnt);
         scale_columns_kernel<<<g2, 256, 0, ctx_->stream>>>(stage_.p, hn_.p, tol_, D_, cplx(C_.p));
         launched(ctx_);
@@ -206,6 +226,7 @@ public:
   // cursor pairs [g_begin, g_end), all with l < basis size at batch start (the
   // reference's row loop re-reads |basis| every row)
   void run_pairs(int64_t g_begin, int64_t g_end) {
+    whole_operators("run_pairs");
     int64_t g = g_begin;
     while (g < g_end) {
       const int64_t nb = basis_size();
@@ -226,6 +247,7 @@ public:
   // certified reject iff it is not null and rn1 <= tol/20 (see apply()). The
   // basis and the counters are left untouched (multi-GPU screening).
   void screen_pairs(int64_t g_begin, int64_t g_end, int32_t* null_out, double* rn_out) {
+    whole_operators("screen_pairs");
     const int64_t nb = basis_size();
     if (g_end > nb * (nb - 1) / 2 || g_begin < 0 || g_end < g_begin)
       throw Error(LIECL_B200_INVALID_INPUT, "screen range refers to basis elements that do not exist yet");
@@ -246,6 +268,7 @@ public:
 
   // the whole closure after the generator loop: all pairs until exhausted
   void run_closure_pairs(int64_t g = 0) {
+    whole_operators("the closure loop");
     for (;;) {
       const int64_t nb = basis_size();
       const int64_t avail = nb * (nb - 1) / 2;
@@ -280,6 +303,7 @@ public:
 
   // single-vector project_residual for the drop-in API (general complex field)
   void project_residual(const double2* h_host, double* r_host, double* coeffs_host) {
+    whole_operators("project_residual");
     if (field_ == Field::kUnset) {
       field_ = Field::kComplex;
       layout_slabs();
@@ -316,6 +340,17 @@ private:
   void check_deadline() {
     if (has_deadline_ && Clock::now() > deadline_)
       throw Error(LIECL_B200_TIMEOUT, "closure computation exceeded its deadline");
+  }
+  void whole_operators(const char* what) const {
+    if (red_)
+      throw Error(LIECL_B200_INVALID_INPUT,
+                  std::string(what) + " needs whole operators; a D-sharded session only checks candidates");
+  }
+  // squared-norm partials -> over ranks -> sqrt(.)/sqrt(d), in place
+  void sharded_norms(double* v, int count) {
+    red_->sum(v, count, ctx_->stream);
+    norm_finalize_kernel<<<(count + 255) / 256, 256, 0, ctx_->stream>>>(v, 1, count, sqrt_d_, v);
+    launched(ctx_);
   }
 
   // field of a batch of complex operators (exact anti-Hermitian test on device)
@@ -440,11 +475,15 @@ private:
       mtiles = static_cast<int>((D_ + rg::BM - 1) / rg::BM);
     } else {
       gemm_project(ctx_, cplx(Vb), n, D_, cplx(X), count, cplx(P_.p), 1.0 / d_);
+      // D-shard: this rank's beta is a partial sum over its slice
+      if (red_ && n > 0) red_->sum(P_.p, 2 * n * count, ctx_->stream);
       gemm_subtract(ctx_, cplx(Vb), n, D_, cplx(P_.p), cplx(X), count, cplx(Rout), partial_.p);
       mtiles = static_cast<int>((D_ + zg::BM - 1) / zg::BM);
     }
-    norm_finalize_kernel<<<(count + 255) / 256, 256, 0, ctx_->stream>>>(partial_.p, mtiles, count, sqrt_d_, rn);
+    norm_finalize_kernel<<<(count + 255) / 256, 256, 0, ctx_->stream>>>(partial_.p, mtiles, count,
+                                                                       red_ ? 0.0 : sqrt_d_, rn);
     launched(ctx_);
+    if (red_) sharded_norms(rn, count);
   }
 
   void launch_commutators(int64_t g0, int cnt) {
@@ -670,6 +709,7 @@ private:
   double tol_;
   bool record_;
   bool force_complex_;
+  std::unique_ptr<Reducer> red_;  // set: D-sharded (D_ is this rank's slice)
   Field field_ = Field::kUnset;
   Field slab_field_ = Field::kUnset;  // layout the basis slabs are allocated for
   DevBuf<double2> unpack_;            // packed -> complex output staging

@@ -442,6 +442,7 @@ void launch_commutator_complex(liecl_b200_ctx* ctx, const double2* basis, int d,
   }
 }
 
+#include "shard.cuh"
 #include "dense_engine.cuh"
 #include "gram_engine.cuh"
 
@@ -1214,6 +1215,37 @@ int liecl_b200_session_check_candidates(liecl_b200_session* s, const double* can
       *stats = s->eng->stats();
       stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
     }
+  });
+}
+
+int liecl_b200_nccl_unique_id(uint8_t* id_out) {
+  return guarded([&] {
+    if (!id_out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    ncclUniqueId id;
+    nccl_check(nccl_api().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, &id, sizeof id);
+  });
+}
+
+int liecl_b200_shard_range(int32_t d, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi) {
+  return guarded([&] {
+    if (!lo || !hi) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    const int64_t D = static_cast<int64_t>(d) * d;
+    if (d < 1 || nranks < 1 || rank < 0 || rank >= nranks || nranks > D)
+      throw Error(LIECL_B200_INVALID_INPUT, "bad shard rank / count");
+    shard_range(D, nranks, rank, *lo, *hi);
+  });
+}
+
+int liecl_b200_session_set_shards(liecl_b200_session* s, int32_t nranks, int32_t rank, const uint8_t* nccl_id,
+                                  liecl_b200_reduce_fn reduce, void* user) {
+  return guarded([&] {
+    if (!s || (!nccl_id && !reduce)) throw Error(LIECL_B200_INVALID_INPUT, "need a session and an NCCL id or a reduce callback");
+    use_device(s->ctx);
+    std::unique_ptr<Reducer> red;
+    if (nccl_id) red = std::make_unique<NcclReducer>(nccl_id, nranks, rank);
+    else red = std::make_unique<HostReducer>(reduce, user);
+    s->eng->set_shards(nranks, rank, std::move(red));
   });
 }
 

@@ -8,13 +8,14 @@ namespace liecl_b200 {
 
 // rn[b] = sqrt(sum_mt partial[mt*N + b]) / sqrt(d)   (dense_norm, R:src/dense.cpp:61-63)
 // Summation over M tiles in fixed order: deterministic across runs.
-__global__ void norm_finalize_kernel(const double* __restrict__ partial, int mtiles, int N, double sqrt_d,
-                                     double* __restrict__ rn) {
+// sqrt_d <= 0 stores the raw sum (a D-shard's partial, summed over ranks
+// before the square root). rn may alias partial when mtiles == 1.
+__global__ void norm_finalize_kernel(const double* partial, int mtiles, int N, double sqrt_d, double* rn) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= N) return;
   double s = 0.0;
   for (int mt = 0; mt < mtiles; ++mt) s += partial[static_cast<int64_t>(mt) * N + b];
-  rn[b] = sqrt(s) / sqrt_d;
+  rn[b] = sqrt_d > 0.0 ? sqrt(s) / sqrt_d : s;
 }
 
 // dst[j] = src[idx[j]] for D-element complex columns.
@@ -101,7 +102,7 @@ __global__ void column_norm_kernel(const double2* __restrict__ x, int64_t D, dou
   if (threadIdx.x < 32) {
     double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
     v = warp_sum(v);
-    if (threadIdx.x == 0) out[blockIdx.x] = sqrt(v) / sqrt_d;
+    if (threadIdx.x == 0) out[blockIdx.x] = sqrt_d > 0.0 ? sqrt(v) / sqrt_d : v;  // <= 0: raw sum
   }
 }
 

@@ -22,6 +22,15 @@ Verdicts, statistics and the final basis therefore equal the single-GPU run,
 whatever the rank count. The collective is one 8-byte all-reduce per batch
 (plus an all-gather of the per-pair verdict data when a decision log is
 requested).
+
+Config 3 (an independence check over a fixed basis, no commutators) is
+sharded the other way, `ShardedCheck`: along D. Each rank holds a contiguous
+slice of every vector (16384 x 65536 complex: 17 GB, 2.1 GB per rank at 8),
+the projection GEMMs yield partial overlaps, and the engine sums beta and the
+squared residual norms over ranks in place through NCCL (one all-reduce of
+16 n B bytes per pass over a batch of B candidates against n vectors), so
+every rank takes the same verdicts and appends its slice of the same vectors.
+The closure loop cannot shard this way: a commutator needs whole operators.
 """
 from __future__ import annotations
 
@@ -51,6 +60,12 @@ class _Solo:
     def gather_objects(self, obj):
         return [obj]
 
+    def broadcast_bytes(self, data):
+        return data
+
+    def sum_doubles(self, values) -> None:
+        pass
+
 
 class TorchComm:
     """torch.distributed collectives (NCCL on GPUs, gloo on CPU)."""
@@ -71,6 +86,20 @@ class TorchComm:
         out = [None] * self.world
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
+
+    def sum_doubles(self, values) -> None:
+        """In-place sum over ranks of a float64 numpy array (identical bits on
+        every rank); usable as ClosureSession.set_shards(reduce=...) where no
+        NCCL communicator is wanted."""
+        t = self.torch.from_numpy(np.ascontiguousarray(values)).to(self.device or "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        values[:] = t.cpu().numpy()
+
+    def broadcast_bytes(self, data):
+        """rank 0's `data` on every rank"""
+        box = [data if self.rank == 0 else None]
+        self.dist.broadcast_object_list(box, src=0, group=self.group)
+        return box[0]
 
 
 @dataclass
@@ -163,3 +192,53 @@ class DistributedClosure:
             cnt = min(self.batch, avail - g)
             self._adapt(self._batch(g, cnt), cnt)
             g += cnt
+
+
+def shard_bounds(d: int, world: int, rank: int) -> tuple[int, int]:
+    """Elements [lo, hi) of a d*d operator held by D-shard `rank` (the engine's
+    shard_range, csrc/shard.cuh): floor(D r / P) .. floor(D (r+1) / P)."""
+    D = d * d
+    return D * rank // world, D * (rank + 1) // world
+
+
+class ShardedCheck:
+    """Config-3 independence check, D-sharded over the ranks of `comm`.
+
+    Every rank passes the FULL-width basis / candidates (host arrays or torch
+    tensors, (n, d*d)); only the rank's column slice [lo, hi) is handed to the
+    engine. Verdicts and residual norms come back identical on every rank;
+    `basis_slice()` is this rank's slice of the resulting basis.
+    """
+
+    def __init__(self, d: int, config=None, comm=None, device: int = 0, nccl_id: bytes | None = None):
+        from . import liecl
+        self.comm = comm or _Solo()
+        self.d = d
+        self.lo, self.hi = shard_bounds(d, self.comm.world, self.comm.rank)
+        self.session = liecl.ClosureSession(d, config=config, device=device)
+        if nccl_id is None:
+            nccl_id = self.comm.broadcast_bytes(liecl.nccl_unique_id() if self.comm.rank == 0 else None)
+        self.session.set_shards(self.comm.world, self.comm.rank, nccl_id=nccl_id)
+
+    def local(self, X):
+        """This rank's contiguous column slice of full-width rows."""
+        return X[:, self.lo:self.hi]
+
+    def set_basis(self, V):
+        import numpy as _np
+        if isinstance(V, _np.ndarray):
+            self.session.set_basis(_np.ascontiguousarray(self.local(V)))
+        else:  # torch tensor on this rank's device
+            loc = self.local(V).contiguous()
+            self.session.set_basis(loc.data_ptr(), on_device=True, n=loc.shape[0])
+            return loc
+
+    def check_candidates(self, C):
+        import numpy as _np
+        if isinstance(C, _np.ndarray):
+            return self.session.check_candidates(_np.ascontiguousarray(self.local(C)))
+        loc = self.local(C).contiguous()
+        return self.session.check_candidates(loc.data_ptr(), on_device=True, n=loc.shape[0])
+
+    def basis_slice(self):
+        return self.session.basis()

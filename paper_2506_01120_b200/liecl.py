@@ -525,18 +525,63 @@ def norm(a: DenseOperator, device: int = 0) -> float:
 # --------------------------------------------------------------- sessions ---
 
 
+def shard_range(d: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Elements [lo, hi) of a d*d operator held by D-shard `rank` of `nranks`."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(native.load().liecl_b200_shard_range(C.c_int32(d), C.c_int32(nranks), C.c_int32(rank), C.byref(lo),
+                                                 C.byref(hi)))
+    return lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for ClosureSession.set_shards."""
+    buf = (C.c_uint8 * 128)()
+    _check(native.load().liecl_b200_nccl_unique_id(buf))
+    return bytes(buf)
+
+
 class ClosureSession:
     """Device-resident basis + cursor loop (include/liecl_b200.h sessions)."""
 
-    def __init__(self, d: int, keep_original: bool = False, config: ClosureConfig | None = None, device: int = 0):
+    def __init__(self, d: int, keep_original: bool = False, config: ClosureConfig | None = None, device: int = 0,
+                 ctx=None):
         self.d = d
+        self.width = d * d  # elements of each operator this session holds (a slice once D-sharded)
         self.device = device
         self.lib = native.load()
         cfg = (config or ClosureConfig()).native()
         self.ptr = C.c_void_p()
-        _check(self.lib.liecl_b200_session_create_dense(native.context(device), C.c_int32(d),
-                                                        C.c_int32(int(keep_original)), C.byref(cfg),
+        self._reduce = None
+        _check(self.lib.liecl_b200_session_create_dense(ctx if ctx is not None else native.context(device),
+                                                        C.c_int32(d), C.c_int32(int(keep_original)), C.byref(cfg),
                                                         C.byref(self.ptr)))
+
+    def set_shards(self, nranks: int, rank: int, nccl_id: bytes | None = None, reduce=None):
+        """D-shard this (fresh) session: it then holds elements shard_range(d, nranks, rank)
+        of every operator; overlaps and squared norms are summed over ranks through
+        NCCL (`nccl_id` from nccl_unique_id(), shared by the caller) or through
+        `reduce(values: np.ndarray)`, which must replace `values` in place by the
+        sum over ranks with identical bits on every rank."""
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise InvalidInputError("an NCCL unique id is 128 bytes")
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            _check(self.lib.liecl_b200_session_set_shards(self.ptr, C.c_int32(nranks), C.c_int32(rank), buf,
+                                                          native.ReduceFn(), None))
+        elif reduce is not None:
+            def trampoline(values, count, _user):
+                try:
+                    reduce(np.ctypeslib.as_array(values, shape=(count,)))
+                    return 0
+                except Exception:  # reported as a failed reduction by the engine
+                    return 1
+            self._reduce = native.ReduceFn(trampoline)  # keep alive as long as the session
+            _check(self.lib.liecl_b200_session_set_shards(self.ptr, C.c_int32(nranks), C.c_int32(rank), None,
+                                                          self._reduce, None))
+        else:
+            raise InvalidInputError("set_shards needs nccl_id or reduce")
+        lo, hi = shard_range(self.d, nranks, rank)
+        self.width = hi - lo
 
     def close(self):
         if self.ptr:
@@ -591,7 +636,7 @@ class ClosureSession:
 
     def basis(self) -> np.ndarray:
         n = self.size()
-        out = np.zeros((n, self.d * self.d), np.complex128)
+        out = np.zeros((n, self.width), np.complex128)
         _check(self.lib.liecl_b200_session_get_basis(self.ptr, _dp(out.view(np.float64)), C.c_int64(n)))
         return out
 

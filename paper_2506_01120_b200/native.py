@@ -29,7 +29,11 @@ EXPORTED = [
     "liecl_b200_session_get_vectors", "liecl_b200_session_screen_pairs",
     "liecl_b200_session_get_log",
     "liecl_b200_session_check_candidates",
+    "liecl_b200_nccl_unique_id", "liecl_b200_shard_range", "liecl_b200_session_set_shards",
 ]
+
+# int (*liecl_b200_reduce_fn)(double* values, int64_t count, void* user)
+ReduceFn = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_void_p)
 
 
 class NativeUnavailable(RuntimeError):
@@ -98,6 +102,20 @@ def context(device: int = 0) -> C.c_void_p:
                 raise NativeUnavailable(f"liecl_b200_ctx_create(device={device}) failed: {last_error()}")
             _contexts[device] = ctx
         return _contexts[device]
+
+
+def new_context(device: int = 0) -> C.c_void_p:
+    """A private context (own stream and workspaces), e.g. one per thread driving
+    its own session; release with destroy_context."""
+    lib = load()
+    ctx = C.c_void_p()
+    if lib.liecl_b200_ctx_create(C.c_int(device), C.byref(ctx)) != OK:
+        raise NativeUnavailable(f"liecl_b200_ctx_create(device={device}) failed: {last_error()}")
+    return ctx
+
+
+def destroy_context(ctx) -> None:
+    load().liecl_b200_ctx_destroy(ctx)
 
 
 def kernel_count(device: int = 0) -> int:

@@ -81,3 +81,18 @@ def test_pair_index_roundtrip():
             assert pair_from_index(g) == (l, m)
             g += 1
     assert pair_from_index(8382464) == (4094, 4093)
+
+
+def test_shard_range_partitions_every_operator():
+    # liecl_b200_shard_range makes no CUDA call; the host mirror must agree
+    from paper_2506_01120_b200.distributed import shard_bounds
+    for d in (1, 2, 3, 16, 256):
+        for P in range(1, 9):
+            if P > d * d:
+                continue
+            got = [liecl.shard_range(d, P, r) for r in range(P)]
+            assert got == [shard_bounds(d, P, r) for r in range(P)]
+            assert got[0][0] == 0 and got[-1][1] == d * d
+            assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
+    with pytest.raises(liecl.InvalidInputError):
+        liecl.shard_range(2, 5, 0)

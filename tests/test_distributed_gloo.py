@@ -147,3 +147,81 @@ def test_two_ranks_match_single_process(tmp_path, batch_max):
         assert st[2] == ref_stats.accepted
         assert np.array_equal(got["V"], ref_V)  # replicas identical, bit for bit
     assert got["stats"][3] > 0  # some batches were sharded (saturated tail)
+
+
+# ---- D-sharded independence check (ShardedCheck / set_shards protocol) ----
+
+def sharded_check_model(Vloc, Cloc, d, tol, reduce):
+    """numpy model of the engine's D-sharded check: each rank holds column
+    slices; every inner product and squared norm is a partial sum completed by
+    `reduce` (in place, over ranks) -- the only cross-rank data."""
+    V = [v.copy() for v in Vloc]
+    ind, rns = [], []
+
+    def gnorm(x):
+        s = np.array([np.vdot(x, x).real])
+        reduce(s)
+        return np.sqrt(s[0]) / np.sqrt(d)
+
+    def gproject(r):
+        if not V:
+            return r
+        b = (np.array([np.vdot(v, r) for v in V]) / d).view(np.float64).copy()
+        reduce(b)
+        beta = b.view(np.complex128)
+        return r - np.tensordot(beta, np.array(V), axes=1)
+
+    for c in Cloc:
+        hn = gnorm(c)
+        if not hn > tol:
+            ind.append(0)
+            rns.append(0.0)
+            continue
+        r = gproject(gproject(c / hn))
+        rn = gnorm(r)
+        ind.append(int(rn > tol))
+        rns.append(rn)
+        if rn > tol:
+            V.append(r / rn)
+    return np.array(ind), np.array(rns), np.array(V)
+
+
+def _sharded_problem():
+    rng = np.random.default_rng(5)
+    d, n = 4, 5
+    D = d * d
+    Q, _ = np.linalg.qr(rng.standard_normal((D, n)) + 1j * rng.standard_normal((D, n)))
+    V = (Q.T * np.sqrt(d)).astype(np.complex128)
+    C = [rng.standard_normal(D) + 1j * rng.standard_normal(D), (1 - 2j) * V[1] + V[3], np.zeros(D)]
+    C.append(2.0 * C[0] - V[0])  # dependent on an in-stream accept
+    C.append(rng.standard_normal(D) + 0j)
+    return d, V, np.array(C)
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    from paper_2506_01120_b200.distributed import shard_bounds
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    comm = TorchComm()
+    token = comm.broadcast_bytes(bytes(range(128)) if rank == 0 else None)  # the NCCL-id handoff
+    d, V, C = _sharded_problem()
+    lo, hi = shard_bounds(d, world, rank)
+    ind, rn, B = sharded_check_model(V[:, lo:hi], C[:, lo:hi], d, 1e-10, comm.sum_doubles)
+    np.savez(os.path.join(out_dir, f"shard{rank}.npz"), ind=ind, rn=rn, B=B, lo=lo, hi=hi,
+             token=np.frombuffer(token, np.uint8))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_d_shards_match_unsharded(tmp_path):
+    d, V, C = _sharded_problem()
+    ind0, rn0, B0 = sharded_check_model(V, C, d, 1e-10, lambda v: None)
+    assert ind0.tolist() == [1, 0, 0, 0, 1]
+    mp.spawn(_sharded_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    got = [np.load(tmp_path / f"shard{r}.npz") for r in range(2)]
+    for g in got:
+        assert np.array_equal(g["ind"], ind0)
+        assert np.array_equal(g["rn"], got[0]["rn"])  # every rank, same bits
+        np.testing.assert_allclose(g["rn"], rn0, rtol=1e-13, atol=1e-15)
+        np.testing.assert_allclose(g["B"], B0[:, int(g["lo"]):int(g["hi"])], atol=1e-13)
+        assert bytes(g["token"]) == bytes(range(128))
+    assert int(got[0]["hi"]) == int(got[1]["lo"]) and int(got[1]["hi"]) == d * d
