@@ -165,6 +165,29 @@ int liecl_b200_closure_pauli(liecl_b200_ctx* ctx, const uint64_t* x, const uint6
                              liecl_b200_stats* stats, char* warnings, int64_t warnings_len,
                              liecl_b200_decision* log, int64_t log_cap, int64_t* log_len);
 
+/*
+ * run_closure for general (multi-term) Pauli generators, orthonormal methods
+ * (R:src/closure.cpp:541-564 on the Pauli backend, R:src/pauli.cpp:78-228),
+ * bit-exact with the reference: same verdicts, decision log, warnings and
+ * coefficient bits. Generator i = terms [offsets[i], offsets[i+1]) of
+ * (x, z, coef re/im) in PauliSum form (unique strings sorted by (z, x));
+ * qubits <= 31. Outputs result.basis as basis_offsets (dimension + 1 entries,
+ * dimension <= cap) and its terms (term_cap entries), and, when ortho_offsets
+ * != NULL, result.orthonormal_basis likewise. terms_needed[0..1] (basis,
+ * orthonormal) and *stats are always written; LIECL_B200_CAPACITY ("output
+ * buffers too small") when cap / term caps do not suffice -- call again with
+ * the sizes reported.
+ */
+int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                  const uint64_t* z, const double* coef, int32_t ngens, uint32_t qubits,
+                                  int32_t method, const liecl_b200_config* cfg, int64_t cap,
+                                  int64_t* basis_offsets, uint64_t* basis_x, uint64_t* basis_z,
+                                  double* basis_coef, int64_t term_cap, int64_t* ortho_offsets, uint64_t* ortho_x,
+                                  uint64_t* ortho_z, double* ortho_coef, int64_t ortho_term_cap,
+                                  int64_t* terms_needed, liecl_b200_stats* stats, char* warnings,
+                                  int64_t warnings_len, liecl_b200_decision* log, int64_t log_cap,
+                                  int64_t* log_len);
+
 /* project_residual (R:include/liecl/closure.hpp:139-140): residual after two
  * projection passes against the orthonormal tuple V (n operators), plus the
  * first-pass coefficients (n complex). Host buffers. */

@@ -21,6 +21,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libliecl_ref.so")
+# the reference's default-ISA rounding (no FMA contraction in any file), see Makefile
+REF_EXACT_SO = os.path.join(HERE, "_ref", "libliecl_ref_exact.so")
 PORT_SO = os.path.join(HERE, "_build", "liecl_oracle.so")
 REF_SOURCES = "/root/reference/proj/core"
 
@@ -123,7 +125,7 @@ class Ref:
         z = np.ascontiguousarray(z, np.uint64)
         coef = np.ascontiguousarray(coef, np.float64)
         basis_cap = basis_cap or (max_dim or 4 ** qubits)
-        term_cap = term_cap or basis_cap * 4
+        term_cap = term_cap or max(basis_cap * 4, 1 << 20)
         oo = np.zeros(basis_cap + 1, np.int64)
         ox = np.zeros(term_cap, np.uint64)
         oz = np.zeros(term_cap, np.uint64)
@@ -158,13 +160,14 @@ class Ref:
         n = dim.value
         return ClosureOut(n, basis[:n].copy(), ortho[:n].copy(), {}, log[: min(nlog.value, log_cap)].copy())
 
-    def decision_log_pauli(self, offsets, x, z, coef, qubits, keep_original=False, tol=1e-10, threads=1):
+    def decision_log_pauli(self, offsets, x, z, coef, qubits, keep_original=False, tol=1e-10, threads=1,
+                           term_cap=None):
         offsets = np.ascontiguousarray(offsets, np.int64)
         x = np.ascontiguousarray(x, np.uint64)
         z = np.ascontiguousarray(z, np.uint64)
         coef = np.ascontiguousarray(coef, np.float64)
         basis_cap = 4 ** qubits
-        term_cap = basis_cap * 4
+        term_cap = term_cap or max(basis_cap * 4, 1 << 20)
         log_cap = 1 << 22
         log = np.zeros(log_cap, DECISION_DTYPE)
         oo = np.zeros(basis_cap + 1, np.int64)

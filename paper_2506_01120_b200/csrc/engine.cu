@@ -24,6 +24,7 @@
 // The Pauli single-string path (pauli.cuh) is bit-exact and runs frontier
 // batches of all available pairs.
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -42,6 +43,7 @@
 #include "commutator.cuh"
 #include "dgemm_dmma.cuh"
 #include "pauli.cuh"
+#include "pauli_sum.cuh"
 #include "tiny.cuh"
 #include "vecops.cuh"
 #include "zgemm_dmma.cuh"
@@ -806,6 +808,8 @@ void run_gram_closure(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, in
   eng.download_gram(gram_out, inverse_out);
 }
 
+#include "sum_engine.cuh"
+
 } // namespace
 
 struct liecl_b200_session {
@@ -975,6 +979,49 @@ int liecl_b200_closure_pauli(liecl_b200_ctx* ctx, const uint64_t* x, const uint6
     copy_log(eng.log(), log, log_cap, log_len);
     if (eng.size() > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
     eng.download(basis_x, basis_z, basis_coef, ortho_coef);
+  });
+}
+
+int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x, const uint64_t* z,
+                                  const double* coef, int32_t ngens, uint32_t qubits, int32_t method,
+                                  const liecl_b200_config* cfg_in, int64_t cap, int64_t* basis_offsets,
+                                  uint64_t* basis_x, uint64_t* basis_z, double* basis_coef, int64_t term_cap,
+                                  int64_t* ortho_offsets, uint64_t* ortho_x, uint64_t* ortho_z, double* ortho_coef,
+                                  int64_t ortho_term_cap, int64_t* terms_needed, liecl_b200_stats* stats,
+                                  char* warnings, int64_t warnings_len, liecl_b200_decision* log, int64_t log_cap,
+                                  int64_t* log_len) {
+  return guarded([&] {
+    if (!ctx || !offsets || !stats || !terms_needed || !basis_offsets)
+      throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (ngens <= 0) throw Error(LIECL_B200_INVALID_INPUT, "closure requires a non-empty generator tuple");
+    if (qubits < 1 || qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..31 qubits");
+    if (offsets[0] != 0) throw Error(LIECL_B200_INVALID_INPUT, "offsets[0] must be 0");
+    for (int i = 0; i < ngens; ++i) {
+      if (offsets[i + 1] < offsets[i]) throw Error(LIECL_B200_INVALID_INPUT, "offsets must be non-decreasing");
+      for (int64_t t = offsets[i] + 1; t < offsets[i + 1]; ++t)  // PauliSum form: unique, sorted by (z, x)
+        if (pauli::pack(x[t], z[t]) <= pauli::pack(x[t - 1], z[t - 1]))
+          throw Error(LIECL_B200_INVALID_INPUT, "generator terms must be unique and sorted by (z, x)");
+    }
+    if (offsets[ngens] > 0 && (!x || !z || !coef)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    use_device(ctx);
+    const auto t0 = Clock::now();
+    const liecl_b200_config cfg = default_config(cfg_in);
+    const uint64_t k0 = ctx->kernels;
+    SumEngine eng(ctx, qubits, keep_for(method), cfg);
+    eng.run(offsets, x, z, coef, ngens);
+    *stats = eng.stats();
+    stats->kernels = ctx->kernels - k0;
+    stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+    write_warnings(eng.warnings(), warnings, warnings_len);
+    copy_log(eng.log(), log, log_cap, log_len);
+    terms_needed[0] = eng.terms(false);
+    terms_needed[1] = eng.terms(true);
+    if (eng.size() > cap || terms_needed[0] > term_cap || (ortho_offsets && terms_needed[1] > ortho_term_cap))
+      throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    if (terms_needed[0] > 0 && (!basis_x || !basis_z || !basis_coef))
+      throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    eng.download(false, basis_offsets, basis_x, basis_z, basis_coef);
+    if (ortho_offsets) eng.download(true, ortho_offsets, ortho_x, ortho_z, ortho_coef);
   });
 }
 

@@ -1,0 +1,650 @@
+// SumEngine -- the closure loop over multi-term PauliSums on the B200 (SURVEY
+// §8 row f2). Replaces run_engine + OrthonormStrategy on the Pauli backend
+// (R:src/closure.cpp:142-162, 267-310, 356-473 over R:src/pauli.cpp:78-228,
+// R:src/operator.cpp:137-182) bit for bit. Included by engine.cu inside its
+// anonymous namespace (Error, CU, DevBuf, HostBuf, launched, Warning, Clock,
+// fmt_double, borderline, pair_from_index).
+//
+// Verdict order is the reference's exactly:
+//   * generators are checked one by one against the then-current basis; a
+//     batch of generators is checked against the batch-start basis and cut
+//     after its first accept (later ones are re-run);
+//   * cursor rows are speculative like run_engine: every pair of row l is
+//     checked against the row-start basis (basis elements l' < n_limit), then
+//     applied in cursor order -- after an accept in the row, a "dependent"
+//     speculation stands and an "independent" one is recomputed against the
+//     current basis (R:src/closure.cpp:412-460). A device batch spans whole or
+//     partial rows; it stops at the end of the first row in which the basis
+//     grew, so every row is speculated against its own row-start basis.
+// Basis elements live in one append-only term pool (keys + coefficients,
+// element l = [off[l], off[l+1])); a key -> (l, coefficient) index with
+// per-key lists in ascending l serves sum_inner_product's merge join.
+
+class SumEngine {
+public:
+  SumEngine(liecl_b200_ctx* ctx, unsigned qubits, bool keep_original, const liecl_b200_config& cfg)
+      : ctx_(ctx), q_(qubits), keep_(keep_original), tol_(cfg.tolerance), record_(cfg.record_log != 0) {
+    if (qubits < 1 || qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..31 qubits");
+    if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
+    const uint64_t full = 1ull << (2 * qubits);
+    cap_ = cfg.max_dim ? static_cast<int64_t>(std::min<uint64_t>(cfg.max_dim, full)) : static_cast<int64_t>(full);
+    budget_ = cfg.batch_max > 0 ? cfg.batch_max : (int64_t(1) << 24);
+    if (cfg.deadline_seconds > 0) {
+      has_deadline_ = true;
+      deadline_ = Clock::now() + std::chrono::duration_cast<Clock::duration>(
+                                     std::chrono::duration<double>(cfg.deadline_seconds));
+    }
+    voff_.assign(1, 0);
+    ooff_.assign(1, 0);
+    dvoff_.ensure(1024);
+    CU(cudaMemsetAsync(dvoff_.p, 0, sizeof(int64_t), ctx_->stream));
+    if (keep_) {
+      dooff_.ensure(1024);
+      CU(cudaMemsetAsync(dooff_.p, 0, sizeof(int64_t), ctx_->stream));
+    }
+    grow_index(1 << 12);
+    small_.ensure(4);
+  }
+
+  int64_t size() const { return n_; }
+  int64_t terms(bool ortho) const { return (ortho || !keep_) ? voff_.back() : ooff_.back(); }
+  liecl_b200_stats stats() const {
+    liecl_b200_stats s = st_;
+    s.dimension = static_cast<uint64_t>(n_);
+    s.warnings = warns_.size();
+    return s;
+  }
+  const std::vector<Warning>& warnings() const { return warns_; }
+  const std::vector<liecl_b200_decision>& log() const { return log_; }
+
+  // generators: ngens sums, terms [goff[i], goff[i+1]) of (x, z, coef re/im)
+  void run(const int64_t* goff, const uint64_t* gx, const uint64_t* gz, const double* gc, int ngens) {
+    const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
+    const int64_t nt = ngens > 0 ? goff[ngens] : 0;
+    if (nt > (int64_t(1) << 30)) throw Error(LIECL_B200_CAPACITY, "generator terms exceed 2^30");
+    std::vector<int> hoff(static_cast<size_t>(ngens) + 1);
+    std::vector<unsigned long long> hkey(static_cast<size_t>(std::max<int64_t>(nt, 1)));
+    for (int i = 0; i <= ngens; ++i) hoff[i] = static_cast<int>(goff[i]);
+    for (int64_t t = 0; t < nt; ++t) {
+      if ((gx[t] & ~kmask) || (gz[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
+      hkey[t] = pauli::pack(gx[t], gz[t]);
+    }
+    Segs g;
+    g.shape(ngens, static_cast<int>(nt));
+    CU(cudaMemcpyAsync(g.off.p, hoff.data(), hoff.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+    if (nt > 0) {
+      CU(cudaMemcpyAsync(g.key.p, hkey.data(), nt * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                         ctx_->stream));
+      CU(cudaMemcpyAsync(g.val.p, gc, nt * sizeof(psum::C2), cudaMemcpyHostToDevice, ctx_->stream));
+    }
+    // generator loop (R:src/closure.cpp:378-403): norms, units, then checks
+    DevBuf<double> gn;
+    gn.ensure(std::max(ngens, 1));
+    std::vector<double> h_gn(static_cast<size_t>(std::max(ngens, 1)));
+    if (ngens > 0) {
+      psum::seg_norm_kernel<<<grid(ngens), 256, 0, ctx_->stream>>>(g.off.p, ngens, g.val.p, gn.p);
+      launched(ctx_);
+      psum::seg_scale_kernel<<<std::min(ngens, 4096), 256, 0, ctx_->stream>>>(g.off.p, ngens, gn.p, tol_, g.val.p);
+      launched(ctx_);
+      CU(cudaMemcpyAsync(h_gn.data(), gn.p, ngens * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+    }
+    int i = 0;
+    while (i < ngens) {
+      check_deadline();
+      Segs sub;
+      subrange(g, i, ngens, sub);
+      std::vector<double> rn;
+      Segs res;
+      check(sub, static_cast<int>(n_), res, rn);
+      int next = ngens;
+      for (int k = 0; i + k < ngens; ++k) {
+        const int gi = i + k;
+        if (!(h_gn[gi] > tol_)) {
+          warns_.push_back({"null_generator",
+                            "generator " + std::to_string(gi) + " has norm " + fmt_double(h_gn[gi]) +
+                                " and was skipped",
+                            h_gn[gi]});
+          log_decision(gi, -1, 1, 0, 0, h_gn[gi]);
+          continue;
+        }
+        ++st_.independence_checks;
+        const bool ind = rn[k] > tol_;
+        note(gi, -1, rn[k], ind);
+        log_decision(gi, -1, 0, ind ? 1 : 0, 0, rn[k]);
+        if (ind) {
+          accept(res, k, rn[k], sub, k);
+          next = gi + 1;  // later generators see the new basis
+          break;
+        }
+      }
+      i = next;
+    }
+    ++st_.batches;
+    cursor_loop();
+  }
+
+  // basis (or orthonormal tuple) -> host arrays: offsets (n+1), x, z, coef
+  void download(bool ortho, int64_t* off, uint64_t* x, uint64_t* z, double* coef) {
+    const bool v = ortho || !keep_;
+    const std::vector<int64_t>& o = v ? voff_ : ooff_;
+    const int64_t nt = o.back();
+    for (int64_t l = 0; l <= n_; ++l) off[l] = o[l];
+    if (nt == 0) return;
+    std::vector<unsigned long long> k(static_cast<size_t>(nt));
+    CU(cudaMemcpyAsync(k.data(), (v ? vkey_ : okey_).p, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx_->stream));
+    CU(cudaMemcpyAsync(coef, (v ? vval_ : oval_).p, nt * sizeof(psum::C2), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    for (int64_t t = 0; t < nt; ++t) {
+      x[t] = k[t] & 0xffffffffull;
+      z[t] = k[t] >> 32;
+    }
+  }
+
+private:
+  using C2 = psum::C2;
+  struct Segs {  // nseg sums on the device: terms [off[p], off[p+1])
+    int nseg = 0, total = 0;
+    DevBuf<int> off;
+    DevBuf<unsigned long long> key;
+    DevBuf<C2> val;
+    void shape(int ns, int tot) {
+      nseg = ns;
+      total = tot;
+      off.ensure(static_cast<size_t>(ns) + 1);
+      key.ensure(static_cast<size_t>(std::max(tot, 1)));
+      val.ensure(static_cast<size_t>(std::max(tot, 1)));
+    }
+    void swap(Segs& o) {
+      std::swap(nseg, o.nseg);
+      std::swap(total, o.total);
+      std::swap(off.p, o.off.p), std::swap(off.n, o.off.n);
+      std::swap(key.p, o.key.p), std::swap(key.n, o.key.n);
+      std::swap(val.p, o.val.p), std::swap(val.n, o.val.n);
+    }
+  };
+  static unsigned grid(int64_t n) { return static_cast<unsigned>(std::clamp<int64_t>((n + 255) / 256, 1, 8192)); }
+  static constexpr int64_t kMaxItems = int64_t(1) << 30;
+
+  void check_deadline() {
+    if (has_deadline_ && Clock::now() > deadline_)
+      throw Error(LIECL_B200_TIMEOUT, "closure computation exceeded its deadline");
+  }
+  void log_decision(int64_t l, int64_t m, int nul, int ind, int rc, double rn) {
+    if (record_) log_.push_back({l, m, nul, ind, rc, 0, rn});
+  }
+  std::string where_str(int64_t l, int64_t m) const {
+    return m < 0 ? "generator " + std::to_string(l) : "pair (" + std::to_string(l) + "," + std::to_string(m) + ")";
+  }
+  void note(int64_t l, int64_t m, double rn, bool ind) {  // R:src/closure.cpp:324-337
+    if (borderline(rn, tol_))
+      warns_.push_back({"borderline_residual",
+                        where_str(l, m) + ": residual " + fmt_double(rn) + " within 10x of tolerance " +
+                            fmt_double(tol_) + (ind ? " (accepted)" : " (rejected)"),
+                        rn});
+  }
+  int read_int(const int* dev) {
+    int v = 0;
+    CU(cudaMemcpyAsync(&v, dev, sizeof v, cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    return v;
+  }
+  long long read_ll(const long long* dev) {
+    long long v = 0;
+    CU(cudaMemcpyAsync(&v, dev, sizeof v, cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    return v;
+  }
+  template <class T> void grow_keep(DevBuf<T>& b, size_t used, size_t need) {
+    if (need <= b.n) return;
+    DevBuf<T> nb;
+    nb.ensure(std::max(need, 2 * b.n));
+    if (used) CU(cudaMemcpyAsync(nb.p, b.p, used * sizeof(T), cudaMemcpyDeviceToDevice, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    std::swap(b.p, nb.p);
+    std::swap(b.n, nb.n);
+  }
+  void ensure_temp(size_t bytes) { temp_.ensure(bytes); }
+
+  // int exclusive sum of n flags -> pos; returns the total
+  int scan_flags(const int* flag, int* pos, int n) {
+    size_t bytes = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag, pos, n, ctx_->stream));
+    ensure_temp(bytes);
+    CU(cub::DeviceScan::ExclusiveSum(temp_.p, bytes, flag, pos, n, ctx_->stream));
+    psum::scan_total_kernel<<<1, 1, 0, ctx_->stream>>>(pos, flag, n, small_.p);
+    launched(ctx_);
+    return read_int(small_.p);
+  }
+  // 64-bit exclusive sum of n counts -> pos; returns the total
+  long long scan_counts(const long long* cnt, long long* pos, int n) {
+    size_t bytes = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, pos, n, ctx_->stream));
+    ensure_temp(bytes);
+    CU(cub::DeviceScan::ExclusiveSum(temp_.p, bytes, cnt, pos, n, ctx_->stream));
+    total_ll_.ensure(1);
+    psum::scan_total64_kernel<<<1, 1, 0, ctx_->stream>>>(pos, cnt, n, total_ll_.p);
+    launched(ctx_);
+    return read_ll(total_ll_.p);
+  }
+
+  // PauliSum::from_terms on every segment of (off, key, val), n items:
+  // out = the merged sums (drop = true) or the raw runs (drop = false, with
+  // run_seg_ = each run's segment)
+  void merge(int nseg, const int* off, const unsigned long long* key, const C2* val, int n, bool drop, Segs& out) {
+    if (n == 0) {
+      out.shape(nseg, 0);
+      CU(cudaMemsetAsync(out.off.p, 0, (nseg + 1) * sizeof(int), ctx_->stream));
+      return;
+    }
+    ks_.ensure(n);
+    idx_.ensure(n);
+    is_.ensure(n);
+    seg_.ensure(n);
+    flag_.ensure(n);
+    pos_.ensure(n);
+    psum::iota_kernel<<<grid(n), 256, 0, ctx_->stream>>>(idx_.p, n);
+    launched(ctx_);
+    size_t bytes = 0;
+    CU(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off, off + 1,
+                                                 ctx_->stream));
+    ensure_temp(bytes);
+    CU(cub::DeviceSegmentedSort::StableSortPairs(temp_.p, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off, off + 1,
+                                                 ctx_->stream));
+    launched(ctx_);
+    psum::seg_of_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, n, seg_.p);
+    psum::heads_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ks_.p, seg_.p, n, flag_.p);
+    launched(ctx_), launched(ctx_);
+    const int nruns = scan_flags(flag_.p, pos_.p, n);
+    rkey_.ensure(std::max(nruns, 1));
+    rval_.ensure(std::max(nruns, 1));
+    rmag_.ensure(std::max(nruns, 1));
+    run_seg_.ensure(std::max(nruns, 1));
+    roff_.ensure(nseg + 1);
+    psum::run_sum_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ks_.p, is_.p, val, seg_.p, flag_.p, pos_.p, n, rkey_.p,
+                                                             rval_.p, rmag_.p, run_seg_.p);
+    psum::seg_positions_kernel<<<grid(nseg + 1), 256, 0, ctx_->stream>>>(off, nseg, n, pos_.p, nruns, roff_.p);
+    launched(ctx_), launched(ctx_);
+    if (!drop) {
+      out.shape(nseg, nruns);
+      std::swap(out.key.p, rkey_.p), std::swap(out.key.n, rkey_.n);
+      std::swap(out.val.p, rval_.p), std::swap(out.val.n, rval_.n);
+      std::swap(out.off.p, roff_.p), std::swap(out.off.n, roff_.n);
+      return;
+    }
+    keep_flag_.ensure(std::max(nruns, 1));
+    kpos_.ensure(std::max(nruns, 1));
+    psum::floor_keep_kernel<<<static_cast<unsigned>((nseg + 7) / 8), 256, 0, ctx_->stream>>>(roff_.p, nseg, rmag_.p,
+                                                                                        keep_flag_.p);
+    launched(ctx_);
+    const int nk = nruns > 0 ? scan_flags(keep_flag_.p, kpos_.p, nruns) : 0;
+    out.shape(nseg, nk);
+    if (nruns > 0) {
+      psum::compact_kernel<<<grid(nruns), 256, 0, ctx_->stream>>>(keep_flag_.p, kpos_.p, nruns, rkey_.p, rval_.p,
+                                                                  out.key.p, out.val.p);
+      launched(ctx_);
+    }
+    psum::seg_positions_kernel<<<grid(nseg + 1), 256, 0, ctx_->stream>>>(roff_.p, nseg, nruns, kpos_.p, nk,
+                                                                         out.off.p);
+    launched(ctx_);
+  }
+
+  // One linear_combination pass (project_residual, R:src/closure.cpp:142-162):
+  // out = from_terms(in * (1,0) ++ V_l * (-beta_l)), beta_l = <V_l, in>, for
+  // basis elements l < n_limit. Returns false when the batch is too large
+  // (the caller splits it).
+  bool pass(const Segs& in, int n_limit, Segs& out) {
+    const int n = in.total, nseg = in.nseg;
+    cnt_.ensure(std::max(n, 1));
+    cpos_.ensure(std::max(n, 1));
+    if (n > 0) {
+      psum::beta_count_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ix_, in.key.p, n, n_limit, cnt_.p);
+      launched(ctx_);
+    }
+    const long long nb = n > 0 ? scan_counts(cnt_.p, cpos_.p, n) : 0;
+    if (nb > kMaxItems) return false;
+    bl_.ensure(std::max<long long>(nb, 1));
+    bv_.ensure(std::max<long long>(nb, 1));
+    boff_.ensure(nseg + 1);
+    if (n > 0) {
+      psum::beta_fill_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ix_, in.key.p, in.val.p, n, n_limit, cpos_.p, bl_.p,
+                                                                bv_.p);
+      launched(ctx_);
+    }
+    psum::seg_offsets64_kernel<<<grid(nseg + 1), 256, 0, ctx_->stream>>>(in.off.p, nullptr, nseg, n, cpos_.p, nb,
+                                                                         boff_.p);
+    launched(ctx_);
+    merge(nseg, boff_.p, bl_.p, bv_.p, static_cast<int>(nb), false, beta_);  // beta runs, ascending l per segment
+    const int nruns = beta_.total;
+    const int nch = nseg + nruns;
+    chunks_.ensure(std::max(nch, 1));
+    clen_.ensure(std::max(nch, 1));
+    chpos_.ensure(std::max(nch, 1));
+    psum::chunk_base_kernel<<<grid(nseg), 256, 0, ctx_->stream>>>(in.off.p, beta_.off.p, nseg, chunks_.p, clen_.p);
+    launched(ctx_);
+    if (nruns > 0) {
+      psum::chunk_basis_kernel<<<grid(nruns), 256, 0, ctx_->stream>>>(beta_.key.p, beta_.val.p, run_seg_.p, nruns,
+                                                                      dvoff_.p, chunks_.p, clen_.p);
+      launched(ctx_);
+    }
+    const long long nt = scan_counts(clen_.p, chpos_.p, nch);
+    if (nt > kMaxItems) return false;
+    lc_.shape(nseg, static_cast<int>(nt));
+    psum::seg_offsets64_kernel<<<grid(nseg + 1), 256, 0, ctx_->stream>>>(nullptr, beta_.off.p, nseg, nch, chpos_.p,
+                                                                         nt, lc_.off.p);
+    launched(ctx_);
+    if (nt > 0) {
+      psum::chunk_fill_kernel<<<static_cast<unsigned>(std::min(nch, 65535)), 256, 0, ctx_->stream>>>(
+          chunks_.p, chpos_.p, nch, in.key.p, in.val.p, vkey_.p, vval_.p, lc_.key.p, lc_.val.p);
+      launched(ctx_);
+    }
+    merge(nseg, lc_.off.p, lc_.key.p, lc_.val.p, static_cast<int>(nt), true, out);
+    return true;
+  }
+
+  // OrthonormStrategy::check for every segment of h (unit candidates):
+  // residual sums and their norms, against basis elements l < n_limit
+  void check(const Segs& h, int n_limit, Segs& res, std::vector<double>& rn) {
+    rn.assign(static_cast<size_t>(h.nseg), 0.0);
+    if (h.nseg == 0) return;
+    if (n_limit == 0) {  // project_residual of an empty tuple returns h itself
+      copy_segs(h, res);
+    } else {
+      Segs& r1 = depth_ == 0 ? r1_ : *new_scratch();
+      ++depth_;
+      const bool ok = pass(h, n_limit, r1) && pass(r1, n_limit, res);
+      --depth_;
+      if (!ok) {
+        if (h.nseg == 1) throw Error(LIECL_B200_CAPACITY, "one projection exceeds 2^30 terms");
+        // split the batch: segments are independent
+        const int half = h.nseg / 2;
+        Segs a, b, ra, rb;
+        subrange(h, 0, half, a);
+        subrange(h, half, h.nseg, b);
+        std::vector<double> na, nb;
+        check(a, n_limit, ra, na);
+        check(b, n_limit, rb, nb);
+        concat(ra, rb, res);
+        std::copy(na.begin(), na.end(), rn.begin());
+        std::copy(nb.begin(), nb.end(), rn.begin() + half);
+        return;
+      }
+    }
+    rn_dev_.ensure(h.nseg);
+    psum::seg_norm_kernel<<<grid(h.nseg), 256, 0, ctx_->stream>>>(res.off.p, res.nseg, res.val.p, rn_dev_.p);
+    launched(ctx_);
+    CU(cudaMemcpyAsync(rn.data(), rn_dev_.p, h.nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+  }
+
+  void copy_segs(const Segs& a, Segs& b) {
+    b.shape(a.nseg, a.total);
+    CU(cudaMemcpyAsync(b.off.p, a.off.p, (a.nseg + 1) * sizeof(int), cudaMemcpyDeviceToDevice, ctx_->stream));
+    if (a.total > 0) {
+      CU(cudaMemcpyAsync(b.key.p, a.key.p, a.total * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                         ctx_->stream));
+      CU(cudaMemcpyAsync(b.val.p, a.val.p, a.total * sizeof(C2), cudaMemcpyDeviceToDevice, ctx_->stream));
+    }
+  }
+  // segments [a, b) of src as a batch of their own
+  void subrange(const Segs& src, int a, int b, Segs& dst) {
+    int lo = 0, hi = 0;
+    CU(cudaMemcpyAsync(&lo, src.off.p + a, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(&hi, src.off.p + b, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    dst.shape(b - a, hi - lo);
+    psum::rebase_kernel<<<grid(b - a + 1), 256, 0, ctx_->stream>>>(src.off.p, a, b - a, dst.off.p);
+    launched(ctx_);
+    if (hi > lo) {
+      CU(cudaMemcpyAsync(dst.key.p, src.key.p + lo, (hi - lo) * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                         ctx_->stream));
+      CU(cudaMemcpyAsync(dst.val.p, src.val.p + lo, (hi - lo) * sizeof(C2), cudaMemcpyDeviceToDevice, ctx_->stream));
+    }
+  }
+  void concat(const Segs& a, const Segs& b, Segs& out) {
+    out.shape(a.nseg + b.nseg, a.total + b.total);
+    std::vector<int> ho(static_cast<size_t>(a.nseg + b.nseg) + 1);
+    CU(cudaMemcpyAsync(ho.data(), a.off.p, (a.nseg + 1) * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(ho.data() + a.nseg, b.off.p, (b.nseg + 1) * sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    for (int p = a.nseg; p <= a.nseg + b.nseg; ++p) ho[p] += a.total;
+    CU(cudaMemcpyAsync(out.off.p, ho.data(), ho.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+    if (a.total) {
+      CU(cudaMemcpyAsync(out.key.p, a.key.p, a.total * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                         ctx_->stream));
+      CU(cudaMemcpyAsync(out.val.p, a.val.p, a.total * sizeof(C2), cudaMemcpyDeviceToDevice, ctx_->stream));
+    }
+    if (b.total) {
+      CU(cudaMemcpyAsync(out.key.p + a.total, b.key.p, b.total * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                         ctx_->stream));
+      CU(cudaMemcpyAsync(out.val.p + a.total, b.val.p, b.total * sizeof(C2), cudaMemcpyDeviceToDevice,
+                         ctx_->stream));
+    }
+    CU(cudaStreamSynchronize(ctx_->stream));  // ho is a stack buffer
+  }
+
+  // ---- basis pools + index ----------------------------------------------
+  void grow_index(uint64_t slots) {
+    DevBuf<unsigned long long> k;
+    DevBuf<int> h, t, c;
+    k.ensure(slots);
+    h.ensure(slots);
+    t.ensure(slots);
+    c.ensure(slots);
+    psum::Index nx = ix_;
+    nx.key = k.p, nx.head = h.p, nx.tail = t.p, nx.count = c.p, nx.mask = slots - 1;
+    psum::index_reset_kernel<<<grid(static_cast<int64_t>(slots)), 256, 0, ctx_->stream>>>(nx, slots);
+    launched(ctx_);
+    if (slots_ > 0) {
+      psum::index_rehash_kernel<<<grid(static_cast<int64_t>(slots_)), 256, 0, ctx_->stream>>>(ix_, slots_, nx);
+      launched(ctx_);
+    }
+    CU(cudaStreamSynchronize(ctx_->stream));
+    std::swap(skey_.p, k.p), std::swap(skey_.n, k.n);
+    std::swap(shead_.p, h.p), std::swap(shead_.n, h.n);
+    std::swap(stail_.p, t.p), std::swap(stail_.n, t.n);
+    std::swap(scount_.p, c.p), std::swap(scount_.n, c.n);
+    slots_ = slots;
+    sync_index();
+  }
+  void sync_index() {
+    ix_.key = skey_.p, ix_.head = shead_.p, ix_.tail = stail_.p, ix_.count = scount_.p, ix_.mask = slots_ - 1;
+    ix_.e_l = el_.p, ix_.e_v = ev_.p, ix_.e_next = enext_.p;
+  }
+
+  // accept residual segment k (norm rn) of res; the candidate h_unit is
+  // segment hk of h (the original kept by Alg. 3)
+  void accept(const Segs& res, int k, double rn, const Segs& h, int hk) {
+    if (n_ >= cap_)
+      throw Error(LIECL_B200_CAPACITY,
+                  "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
+    int r0 = 0, r1 = 0;
+    CU(cudaMemcpyAsync(&r0, res.off.p + k, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(&r1, res.off.p + k + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    const int T = r1 - r0;
+    const int64_t vt = voff_.back();
+    grow_keep(vkey_, static_cast<size_t>(vt), static_cast<size_t>(vt + T));
+    grow_keep(vval_, static_cast<size_t>(vt), static_cast<size_t>(vt + T));
+    if (T > 0) {
+      psum::append_scaled_kernel<<<grid(T), 256, 0, ctx_->stream>>>(res.key.p + r0, res.val.p + r0, T, rn,
+                                                                    vkey_.p + vt, vval_.p + vt);
+      launched(ctx_);
+    }
+    // index: keys of one element are distinct; keep the load factor <= 1/2
+    keys_upper_ += static_cast<uint64_t>(T);
+    if (2 * keys_upper_ > slots_) {
+      uint64_t s = slots_;
+      while (2 * keys_upper_ > s) s *= 2;
+      grow_index(s);
+    }
+    grow_keep(el_, static_cast<size_t>(entries_), static_cast<size_t>(entries_ + T));
+    grow_keep(ev_, static_cast<size_t>(entries_), static_cast<size_t>(entries_ + T));
+    grow_keep(enext_, static_cast<size_t>(entries_), static_cast<size_t>(entries_ + T));
+    sync_index();
+    if (T > 0) {
+      psum::index_insert_kernel<<<grid(T), 256, 0, ctx_->stream>>>(ix_, vkey_.p + vt, vval_.p + vt, T,
+                                                                   static_cast<int>(n_), static_cast<int>(entries_));
+      launched(ctx_);
+    }
+    entries_ += T;
+    voff_.push_back(vt + T);
+    grow_keep(dvoff_, voff_.size() - 1, voff_.size());
+    CU(cudaMemcpyAsync(dvoff_.p + n_ + 1, &voff_.back(), sizeof(int64_t), cudaMemcpyHostToDevice, ctx_->stream));
+    if (keep_) {
+      int h0 = 0, h1 = 0;
+      CU(cudaMemcpyAsync(&h0, h.off.p + hk, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaMemcpyAsync(&h1, h.off.p + hk + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      const int64_t ot = ooff_.back();
+      grow_keep(okey_, static_cast<size_t>(ot), static_cast<size_t>(ot + h1 - h0));
+      grow_keep(oval_, static_cast<size_t>(ot), static_cast<size_t>(ot + h1 - h0));
+      if (h1 > h0) {
+        CU(cudaMemcpyAsync(okey_.p + ot, h.key.p + h0, (h1 - h0) * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToDevice, ctx_->stream));
+        CU(cudaMemcpyAsync(oval_.p + ot, h.val.p + h0, (h1 - h0) * sizeof(C2), cudaMemcpyDeviceToDevice,
+                           ctx_->stream));
+      }
+      ooff_.push_back(ot + h1 - h0);
+      grow_keep(dooff_, ooff_.size() - 1, ooff_.size());
+      CU(cudaMemcpyAsync(dooff_.p + n_ + 1, &ooff_.back(), sizeof(int64_t), cudaMemcpyHostToDevice, ctx_->stream));
+    }
+    CU(cudaStreamSynchronize(ctx_->stream));  // the host offset sources above are vector slots
+    ++n_;
+    ++st_.accepted;
+  }
+
+  // ---- the cursor loop (R:src/closure.cpp:412-460) -----------------------
+  void cursor_loop() {
+    int64_t l = 1, m = 0;
+    int64_t row_start_n = n_;
+    while (l < n_) {
+      check_deadline();
+      if (m == 0) row_start_n = n_;
+      const int n_limit = static_cast<int>(row_start_n);
+      // pairs from (l, m) in cursor order, whole rows while the basis has not
+      // grown in this row, within the product budget (at least one pair)
+      const std::vector<int64_t>& bo = keep_ ? ooff_ : voff_;
+      const int64_t g0 = pair_index(l, m);
+      std::vector<int> poff(1, 0);
+      int64_t prods = 0, ll = l, mm = m;
+      for (;;) {
+        const int64_t c = (bo[ll + 1] - bo[ll]) * (bo[mm + 1] - bo[mm]);
+        if (poff.size() > 1 && prods + c > budget_) break;
+        if (prods + c > kMaxItems) throw Error(LIECL_B200_CAPACITY, "one bracket exceeds 2^30 term products");
+        prods += c;
+        poff.push_back(static_cast<int>(prods));
+        if (++mm == ll) {
+          ++ll;
+          mm = 0;
+          if (ll >= n_ || n_ != row_start_n) break;  // next row: only if it exists and nothing grew
+        }
+        if (static_cast<int64_t>(poff.size()) > (int64_t(1) << 20)) break;
+      }
+      const int cnt = static_cast<int>(poff.size()) - 1;
+      // commutators -> merged sums -> norms -> units (K1, R:src/closure.cpp:419-423)
+      poff_.ensure(cnt + 1);
+      CU(cudaMemcpyAsync(poff_.p, poff.data(), poff.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+      pk_.ensure(std::max<int64_t>(prods, 1));
+      pv_.ensure(std::max<int64_t>(prods, 1));
+      const int64_t* bdoff = keep_ ? dooff_.p : dvoff_.p;
+      const unsigned long long* bkey = keep_ ? okey_.p : vkey_.p;
+      const C2* bval = keep_ ? oval_.p : vval_.p;
+      psum::products_kernel<<<cnt, 256, 0, ctx_->stream>>>(g0, cnt, poff_.p, bdoff, bkey, bval, pk_.p, pv_.p);
+      launched(ctx_);
+      Segs& h = h_;
+      merge(cnt, poff_.p, pk_.p, pv_.p, static_cast<int>(prods), true, h);
+      hn_.ensure(cnt);
+      psum::seg_norm_kernel<<<grid(cnt), 256, 0, ctx_->stream>>>(h.off.p, cnt, h.val.p, hn_.p);
+      psum::seg_scale_kernel<<<std::min(cnt, 4096), 256, 0, ctx_->stream>>>(h.off.p, cnt, hn_.p, tol_, h.val.p);
+      launched(ctx_), launched(ctx_);
+      std::vector<double> hn(static_cast<size_t>(cnt));
+      CU(cudaMemcpyAsync(hn.data(), hn_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      // speculative checks against the row-start basis
+      Segs& res = res_;
+      std::vector<double> rn;
+      check(h, n_limit, res, rn);
+      ++st_.batches;
+      // ordered apply
+      int j = 0;
+      for (; j < cnt; ++j) {
+        int64_t pl, pm;
+        pair_from_index(g0 + j, pl, pm);
+        if (pm == 0 && j > 0 && n_ != row_start_n) break;  // row after growth: speculate again
+        if (pm == 0) row_start_n = n_;
+        ++st_.commutators_evaluated;
+        if (!(hn[j] > tol_)) {
+          log_decision(pl, pm, 1, 0, 0, 0.0);
+          continue;
+        }
+        ++st_.independence_checks;
+        double r = rn[j];
+        int rc = 0;
+        if (n_ != row_start_n && r > tol_) {  // stale "independent": recompute (R:src/closure.cpp:440-444)
+          Segs &one = one_, &rres = rres_;
+          std::vector<double> rr;
+          subrange(h, j, j + 1, one);
+          check(one, static_cast<int>(n_), rres, rr);
+          r = rr[0];
+          rc = 1;
+          ++st_.rechecks;
+          const bool ind = r > tol_;
+          note(pl, pm, r, ind);
+          log_decision(pl, pm, 0, ind ? 1 : 0, rc, r);
+          if (ind) accept(rres, 0, r, one, 0);
+          continue;
+        }
+        const bool ind = r > tol_;
+        note(pl, pm, r, ind);
+        log_decision(pl, pm, 0, ind ? 1 : 0, rc, r);
+        if (ind) accept(res, j, r, h, j);
+      }
+      const int64_t g_next = g0 + j;
+      pair_from_index(g_next, l, m);
+    }
+  }
+
+  liecl_b200_ctx* ctx_;
+  unsigned q_;
+  bool keep_;
+  double tol_;
+  bool record_;
+  int64_t cap_ = 0, budget_ = 0;
+  bool has_deadline_ = false;
+  Clock::time_point deadline_{};
+  int64_t n_ = 0;
+  liecl_b200_stats st_{};
+  std::vector<Warning> warns_;
+  std::vector<liecl_b200_decision> log_;
+  // basis pools: orthonormal tuple V; originals O (Alg. 3, commutator basis)
+  std::vector<int64_t> voff_, ooff_;
+  DevBuf<int64_t> dvoff_, dooff_;
+  DevBuf<unsigned long long> vkey_, okey_;
+  DevBuf<C2> vval_, oval_;
+  // index
+  psum::Index ix_{};
+  uint64_t slots_ = 0, keys_upper_ = 0;
+  int64_t entries_ = 0;
+  DevBuf<unsigned long long> skey_;
+  DevBuf<int> shead_, stail_, scount_, el_, enext_;
+  DevBuf<C2> ev_;
+  // batch scratch
+  DevBuf<unsigned char> temp_;
+  DevBuf<int> small_, poff_, seg_, flag_, pos_, run_seg_, roff_, keep_flag_, kpos_, boff_;
+  DevBuf<long long> cnt_, cpos_, clen_, chpos_, total_ll_;
+  DevBuf<unsigned> idx_, is_;
+  DevBuf<unsigned long long> ks_, rkey_, pk_, bl_;
+  DevBuf<C2> rval_, pv_, bv_;
+  DevBuf<double> rmag_, hn_, rn_dev_;
+  DevBuf<psum::Chunk> chunks_;
+  Segs beta_, lc_, h_, res_, r1_, one_, rres_;
+  int depth_ = 0;  // check() recursion (batch splits) takes fresh scratch
+  std::vector<std::unique_ptr<Segs>> spill_;
+  Segs* new_scratch() {
+    spill_.push_back(std::make_unique<Segs>());
+    return spill_.back().get();
+  }
+};

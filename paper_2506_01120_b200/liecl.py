@@ -355,9 +355,66 @@ def closure_pauli_arrays(x, z, coef, qubits: int, method: Method = Method.orthon
                          (bx[:n].copy(), bz[:n].copy(), bc[:n].copy()), oc[:n].copy())
 
 
+def closure_pauli_sums_arrays(offsets, x, z, coef, qubits: int, method: Method = Method.orthonorm_dimonly,
+                              config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
+    """Array-level entry for general (multi-term) Pauli generators: generator i
+    = terms [offsets[i], offsets[i+1]) of x, z (uint64 masks) and coef (t, 2),
+    in PauliSum form. Result sums are returned as PauliSum lists and as arrays
+    (`basis_array` = (offsets, x, z, coef))."""
+    config = config or ClosureConfig()
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    x = np.ascontiguousarray(x, np.uint64)
+    z = np.ascontiguousarray(z, np.uint64)
+    coef = np.ascontiguousarray(coef, np.float64).reshape(-1, 2)
+    lib = native.load()
+    u64, i64 = C.POINTER(C.c_uint64), C.POINTER(C.c_int64)
+    cap = int(config.max_dim or min(4 ** qubits, 1 << 20))
+    tcap = max(1 << 16, 8 * len(x))
+    while True:
+        bo, oo = np.zeros(cap + 1, np.int64), np.zeros(cap + 1, np.int64)
+        bx, bz, bc = np.zeros(tcap, np.uint64), np.zeros(tcap, np.uint64), np.zeros((tcap, 2))
+        ox, oz, ocf = np.zeros(tcap, np.uint64), np.zeros(tcap, np.uint64), np.zeros((tcap, 2))
+        need = np.zeros(2, np.int64)
+        st = native.Stats()
+        wbuf = C.create_string_buffer(1 << 20)
+        log_cap = (1 << 24) if config.record_log else 0
+        log = np.zeros(max(log_cap, 1), DECISION_DTYPE)
+        log_len = C.c_int64()
+        cfg = config.native()
+        status = lib.liecl_b200_closure_pauli_sums(
+            native.context(device), offsets.ctypes.data_as(i64), x.ctypes.data_as(u64), z.ctypes.data_as(u64),
+            _dp(coef), C.c_int32(len(offsets) - 1), C.c_uint32(qubits), C.c_int32(method.value), C.byref(cfg),
+            C.c_int64(cap), bo.ctypes.data_as(i64), bx.ctypes.data_as(u64), bz.ctypes.data_as(u64), _dp(bc),
+            C.c_int64(tcap), oo.ctypes.data_as(i64), ox.ctypes.data_as(u64), oz.ctypes.data_as(u64), _dp(ocf),
+            C.c_int64(tcap), need.ctypes.data_as(i64), C.byref(st), wbuf, C.c_int64(len(wbuf)),
+            log.ctypes.data_as(C.c_void_p) if config.record_log else None, C.c_int64(log_cap), C.byref(log_len))
+        if status == native.CAPACITY and native.last_error() == "output buffers too small" \
+                and (need.max() > tcap or int(st.dimension) > cap):
+            tcap = int(need.max())
+            cap = max(cap, int(st.dimension))
+            continue
+        _check(status)
+        break
+    n = int(st.dimension)
+    warnings = _parse_warnings(wbuf.value)
+    stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds, warnings,
+                         {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
+
+    def sums(off, xs, zs, cs):
+        return [PauliSum(qubits, [(PauliString(int(xs[t]), int(zs[t]), qubits), complex(cs[t, 0], cs[t, 1]))
+                                  for t in range(off[i], off[i + 1])]) for i in range(n)]
+
+    def arrays(off, xs, zs, cs):
+        t = int(off[n])
+        return off[: n + 1].copy(), xs[:t].copy(), zs[:t].copy(), cs[:t].copy()
+    return ClosureResult(sums(bo, bx, bz, bc), sums(oo, ox, oz, ocf), n, method, Backend.pauli, config.tolerance,
+                         stats, log[: log_len.value].copy() if config.record_log else None,
+                         arrays(bo, bx, bz, bc), arrays(oo, ox, oz, ocf))
+
+
 def run_closure(generators, method: Method, config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
-    """R:src/closure.cpp:541-564: orthonormal methods (dense + single-string
-    Pauli) and matrix inversion (dense)."""
+    """R:src/closure.cpp:541-564: orthonormal methods (dense, single-string
+    and multi-term Pauli) and matrix inversion (dense)."""
     if method == Method.standard_rank:
         raise InvalidInputError(f"{to_string(method)}: not on the B200 hot path")
     backend, dim = _validate(generators)
@@ -367,14 +424,20 @@ def run_closure(generators, method: Method, config: ClosureConfig | None = None,
         gens = np.stack([g.vec() if g is not None else np.zeros(dim * dim, np.complex128) for g in generators])
         return closure_dense_arrays(gens, dim, method, config, device)
     qubits = next(g.qubits for g in generators if g is not None)
+    if any(g is not None and len(g.terms) > 1 for g in generators):
+        # general sums: the multi-term engine
+        offs, xs, zs, cs = [0], [], [], []
+        for g in generators:
+            for s_, c in (g.terms if g is not None else []):
+                xs.append(s_.x); zs.append(s_.z); cs.append((complex(c).real, complex(c).imag))
+            offs.append(len(xs))
+        return closure_pauli_sums_arrays(np.array(offs, np.int64), np.array(xs, np.uint64), np.array(zs, np.uint64),
+                                         np.array(cs, np.float64).reshape(-1, 2), qubits, method, config, device)
     xs, zs, cs = [], [], []
     for g in generators:
         if g is None or len(g.terms) == 0:
             xs.append(0); zs.append(0); cs.append((0.0, 0.0))
             continue
-        if len(g.terms) != 1:
-            raise InvalidInputError("B200 Pauli path: generators must be single Pauli strings "
-                                    "(multi-term sums are not on the hot path yet)")
         s, c = g.terms[0]
         xs.append(s.x); zs.append(s.z); cs.append((complex(c).real, complex(c).imag))
     return closure_pauli_arrays(np.array(xs, np.uint64), np.array(zs, np.uint64), np.array(cs), qubits, method,

@@ -27,6 +27,16 @@ def ref():
 
 
 @pytest.fixture(scope="session")
+def ref_exact():
+    """The reference built with its default rounding (no FMA contraction
+    anywhere, oracle/Makefile): the bit-exact pin for PauliSum arithmetic."""
+    from oracle.oracle import REF_EXACT_SO, Ref
+    if not os.path.exists(REF_EXACT_SO):
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    return Ref(REF_EXACT_SO)
+
+
+@pytest.fixture(scope="session")
 def golden():
     import json
 
