@@ -153,7 +153,75 @@ ClosureResult close_dense(std::span<const Operator> generators, const ClosureCon
   return r;
 }
 
+// general (multi-term) sums: liecl_b200_closure_pauli_sums, bit-exact
+ClosureResult close_pauli_sums(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
+  std::uint32_t qubits = 0;
+  std::vector<std::int64_t> off(1, 0);
+  std::vector<std::uint64_t> x, z;
+  std::vector<double> c;
+  for (const Operator& g : generators) {
+    if (!g.is_null()) {
+      qubits = g.pauli().qubits();
+      for (const auto& t : g.pauli().terms()) {
+        x.push_back(t.string.x);
+        z.push_back(t.string.z);
+        c.push_back(t.coefficient.real());
+        c.push_back(t.coefficient.imag());
+      }
+    }
+    off.push_back(static_cast<std::int64_t>(x.size()));
+  }
+  const liecl_b200_config cfg = to_native(config);
+  std::int64_t cap = config.max_dim ? static_cast<std::int64_t>(config.max_dim)
+                                    : (qubits < 10 ? (std::int64_t{1} << (2 * qubits)) : (std::int64_t{1} << 20));
+  std::int64_t tcap = std::max<std::int64_t>(std::int64_t{1} << 16, 8 * static_cast<std::int64_t>(x.size()));
+  for (;;) {
+    std::vector<std::int64_t> bo(cap + 1), oo(cap + 1), need(2);
+    std::vector<std::uint64_t> bx(tcap), bz(tcap), ox(tcap), oz(tcap);
+    std::vector<double> bc(2 * tcap), ocf(2 * tcap);
+    liecl_b200_stats st{};
+    std::vector<char> wbuf(1 << 20);
+    const int s = liecl_b200_closure_pauli_sums(
+        context(), off.data(), x.data(), z.data(), c.data(), static_cast<int32_t>(generators.size()), qubits,
+        keep ? LIECL_B200_METHOD_ORTHONORM : LIECL_B200_METHOD_ORTHONORM_DIMONLY, &cfg, cap, bo.data(), bx.data(),
+        bz.data(), bc.data(), tcap, oo.data(), ox.data(), oz.data(), ocf.data(), tcap, need.data(), &st, wbuf.data(),
+        static_cast<std::int64_t>(wbuf.size()), nullptr, 0, nullptr);
+    if (s == LIECL_B200_CAPACITY && std::string(liecl_b200_last_error()) == "output buffers too small") {
+      tcap = std::max(need[0], need[1]);
+      cap = std::max<std::int64_t>(cap, static_cast<std::int64_t>(st.dimension));
+      continue;
+    }
+    check(s);
+    // unique sorted terms without -0 components: from_terms rebuilds the
+    // engine's sums value for value
+    auto unpack = [&](const std::vector<std::int64_t>& o, const std::vector<std::uint64_t>& xs,
+                      const std::vector<std::uint64_t>& zs, const std::vector<double>& cs) {
+      OperatorTuple t;
+      t.reserve(st.dimension);
+      std::vector<PauliSum::Term> terms;
+      for (size_t k = 0; k < st.dimension; ++k) {
+        terms.clear();
+        for (std::int64_t i = o[k]; i < o[k + 1]; ++i)
+          terms.push_back({PauliString{xs[i], zs[i], qubits}, Complex{cs[2 * i], cs[2 * i + 1]}});
+        t.emplace_back(PauliSum::from_terms(qubits, terms));
+      }
+      return t;
+    };
+    ClosureResult r;
+    r.basis = unpack(bo, bx, bz, bc);
+    r.orthonormal_basis = unpack(oo, ox, oz, ocf);
+    r.dimension = st.dimension;
+    r.method = keep ? Method::orthonorm : Method::orthonorm_dimonly;
+    r.backend = Backend::pauli;
+    r.tolerance = config.tolerance;
+    fill_stats(r, st, wbuf);
+    return r;
+  }
+}
+
 ClosureResult close_pauli(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
+  for (const Operator& g : generators)
+    if (!g.is_null() && g.pauli().size() > 1) return close_pauli_sums(generators, config, keep);
   std::uint32_t qubits = 0;
   std::vector<std::uint64_t> x, z;
   std::vector<double> c;
@@ -166,9 +234,6 @@ ClosureResult close_pauli(std::span<const Operator> generators, const ClosureCon
       continue;
     }
     qubits = g.pauli().qubits();
-    if (g.pauli().size() != 1)
-      throw InvalidInputError("B200 Pauli path: generators must be single Pauli strings "
-                              "(multi-term sums are not on the hot path yet)");
     const auto& t = g.pauli().terms()[0];
     x.push_back(t.string.x);
     z.push_back(t.string.z);

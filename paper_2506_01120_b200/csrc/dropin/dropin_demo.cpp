@@ -10,6 +10,7 @@
 #include "liecl/closure.hpp"
 #include "liecl/dense.hpp"
 #include "liecl/errors.hpp"
+#include "liecl/generators.hpp"
 #include "liecl/pauli.hpp"
 
 using namespace liecl;
@@ -77,6 +78,28 @@ int main() {
       const auto& t = r.basis[k].pauli().terms()[0];
       std::printf("%s[%llu,%llu,%.17g,%.17g]", k ? "," : "", static_cast<unsigned long long>(t.string.x),
                   static_cast<unsigned long long>(t.string.z), t.coefficient.real(), t.coefficient.imag());
+    }
+    std::printf("]}, ");
+  }
+  // multi-term Pauli sums: the reference's TFIM-open HVA generators, n = 6
+  for (const Method m : {Method::orthonorm_dimonly, Method::orthonorm}) {
+    AnsatzSpec spec;
+    spec.family = AnsatzFamily::tfim_hva_open;
+    spec.qubits = 6;
+    std::vector<Operator> gens;
+    for (auto& s : build_generators(spec)) gens.emplace_back(std::move(s));
+    const ClosureResult r = run_closure(gens, m, cfg);
+    std::printf("\"tfim6_%s\": ", to_string(m).c_str());
+    print_stats(r);
+    std::printf(", \"sums\": [");
+    for (size_t k = 0; k < r.basis.size(); ++k) {
+      std::printf("%s[", k ? "," : "");
+      const auto terms = r.basis[k].pauli().terms();
+      for (size_t i = 0; i < terms.size(); ++i)
+        std::printf("%s[%llu,%llu,%.17g,%.17g]", i ? "," : "", static_cast<unsigned long long>(terms[i].string.x),
+                    static_cast<unsigned long long>(terms[i].string.z), terms[i].coefficient.real(),
+                    terms[i].coefficient.imag());
+      std::printf("]");
     }
     std::printf("]}, ");
   }

@@ -23,6 +23,7 @@
 //
 // The Pauli single-string path (pauli.cuh) is bit-exact and runs frontier
 // batches of all available pairs.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cusolverDn.h>
@@ -33,6 +34,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>

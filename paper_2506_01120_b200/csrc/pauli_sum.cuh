@@ -86,6 +86,46 @@ __global__ void seg_of_kernel(const int* __restrict__ off, int nseg, int n, int*
   }
 }
 
+// Combined sort key (segment | invalid | key) for one stable LSD radix sort of
+// the whole batch over only its live bits: Pauli keys compact to 2q bits
+// x | z << q (the (z, x) order is kept), index keys (basis l) use kbits bits.
+__global__ void combine_kernel(const int* __restrict__ off, int nseg, int n, const unsigned long long* __restrict__ key,
+                               int pauli_q, int kbits, unsigned long long* __restrict__ ck) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off[mid] <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    const unsigned long long k = key[i];
+    unsigned long long c;
+    if (pauli_q > 0) {
+      const bool inv = k == kInvalid;
+      c = inv ? (1ull << kbits) : (key_x(k) | (key_z(k) << pauli_q));
+    } else {
+      c = k;
+    }
+    ck[i] = (static_cast<unsigned long long>(lo) << (kbits + 1)) | c;
+  }
+}
+__global__ void split_kernel(const unsigned long long* __restrict__ ck, int n, int pauli_q, int kbits,
+                             unsigned long long* __restrict__ ks, int* __restrict__ seg) {
+  const unsigned long long kmask = (1ull << kbits) - 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long c = ck[i];
+    seg[i] = static_cast<int>(c >> (kbits + 1));
+    if ((c >> kbits) & 1ull) {
+      ks[i] = kInvalid;
+    } else if (pauli_q > 0) {
+      const unsigned long long k = c & kmask, qm = (1ull << pauli_q) - 1;
+      ks[i] = pauli::pack(k & qm, k >> pauli_q);
+    } else {
+      ks[i] = c & kmask;
+    }
+  }
+}
+
 // first element of each (segment, key) run of the sorted keys
 __global__ void heads_kernel(const unsigned long long* __restrict__ ks, const int* __restrict__ seg, int n,
                              int* __restrict__ flag) {

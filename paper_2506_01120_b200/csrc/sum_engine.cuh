@@ -36,14 +36,25 @@ public:
     }
     voff_.assign(1, 0);
     ooff_.assign(1, 0);
-    dvoff_.ensure(1024);
+    need(dvoff_, 1024);
     CU(cudaMemsetAsync(dvoff_.p, 0, sizeof(int64_t), ctx_->stream));
     if (keep_) {
-      dooff_.ensure(1024);
+      need(dooff_, 1024);
       CU(cudaMemsetAsync(dooff_.p, 0, sizeof(int64_t), ctx_->stream));
     }
     grow_index(1 << 12);
-    small_.ensure(4);
+    need(small_, 4);
+  }
+
+  ~SumEngine() {
+    if (trace_) {
+      std::fprintf(stderr, "[sum_engine] n=%lld batches=%llu rechecks=%llu accepts=%llu\n", (long long)n_,
+                   (unsigned long long)st_.batches, (unsigned long long)st_.rechecks,
+                   (unsigned long long)st_.accepted);
+      for (const auto& kv : tsum_)
+        std::fprintf(stderr, "[sum_engine] %-10s %9.3f ms  %8llu calls\n", kv.first.c_str(), kv.second.first,
+                     (unsigned long long)kv.second.second);
+    }
   }
 
   int64_t size() const { return n_; }
@@ -59,6 +70,7 @@ public:
 
   // generators: ngens sums, terms [goff[i], goff[i+1]) of (x, z, coef re/im)
   void run(const int64_t* goff, const uint64_t* gx, const uint64_t* gz, const double* gc, int ngens) {
+    Stage st_run(this, "run");
     const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
     const int64_t nt = ngens > 0 ? goff[ngens] : 0;
     if (nt > (int64_t(1) << 30)) throw Error(LIECL_B200_CAPACITY, "generator terms exceed 2^30");
@@ -121,6 +133,7 @@ public:
       i = next;
     }
     ++st_.batches;
+    Stage st_cur(this, "cursor");
     cursor_loop();
   }
 
@@ -144,6 +157,33 @@ public:
 
 private:
   using C2 = psum::C2;
+  // LIECL_B200_TRACE=1: synchronised per-stage wall times (diagnostics)
+  bool trace_ = std::getenv("LIECL_B200_TRACE") != nullptr;
+  std::map<std::string, std::pair<double, uint64_t>> tsum_;
+  struct Stage {
+    SumEngine* e;
+    const char* name;
+    Clock::time_point t0;
+    Stage(SumEngine* eng, const char* n) : e(eng), name(n) {
+      if (e->trace_) {
+        cudaStreamSynchronize(e->ctx_->stream);
+        t0 = Clock::now();
+      }
+    }
+    ~Stage() {
+      if (e->trace_) {
+        cudaStreamSynchronize(e->ctx_->stream);
+        auto& v = e->tsum_[name];
+        v.first += std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+        ++v.second;
+      }
+    }
+  };
+  // scratch grows geometrically: batch sizes vary call to call, and every
+  // exact-size reallocation would be a device-synchronising cudaFree
+  template <class T> static void need(DevBuf<T>& b, size_t n) {
+    if (n > b.n) b.ensure(std::max(n, b.n + b.n / 2));
+  }
   struct Segs {  // nseg sums on the device: terms [off[p], off[p+1])
     int nseg = 0, total = 0;
     DevBuf<int> off;
@@ -152,9 +192,9 @@ private:
     void shape(int ns, int tot) {
       nseg = ns;
       total = tot;
-      off.ensure(static_cast<size_t>(ns) + 1);
-      key.ensure(static_cast<size_t>(std::max(tot, 1)));
-      val.ensure(static_cast<size_t>(std::max(tot, 1)));
+      need(off, static_cast<size_t>(ns) + 1);
+      need(key, static_cast<size_t>(std::max(tot, 1)));
+      need(val, static_cast<size_t>(std::max(tot, 1)));
     }
     void swap(Segs& o) {
       std::swap(nseg, o.nseg);
@@ -197,6 +237,7 @@ private:
     return v;
   }
   template <class T> void grow_keep(DevBuf<T>& b, size_t used, size_t need) {
+    Stage st_g(this, "grow_keep");
     if (need <= b.n) return;
     DevBuf<T> nb;
     nb.ensure(std::max(need, 2 * b.n));
@@ -205,10 +246,14 @@ private:
     std::swap(b.p, nb.p);
     std::swap(b.n, nb.n);
   }
-  void ensure_temp(size_t bytes) { temp_.ensure(bytes); }
+  void ensure_temp(size_t bytes) {
+    Stage st_t(this, "temp");
+    need(temp_, bytes);
+  }
 
   // int exclusive sum of n flags -> pos; returns the total
   int scan_flags(const int* flag, int* pos, int n) {
+    Stage st_sc(this, "scan");
     size_t bytes = 0;
     CU(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag, pos, n, ctx_->stream));
     ensure_temp(bytes);
@@ -223,7 +268,7 @@ private:
     CU(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, pos, n, ctx_->stream));
     ensure_temp(bytes);
     CU(cub::DeviceScan::ExclusiveSum(temp_.p, bytes, cnt, pos, n, ctx_->stream));
-    total_ll_.ensure(1);
+    need(total_ll_, 1);
     psum::scan_total64_kernel<<<1, 1, 0, ctx_->stream>>>(pos, cnt, n, total_ll_.p);
     launched(ctx_);
     return read_ll(total_ll_.p);
@@ -232,36 +277,64 @@ private:
   // PauliSum::from_terms on every segment of (off, key, val), n items:
   // out = the merged sums (drop = true) or the raw runs (drop = false, with
   // run_seg_ = each run's segment)
-  void merge(int nseg, const int* off, const unsigned long long* key, const C2* val, int n, bool drop, Segs& out) {
+  // pauli_q > 0: keys are packed Pauli strings (kbits = 2q); 0: basis indices
+  // below 2^kbits
+  void merge(int nseg, const int* off, const unsigned long long* key, const C2* val, int n, bool drop, Segs& out,
+             int pauli_q, int kbits) {
+    Stage st_merge(this, drop ? "merge" : "merge_beta");
     if (n == 0) {
       out.shape(nseg, 0);
       CU(cudaMemsetAsync(out.off.p, 0, (nseg + 1) * sizeof(int), ctx_->stream));
       return;
     }
-    ks_.ensure(n);
-    idx_.ensure(n);
-    is_.ensure(n);
-    seg_.ensure(n);
-    flag_.ensure(n);
-    pos_.ensure(n);
+    need(ks_, n);
+    need(idx_, n);
+    need(is_, n);
+    need(seg_, n);
+    need(flag_, n);
+    need(pos_, n);
     psum::iota_kernel<<<grid(n), 256, 0, ctx_->stream>>>(idx_.p, n);
     launched(ctx_);
+    int segbits = 1;
+    while ((1ll << segbits) < nseg) ++segbits;
+    const int end_bit = segbits + kbits + 1;
     size_t bytes = 0;
-    CU(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off, off + 1,
-                                                 ctx_->stream));
-    ensure_temp(bytes);
-    CU(cub::DeviceSegmentedSort::StableSortPairs(temp_.p, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off, off + 1,
-                                                 ctx_->stream));
-    launched(ctx_);
-    psum::seg_of_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, n, seg_.p);
+    if (end_bit <= 64) {
+      // one stable radix sort of (segment | invalid | key) over end_bit bits
+      need(ck_, n);
+      need(cks_, n);
+      psum::combine_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, n, key, pauli_q, kbits, ck_.p);
+      launched(ctx_);
+      CU(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ck_.p, cks_.p, idx_.p, is_.p, n, 0, end_bit, ctx_->stream));
+      ensure_temp(bytes);
+      {
+        Stage st_s(this, "radixsort");
+        CU(cub::DeviceRadixSort::SortPairs(temp_.p, bytes, ck_.p, cks_.p, idx_.p, is_.p, n, 0, end_bit,
+                                           ctx_->stream));
+      }
+      psum::split_kernel<<<grid(n), 256, 0, ctx_->stream>>>(cks_.p, n, pauli_q, kbits, ks_.p, seg_.p);
+      launched(ctx_), launched(ctx_);
+    } else {
+      CU(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off, off + 1,
+                                                   ctx_->stream));
+      ensure_temp(bytes);
+      {
+        Stage st_s(this, "segsort");
+        CU(cub::DeviceSegmentedSort::StableSortPairs(temp_.p, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off,
+                                                     off + 1, ctx_->stream));
+      }
+      launched(ctx_);
+      psum::seg_of_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, n, seg_.p);
+      launched(ctx_);
+    }
     psum::heads_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ks_.p, seg_.p, n, flag_.p);
-    launched(ctx_), launched(ctx_);
+    launched(ctx_);
     const int nruns = scan_flags(flag_.p, pos_.p, n);
-    rkey_.ensure(std::max(nruns, 1));
-    rval_.ensure(std::max(nruns, 1));
-    rmag_.ensure(std::max(nruns, 1));
-    run_seg_.ensure(std::max(nruns, 1));
-    roff_.ensure(nseg + 1);
+    need(rkey_, std::max(nruns, 1));
+    need(rval_, std::max(nruns, 1));
+    need(rmag_, std::max(nruns, 1));
+    need(run_seg_, std::max(nruns, 1));
+    need(roff_, nseg + 1);
     psum::run_sum_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ks_.p, is_.p, val, seg_.p, flag_.p, pos_.p, n, rkey_.p,
                                                              rval_.p, rmag_.p, run_seg_.p);
     psum::seg_positions_kernel<<<grid(nseg + 1), 256, 0, ctx_->stream>>>(off, nseg, n, pos_.p, nruns, roff_.p);
@@ -273,8 +346,8 @@ private:
       std::swap(out.off.p, roff_.p), std::swap(out.off.n, roff_.n);
       return;
     }
-    keep_flag_.ensure(std::max(nruns, 1));
-    kpos_.ensure(std::max(nruns, 1));
+    need(keep_flag_, std::max(nruns, 1));
+    need(kpos_, std::max(nruns, 1));
     psum::floor_keep_kernel<<<static_cast<unsigned>((nseg + 7) / 8), 256, 0, ctx_->stream>>>(roff_.p, nseg, rmag_.p,
                                                                                         keep_flag_.p);
     launched(ctx_);
@@ -295,18 +368,19 @@ private:
   // basis elements l < n_limit. Returns false when the batch is too large
   // (the caller splits it).
   bool pass(const Segs& in, int n_limit, Segs& out) {
+    Stage st_pass(this, "pass");
     const int n = in.total, nseg = in.nseg;
-    cnt_.ensure(std::max(n, 1));
-    cpos_.ensure(std::max(n, 1));
+    need(cnt_, std::max(n, 1));
+    need(cpos_, std::max(n, 1));
     if (n > 0) {
       psum::beta_count_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ix_, in.key.p, n, n_limit, cnt_.p);
       launched(ctx_);
     }
     const long long nb = n > 0 ? scan_counts(cnt_.p, cpos_.p, n) : 0;
     if (nb > kMaxItems) return false;
-    bl_.ensure(std::max<long long>(nb, 1));
-    bv_.ensure(std::max<long long>(nb, 1));
-    boff_.ensure(nseg + 1);
+    need(bl_, std::max<long long>(nb, 1));
+    need(bv_, std::max<long long>(nb, 1));
+    need(boff_, nseg + 1);
     if (n > 0) {
       psum::beta_fill_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ix_, in.key.p, in.val.p, n, n_limit, cpos_.p, bl_.p,
                                                                 bv_.p);
@@ -315,12 +389,14 @@ private:
     psum::seg_offsets64_kernel<<<grid(nseg + 1), 256, 0, ctx_->stream>>>(in.off.p, nullptr, nseg, n, cpos_.p, nb,
                                                                          boff_.p);
     launched(ctx_);
-    merge(nseg, boff_.p, bl_.p, bv_.p, static_cast<int>(nb), false, beta_);  // beta runs, ascending l per segment
+    int lbits = 1;
+    while ((1ll << lbits) < n_limit) ++lbits;
+    merge(nseg, boff_.p, bl_.p, bv_.p, static_cast<int>(nb), false, beta_, 0, lbits);  // beta runs, ascending l
     const int nruns = beta_.total;
     const int nch = nseg + nruns;
-    chunks_.ensure(std::max(nch, 1));
-    clen_.ensure(std::max(nch, 1));
-    chpos_.ensure(std::max(nch, 1));
+    need(chunks_, std::max(nch, 1));
+    need(clen_, std::max(nch, 1));
+    need(chpos_, std::max(nch, 1));
     psum::chunk_base_kernel<<<grid(nseg), 256, 0, ctx_->stream>>>(in.off.p, beta_.off.p, nseg, chunks_.p, clen_.p);
     launched(ctx_);
     if (nruns > 0) {
@@ -339,7 +415,8 @@ private:
           chunks_.p, chpos_.p, nch, in.key.p, in.val.p, vkey_.p, vval_.p, lc_.key.p, lc_.val.p);
       launched(ctx_);
     }
-    merge(nseg, lc_.off.p, lc_.key.p, lc_.val.p, static_cast<int>(nt), true, out);
+    merge(nseg, lc_.off.p, lc_.key.p, lc_.val.p, static_cast<int>(nt), true, out, static_cast<int>(q_),
+          2 * static_cast<int>(q_));
     return true;
   }
 
@@ -371,7 +448,7 @@ private:
         return;
       }
     }
-    rn_dev_.ensure(h.nseg);
+    need(rn_dev_, h.nseg);
     psum::seg_norm_kernel<<<grid(h.nseg), 256, 0, ctx_->stream>>>(res.off.p, res.nseg, res.val.p, rn_dev_.p);
     launched(ctx_);
     CU(cudaMemcpyAsync(rn.data(), rn_dev_.p, h.nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
@@ -457,6 +534,7 @@ private:
   // accept residual segment k (norm rn) of res; the candidate h_unit is
   // segment hk of h (the original kept by Alg. 3)
   void accept(const Segs& res, int k, double rn, const Segs& h, int hk) {
+    Stage st_acc(this, "accept");
     if (n_ >= cap_)
       throw Error(LIECL_B200_CAPACITY,
                   "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
@@ -545,18 +623,23 @@ private:
       }
       const int cnt = static_cast<int>(poff.size()) - 1;
       // commutators -> merged sums -> norms -> units (K1, R:src/closure.cpp:419-423)
-      poff_.ensure(cnt + 1);
+      need(poff_, cnt + 1);
       CU(cudaMemcpyAsync(poff_.p, poff.data(), poff.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
-      pk_.ensure(std::max<int64_t>(prods, 1));
-      pv_.ensure(std::max<int64_t>(prods, 1));
+      need(pk_, std::max<int64_t>(prods, 1));
+      need(pv_, std::max<int64_t>(prods, 1));
       const int64_t* bdoff = keep_ ? dooff_.p : dvoff_.p;
       const unsigned long long* bkey = keep_ ? okey_.p : vkey_.p;
       const C2* bval = keep_ ? oval_.p : vval_.p;
+      Stage st_p(this, "products");
       psum::products_kernel<<<cnt, 256, 0, ctx_->stream>>>(g0, cnt, poff_.p, bdoff, bkey, bval, pk_.p, pv_.p);
       launched(ctx_);
       Segs& h = h_;
-      merge(cnt, poff_.p, pk_.p, pv_.p, static_cast<int>(prods), true, h);
-      hn_.ensure(cnt);
+      {
+        Stage st_c(this, "commutator");
+        merge(cnt, poff_.p, pk_.p, pv_.p, static_cast<int>(prods), true, h, static_cast<int>(q_),
+              2 * static_cast<int>(q_));
+      }
+      need(hn_, cnt);
       psum::seg_norm_kernel<<<grid(cnt), 256, 0, ctx_->stream>>>(h.off.p, cnt, h.val.p, hn_.p);
       psum::seg_scale_kernel<<<std::min(cnt, 4096), 256, 0, ctx_->stream>>>(h.off.p, cnt, hn_.p, tol_, h.val.p);
       launched(ctx_), launched(ctx_);
@@ -566,9 +649,13 @@ private:
       // speculative checks against the row-start basis
       Segs& res = res_;
       std::vector<double> rn;
-      check(h, n_limit, res, rn);
+      {
+        Stage st_k(this, "check");
+        check(h, n_limit, res, rn);
+      }
       ++st_.batches;
       // ordered apply
+      Stage st_apply(this, "apply");
       int j = 0;
       for (; j < cnt; ++j) {
         int64_t pl, pm;
@@ -584,6 +671,7 @@ private:
         double r = rn[j];
         int rc = 0;
         if (n_ != row_start_n && r > tol_) {  // stale "independent": recompute (R:src/closure.cpp:440-444)
+          Stage st_rc(this, "recheck");
           Segs &one = one_, &rres = rres_;
           std::vector<double> rr;
           subrange(h, j, j + 1, one);
@@ -636,7 +724,7 @@ private:
   DevBuf<int> small_, poff_, seg_, flag_, pos_, run_seg_, roff_, keep_flag_, kpos_, boff_;
   DevBuf<long long> cnt_, cpos_, clen_, chpos_, total_ll_;
   DevBuf<unsigned> idx_, is_;
-  DevBuf<unsigned long long> ks_, rkey_, pk_, bl_;
+  DevBuf<unsigned long long> ks_, rkey_, pk_, bl_, ck_, cks_;
   DevBuf<C2> rval_, pv_, bv_;
   DevBuf<double> rmag_, hn_, rn_dev_;
   DevBuf<psum::Chunk> chunks_;

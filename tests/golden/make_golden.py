@@ -6,7 +6,10 @@ Runs the unmodified liecl sources (oracle/_ref/libliecl_ref.so, built from
 /root/reference (this container only); the fixtures travel, the reference
 does not.
 
-    python tests/golden/make_golden.py [--c2]      (--c2: ~10+ min)
+    python tests/golden/make_golden.py [--c2] [--only-sums]   (--c2: ~10+ min)
+
+Multi-term PauliSum fixtures come from the default-rounding
+build oracle/_ref/libliecl_ref_exact.so (see oracle/Makefile).
 """
 import argparse
 import json
@@ -17,7 +20,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-from oracle.oracle import Ref, build, pauli_single_arrays  # noqa: E402
+from oracle.oracle import REF_EXACT_SO, Ref, build, pauli_single_arrays  # noqa: E402
 from paper_2506_01120_b200 import workloads as w  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -68,11 +71,39 @@ def save(tag, meta, arrays):
     print("wrote", tag, meta.get("dimension"), meta.get("stats"))
 
 
+SUM_CASES = (("tfim_hva_open", 6), ("spin_glass_hva", 3))
+
+
+def sums_cases():
+    refx = Ref(REF_EXACT_SO)
+    for family, n in SUM_CASES:
+        off, x, z, co = refx.build_generators(family, n)
+        for method in ("orthonorm-dimonly", "orthonorm"):
+            full = refx.closure_pauli(off, x, z, co, n, method=method, tol=1e-10)
+            rep = refx.decision_log_pauli(off, x, z, co, n, keep_original=(method == "orthonorm"), tol=1e-10)
+            bo, bx, bz, bc = full.basis
+            ro, rx, rz, rc = rep.basis
+            assert np.array_equal(bo, ro) and np.array_equal(bc.view(np.uint64), rc.view(np.uint64))
+            meta = {"name": f"{family}_n{n}", "method": method, "qubits": n, "tol": 1e-10,
+                    "dimension": int(full.dimension), "build": "libliecl_ref_exact.so",
+                    "stats": {k: int(v) for k, v in full.stats.items() if k not in ("wall_seconds", "extra")},
+                    "warnings": full.warnings}
+            arrays = {"gen_offsets": off, "gen_x": x, "gen_z": z, "gen_coef_bits": co.view(np.uint64),
+                      "offsets": bo, "x": bx, "z": bz, "coef_bits": bc.view(np.uint64),
+                      "log_l": rep.log["l"], "log_m": rep.log["m"], "log_null": rep.log["null_cand"],
+                      "log_indep": rep.log["independent"], "log_rn_bits": rep.log["residual_norm"].view(np.uint64)}
+            save(f"sums_{family}_n{n}_{method}", meta, arrays)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true")
+    ap.add_argument("--only-sums", action="store_true")
     a = ap.parse_args()
     build()
+    sums_cases()
+    if a.only_sums:
+        return
     ref = Ref()
     for cfg in (w.config0(), w.config1()):
         for method in ("orthonorm-dimonly", "orthonorm"):

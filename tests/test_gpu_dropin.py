@@ -63,3 +63,21 @@ def test_dropin_matrix_inversion(demo, ref):
     assert r["commutators_evaluated"] == theirs.stats["commutators_evaluated"]
     assert r["independence_checks"] == theirs.stats["independence_checks"]
     assert r["gram_size"] == 9 and r["inverse_error"] < 1e-10
+
+
+@pytest.mark.parametrize("method", ["orthonorm-dimonly", "orthonorm"])
+def test_dropin_multi_term_pauli_closure(demo, ref_exact, method):
+    # run_closure over multi-term sums through the drop-in: every term's
+    # string and coefficient value equal to the reference build's
+    off, x, z, c = ref_exact.build_generators("tfim_hva_open", 6)
+    o = ref_exact.closure_pauli(off, x, z, c, 6, method=method, tol=1e-10)
+    r = demo[f"tfim6_{method}"]
+    assert r["dimension"] == o.dimension == 36
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert r[k] == o.stats[k]
+    ro, rx, rz, rc = o.basis
+    got = [np.array(s_) for s_ in r["sums"]]
+    assert [len(s_) for s_ in got] == np.diff(ro).tolist()
+    allt = np.concatenate(got)
+    assert np.array_equal(allt[:, 0].astype(np.uint64), rx) and np.array_equal(allt[:, 1].astype(np.uint64), rz)
+    assert np.array_equal(allt[:, 2:], rc)

@@ -119,3 +119,24 @@ def test_small_batches_same_bits(ref):
     for u, v in zip(a.basis_array, b.basis_array):
         assert np.array_equal(np.asarray(u).view(np.uint64), np.asarray(v).view(np.uint64))
     assert b.stats.engine["batches"] > a.stats.engine["batches"]
+
+
+@pytest.mark.parametrize("tag", ["sums_tfim_hva_open_n6_orthonorm-dimonly", "sums_tfim_hva_open_n6_orthonorm",
+                                 "sums_spin_glass_hva_n3_orthonorm-dimonly", "sums_spin_glass_hva_n3_orthonorm"])
+def test_golden_fixtures_bit_exact(golden, tag):
+    # committed fixtures from the reference build: no reference needed at run time
+    meta, g = golden(tag)
+    method = liecl.method_from_string(meta["method"])
+    res = liecl.closure_pauli_sums_arrays(g["gen_offsets"], g["gen_x"], g["gen_z"],
+                                          g["gen_coef_bits"].view(np.float64), meta["qubits"], method,
+                                          liecl.ClosureConfig(tolerance=meta["tol"], record_log=True))
+    assert res.dimension == meta["dimension"]
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(res.stats, k) == meta["stats"][k]
+    bo, bx, bz, bc = res.basis_array
+    assert np.array_equal(bo, g["offsets"]) and np.array_equal(bx, g["x"]) and np.array_equal(bz, g["z"])
+    assert np.array_equal(bc.view(np.uint64), g["coef_bits"])
+    log = res.decision_log
+    assert np.array_equal(log["l"], g["log_l"]) and np.array_equal(log["m"], g["log_m"])
+    assert np.array_equal(log["null_cand"], g["log_null"]) and np.array_equal(log["independent"], g["log_indep"])
+    assert np.array_equal(log["residual_norm"].view(np.uint64), g["log_rn_bits"])

@@ -166,3 +166,15 @@ def test_c2_growth_prefix_port_vs_reference(ref, port):
     assert mine.dimension == rep.dimension
     assert same_verdicts(mine.log, rep.log)
     assert np.abs(mine.basis - rep.basis).max() < 1e-11
+
+
+@pytest.mark.parametrize("tag", ["sums_tfim_hva_open_n6_orthonorm-dimonly", "sums_spin_glass_hva_n3_orthonorm"])
+def test_exact_reference_build_reproduces_sum_fixtures(ref_exact, golden, tag):
+    # the default-rounding reference build (oracle/_ref/libliecl_ref_exact.so)
+    # is deterministic and is what the multi-term fixtures pin
+    meta, g = golden(tag)
+    o = ref_exact.closure_pauli(g["gen_offsets"], g["gen_x"], g["gen_z"], g["gen_coef_bits"].view(np.float64),
+                                meta["qubits"], method=meta["method"], tol=meta["tol"])
+    bo, bx, bz, bc = o.basis
+    assert o.dimension == meta["dimension"]
+    assert np.array_equal(bo, g["offsets"]) and np.array_equal(bc.view(np.uint64), g["coef_bits"])
