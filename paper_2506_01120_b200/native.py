@@ -10,7 +10,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libliecl_b200.so")
+LIB_PATH = os.environ.get("LIECL_B200_LIB") or os.path.join(HERE, "lib", "libliecl_b200.so")  # env: A/B builds
 
 # status codes (include/liecl_b200.h)
 OK, INVALID_INPUT, CAPACITY, DEGENERACY, TIMEOUT, PARSE, CUDA, NOMEM, INTERNAL = 0, 1, 2, 3, 4, 5, 6, 7, 9

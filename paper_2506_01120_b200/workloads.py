@@ -172,6 +172,39 @@ def _dense(name, n, sums, tol=1e-10) -> DenseConfig:
     return DenseConfig(name, n, gens, tol, sums)
 
 
+# ---- the reference's HVA generator catalog (multi-term sums, §8 f2) --------
+
+def tfim_hva_open(n: int) -> list:
+    """R:src/generators.cpp:98-110: H1 = sum_i Z_i Z_{i+1} (open chain), H2 = sum_i X_i."""
+    h1 = PauliSumSpec.from_terms(n, [((0, (1 << i) | (1 << (i + 1))), complex(1.0, 0.0)) for i in range(n - 1)])
+    h2 = PauliSumSpec.from_terms(n, [((1 << i, 0), complex(1.0, 0.0)) for i in range(n)])
+    return [h1, h2]
+
+
+def xxz_hva(n: int, delta: float = 1.5) -> list:
+    """R:src/generators.cpp:81-96: even- and odd-bond XX + YY + delta ZZ on the
+    periodic chain (n even)."""
+    def bond_sum(parity):
+        terms = []
+        for i in range(parity, n, 2):
+            b = (1 << i) | (1 << ((i + 1) % n))
+            terms += [((b, 0), complex(1.0, 0.0)), ((b, b), complex(1.0, 0.0)), ((0, b), complex(delta, 0.0))]
+        return PauliSumSpec.from_terms(n, terms)
+    return [bond_sum(0), bond_sum(1)]
+
+
+def sum_arrays(sums) -> tuple:
+    """(offsets, x, z, coef (t, 2)) of a list of PauliSumSpec, the C-ABI layout."""
+    off, xs, zs, cs = [0], [], [], []
+    for s in sums:
+        xs += list(s.x)
+        zs += list(s.z)
+        cs += [(complex(c).real, complex(c).imag) for c in s.coef]
+        off.append(len(xs))
+    return (np.array(off, np.int64), np.array(xs, np.uint64), np.array(zs, np.uint64),
+            np.array(cs, np.float64).reshape(-1, 2))
+
+
 def config0() -> DenseConfig:
     """n=3 TFIM: i*(X0+X1+X2), i*(Z0Z1+Z1Z2) (BASELINE configs[0])."""
     n = 3
