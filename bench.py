@@ -14,8 +14,9 @@ growth phase on the GPU.
 
   value  : brackets/s, whole job, basis resident in HBM (inputs > L2)
   e2e    : same metric through the C-ABI session with HOST buffers: each step
-           re-uploads the 268 MB basis from pinned memory, runs the window and
-           reads the per-candidate verdict data back
+           uploads its 268 MB basis from pinned memory (the next step's copy
+           is prefetched on a side stream while the current window runs),
+           runs the window and reads the per-candidate verdict data back
   roofline: the projection GEMMs (K2a + K2b, zgemm_dmma) against the FP64
            tensor peak measured in-run (cuBLAS ZGEMM via torch.matmul;
            MEASURED_PEAKS.json has no FP64 figure)
@@ -418,23 +419,27 @@ def run_b200_arm(a):
         sess2 = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol), device=local)
         vptr = host_V.data_ptr()
 
-        def e2e_step(r0, r1):
+        def e2e_step(r0, r1, prefetch_next):
+            # this step's basis: H2D from pinned memory (or the copy the previous
+            # step prefetched on the side stream, which overlapped its window)
             import ctypes as C
             lib = native.load()
             st = lib.liecl_b200_session_set_basis(sess2.ptr, C.cast(C.c_void_p(vptr), C.POINTER(C.c_double)),
                                                   C.c_int64(4095), C.c_int32(0))
             if st:
                 raise RuntimeError(native.last_error())
+            if prefetch_next:  # the next step's input, copied while this window runs
+                sess2.prefetch_basis(vptr, 4095)
             return sess2.run_rows(r0, r1)
         for s in range(a.warmup):
-            e2e_step(*window_rows(s, rank, world, a.row0, a.rows_per_step))
+            e2e_step(*window_rows(s, rank, world, a.row0, a.rows_per_step), prefetch_next=s + 1 < a.warmup)
         barrier()
         torch.cuda.synchronize(device)
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for r0, r1 in windows:
-            e2e_step(r0, r1)
+        for k, (r0, r1) in enumerate(windows):
+            e2e_step(r0, r1, prefetch_next=k + 1 < len(windows))
         f1.record(stream)
         torch.cuda.synchronize(device)
         e2e_ms = max_over_ranks(f0.elapsed_time(f1))
@@ -442,7 +447,8 @@ def run_b200_arm(a):
         e2e = {"value": total_brackets / (e2e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 4095 * DIM * DIM * 16,
                "d2h_bytes_per_step": int(12 * my_brackets / a.steps),
-               "path": "liecl_b200_session_set_basis(host pinned) + liecl_b200_session_run_rows"}
+               "path": "liecl_b200_session_set_basis(host pinned) + liecl_b200_session_run_rows; the next "
+                       "step's basis H2D (liecl_b200_session_prefetch_basis) overlaps the current window"}
 
     # ---- the general complex path on the same windows (for comparison)
     general = None

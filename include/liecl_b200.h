@@ -226,6 +226,12 @@ int liecl_b200_session_create_dense(liecl_b200_ctx* ctx, int32_t d, int32_t keep
                                     const liecl_b200_config* cfg, liecl_b200_session** out);
 void liecl_b200_session_destroy(liecl_b200_session* s);
 int liecl_b200_session_set_basis(liecl_b200_session* s, const double* V, int64_t n, int32_t on_device);
+/* Start copying the host basis V (n operators; pinned memory makes it
+ * asynchronous) to the device on a side stream, overlapping the work in
+ * flight (e.g. the current window); the next set_basis(V, n, on_device = 0)
+ * with the same pointer and count waits for that copy instead of copying.
+ * V must stay unchanged until then. */
+int liecl_b200_session_prefetch_basis(liecl_b200_session* s, const double* V, int64_t n);
 int liecl_b200_session_run_pairs(liecl_b200_session* s, int64_t g_begin, int64_t g_end,
                                  liecl_b200_stats* stats);
 int liecl_b200_session_run_rows(liecl_b200_session* s, int64_t row_begin, int64_t row_end,

@@ -658,14 +658,21 @@ class ClosureSession:
             pass
 
     def set_basis(self, V, on_device: bool = False, n: int | None = None):
-        """V: (n, d*d) complex128 host array, or a device pointer (int) with on_device."""
-        if on_device:
+        """V: (n, width) complex128 host array, or a pointer (int; device memory
+        with on_device, else host -- e.g. pinned memory a prefetch_basis started)."""
+        if on_device or isinstance(V, int):
             _check(self.lib.liecl_b200_session_set_basis(self.ptr, C.cast(C.c_void_p(V), C.POINTER(C.c_double)),
-                                                         C.c_int64(n), C.c_int32(1)))
+                                                         C.c_int64(n), C.c_int32(int(on_device))))
         else:
             V = np.ascontiguousarray(V, np.complex128)
             _check(self.lib.liecl_b200_session_set_basis(self.ptr, _dp(V.view(np.float64)), C.c_int64(len(V)),
                                                          C.c_int32(0)))
+
+    def prefetch_basis(self, V_ptr: int, n: int):
+        """Start the async H2D copy of the host basis at V_ptr (pinned, (n, width)
+        complex128) for the next set_basis(V_ptr, n=n) -- overlaps the current work."""
+        _check(self.lib.liecl_b200_session_prefetch_basis(self.ptr, C.cast(C.c_void_p(V_ptr), C.POINTER(C.c_double)),
+                                                          C.c_int64(n)))
 
     def run_pairs(self, g_begin: int, g_end: int) -> dict:
         st = native.Stats()

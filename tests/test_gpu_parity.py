@@ -352,3 +352,24 @@ def test_sparse_hea_paper_table(port, n):
     bx, bz, bc = res.basis_array
     assert np.array_equal(bx, o.basis[0]) and np.array_equal(bz, o.basis[1])
     assert np.array_equal(bc.view(np.uint64), o.basis[2].view(np.uint64))
+
+
+def test_prefetch_basis_matches_plain_upload():
+    import torch
+    cfg = w.config0()
+    full = liecl.closure_dense_arrays(cfg.generators, cfg.d, liecl.Method.orthonorm_dimonly,
+                                      liecl.ClosureConfig(tolerance=cfg.tol))
+    B = full.basis_array
+    a = torch.from_numpy(B.copy()).pin_memory()
+    b = torch.from_numpy(B[::-1].copy()).pin_memory()
+    s = liecl.ClosureSession(cfg.d, config=liecl.ClosureConfig(tolerance=cfg.tol))
+    s.set_basis(a.data_ptr(), n=len(B))  # host pointer, plain upload
+    assert np.array_equal(s.basis(), B)
+    s.prefetch_basis(b.data_ptr(), len(B))  # consumed by the matching set_basis
+    s.set_basis(b.data_ptr(), n=len(B))
+    assert np.array_equal(s.basis(), B[::-1])
+    s.prefetch_basis(a.data_ptr(), len(B))  # superseded: a different pointer is uploaded normally
+    s.set_basis(B[:5])
+    assert np.array_equal(s.basis(), B[:5])
+    st = s.run_rows(1, 5)
+    assert st["commutators_evaluated"] == 10
