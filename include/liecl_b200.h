@@ -68,6 +68,9 @@ typedef struct {
    * (the reference defaults are 1e-12 and 256; interval 0 = no cadence refresh) */
   double conditioning_floor;
   uint64_t gram_refresh_interval;
+  /* rank method (Alg. 1): ClosureConfig::rank_tolerance (R:include/liecl/closure.hpp:89-91),
+   * relative singular-value threshold; <= 0 selects eps * max(d^2, n+1) */
+  double rank_tolerance;
 } liecl_b200_config;
 
 /* liecl::ClosureStats (R:include/liecl/closure.hpp:63-69) + engine counters */
@@ -129,7 +132,9 @@ int liecl_b200_ctx_kernel_times(liecl_b200_ctx* ctx, liecl_b200_kernel_time* out
  * `cap` operators (ortho_out may be NULL). Warnings are written as lines
  * "kind\tvalue\tdetail\n" (R:include/liecl/closure.hpp:57-61). The decision
  * log is filled when cfg->record_log (log may be NULL otherwise).
- * Other methods return LIECL_B200_INVALID_INPUT (outside the hot path).
+ * LIECL_B200_METHOD_STANDARD_RANK runs the rank method (Alg. 1,
+ * close_standard: ortho_out unused, log residual norms 0 like the reference);
+ * LIECL_B200_METHOD_MATRIX_INVERSION runs Alg. 2 (see closure_dense_gram).
  */
 int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d,
                              int32_t method, const liecl_b200_config* cfg, double* basis_out,

@@ -102,7 +102,8 @@ class Ref:
             raise OracleError(status, self.lib.liecl_ref_last_error().decode())
 
     # -- closures ------------------------------------------------------------
-    def closure_dense(self, gens, d, method="orthonorm-dimonly", tol=1e-10, threads=1, max_dim=0):
+    def closure_dense(self, gens, d, method="orthonorm-dimonly", tol=1e-10, threads=1, max_dim=0, rank_tol=0.0):
+        self.lib.liecl_ref_set_rank_tolerance(C.c_double(rank_tol))
         gens = _c128(gens)
         cap = max_dim or d * d
         basis = np.zeros((cap, d * d), np.complex128)

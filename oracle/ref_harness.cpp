@@ -134,9 +134,12 @@ std::int64_t pauli_out(const OperatorTuple& ops, std::int64_t* offsets, std::uin
   return k;
 }
 
+double g_rank_tolerance = 0.0;  // ClosureConfig::rank_tolerance for the next calls (test knob)
+
 liecl::ClosureConfig make_config(double tol, unsigned threads, std::uint64_t max_dim) {
   liecl::ClosureConfig cfg;
   cfg.tolerance = tol;
+  cfg.rank_tolerance = g_rank_tolerance;
   cfg.threads = threads == 0 ? 1 : threads;
   cfg.max_dim = static_cast<std::size_t>(max_dim);
   return cfg;
@@ -158,6 +161,8 @@ void write_warnings(const liecl::ClosureStats& st, char* buf, std::int64_t len) 
 } // namespace
 
 extern "C" {
+
+void liecl_ref_set_rank_tolerance(double v) { g_rank_tolerance = v; }
 
 struct RefStats {
   std::uint64_t commutators_evaluated;

@@ -13,8 +13,7 @@
 //   to_string / method_from_string (:22-23), basis_listing (:143)
 //   GramState methods, check_matrix_inversion -- host utilities on the
 //       caller's own state (the closure builds its state on the GPU)
-//   close_standard (rank method, Alg. 1) -- off the hot path: raises
-//       InvalidInputError instead of silently running a CPU fallback.
+//   close_standard             (:108-109)  rank method (Alg. 1) -> GPU (dense)
 //
 // Status codes of the C-ABI map back onto the reference's exception types
 // (R:include/liecl/errors.hpp:10-61).
@@ -65,6 +64,9 @@ liecl_b200_config to_native(const ClosureConfig& c) {
   n.threads = c.threads;
   n.record_log = 0;
   n.batch_max = 0;
+  n.conditioning_floor = c.conditioning_floor;
+  n.gram_refresh_interval = c.gram_refresh_interval;
+  n.rank_tolerance = c.rank_tolerance;
   if (c.deadline) {
     const double rel = std::chrono::duration<double>(*c.deadline - std::chrono::steady_clock::now()).count();
     n.deadline_seconds = rel > 0 ? rel : 1e-9;
@@ -355,7 +357,50 @@ double GramState::inverse_error() const {
   return ((gram_ * inverse_) - Eigen::MatrixXcd::Identity(gram_.rows(), gram_.cols())).cwiseAbs().maxCoeff();
 }
 
-ClosureResult close_standard(std::span<const Operator>, const ClosureConfig&) { off_path("close_standard"); }
+// Alg. 1, the rank method (R:src/closure.cpp:500-517) on the GPU: rank of
+// [B | vec(h)] from the singular values of the small triangular factor
+ClosureResult close_standard(std::span<const Operator> generators, const ClosureConfig& config) {
+  const std::optional<Backend> backend = validate(generators);
+  if (backend && *backend != Backend::dense)
+    throw InvalidInputError("close_standard requires the dense backend; the rank check vectorizes operators");
+  Eigen::Index d = 0;
+  for (const Operator& g : generators)
+    if (!g.is_null()) d = g.dim();
+  ClosureResult r;
+  r.method = Method::standard_rank;
+  r.backend = Backend::dense;
+  r.tolerance = config.tolerance;
+  if (d == 0) {  // every generator null
+    for (size_t i = 0; i < generators.size(); ++i)
+      r.stats.warnings.push_back({"null_generator",
+                                  "generator " + std::to_string(i) + " has norm " + std::to_string(0.0) +
+                                      " and was skipped",
+                                  0.0});
+    return r;
+  }
+  const size_t D = static_cast<size_t>(d) * d;
+  std::vector<double> gens(2 * D * generators.size(), 0.0);
+  for (size_t i = 0; i < generators.size(); ++i)
+    if (!generators[i].is_null())
+      std::memcpy(gens.data() + 2 * D * i, generators[i].dense().matrix().data(), sizeof(double) * 2 * D);
+  const size_t cap = config.max_dim ? config.max_dim : D;
+  std::vector<double> basis(2 * D * cap);
+  liecl_b200_stats st{};
+  std::vector<char> wbuf(1 << 20);
+  const liecl_b200_config cfg = to_native(config);
+  check(liecl_b200_closure_dense(context(), gens.data(), static_cast<int32_t>(generators.size()),
+                                 static_cast<int32_t>(d), LIECL_B200_METHOD_STANDARD_RANK, &cfg, basis.data(), nullptr,
+                                 static_cast<int64_t>(cap), &st, wbuf.data(), static_cast<int64_t>(wbuf.size()),
+                                 nullptr, 0, nullptr));
+  for (size_t k = 0; k < st.dimension; ++k) {
+    Eigen::MatrixXcd m(d, d);
+    std::memcpy(static_cast<void*>(m.data()), basis.data() + 2 * D * k, sizeof(double) * 2 * D);
+    r.basis.emplace_back(DenseOperator(std::move(m)));
+  }
+  r.dimension = st.dimension;
+  fill_stats(r, st, wbuf);
+  return r;
+}
 
 // Alg. 2 (R:src/closure.cpp:519-527) on the GPU for dense generators
 ClosureResult close_matrix_inversion(std::span<const Operator> generators, const ClosureConfig& config) {
@@ -449,7 +494,7 @@ ClosureResult close_orthonormalization(std::span<const Operator> generators, con
 
 ClosureResult run_closure(std::span<const Operator> generators, Method method, const ClosureConfig& config) {
   switch (method) {
-  case Method::standard_rank: off_path("run_closure(standard-rank)");
+  case Method::standard_rank: return close_standard(generators, config);
   case Method::matrix_inversion: return close_matrix_inversion(generators, config);
   case Method::orthonorm: return close_orthonormalization(generators, config, true);
   case Method::orthonorm_dimonly: return close_orthonormalization(generators, config, false);

@@ -36,7 +36,7 @@ int main() {
     for (std::uint32_t j = 0; j + 1 < n; ++j) t1.push_back({PauliString{0, (1ull << j) | (1ull << (j + 1)), n}, I});
     const std::vector<Operator> gens{Operator(from_pauli(PauliSum::from_terms(n, t0))),
                                      Operator(from_pauli(PauliSum::from_terms(n, t1)))};
-    for (const Method m : {Method::orthonorm_dimonly, Method::orthonorm}) {
+    for (const Method m : {Method::orthonorm_dimonly, Method::orthonorm, Method::standard_rank}) {
       const ClosureResult r = run_closure(gens, m, cfg);
       std::printf("\"c0_%s\": ", to_string(m).c_str());
       print_stats(r);

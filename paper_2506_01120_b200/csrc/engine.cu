@@ -449,6 +449,7 @@ void launch_commutator_complex(liecl_b200_ctx* ctx, const double2* basis, int d,
 #include "shard.cuh"
 #include "dense_engine.cuh"
 #include "gram_engine.cuh"
+#include "rank_engine.cuh"
 
 // --------------------------------------------------------- Pauli engine ---
 
@@ -786,13 +787,29 @@ liecl_b200_config default_config(const liecl_b200_config* cfg) {
 bool keep_for(int method) {
   if (method == LIECL_B200_METHOD_ORTHONORM) return true;
   if (method == LIECL_B200_METHOD_ORTHONORM_DIMONLY) return false;
-  if (method == LIECL_B200_METHOD_STANDARD_RANK || method == LIECL_B200_METHOD_MATRIX_INVERSION)
+  if (method == LIECL_B200_METHOD_STANDARD_RANK)  // R:src/closure.cpp:502-505
     throw Error(LIECL_B200_INVALID_INPUT,
-                "method not on the B200 hot path (orthonorm / orthonorm-dimonly only)");
+                "close_standard requires the dense backend; the rank check vectorizes operators");
+  if (method == LIECL_B200_METHOD_MATRIX_INVERSION)
+    throw Error(LIECL_B200_INVALID_INPUT, "matrix-inversion on the B200 path takes dense generators");
   throw Error(LIECL_B200_INVALID_INPUT, "run_closure: unknown method");
 }
 
 void use_device(liecl_b200_ctx* ctx) { CU(cudaSetDevice(ctx->device)); }
+
+// close_standard (R:src/closure.cpp:500-517) on the RankEngine
+void run_rank_closure(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d, const liecl_b200_config& cfg,
+                      double* basis_out, int64_t cap, liecl_b200_stats* stats, char* warnings, int64_t warnings_len,
+                      liecl_b200_decision* log, int64_t log_cap, int64_t* log_len) {
+  RankEngine eng(ctx, d, cfg);
+  eng.run_generators(reinterpret_cast<const double2*>(gens), ngens);
+  eng.run_closure_pairs();
+  *stats = eng.stats();
+  write_warnings(eng.warnings(), warnings, warnings_len);
+  copy_log(eng.log(), log, log_cap, log_len);
+  if (eng.size() > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
+  eng.download_basis(basis_out);
+}
 
 // close_matrix_inversion (R:src/closure.cpp:519-527) on the GramEngine
 void run_gram_closure(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d, const liecl_b200_config& cfg,
@@ -900,6 +917,12 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
     if (method == LIECL_B200_METHOD_MATRIX_INVERSION) {
       run_gram_closure(ctx, gens, ngens, d, cfg, basis_out, cap, nullptr, nullptr, stats, warnings, warnings_len, log,
                        log_cap, log_len);
+      stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+      return;
+    }
+    if (method == LIECL_B200_METHOD_STANDARD_RANK) {
+      run_rank_closure(ctx, gens, ngens, d, cfg, basis_out, cap, stats, warnings, warnings_len, log, log_cap,
+                       log_len);
       stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
       return;
     }

@@ -1,0 +1,353 @@
+// RankEngine -- the rank strategy (Alg. 1) on the B200:
+// RankStrategy + rank_independence_check (R:src/closure.cpp:185-212, 500-517;
+// R:src/dense.cpp:119-147) inside the same batched cursor loop as the other
+// engines. Included by engine.cu inside its anonymous namespace.
+//
+// The reference stacks vec(B_1..B_n, h) into a d^2 x (n+1) matrix S, takes
+// its singular values (BDCSVD) and calls h independent iff all n+1 exceed
+// thr * sigma_max, thr = rank_tolerance or eps * max(d^2, n+1). Here S is
+// never formed: the engine keeps an orthonormal tuple V and the triangular
+// factor R with B = V R (the accepted columns' CGS2 coefficients), so
+//   S = [B | h] = [V | r/rho] * T,   T = [[R, beta], [0, rho]],
+// beta = beta_1 + beta_2 (both projection passes), rho = ||h - V beta||.
+// S and T share their singular values (the left factor has orthonormal
+// columns); T is (n+1) x (n+1). One CTA per candidate runs a one-sided
+// (Hestenes) Jacobi SVD on T -- high relative accuracy -- and counts. The
+// relative threshold is invariant under the 1/sqrt(d) scaling of the
+// reference inner product that V and R use.
+
+// T of candidate j (m = n + 1 columns, m_pad even, column-major in W_j):
+// columns < n from R (upper triangle, ld ldr), column n = (beta_j, rho_j),
+// padding column zero.
+__global__ void rank_build_t_kernel(const double2* __restrict__ R, int64_t ldr, int n, const double2* __restrict__ beta,
+                                    int64_t ldb, const double* __restrict__ rho, int m_pad, double2* __restrict__ W) {
+  const int j = blockIdx.y;
+  double2* T = W + static_cast<int64_t>(j) * m_pad * m_pad;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < static_cast<int64_t>(m_pad) * m_pad;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e % m_pad), k = static_cast<int>(e / m_pad);
+    double2 v = make_double2(0.0, 0.0);
+    if (k < n) {
+      if (i <= k) v = R[i + k * ldr];
+    } else if (k == n) {
+      if (i < n) v = beta[i + j * ldb];
+      else if (i == n) v = make_double2(rho[j], 0.0);
+    }
+    T[e] = v;
+  }
+}
+
+// One-sided Jacobi on the m_pad columns of T_j (one CTA, round-robin
+// tournament: the m_pad/2 disjoint pairs of a step go to the warps in
+// parallel). Writes indep[j] = (#sigma > thr * sigma_max == m) and the
+// extreme singular values.
+__global__ void rank_jacobi_kernel(double2* __restrict__ W, int m, int m_pad, double thr, int max_sweeps,
+                                   int* __restrict__ indep, double* __restrict__ smin, double* __restrict__ smax) {
+  extern __shared__ double s_norm2[];  // m_pad column norms^2
+  __shared__ int s_rot;
+  const int j = blockIdx.x;
+  double2* T = W + static_cast<int64_t>(j) * m_pad * m_pad;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const double eps = 2.220446049250313e-16;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) s_rot = 0;
+    __syncthreads();
+    for (int step = 0; step < m_pad - 1; ++step) {
+      for (int pr = warp; pr < m_pad / 2; pr += nwarps) {
+        // round-robin: position 0 fixed, the others rotate
+        const int a = pr == 0 ? 0 : 1 + (pr - 1 + step) % (m_pad - 1);
+        const int b = 1 + (m_pad - 2 - pr + step) % (m_pad - 1);
+        const int p = min(a, b), q = max(a, b);
+        double2* tp = T + static_cast<int64_t>(p) * m_pad;
+        double2* tq = T + static_cast<int64_t>(q) * m_pad;
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        for (int i = lane; i < m_pad; i += 32) {
+          const double2 u = tp[i], v = tq[i];
+          al += u.x * u.x + u.y * u.y;
+          be += v.x * v.x + v.y * v.y;
+          gr += u.x * v.x + u.y * v.y;  // conj(u) * v
+          gi += u.x * v.y - u.y * v.x;
+        }
+        al = warp_sum(al), be = warp_sum(be), gr = warp_sum(gr), gi = warp_sum(gi);
+        const double g = sqrt(gr * gr + gi * gi);
+        if (g == 0.0 || g <= eps * sqrt(al * be)) continue;  // already orthogonal
+        if (lane == 0) s_rot = 1;
+        const double cph = gr / g, sph = gi / g;  // e^{i phi} = gamma / |gamma|
+        const double zeta = (be - al) / (2.0 * g);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        for (int i = lane; i < m_pad; i += 32) {
+          const double2 u = tp[i], v0 = tq[i];
+          const double2 v = make_double2(cph * v0.x + sph * v0.y, cph * v0.y - sph * v0.x);  // e^{-i phi} v
+          tp[i] = make_double2(c * u.x - s * v.x, c * u.y - s * v.y);
+          tq[i] = make_double2(s * u.x + c * v.x, s * u.y + c * v.y);
+        }
+      }
+      __syncthreads();
+    }
+    const int rotated = s_rot;
+    __syncthreads();
+    if (!rotated) break;
+  }
+  for (int k = warp; k < m_pad; k += nwarps) {
+    const double2* tk = T + static_cast<int64_t>(k) * m_pad;
+    double a = 0.0;
+    for (int i = lane; i < m_pad; i += 32) a += tk[i].x * tk[i].x + tk[i].y * tk[i].y;
+    a = warp_sum(a);
+    if (lane == 0) s_norm2[k] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int k = 0; k < m_pad; ++k) mx = fmax(mx, sqrt(s_norm2[k]));
+    int rank = 0;
+    double mn = mx;
+    for (int k = 0; k < m_pad; ++k) {
+      const double sv = sqrt(s_norm2[k]);
+      if (sv > thr * mx) ++rank;
+      if (k < m) mn = fmin(mn, sv);
+    }
+    indep[j] = rank == m;
+    smin[j] = mn;
+    smax[j] = mx;
+  }
+}
+
+__global__ void add_columns_kernel(double2* __restrict__ acc, const double2* __restrict__ add, int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    acc[e] = make_double2(acc[e].x + add[e].x, acc[e].y + add[e].y);
+}
+
+// R column n = (beta, rho)
+__global__ void rank_append_r_kernel(double2* __restrict__ R, int64_t ldr, int n, const double2* __restrict__ beta,
+                                     const double* __restrict__ rho) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
+    R[i + static_cast<int64_t>(n) * ldr] = i < n ? beta[i] : make_double2(*rho, 0.0);
+}
+
+class RankEngine {
+public:
+  RankEngine(liecl_b200_ctx* ctx, int d, const liecl_b200_config& cfg)
+      : ctx_(ctx), d_(d), D_(static_cast<int64_t>(d) * d), tol_(cfg.tolerance), rank_tol_(cfg.rank_tolerance),
+        record_(cfg.record_log != 0) {
+    if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
+    if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
+    cap_ = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : D_;
+    bmax_ = cfg.batch_max > 0 ? cfg.batch_max : std::clamp<int64_t>((int64_t(4) << 30) / (3 * D_ * 16), 16, 1024);
+    if (cfg.deadline_seconds > 0) {
+      has_deadline_ = true;
+      deadline_ = Clock::now() + std::chrono::duration_cast<Clock::duration>(
+                                     std::chrono::duration<double>(cfg.deadline_seconds));
+    }
+    sqrt_d_ = std::sqrt(static_cast<double>(d));
+    const int64_t slots = cap_ + 1;
+    B_.ensure(static_cast<size_t>(slots * D_));
+    V_.ensure(static_cast<size_t>(slots * D_));
+    R_.ensure(static_cast<size_t>(slots * slots));
+    C_.ensure(static_cast<size_t>(bmax_ * D_));
+    X_.ensure(static_cast<size_t>(bmax_ * D_));
+    P1_.ensure(static_cast<size_t>(slots * bmax_));
+    P2_.ensure(static_cast<size_t>(slots * bmax_));
+    partial_.ensure(static_cast<size_t>(((D_ + zg::BM - 1) / zg::BM) * bmax_));
+    rn_.ensure(bmax_); hn_.ensure(bmax_); nul_.ensure(bmax_); ind_.ensure(bmax_); smin_.ensure(bmax_);
+    smax_.ensure(bmax_);
+    h_hn_.ensure(bmax_); h_nul_.ensure(bmax_); h_ind_.ensure(bmax_); h_one_.ensure(2);
+  }
+
+  int64_t size() const { return n_; }
+  liecl_b200_stats stats() {
+    liecl_b200_stats s = st_;
+    s.dimension = static_cast<uint64_t>(n_);
+    s.warnings = warns_.size();
+    s.kernels = ctx_->kernels - kernels0_;
+    return s;
+  }
+  const std::vector<Warning>& warnings() const { return warns_; }
+  const std::vector<liecl_b200_decision>& log() const { return log_; }
+
+  void run_generators(const double2* gens, int ngens) {
+    kernels0_ = ctx_->kernels;
+    for (int64_t c0 = 0; c0 < ngens; c0 += bmax_) {
+      const int cnt = static_cast<int>(std::min<int64_t>(bmax_, ngens - c0));
+      CU(cudaMemcpyAsync(X_.p, gens + c0 * D_, static_cast<size_t>(cnt * D_) * sizeof(double2),
+                         cudaMemcpyHostToDevice, ctx_->stream));
+      column_norm_kernel<<<cnt, 256, 0, ctx_->stream>>>(X_.p, D_, sqrt_d_, hn_.p);
+      launched(ctx_);
+      dim3 g2(static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 64)), cnt);
+      scale_columns_kernel<<<g2, 256, 0, ctx_->stream>>>(X_.p, hn_.p, tol_, D_, C_.p);
+      launched(ctx_);
+      check(C_.p, cnt, X_.p, P1_.p, rn_.p, ind_.p);
+      CU(cudaMemcpyAsync(h_hn_.p, hn_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      for (int j = 0; j < cnt; ++j) h_nul_.p[j] = !(h_hn_.p[j] > tol_);
+      ++st_.batches;
+      apply(cnt, -1, c0, true);
+    }
+  }
+
+  void run_closure_pairs() {
+    int64_t g = 0;
+    for (;;) {
+      const int64_t avail = n_ * (n_ - 1) / 2;
+      if (g >= avail) break;
+      if (has_deadline_ && Clock::now() > deadline_)
+        throw Error(LIECL_B200_TIMEOUT, "closure computation exceeded its deadline");
+      const int cnt = static_cast<int>(std::min<int64_t>(batch_limit(), avail - g));
+      launch_commutator_complex(ctx_, B_.p, d_, g, cnt, tol_, C_.p, hn_.p, nul_.p);
+      check(C_.p, cnt, X_.p, P1_.p, rn_.p, ind_.p);
+      CU(cudaMemcpyAsync(h_nul_.p, nul_.p, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      st_.commutators_evaluated += static_cast<uint64_t>(cnt);
+      ++st_.batches;
+      apply(cnt, g, 0, false);
+      g += cnt;
+    }
+  }
+
+  void download_basis(double* out) {
+    if (n_ == 0) return;
+    CU(cudaMemcpyAsync(out, B_.p, static_cast<size_t>(n_ * D_) * sizeof(double2), cudaMemcpyDeviceToHost,
+                       ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+  }
+
+private:
+  int64_t ldr() const { return cap_ + 1; }
+  int m_pad() const { return static_cast<int>((n_ + 2) & ~int64_t(1)); }
+  // candidates per batch: the T matrices (m_pad^2 complex each) within 1 GB
+  int64_t batch_limit() const {
+    const int64_t m = m_pad();
+    return std::clamp<int64_t>((int64_t(1) << 30) / (m * m * 16), 1, bmax_);
+  }
+  double threshold() const {  // R:src/dense.cpp:133-137
+    return rank_tol_ > 0.0 ? rank_tol_ : 2.220446049250313e-16 * static_cast<double>(std::max<int64_t>(D_, n_ + 1));
+  }
+
+  // rank verdicts of cnt unit candidates (columns of Cc) against the current
+  // state -> ind (device) and h_ind_; residuals -> Xo, beta_1 + beta_2 ->
+  // Pacc (ld n), their norms -> rho
+  void check(const double2* Cc, int cnt, double2* Xo, double2* Pacc, double* rho, int* ind) {
+    const int m = static_cast<int>(n_ + 1), mp = m_pad();
+    W_.ensure(static_cast<size_t>(cnt) * mp * mp);
+    if (n_ == 0) {
+      column_norm_kernel<<<cnt, 256, 0, ctx_->stream>>>(Cc, D_, sqrt_d_, rho);
+      launched(ctx_);
+      CU(cudaMemcpyAsync(Xo, Cc, static_cast<size_t>(cnt * D_) * sizeof(double2), cudaMemcpyDeviceToDevice,
+                         ctx_->stream));
+    } else {
+      // two CGS passes; T's last column collects both passes' coefficients
+      P2_.ensure(static_cast<size_t>(n_) * cnt);
+      gemm_project(ctx_, V_.p, n_, D_, Cc, cnt, Pacc, 1.0 / d_);
+      gemm_subtract(ctx_, V_.p, n_, D_, Pacc, Cc, cnt, Xo, partial_.p);
+      gemm_project(ctx_, V_.p, n_, D_, Xo, cnt, P2_.p, 1.0 / d_);
+      gemm_subtract(ctx_, V_.p, n_, D_, P2_.p, Xo, cnt, Xo, partial_.p);
+      const int mtiles = static_cast<int>((D_ + zg::BM - 1) / zg::BM);
+      norm_finalize_kernel<<<(cnt + 255) / 256, 256, 0, ctx_->stream>>>(partial_.p, mtiles, cnt, sqrt_d_, rho);
+      add_columns_kernel<<<grid_for(n_ * cnt), 256, 0, ctx_->stream>>>(Pacc, P2_.p, n_ * cnt);
+      launched(ctx_), launched(ctx_);
+    }
+    dim3 gb(static_cast<unsigned>(std::min<int64_t>((static_cast<int64_t>(mp) * mp + 255) / 256, 256)), cnt);
+    rank_build_t_kernel<<<gb, 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), Pacc, n_, rho, mp, W_.p);
+    rank_jacobi_kernel<<<cnt, 256, static_cast<size_t>(mp) * sizeof(double), ctx_->stream>>>(
+        W_.p, m, mp, threshold(), 60, ind, smin_.p, smax_.p);
+    launched(ctx_), launched(ctx_);
+    CU(cudaMemcpyAsync(h_ind_.p, ind, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+  }
+  static unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::clamp<int64_t>((n + 255) / 256, 1, 4096)); }
+
+  std::string where_str(int64_t l, int64_t m) const {
+    return m < 0 ? "generator " + std::to_string(l) : "pair (" + std::to_string(l) + "," + std::to_string(m) + ")";
+  }
+
+  // verdicts in cursor order (R:src/closure.cpp:440-444): a stale
+  // "independent" after an in-batch accept is re-run against the current
+  // state; "dependent" stands. The rank check has no residual scale: the log
+  // carries 0 like the reference's outcome.
+  void apply(int cnt, int64_t pair_g0, int64_t cand0, bool generators) {
+    const int64_t n_bs = n_;
+    std::vector<int> ind(h_ind_.p, h_ind_.p + cnt);
+    for (int j = 0; j < cnt; ++j) {
+      int64_t l, m;
+      if (pair_g0 >= 0) pair_from_index(pair_g0 + j, l, m);
+      else { l = cand0 + j; m = -1; }
+      if (h_nul_.p[j]) {
+        if (generators)
+          warns_.push_back({"null_generator",
+                            "generator " + std::to_string(l) + " has norm " + fmt_double(h_hn_.p[j]) +
+                                " and was skipped",
+                            h_hn_.p[j]});
+        if (record_) log_.push_back({l, m, 1, 0, 0, 0, generators ? h_hn_.p[j] : 0.0});
+        continue;
+      }
+      ++st_.independence_checks;
+      const double2* h = C_.p + static_cast<int64_t>(j) * D_;
+      bool indep = ind[j] != 0;
+      int rc = 0;
+      const double2* resid = X_.p + static_cast<int64_t>(j) * D_;
+      const double2* beta = P1_.p + j * n_bs;
+      const double* rho = rn_.p + j;
+      if (n_ != n_bs && indep) {  // stale "independent": recompute against the current state
+        Y_.ensure(static_cast<size_t>(D_));
+        CU(cudaMemcpyAsync(Y_.p, h, D_ * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
+        recheck(Y_.p);
+        indep = h_ind_.p[0] != 0;
+        resid = Xr_.p;
+        beta = Pr_.p;
+        rho = rnr_.p;
+        rc = 1;
+        ++st_.rechecks;
+      }
+      if (record_) log_.push_back({l, m, 0, indep ? 1 : 0, rc, 0, 0.0});
+      if (!indep) continue;
+      if (n_ >= cap_)
+        throw Error(LIECL_B200_CAPACITY,
+                    "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
+      accept(h, resid, beta, rho);
+    }
+  }
+
+  // single-candidate check against the current state into the recheck buffers
+  void recheck(const double2* h) {
+    Xr_.ensure(static_cast<size_t>(D_));
+    Pr_.ensure(static_cast<size_t>(std::max<int64_t>(n_, 1)));
+    rnr_.ensure(1);
+    indr_.ensure(1);
+    check(h, 1, Xr_.p, Pr_.p, rnr_.p, indr_.p);
+  }
+
+  // RankStrategy::accept (R:src/closure.cpp:200-203): B gets h; V and R grow
+  // with the CGS2 residual (rho = 0 cannot be accepted: sigma_min <= rho)
+  void accept(const double2* h, const double2* resid, const double2* beta, const double* rho) {
+    CU(cudaMemcpyAsync(B_.p + n_ * D_, h, D_ * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
+    CU(cudaMemcpyAsync(h_one_.p, rho, sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    const double r = h_one_.p[0];
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 256));
+    append_scaled_kernel<<<blocks, 256, 0, ctx_->stream>>>(resid, 1.0 / r, D_, V_.p + n_ * D_, nullptr, nullptr);
+    rank_append_r_kernel<<<grid_for(n_ + 1), 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), beta, rho);
+    launched(ctx_), launched(ctx_);
+    ++n_;
+    ++st_.accepted;
+  }
+
+  liecl_b200_ctx* ctx_;
+  int d_;
+  int64_t D_;
+  double tol_, rank_tol_;
+  bool record_;
+  int64_t cap_ = 0, bmax_ = 0, n_ = 0;
+  uint64_t kernels0_ = 0;
+  double sqrt_d_ = 1.0;
+  bool has_deadline_ = false;
+  Clock::time_point deadline_{};
+  liecl_b200_stats st_{};
+  std::vector<Warning> warns_;
+  std::vector<liecl_b200_decision> log_;
+  DevBuf<double2> B_, V_, R_, C_, X_, Y_, P1_, P2_, W_, Xr_, Pr_;
+  DevBuf<double> partial_, rn_, hn_, smin_, smax_, rnr_;
+  DevBuf<int> nul_, ind_, indr_;
+  HostBuf<double> h_hn_, h_one_;
+  HostBuf<int> h_nul_, h_ind_;
+};

@@ -196,7 +196,8 @@ class ClosureConfig:
             raise InvalidInputError(f"unknown field '{self.field}' (expected auto or complex)")
         return native.Config(float(self.tolerance), int(self.max_dim), int(self.threads), int(self.record_log),
                              rel, int(self.batch_max), 1 if self.field == "complex" else 0, 0,
-                             float(self.conditioning_floor), int(self.gram_refresh_interval))
+                             float(self.conditioning_floor), int(self.gram_refresh_interval),
+                             float(self.rank_tolerance))
 
 
 @dataclass
@@ -281,7 +282,7 @@ def closure_dense_arrays(gens: np.ndarray, d: int, method: Method = Method.ortho
     stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds, warnings,
                          {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
     b = basis[:n]
-    o = ortho[:n] if ortho is not None else b
+    o = ortho[:n] if ortho is not None else (b[:0] if method == Method.standard_rank else b)
     return ClosureResult([DenseOperator.from_vec(v, d) for v in b], [DenseOperator.from_vec(v, d) for v in o], n,
                          method, Backend.dense, config.tolerance, stats,
                          log[: log_len.value].copy() if config.record_log else None, b, o)
@@ -415,9 +416,9 @@ def closure_pauli_sums_arrays(offsets, x, z, coef, qubits: int, method: Method =
 def run_closure(generators, method: Method, config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
     """R:src/closure.cpp:541-564: orthonormal methods (dense, single-string
     and multi-term Pauli) and matrix inversion (dense)."""
-    if method == Method.standard_rank:
-        raise InvalidInputError(f"{to_string(method)}: not on the B200 hot path")
     backend, dim = _validate(generators)
+    if method == Method.standard_rank and backend != Backend.dense:
+        raise InvalidInputError("close_standard requires the dense backend; the rank check vectorizes operators")
     if method == Method.matrix_inversion and backend != Backend.dense:
         raise InvalidInputError("matrix-inversion on the B200 path takes dense generators")
     if backend == Backend.dense:

@@ -44,7 +44,7 @@ class Config(C.Structure):
     _fields_ = [("tolerance", C.c_double), ("max_dim", C.c_uint64), ("threads", C.c_uint32),
                 ("record_log", C.c_uint32), ("deadline_seconds", C.c_double), ("batch_max", C.c_int64),
                 ("field", C.c_uint32), ("reserved", C.c_uint32), ("conditioning_floor", C.c_double),
-                ("gram_refresh_interval", C.c_uint64)]
+                ("gram_refresh_interval", C.c_uint64), ("rank_tolerance", C.c_double)]
 
 
 class Stats(C.Structure):
@@ -63,7 +63,7 @@ class Decision(C.Structure):
 
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()  # context() reports errors through load()
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:

@@ -61,8 +61,8 @@ def test_validation_errors_before_device():
     b = liecl.DenseOperator(np.eye(4))
     with pytest.raises(liecl.InvalidInputError):
         liecl.run_closure([a, b], liecl.Method.orthonorm_dimonly)
-    with pytest.raises(liecl.InvalidInputError):
-        liecl.run_closure([a], liecl.Method.standard_rank)
+    with pytest.raises(liecl.InvalidInputError):  # the rank method vectorizes dense operators only
+        liecl.run_closure([liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)], liecl.Method.standard_rank)
 
 
 def test_pair_index_roundtrip():
@@ -96,3 +96,13 @@ def test_shard_range_partitions_every_operator():
             assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
     with pytest.raises(liecl.InvalidInputError):
         liecl.shard_range(2, 5, 0)
+
+
+def test_no_device_fails_loudly_without_deadlock():
+    # no GPU here: the product path must raise (never fall back to the CPU)
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    import numpy as np
+    with pytest.raises((native.NativeUnavailable, liecl.Error)):
+        liecl.run_closure([liecl.DenseOperator(np.eye(2))], liecl.Method.standard_rank)

@@ -81,3 +81,16 @@ def test_dropin_multi_term_pauli_closure(demo, ref_exact, method):
     allt = np.concatenate(got)
     assert np.array_equal(allt[:, 0].astype(np.uint64), rx) and np.array_equal(allt[:, 1].astype(np.uint64), rz)
     assert np.array_equal(allt[:, 2:], rc)
+
+
+def test_dropin_rank_method(demo, ref):
+    # close_standard (Alg. 1) through the drop-in: same closure as the reference
+    from paper_2506_01120_b200 import workloads as w
+    cfg = w.config0()
+    theirs = ref.closure_dense(cfg.generators, cfg.d, method="standard-rank", tol=cfg.tol)
+    r = demo["c0_standard-rank"]
+    assert r["dimension"] == theirs.dimension == 9
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert r[k] == theirs.stats[k]
+    basis = np.array(r["basis"]).reshape(9, -1, 2)
+    assert np.abs(basis[..., 0] + 1j * basis[..., 1] - theirs.basis).max() < 1e-10

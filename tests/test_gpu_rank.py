@@ -1,0 +1,66 @@
+"""Rank method (Alg. 1) on the GPU against the reference
+build (oracle/_ref runs the reference's own RankStrategy: BDCSVD of the
+stacked d^2 x (n+1) matrix, R:src/closure.cpp:185-212, R:src/dense.cpp:119-147).
+The GPU takes the singular values of the (n+1) x (n+1) triangular factor of
+the same matrix; verdicts, statistics and the accepted basis must agree."""
+import numpy as np
+import pytest
+
+from paper_2506_01120_b200 import liecl
+from paper_2506_01120_b200 import workloads as w
+
+pytestmark = pytest.mark.gpu
+RANK = liecl.Method.standard_rank
+
+
+def compare(ref, gens, d, tol=1e-10, rank_tol=0.0):
+    mine = liecl.closure_dense_arrays(gens, d, RANK, liecl.ClosureConfig(tolerance=tol, rank_tolerance=rank_tol,
+                                                                         record_log=True))
+    theirs = ref.closure_dense(gens, d, method="standard-rank", tol=tol, rank_tol=rank_tol)
+    assert mine.dimension == theirs.dimension
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(mine.stats, k) == theirs.stats[k], k
+    # the basis is the accepted unit candidates, in order
+    err = np.abs(mine.basis_array - theirs.basis).max() / max(np.abs(theirs.basis).max(), 1e-300)
+    assert err < 1e-10
+    kinds = sorted(line.split("\t")[0] for line in theirs.warnings.splitlines() if line)
+    assert sorted(wr.kind for wr in mine.stats.warnings) == kinds
+    assert mine.orthonormal_basis == []  # RankStrategy::finalize sets only result.basis
+    assert (mine.decision_log["residual_norm"] == 0).all()  # no residual scale (R:src/closure.cpp:194-195)
+    return mine
+
+
+def dense_family(ref, family, n, scale=1j):
+    off, x, z, c = ref.build_generators(family, n)
+    return np.stack([scale * ref.from_pauli(x[off[i]:off[i + 1]], z[off[i]:off[i + 1]], c[off[i]:off[i + 1]], n)
+                     for i in range(len(off) - 1)])
+
+
+@pytest.mark.parametrize("make", [w.config0, w.config1], ids=["c0", "c1"])
+def test_rank_method_configs_match_reference(ref, make):
+    cfg = make()
+    res = compare(ref, cfg.generators, cfg.d, cfg.tol)
+    assert res.dimension == {"c0_tfim_n3": 9}.get(cfg.name, res.dimension)
+
+
+@pytest.mark.parametrize("family,n,dim", [("hea", 2, 15), ("hea", 3, 63), ("spin_glass_hva", 3, 63),
+                                          ("tfim_hva_open", 4, 16)])
+def test_rank_method_paper_dims(ref, family, n, dim):
+    res = compare(ref, dense_family(ref, family, n), 1 << n)
+    assert res.dimension == dim
+
+
+def test_rank_tolerance_knob(ref):
+    # a loose relative threshold rejects candidates the default keeps
+    gens = dense_family(ref, "hea", 3)
+    loose = compare(ref, gens, 8, rank_tol=1e-2)
+    default = compare(ref, gens, 8)
+    assert loose.dimension <= default.dimension
+
+
+def test_rank_method_rejects_pauli_and_honours_capacity():
+    with pytest.raises(liecl.InvalidInputError, match="dense backend"):
+        liecl.run_closure([liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)], RANK)
+    cfg = w.config0()
+    with pytest.raises(liecl.CapacityError):
+        liecl.closure_dense_arrays(cfg.generators, cfg.d, RANK, liecl.ClosureConfig(tolerance=cfg.tol, max_dim=4))
