@@ -41,12 +41,21 @@ __global__ void rank_build_t_kernel(const double2* __restrict__ R, int64_t ldr, 
 // tournament: the m_pad/2 disjoint pairs of a step go to the warps in
 // parallel). Writes indep[j] = (#sigma > thr * sigma_max == m) and the
 // extreme singular values.
+// T lives in shared memory when it fits (in_smem; every step is then a
+// shared-memory round trip instead of an L2 one), else in its global slot.
 __global__ void rank_jacobi_kernel(double2* __restrict__ W, int m, int m_pad, double thr, int max_sweeps,
-                                   int* __restrict__ indep, double* __restrict__ smin, double* __restrict__ smax) {
-  extern __shared__ double s_norm2[];  // m_pad column norms^2
+                                   int in_smem, int* __restrict__ indep, double* __restrict__ smin,
+                                   double* __restrict__ smax) {
+  extern __shared__ double2 s_dyn[];  // [T (m_pad^2) if in_smem] [m_pad column norms^2]
   __shared__ int s_rot;
   const int j = blockIdx.x;
   double2* T = W + static_cast<int64_t>(j) * m_pad * m_pad;
+  double* s_norm2 = reinterpret_cast<double*>(s_dyn + (in_smem ? static_cast<int64_t>(m_pad) * m_pad : 0));
+  if (in_smem) {
+    for (int e = threadIdx.x; e < m_pad * m_pad; e += blockDim.x) s_dyn[e] = T[e];
+    T = s_dyn;
+    __syncthreads();
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const double eps = 2.220446049250313e-16;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
@@ -70,7 +79,9 @@ __global__ void rank_jacobi_kernel(double2* __restrict__ W, int m, int m_pad, do
         }
         al = warp_sum(al), be = warp_sum(be), gr = warp_sum(gr), gi = warp_sum(gi);
         const double g = sqrt(gr * gr + gi * gi);
-        if (g == 0.0 || g <= eps * sqrt(al * be)) continue;  // already orthogonal
+        // orthogonal to working accuracy (the one-sided Jacobi SVD test
+        // |a^H b| <= m eps ||a|| ||b||; tighter never settles under roundoff)
+        if (g == 0.0 || g <= m_pad * eps * sqrt(al * be)) continue;
         if (lane == 0) s_rot = 1;
         const double cph = gr / g, sph = gi / g;  // e^{i phi} = gamma / |gamma|
         const double zeta = (be - al) / (2.0 * g);
@@ -213,6 +224,8 @@ public:
   }
 
 private:
+  static constexpr size_t kJacobiSmem = 200 * 1024;
+  bool jacobi_attr_ = false;
   int64_t ldr() const { return cap_ + 1; }
   int m_pad() const { return static_cast<int>((n_ + 2) & ~int64_t(1)); }
   // candidates per batch: the T matrices (m_pad^2 complex each) within 1 GB
@@ -249,8 +262,15 @@ private:
     }
     dim3 gb(static_cast<unsigned>(std::min<int64_t>((static_cast<int64_t>(mp) * mp + 255) / 256, 256)), cnt);
     rank_build_t_kernel<<<gb, 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), Pacc, n_, rho, mp, W_.p);
-    rank_jacobi_kernel<<<cnt, 256, static_cast<size_t>(mp) * sizeof(double), ctx_->stream>>>(
-        W_.p, m, mp, threshold(), 60, ind, smin_.p, smax_.p);
+    const size_t t_bytes = static_cast<size_t>(mp) * mp * sizeof(double2);
+    const bool in_smem = t_bytes + mp * sizeof(double) <= kJacobiSmem;
+    if (!jacobi_attr_) {
+      CU(cudaFuncSetAttribute(rank_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kJacobiSmem)));
+      jacobi_attr_ = true;
+    }
+    rank_jacobi_kernel<<<cnt, 256, (in_smem ? t_bytes : 0) + mp * sizeof(double), ctx_->stream>>>(
+        W_.p, m, mp, threshold(), 30, in_smem ? 1 : 0, ind, smin_.p, smax_.p);
     launched(ctx_), launched(ctx_);
     CU(cudaMemcpyAsync(h_ind_.p, ind, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
@@ -268,6 +288,13 @@ private:
   void apply(int cnt, int64_t pair_g0, int64_t cand0, bool generators) {
     const int64_t n_bs = n_;
     std::vector<int> ind(h_ind_.p, h_ind_.p + cnt);
+    // re-checks are batched: every stale "independent" left in the batch is
+    // re-run at once against the current state; those results hold until the
+    // next accept (then the rest is re-run again) -- the same verdicts as
+    // re-checking one at a time, with one SVD launch per accept instead of one
+    // per candidate
+    std::vector<int> rslot(static_cast<size_t>(cnt), -1), rind;
+    int64_t r_state = -1;  // basis size the re-check results refer to
     for (int j = 0; j < cnt; ++j) {
       int64_t l, m;
       if (pair_g0 >= 0) pair_from_index(pair_g0 + j, l, m);
@@ -289,13 +316,20 @@ private:
       const double2* beta = P1_.p + j * n_bs;
       const double* rho = rn_.p + j;
       if (n_ != n_bs && indep) {  // stale "independent": recompute against the current state
-        Y_.ensure(static_cast<size_t>(D_));
-        CU(cudaMemcpyAsync(Y_.p, h, D_ * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
-        recheck(Y_.p);
-        indep = h_ind_.p[0] != 0;
-        resid = Xr_.p;
-        beta = Pr_.p;
-        rho = rnr_.p;
+        if (r_state != n_) {
+          std::vector<int> todo;
+          for (int k = j; k < cnt; ++k)
+            if (!h_nul_.p[k] && ind[k]) todo.push_back(k);
+          rind = recheck(todo);
+          std::fill(rslot.begin(), rslot.end(), -1);
+          for (size_t q = 0; q < todo.size(); ++q) rslot[todo[q]] = static_cast<int>(q);
+          r_state = n_;
+        }
+        const int q = rslot[j];
+        indep = rind[q] != 0;
+        resid = Xr_.p + static_cast<int64_t>(q) * D_;
+        beta = Pr_.p + static_cast<int64_t>(q) * n_;
+        rho = rnr_.p + q;
         rc = 1;
         ++st_.rechecks;
       }
@@ -308,13 +342,22 @@ private:
     }
   }
 
-  // single-candidate check against the current state into the recheck buffers
-  void recheck(const double2* h) {
-    Xr_.ensure(static_cast<size_t>(D_));
-    Pr_.ensure(static_cast<size_t>(std::max<int64_t>(n_, 1)));
-    rnr_.ensure(1);
-    indr_.ensure(1);
-    check(h, 1, Xr_.p, Pr_.p, rnr_.p, indr_.p);
+  // batch candidates `todo` (columns of C_) checked against the current state
+  // into the re-check buffers; returns their verdicts (slot q = todo[q])
+  std::vector<int> recheck(const std::vector<int>& todo) {
+    const int k = static_cast<int>(todo.size());
+    Yb_.ensure(static_cast<size_t>(k) * D_);
+    Xr_.ensure(static_cast<size_t>(k) * D_);
+    Pr_.ensure(static_cast<size_t>(std::max<int64_t>(n_, 1)) * k);
+    rnr_.ensure(k);
+    indr_.ensure(k);
+    idx_.ensure(k);
+    CU(cudaMemcpyAsync(idx_.p, todo.data(), k * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+    dim3 gg(static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 64)), k);
+    gather_columns_kernel<<<gg, 256, 0, ctx_->stream>>>(C_.p, idx_.p, D_, Yb_.p);
+    launched(ctx_);
+    check(Yb_.p, k, Xr_.p, Pr_.p, rnr_.p, indr_.p);
+    return std::vector<int>(h_ind_.p, h_ind_.p + k);
   }
 
   // RankStrategy::accept (R:src/closure.cpp:200-203): B gets h; V and R grow
@@ -345,9 +388,9 @@ private:
   liecl_b200_stats st_{};
   std::vector<Warning> warns_;
   std::vector<liecl_b200_decision> log_;
-  DevBuf<double2> B_, V_, R_, C_, X_, Y_, P1_, P2_, W_, Xr_, Pr_;
+  DevBuf<double2> B_, V_, R_, C_, X_, Y_, Yb_, P1_, P2_, W_, Xr_, Pr_;
   DevBuf<double> partial_, rn_, hn_, smin_, smax_, rnr_;
-  DevBuf<int> nul_, ind_, indr_;
+  DevBuf<int> nul_, ind_, indr_, idx_;
   HostBuf<double> h_hn_, h_one_;
   HostBuf<int> h_nul_, h_ind_;
 };
