@@ -389,3 +389,260 @@ __global__ void append_scaled_kernel(const unsigned long long* __restrict__ key,
 
 } // namespace psum
 } // namespace liecl_b200
+
+namespace liecl_b200 {
+namespace psum {
+
+// ---- fused single-candidate check (small sums) ------------------------------
+// One CTA runs OrthonormStrategy::check for one candidate entirely in shared
+// memory: two linear_combination passes (R:src/closure.cpp:142-162) and the
+// residual norm. Same arithmetic, same order as the multi-kernel merges:
+//  - beta_l: every term's (l, conj(v) h_t) contributions are listed in term
+//    order (sorted keys), then one thread adds them from +0 per l in list
+//    order -- sum_inner_product's order;
+//  - the residual: sources merged one after another (the base terms, then
+//    V_l * -beta_l for l ascending); keys are distinct inside a source, so a
+//    source is merged in parallel (one thread per key owns its slot) and a
+//    barrier separates sources: every slot adds in the reference's order from
+//    +0 (PauliSum::from_terms);
+//  - drop |c| <= 1e-14 max |c|, bitonic sort of the survivors by key, norm
+//    summed in sorted order.
+// A candidate whose sums outgrow the shared buffers reports status 1 and the
+// engine re-runs the batch through the general merges.
+constexpr int kFusedThreads = 256;
+
+struct FusedSmem {
+  unsigned long long* hkey;  // open-addressed accumulation slots [hc]
+  C2* hval;
+  unsigned long long* skey;  // sorted pass input / output [hc]
+  C2* sval;
+  unsigned long long* ckey;  // beta contributions: basis index [hc]
+  C2* cval;
+  C2* beta;                  // [nb]
+  unsigned* touched;         // [nb / 32 + 1]
+};
+
+__device__ __forceinline__ void fused_bitonic(unsigned long long* key, C2* val, int count, int npow2) {
+  for (int i = count + threadIdx.x; i < npow2; i += blockDim.x) key[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= npow2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          if ((key[i] > key[p]) == up) {
+            const unsigned long long tk = key[i];
+            key[i] = key[p];
+            key[p] = tk;
+            const C2 tv = val[i];
+            val[i] = val[p];
+            val[p] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// one pass: input = (s.skey, s.sval, n_in) sorted; output replaces it; returns
+// the output count or -1 on overflow
+__device__ int fused_pass(const FusedSmem& s, int hc, int n_in, const Index& ix, int n_limit,
+                          const int64_t* __restrict__ voff, const unsigned long long* __restrict__ vkey,
+                          const C2* __restrict__ vval, int* s_scratch) {
+  int* s_count = s_scratch;      // [0] contributions, [1] distinct keys, [2] kept, [3] overflow
+  int* s_pos = s_scratch + 4;    // per-term contribution offsets [kFusedThreads + 1] chunk scan
+  for (int l = threadIdx.x; l < n_limit; l += blockDim.x) s.beta[l] = {0.0, 0.0};
+  for (int w = threadIdx.x; w < n_limit / 32 + 1; w += blockDim.x) s.touched[w] = 0u;
+  for (int i = threadIdx.x; i < hc; i += blockDim.x) s.hkey[i] = pauli::kEmpty;
+  if (threadIdx.x < 4) s_count[threadIdx.x] = 0;
+  __syncthreads();
+  // (a) contributions, term-major: chunks of blockDim terms, each chunk
+  // scanned so the list keeps term order
+  for (int t0 = 0; t0 < n_in; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    int sl = -1, c = 0;
+    if (t < n_in) {
+      sl = index_find(ix, s.skey[t]);
+      if (sl >= 0)
+        for (int e = ix.head[sl]; e >= 0 && ix.e_l[e] < n_limit; e = ix.e_next[e]) ++c;
+    }
+    s_pos[threadIdx.x] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive scan of the chunk's counts
+      int acc = s_count[0];
+      for (int i = 0; i < blockDim.x; ++i) {
+        const int v = s_pos[i];
+        s_pos[i] = acc;
+        acc += v;
+      }
+      s_count[0] = acc;
+      if (acc > hc) s_count[3] = 1;
+    }
+    __syncthreads();
+    if (s_count[3]) return -1;
+    if (sl >= 0) {
+      int w = s_pos[threadIdx.x];
+      const C2 h = s.sval[t];
+      for (int e = ix.head[sl]; e >= 0 && ix.e_l[e] < n_limit; e = ix.e_next[e], ++w) {
+        const C2 v = ix.e_v[e];
+        s.ckey[w] = static_cast<unsigned long long>(ix.e_l[e]);
+        s.cval[w] = cmul({v.re, -v.im}, h);
+      }
+    }
+    __syncthreads();
+  }
+  // (b) beta_l += contributions in list order, from +0
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < s_count[0]; ++i) {
+      const int l = static_cast<int>(s.ckey[i]);
+      s.beta[l] = cadd(s.beta[l], s.cval[i]);
+      s.touched[l >> 5] |= 1u << (l & 31);
+    }
+  }
+  __syncthreads();
+  // (c) residual slots: the base terms (x (1, 0)), then V_l * -beta_l
+  // keys are distinct inside a source, so each key's slot has one writer per
+  // source; a new key first reserves capacity (<= 3/4 of the table, the
+  // spare quarter >= one CTA of in-flight claims), so probing always ends
+  const int limit = (hc * 3) / 4;
+  auto merge_source = [&](const unsigned long long* key, const C2* val, int n, C2 mult) {
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const unsigned long long k = key[t];
+      const C2 v = cmul(mult, val[t]);
+      for (uint64_t p = pauli::mix(k) & static_cast<uint64_t>(hc - 1);; p = (p + 1) & static_cast<uint64_t>(hc - 1)) {
+        const unsigned long long cur = s.hkey[p];
+        if (cur == k) {
+          s.hval[p] = cadd(s.hval[p], v);
+          break;
+        }
+        if (cur != pauli::kEmpty) continue;
+        const unsigned long long prev = atomicCAS(&s.hkey[p], pauli::kEmpty, k);
+        if (prev == pauli::kEmpty) {
+          if (atomicAdd(&s_count[1], 1) >= limit) s_count[3] = 1;
+          s.hval[p] = pauli::slot(v);
+          break;
+        }
+        if (prev == k) {  // cannot happen within one source; kept for safety
+          s.hval[p] = cadd(s.hval[p], v);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  };
+  merge_source(s.skey, s.sval, n_in, {1.0, 0.0});
+  for (int w = 0; w < n_limit / 32 + 1 && !s_count[3]; ++w) {
+    unsigned bits = s.touched[w];
+    while (bits) {
+      const int l = w * 32 + __ffs(bits) - 1;
+      bits &= bits - 1;
+      const C2 b = s.beta[l];
+      if (b.re == 0.0 && b.im == 0.0) continue;  // zero products change no slot
+      merge_source(vkey + voff[l], vval + voff[l], static_cast<int>(voff[l + 1] - voff[l]), {-b.re, -b.im});
+      if (s_count[3]) break;
+    }
+  }
+  if (s_count[3]) return -1;
+  // (d) drop rule, compaction, sort
+  __shared__ double s_max[kFusedThreads / 32];
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < hc; i += blockDim.x)
+    if (s.hkey[i] != pauli::kEmpty) mx = fmax(mx, hypot(s.hval[i].re, s.hval[i].im));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < kFusedThreads / 32; ++i) m = fmax(m, s_max[i]);
+    s_max[0] = m;
+  }
+  __syncthreads();
+  const double floor = __dmul_rn(kDropTolerance, s_max[0]);
+  for (int i = threadIdx.x; i < hc; i += blockDim.x)
+    if (s.hkey[i] != pauli::kEmpty && hypot(s.hval[i].re, s.hval[i].im) > floor) {
+      const int w = atomicAdd(&s_count[2], 1);
+      s.skey[w] = s.hkey[i];
+      s.sval[w] = s.hval[i];
+    }
+  __syncthreads();
+  const int nk = s_count[2];
+  int np2 = 1;
+  while (np2 < nk) np2 <<= 1;
+  fused_bitonic(s.skey, s.sval, nk, np2);
+  return nk;
+}
+
+// OrthonormStrategy::check of segment p of h against basis elements l < n_limit
+__global__ void __launch_bounds__(kFusedThreads)
+fused_check_kernel(const int* __restrict__ off, int nseg, const unsigned long long* __restrict__ hkey,
+                   const C2* __restrict__ hval, Index ix, int n_limit, const int64_t* __restrict__ voff,
+                   const unsigned long long* __restrict__ vkey, const C2* __restrict__ vval, int hc,
+                   unsigned long long* __restrict__ okey, C2* __restrict__ oval, int* __restrict__ olen,
+                   double* __restrict__ rn, int* __restrict__ status) {
+  extern __shared__ unsigned char s_raw[];
+  __shared__ int s_scratch[4 + kFusedThreads];
+  FusedSmem s;
+  s.hkey = reinterpret_cast<unsigned long long*>(s_raw);
+  s.skey = s.hkey + hc;
+  s.ckey = s.skey + hc;
+  s.hval = reinterpret_cast<C2*>(s.ckey + hc);
+  s.sval = s.hval + hc;
+  s.cval = s.sval + hc;
+  s.beta = s.cval + hc;
+  s.touched = reinterpret_cast<unsigned*>(s.beta + n_limit);
+  for (int p = blockIdx.x; p < nseg; p += gridDim.x) {
+    const int b0 = off[p], n_in = off[p + 1] - b0;
+    if (n_in > hc) {  // the input alone does not fit
+      if (threadIdx.x == 0) status[p] = 1;
+      continue;
+    }
+    for (int t = threadIdx.x; t < n_in; t += blockDim.x) {
+      s.skey[t] = hkey[b0 + t];
+      s.sval[t] = hval[b0 + t];
+    }
+    __syncthreads();
+    int n = n_in;
+    if (n_limit > 0) {  // project_residual of an empty tuple returns h itself
+      n = fused_pass(s, hc, n, ix, n_limit, voff, vkey, vval, s_scratch);
+      if (n > 0) n = fused_pass(s, hc, n, ix, n_limit, voff, vkey, vval, s_scratch);
+    }
+    if (n < 0) {
+      if (threadIdx.x == 0) status[p] = 1;
+      __syncthreads();
+      continue;
+    }
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      okey[static_cast<int64_t>(p) * hc + t] = s.skey[t];
+      oval[static_cast<int64_t>(p) * hc + t] = s.sval[t];
+    }
+    if (threadIdx.x == 0) {
+      double acc = 0.0;  // sum_norm in term order
+      for (int t = 0; t < n; ++t)
+        acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(s.sval[t].re, s.sval[t].re), __dmul_rn(s.sval[t].im, s.sval[t].im)));
+      rn[p] = __dsqrt_rn(acc);
+      olen[p] = n;
+      status[p] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+// strided fused outputs (row p at p * hc) -> contiguous segments
+__global__ void strided_to_segs_kernel(const unsigned long long* __restrict__ sk, const C2* __restrict__ sv, int hc,
+                                       const int* __restrict__ off, int nseg, unsigned long long* __restrict__ ok,
+                                       C2* __restrict__ ov) {
+  for (int p = blockIdx.x; p < nseg; p += gridDim.x)
+    for (int t = threadIdx.x; t < off[p + 1] - off[p]; t += blockDim.x) {
+      ok[off[p] + t] = sk[static_cast<int64_t>(p) * hc + t];
+      ov[off[p] + t] = sv[static_cast<int64_t>(p) * hc + t];
+    }
+}
+
+inline size_t fused_smem_bytes(int hc, int n_limit) {
+  return static_cast<size_t>(hc) * 3 * (sizeof(unsigned long long) + sizeof(C2)) +
+         static_cast<size_t>(n_limit) * sizeof(C2) + (static_cast<size_t>(n_limit) / 32 + 1) * sizeof(unsigned);
+}
+
+} // namespace psum
+} // namespace liecl_b200

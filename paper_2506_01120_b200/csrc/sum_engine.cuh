@@ -48,9 +48,10 @@ public:
 
   ~SumEngine() {
     if (trace_) {
-      std::fprintf(stderr, "[sum_engine] n=%lld batches=%llu rechecks=%llu accepts=%llu\n", (long long)n_,
-                   (unsigned long long)st_.batches, (unsigned long long)st_.rechecks,
-                   (unsigned long long)st_.accepted);
+      std::fprintf(stderr, "[sum_engine] n=%lld batches=%llu rechecks=%llu accepts=%llu fused=%llu fallbacks=%llu\n",
+                   (long long)n_, (unsigned long long)st_.batches, (unsigned long long)st_.rechecks,
+                   (unsigned long long)st_.accepted, (unsigned long long)fused_batches_,
+                   (unsigned long long)fused_fallbacks_);
       for (const auto& kv : tsum_)
         std::fprintf(stderr, "[sum_engine] %-10s %9.3f ms  %8llu calls\n", kv.first.c_str(), kv.second.first,
                      (unsigned long long)kv.second.second);
@@ -422,9 +423,59 @@ private:
 
   // OrthonormStrategy::check for every segment of h (unit candidates):
   // residual sums and their norms, against basis elements l < n_limit
+  // The fused single-CTA check (pauli_sum.cuh) for batches whose sums fit in
+  // shared memory: one launch and one synchronisation instead of two merge
+  // pipelines; false (nothing changed) when some candidate outgrows it.
+  bool fused_check(const Segs& h, int n_limit, Segs& res, std::vector<double>& rn) {
+    // latency path: re-checks and short batches (large batches run faster
+    // through the throughput-oriented merges); it switches itself off once
+    // candidates keep outgrowing it
+    if (!fused_ || h.nseg > kFusedMaxBatch || fused_fallbacks_ > fused_batches_ + 8) return false;
+    const int hc = n_limit <= 4096 ? 2048 : (n_limit <= 8192 ? 1024 : 0);
+    if (hc == 0) return false;
+    const size_t smem = psum::fused_smem_bytes(hc, n_limit);
+    if (smem > kFusedSmemMax) return false;
+    if (!fused_attr_) {
+      CU(cudaFuncSetAttribute(psum::fused_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kFusedSmemMax)));
+      fused_attr_ = true;
+    }
+    const int ns = h.nseg;
+    need(fk_, static_cast<size_t>(ns) * hc);
+    need(fv_, static_cast<size_t>(ns) * hc);
+    need(flen_, ns);
+    need(fst_, ns);
+    need(frn_, ns);
+    psum::fused_check_kernel<<<static_cast<unsigned>(std::min(ns, 65535)), psum::kFusedThreads, smem, ctx_->stream>>>(
+        h.off.p, ns, h.key.p, h.val.p, ix_, n_limit, dvoff_.p, vkey_.p, vval_.p, hc, fk_.p, fv_.p, flen_.p, frn_.p,
+        fst_.p);
+    launched(ctx_);
+    std::vector<int> st(static_cast<size_t>(ns)), len(static_cast<size_t>(ns));
+    CU(cudaMemcpyAsync(st.data(), fst_.p, ns * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(len.data(), flen_.p, ns * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(rn.data(), frn_.p, ns * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    for (int p = 0; p < ns; ++p)
+      if (st[p] != 0) {
+        ++fused_fallbacks_;
+        return false;
+      }
+    std::vector<int> off(static_cast<size_t>(ns) + 1, 0);
+    for (int p = 0; p < ns; ++p) off[p + 1] = off[p] + len[p];
+    res.shape(ns, off[ns]);
+    CU(cudaMemcpyAsync(res.off.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+    psum::strided_to_segs_kernel<<<static_cast<unsigned>(std::min(ns, 65535)), 256, 0, ctx_->stream>>>(
+        fk_.p, fv_.p, hc, res.off.p, ns, res.key.p, res.val.p);
+    launched(ctx_);
+    CU(cudaStreamSynchronize(ctx_->stream));  // `off` is a stack buffer
+    ++fused_batches_;
+    return true;
+  }
+
   void check(const Segs& h, int n_limit, Segs& res, std::vector<double>& rn) {
     rn.assign(static_cast<size_t>(h.nseg), 0.0);
     if (h.nseg == 0) return;
+    if (fused_check(h, n_limit, res, rn)) return;
     if (n_limit == 0) {  // project_residual of an empty tuple returns h itself
       copy_segs(h, res);
     } else {
@@ -729,6 +780,20 @@ private:
   DevBuf<double> rmag_, hn_, rn_dev_;
   DevBuf<psum::Chunk> chunks_;
   Segs beta_, lc_, h_, res_, r1_, one_, rres_;
+  // fused check (LIECL_B200_SUMS_FUSED=0 disables it, e.g. to exercise the
+  // general merges)
+  static constexpr size_t kFusedSmemMax = 220 * 1024;
+  static constexpr int kFusedMaxBatch = 16;
+  bool fused_ = [] {
+    const char* e = std::getenv("LIECL_B200_SUMS_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  bool fused_attr_ = false;
+  uint64_t fused_batches_ = 0, fused_fallbacks_ = 0;
+  DevBuf<unsigned long long> fk_;
+  DevBuf<C2> fv_;
+  DevBuf<int> flen_, fst_;
+  DevBuf<double> frn_;
   int depth_ = 0;  // check() recursion (batch splits) takes fresh scratch
   std::vector<std::unique_ptr<Segs>> spill_;
   Segs* new_scratch() {

@@ -140,3 +140,11 @@ def test_golden_fixtures_bit_exact(golden, tag):
     assert np.array_equal(log["l"], g["log_l"]) and np.array_equal(log["m"], g["log_m"])
     assert np.array_equal(log["null_cand"], g["log_null"]) and np.array_equal(log["independent"], g["log_indep"])
     assert np.array_equal(log["residual_norm"].view(np.uint64), g["log_rn_bits"])
+
+
+@pytest.mark.parametrize("tag", ["sums_tfim_hva_open_n6_orthonorm-dimonly", "sums_spin_glass_hva_n3_orthonorm"])
+def test_general_merge_path_bit_exact(golden, tag, monkeypatch):
+    # small sums take the fused single-CTA check by default; the general
+    # multi-kernel merges (large sums) must give the same bits
+    monkeypatch.setenv("LIECL_B200_SUMS_FUSED", "0")
+    test_golden_fixtures_bit_exact(golden, tag)
