@@ -180,8 +180,8 @@ int liecl_b200_closure_pauli(liecl_b200_ctx* ctx, const uint64_t* x, const uint6
  * dimension <= cap) and its terms (term_cap entries), and, when ortho_offsets
  * != NULL, result.orthonormal_basis likewise. terms_needed[0..1] (basis,
  * orthonormal) and *stats are always written; LIECL_B200_CAPACITY ("output
- * buffers too small") when cap / term caps do not suffice -- call again with
- * the sizes reported.
+ * buffers too small") when cap / term caps do not suffice -- then fetch the
+ * result with buffers of the sizes reported (no recomputation).
  */
 int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
                                   const uint64_t* z, const double* coef, int32_t ngens, uint32_t qubits,
@@ -192,6 +192,12 @@ int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, c
                                   int64_t* terms_needed, liecl_b200_stats* stats, char* warnings,
                                   int64_t warnings_len, liecl_b200_decision* log, int64_t log_cap,
                                   int64_t* log_len);
+
+/* Copy the last liecl_b200_closure_pauli_sums result of this context (same
+ * output layout) into buffers sized from stats->dimension / terms_needed. */
+int liecl_b200_pauli_sums_fetch(liecl_b200_ctx* ctx, int64_t cap, int64_t* basis_offsets, uint64_t* basis_x,
+                                uint64_t* basis_z, double* basis_coef, int64_t term_cap, int64_t* ortho_offsets,
+                                uint64_t* ortho_x, uint64_t* ortho_z, double* ortho_coef, int64_t ortho_term_cap);
 
 /* project_residual (R:include/liecl/closure.hpp:139-140): residual after two
  * projection passes against the orthonormal tuple V (n operators), plus the

@@ -189,11 +189,17 @@ ClosureResult close_pauli_sums(std::span<const Operator> generators, const Closu
         bz.data(), bc.data(), tcap, oo.data(), ox.data(), oz.data(), ocf.data(), tcap, need.data(), &st, wbuf.data(),
         static_cast<std::int64_t>(wbuf.size()), nullptr, 0, nullptr);
     if (s == LIECL_B200_CAPACITY && std::string(liecl_b200_last_error()) == "output buffers too small") {
+      // the result stays on the device: fetch it with exact sizes
       tcap = std::max(need[0], need[1]);
       cap = std::max<std::int64_t>(cap, static_cast<std::int64_t>(st.dimension));
-      continue;
+      bo.assign(cap + 1, 0), oo.assign(cap + 1, 0);
+      bx.assign(tcap, 0), bz.assign(tcap, 0), ox.assign(tcap, 0), oz.assign(tcap, 0);
+      bc.assign(2 * tcap, 0.0), ocf.assign(2 * tcap, 0.0);
+      check(liecl_b200_pauli_sums_fetch(context(), cap, bo.data(), bx.data(), bz.data(), bc.data(), tcap, oo.data(),
+                                        ox.data(), oz.data(), ocf.data(), tcap));
+    } else {
+      check(s);
     }
-    check(s);
     // unique sorted terms without -0 components: from_terms rebuilds the
     // engine's sums value for value
     auto unpack = [&](const std::vector<std::int64_t>& o, const std::vector<std::uint64_t>& xs,

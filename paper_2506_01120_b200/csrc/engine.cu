@@ -136,6 +136,7 @@ struct liecl_b200_ctx {
   uint64_t kernels = 0;
   DevBuf<double2> splitk_ws;  // split-K partial products of the projection GEMMs
   std::shared_ptr<void> dense_cache, pauli_cache;  // workspaces of the last one-shot closure
+  std::shared_ptr<void> sum_cache;                  // the last multi-term Pauli closure (fetch)
   // per-kernel-class event timing (liecl_b200_ctx_set_timing)
   bool timing = false;
   struct Timed {
@@ -1032,8 +1033,10 @@ int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, c
     const auto t0 = Clock::now();
     const liecl_b200_config cfg = default_config(cfg_in);
     const uint64_t k0 = ctx->kernels;
-    SumEngine eng(ctx, qubits, keep_for(method), cfg);
+    auto holder = std::make_shared<SumEngine>(ctx, qubits, keep_for(method), cfg);
+    SumEngine& eng = *holder;
     eng.run(offsets, x, z, coef, ngens);
+    ctx->sum_cache = holder;  // liecl_b200_pauli_sums_fetch copies from it without recomputing
     *stats = eng.stats();
     stats->kernels = ctx->kernels - k0;
     stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
@@ -1047,6 +1050,23 @@ int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, c
       throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     eng.download(false, basis_offsets, basis_x, basis_z, basis_coef);
     if (ortho_offsets) eng.download(true, ortho_offsets, ortho_x, ortho_z, ortho_coef);
+  });
+}
+
+int liecl_b200_pauli_sums_fetch(liecl_b200_ctx* ctx, int64_t cap, int64_t* basis_offsets, uint64_t* basis_x,
+                                uint64_t* basis_z, double* basis_coef, int64_t term_cap, int64_t* ortho_offsets,
+                                uint64_t* ortho_x, uint64_t* ortho_z, double* ortho_coef, int64_t ortho_term_cap) {
+  return guarded([&] {
+    if (!ctx || !basis_offsets) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    auto eng = std::static_pointer_cast<SumEngine>(ctx->sum_cache);
+    if (!eng) throw Error(LIECL_B200_INVALID_INPUT, "no multi-term Pauli closure to fetch on this context");
+    use_device(ctx);
+    if (eng->size() > cap || eng->terms(false) > term_cap || (ortho_offsets && eng->terms(true) > ortho_term_cap))
+      throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    if (eng->terms(false) > 0 && (!basis_x || !basis_z || !basis_coef))
+      throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    eng->download(false, basis_offsets, basis_x, basis_z, basis_coef);
+    if (ortho_offsets) eng->download(true, ortho_offsets, ortho_x, ortho_z, ortho_coef);
   });
 }
 

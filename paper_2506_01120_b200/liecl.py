@@ -357,7 +357,8 @@ def closure_pauli_arrays(x, z, coef, qubits: int, method: Method = Method.orthon
 
 
 def closure_pauli_sums_arrays(offsets, x, z, coef, qubits: int, method: Method = Method.orthonorm_dimonly,
-                              config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
+                              config: ClosureConfig | None = None, device: int = 0,
+                              term_cap: int | None = None) -> ClosureResult:
     """Array-level entry for general (multi-term) Pauli generators: generator i
     = terms [offsets[i], offsets[i+1]) of x, z (uint64 masks) and coef (t, 2),
     in PauliSum form. Result sums are returned as PauliSum lists and as arrays
@@ -370,7 +371,7 @@ def closure_pauli_sums_arrays(offsets, x, z, coef, qubits: int, method: Method =
     lib = native.load()
     u64, i64 = C.POINTER(C.c_uint64), C.POINTER(C.c_int64)
     cap = int(config.max_dim or min(4 ** qubits, 1 << 20))
-    tcap = max(1 << 16, 8 * len(x))
+    tcap = term_cap or max(1 << 16, 8 * len(x))  # first guess; a larger result is fetched, not recomputed
     while True:
         bo, oo = np.zeros(cap + 1, np.int64), np.zeros(cap + 1, np.int64)
         bx, bz, bc = np.zeros(tcap, np.uint64), np.zeros(tcap, np.uint64), np.zeros((tcap, 2))
@@ -391,9 +392,16 @@ def closure_pauli_sums_arrays(offsets, x, z, coef, qubits: int, method: Method =
             log.ctypes.data_as(C.c_void_p) if config.record_log else None, C.c_int64(log_cap), C.byref(log_len))
         if status == native.CAPACITY and native.last_error() == "output buffers too small" \
                 and (need.max() > tcap or int(st.dimension) > cap):
+            # the result stays on the device: fetch it with exact sizes
             tcap = int(need.max())
             cap = max(cap, int(st.dimension))
-            continue
+            bo, oo = np.zeros(cap + 1, np.int64), np.zeros(cap + 1, np.int64)
+            bx, bz, bc = np.zeros(tcap, np.uint64), np.zeros(tcap, np.uint64), np.zeros((tcap, 2))
+            ox, oz, ocf = np.zeros(tcap, np.uint64), np.zeros(tcap, np.uint64), np.zeros((tcap, 2))
+            status = lib.liecl_b200_pauli_sums_fetch(
+                native.context(device), C.c_int64(cap), bo.ctypes.data_as(i64), bx.ctypes.data_as(u64),
+                bz.ctypes.data_as(u64), _dp(bc), C.c_int64(tcap), oo.ctypes.data_as(i64), ox.ctypes.data_as(u64),
+                oz.ctypes.data_as(u64), _dp(ocf), C.c_int64(tcap))
         _check(status)
         break
     n = int(st.dimension)

@@ -21,7 +21,7 @@ EXPORTED = [
     "liecl_b200_abi_version", "liecl_b200_last_error", "liecl_b200_ctx_create", "liecl_b200_ctx_destroy",
     "liecl_b200_ctx_kernel_count", "liecl_b200_ctx_set_stream", "liecl_b200_ctx_set_timing",
     "liecl_b200_ctx_kernel_times", "liecl_b200_closure_dense", "liecl_b200_closure_dense_gram",
-    "liecl_b200_closure_pauli", "liecl_b200_closure_pauli_sums",
+    "liecl_b200_closure_pauli", "liecl_b200_closure_pauli_sums", "liecl_b200_pauli_sums_fetch",
     "liecl_b200_project_residual_dense", "liecl_b200_commutator_dense", "liecl_b200_inner_product_dense",
     "liecl_b200_norm_dense", "liecl_b200_from_pauli", "liecl_b200_session_create_dense", "liecl_b200_session_destroy",
     "liecl_b200_session_set_basis", "liecl_b200_session_prefetch_basis", "liecl_b200_session_run_pairs", "liecl_b200_session_run_rows",

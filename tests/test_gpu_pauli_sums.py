@@ -148,3 +148,15 @@ def test_general_merge_path_bit_exact(golden, tag, monkeypatch):
     # multi-kernel merges (large sums) must give the same bits
     monkeypatch.setenv("LIECL_B200_SUMS_FUSED", "0")
     test_golden_fixtures_bit_exact(golden, tag)
+
+
+def test_small_output_buffers_fetch_without_recompute(golden):
+    # a result larger than the first output buffers is fetched from the device
+    meta, g = golden("sums_spin_glass_hva_n3_orthonorm-dimonly")
+    res = liecl.closure_pauli_sums_arrays(g["gen_offsets"], g["gen_x"], g["gen_z"],
+                                          g["gen_coef_bits"].view(np.float64), meta["qubits"],
+                                          liecl.Method.orthonorm_dimonly,
+                                          liecl.ClosureConfig(tolerance=meta["tol"]), term_cap=16)
+    bo, bx, bz, bc = res.basis_array
+    assert np.array_equal(bo, g["offsets"]) and np.array_equal(bc.view(np.uint64), g["coef_bits"])
+    assert res.stats.commutators_evaluated == meta["stats"]["commutators_evaluated"]  # one run's counters
