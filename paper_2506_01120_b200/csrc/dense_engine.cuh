@@ -651,10 +651,12 @@ private:
       CU(cudaMemcpyAsync(h_rn2_.p, rn2_.p, nsurv * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
       CU(cudaStreamSynchronize(ctx_->stream));
     }
-    constexpr int kBlock = 64;  // survivors re-projected together against in-batch accepts
+    constexpr int kBlock = kBlockGsMax;  // survivors re-projected together against in-batch accepts
     int s = 0;
     int blk_end = 0;
     int64_t n_blk = n_bs;
+    int blk_start = 0, blk_start_next = 0;
+    bool blk_on_device = false, blk_refreshed = false;
     auto vp = [&](DevBuf<double>& b, int64_t i) { return b.p + i * W; };
     for (int j = 0; j < cnt; ++j) {
       int64_t l, m;
@@ -694,6 +696,32 @@ private:
       } else if (k >= blk_end) {
         blk_end = std::min(nsurv, k + kBlock);
         n_blk = n_o_;
+      }
+      if (k == blk_start_next) {  // a new block: decide it on the device when that applies
+        blk_start = k;
+        blk_start_next = blk_end;
+        blk_on_device = use_block_gs(blk_end - k) && run_block_gs(k, blk_end - k);
+        blk_refreshed = n_o_ > n_bs;
+      }
+      if (blk_on_device) {
+        // verdict and (for accepts) the appended vector came from block_gs_kernel
+        const int q = k - blk_start;
+        if (q == h_bgs_status_.p[1])
+          throw Error(LIECL_B200_CAPACITY,
+                      "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
+        const int fl = h_bgs_flags_.p[q];
+        const double rn = h_bgs_rn_.p[q];
+        const bool ind = (fl & 1) != 0;
+        if (fl & 2) ++st_.rechecks;
+        note(l, m, rn, ind);
+        log_decision(l, m, 0, ind ? 1 : 0, (blk_refreshed || (fl & 2)) ? 1 : 0, rn);
+        if (indep_out) indep_out[j] = ind ? 1 : 0;
+        if (rn_out) rn_out[j] = rn;
+        if (!ind) continue;
+        ++n_o_;
+        if (keep_) ++n_b_;
+        ++st_.accepted;
+        continue;
       }
       double rn = h_rn2_.p[k];
       const double* resid = vp(X_, k);
@@ -742,6 +770,65 @@ private:
     if (!keep_) n_b_ = n_o_;
   }
 
+  // device-resident block decisions (block_gs.cuh): general complex field,
+  // not D-sharded (its sums are grid-local), blocks of two or more survivors
+  bool use_block_gs(int nb) const { return field_ == Field::kComplex && !red_ && nb >= 2 && block_gs_; }
+  bool run_block_gs(int k, int nb) {
+    if (!bgs_grid_) {
+      int sms = 0, per_sm = 0;
+      CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx_->device));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_gs_kernel, kBlockGsThreads, 0));
+      if (per_sm < 1) {
+        block_gs_ = false;
+        return false;
+      }
+      bgs_grid_ = sms;  // one CTA per SM: co-resident, as grid.sync() requires
+      bgs_part_.ensure(static_cast<size_t>(bgs_grid_) * kBlockGsMax);
+      bgs_beta_.ensure(kBlockGsMax);
+      bgs_partn_.ensure(bgs_grid_);
+      bgs_flags_.ensure(kBlockGsMax);
+      bgs_rn_.ensure(kBlockGsMax);
+      bgs_status_.ensure(2);
+      h_bgs_flags_.ensure(kBlockGsMax);
+      h_bgs_rn_.ensure(kBlockGsMax);
+      h_bgs_status_.ensure(2);
+    }
+    ensure_capacity(std::min<int64_t>(cap_ + 2, n_o_ + nb + 2));  // slots for every possible accept
+    const int64_t W = vw();
+    BlockGsArgs a{};
+    a.X = cplx(X_.p + k * W);
+    a.nb = nb;
+    a.cand = idx_.p + k;
+    a.C = cplx(C_.p);
+    a.V = cplx(V_.p);
+    a.n_o = n_o_;
+    a.O = keep_ ? cplx(O_.p) : nullptr;
+    a.n_b = n_b_;
+    a.rn2 = rn2_.p + k;
+    a.D = D_;
+    a.inv_d = 1.0 / d_;
+    a.sqrt_d = sqrt_d_;
+    a.tol = tol_;
+    a.cap_left = static_cast<int>(std::max<int64_t>(0, cap_ - basis_size()));
+    a.part = bgs_part_.p;
+    a.beta = bgs_beta_.p;
+    a.partn = bgs_partn_.p;
+    a.flags = bgs_flags_.p;
+    a.rn = bgs_rn_.p;
+    a.status = bgs_status_.p;
+    const int init[2] = {0, -1};
+    CU(cudaMemcpyAsync(bgs_status_.p, init, sizeof init, cudaMemcpyHostToDevice, ctx_->stream));
+    void* args[] = {&a};
+    CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(block_gs_kernel), dim3(bgs_grid_), dim3(kBlockGsThreads),
+                                   args, 0, ctx_->stream));
+    launched(ctx_);
+    CU(cudaMemcpyAsync(h_bgs_flags_.p, bgs_flags_.p, nb * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(h_bgs_rn_.p, bgs_rn_.p, nb * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(h_bgs_status_.p, bgs_status_.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    return true;
+  }
+
   liecl_b200_ctx* ctx_;
   int d_;
   int64_t D_;
@@ -766,6 +853,16 @@ private:
   DevBuf<double> V_, Vw_, O_, C_, R_, X_, Y_, P_;  // element width ew() doubles
   DevBuf<double2> stage_;                          // complex input staging
   DevBuf<double2> basis_stage_;                    // set_basis staging (kept across calls)
+  bool block_gs_ = [] {  // LIECL_B200_BLOCK_GS=0: host-driven re-checks (diagnostics)
+    const char* e = std::getenv("LIECL_B200_BLOCK_GS");
+    return !(e && e[0] == '0');
+  }();
+  int bgs_grid_ = 0;
+  DevBuf<double2> bgs_part_, bgs_beta_;
+  DevBuf<double> bgs_partn_, bgs_rn_;
+  DevBuf<int> bgs_flags_, bgs_status_;
+  HostBuf<int> h_bgs_flags_, h_bgs_status_;
+  HostBuf<double> h_bgs_rn_;
   cudaStream_t copy_stream_ = nullptr;             // prefetch_basis
   cudaEvent_t prefetch_done_ = nullptr;
   const double2* prefetch_src_ = nullptr;

@@ -23,6 +23,7 @@
 //
 // The Pauli single-string path (pauli.cuh) is bit-exact and runs frontier
 // batches of all available pairs.
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -42,6 +43,7 @@
 
 #include "../../include/liecl_b200.h"
 #include "ah.cuh"
+#include "block_gs.cuh"
 #include "commutator.cuh"
 #include "dgemm_dmma.cuh"
 #include "pauli.cuh"
