@@ -628,6 +628,17 @@ fused_check_kernel(const int* __restrict__ off, int nseg, const unsigned long lo
   }
 }
 
+// segments starting at src[q] (lengths from off) -> contiguous batch
+__global__ void gather_segs_kernel(const unsigned long long* __restrict__ key, const C2* __restrict__ val,
+                                   const int* __restrict__ src, const int* __restrict__ off, int nseg,
+                                   unsigned long long* __restrict__ okey, C2* __restrict__ oval) {
+  for (int q = blockIdx.x; q < nseg; q += gridDim.x)
+    for (int t = threadIdx.x; t < off[q + 1] - off[q]; t += blockDim.x) {
+      okey[off[q] + t] = key[src[q] + t];
+      oval[off[q] + t] = val[src[q] + t];
+    }
+}
+
 // strided fused outputs (row p at p * hc) -> contiguous segments
 __global__ void strided_to_segs_kernel(const unsigned long long* __restrict__ sk, const C2* __restrict__ sv, int hc,
                                        const int* __restrict__ off, int nseg, unsigned long long* __restrict__ ok,

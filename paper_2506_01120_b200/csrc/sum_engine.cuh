@@ -46,7 +46,7 @@ public:
     need(small_, 4);
   }
 
-  ~SumEngine() {
+  void print_trace() const {
     if (trace_) {
       std::fprintf(stderr, "[sum_engine] n=%lld batches=%llu rechecks=%llu accepts=%llu fused=%llu fallbacks=%llu\n",
                    (long long)n_, (unsigned long long)st_.batches, (unsigned long long)st_.rechecks,
@@ -134,8 +134,11 @@ public:
       i = next;
     }
     ++st_.batches;
-    Stage st_cur(this, "cursor");
-    cursor_loop();
+    {
+      Stage st_cur(this, "cursor");
+      cursor_loop();
+    }
+    print_trace();
   }
 
   // basis (or orthonormal tuple) -> host arrays: offsets (n+1), x, z, coef
@@ -472,6 +475,83 @@ private:
     return true;
   }
 
+  // check() with the certified-reject screen (as DenseEngine::apply): after
+  // pass 1, a candidate with rn1 <= tol/20 cannot come out independent of
+  // pass 2 (||r2|| <= ||r1|| up to rounding; the drop rule only removes
+  // terms), nor borderline (tol/20 < tol/10), so pass 2 runs on the others
+  // only. Basis, statistics and warnings are the reference's bits either way;
+  // only a rejected candidate's log entry would carry rn1, so with the
+  // decision log on every candidate takes both passes. index[p] = segment of
+  // `res` holding candidate p's residual (-1: certified reject).
+  void check_screened(const Segs& h, int n_limit, Segs& res, std::vector<double>& rn, std::vector<int>& index) {
+    index.resize(static_cast<size_t>(h.nseg));
+    for (int p = 0; p < h.nseg; ++p) index[p] = p;
+    if (record_ || n_limit == 0 || h.nseg <= kFusedMaxBatch) {
+      check(h, n_limit, res, rn);
+      return;
+    }
+    rn.assign(static_cast<size_t>(h.nseg), 0.0);
+    Segs& r1 = r1_;
+    if (!pass(h, n_limit, r1)) {  // too large for one batch: the splitting path
+      check(h, n_limit, res, rn);
+      return;
+    }
+    std::vector<double> rn1(static_cast<size_t>(h.nseg));
+    need(rn_dev_, h.nseg);
+    psum::seg_norm_kernel<<<grid(h.nseg), 256, 0, ctx_->stream>>>(r1.off.p, r1.nseg, r1.val.p, rn_dev_.p);
+    launched(ctx_);
+    std::vector<int> off1(static_cast<size_t>(h.nseg) + 1);
+    CU(cudaMemcpyAsync(rn1.data(), rn_dev_.p, h.nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(off1.data(), r1.off.p, off1.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    const double screen = tol_ / 20.0;
+    std::vector<int> surv;
+    for (int p = 0; p < h.nseg; ++p)
+      if (rn1[p] > screen) surv.push_back(p);
+    st_.survivors += surv.size();
+    const int ns = static_cast<int>(surv.size());
+    if (ns == h.nseg) {
+      if (!pass(r1, n_limit, res)) {
+        check(h, n_limit, res, rn);
+        return;
+      }
+    } else {
+      // survivors' pass-1 residuals as a batch of their own
+      std::vector<int> goff(static_cast<size_t>(ns) + 1, 0), gsrc(static_cast<size_t>(std::max(ns, 1)));
+      for (int q = 0; q < ns; ++q) {
+        gsrc[q] = off1[surv[q]];
+        goff[q + 1] = goff[q] + off1[surv[q] + 1] - off1[surv[q]];
+      }
+      Segs& sv = rs_;
+      sv.shape(ns, goff[ns]);
+      need(gsrc_, std::max(ns, 1));
+      CU(cudaMemcpyAsync(sv.off.p, goff.data(), goff.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+      CU(cudaMemcpyAsync(gsrc_.p, gsrc.data(), std::max(ns, 1) * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+      if (ns > 0) {
+        psum::gather_segs_kernel<<<static_cast<unsigned>(std::min(ns, 65535)), 256, 0, ctx_->stream>>>(
+            r1.key.p, r1.val.p, gsrc_.p, sv.off.p, ns, sv.key.p, sv.val.p);
+        launched(ctx_);
+      }
+      CU(cudaStreamSynchronize(ctx_->stream));  // goff / gsrc are host vectors
+      if (ns > 0 && !pass(sv, n_limit, res)) {
+        check(h, n_limit, res, rn);
+        for (int p = 0; p < h.nseg; ++p) index[p] = p;
+        return;
+      }
+      if (ns == 0) res.shape(0, 0);
+      std::fill(index.begin(), index.end(), -1);
+      for (int q = 0; q < ns; ++q) index[surv[q]] = q;
+    }
+    std::vector<double> rn2(static_cast<size_t>(std::max(ns, 1)));
+    if (ns > 0) {
+      psum::seg_norm_kernel<<<grid(ns), 256, 0, ctx_->stream>>>(res.off.p, ns, res.val.p, rn_dev_.p);
+      launched(ctx_);
+      CU(cudaMemcpyAsync(rn2.data(), rn_dev_.p, ns * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+    }
+    for (int p = 0; p < h.nseg; ++p) rn[p] = index[p] >= 0 ? rn2[index[p]] : rn1[p];
+  }
+
   void check(const Segs& h, int n_limit, Segs& res, std::vector<double>& rn) {
     rn.assign(static_cast<size_t>(h.nseg), 0.0);
     if (h.nseg == 0) return;
@@ -702,7 +782,7 @@ private:
       std::vector<double> rn;
       {
         Stage st_k(this, "check");
-        check(h, n_limit, res, rn);
+        check_screened(h, n_limit, res, rn, res_index_);
       }
       ++st_.batches;
       // ordered apply
@@ -739,7 +819,7 @@ private:
         const bool ind = r > tol_;
         note(pl, pm, r, ind);
         log_decision(pl, pm, 0, ind ? 1 : 0, rc, r);
-        if (ind) accept(res, j, r, h, j);
+        if (ind) accept(res, res_index_[j], r, h, j);  // independent => a pass-2 survivor
       }
       const int64_t g_next = g0 + j;
       pair_from_index(g_next, l, m);
@@ -779,7 +859,9 @@ private:
   DevBuf<C2> rval_, pv_, bv_;
   DevBuf<double> rmag_, hn_, rn_dev_;
   DevBuf<psum::Chunk> chunks_;
-  Segs beta_, lc_, h_, res_, r1_, one_, rres_;
+  Segs beta_, lc_, h_, res_, r1_, one_, rres_, rs_;
+  std::vector<int> res_index_;
+  DevBuf<int> gsrc_;
   // fused check (LIECL_B200_SUMS_FUSED=0 disables it, e.g. to exercise the
   // general merges)
   static constexpr size_t kFusedSmemMax = 220 * 1024;

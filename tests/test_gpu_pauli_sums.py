@@ -160,3 +160,23 @@ def test_small_output_buffers_fetch_without_recompute(golden):
     bo, bx, bz, bc = res.basis_array
     assert np.array_equal(bo, g["offsets"]) and np.array_equal(bc.view(np.uint64), g["coef_bits"])
     assert res.stats.commutators_evaluated == meta["stats"]["commutators_evaluated"]  # one run's counters
+
+
+@pytest.mark.parametrize("tag", ["sums_tfim_hva_open_n6_orthonorm-dimonly", "sums_spin_glass_hva_n3_orthonorm-dimonly",
+                                 "sums_spin_glass_hva_n3_orthonorm"])
+def test_certified_reject_screen_keeps_results_bit_exact(golden, tag):
+    # without the decision log, certified rejects skip the second pass; the
+    # basis, statistics and warnings must still be the reference's bits
+    meta, g = golden(tag)
+    method = liecl.method_from_string(meta["method"])
+    res = liecl.closure_pauli_sums_arrays(g["gen_offsets"], g["gen_x"], g["gen_z"],
+                                          g["gen_coef_bits"].view(np.float64), meta["qubits"], method,
+                                          liecl.ClosureConfig(tolerance=meta["tol"]))
+    assert res.dimension == meta["dimension"]
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(res.stats, k) == meta["stats"][k]
+    bo, bx, bz, bc = res.basis_array
+    assert np.array_equal(bo, g["offsets"]) and np.array_equal(bc.view(np.uint64), g["coef_bits"])
+    kinds = sorted(line.split("\t")[0] for line in meta["warnings"].splitlines() if line)
+    assert sorted(wr.kind for wr in res.stats.warnings) == kinds
+    assert res.stats.engine["survivors"] > 0  # the screened path ran (batches > the fused size)
