@@ -1,0 +1,89 @@
+"""Edge cases of the newer paths (multi-term sums, rank, Alg. 2, sessions),
+mirroring the reference's error behaviour (R:include/liecl/errors.hpp)."""
+import time
+
+import numpy as np
+import pytest
+
+from paper_2506_01120_b200 import liecl
+from paper_2506_01120_b200 import workloads as w
+
+pytestmark = pytest.mark.gpu
+
+
+def sums(n, terms_list):
+    return [liecl.pauli_sum_from_terms(n, [(liecl.PauliString(x, z, n), complex(c)) for (x, z), c in terms])
+            for terms in terms_list]
+
+
+def test_sums_unsorted_or_duplicate_terms_rejected():
+    off = np.array([0, 2], np.int64)
+    x = np.array([3, 1], np.uint64)  # (z, x) order violated
+    z = np.array([0, 0], np.uint64)
+    c = np.ones((2, 2))
+    with pytest.raises(liecl.InvalidInputError, match="sorted"):
+        liecl.closure_pauli_sums_arrays(off, x, z, c, 2)
+    x2 = np.array([1, 1], np.uint64)  # duplicate string
+    with pytest.raises(liecl.InvalidInputError, match="sorted"):
+        liecl.closure_pauli_sums_arrays(off, x2, z, c, 2)
+
+
+def test_sums_qubit_limits_and_masks():
+    with pytest.raises(liecl.InvalidInputError):
+        liecl.closure_pauli_sums_arrays(np.array([0, 2], np.int64), np.array([1, 2], np.uint64),
+                                        np.array([0, 0], np.uint64), np.ones((2, 2)), 32)
+    with pytest.raises(liecl.InvalidInputError, match="exceeds"):
+        liecl.closure_pauli_sums_arrays(np.array([0, 2], np.int64), np.array([1, 8], np.uint64),
+                                        np.array([0, 0], np.uint64), np.ones((2, 2)), 2)
+
+
+def test_sums_all_null_and_commuting_generators():
+    # every generator empty: no basis, one null_generator warning each
+    res = liecl.run_closure([liecl.PauliSum(3, []), liecl.PauliSum(3, [])] +
+                            sums(3, [[((0, 1), 1.0), ((0, 2), 1.0)]]), liecl.Method.orthonorm_dimonly)
+    assert res.dimension == 1 and [wr.kind for wr in res.stats.warnings] == ["null_generator"] * 2
+    # commuting multi-term generators: the closure is their span
+    res = liecl.run_closure(sums(3, [[((0, 1), 1.0), ((0, 2), 1.0)], [((0, 3), 1.0), ((0, 4), 1.0)]]),
+                            liecl.Method.orthonorm_dimonly)
+    assert res.dimension == 2 and res.stats.commutators_evaluated == 1
+
+
+def test_sums_deadline_raises_timeout():
+    off, x, z, c = w.sum_arrays(w.tfim_hva_open(20))
+    with pytest.raises(liecl.TimeoutError):
+        liecl.closure_pauli_sums_arrays(off, x, z, c, 20, liecl.Method.orthonorm_dimonly,
+                                        liecl.ClosureConfig(tolerance=1e-10, deadline=time.monotonic() + 0.05))
+
+
+def test_sums_capacity_keep_original():
+    off, x, z, c = w.sum_arrays(w.tfim_hva_open(6))
+    with pytest.raises(liecl.CapacityError):
+        liecl.closure_pauli_sums_arrays(off, x, z, c, 6, liecl.Method.orthonorm,
+                                        liecl.ClosureConfig(tolerance=1e-10, max_dim=10))
+
+
+def test_one_by_one_operators():
+    # d = 1: i*1 spans u(1); a second multiple of it is dependent
+    g = np.array([[1j], [2j]])
+    for m in (liecl.Method.orthonorm_dimonly, liecl.Method.matrix_inversion, liecl.Method.standard_rank):
+        res = liecl.closure_dense_arrays(g, 1, m, liecl.ClosureConfig(tolerance=1e-10))
+        assert res.dimension == 1, m
+
+
+def test_rank_and_gram_null_generators_warn():
+    cfg = w.config0()
+    gens = np.concatenate([np.zeros((1, cfg.d * cfg.d), np.complex128), cfg.generators])
+    for m in (liecl.Method.standard_rank, liecl.Method.matrix_inversion):
+        res = liecl.closure_dense_arrays(gens, cfg.d, m, liecl.ClosureConfig(tolerance=cfg.tol))
+        assert res.dimension == 9
+        assert [wr.kind for wr in res.stats.warnings].count("null_generator") == 1
+
+
+def test_session_window_past_basis_is_rejected():
+    cfg = w.config0()
+    full = liecl.closure_dense_arrays(cfg.generators, cfg.d, liecl.Method.orthonorm_dimonly,
+                                      liecl.ClosureConfig(tolerance=cfg.tol))
+    s = liecl.ClosureSession(cfg.d, config=liecl.ClosureConfig(tolerance=cfg.tol))
+    s.set_basis(full.basis_array[:3])
+    with pytest.raises(liecl.InvalidInputError):
+        s.run_pairs(0, 100)  # pair 3 needs basis element 3, which does not exist yet
