@@ -1,4 +1,4 @@
-// Device-resident in-block Gram-Schmidt for survivors (general complex field).
+// Device-resident in-block Gram-Schmidt for survivors (both arithmetic fields).
 //
 // After a block of up to 64 survivors has been re-projected against every
 // vector accepted since batch start (two GEMM passes, DenseEngine::apply),
@@ -12,6 +12,9 @@
 // phases), so every CTA computes the same residual norm and takes the same
 // verdict; an accepted residual is scaled by (1/rn, 0) straight into the next
 // basis slot (and the candidate into the originals slab for Alg. 3).
+// Packed anti-Hermitian field (ah.cuh): real d^2-element vectors, overlaps
+// against the weighted copy Vw, squared norms with the exact weights
+// (2 off the diagonal, 1 on it), appends write V and Vw.
 // Data another CTA wrote in this launch (partials, beta) is read with __ldcg:
 // grid.sync() orders the writes but does not invalidate this SM's L1, and the
 // same addresses are rewritten for every survivor. A CTA reads the vectors
@@ -28,14 +31,16 @@ constexpr int kBlockGsMax = 64;  // survivors per block (DenseEngine::apply)
 constexpr int kBlockGsThreads = 256;
 
 struct BlockGsArgs {
-  double2* X;               // nb survivor residuals (stride D), updated in place
+  double* X;                // nb survivor residuals (stride D elements), updated in place
   int nb;
   const int* cand;          // batch column of each survivor (originals)
-  const double2* C;         // batch candidates (h_unit)
-  double2* V;               // basis slab; this block's accepts go to V[n_o + a]
+  const double* C;          // batch candidates (h_unit)
+  double* V;                // basis slab; this block's accepts go to V[n_o + a]
+  double* Vw;               // packed field: weighted copy of V (else null)
   int64_t n_o;
-  double2* O;               // originals slab (Alg. 3) or null
+  double* O;                // originals slab (Alg. 3) or null
   int64_t n_b;
+  int d;                    // operator dimension (packed weights)
   const double* rn2;        // norms after the block refresh
   int64_t D;
   double inv_d, sqrt_d, tol;
@@ -59,8 +64,15 @@ __device__ __forceinline__ double block_sum(double v, double* s_red) {
   return t;  // valid in thread 0
 }
 
+// one vector element: complex (general field) or real (packed field)
+template <bool PACKED> struct GsElem;
+template <> struct GsElem<false> { using T = double2; };
+template <> struct GsElem<true> { using T = double; };
+
+template <bool PACKED>
 __global__ void __launch_bounds__(kBlockGsThreads) block_gs_kernel(BlockGsArgs a) {
   namespace cg = cooperative_groups;
+  using T = typename GsElem<PACKED>::T;
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = kBlockGsThreads / 32;
@@ -68,21 +80,30 @@ __global__ void __launch_bounds__(kBlockGsThreads) block_gs_kernel(BlockGsArgs a
   __shared__ double s_red[kBlockGsThreads / 32];
   __shared__ double2 s_beta[kBlockGsMax];
   __shared__ double s_rn;
-  const double2* Vnew = a.V + a.n_o * a.D;  // this block's accepts
+  T* const X = reinterpret_cast<T*>(a.X);
+  T* const V = reinterpret_cast<T*>(a.V);
+  const T* const Vnew = V + a.n_o * a.D;  // this block's accepts
+  const double* const Vwnew = PACKED ? a.Vw + a.n_o * a.D : nullptr;
+  auto weight = [&](int64_t e) { return (e % (a.d + 1)) == 0 ? 1.0 : 2.0; };
   int acc = 0;
   for (int k = 0; k < a.nb; ++k) {
-    double2* y = a.X + static_cast<int64_t>(k) * a.D;
+    T* y = X + static_cast<int64_t>(k) * a.D;
     double rn = a.rn2[k];
     if (acc > 0 && rn > a.tol) {  // a "dependent" verdict stands; an "independent" one is re-checked
       for (int pass = 0; pass < 2; ++pass) {
         // partial overlaps <V_i, y> over this CTA's slice (one warp per vector)
         for (int i = warp; i < acc; i += nwarps) {
-          const double2* v = Vnew + static_cast<int64_t>(i) * a.D;
           double re = 0.0, im = 0.0;
-          for (int64_t e = lo + lane; e < hi; e += 32) {
-            const double2 p = v[e], q = y[e];
-            re += p.x * q.x + p.y * q.y;
-            im += p.x * q.y - p.y * q.x;
+          if constexpr (PACKED) {
+            const double* vw = Vwnew + static_cast<int64_t>(i) * a.D;
+            for (int64_t e = lo + lane; e < hi; e += 32) re += vw[e] * y[e];
+          } else {
+            const double2* v = Vnew + static_cast<int64_t>(i) * a.D;
+            for (int64_t e = lo + lane; e < hi; e += 32) {
+              const double2 p = v[e], q = y[e];
+              re += p.x * q.x + p.y * q.y;
+              im += p.x * q.y - p.y * q.x;
+            }
           }
           re = warp_sum(re);
           im = warp_sum(im);
@@ -107,14 +128,21 @@ __global__ void __launch_bounds__(kBlockGsThreads) block_gs_kernel(BlockGsArgs a
         // y -= V beta on the slice (+ squared norm in the second pass)
         double nn = 0.0;
         for (int64_t e = lo + threadIdx.x; e < hi; e += kBlockGsThreads) {
-          double2 q = y[e];
-          for (int i = 0; i < acc; ++i) {
-            const double2 v = Vnew[static_cast<int64_t>(i) * a.D + e], b = s_beta[i];
-            q.x -= b.x * v.x - b.y * v.y;
-            q.y -= b.x * v.y + b.y * v.x;
+          if constexpr (PACKED) {
+            double q = y[e];
+            for (int i = 0; i < acc; ++i) q -= s_beta[i].x * Vnew[static_cast<int64_t>(i) * a.D + e];
+            y[e] = q;
+            nn += weight(e) * q * q;
+          } else {
+            double2 q = y[e];
+            for (int i = 0; i < acc; ++i) {
+              const double2 v = Vnew[static_cast<int64_t>(i) * a.D + e], b = s_beta[i];
+              q.x -= b.x * v.x - b.y * v.y;
+              q.y -= b.x * v.y + b.y * v.x;
+            }
+            y[e] = q;
+            nn += q.x * q.x + q.y * q.y;
           }
-          y[e] = q;
-          nn += q.x * q.x + q.y * q.y;
         }
         __syncthreads();  // the next pass reads y with the warp-per-vector mapping
         if (pass == 1) {
@@ -142,12 +170,18 @@ __global__ void __launch_bounds__(kBlockGsThreads) block_gs_kernel(BlockGsArgs a
     }
     if (ind) {
       const double s = 1.0 / rn;
-      double2* dst = a.V + (a.n_o + acc) * a.D;
-      const double2* src_o = a.O ? a.C + static_cast<int64_t>(a.cand[k]) * a.D : nullptr;
-      double2* dst_o = a.O ? a.O + (a.n_b + acc) * a.D : nullptr;
+      T* dst = V + (a.n_o + acc) * a.D;
+      const T* src_o = a.O ? reinterpret_cast<const T*>(a.C) + static_cast<int64_t>(a.cand[k]) * a.D : nullptr;
+      T* dst_o = a.O ? reinterpret_cast<T*>(a.O) + (a.n_b + acc) * a.D : nullptr;
       for (int64_t e = lo + threadIdx.x; e < hi; e += kBlockGsThreads) {
-        const double2 v = y[e];
-        dst[e] = make_double2(v.x * s - v.y * 0.0, v.x * 0.0 + v.y * s);  // Complex{1/rn, 0} * residual
+        if constexpr (PACKED) {  // append_ah_kernel: V = r / rn, Vw = w V
+          const double x = y[e] * s;
+          dst[e] = x;
+          a.Vw[(a.n_o + acc) * a.D + e] = weight(e) * x;
+        } else {
+          const double2 v = y[e];
+          dst[e] = make_double2(v.x * s - v.y * 0.0, v.x * 0.0 + v.y * s);  // Complex{1/rn, 0} * residual
+        }
         if (dst_o) dst_o[e] = src_o[e];
       }
       ++acc;

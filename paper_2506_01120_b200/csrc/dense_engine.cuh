@@ -770,14 +770,17 @@ private:
     if (!keep_) n_b_ = n_o_;
   }
 
-  // device-resident block decisions (block_gs.cuh): general complex field,
-  // not D-sharded (its sums are grid-local), blocks of two or more survivors
-  bool use_block_gs(int nb) const { return field_ == Field::kComplex && !red_ && nb >= 2 && block_gs_; }
+  // device-resident block decisions (block_gs.cuh): either field, not
+  // D-sharded (its sums are grid-local), blocks of two or more survivors
+  bool use_block_gs(int nb) const { return field_ != Field::kUnset && !red_ && nb >= 2 && block_gs_; }
   bool run_block_gs(int k, int nb) {
     if (!bgs_grid_) {
       int sms = 0, per_sm = 0;
       CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx_->device));
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_gs_kernel, kBlockGsThreads, 0));
+      int per_sm2 = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_gs_kernel<false>, kBlockGsThreads, 0));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, block_gs_kernel<true>, kBlockGsThreads, 0));
+      per_sm = std::min(per_sm, per_sm2);
       if (per_sm < 1) {
         block_gs_ = false;
         return false;
@@ -795,15 +798,18 @@ private:
     }
     ensure_capacity(std::min<int64_t>(cap_ + 2, n_o_ + nb + 2));  // slots for every possible accept
     const int64_t W = vw();
+    const bool packed = field_ == Field::kAntiHerm;
     BlockGsArgs a{};
-    a.X = cplx(X_.p + k * W);
+    a.X = X_.p + k * W;
     a.nb = nb;
     a.cand = idx_.p + k;
-    a.C = cplx(C_.p);
-    a.V = cplx(V_.p);
+    a.C = C_.p;
+    a.V = V_.p;
+    a.Vw = packed ? Vw_.p : nullptr;
     a.n_o = n_o_;
-    a.O = keep_ ? cplx(O_.p) : nullptr;
+    a.O = keep_ ? O_.p : nullptr;
     a.n_b = n_b_;
+    a.d = d_;
     a.rn2 = rn2_.p + k;
     a.D = D_;
     a.inv_d = 1.0 / d_;
@@ -819,8 +825,9 @@ private:
     const int init[2] = {0, -1};
     CU(cudaMemcpyAsync(bgs_status_.p, init, sizeof init, cudaMemcpyHostToDevice, ctx_->stream));
     void* args[] = {&a};
-    CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(block_gs_kernel), dim3(bgs_grid_), dim3(kBlockGsThreads),
-                                   args, 0, ctx_->stream));
+    CU(cudaLaunchCooperativeKernel(packed ? reinterpret_cast<void*>(block_gs_kernel<true>)
+                                          : reinterpret_cast<void*>(block_gs_kernel<false>),
+                                   dim3(bgs_grid_), dim3(kBlockGsThreads), args, 0, ctx_->stream));
     launched(ctx_);
     CU(cudaMemcpyAsync(h_bgs_flags_.p, bgs_flags_.p, nb * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaMemcpyAsync(h_bgs_rn_.p, bgs_rn_.p, nb * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
