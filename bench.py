@@ -587,6 +587,30 @@ def run_c3(a):
     accepted = int(ind.sum())
     even = ind[0::2].all() and not ind[1::2].any()
     ms = sum(times) / len(times)
+    # e2e: the candidate stream (this rank's slice) from pinned host memory
+    # every step through the public session call; verdicts and residual norms
+    # come back to the host inside it
+    e2e = None
+    if not a.no_e2e:
+        host_c = torch.empty(cands.shape, dtype=cands.dtype, pin_memory=True)
+        host_c.copy_(cands)
+        e2e_ms = []
+        for _ in range(a.steps):
+            sess.set_basis(V.data_ptr(), on_device=True, n=c3.n)  # reset (untimed)
+            barrier()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            ind_e, _, _ = sess.check_candidates(host_c.data_ptr(), on_device=False, n=c3.ncand)
+            f1.record(stream)
+            torch.cuda.synchronize(device)
+            e2e_ms.append(max_over_ranks(f0.elapsed_time(f1)))
+            assert (ind_e == ind).all()
+        em = sum(e2e_ms) / len(e2e_ms)
+        e2e = {"value": (c3.ncand if sharded else c3.ncand * world) / (em / 1e3), "unit": "candidates/s",
+               "h2d_bytes_per_step": int(host_c.numel() * 16), "d2h_bytes_per_step": int(c3.ncand * 12),
+               "path": "liecl_b200_session_check_candidates (host pinned candidates, basis resident)"}
+        del host_c
     peak = fp64_peak_tflops(torch, device)
     gms = kt["zgemm_project"]["ms"] + kt["zgemm_subtract"]["ms"]
     gfl = kt["zgemm_project"]["flops"] + kt["zgemm_subtract"]["flops"]
@@ -622,7 +646,7 @@ def run_c3(a):
                          "peak": peak, "unit": "TFLOP/s", "frac": gfl / (gms / 1e3) / 1e12 / peak,
                          "share_of_step": gms / sum(times), "traffic": None,
                          "peak_source": "measured in-run: cuBLAS ZGEMM 4096^3 (torch.matmul complex128)"},
-            "cpu_baseline": cpu, "gpu_launches": launches // max(a.steps, 1), "clocks": clocks.summary()}
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches // max(a.steps, 1), "clocks": clocks.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -669,6 +669,8 @@ class ClosureSession:
     def set_basis(self, V, on_device: bool = False, n: int | None = None):
         """V: (n, width) complex128 host array, or a pointer (int; device memory
         with on_device, else host -- e.g. pinned memory a prefetch_basis started)."""
+        if (on_device or isinstance(V, int)) and n is None:
+            raise InvalidInputError("set_basis with a pointer needs the basis size n")
         if on_device or isinstance(V, int):
             _check(self.lib.liecl_b200_session_set_basis(self.ptr, C.cast(C.c_void_p(V), C.POINTER(C.c_double)),
                                                          C.c_int64(n), C.c_int32(int(on_device))))
@@ -734,7 +736,11 @@ class ClosureSession:
         return out[: n.value]
 
     def check_candidates(self, cands, on_device: bool = False, n: int | None = None):
-        if on_device:
+        """cands: (n, width) complex128 host array, or a pointer (int; device memory
+        with on_device, else host -- e.g. pinned) with the count n."""
+        if on_device or isinstance(cands, int):
+            if n is None:
+                raise InvalidInputError("check_candidates with a pointer needs the candidate count n")
             ptr = C.cast(C.c_void_p(cands), C.POINTER(C.c_double))
         else:
             cands = np.ascontiguousarray(cands, np.complex128)

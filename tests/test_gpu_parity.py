@@ -373,3 +373,22 @@ def test_prefetch_basis_matches_plain_upload():
     assert np.array_equal(s.basis(), B[:5])
     st = s.run_rows(1, 5)
     assert st["commutators_evaluated"] == 10
+
+
+def test_session_accepts_host_pointers():
+    # pinned host buffers passed as pointers (the e2e pattern) = numpy arrays
+    import torch
+    cfg = w.config1()
+    full = liecl.closure_dense_arrays(cfg.generators, cfg.d, liecl.Method.orthonorm_dimonly,
+                                      liecl.ClosureConfig(tolerance=cfg.tol))
+    B = full.basis_array[:10]
+    cands = full.basis_array[10:20] + 0.5 * full.basis_array[:10]
+    s = liecl.ClosureSession(cfg.d, config=liecl.ClosureConfig(tolerance=cfg.tol))
+    s.set_basis(B)
+    ind_a, rn_a, _ = s.check_candidates(cands)
+    hb, hc = torch.from_numpy(B.copy()).pin_memory(), torch.from_numpy(cands.copy()).pin_memory()
+    s.set_basis(hb.data_ptr(), n=len(B))
+    ind_b, rn_b, _ = s.check_candidates(hc.data_ptr(), n=len(cands))
+    assert np.array_equal(ind_a, ind_b) and np.array_equal(rn_a, rn_b) and ind_a.sum() == 10
+    with pytest.raises(liecl.InvalidInputError):
+        s.check_candidates(hc.data_ptr())
