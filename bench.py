@@ -295,7 +295,34 @@ def secondary_closures():
                  "brackets_per_s": r.stats.commutators_evaluated / best}
         entry["cpu_baseline"] = sums_cpu_baseline(off, x, z, c, n, r)
         out[f"{fam}_sums_n{n}"] = entry
+    # the other strategies on dense i*H generators
+    for name, method, specs, n in (("matrix_inversion_hea_n4", liecl.Method.matrix_inversion, w.hea(4), 4),
+                                   ("rank_spin_glass_n3", liecl.Method.standard_rank, w.spin_glass_hva(3), 3)):
+        gens = np.stack([w.vec(1j * w.from_pauli(sp)) for sp in specs])
+        best, r = None, None
+        for _ in range(2):
+            t0 = time.perf_counter()
+            r = liecl.closure_dense_arrays(gens, 1 << n, method, liecl.ClosureConfig(tolerance=1e-10))
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        out[name] = {"dimension": r.dimension, "brackets": r.stats.commutators_evaluated, "seconds": best,
+                     "cpu_baseline": dense_cpu_baseline(gens, 1 << n, liecl.to_string(method), r.dimension)}
     return out
+
+
+def dense_cpu_baseline(gens, d, method, dim):
+    """cpu_baseline leg of a dense closure: the reference build, all host threads."""
+    try:
+        from oracle.oracle import REF_SO, Ref
+    except ImportError:
+        return None
+    if not os.path.exists(REF_SO):
+        return None
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    o = Ref().closure_dense(gens, d, method=method, tol=1e-10, threads=threads)
+    return {"value": time.perf_counter() - t0, "unit": "s", "cores": threads, "kind": "reference",
+            "sample": "the whole closure, same generators", "same_dimension": bool(o.dimension == dim)}
 
 
 def sums_cpu_baseline(off, x, z, c, n, r):

@@ -193,6 +193,25 @@ def xxz_hva(n: int, delta: float = 1.5) -> list:
     return [bond_sum(0), bond_sum(1)]
 
 
+def hea(n: int) -> list:
+    """R:src/generators.cpp:37-53: X_i, Z_i, then Z_i Z_{i+1}, one term each."""
+    return ([PauliSumSpec.from_terms(n, [((1 << i, 0), complex(1.0, 0.0))]) for i in range(n)] +
+            [PauliSumSpec.from_terms(n, [((0, 1 << i), complex(1.0, 0.0))]) for i in range(n)] +
+            [PauliSumSpec.from_terms(n, [((0, (1 << i) | (1 << (i + 1))), complex(1.0, 0.0))])
+             for i in range(n - 1)])
+
+
+def spin_glass_hva(n: int, seed: int = 0) -> list:
+    """R:src/generators.cpp:55-77: H1 = sum_i a_i Z_i + sum_{i<j} J_ij Z_i Z_j
+    (seeded uniform(-1, 1), a first, then J in (i, j) order), H2 = sum_i X_i."""
+    rng = SplitMix64(seed)
+    sym = lambda: 2.0 * rng.uniform() - 1.0  # uniform_symmetric, R:include/liecl/rng.hpp:36
+    h1 = [((0, 1 << i), complex(sym(), 0.0)) for i in range(n)]
+    h1 += [((0, (1 << i) | (1 << j)), complex(sym(), 0.0)) for i in range(n) for j in range(i + 1, n)]
+    h2 = [((1 << i, 0), complex(1.0, 0.0)) for i in range(n)]
+    return [PauliSumSpec.from_terms(n, h1), PauliSumSpec.from_terms(n, h2)]
+
+
 def sum_arrays(sums) -> tuple:
     """(offsets, x, z, coef (t, 2)) of a list of PauliSumSpec, the C-ABI layout."""
     off, xs, zs, cs = [0], [], [], []

@@ -180,7 +180,8 @@ def test_exact_reference_build_reproduces_sum_fixtures(ref_exact, golden, tag):
     assert np.array_equal(bo, g["offsets"]) and np.array_equal(bc.view(np.uint64), g["coef_bits"])
 
 
-@pytest.mark.parametrize("family,n", [("tfim_hva_open", 4), ("tfim_hva_open", 20), ("xxz_hva", 6), ("xxz_hva", 10)])
+@pytest.mark.parametrize("family,n", [("tfim_hva_open", 4), ("tfim_hva_open", 20), ("xxz_hva", 6), ("xxz_hva", 10),
+                                      ("hea", 4), ("spin_glass_hva", 3), ("spin_glass_hva", 5)])
 def test_hva_generators_match_reference_catalog(ref, family, n):
     # workloads.py restates the catalog so bench.py needs no oracle for inputs
     mine = w.sum_arrays(getattr(w, family)(n))
