@@ -253,7 +253,8 @@ def secondary_closures():
                                        liecl.ClosureConfig(tolerance=cfg.tol))
         dt = time.perf_counter() - t0
         out[name] = {"dimension": r.dimension, "brackets": r.stats.commutators_evaluated, "seconds": dt,
-                     "brackets_per_s": r.stats.commutators_evaluated / dt}
+                     "brackets_per_s": r.stats.commutators_evaluated / dt,
+                     "cpu_baseline": dense_cpu_baseline(cfg.generators, cfg.d, "orthonorm-dimonly", r.dimension)}
     p = w.config4()
     liecl.closure_pauli_arrays(p.x, p.z, p.coef, p.qubits, liecl.Method.orthonorm_dimonly,
                                liecl.ClosureConfig(tolerance=p.tol))
@@ -263,6 +264,11 @@ def secondary_closures():
     dt = time.perf_counter() - t0
     out["c4"] = {"dimension": r.dimension, "brackets": r.stats.commutators_evaluated, "seconds": dt,
                  "brackets_per_s": r.stats.commutators_evaluated / dt}
+    bx, bz, bc = r.basis_array  # one term per element
+    out["c4"]["cpu_baseline"] = sums_cpu_baseline(
+        np.arange(len(p.x) + 1, dtype=np.int64), np.asarray(p.x, np.uint64), np.asarray(p.z, np.uint64),
+        np.asarray(p.coef, np.float64).reshape(-1, 2), p.qubits, r.dimension,
+        (np.arange(r.dimension + 1, dtype=np.int64), bx, bz, bc))
     # PAPER.md §4.2 sparse-Pauli HEA (dims 4095 / 16383; the paper: 429 s / 2345 s
     # on "a many-core CPU"): per-qubit X, Z and nearest-neighbour ZZ strings
     for n in (6, 7):
@@ -293,7 +299,7 @@ def secondary_closures():
         entry = {"dimension": r.dimension, "brackets": r.stats.commutators_evaluated,
                  "terms": int(r.basis_array[0][-1]), "seconds": best,
                  "brackets_per_s": r.stats.commutators_evaluated / best}
-        entry["cpu_baseline"] = sums_cpu_baseline(off, x, z, c, n, r)
+        entry["cpu_baseline"] = sums_cpu_baseline(off, x, z, c, n, r.dimension, r.basis_array)
         out[f"{fam}_sums_n{n}"] = entry
     # the other strategies on dense i*H generators
     for name, method, specs, n in (("matrix_inversion_hea_n4", liecl.Method.matrix_inversion, w.hea(4), 4),
@@ -325,10 +331,11 @@ def dense_cpu_baseline(gens, d, method, dim):
             "sample": "the whole closure, same generators", "same_dimension": bool(o.dimension == dim)}
 
 
-def sums_cpu_baseline(off, x, z, c, n, r):
-    """cpu_baseline leg of a multi-term closure: the reference built with its
+def sums_cpu_baseline(off, x, z, c, n, dim, basis):
+    """cpu_baseline leg of a Pauli closure: the reference built with its
     default rounding (oracle/_ref/libliecl_ref_exact.so), all host threads,
-    same generators; also the bit-exact check of the GPU basis against it."""
+    same generators; also the bit-exact check of the GPU basis (offsets, x, z,
+    coef) against it."""
     try:
         from oracle.oracle import REF_EXACT_SO, Ref
     except ImportError:
@@ -339,10 +346,10 @@ def sums_cpu_baseline(off, x, z, c, n, r):
     ref = Ref(REF_EXACT_SO)
     t0 = time.perf_counter()
     o = ref.closure_pauli(off, x, z, c, n, method="orthonorm-dimonly", tol=1e-10, threads=threads,
-                          basis_cap=r.dimension + 1, term_cap=max(1 << 20, 4 * int(r.basis_array[0][-1])))
+                          basis_cap=dim + 1, term_cap=max(1 << 20, 4 * int(basis[0][-1])))
     secs = time.perf_counter() - t0
     same = all(np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64))
-               for a, b in zip(r.basis_array, o.basis))
+               for a, b in zip(basis, o.basis))
     return {"value": secs, "unit": "s", "cores": threads, "kind": "reference",
             "sample": "the whole closure, same generators", "bit_exact": bool(same)}
 
