@@ -106,3 +106,19 @@ def test_no_device_fails_loudly_without_deadlock():
     import numpy as np
     with pytest.raises((native.NativeUnavailable, liecl.Error)):
         liecl.run_closure([liecl.DenseOperator(np.eye(2))], liecl.Method.standard_rank)
+
+
+def test_header_is_plain_c_and_links():
+    # the C-ABI is C: a C11 translation unit includes the header and links the library
+    import shutil
+    import subprocess
+    import tempfile
+    gcc = shutil.which("gcc")
+    if not gcc:
+        pytest.skip("gcc missing")
+    with tempfile.TemporaryDirectory() as tmp:
+        exe = os.path.join(tmp, "c_abi_demo")
+        r = subprocess.run([gcc, "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                            os.path.join(ROOT, "examples", "c_abi_demo.c"), "-L", os.path.dirname(native.LIB_PATH),
+                            "-lliecl_b200", "-o", exe], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
