@@ -455,7 +455,18 @@ def run_closure(generators, method: Method, config: ClosureConfig | None = None,
 
 def close_orthonormalization(generators, config: ClosureConfig | None = None, keep_original: bool = True,
                              device: int = 0) -> ClosureResult:
+    """R:include/liecl/closure.hpp:119-121 (Alg. 3 / dimension only)."""
     return run_closure(generators, Method.orthonorm if keep_original else Method.orthonorm_dimonly, config, device)
+
+
+def close_matrix_inversion(generators, config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
+    """R:include/liecl/closure.hpp:112-113 (Alg. 2); result.gram = (A, A^-1)."""
+    return run_closure(generators, Method.matrix_inversion, config, device)
+
+
+def close_standard(generators, config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
+    """R:include/liecl/closure.hpp:107-108 (Alg. 1, the rank method; dense generators)."""
+    return run_closure(generators, Method.standard_rank, config, device)
 
 
 # ------------------------------------------------- I/O plumbing (§8 f3) ----

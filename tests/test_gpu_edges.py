@@ -87,3 +87,13 @@ def test_session_window_past_basis_is_rejected():
     s.set_basis(full.basis_array[:3])
     with pytest.raises(liecl.InvalidInputError):
         s.run_pairs(0, 100)  # pair 3 needs basis element 3, which does not exist yet
+
+
+def test_reference_named_entry_points():
+    cfg = w.config0()
+    gens = [liecl.DenseOperator.from_vec(g, cfg.d) for g in cfg.generators]
+    conf = liecl.ClosureConfig(tolerance=cfg.tol)
+    assert liecl.close_standard(gens, conf).dimension == 9
+    r = liecl.close_matrix_inversion(gens, conf)
+    assert r.dimension == 9 and r.gram[0].shape == (9, 9)
+    assert liecl.close_orthonormalization(gens, conf).dimension == 9
