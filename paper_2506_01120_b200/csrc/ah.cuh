@@ -140,10 +140,10 @@ __device__ __forceinline__ void ah_elem(const double* p, int i, int k, double& r
 // fragments gathered straight from the packed inputs in shared memory; each
 // warp owns whole tile rows of P (A fragments reused across the row); P is
 // written back over the consumed inputs and h = P - P^dagger is read out in
-// the packed layout. ~70 KB per pair at d = 64: three CTAs per SM overlap
-// their load and compute phases.
+// the packed layout. ~70 KB per pair at d = 64: three CTAs per SM (80
+// registers, full carveout) overlap their load and compute phases.
 template <int DIM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, double tol, bool normalize,
                      double* __restrict__ out, double* __restrict__ hnorm, int* __restrict__ is_null) {
   using S = CommAhShape<DIM>;

@@ -577,6 +577,8 @@ private:
     static bool attr = false;
     if (!attr) {
       CU(cudaFuncSetAttribute(commutator_ah_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, SA::SMEM));
+      // the full shared-memory carveout: three ~70 KB CTAs per SM
+      CU(cudaFuncSetAttribute(commutator_ah_kernel<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       attr = true;
     }
     const int blocks = (cnt + SA::PAIRS_PER_CTA - 1) / SA::PAIRS_PER_CTA;

@@ -171,7 +171,22 @@ dgemm_dmma_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
       const int gm = m0 + wm * WTM + i * 8 + g;
-      if (gm >= M) continue;
+      if (gm >= M) {
+        // pad rows M <= row < ldc (the even leading dimension of beta) are
+        // written as zeros: the subtract GEMM reads one row past an odd basis
+        // count, where V is zero and beta must be finite (0 * NaN from a
+        // recycled workspace would poison the residual)
+        if (gm < ldc) {
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int gn = n0 + wn * WTN + j * 8 + 2 * t + h;
+              if (gn < N) Cout[static_cast<int64_t>(gn) * ldc + gm] = 0.0;
+            }
+        }
+        continue;
+      }
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll
