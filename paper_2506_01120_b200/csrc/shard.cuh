@@ -35,8 +35,11 @@ struct NcclApi {
 
 inline const NcclApi& nccl_api() {
   static const NcclApi api = [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);  // torch's copy, if loaded
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // an already-resident copy first (torch's bundled build: the Python layer
+    // imports torch before calling here), else the system's; local scope so
+    // its symbols do not leak into later loads
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) throw Error(LIECL_B200_CUDA, std::string("cannot load libnccl.so.2: ") + dlerror());
     NcclApi a;
     auto sym = [&](const char* name) {

@@ -616,8 +616,19 @@ def shard_range(d: int, nranks: int, rank: int) -> tuple[int, int]:
     return lo.value, hi.value
 
 
+def _resident_nccl() -> None:
+    """Make torch's NCCL the process's libnccl.so.2 before the engine dlopens
+    one: a later `import torch` would otherwise bind libtorch_cuda to whichever
+    libnccl.so.2 is already loaded (an older system copy lacks its symbols)."""
+    try:
+        import torch  # noqa: F401  (loads libtorch_cuda and its bundled libnccl)
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """A fresh NCCL unique id (128 bytes) for ClosureSession.set_shards."""
+    _resident_nccl()
     buf = (C.c_uint8 * 128)()
     _check(native.load().liecl_b200_nccl_unique_id(buf))
     return bytes(buf)
@@ -648,6 +659,7 @@ class ClosureSession:
         if nccl_id is not None:
             if len(nccl_id) != 128:
                 raise InvalidInputError("an NCCL unique id is 128 bytes")
+            _resident_nccl()
             buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             _check(self.lib.liecl_b200_session_set_shards(self.ptr, C.c_int32(nranks), C.c_int32(rank), buf,
                                                           native.ReduceFn(), None))
