@@ -597,10 +597,12 @@ private:
     run_pair_batch(g, static_cast<int>(cnt));
     const uint64_t acc = st_.accepted - before;
     if (acc == 0) B_cur_ = std::min<int64_t>(2 * B_cur_, bmax_);
-    else if (acc * 4 > static_cast<uint64_t>(cnt)) B_cur_ = std::max<int64_t>(64, B_cur_ / 2);
+    else if (acc * 4 > static_cast<uint64_t>(cnt))  // floor 64, never above the cap the buffers are sized for
+      B_cur_ = std::max<int64_t>(std::min<int64_t>(64, bmax_), B_cur_ / 2);
   }
 
   void run_pair_batch(int64_t g0, int cnt) {
+    if (cnt > bmax_) throw Error(LIECL_B200_INTERNAL, "pair batch exceeds the batch buffers");
     launch_commutators(g0, cnt);
     project(V_.p, Vw_.p, n_o_, C_.p, cnt, R_.p, rn1_.p);
     CU(cudaMemcpyAsync(h_nul_.p, nul_.p, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));

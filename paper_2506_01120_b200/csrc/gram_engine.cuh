@@ -152,7 +152,7 @@ public:
       g += cnt;
       const uint64_t acc = st_.accepted - before;
       if (acc == 0) B = std::min<int64_t>(2 * B, bmax_);
-      else if (acc * 4 > static_cast<uint64_t>(cnt)) B = std::max<int64_t>(64, B / 2);
+      else if (acc * 4 > static_cast<uint64_t>(cnt)) B = std::max<int64_t>(std::min<int64_t>(64, bmax_), B / 2);
     }
   }
 

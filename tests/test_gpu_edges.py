@@ -97,3 +97,53 @@ def test_reference_named_entry_points():
     r = liecl.close_matrix_inversion(gens, conf)
     assert r.dimension == 9 and r.gram[0].shape == (9, 9)
     assert liecl.close_orthonormalization(gens, conf).dimension == 9
+
+
+def _random_ah(rng, d, k):
+    m = rng.standard_normal((k, d, d)) + 1j * rng.standard_normal((k, d, d))
+    return np.stack([(a - a.conj().T).ravel(order="F") for a in m])
+
+
+@pytest.mark.parametrize("field", ["auto", "complex"])
+def test_batch_cap_below_the_adaptive_floor(field):
+    """batch_max under 64: the adaptive batch used to halve back UP to 64 and
+    overrun buffers sized for batch_max (d = 16, growth phase accepts)."""
+    rng = np.random.default_rng(5)
+    gens = _random_ah(rng, 16, 2)
+    base = liecl.closure_dense_arrays(gens, 16, liecl.Method.orthonorm_dimonly,
+                                      liecl.ClosureConfig(tolerance=1e-10, field=field))
+    assert base.dimension >= 255  # u(16) (su(16) when traceless)
+    for bs in (1, 16, 63):
+        r = liecl.closure_dense_arrays(gens, 16, liecl.Method.orthonorm_dimonly,
+                                       liecl.ClosureConfig(tolerance=1e-10, field=field, batch_max=bs))
+        assert r.dimension == base.dimension, bs
+        assert np.abs(r.basis_array - base.basis_array).max() < 1e-9, bs
+
+
+def test_batch_cap_below_floor_matrix_inversion():
+    # HEA n = 3: orthogonal Pauli directions, Gram condition 1 (random dense
+    # generators of u(8) are past Alg. 2's conditioning: the reference itself
+    # raises CapacityError on them)
+    gens = np.stack([w.vec(1j * w.from_pauli(sp)) for sp in w.hea(3)])
+    base = liecl.closure_dense_arrays(gens, 8, liecl.Method.matrix_inversion, liecl.ClosureConfig(tolerance=1e-10))
+    assert base.dimension == 63
+    for bs in (1, 16):
+        r = liecl.closure_dense_arrays(gens, 8, liecl.Method.matrix_inversion,
+                                       liecl.ClosureConfig(tolerance=1e-10, batch_max=bs))
+        assert r.dimension == base.dimension, bs
+
+
+@pytest.mark.parametrize("field", ["auto", "complex"])
+def test_rounding_decided_input_is_flagged(field):
+    """tests/golden/illcond_pauli_d16.npy: sparse Pauli-sum generators whose
+    closure accepts residuals within 10x of tol (the reference build itself
+    reaches 256, its C restatement 30). Any verdict there is rounding; the
+    contract is the reference's: finish within D and raise the
+    borderline_residual warning (R:src/closure.cpp:325-336)."""
+    import os
+    gens = np.load(os.path.join(os.path.dirname(__file__), "golden", "illcond_pauli_d16.npy"))
+    r = liecl.closure_dense_arrays(gens, 16, liecl.Method.orthonorm_dimonly,
+                                   liecl.ClosureConfig(tolerance=1e-10, field=field))
+    assert 30 <= r.dimension <= 256
+    kinds = {w.kind for w in r.stats.warnings}
+    assert "borderline_residual" in kinds

@@ -5,6 +5,7 @@ the C restatement and the reference build."""
 import numpy as np
 import pytest
 
+from oracle.conditioning import dense_sensitivity
 from paper_2506_01120_b200 import liecl
 
 pytestmark = pytest.mark.gpu
@@ -25,16 +26,25 @@ def random_antiherm_pauli(rng, n, k):
     return np.stack([o.ravel(order="F") for o in ops])
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(16))
 def test_dense_random_closures_vs_port(port, seed):
     rng = np.random.default_rng(1000 + seed)
-    n = int(rng.integers(2, 5))
+    n = int(rng.integers(2, 6))
     d = 1 << n
     gens = random_antiherm_pauli(rng, n, int(rng.integers(2, 4)))
     if seed % 3 == 0:
         gens = np.concatenate([gens, gens[:1] * (2 - 1j)])  # a dependent (complex multiple) generator
     for method in (DIMONLY, KEEP):
         o = port.closure_dense(gens, d, keep_original=(method == KEEP), tol=1e-10)
+        if dense_sensitivity(o.log, o.basis, d, 1e-10)["sensitive"]:
+            # verdicts rounding-decided for ANY implementation (oracle/conditioning.py):
+            # only the reference's contract holds - finish or raise its CapacityError
+            for field in ("auto", "complex"):
+                try:
+                    liecl.closure_dense_arrays(gens, d, method, liecl.ClosureConfig(tolerance=1e-10, field=field))
+                except liecl.CapacityError:
+                    pass
+            continue
         for field in ("auto", "complex"):
             r = liecl.closure_dense_arrays(gens, d, method, liecl.ClosureConfig(tolerance=1e-10, field=field,
                                                                                 record_log=True))

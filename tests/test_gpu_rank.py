@@ -64,3 +64,18 @@ def test_rank_method_rejects_pauli_and_honours_capacity():
     cfg = w.config0()
     with pytest.raises(liecl.CapacityError):
         liecl.closure_dense_arrays(cfg.generators, cfg.d, RANK, liecl.ClosureConfig(tolerance=cfg.tol, max_dim=4))
+
+
+def test_small_bracket_rank_tolerance():
+    """tests/golden/rank_small_bracket_d8.npy: a bracket of norm 1.7e-4 turns
+    1-ulp input differences into ~1e-12 out-of-span noise, 50x the default
+    rank threshold eps * d^2 (R:src/dense.cpp:133-137) -- there the verdict is
+    rounding for any implementation (oracle/conditioning.py). With an explicit
+    rank_tolerance the closure is well defined: the reference build's 11."""
+    import os
+    gens = np.load(os.path.join(os.path.dirname(__file__), "golden", "rank_small_bracket_d8.npy"))
+    r = liecl.closure_dense_arrays(gens, 8, liecl.Method.standard_rank,
+                                   liecl.ClosureConfig(tolerance=1e-10, rank_tolerance=1e-10))
+    assert r.dimension == 11
+    o = liecl.closure_dense_arrays(gens, 8, liecl.Method.orthonorm, liecl.ClosureConfig(tolerance=1e-10))
+    assert o.dimension == 11

@@ -188,3 +188,20 @@ def test_hva_generators_match_reference_catalog(ref, family, n):
     theirs = ref.build_generators(family, n)
     for a, b in zip(mine, theirs):
         assert np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64))
+
+
+def test_conditioning_predicate(ref):
+    """oracle/conditioning.py flags the rounding-decided fixture (the reference
+    accepts a residual of 1.19e-10 at tol 1e-10) and passes a clean closure."""
+    import os
+    from oracle.conditioning import dense_sensitivity
+    gens = np.load(os.path.join(os.path.dirname(__file__), "golden", "illcond_pauli_d16.npy"))
+    o = ref.decision_log_dense(gens, 16, tol=1e-10)
+    s = dense_sensitivity(o.log, o.basis, 16, 1e-10)
+    assert s["sensitive"] and s["band"] >= 1
+    # su(2) from i X, i Z: brackets of unit norm, residuals 0 or 1
+    X = np.array([[0, 1], [1, 0]], complex); Z = np.diag([1.0, -1.0]).astype(complex)
+    g = np.stack([(1j * X).ravel(order="F"), (1j * Z).ravel(order="F")])
+    o = ref.decision_log_dense(g, 2, tol=1e-10)
+    assert o.dimension == 3
+    assert not dense_sensitivity(o.log, o.basis, 2, 1e-10)["sensitive"]
