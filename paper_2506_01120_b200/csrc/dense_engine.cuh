@@ -190,8 +190,7 @@ public:
     CU(cudaMemcpyAsync(tiny_gens_.p, gens_host, static_cast<size_t>(ngens * D_) * sizeof(double2),
                        cudaMemcpyHostToDevice, ctx_->stream));
     if (smem > 48 * 1024)
-      CU(cudaFuncSetAttribute(tiny_closure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(smem)));
+      func_attr_once(tiny_closure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     tiny_closure_kernel<<<1, tiny_threads(d_), smem, ctx_->stream>>>(tiny_gens_.p, ngens, d_, tol_, cap_,
                                                                      keep_ ? 1 : 0, slots, tiny_v_.p, tiny_o_.p,
                                                                      tiny_state_.p, tiny_log_.p, log_cap);
@@ -560,11 +559,7 @@ private:
   }
   template <int DIM> void launch_comm(const double2* basis, int64_t g0, int cnt) {
     using S = CommShape<DIM>;
-    static bool attr = false;
-    if (!attr) {
-      CU(cudaFuncSetAttribute(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-      attr = true;
-    }
+    func_attr_once(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
     const int blocks = (cnt + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA;
     Timer t(ctx_, 2, 16.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
     commutator_norm_kernel<DIM><<<blocks, 256, S::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, cplx(C_.p),
@@ -574,13 +569,9 @@ private:
   }
   template <int DIM> void launch_comm_ah(const double* basis, int64_t g0, int cnt) {
     using SA = CommAhShape<DIM>;
-    static bool attr = false;
-    if (!attr) {
-      CU(cudaFuncSetAttribute(commutator_ah_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, SA::SMEM));
-      // the full shared-memory carveout: three ~70 KB CTAs per SM
-      CU(cudaFuncSetAttribute(commutator_ah_kernel<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      attr = true;
-    }
+    func_attr_once(commutator_ah_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, SA::SMEM);
+    // the full shared-memory carveout: three ~70 KB CTAs per SM
+    func_attr_once(commutator_ah_kernel<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     const int blocks = (cnt + SA::PAIRS_PER_CTA - 1) / SA::PAIRS_PER_CTA;
     Timer t(ctx_, 2, 8.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
     commutator_ah_kernel<DIM><<<blocks, 256, SA::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, C_.p, hn_.p,

@@ -47,14 +47,23 @@ void check(int status) {
   if (status != LIECL_B200_OK) raise(status);
 }
 
-// One device context per process (stream + workspaces), created on first use.
+// One device context per calling thread (stream + workspaces + cached
+// engines), created on first use and released at thread exit: the reference's
+// entry points are reentrant (R:include/liecl/closure.hpp:94-96), and a
+// context serves one caller at a time (include/liecl_b200.h).
+struct ThreadContext {
+  liecl_b200_ctx* ctx = nullptr;
+  int status = LIECL_B200_OK;
+  ThreadContext() { status = liecl_b200_ctx_create(0, &ctx); }
+  ~ThreadContext() {
+    if (ctx) liecl_b200_ctx_destroy(ctx);
+  }
+};
+
 liecl_b200_ctx* context() {
-  static std::once_flag once;
-  static liecl_b200_ctx* ctx = nullptr;
-  static int status = LIECL_B200_OK;
-  std::call_once(once, [] { status = liecl_b200_ctx_create(0, &ctx); });
-  if (status != LIECL_B200_OK) raise(status);
-  return ctx;
+  thread_local ThreadContext t;
+  if (t.status != LIECL_B200_OK) raise(t.status);
+  return t.ctx;
 }
 
 liecl_b200_config to_native(const ClosureConfig& c) {

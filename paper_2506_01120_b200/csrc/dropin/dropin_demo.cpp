@@ -4,7 +4,9 @@
 // test (tests/test_gpu_dropin.py) compares it with the golden fixtures.
 #include <complex>
 #include <cstdio>
+#include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "liecl/closure.hpp"
@@ -122,7 +124,61 @@ int main() {
     } catch (const CapacityError&) {
       threw = true;
     }
-    std::printf("\"capacity_error\": %s", threw ? "true" : "false");
+    std::printf("\"capacity_error\": %s, ", threw ? "true" : "false");
+  }
+  // concurrent callers (the reference's entry points are reentrant): four
+  // threads, each closing config 0 densely and a 6-qubit HEA as Pauli strings;
+  // every result must equal the serial one bit for bit
+  {
+    const std::uint32_t n = 3;
+    std::vector<PauliSum::Term> t0, t1;
+    for (std::uint32_t j = 0; j < n; ++j) t0.push_back({PauliString{1ull << j, 0, n}, I});
+    for (std::uint32_t j = 0; j + 1 < n; ++j) t1.push_back({PauliString{0, (1ull << j) | (1ull << (j + 1)), n}, I});
+    const std::vector<Operator> dense{Operator(from_pauli(PauliSum::from_terms(n, t0))),
+                                      Operator(from_pauli(PauliSum::from_terms(n, t1)))};
+    std::vector<Operator> strings;
+    for (std::uint32_t j = 0; j < 6; ++j) {
+      const std::vector<PauliSum::Term> x{{PauliString{1ull << j, 0, 6}, Complex{1.0, 0.0}}};
+      const std::vector<PauliSum::Term> z{{PauliString{0, 1ull << j, 6}, Complex{1.0, 0.0}}};
+      strings.emplace_back(PauliSum::from_terms(6, x));
+      strings.emplace_back(PauliSum::from_terms(6, z));
+    }
+    auto fingerprint = [](const ClosureResult& r) {
+      std::vector<double> f{static_cast<double>(r.dimension), static_cast<double>(r.stats.commutators_evaluated)};
+      for (const Operator& b : r.basis) {
+        if (b.backend() == Backend::dense) {
+          const auto& m = b.dense().matrix();
+          for (Eigen::Index e = 0; e < m.size(); ++e) f.push_back(m(e).real()), f.push_back(m(e).imag());
+        } else {
+          for (const auto& t : b.pauli().terms())
+            f.push_back(static_cast<double>(t.string.x)), f.push_back(static_cast<double>(t.string.z)),
+                f.push_back(t.coefficient.real()), f.push_back(t.coefficient.imag());
+        }
+      }
+      return f;
+    };
+    const auto want_d = fingerprint(run_closure(dense, Method::orthonorm_dimonly, cfg));
+    const auto want_p = fingerprint(run_closure(strings, Method::orthonorm_dimonly, cfg));
+    std::vector<int> ok(4, 0);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < 4; ++t)
+      pool.emplace_back([&, t] {
+        try {
+          bool good = true;
+          for (int rep = 0; rep < 3; ++rep) {
+            const auto d = fingerprint(run_closure(dense, Method::orthonorm_dimonly, cfg));
+            const auto p = fingerprint(run_closure(strings, Method::orthonorm_dimonly, cfg));
+            good = good && d.size() == want_d.size() && p.size() == want_p.size() &&
+                   std::memcmp(d.data(), want_d.data(), d.size() * sizeof(double)) == 0 &&
+                   std::memcmp(p.data(), want_p.data(), p.size() * sizeof(double)) == 0;
+          }
+          ok[t] = good ? 1 : 0;
+        } catch (...) {
+          ok[t] = 0;
+        }
+      });
+    for (auto& th : pool) th.join();
+    std::printf("\"concurrent_identical\": %s", (ok[0] && ok[1] && ok[2] && ok[3]) ? "true" : "false");
   }
   std::printf("}\n");
   return 0;

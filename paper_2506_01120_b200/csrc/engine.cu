@@ -37,8 +37,11 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/liecl_b200.h"
@@ -235,13 +238,24 @@ bool borderline(double rn, double tol) {  // R:src/closure.cpp:328-329
 
 // ------------------------------------------------------------ GEMM launch ---
 
+// Function attributes are per device context: a process may drive several
+// devices (one context each), so "already set" is remembered per
+// (kernel, device, attribute, value), under a lock (contexts may be created
+// from several threads).
+template <class K> void func_attr_once(K* kernel, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int, int>> done;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, static_cast<int>(attr), value);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return;
+  CU(cudaFuncSetAttribute(kernel, attr, value));
+  done.insert(key);
+}
+
 template <bool KC, bool CJ, Epilogue E> void gemm_attr_once() {
-  static bool done = false;
-  if (!done) {
-    CU(cudaFuncSetAttribute(zgemm_dmma_kernel<KC, CJ, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            zg::smem_bytes<KC>()));
-    done = true;
-  }
+  func_attr_once(zgemm_dmma_kernel<KC, CJ, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, zg::smem_bytes<KC>());
 }
 
 // Split-K slice count for a grid of `tiles` CTAs over a reduction of length K:
@@ -319,12 +333,7 @@ void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, 
 // ------------------------------------------------ packed-real GEMM launch ---
 
 template <bool KC, REpi E> void rgemm_attr_once() {
-  static bool done = false;
-  if (!done) {
-    CU(cudaFuncSetAttribute(dgemm_dmma_kernel<KC, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            rg::smem_bytes<KC>()));
-    done = true;
-  }
+  func_attr_once(dgemm_dmma_kernel<KC, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, rg::smem_bytes<KC>());
 }
 
 // P[n x count] (ld ldp) = alpha * Vw[:, 0:n]^T X   -- beta on the packed path
@@ -424,11 +433,7 @@ void launch_commutator_complex(liecl_b200_ctx* ctx, const double2* basis, int d,
   auto tmpl = [&](auto dimc) {
     constexpr int DIM = decltype(dimc)::value;
     using S = CommShape<DIM>;
-    static bool attr = false;
-    if (!attr) {
-      CU(cudaFuncSetAttribute(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-      attr = true;
-    }
+    func_attr_once(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
     Timer t(ctx, 2, 16.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
     commutator_norm_kernel<DIM><<<(cnt + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA, 256, S::SMEM, ctx->stream>>>(
         basis, g0, cnt, tol, true, out, hn, nul);
@@ -1107,7 +1112,7 @@ int liecl_b200_commutator_dense(liecl_b200_ctx* ctx, const double* a, const doub
     auto launch = [&](auto dimc) {
       constexpr int DIM = decltype(dimc)::value;
       using S = CommShape<DIM>;
-      CU(cudaFuncSetAttribute(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
+      func_attr_once(commutator_norm_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
       commutator_norm_kernel<DIM><<<1, 256, S::SMEM, ctx->stream>>>(basis.p, 0, 1, -1.0, false, o.p, hn.p, nul.p);
       launched(ctx);
     };

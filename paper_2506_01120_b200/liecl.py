@@ -646,7 +646,9 @@ class ClosureSession:
         cfg = (config or ClosureConfig()).native()
         self.ptr = C.c_void_p()
         self._reduce = None
-        _check(self.lib.liecl_b200_session_create_dense(ctx if ctx is not None else native.context(device),
+        # the session is bound to a context: keep this thread's alive with it
+        self._ctx_ref = native.context_ref(device) if ctx is None else None
+        _check(self.lib.liecl_b200_session_create_dense(ctx if ctx is not None else self._ctx_ref.ptr,
                                                         C.c_int32(d), C.c_int32(int(keep_original)), C.byref(cfg),
                                                         C.byref(self.ptr)))
 

@@ -88,20 +88,44 @@ def last_error() -> str:
     return load().liecl_b200_last_error().decode(errors="replace")
 
 
-_contexts: dict = {}
+class _Context:
+    """Owns one liecl_b200_ctx; destroyed when the last reference goes."""
+
+    def __init__(self, device: int):
+        lib = load()
+        self.ptr = C.c_void_p()
+        if lib.liecl_b200_ctx_create(C.c_int(device), C.byref(self.ptr)) != OK:
+            raise NativeUnavailable(f"liecl_b200_ctx_create(device={device}) failed: {last_error()}")
+        self._lib = lib
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self._lib.liecl_b200_ctx_destroy(self.ptr)
+                self.ptr = C.c_void_p()
+        except Exception:  # interpreter shutdown
+            pass
+
+
+_tls = threading.local()
+
+
+def context_ref(device: int = 0) -> _Context:
+    """This thread's context for `device` (include/liecl_b200.h: one context
+    per device and caller thread -- a context's stream, workspaces and cached
+    engines are not shared between concurrent callers). Holders that outlive
+    the call (sessions) keep the returned object."""
+    ctxs = getattr(_tls, "contexts", None)
+    if ctxs is None:
+        ctxs = _tls.contexts = {}
+    if device not in ctxs:
+        ctxs[device] = _Context(device)
+    return ctxs[device]
 
 
 def context(device: int = 0) -> C.c_void_p:
-    """Process-wide context for `device` (stream + workspaces)."""
-    lib = load()
-    with _lock:
-        if device not in _contexts:
-            ctx = C.c_void_p()
-            st = lib.liecl_b200_ctx_create(C.c_int(device), C.byref(ctx))
-            if st != OK:
-                raise NativeUnavailable(f"liecl_b200_ctx_create(device={device}) failed: {last_error()}")
-            _contexts[device] = ctx
-        return _contexts[device]
+    """This thread's context pointer for `device` (see context_ref)."""
+    return context_ref(device).ptr
 
 
 def new_context(device: int = 0) -> C.c_void_p:

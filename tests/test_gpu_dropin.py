@@ -94,3 +94,9 @@ def test_dropin_rank_method(demo, ref):
         assert r[k] == theirs.stats[k]
     basis = np.array(r["basis"]).reshape(9, -1, 2)
     assert np.abs(basis[..., 0] + 1j * basis[..., 1] - theirs.basis).max() < 1e-10
+
+
+def test_dropin_concurrent_callers(demo):
+    """liecl::run_closure from four threads at once (one device context per
+    calling thread): every result bit-identical to the serial run."""
+    assert demo["concurrent_identical"] is True
