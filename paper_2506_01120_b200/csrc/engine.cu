@@ -34,6 +34,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>

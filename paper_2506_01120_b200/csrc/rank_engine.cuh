@@ -15,14 +15,29 @@
 // (Hestenes) Jacobi SVD on T -- high relative accuracy -- and counts. The
 // relative threshold is invariant under the 1/sqrt(d) scaling of the
 // reference inner product that V and R use.
+//
+// Certified screen (most candidates never need the SVD). Every column of T
+// is the coordinate vector of a unit operator, so 1 <= sigma_max(T) <=
+// sqrt(n+1); the last row of T is rho e_n, so sigma_min(T) <= rho; and with
+// T^{-1} = [[R^{-1}, -R^{-1} beta / rho], [0, 1/rho]] and |beta| <= 1,
+//   sigma_min(T) >= 1 / sqrt(F + (F + 1) / rho^2),   F = ||R^{-1}||_F^2,
+// where F is kept exactly up to rounding on the host (an O(n^2)
+// back-substitution per accept). A candidate is dependent if rho < thr / 8,
+// independent if that lower bound >= 8 thr sqrt(n+1) -- both a factor 8
+// clear of the threshold, where the Jacobi SVD's rounding (~m eps sigma_max)
+// cannot reach -- and otherwise goes to the Jacobi kernel as before.
+// LIECL_B200_RANK_SCREEN=0 sends every candidate to the SVD.
 
 // T of candidate j (m = n + 1 columns, m_pad even, column-major in W_j):
 // columns < n from R (upper triangle, ld ldr), column n = (beta_j, rho_j),
 // padding column zero.
+// sel (optional): slot blockIdx.y builds the T of candidate sel[slot].
 __global__ void rank_build_t_kernel(const double2* __restrict__ R, int64_t ldr, int n, const double2* __restrict__ beta,
-                                    int64_t ldb, const double* __restrict__ rho, int m_pad, double2* __restrict__ W) {
-  const int j = blockIdx.y;
-  double2* T = W + static_cast<int64_t>(j) * m_pad * m_pad;
+                                    int64_t ldb, const double* __restrict__ rho, int m_pad, double2* __restrict__ W,
+                                    const int* __restrict__ sel) {
+  const int slot = blockIdx.y;
+  const int j = sel ? sel[slot] : slot;
+  double2* T = W + static_cast<int64_t>(slot) * m_pad * m_pad;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < static_cast<int64_t>(m_pad) * m_pad;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int i = static_cast<int>(e % m_pad), k = static_cast<int>(e / m_pad);
@@ -260,8 +275,47 @@ private:
       add_columns_kernel<<<grid_for(n_ * cnt), 256, 0, ctx_->stream>>>(Pacc, P2_.p, n_ * cnt);
       launched(ctx_), launched(ctx_);
     }
-    dim3 gb(static_cast<unsigned>(std::min<int64_t>((static_cast<int64_t>(mp) * mp + 255) / 256, 256)), cnt);
-    rank_build_t_kernel<<<gb, 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), Pacc, n_, rho, mp, W_.p);
+    // certified screen on the host (see the header); the rest -> Jacobi SVD
+    h_rho_.ensure(cnt);
+    CU(cudaMemcpyAsync(h_rho_.p, rho, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    const double thr = threshold();
+    const double smax_hi = std::sqrt(static_cast<double>(n_ + 1)) * (1.0 + 1e-12);
+    // sigma_max(T) >= sigma_max(R) >= its largest row norm, and >= 1 (a unit column)
+    const double smax_lo = std::max(1.0, smax_row_) * (1.0 - 1e-12);
+    std::vector<int> amb;
+    amb.reserve(static_cast<size_t>(cnt));
+    for (int j = 0; j < cnt; ++j) {
+      const double r = h_rho_.p[j];
+      if (screen_ && r < thr * smax_lo / 8.0) {
+        h_ind_.p[j] = 0;
+      } else if (screen_ && r > 0.0 && 1.0 / std::sqrt(finv_ + (finv_ + 1.0) / (r * r)) >= 8.0 * thr * smax_hi) {
+        h_ind_.p[j] = 1;
+      } else {
+        amb.push_back(j);
+      }
+    }
+    st_.survivors += amb.size();  // candidates that needed the SVD
+    if (trace_ && !amb.empty()) {
+      int small = 0;
+      double lo = 1e300, hi = 0.0;
+      for (int j : amb) {
+        small += h_rho_.p[j] < 1e-6;
+        lo = std::min(lo, h_rho_.p[j]);
+        hi = std::max(hi, h_rho_.p[j]);
+      }
+      std::fprintf(stderr, "[rank] n=%lld cnt=%d svd=%zu (rho<1e-6: %d) rho in [%.3g, %.3g] F=%.3g thr=%.3g smax_row=%.3g\n",
+                   static_cast<long long>(n_), cnt, amb.size(), small, lo, hi, finv_, thr, smax_row_);
+    }
+    if (amb.empty()) return;
+    const int na = static_cast<int>(amb.size());
+    W_.ensure(static_cast<size_t>(na) * mp * mp);
+    sel_.ensure(na);
+    jind_.ensure(na);
+    CU(cudaMemcpyAsync(sel_.p, amb.data(), na * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+    dim3 gb(static_cast<unsigned>(std::min<int64_t>((static_cast<int64_t>(mp) * mp + 255) / 256, 256)), na);
+    rank_build_t_kernel<<<gb, 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), Pacc, n_, rho, mp, W_.p,
+                                                      sel_.p);
     const size_t t_bytes = static_cast<size_t>(mp) * mp * sizeof(double2);
     const bool in_smem = t_bytes + mp * sizeof(double) <= kJacobiSmem;
     if (!jacobi_attr_) {
@@ -269,11 +323,13 @@ private:
                               static_cast<int>(kJacobiSmem)));
       jacobi_attr_ = true;
     }
-    rank_jacobi_kernel<<<cnt, 256, (in_smem ? t_bytes : 0) + mp * sizeof(double), ctx_->stream>>>(
-        W_.p, m, mp, threshold(), 30, in_smem ? 1 : 0, ind, smin_.p, smax_.p);
+    rank_jacobi_kernel<<<na, 256, (in_smem ? t_bytes : 0) + mp * sizeof(double), ctx_->stream>>>(
+        W_.p, m, mp, threshold(), 30, in_smem ? 1 : 0, jind_.p, smin_.p, smax_.p);
     launched(ctx_), launched(ctx_);
-    CU(cudaMemcpyAsync(h_ind_.p, ind, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    h_jind_.ensure(na);
+    CU(cudaMemcpyAsync(h_jind_.p, jind_.p, na * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
+    for (int q = 0; q < na; ++q) h_ind_.p[amb[q]] = h_jind_.p[q];
   }
   static unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::clamp<int64_t>((n + 255) / 256, 1, 4096)); }
 
@@ -365,8 +421,12 @@ private:
   void accept(const double2* h, const double2* resid, const double2* beta, const double* rho) {
     CU(cudaMemcpyAsync(B_.p + n_ * D_, h, D_ * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
     CU(cudaMemcpyAsync(h_one_.p, rho, sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    h_beta_.ensure(static_cast<size_t>(std::max<int64_t>(n_, 1)));
+    if (n_ > 0)
+      CU(cudaMemcpyAsync(h_beta_.p, beta, n_ * sizeof(double2), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
     const double r = h_one_.p[0];
+    update_finv(h_beta_.p, r);
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 256));
     append_scaled_kernel<<<blocks, 256, 0, ctx_->stream>>>(resid, 1.0 / r, D_, V_.p + n_ * D_, nullptr, nullptr);
     rank_append_r_kernel<<<grid_for(n_ + 1), 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), beta, rho);
@@ -375,10 +435,46 @@ private:
     ++st_.accepted;
   }
 
+  // F = ||R^{-1}||_F^2 after appending the column (beta, rho) to R:
+  // F += (||R^{-1} beta||^2 + 1) / rho^2 (back-substitution on the host copy
+  // hR_ of the upper-triangular R, column-major, ld cap_ + 1)
+  void update_finv(const double2* beta, double rho) {
+    using cd = std::complex<double>;
+    const int64_t n = n_, ld = cap_ + 1;
+    if (hR_.empty()) hR_.assign(static_cast<size_t>(ld * ld), cd(0.0, 0.0));
+    std::vector<cd> x(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) x[i] = cd(beta[i].x, beta[i].y);
+    for (int64_t i = n - 1; i >= 0; --i) {  // R x = beta
+      cd acc = x[i];
+      for (int64_t k = i + 1; k < n; ++k) acc -= hR_[i + k * ld] * x[k];
+      x[i] = acc / hR_[i + i * ld];
+    }
+    double xx = 0.0;
+    for (const cd& v : x) xx += std::norm(v);
+    finv_ += (xx + 1.0) / (rho * rho);
+    for (int64_t i = 0; i < n; ++i) hR_[i + n * ld] = cd(beta[i].x, beta[i].y);
+    hR_[n + n * ld] = cd(rho, 0.0);
+    // row norms of R (lower bounds on sigma_max(R)): the new column adds
+    // |beta_i|^2 to row i, and row n starts at rho^2
+    rows2_.resize(static_cast<size_t>(n + 1), 0.0);
+    for (int64_t i = 0; i < n; ++i) rows2_[i] += std::norm(hR_[i + n * ld]);
+    rows2_[n] = rho * rho;
+    for (double v : rows2_) smax_row_ = std::max(smax_row_, std::sqrt(v));
+  }
+
   liecl_b200_ctx* ctx_;
   int d_;
   int64_t D_;
   double tol_, rank_tol_;
+  bool screen_ = [] {
+    const char* e = std::getenv("LIECL_B200_RANK_SCREEN");
+    return !(e && e[0] == '0');
+  }();
+  double finv_ = 0.0;  // ||R^{-1}||_F^2
+  double smax_row_ = 0.0;  // largest row norm of R
+  std::vector<double> rows2_;
+  bool trace_ = std::getenv("LIECL_B200_TRACE") != nullptr;
+  std::vector<std::complex<double>> hR_;
   bool record_;
   int64_t cap_ = 0, bmax_ = 0, n_ = 0;
   uint64_t kernels0_ = 0;
@@ -390,7 +486,8 @@ private:
   std::vector<liecl_b200_decision> log_;
   DevBuf<double2> B_, V_, R_, C_, X_, Y_, Yb_, P1_, P2_, W_, Xr_, Pr_;
   DevBuf<double> partial_, rn_, hn_, smin_, smax_, rnr_;
-  DevBuf<int> nul_, ind_, indr_, idx_;
-  HostBuf<double> h_hn_, h_one_;
-  HostBuf<int> h_nul_, h_ind_;
+  DevBuf<int> nul_, ind_, indr_, idx_, sel_, jind_;
+  HostBuf<double> h_hn_, h_one_, h_rho_;
+  HostBuf<double2> h_beta_;
+  HostBuf<int> h_nul_, h_ind_, h_jind_;
 };

@@ -79,3 +79,42 @@ def test_small_bracket_rank_tolerance():
     assert r.dimension == 11
     o = liecl.closure_dense_arrays(gens, 8, liecl.Method.orthonorm, liecl.ClosureConfig(tolerance=1e-10))
     assert o.dimension == 11
+
+
+def _rank_log(gens, d, rank_tol, screen):
+    import os
+    old = os.environ.get("LIECL_B200_RANK_SCREEN")
+    os.environ["LIECL_B200_RANK_SCREEN"] = "1" if screen else "0"
+    try:
+        r = liecl.closure_dense_arrays(gens, d, liecl.Method.standard_rank,
+                                       liecl.ClosureConfig(tolerance=1e-10, rank_tolerance=rank_tol, record_log=True))
+    finally:
+        if old is None:
+            del os.environ["LIECL_B200_RANK_SCREEN"]
+        else:
+            os.environ["LIECL_B200_RANK_SCREEN"] = old
+    return r
+
+
+@pytest.mark.parametrize("case", ["hea3", "spin_glass3", "random_d4", "small_bracket"])
+def test_certified_screen_keeps_every_verdict(case):
+    """The sigma-bound screen (rank_engine.cuh) decides only what the Jacobi
+    SVD would decide the same way: identical decision logs with and without."""
+    import os
+    if case == "hea3":
+        gens, d, rt = np.stack([w.vec(1j * w.from_pauli(sp)) for sp in w.hea(3)]), 8, 0.0
+    elif case == "spin_glass3":
+        gens, d, rt = np.stack([w.vec(1j * w.from_pauli(sp)) for sp in w.spin_glass_hva(3)]), 8, 0.0
+    elif case == "random_d4":
+        rng = np.random.default_rng(3)
+        m = rng.standard_normal((2, 4, 4)) + 1j * rng.standard_normal((2, 4, 4))
+        gens, d, rt = np.stack([(a - a.conj().T).ravel(order="F") for a in m]), 4, 0.0
+    else:
+        gens = np.load(os.path.join(os.path.dirname(__file__), "golden", "rank_small_bracket_d8.npy"))
+        d, rt = 8, 1e-10
+    a = _rank_log(gens, d, rt, screen=True)
+    b = _rank_log(gens, d, rt, screen=False)
+    assert a.dimension == b.dimension
+    assert np.array_equal(a.decision_log["independent"], b.decision_log["independent"])
+    assert np.array_equal(a.basis_array.view(np.uint64), b.basis_array.view(np.uint64))
+    assert a.stats.engine["survivors"] < b.stats.engine["survivors"]  # the screen decided some

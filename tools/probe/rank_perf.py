@@ -13,7 +13,8 @@ for fam, n in (("hea", 3), ("spin_glass_hva", 3), ("spin_glass_hva", 4)):
     t = time.perf_counter()
     r = liecl.closure_dense_arrays(gens, 1 << n, liecl.Method.standard_rank, cfg)
     g = time.perf_counter() - t
-    out = {"family": fam, "n": n, "dim": r.dimension, "gpu_s": round(g, 3), "checks": r.stats.independence_checks}
+    out = {"family": fam, "n": n, "dim": r.dimension, "gpu_s": round(g, 3), "checks": r.stats.independence_checks,
+           "svd_candidates": r.stats.engine.get("survivors"), "screen": os.environ.get("LIECL_B200_RANK_SCREEN", "1")}
     if n == 3:
         t = time.perf_counter()
         o = ref.closure_dense(gens, 1 << n, method="standard-rank", tol=1e-10, threads=os.cpu_count())
