@@ -80,17 +80,10 @@ public:
                                      std::chrono::duration<double>(cfg.deadline_seconds));
     }
     sqrt_d_ = std::sqrt(static_cast<double>(d));
-    const int64_t slots = cap_ + 1;
-    B_.ensure(static_cast<size_t>(slots * D_));
-    A_.ensure(static_cast<size_t>(slots * slots));
-    Ainv_.ensure(static_cast<size_t>(slots * slots));
     C_.ensure(static_cast<size_t>(bmax_ * D_));
     R_.ensure(static_cast<size_t>(bmax_ * D_));
-    beta_.ensure(static_cast<size_t>(slots * bmax_));
-    x_.ensure(static_cast<size_t>(slots * bmax_));
     Y_.ensure(static_cast<size_t>(D_));
-    bre_.ensure(static_cast<size_t>(slots));
-    xre_.ensure(static_cast<size_t>(slots));
+    reserve(std::min<int64_t>(cap_ + 1, 64));  // basis slabs grow with the closure
     partial_.ensure(static_cast<size_t>(((D_ + zg::BM - 1) / zg::BM) * bmax_));
     rn_.ensure(bmax_); hn_.ensure(bmax_); nul_.ensure(bmax_); yn_.ensure(1); s_.ensure(1);
     h_rn_.ensure(bmax_); h_hn_.ensure(bmax_); h_nul_.ensure(bmax_); h_one_.ensure(2);
@@ -165,7 +158,7 @@ public:
   // A and A^{-1} as n x n column-major (ld n)
   void download_gram(double* a_out, double* ainv_out) {
     if (n_ == 0) return;
-    const size_t pitch = static_cast<size_t>(cap_ + 1) * sizeof(double2), w = static_cast<size_t>(n_) * sizeof(double2);
+    const size_t pitch = static_cast<size_t>(ld()) * sizeof(double2), w = static_cast<size_t>(n_) * sizeof(double2);
     if (a_out)
       CU(cudaMemcpy2DAsync(a_out, w, A_.p, pitch, w, n_, cudaMemcpyDeviceToHost, ctx_->stream));
     if (ainv_out)
@@ -174,7 +167,42 @@ public:
   }
 
 private:
-  int64_t ld() const { return cap_ + 1; }
+  int64_t ld() const { return vcap_; }
+
+  // Slots for `need` basis elements: B, A, A^{-1} and the per-batch beta / x
+  // scratch grow geometrically up to cap + 1 (a closure of dimension 64 at
+  // d = 256 must not allocate d^2 slots). Contents are kept: the batch's beta
+  // and x (computed before apply) and A, A^{-1} re-pitched to the new ld.
+  void reserve(int64_t need) {
+    if (need <= vcap_) return;
+    const int64_t nc = std::min<int64_t>(cap_ + 1, std::max<int64_t>(need, 2 * vcap_));
+    auto grow1 = [&](DevBuf<double2>& buf, size_t n, size_t live) {
+      DevBuf<double2> nb;
+      nb.ensure(n);
+      if (live > 0) CU(cudaMemcpyAsync(nb.p, buf.p, live * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      std::swap(buf.p, nb.p);
+      std::swap(buf.n, nb.n);
+    };
+    auto grow2 = [&](DevBuf<double2>& buf) {
+      DevBuf<double2> nb;
+      nb.ensure(static_cast<size_t>(nc * nc));
+      if (n_ > 0)
+        CU(cudaMemcpy2DAsync(nb.p, nc * sizeof(double2), buf.p, vcap_ * sizeof(double2), n_ * sizeof(double2), n_,
+                             cudaMemcpyDeviceToDevice, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      std::swap(buf.p, nb.p);
+      std::swap(buf.n, nb.n);
+    };
+    grow1(B_, static_cast<size_t>(nc * D_), static_cast<size_t>(n_ * D_));
+    grow2(A_);
+    grow2(Ainv_);
+    grow1(beta_, static_cast<size_t>(nc * bmax_), beta_.n);
+    grow1(x_, static_cast<size_t>(nc * bmax_), x_.n);
+    grow1(bre_, static_cast<size_t>(nc), bre_.n);
+    grow1(xre_, static_cast<size_t>(nc), xre_.n);
+    vcap_ = nc;
+  }
 
   // beta = B^H C / d, x = A^{-1} beta, R = C - B x, rn = ||R||
   void check(const double2* Cc, int cnt, double2* beta, double2* x, double2* R, double* rn) {
@@ -196,6 +224,7 @@ private:
   }
 
   void apply(int cnt, int64_t pair_g0, int64_t cand0, bool generators) {
+    reserve(std::min<int64_t>(cap_ + 1, n_ + cnt + 1));  // before any pointer into the slabs
     const int64_t n_bs = n_;
     const int64_t ldb = n_bs;  // column stride of the batch's beta / x
     for (int j = 0; j < cnt; ++j) {
@@ -325,6 +354,7 @@ private:
   std::vector<liecl_b200_decision> log_;
   cusolverDnHandle_t solver_ = nullptr;
   DevBuf<double2> B_, A_, Ainv_, Atmp_, C_, R_, beta_, x_, Y_, bre_, xre_, work_;
+  int64_t vcap_ = 0;  // basis slots allocated (ld of A and A^{-1})
   DevBuf<double> partial_, rn_, hn_, yn_, s_;
   DevBuf<int> nul_, info_;
   HostBuf<double> h_rn_, h_hn_, h_one_;

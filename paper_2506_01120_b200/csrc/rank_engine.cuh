@@ -167,14 +167,9 @@ public:
                                      std::chrono::duration<double>(cfg.deadline_seconds));
     }
     sqrt_d_ = std::sqrt(static_cast<double>(d));
-    const int64_t slots = cap_ + 1;
-    B_.ensure(static_cast<size_t>(slots * D_));
-    V_.ensure(static_cast<size_t>(slots * D_));
-    R_.ensure(static_cast<size_t>(slots * slots));
     C_.ensure(static_cast<size_t>(bmax_ * D_));
     X_.ensure(static_cast<size_t>(bmax_ * D_));
-    P1_.ensure(static_cast<size_t>(slots * bmax_));
-    P2_.ensure(static_cast<size_t>(slots * bmax_));
+    reserve(std::min<int64_t>(cap_ + 1, 64));  // basis slabs grow with the closure
     partial_.ensure(static_cast<size_t>(((D_ + zg::BM - 1) / zg::BM) * bmax_));
     rn_.ensure(bmax_); hn_.ensure(bmax_); nul_.ensure(bmax_); ind_.ensure(bmax_); smin_.ensure(bmax_);
     smax_.ensure(bmax_);
@@ -241,7 +236,39 @@ public:
 private:
   static constexpr size_t kJacobiSmem = 200 * 1024;
   bool jacobi_attr_ = false;
-  int64_t ldr() const { return cap_ + 1; }
+  int64_t ldr() const { return vcap_; }
+
+  // Slots for `need` basis elements: B, V, R (re-pitched to the new ld) and
+  // the batch's projection coefficients P1 (computed before apply, kept)
+  // grow geometrically up to cap + 1.
+  void reserve(int64_t need) {
+    if (need <= vcap_) return;
+    const int64_t nc = std::min<int64_t>(cap_ + 1, std::max<int64_t>(need, 2 * vcap_));
+    auto grow1 = [&](DevBuf<double2>& buf, size_t n, size_t live) {
+      DevBuf<double2> nb;
+      nb.ensure(n);
+      if (live > 0) CU(cudaMemcpyAsync(nb.p, buf.p, live * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      std::swap(buf.p, nb.p);
+      std::swap(buf.n, nb.n);
+    };
+    grow1(B_, static_cast<size_t>(nc * D_), static_cast<size_t>(n_ * D_));
+    grow1(V_, static_cast<size_t>(nc * D_), static_cast<size_t>(n_ * D_));
+    {
+      DevBuf<double2> nb;
+      nb.ensure(static_cast<size_t>(nc * nc));
+      CU(cudaMemsetAsync(nb.p, 0, nb.n * sizeof(double2), ctx_->stream));
+      if (n_ > 0)
+        CU(cudaMemcpy2DAsync(nb.p, nc * sizeof(double2), R_.p, vcap_ * sizeof(double2), n_ * sizeof(double2), n_,
+                             cudaMemcpyDeviceToDevice, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      std::swap(R_.p, nb.p);
+      std::swap(R_.n, nb.n);
+    }
+    grow1(P1_, static_cast<size_t>(nc * bmax_), P1_.n);
+    grow1(P2_, static_cast<size_t>(nc * bmax_), 0);
+    vcap_ = nc;
+  }
   int m_pad() const { return static_cast<int>((n_ + 2) & ~int64_t(1)); }
   // candidates per batch: the T matrices (m_pad^2 complex each) within 1 GB
   int64_t batch_limit() const {
@@ -295,6 +322,27 @@ private:
         amb.push_back(j);
       }
     }
+    // second stage for the few left: x = R^{-1} beta exactly (host
+    // back-substitution, O(n^2)) gives ||T^{-1}||_F^2 = F + (|x|^2 + 1) / rho^2
+    // and ||T^{-1} e_n|| = sqrt(|x|^2 + 1) / rho, i.e.
+    //   1 / sqrt(F + (|x|^2 + 1) / rho^2) <= sigma_min(T) <= rho / sqrt(|x|^2 + 1)
+    if (screen_ && !amb.empty() && n_ > 0) {
+      h_bcol_.ensure(static_cast<size_t>(n_) * amb.size());
+      for (size_t q = 0; q < amb.size(); ++q)
+        CU(cudaMemcpyAsync(h_bcol_.p + q * n_, Pacc + static_cast<int64_t>(amb[q]) * n_, n_ * sizeof(double2),
+                           cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      std::vector<int> rest;
+      for (size_t q = 0; q < amb.size(); ++q) {
+        const int j = amb[q];
+        const double r = h_rho_.p[j];
+        const double xx = solve_norm2(h_bcol_.p + q * n_);
+        if (r / std::sqrt(xx + 1.0) < thr * smax_lo / 8.0) h_ind_.p[j] = 0;
+        else if (r > 0.0 && 1.0 / std::sqrt(finv_ + (xx + 1.0) / (r * r)) >= 8.0 * thr * smax_hi) h_ind_.p[j] = 1;
+        else rest.push_back(j);
+      }
+      amb.swap(rest);
+    }
     st_.survivors += amb.size();  // candidates that needed the SVD
     if (trace_ && !amb.empty()) {
       int small = 0;
@@ -342,6 +390,7 @@ private:
   // state; "dependent" stands. The rank check has no residual scale: the log
   // carries 0 like the reference's outcome.
   void apply(int cnt, int64_t pair_g0, int64_t cand0, bool generators) {
+    reserve(std::min<int64_t>(cap_ + 1, n_ + cnt + 1));  // before any pointer into the slabs
     const int64_t n_bs = n_;
     std::vector<int> ind(h_ind_.p, h_ind_.p + cnt);
     // re-checks are batched: every stale "independent" left in the batch is
@@ -435,29 +484,37 @@ private:
     ++st_.accepted;
   }
 
-  // F = ||R^{-1}||_F^2 after appending the column (beta, rho) to R:
-  // F += (||R^{-1} beta||^2 + 1) / rho^2 (back-substitution on the host copy
-  // hR_ of the upper-triangular R, column-major, ld cap_ + 1)
-  void update_finv(const double2* beta, double rho) {
+  // |R^{-1} beta|^2 by back-substitution on the host copy of R
+  double solve_norm2(const double2* beta) const {
     using cd = std::complex<double>;
-    const int64_t n = n_, ld = cap_ + 1;
-    if (hR_.empty()) hR_.assign(static_cast<size_t>(ld * ld), cd(0.0, 0.0));
+    const int64_t n = n_;
     std::vector<cd> x(static_cast<size_t>(n));
     for (int64_t i = 0; i < n; ++i) x[i] = cd(beta[i].x, beta[i].y);
-    for (int64_t i = n - 1; i >= 0; --i) {  // R x = beta
+    for (int64_t i = n - 1; i >= 0; --i) {
       cd acc = x[i];
-      for (int64_t k = i + 1; k < n; ++k) acc -= hR_[i + k * ld] * x[k];
-      x[i] = acc / hR_[i + i * ld];
+      for (int64_t k = i + 1; k < n; ++k) acc -= hR_[k][i] * x[k];
+      x[i] = acc / hR_[i][i];
     }
     double xx = 0.0;
     for (const cd& v : x) xx += std::norm(v);
-    finv_ += (xx + 1.0) / (rho * rho);
-    for (int64_t i = 0; i < n; ++i) hR_[i + n * ld] = cd(beta[i].x, beta[i].y);
-    hR_[n + n * ld] = cd(rho, 0.0);
+    return xx;
+  }
+
+  // F = ||R^{-1}||_F^2 after appending the column (beta, rho) to R:
+  // F += (||R^{-1} beta||^2 + 1) / rho^2 (back-substitution on the host copy
+  // hR_ of the upper-triangular R, one vector per column)
+  void update_finv(const double2* beta, double rho) {
+    using cd = std::complex<double>;
+    const int64_t n = n_;
+    finv_ += (solve_norm2(beta) + 1.0) / (rho * rho);  // hR_[k] = column k, rows 0..k
+    std::vector<cd> col(static_cast<size_t>(n + 1));
+    for (int64_t i = 0; i < n; ++i) col[i] = cd(beta[i].x, beta[i].y);
+    col[n] = cd(rho, 0.0);
     // row norms of R (lower bounds on sigma_max(R)): the new column adds
     // |beta_i|^2 to row i, and row n starts at rho^2
     rows2_.resize(static_cast<size_t>(n + 1), 0.0);
-    for (int64_t i = 0; i < n; ++i) rows2_[i] += std::norm(hR_[i + n * ld]);
+    for (int64_t i = 0; i < n; ++i) rows2_[i] += std::norm(col[i]);
+    hR_.push_back(std::move(col));
     rows2_[n] = rho * rho;
     for (double v : rows2_) smax_row_ = std::max(smax_row_, std::sqrt(v));
   }
@@ -474,7 +531,8 @@ private:
   double smax_row_ = 0.0;  // largest row norm of R
   std::vector<double> rows2_;
   bool trace_ = std::getenv("LIECL_B200_TRACE") != nullptr;
-  std::vector<std::complex<double>> hR_;
+  std::vector<std::vector<std::complex<double>>> hR_;
+  int64_t vcap_ = 0;  // basis slots allocated (ld of R)
   bool record_;
   int64_t cap_ = 0, bmax_ = 0, n_ = 0;
   uint64_t kernels0_ = 0;
@@ -488,6 +546,6 @@ private:
   DevBuf<double> partial_, rn_, hn_, smin_, smax_, rnr_;
   DevBuf<int> nul_, ind_, indr_, idx_, sel_, jind_;
   HostBuf<double> h_hn_, h_one_, h_rho_;
-  HostBuf<double2> h_beta_;
+  HostBuf<double2> h_beta_, h_bcol_;
   HostBuf<int> h_nul_, h_ind_, h_jind_;
 };

@@ -1,0 +1,58 @@
+"""The paper's published rows (BASELINE.md:30-33, other hardware) against this
+framework on one B200: dimension, wall seconds, the engine path used.
+Each row runs in a subprocess with a timeout; results as JSON lines."""
+import json, os, subprocess, sys, time
+
+ROWS = [  # (method, family, n, path, published seconds)
+    ("standard-rank", "hea", 2, "dense", 0.6), ("standard-rank", "hea", 3, "dense", 3.0),
+    ("standard-rank", "hea", 4, "dense", 251.0),
+    ("orthonorm-dimonly", "spin_glass_hva", 3, "dense", 0.5), ("orthonorm-dimonly", "spin_glass_hva", 4, "dense", 0.6),
+    ("orthonorm-dimonly", "spin_glass_hva", 5, "dense", 1.0), ("orthonorm-dimonly", "spin_glass_hva", 6, "dense", 8.0),
+    ("standard-rank", "spin_glass_hva", 3, "dense", 1.0), ("standard-rank", "spin_glass_hva", 4, "dense", 14.0),
+    ("standard-rank", "spin_glass_hva", 5, "dense", 571.0),
+    ("orthonorm-dimonly", "xxz_hva", 4, "sums", 0.7), ("orthonorm-dimonly", "xxz_hva", 6, "sums", 2.0),
+    ("orthonorm-dimonly", "xxz_hva", 8, "sums", 5.0),
+    ("standard-rank", "xxz_hva", 4, "dense", 0.5), ("standard-rank", "xxz_hva", 6, "dense", 3.0),
+    ("orthonorm-dimonly", "tfim_hva_open", 4, "sums", 1.4), ("orthonorm-dimonly", "tfim_hva_open", 6, "sums", 1.8),
+    ("orthonorm-dimonly", "tfim_hva_open", 8, "sums", 3.2), ("orthonorm-dimonly", "tfim_hva_open", 10, "sums", 35.0),
+    ("standard-rank", "tfim_hva_open", 4, "dense", 0.5), ("standard-rank", "tfim_hva_open", 6, "dense", 3.0),
+    ("standard-rank", "tfim_hva_open", 8, "dense", 505.0), ("standard-rank", "tfim_hva_open", 10, "dense", 1390.0),
+]
+
+CHILD = r'''
+import json, sys, time, os
+sys.path.insert(0, os.getcwd())
+import numpy as np
+from paper_2506_01120_b200 import liecl, workloads as w
+method, fam, n, path = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]
+specs = getattr(w, fam)(n)
+m = liecl.to_method(method) if hasattr(liecl, "to_method") else {"standard-rank": liecl.Method.standard_rank, "orthonorm-dimonly": liecl.Method.orthonorm_dimonly}[method]
+cfg = liecl.ClosureConfig(tolerance=1e-10)
+if path == "dense":
+    gens = np.stack([w.vec(1j * w.from_pauli(sp)) for sp in specs])
+    run = lambda: liecl.closure_dense_arrays(gens, 1 << n, m, cfg)
+else:
+    off, x, z, c = w.sum_arrays(specs)
+    run = lambda: liecl.closure_pauli_sums_arrays(off, x, z, c, n, m, cfg)
+t0 = time.perf_counter(); r = run(); t1 = time.perf_counter() - t0
+best = t1
+if t1 < 5.0:  # warm rerun (first call pays engine set-up)
+    t0 = time.perf_counter(); r = run(); best = min(best, time.perf_counter() - t0)
+print(json.dumps({"dimension": r.dimension, "seconds": round(best, 4), "first_call_s": round(t1, 4),
+                  "brackets": r.stats.commutators_evaluated, "checks": r.stats.independence_checks}))
+'''
+
+limit = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
+for method, fam, n, path, paper in ROWS:
+    row = {"method": method, "family": fam, "n": n, "path": path, "paper_s": paper}
+    try:
+        out = subprocess.run([sys.executable, "-c", CHILD, method, fam, str(n), path], capture_output=True, text=True,
+                             timeout=limit)
+        if out.returncode == 0:
+            row.update(json.loads(out.stdout.strip().splitlines()[-1]))
+            row["speedup_vs_paper"] = round(paper / row["seconds"], 1) if row["seconds"] > 0 else None
+        else:
+            row["error"] = (out.stderr.strip().splitlines() or ["?"])[-1][:200]
+    except subprocess.TimeoutExpired:
+        row["error"] = f"timeout {limit:.0f} s"
+    print(json.dumps(row), flush=True)
