@@ -40,7 +40,6 @@
 #include <map>
 #include <memory>
 #include <mutex>
-#include <set>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -241,19 +240,24 @@ bool borderline(double rn, double tol) {  // R:src/closure.cpp:328-329
 // ------------------------------------------------------------ GEMM launch ---
 
 // Function attributes are per device context: a process may drive several
-// devices (one context each), so "already set" is remembered per
-// (kernel, device, attribute, value), under a lock (contexts may be created
-// from several threads).
+// devices (one context each), so the value last set is remembered per
+// (kernel, device, attribute), under a lock (contexts may be created from
+// several threads). An attribute holds ONE value: the dynamic shared-memory
+// limit only ever rises (a launch needing less still fits), anything else is
+// set whenever it differs.
 template <class K> void func_attr_once(K* kernel, cudaFuncAttribute attr, int value) {
   static std::mutex mu;
-  static std::set<std::tuple<const void*, int, int, int>> done;
+  static std::map<std::tuple<const void*, int, int>, int> current;
   int dev = 0;
   CU(cudaGetDevice(&dev));
-  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, static_cast<int>(attr), value);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, static_cast<int>(attr));
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count(key)) return;
+  const auto it = current.find(key);
+  if (it != current.end()) {
+    if (attr == cudaFuncAttributeMaxDynamicSharedMemorySize ? it->second >= value : it->second == value) return;
+  }
   CU(cudaFuncSetAttribute(kernel, attr, value));
-  done.insert(key);
+  current[key] = value;
 }
 
 template <bool KC, bool CJ, Epilogue E> void gemm_attr_once() {

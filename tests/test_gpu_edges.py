@@ -147,3 +147,19 @@ def test_rounding_decided_input_is_flagged(field):
     assert 30 <= r.dimension <= 256
     kinds = {w.kind for w in r.stats.warnings}
     assert "borderline_residual" in kinds
+
+
+def test_tiny_kernel_shared_memory_up_down_up():
+    """The single-CTA closure kernel's dynamic shared memory depends on d, the
+    capacity and the method (d = 8: ~136 KB keep, ~68 KB dimonly). The
+    attribute holds one value, so a cache keyed by the requested size
+    lowered it to 68 KB and the next 136 KB launch failed (invalid argument)."""
+    gens = np.stack([w.vec(1j * w.from_pauli(sp)) for sp in w.hea(3)])
+    want = {}
+    for m in (liecl.Method.orthonorm, liecl.Method.orthonorm_dimonly, liecl.Method.orthonorm,
+              liecl.Method.orthonorm_dimonly, liecl.Method.orthonorm):
+        r = liecl.closure_dense_arrays(gens, 8, m, liecl.ClosureConfig(tolerance=1e-10))
+        assert r.dimension == 63
+        if m in want:
+            assert np.array_equal(r.basis_array.view(np.uint64), want[m])
+        want[m] = r.basis_array.view(np.uint64).copy()

@@ -46,6 +46,9 @@ def rounding_decided(gens, d, gram=False, rank_tol=None):
 
 t0 = time.time()
 for it in range(ITERS):
+    t_it = time.time()
+    if os.environ.get("SOAK_PROGRESS"):
+        print("it", it, flush=True)
     kind = random.choice(["dense", "dense", "gram", "rank", "single", "sums"])
     counts[kind] = counts.get(kind, 0) + 1
     try:
@@ -92,7 +95,9 @@ for it in range(ITERS):
             bx, bz, bc = r.basis_array
             ok = r.dimension == o.dimension and np.array_equal(bc.view(np.uint64), o.basis[2].view(np.uint64))
         else:
-            n = int(rng.integers(2, 6))
+            # n <= 4: random complex sums at n = 5 close to most of gl(32) with
+            # ~1000-term elements; the reference build itself needs > 5 min there
+            n = int(rng.integers(2, 5))
             offs, xs, zs, cs = [0], [], [], []
             for _ in range(int(rng.integers(2, 4))):
                 s = liecl.pauli_sum_from_terms(n, [(liecl.PauliString(int(rng.integers(0, 1 << n)), int(rng.integers(0, 1 << n)), n),
