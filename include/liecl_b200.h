@@ -213,6 +213,17 @@ int liecl_b200_inner_product_dense(liecl_b200_ctx* ctx, const double* a, const d
                                    double* out_re_im);
 int liecl_b200_norm_dense(liecl_b200_ctx* ctx, const double* a, int32_t d, double* out);
 
+/* linear_combination, dense branch (R:src/operator.cpp:137-162):
+ * out = base_coeff * base + sum_l coeffs[l] * tuple[l] over the n operators of
+ * `tuple` (n * d*d complex, vec layout) in index order, each product and sum
+ * rounded separately. `is_null` (optional, n flags) marks null tuple entries,
+ * which are skipped; base == NULL is a null base: the chain then starts from
+ * the first non-null entry (R:src/operator.cpp:147-154; all null -> out = 0
+ * and *out_null = 1). coeffs: n complex (re, im). Host buffers. */
+int liecl_b200_linear_combination_dense(liecl_b200_ctx* ctx, const double* base, double base_re, double base_im,
+                                        const double* tuple, const double* coeffs, const int32_t* is_null,
+                                        int64_t n, int32_t d, double* out, int32_t* out_null);
+
 /* from_pauli (R:include/liecl/dense.hpp:35-40, R:src/dense.cpp:70-98) on the
  * device, bit-exact: `count` Pauli sums given as terms [offsets[c],
  * offsets[c+1]) of (x, z, coef re/im), each sum's terms sorted by (z, x) as a

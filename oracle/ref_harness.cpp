@@ -547,6 +547,29 @@ int liecl_ref_sum_commutator(const std::int64_t* offsets, const std::uint64_t* x
   });
 }
 
+/// linear_combination (R:src/operator.cpp:137-182) over Pauli sums: operator 0
+/// is the base, 1..n the tuple; is_null[0..n] marks null operators (an empty
+/// but non-null sum is a PauliSum with no terms).
+int liecl_ref_linear_combination_pauli(const std::int64_t* offsets, const std::uint64_t* x,
+                                       const std::uint64_t* z, const double* coef, std::int64_t n,
+                                       unsigned qubits, const int* is_null, double br, double bi,
+                                       const double* coeffs, std::int64_t* out_offsets, std::uint64_t* out_x,
+                                       std::uint64_t* out_z, double* out_coef, std::int64_t term_cap,
+                                       int* out_null) {
+  return guarded([&] {
+    OperatorTuple all = pauli_tuple(offsets, x, z, coef, static_cast<int>(n + 1), qubits);
+    for (std::int64_t k = 0; k <= n; ++k)
+      if (is_null[k]) all[static_cast<std::size_t>(k)] = Operator{};
+    std::vector<Complex> c(static_cast<std::size_t>(n));
+    for (std::int64_t l = 0; l < n; ++l) c[static_cast<std::size_t>(l)] = {coeffs[2 * l], coeffs[2 * l + 1]};
+    const Operator r = liecl::linear_combination(all[0], Complex{br, bi},
+                                                 std::span<const Operator>(all).subspan(1), c);
+    *out_null = r.is_null() ? 1 : 0;
+    if (pauli_out(OperatorTuple{r}, out_offsets, out_x, out_z, out_coef, term_cap) < 0)
+      throw liecl::CapacityError("harness: term output capacity too small");
+  });
+}
+
 /// Generator catalog (R:src/generators.cpp:132-148) as Pauli term arrays.
 int liecl_ref_build_generators(int family, unsigned qubits, std::uint64_t seed, double delta,
                                std::int64_t* out_offsets, std::uint64_t* out_x,

@@ -237,6 +237,24 @@ bool borderline(double rn, double tol) {  // R:src/closure.cpp:328-329
   return rn > 0.0 && rn >= tol / 10.0 && rn <= tol * 10.0;
 }
 
+// linear_combination's dense chain (R:src/operator.cpp:155-161, 147-154):
+// acc = c_0 * op_0, then acc = acc + c_k * op_k in order; complex products as
+// (cr vr - ci vi, cr vi + ci vr) with every product and sum rounded on its own
+__global__ void linear_combination_kernel(const double2* __restrict__ ops, const double2* __restrict__ cf, int64_t m,
+                                          int64_t D, double2* __restrict__ out) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < D;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t k = 0; k < m; ++k) {
+      const double2 c = cf[k], v = ops[k * D + e];
+      const double2 p = make_double2(__dsub_rn(__dmul_rn(c.x, v.x), __dmul_rn(c.y, v.y)),
+                                     __dadd_rn(__dmul_rn(c.x, v.y), __dmul_rn(c.y, v.x)));
+      acc = k == 0 ? p : make_double2(__dadd_rn(acc.x, p.x), __dadd_rn(acc.y, p.y));
+    }
+    out[e] = acc;
+  }
+}
+
 // ------------------------------------------------------------ GEMM launch ---
 
 // Function attributes are per device context: a process may drive several
@@ -1207,6 +1225,50 @@ int liecl_b200_norm_dense(liecl_b200_ctx* ctx, const double* a, int32_t d, doubl
     column_norm_kernel<<<1, 256, 0, ctx->stream>>>(va.p, D, std::sqrt(static_cast<double>(d)), n.p);
     launched(ctx);
     CU(cudaMemcpyAsync(out, n.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int liecl_b200_linear_combination_dense(liecl_b200_ctx* ctx, const double* base, double base_re, double base_im,
+                                        const double* tuple, const double* coeffs, const int32_t* is_null,
+                                        int64_t n, int32_t d, double* out, int32_t* out_null) {
+  return guarded([&] {
+    if (!ctx || !out || n < 0 || (n > 0 && (!tuple || !coeffs)) || d < 1 || d > 1024)
+      throw Error(LIECL_B200_INVALID_INPUT, "linear_combination: bad arguments");
+    use_device(ctx);
+    const int64_t D = static_cast<int64_t>(d) * d;
+    // the chain's terms in order: (operator index or -1 for the base, coefficient)
+    std::vector<int64_t> idx;
+    std::vector<double2> cf;
+    if (base) {
+      idx.push_back(-1);
+      cf.push_back(make_double2(base_re, base_im));
+    }
+    for (int64_t l = 0; l < n; ++l) {
+      if (is_null && is_null[l]) continue;
+      idx.push_back(l);
+      cf.push_back(make_double2(coeffs[2 * l], coeffs[2 * l + 1]));
+    }
+    if (out_null) *out_null = idx.empty() ? 1 : 0;
+    if (idx.empty()) {
+      std::memset(out, 0, static_cast<size_t>(D) * sizeof(double2));
+      return;
+    }
+    const int64_t m = static_cast<int64_t>(idx.size());
+    DevBuf<double2> ops, acc;
+    DevBuf<double2> dcf;
+    ops.ensure(static_cast<size_t>(m * D));
+    acc.ensure(static_cast<size_t>(D));
+    dcf.ensure(static_cast<size_t>(m));
+    for (int64_t k = 0; k < m; ++k) {
+      const double* src = idx[k] < 0 ? base : tuple + 2 * idx[k] * D;
+      CU(cudaMemcpyAsync(ops.p + k * D, src, D * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CU(cudaMemcpyAsync(dcf.p, cf.data(), m * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    linear_combination_kernel<<<static_cast<unsigned>(std::min<int64_t>((D + 255) / 256, 4096)), 256, 0,
+                                ctx->stream>>>(ops.p, dcf.p, m, D, acc.p);
+    launched(ctx);
+    CU(cudaMemcpyAsync(out, acc.p, D * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
   });
 }

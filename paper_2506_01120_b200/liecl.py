@@ -605,6 +605,89 @@ def norm(a: DenseOperator, device: int = 0) -> float:
     return out.value
 
 
+def _pauli_add(a: PauliSum, b: PauliSum) -> PauliSum:
+    """PauliSum::operator+ (R:src/pauli.cpp:128-159): sorted merge, equal
+    strings add (a + b), then |c| <= 1e-14 * max|c| is dropped."""
+    if a.qubits != b.qubits:
+        raise InvalidInputError("PauliSum::operator+: qubit counts differ")
+    ka = {(s.z, s.x): (s, c) for s, c in a.terms}
+    kb = {(s.z, s.x): (s, c) for s, c in b.terms}
+    merged = []
+    for k in sorted(set(ka) | set(kb)):
+        if k in ka and k in kb:
+            ca, cb = ka[k][1], kb[k][1]
+            merged.append((ka[k][0], complex(ca.real + cb.real, ca.imag + cb.imag)))
+        else:
+            merged.append(ka[k] if k in ka else kb[k])
+    floor = 1e-14 * max((abs(c) for _, c in merged), default=0.0)
+    return PauliSum(a.qubits, [(s, c) for s, c in merged if abs(c) > floor])
+
+
+def _pauli_scale(a: PauliSum, c: complex) -> PauliSum:
+    """PauliSum::operator*(Complex) (R:src/pauli.cpp:166-177)."""
+    c = complex(c)
+    if c == 0:
+        return PauliSum(a.qubits, [])
+    return PauliSum(a.qubits, [(s, complex(t) * c) for s, t in a.terms])
+
+
+def linear_combination(base, base_coeff: complex, tuple_, coeffs, device: int = 0):
+    """linear_combination (R:src/operator.cpp:137-182): base_coeff * base +
+    sum_l coeffs[l] * tuple_[l] in index order. Operators are DenseOperator,
+    PauliSum or None (null). Dense: on the GPU, products and sums rounded one
+    by one as the reference does. Pauli: one from_terms over the scaled terms
+    (the reference's construction). A null or empty-Pauli base falls back to
+    the chained addition of the reference (:147-154)."""
+    tuple_ = list(tuple_)
+    coeffs = [complex(c) for c in coeffs]
+    if len(tuple_) != len(coeffs):
+        raise InvalidInputError("linear_combination: tuple and coefficient lengths differ")
+    ops = [o for o in [base] + tuple_ if o is not None]
+    if ops:
+        kind, dim = type(ops[0]), ops[0].dim
+        if any(type(o) is not kind or o.dim != dim for o in ops):
+            raise InvalidInputError("linear_combination: operators have mismatched backends or dimensions")
+    if base is None or (isinstance(base, PauliSum) and not base.terms):
+        if ops and isinstance(ops[0], DenseOperator):
+            return _linear_combination_dense(None, 0j, tuple_, coeffs, device)
+        acc = base
+        for op, c in zip(tuple_, coeffs):
+            if op is None:
+                continue
+            term = _pauli_scale(op, c)
+            acc = term if acc is None else _pauli_add(acc, term)
+        return acc
+    if isinstance(base, DenseOperator):
+        return _linear_combination_dense(base, complex(base_coeff), tuple_, coeffs, device)
+    terms = [(s, complex(t) * complex(base_coeff)) for s, t in base.terms]
+    for op, c in zip(tuple_, coeffs):
+        if op is not None:
+            terms += [(s, complex(t) * c) for s, t in op.terms]
+    return pauli_sum_from_terms(base.qubits, terms)
+
+
+def _linear_combination_dense(base, base_coeff, tuple_, coeffs, device):
+    ref = base if base is not None else next(o for o in tuple_ if o is not None)
+    d = ref.dim
+    n = len(tuple_)
+    T = np.zeros((max(n, 1), d * d), np.complex128)
+    nul = np.zeros(max(n, 1), np.int32)
+    for l, op in enumerate(tuple_):
+        if op is None:
+            nul[l] = 1
+        else:
+            T[l] = op.vec()
+    cf = np.array([[c.real, c.imag] for c in coeffs] or [[0.0, 0.0]], np.float64)
+    out = np.zeros(d * d, np.complex128)
+    out_null = C.c_int32()
+    bv = np.ascontiguousarray(base.vec()) if base is not None else None
+    _check(native.load().liecl_b200_linear_combination_dense(
+        native.context(device), _dp(bv.view(np.float64)) if bv is not None else None, C.c_double(base_coeff.real),
+        C.c_double(base_coeff.imag), _dp(T.view(np.float64)), _dp(cf), nul.ctypes.data_as(C.POINTER(C.c_int32)),
+        C.c_int64(n), C.c_int32(d), _dp(out.view(np.float64)), C.byref(out_null)))
+    return None if out_null.value else DenseOperator.from_vec(out, d)
+
+
 # --------------------------------------------------------------- sessions ---
 
 
