@@ -48,8 +48,12 @@ public:
 
   void print_trace() const {
     if (trace_) {
-      std::fprintf(stderr, "[sum_engine] n=%lld batches=%llu rechecks=%llu accepts=%llu fused=%llu fallbacks=%llu\n",
-                   (long long)n_, (unsigned long long)st_.batches, (unsigned long long)st_.rechecks,
+      std::fprintf(stderr,
+                   "[sum_engine] n=%lld basis_terms=%lld brackets=%llu batches=%llu rechecks=%llu accepts=%llu "
+                   "fused=%llu fallbacks=%llu\n",
+                   (long long)n_, (long long)(voff_.empty() ? 0 : voff_.back()),
+                   (unsigned long long)st_.commutators_evaluated, (unsigned long long)st_.batches,
+                   (unsigned long long)st_.rechecks,
                    (unsigned long long)st_.accepted, (unsigned long long)fused_batches_,
                    (unsigned long long)fused_fallbacks_);
       for (const auto& kv : tsum_)
@@ -71,6 +75,15 @@ public:
 
   // generators: ngens sums, terms [goff[i], goff[i+1]) of (x, z, coef re/im)
   void run(const int64_t* goff, const uint64_t* gx, const uint64_t* gz, const double* gc, int ngens) {
+    try {
+      run_impl(goff, gx, gz, gc, ngens);
+    } catch (...) {
+      print_trace();  // a deadline or capacity stop still reports where the time went
+      throw;
+    }
+  }
+
+  void run_impl(const int64_t* goff, const uint64_t* gx, const uint64_t* gz, const double* gc, int ngens) {
     Stage st_run(this, "run");
     const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
     const int64_t nt = ngens > 0 ? goff[ngens] : 0;
