@@ -587,7 +587,25 @@ def commutator(a: DenseOperator, b: DenseOperator, device: int = 0) -> DenseOper
     return DenseOperator.from_vec(out, a.dim)
 
 
-def inner_product(a: DenseOperator, b: DenseOperator, device: int = 0) -> complex:
+def inner_product(a, b, device: int = 0) -> complex:
+    """(1/d) tr(a^dagger b) (R:src/operator.cpp:66-75): null -> 0; Pauli sums by
+    the sorted merge of sum_inner_product (R:src/pauli.cpp:202-220); dense on
+    the GPU."""
+    if a is None or b is None:
+        return complex(0.0, 0.0)
+    if isinstance(a, PauliSum) or isinstance(b, PauliSum):
+        if not (isinstance(a, PauliSum) and isinstance(b, PauliSum)) or a.qubits != b.qubits:
+            raise InvalidInputError("inner_product: operators have mismatched backends or dimensions")
+        kb = {(s.z, s.x): c for s, c in b.terms}
+        re = im = 0.0
+        for s, ca in a.terms:  # both sorted by (z, x): the merge visits matches in this order
+            cb = kb.get((s.z, s.x))
+            if cb is None:
+                continue
+            ca, cb = complex(ca), complex(cb)
+            re += ca.real * cb.real + ca.imag * cb.imag
+            im += ca.real * cb.imag - ca.imag * cb.real
+        return complex(re, im)
     if a.dim != b.dim:
         raise InvalidInputError("inner_product: operators have mismatched backends or dimensions")
     out = np.zeros(2)
@@ -597,12 +615,52 @@ def inner_product(a: DenseOperator, b: DenseOperator, device: int = 0) -> comple
     return complex(out[0], out[1])
 
 
-def norm(a: DenseOperator, device: int = 0) -> float:
+def norm(a, device: int = 0) -> float:
+    """sqrt(inner_product(a, a)) (R:src/operator.cpp:77-82): null -> 0; Pauli
+    sums sqrt(sum |c|^2) in term order (R:src/pauli.cpp:222-228); dense on the
+    GPU."""
+    if a is None:
+        return 0.0
+    if isinstance(a, PauliSum):
+        acc = 0.0
+        for _, c in a.terms:
+            c = complex(c)
+            acc += c.real * c.real + c.imag * c.imag
+        return float(np.sqrt(acc))
     out = C.c_double()
     av = np.ascontiguousarray(a.vec())
     _check(native.load().liecl_b200_norm_dense(native.context(device), _dp(av.view(np.float64)), C.c_int32(a.dim),
                                                C.byref(out)))
     return out.value
+
+
+def axpy_dot(tuple_, coeffs, device: int = 0):
+    """sum_l coeffs[l] * tuple_[l]; the empty combination is null
+    (R:src/operator.cpp:123-135)."""
+    tuple_, coeffs = list(tuple_), list(coeffs)
+    if len(tuple_) != len(coeffs):
+        raise InvalidInputError(f"axpy_dot: tuple and coefficient lengths differ ({len(tuple_)} vs {len(coeffs)})")
+    if not tuple_:
+        return None
+    return linear_combination(tuple_[0], coeffs[0], tuple_[1:], coeffs[1:], device)
+
+
+def is_zero(a, tol: float, device: int = 0) -> bool:
+    """norm(a) <= tol (R:src/operator.cpp:183-188)."""
+    if tol < 0.0:
+        raise InvalidInputError("is_zero: tolerance must be non-negative")
+    return norm(a, device) <= tol
+
+
+def normalized(a, device: int = 0):
+    """Complex{1/norm(a), 0} * a (R:src/operator.cpp:190-196)."""
+    n = norm(a, device)
+    if n == 0.0:
+        raise InvalidInputError("normalized: null operator")
+    s = complex(1.0 / n, 0.0)
+    if isinstance(a, PauliSum):
+        return _pauli_scale(a, s)
+    return _linear_combination_dense(a, s, [], [], device)
 
 
 def _pauli_add(a: PauliSum, b: PauliSum) -> PauliSum:

@@ -113,3 +113,36 @@ def test_dense_branch_matches_reference(ref_exact, case):
         bv.ctypes.data_as(dp), C.c_double(c0.real), C.c_double(c0.imag), T.ctypes.data_as(dp), cf.ctypes.data_as(dp),
         C.c_int64(len(rest)), C.c_int(d), out.ctypes.data_as(dp)) == 0
     assert np.array_equal(got.vec().view(np.uint64), out.view(np.uint64))
+
+
+def test_pauli_norm_inner_product_axpy_dot_and_helpers():
+    rng = np.random.default_rng(9)
+    a, b = _rand_sum(rng, 3, 5), _rand_sum(rng, 3, 5)
+    ka = {(s.z, s.x): c for s, c in a.terms}
+    want = sum((np.conj(ka[(s.z, s.x)]) * c for s, c in b.terms if (s.z, s.x) in ka), 0j)
+    assert abs(liecl.inner_product(a, b) - want) < 1e-15
+    assert liecl.inner_product(None, b) == 0 and liecl.norm(None) == 0.0
+    assert abs(liecl.norm(a) - np.sqrt(sum(abs(c) ** 2 for _, c in a.terms))) < 1e-15
+    assert liecl.axpy_dot([], []) is None
+    with pytest.raises(liecl.InvalidInputError, match="lengths differ"):
+        liecl.axpy_dot([a], [])
+    assert _mine(liecl.axpy_dot([a, b], [2.0, 1j])) == _mine(liecl.linear_combination(a, 2.0, [b], [1j]))
+    u = liecl.normalized(a)
+    assert abs(liecl.norm(u) - 1.0) < 1e-15
+    assert liecl.is_zero(None, 0.0) and not liecl.is_zero(a, 1e-3)
+    with pytest.raises(liecl.InvalidInputError):
+        liecl.is_zero(a, -1.0)
+    with pytest.raises(liecl.InvalidInputError, match="null operator"):
+        liecl.normalized(liecl.PauliSum(3, []))
+
+
+@pytest.mark.gpu
+def test_dense_normalized_and_axpy_dot():
+    rng = np.random.default_rng(10)
+    d = 4
+    mk = lambda: liecl.DenseOperator.from_vec(rng.standard_normal(d * d) + 1j * rng.standard_normal(d * d), d)
+    a, b = mk(), mk()
+    u = liecl.normalized(a)
+    assert abs(liecl.norm(u) - 1.0) < 1e-14
+    s = liecl.axpy_dot([a, b], [1.5, -2j])
+    assert np.allclose(s.vec(), 1.5 * a.vec() - 2j * b.vec(), rtol=0, atol=1e-13)
