@@ -382,6 +382,15 @@ def run_b200_arm(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(x):
+        # ranks take different rows, so their bracket counts differ (row l has l)
+        if not launched_by_torchrun:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     def grown_session(field):
         """Setup (untimed): generator loop + growth phase on the GPU."""
         s = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol, field=field), device=local)
@@ -439,7 +448,7 @@ def run_b200_arm(a):
     peak = fp64_peak_tflops(torch, device)
     windows, my_ms, max_ms, kt, launches, clocks = measure(sess, 0, a.steps, profile=True)
     my_brackets = sum(brackets_in(*wnd) for wnd in windows)
-    total_brackets = my_brackets * world
+    total_brackets = sum_over_ranks(my_brackets)
     value = total_brackets / (max_ms / 1e3)
     roof = gemm_roofline(kt, my_ms, peak)
     field = sess.field()
@@ -489,7 +498,7 @@ def run_b200_arm(a):
     if not a.no_general:
         gsess, _, _ = grown_session("complex")
         gw, g_my_ms, g_max_ms, gkt, _, _ = measure(gsess, 0, max(2, a.steps // 2))
-        gb = sum(brackets_in(*wnd) for wnd in gw) * world
+        gb = sum_over_ranks(sum(brackets_in(*wnd) for wnd in gw))
         general = {"value": gb / (g_max_ms / 1e3), "unit": UNIT, **gemm_roofline(gkt, g_my_ms, peak),
                    "flops_per_unit": "8*N*D per candidate per complex GEMM; commutator 16 d^3"}
         gsess.close()
