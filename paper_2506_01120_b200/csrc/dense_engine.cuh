@@ -534,6 +534,10 @@ private:
       case 32: launch_comm_ah<32>(basis, g0, cnt); return;
       case 64: launch_comm_ah<64>(basis, g0, cnt); return;
       default: {
+        if (use_large_commutator(d_)) {
+          commutator_large(ctx_, basis, true, d_, g0, cnt, tol_, C_.p, hn_.p, nul_.p);
+          return;
+        }
         Timer t(ctx_, 2, 8.0 * d_ * d_ * static_cast<double>(d_) * cnt);
         commutator_ah_generic_kernel<<<cnt, 256, 0, ctx_->stream>>>(basis, d_, g0, cnt, tol_, true, C_.p, hn_.p,
                                                                     nul_.p);
@@ -549,6 +553,10 @@ private:
     case 32: launch_comm<32>(cplx(basis), g0, cnt); break;
     case 64: launch_comm<64>(cplx(basis), g0, cnt); break;
     default: {
+      if (use_large_commutator(d_)) {
+        commutator_large(ctx_, basis, false, d_, g0, cnt, tol_, C_.p, hn_.p, nul_.p);
+        break;
+      }
       Timer t(ctx_, 2, 16.0 * d_ * d_ * static_cast<double>(d_) * cnt);
       commutator_generic_kernel<<<cnt, 256, 0, ctx_->stream>>>(cplx(basis), d_, g0, cnt, tol_, true, cplx(C_.p),
                                                                hn_.p, nul_.p);

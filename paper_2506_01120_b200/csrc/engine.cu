@@ -141,6 +141,8 @@ struct liecl_b200_ctx {
   cudaStream_t stream = nullptr;  // own_stream or a caller-provided stream
   uint64_t kernels = 0;
   DevBuf<double2> splitk_ws;  // split-K partial products of the projection GEMMs
+  DevBuf<double> comm_partial;   // d >= 128 commutators: squared-norm partials
+  DevBuf<double2> comm_scratch;  // ... and unpacked operands / result (packed field)
   std::shared_ptr<void> dense_cache, pauli_cache;  // workspaces of the last one-shot closure
   std::shared_ptr<void> sum_cache;                  // the last multi-term Pauli closure (fetch)
   // per-kernel-class event timing (liecl_b200_ctx_set_timing)
@@ -451,6 +453,87 @@ void gemm_mc_store(liecl_b200_ctx* ctx, const double2* A, int64_t lda, int64_t M
   t.stop();
 }
 
+// ---- K1 for d >= 128 on the DMMA GEMMs (the single-CTA commutator kernels
+// keep both operands in shared memory, which stops at d = 64): per pair
+// P = A B (gemm_mc_store into the output slot), h = P - B A in place with
+// fused squared-norm partials (gemm_subtract), then ||h|| / null / normalise
+// (R:src/closure.cpp:416-424) -- the same epilogue as the small kernels.
+__global__ void comm_norm_kernel(const double* __restrict__ partial, int64_t np, double sqrt_d, double tol,
+                                 double* __restrict__ hn, int* __restrict__ nul) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < np; i += blockDim.x) s += partial[i];  // fixed order
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+    const double h = sqrt(t) / sqrt_d;
+    *hn = h;
+    *nul = !(h > tol) ? 1 : 0;
+  }
+}
+
+__global__ void comm_scale_kernel(double2* __restrict__ o, int64_t D, const double* __restrict__ hn,
+                                  const int* __restrict__ nul) {
+  const double s = *nul ? 0.0 : 1.0 / *hn;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < D;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double2 v = o[e];
+    o[e] = make_double2(v.x * s, v.y * s);
+  }
+}
+
+// basis: complex vec slab, or the packed anti-Hermitian slab (packed = true;
+// operands unpacked, h packed back); out / hn / nul as the small kernels
+bool use_large_commutator(int d) {
+  static const int min_d = [] {
+    const char* e = std::getenv("LIECL_B200_LARGE_COMM_MIN_D");  // 0 disables
+    return e ? std::atoi(e) : 128;
+  }();
+  return min_d > 0 && d >= min_d;
+}
+
+void commutator_large(liecl_b200_ctx* ctx, const double* basis, bool packed, int d, int64_t g0, int cnt, double tol,
+                      double* out, double* hn, int* nul) {
+  const int64_t D = static_cast<int64_t>(d) * d;
+  const int mtiles = (d + zg::BM - 1) / zg::BM;
+  ctx->comm_partial.ensure(static_cast<size_t>(mtiles) * d);
+  if (packed) ctx->comm_scratch.ensure(static_cast<size_t>(3 * D));
+  const unsigned gs = static_cast<unsigned>(std::min<int64_t>((D + 255) / 256, 4096));
+  const double sqrt_d = std::sqrt(static_cast<double>(d));
+  for (int j = 0; j < cnt; ++j) {
+    int64_t l, m;
+    pair_from_index(g0 + j, l, m);
+    const double2 *A, *B;
+    double2* o;
+    if (packed) {
+      double2* sc = ctx->comm_scratch.p;
+      unpack_ah_kernel<<<gs, 256, 0, ctx->stream>>>(basis + l * D, 1, d, sc);
+      unpack_ah_kernel<<<gs, 256, 0, ctx->stream>>>(basis + m * D, 1, d, sc + D);
+      launched(ctx), launched(ctx);
+      A = sc;
+      B = sc + D;
+      o = sc + 2 * D;
+    } else {
+      A = reinterpret_cast<const double2*>(basis) + l * D;
+      B = reinterpret_cast<const double2*>(basis) + m * D;
+      o = reinterpret_cast<double2*>(out) + j * D;
+    }
+    gemm_mc_store(ctx, A, d, d, d, B, d, d, o, d, 1.0);                  // o = A B
+    gemm_subtract(ctx, B, d, d, A, o, d, o, ctx->comm_partial.p);        // o = A B - B A
+    comm_norm_kernel<<<1, 256, 0, ctx->stream>>>(ctx->comm_partial.p, static_cast<int64_t>(mtiles) * d, sqrt_d, tol,
+                                                 hn + j, nul + j);
+    comm_scale_kernel<<<gs, 256, 0, ctx->stream>>>(o, D, hn + j, nul + j);
+    launched(ctx), launched(ctx);
+    if (packed) {
+      pack_ah_kernel<<<gs, 256, 0, ctx->stream>>>(o, 1, d, out + j * D);
+      launched(ctx);
+    }
+  }
+}
+
 // K1 for the general complex field over basis slab `basis` (pairs [g0, g0+cnt))
 void launch_commutator_complex(liecl_b200_ctx* ctx, const double2* basis, int d, int64_t g0, int cnt, double tol,
                                double2* out, double* hn, int* nul) {
@@ -470,6 +553,11 @@ void launch_commutator_complex(liecl_b200_ctx* ctx, const double2* basis, int d,
   case 32: tmpl(std::integral_constant<int, 32>{}); break;
   case 64: tmpl(std::integral_constant<int, 64>{}); break;
   default: {
+    if (use_large_commutator(d)) {
+      commutator_large(ctx, reinterpret_cast<const double*>(basis), false, d, g0, cnt, tol,
+                       reinterpret_cast<double*>(out), hn, nul);
+      break;
+    }
     Timer t(ctx, 2, 16.0 * d * d * static_cast<double>(d) * cnt);
     commutator_generic_kernel<<<cnt, 256, 0, ctx->stream>>>(basis, d, g0, cnt, tol, true, out, hn, nul);
     launched(ctx);

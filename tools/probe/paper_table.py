@@ -11,7 +11,7 @@ ROWS = [  # (method, family, n, path, published seconds)
     ("standard-rank", "spin_glass_hva", 3, "dense", 1.0), ("standard-rank", "spin_glass_hva", 4, "dense", 14.0),
     ("standard-rank", "spin_glass_hva", 5, "dense", 571.0),
     ("orthonorm-dimonly", "xxz_hva", 4, "sums", 0.7), ("orthonorm-dimonly", "xxz_hva", 6, "sums", 2.0),
-    ("orthonorm-dimonly", "xxz_hva", 8, "sums", 5.0),
+    ("orthonorm-dimonly", "xxz_hva", 8, "sums", 5.0), ("orthonorm-dimonly", "xxz_hva", 8, "dense", 5.0),
     ("standard-rank", "xxz_hva", 4, "dense", 0.5), ("standard-rank", "xxz_hva", 6, "dense", 3.0),
     ("orthonorm-dimonly", "tfim_hva_open", 4, "sums", 1.4), ("orthonorm-dimonly", "tfim_hva_open", 6, "sums", 1.8),
     ("orthonorm-dimonly", "tfim_hva_open", 8, "sums", 3.2), ("orthonorm-dimonly", "tfim_hva_open", 10, "sums", 35.0),
