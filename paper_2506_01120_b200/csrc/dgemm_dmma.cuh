@@ -25,6 +25,7 @@ namespace liecl_b200 {
 
 namespace rg {
 constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3;
+constexpr int GROUP = 16;  // M-tiles per raster group: 16 x 4 MB basis tiles stay in L2 while the candidates stream
 constexpr int WM = 2, WN = 2, THREADS = 32 * WM * WN;  // 4 warps, 2 CTAs per SM
 constexpr int WTM = BM / WM, WTN = BN / WN;  // 64 x 32 warp tile
 constexpr int MT = WTM / 8, NT = WTN / 8;    // 8 x 4 m8n8 tiles
@@ -70,7 +71,7 @@ dgemm_dmma_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % WM, wn = warp / WM;
   int m_tile, n_tile;
-  grouped_tile<8>(blockIdx.x + blockIdx.y * gridDim.x, gridDim.x, gridDim.y, m_tile, n_tile);
+  grouped_tile<GROUP>(blockIdx.x + blockIdx.y * gridDim.x, gridDim.x, gridDim.y, m_tile, n_tile);
   const int m0 = m_tile * BM, n0 = n_tile * BN;
   const int KT = K > 0 ? (K + BK - 1) / BK : 0;
 
