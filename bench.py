@@ -77,6 +77,19 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def reduce_over_ranks(x: float, op: str, device=None) -> float:
+    """max / sum of a per-rank scalar over the process group (identity without
+    one): times are maxima over ranks, bracket counts sums (ranks take
+    different rows, so their counts differ)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def window_rows(step_index: int, rank: int, world: int, row0: int, rows: int):
     """Disjoint windows per (step, rank); wraps inside the saturated phase."""
     span = 4095 - row0
@@ -375,21 +388,10 @@ def run_b200_arm(a):
             dist.barrier()
 
     def max_over_ranks(x):
-        if not launched_by_torchrun:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_over_ranks(x, "max", device)
 
     def sum_over_ranks(x):
-        # ranks take different rows, so their bracket counts differ (row l has l)
-        if not launched_by_torchrun:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return reduce_over_ranks(x, "sum", device)
 
     def grown_session(field):
         """Setup (untimed): generator loop + growth phase on the GPU."""
@@ -598,11 +600,7 @@ def run_c3(a):
         torch.cuda.synchronize(device)
 
     def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_over_ranks(x, "max", device)
 
     def step():
         sess.set_basis(V.data_ptr(), on_device=True, n=c3.n)  # reset (untimed)
