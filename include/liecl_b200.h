@@ -62,7 +62,13 @@ typedef struct {
   uint32_t field;           /* 0 = auto: exactly anti-Hermitian operators take the
                                packed-real path (su(d)/u(d), 4x fewer projection
                                flops); 1 = always the general complex path     */
-  uint32_t reserved;
+  uint32_t stop_when_complete; /* 1: an extension (the reference visits every pair):
+                               the dense orthonormal closure loop stops once the
+                               basis provably spans every bracket (n = d^2, or
+                               n = d^2 - 1 with a traceless span, certified to
+                               tol/100). Basis and dimension are unchanged;
+                               commutators_evaluated / independence_checks count
+                               the pairs visited. Default 0.                  */
   /* matrix-inversion method (Alg. 2): ClosureConfig::conditioning_floor and
    * gram_refresh_interval (R:include/liecl/closure.hpp:97-100), used as given
    * (the reference defaults are 1e-12 and 256; interval 0 = no cadence refresh) */

@@ -21,7 +21,7 @@ class DenseEngine {
 public:
   DenseEngine(liecl_b200_ctx* ctx, int d, bool keep_original, const liecl_b200_config& cfg)
       : ctx_(ctx), d_(d), D_(static_cast<int64_t>(d) * d), keep_(keep_original), tol_(cfg.tolerance),
-        record_(cfg.record_log != 0), force_complex_(cfg.field == 1) {
+        record_(cfg.record_log != 0), force_complex_(cfg.field == 1), stop_complete_(cfg.stop_when_complete != 0) {
     if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
     cap_ = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : D_;
@@ -73,6 +73,8 @@ public:
   }
   void reset(const liecl_b200_config& cfg) {
     tol_ = cfg.tolerance;
+    stop_complete_ = cfg.stop_when_complete != 0;
+    complete_n_ = -1;
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
     record_ = cfg.record_log != 0;
     set_deadline(cfg);
@@ -316,7 +318,38 @@ public:
       const int64_t cnt = std::min(B_cur_, avail - g);
       run_adaptive_batch(g, cnt);
       g += cnt;
+      if (stop_complete_ && complete()) break;  // opt-in: every later bracket is dependent
     }
+  }
+
+  // stop_when_complete (an extension; the reference always visits every pair):
+  // the orthonormal tuple spans every operator a bracket can produce. Brackets
+  // are traceless, so that holds when n = D, or when n = D - 1 and the
+  // normalised traces c_k = tr V_k / d have ||c|| <= tol / 100: then no
+  // traceless unit candidate can leave a residual above tol / 100.
+  bool complete() {
+    const int64_t n = n_o_;
+    if (n >= D_) return true;
+    if (n != D_ - 1) return false;
+    if (complete_n_ == n) return complete_;
+    DevBuf<double> tr;
+    tr.ensure(static_cast<size_t>(n));
+    trace_abs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx_->stream>>>(
+        V_.p, n, vw(), d_, field_ == Field::kAntiHerm ? 1 : 0, tr.p);
+    launched(ctx_);
+    std::vector<double> h(static_cast<size_t>(n));
+    CU(cudaMemcpyAsync(h.data(), tr.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    // the span's normal is e - sum_k c_k V_k (normalised), c_k = <V_k, I> = conj(tr V_k) / d,
+    // so a traceless unit h has |<normal, h>| = |sum_k conj(c_k) <V_k, h>| <= ||c|| (Cauchy-Schwarz)
+    double c2 = 0.0;
+    for (double v : h) c2 += (v / d_) * (v / d_);
+    complete_ = std::sqrt(c2) <= tol_ / 100.0;
+    complete_n_ = n;
+    if (std::getenv("LIECL_B200_TRACE"))
+      std::fprintf(stderr, "[dense] n=%lld complete-span certificate ||c||=%.3g (needs <= %.3g)\n",
+                   static_cast<long long>(n), std::sqrt(c2), tol_ / 100.0);
+    return complete_;
   }
 
   // basis (originals for Alg. 3) or orthonormal tuple -> host, complex vec layout
@@ -846,6 +879,9 @@ private:
   double tol_;
   bool record_;
   bool force_complex_;
+  bool stop_complete_ = false;
+  int64_t complete_n_ = -1;
+  bool complete_ = false;
   std::unique_ptr<Reducer> red_;  // set: D-sharded (D_ is this rank's slice)
   Field field_ = Field::kUnset;
   Field slab_field_ = Field::kUnset;  // layout the basis slabs are allocated for

@@ -257,6 +257,22 @@ __global__ void linear_combination_kernel(const double2* __restrict__ ops, const
   }
 }
 
+// |tr V_k| of n basis vectors (stride vw doubles): complex vec layout, or the
+// packed anti-Hermitian layout (A(i,i) = i M(i,i))
+__global__ void trace_abs_kernel(const double* __restrict__ V, int64_t n, int64_t vw, int d, int packed,
+                                 double* __restrict__ out) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const double* v = V + k * vw;
+  double re = 0.0, im = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const int64_t e = static_cast<int64_t>(i) * (d + 1);
+    if (packed) im += v[e];
+    else re += v[2 * e], im += v[2 * e + 1];
+  }
+  out[k] = sqrt(re * re + im * im);
+}
+
 // ------------------------------------------------------------ GEMM launch ---
 
 // Function attributes are per device context: a process may drive several

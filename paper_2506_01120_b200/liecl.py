@@ -185,6 +185,10 @@ class ClosureConfig:
     # "auto": exactly anti-Hermitian operators (i*H, every dense BASELINE
     # config) take the packed-real path; "complex": always the general path
     field: str = "auto"
+    # extension (not in the reference): stop the dense orthonormal closure once
+    # the basis provably spans every bracket; the basis is unchanged, the
+    # pair counts cover only the pairs visited
+    stop_when_complete: bool = False
 
     def native(self) -> native.Config:
         rel = 0.0
@@ -195,7 +199,8 @@ class ClosureConfig:
         if self.field not in ("auto", "complex"):
             raise InvalidInputError(f"unknown field '{self.field}' (expected auto or complex)")
         return native.Config(float(self.tolerance), int(self.max_dim), int(self.threads), int(self.record_log),
-                             rel, int(self.batch_max), 1 if self.field == "complex" else 0, 0,
+                             rel, int(self.batch_max), 1 if self.field == "complex" else 0,
+                             int(bool(self.stop_when_complete)),
                              float(self.conditioning_floor), int(self.gram_refresh_interval),
                              float(self.rank_tolerance))
 

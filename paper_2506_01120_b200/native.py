@@ -43,7 +43,7 @@ class NativeUnavailable(RuntimeError):
 class Config(C.Structure):
     _fields_ = [("tolerance", C.c_double), ("max_dim", C.c_uint64), ("threads", C.c_uint32),
                 ("record_log", C.c_uint32), ("deadline_seconds", C.c_double), ("batch_max", C.c_int64),
-                ("field", C.c_uint32), ("reserved", C.c_uint32), ("conditioning_floor", C.c_double),
+                ("field", C.c_uint32), ("stop_when_complete", C.c_uint32), ("conditioning_floor", C.c_double),
                 ("gram_refresh_interval", C.c_uint64), ("rank_tolerance", C.c_double)]
 
 

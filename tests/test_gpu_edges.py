@@ -189,3 +189,24 @@ def test_large_d_commutator_matches_pauli_sums(field):
         assert min(np.abs(got - ph * want).max() for ph in (1, -1, 1j, -1j)) < 1e-9, k
     rk = liecl.closure_dense_arrays(gens, 1 << n, liecl.Method.standard_rank, liecl.ClosureConfig(tolerance=1e-10))
     assert rk.dimension == r.dimension
+
+
+@pytest.mark.parametrize("field", ["auto", "complex"])
+def test_stop_when_complete_keeps_the_basis(field):
+    """Opt-in early stop (an extension): spin-glass n = 4 closes to su(16)
+    (255 = d^2 - 1, traceless span); the stopped closure returns the same
+    basis bit for bit after visiting fewer pairs. A closure that never fills
+    the space (TFIM n = 4, dim 16) is unaffected."""
+    gens = np.stack([w.vec(1j * w.from_pauli(sp)) for sp in w.spin_glass_hva(4)])
+    full = liecl.closure_dense_arrays(gens, 16, liecl.Method.orthonorm_dimonly,
+                                      liecl.ClosureConfig(tolerance=1e-10, field=field))
+    stop = liecl.closure_dense_arrays(gens, 16, liecl.Method.orthonorm_dimonly,
+                                      liecl.ClosureConfig(tolerance=1e-10, field=field, stop_when_complete=True))
+    assert full.dimension == stop.dimension == 255
+    assert np.array_equal(full.basis_array.view(np.uint64), stop.basis_array.view(np.uint64))
+    assert stop.stats.commutators_evaluated < full.stats.commutators_evaluated == 255 * 254 // 2
+    tf = np.stack([w.vec(1j * w.from_pauli(sp)) for sp in w.tfim_hva_open(4)])
+    a = liecl.closure_dense_arrays(tf, 16, liecl.Method.orthonorm_dimonly, liecl.ClosureConfig(tolerance=1e-10, field=field))
+    b = liecl.closure_dense_arrays(tf, 16, liecl.Method.orthonorm_dimonly,
+                                   liecl.ClosureConfig(tolerance=1e-10, field=field, stop_when_complete=True))
+    assert a.dimension == b.dimension and a.stats.commutators_evaluated == b.stats.commutators_evaluated
