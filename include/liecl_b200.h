@@ -260,6 +260,14 @@ int liecl_b200_session_set_basis(liecl_b200_session* s, const double* V, int64_t
  * with the same pointer and count waits for that copy instead of copying.
  * V must stay unchanged until then. */
 int liecl_b200_session_prefetch_basis(liecl_b200_session* s, const double* V, int64_t n);
+
+/* Start the host -> device copy of a candidate stream (n operators, pinned host
+ * memory) on a side stream, so it overlaps the work in flight; the next
+ * liecl_b200_session_check_candidates(s, cands, n, 0, ...) with the same
+ * pointer and count reads the device copy. Two copies may be in flight (the
+ * next step's while the current one is checked). The host memory must stay
+ * unchanged until that check returns. */
+int liecl_b200_session_prefetch_candidates(liecl_b200_session* s, const double* cands, int64_t n);
 int liecl_b200_session_run_pairs(liecl_b200_session* s, int64_t g_begin, int64_t g_end,
                                  liecl_b200_stats* stats);
 int liecl_b200_session_run_rows(liecl_b200_session* s, int64_t row_begin, int64_t row_end,

@@ -1411,6 +1411,14 @@ int liecl_b200_session_prefetch_basis(liecl_b200_session* s, const double* V, in
   });
 }
 
+int liecl_b200_session_prefetch_candidates(liecl_b200_session* s, const double* cands, int64_t n) {
+  return guarded([&] {
+    if (!s || (n > 0 && !cands) || n < 0) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    use_device(s->ctx);
+    s->eng->prefetch_candidates(reinterpret_cast<const double2*>(cands), n);
+  });
+}
+
 int liecl_b200_session_run_pairs(liecl_b200_session* s, int64_t g_begin, int64_t g_end, liecl_b200_stats* stats) {
   return guarded([&] {
     if (!s) throw Error(LIECL_B200_INVALID_INPUT, "null session");

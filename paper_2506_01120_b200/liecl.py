@@ -856,6 +856,14 @@ class ClosureSession:
         _check(self.lib.liecl_b200_session_prefetch_basis(self.ptr, C.cast(C.c_void_p(V_ptr), C.POINTER(C.c_double)),
                                                           C.c_int64(n)))
 
+    def prefetch_candidates(self, cands_ptr: int, n: int):
+        """Start the async H2D copy of n host candidates at cands_ptr (pinned,
+        (n, width) complex128); the next check_candidates(cands_ptr, n=n) reads
+        the device copy. Up to two copies in flight (the next step's while the
+        current one is checked); the host memory must stay unchanged until then."""
+        _check(self.lib.liecl_b200_session_prefetch_candidates(
+            self.ptr, C.cast(C.c_void_p(cands_ptr), C.POINTER(C.c_double)), C.c_int64(n)))
+
     def run_pairs(self, g_begin: int, g_end: int) -> dict:
         st = native.Stats()
         _check(self.lib.liecl_b200_session_run_pairs(self.ptr, C.c_int64(g_begin), C.c_int64(g_end), C.byref(st)))

@@ -24,7 +24,7 @@ EXPORTED = [
     "liecl_b200_closure_pauli", "liecl_b200_closure_pauli_sums", "liecl_b200_pauli_sums_fetch",
     "liecl_b200_project_residual_dense", "liecl_b200_commutator_dense", "liecl_b200_inner_product_dense",
     "liecl_b200_norm_dense", "liecl_b200_linear_combination_dense", "liecl_b200_from_pauli", "liecl_b200_session_create_dense", "liecl_b200_session_destroy",
-    "liecl_b200_session_set_basis", "liecl_b200_session_prefetch_basis", "liecl_b200_session_run_pairs", "liecl_b200_session_run_rows",
+    "liecl_b200_session_set_basis", "liecl_b200_session_prefetch_basis", "liecl_b200_session_prefetch_candidates", "liecl_b200_session_run_pairs", "liecl_b200_session_run_rows",
     "liecl_b200_session_size", "liecl_b200_session_field", "liecl_b200_session_get_basis",
     "liecl_b200_session_get_vectors", "liecl_b200_session_screen_pairs",
     "liecl_b200_session_get_log",

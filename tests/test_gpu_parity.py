@@ -392,3 +392,39 @@ def test_session_accepts_host_pointers():
     assert np.array_equal(ind_a, ind_b) and np.array_equal(rn_a, rn_b) and ind_a.sum() == 10
     with pytest.raises(liecl.InvalidInputError):
         s.check_candidates(hc.data_ptr())
+
+
+def test_candidate_prefetch_matches_direct_checks():
+    """prefetch_candidates: the next stream's H2D on a side stream, consumed by
+    the matching check_candidates; two copies in flight (alternating pinned
+    buffers) give the same verdicts and norms as direct host checks."""
+    import torch
+    rng = np.random.default_rng(21)
+    d = 8
+    D = d * d
+    V = []
+    while len(V) < 20:  # orthonormal (1/d inner product) complex basis
+        v = rng.standard_normal(D) + 1j * rng.standard_normal(D)
+        for u in V:
+            v = v - (np.vdot(u, v) / d) * u
+        V.append(v / np.sqrt(np.vdot(v, v).real / d))
+    V = np.array(V)
+    streams = []
+    for s in range(4):
+        c = rng.standard_normal((30, D)) + 1j * rng.standard_normal((30, D))
+        c[::3] = rng.standard_normal((10, 20)) @ V  # in-span rows
+        streams.append(c)
+    ref = liecl.ClosureSession(d, config=liecl.ClosureConfig(tolerance=1e-10))
+    ses = liecl.ClosureSession(d, config=liecl.ClosureConfig(tolerance=1e-10))
+    bufs = [torch.empty((30, D), dtype=torch.complex128, pin_memory=True) for _ in range(2)]
+    bufs[0].numpy()[:] = streams[0]
+    for k in range(4):
+        ref.set_basis(V)
+        ses.set_basis(V)
+        if k + 1 < 4:
+            bufs[(k + 1) % 2].numpy()[:] = streams[k + 1]
+            ses.prefetch_candidates(bufs[(k + 1) % 2].data_ptr(), 30)
+        want = ref.check_candidates(streams[k])
+        got = ses.check_candidates(bufs[k % 2].data_ptr(), n=30)
+        assert np.array_equal(got[0], want[0])
+        assert np.allclose(got[1], want[1], rtol=1e-12, atol=1e-14)
