@@ -268,6 +268,18 @@ def secondary_closures():
         out[name] = {"dimension": r.dimension, "brackets": r.stats.commutators_evaluated, "seconds": dt,
                      "brackets_per_s": r.stats.commutators_evaluated / dt,
                      "cpu_baseline": dense_cpu_baseline(cfg.generators, cfg.d, "orthonorm-dimonly", r.dimension)}
+    # config 2 as a whole closure (growth + all 8,382,465 pairs, the reference's
+    # semantics) and with the opt-in stop_when_complete extension (same basis;
+    # stops once a trace certificate proves it spans su(64)). Same size as the
+    # paper's spin-glass n = 6 row (dim 4095, 8 s; BASELINE.md:31)
+    c2 = w.config2()
+    for key, stop in (("c2_full_closure", False), ("c2_full_closure_stop_when_complete", True)):
+        t0 = time.perf_counter()
+        r = liecl.closure_dense_arrays(c2.generators, c2.d, liecl.Method.orthonorm_dimonly,
+                                       liecl.ClosureConfig(tolerance=c2.tol, stop_when_complete=stop))
+        dt = time.perf_counter() - t0
+        out[key] = {"dimension": r.dimension, "brackets": r.stats.commutators_evaluated, "seconds": dt,
+                    "brackets_per_s": r.stats.commutators_evaluated / dt}
     p = w.config4()
     liecl.closure_pauli_arrays(p.x, p.z, p.coef, p.qubits, liecl.Method.orthonorm_dimonly,
                                liecl.ClosureConfig(tolerance=p.tol))
