@@ -60,20 +60,28 @@ for it in range(ITERS):
     cands = np.array(cands)
     want_ind, want_rn, _ = port.check_sequence_dense(V, cands, d, tol=1e-10, append=True)
     s = liecl.ClosureSession(d, config=liecl.ClosureConfig(tolerance=1e-10, batch_max=random.choice([0, 1, 7, 64])))
-    mode = random.choice(["numpy", "pinned"])
+    mode = random.choice(["numpy", "pinned", "prefetch"])
     if n:
         s.set_basis(V)
     got_ind, got_rn = [], []
     pos = 0
-    pinned = torch.from_numpy(cands.copy()).pin_memory() if mode == "pinned" else None
+    pinned = torch.from_numpy(cands.copy()).pin_memory() if mode != "numpy" else None
+    chunks = []
     while pos < len(cands):
         k = int(rng.integers(1, len(cands) - pos + 1))
-        if mode == "numpy":
-            ind, rn, _ = s.check_candidates(cands[pos:pos + k])
-        else:
-            ind, rn, _ = s.check_candidates(pinned.data_ptr() + pos * D * 16, n=k)
-        got_ind += list(ind); got_rn += list(rn)
+        chunks.append((pos, k))
         pos += k
+    if mode == "prefetch":  # chunk i+1's H2D in flight while chunk i is checked
+        s.prefetch_candidates(pinned.data_ptr() + chunks[0][0] * D * 16, chunks[0][1])
+    for i, (p0, k) in enumerate(chunks):
+        if mode == "numpy":
+            ind, rn, _ = s.check_candidates(cands[p0:p0 + k])
+        else:
+            if mode == "prefetch" and i + 1 < len(chunks):
+                q0, qk = chunks[i + 1]
+                s.prefetch_candidates(pinned.data_ptr() + q0 * D * 16, qk)
+            ind, rn, _ = s.check_candidates(pinned.data_ptr() + p0 * D * 16, n=k)
+        got_ind += list(ind); got_rn += list(rn)
     got_ind, got_rn = np.array(got_ind), np.array(got_rn)
     ok = np.array_equal(got_ind, want_ind) and np.allclose(got_rn, want_rn, rtol=1e-9, atol=1e-12)
     ok = ok and s.size() == n + int(want_ind.sum())
