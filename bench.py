@@ -648,7 +648,10 @@ def run_c3(a):
         # two pinned buffers, as a streaming producer fills them: step s reads
         # buffer s % 2 while buffer (s+1) % 2 is copied to the device on a side
         # stream (liecl_b200_session_prefetch_candidates). Every step's copy
-        # sits inside a timed step: the first timed step copies its own.
+        # sits inside a timed step: the first timed step copies its own, and
+        # a device-wide synchronize before f1 holds each step open until the
+        # next step's prefetch has landed (so no copy hides in the untimed
+        # reset between steps).
         host_c = [torch.empty(cands.shape, dtype=cands.dtype, pin_memory=True) for _ in range(2)]
         for h in host_c:
             h.copy_(cands)
@@ -662,6 +665,7 @@ def run_c3(a):
             if k + 1 < a.steps:
                 sess.prefetch_candidates(host_c[(k + 1) % 2].data_ptr(), c3.ncand)
             ind_e, _, _ = sess.check_candidates(host_c[k % 2].data_ptr(), on_device=False, n=c3.ncand)
+            torch.cuda.synchronize(device)  # includes the side stream's prefetch of step k+1
             f1.record(stream)
             torch.cuda.synchronize(device)
             e2e_ms.append(max_over_ranks(f0.elapsed_time(f1)))

@@ -186,6 +186,7 @@ public:
       CU(cudaMemcpyAsync(tmp_o, orig, static_cast<size_t>(n_orig * D_) * sizeof(double2), kind, ctx_->stream));
     const Field f = classify(tmp, n + (orig ? n_orig : 0));
     n_o_ = n_b_ = 0;
+    complete_n_ = -1;  // the completeness certificate belongs to the old basis
     field_ = f;
     layout_slabs();
     alloc_batch();
@@ -383,8 +384,8 @@ public:
   // stop_when_complete (an extension; the reference always visits every pair):
   // the orthonormal tuple spans every operator a bracket can produce. Brackets
   // are traceless, so that holds when n = D, or when n = D - 1 and the
-  // normalised traces c_k = tr V_k / d have ||c|| <= tol / 100: then no
-  // traceless unit candidate can leave a residual above tol / 100.
+  // normalised traces c_k = tr V_k / d satisfy ||c|| / sqrt(1 - ||c||^2) <=
+  // tol / 100: then no traceless unit candidate can leave a residual above tol / 100.
   bool complete() {
     const int64_t n = n_o_;
     if (n >= D_) return true;
@@ -398,11 +399,12 @@ public:
     std::vector<double> h(static_cast<size_t>(n));
     CU(cudaMemcpyAsync(h.data(), tr.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
-    // the span's normal is e - sum_k c_k V_k (normalised), c_k = <V_k, I> = conj(tr V_k) / d,
-    // so a traceless unit h has |<normal, h>| = |sum_k conj(c_k) <V_k, h>| <= ||c|| (Cauchy-Schwarz)
+    // the span's normal is u = (e - sum_k c_k V_k) / sqrt(1 - ||c||^2), c_k = <V_k, e> = conj(tr V_k) / d
+    // (e = I / ||I||); a traceless unit h has <e, h> = 0, so its residual is
+    // |<u, h>| = |sum_k conj(c_k) <V_k, h>| / sqrt(1 - ||c||^2) <= ||c|| / sqrt(1 - ||c||^2) (Cauchy-Schwarz)
     double c2 = 0.0;
     for (double v : h) c2 += (v / d_) * (v / d_);
-    complete_ = std::sqrt(c2) <= tol_ / 100.0;
+    complete_ = c2 < 1.0 && std::sqrt(c2 / (1.0 - c2)) <= tol_ / 100.0;
     complete_n_ = n;
     if (std::getenv("LIECL_B200_TRACE"))
       std::fprintf(stderr, "[dense] n=%lld complete-span certificate ||c||=%.3g (needs <= %.3g)\n",
@@ -768,7 +770,11 @@ private:
         continue;
       }
       ++st_.independence_checks;
-      if (s >= nsurv || h_idx_.p[s] != j) {  // certified reject from pass 1
+      if (s >= nsurv || h_idx_.p[s] != j) {
+        // certified reject from pass 1. The norm reported (log, check_candidates)
+        // is the pass-1 residual: an upper bound (up to O(eps)) of the reference's
+        // CGS2 norm (R:src/closure.cpp:277-280), both <= tol/20 + 1e-14. Pinned by
+        // tests/test_gpu_parity.py::test_reject_norms_are_pass1_bounds.
         log_decision(l, m, 0, 0, 0, h_rn1_.p[j]);
         if (indep_out) indep_out[j] = 0;
         if (rn_out) rn_out[j] = h_rn1_.p[j];

@@ -15,6 +15,10 @@
 #include "liecl/generators.hpp"
 #include "liecl/pauli.hpp"
 
+#ifndef LIECL_DROPIN_SRC_SHA
+#define LIECL_DROPIN_SRC_SHA "unknown"
+#endif
+
 using namespace liecl;
 
 static void print_stats(const ClosureResult& r) {
@@ -178,8 +182,9 @@ int main() {
         }
       });
     for (auto& th : pool) th.join();
-    std::printf("\"concurrent_identical\": %s", (ok[0] && ok[1] && ok[2] && ok[3]) ? "true" : "false");
+    std::printf("\"concurrent_identical\": %s, ", (ok[0] && ok[1] && ok[2] && ok[3]) ? "true" : "false");
   }
-  std::printf("}\n");
+  // the sources this binary was built from (tests refuse a stale binary)
+  std::printf("\"src_sha\": \"%s\"}\n", LIECL_DROPIN_SRC_SHA);
   return 0;
 }

@@ -327,3 +327,86 @@ class Config3:
             a = cgauss(n_odd, self.n)
             cands[1::2] = a @ V + self.noise * cgauss(n_odd, self.D)
         return V, cands
+
+
+@dataclass(frozen=True)
+class Config3Exact:
+    """Config 3's recipe at a size the reference finishes in about a minute,
+    with inputs that any machine regenerates bit for bit from the seed using
+    numpy alone (the reference-generated golden tests/golden/c3_exact_*.npz
+    stores only the reference's outputs; the inputs are 134 MB).
+
+    basis: V_j[e] = ph[e] * H[s_j, p(e)] / sqrt(d), with H the D x D
+    Sylvester-Hadamard matrix (entries +-1), s a random row subset, p a random
+    element permutation and ph a random phase in {1, i, -1, -i} per element:
+    exactly orthonormal under <a, b> = vdot(a, b) / d (R:src/dense.cpp:57),
+    every entry exactly (+-1 or +-i) / 8 at d = 64.
+    candidates: k even complex Gaussian (PCG64 normals); k odd sum_j a_j V_j
+    with dyadic a_j = round(2^10 N(0,1)) / 2^10 (every partial sum of the
+    combination is an integer multiple of 2^-13 below 2^53, so any summation
+    order gives the same bits), plus noise sigma = 1e-14 per re/im component
+    as in config 3."""
+    d: int = 64
+    n: int = 2048
+    ncand: int = 512
+    noise: float = 1e-14
+    seed: int = 7
+    tol: float = 1e-10
+
+    @property
+    def D(self) -> int:
+        return self.d * self.d
+
+    @property
+    def name(self) -> str:
+        return f"c3_exact_d{self.d}_n{self.n}_c{self.ncand}_s{self.seed}"
+
+    def generate_numpy(self):
+        import numpy as np
+        D = self.D
+        rng = np.random.default_rng(self.seed)
+        rows = np.sort(rng.choice(D, size=self.n, replace=False))
+        perm = rng.permutation(D)
+        ph = rng.integers(0, 4, size=D)
+        # Sylvester-Hadamard rows: H[r, e] = (-1)^popcount(r & e)
+        e = perm.astype(np.int64)
+        par = np.zeros((self.n, D), np.int64)
+        r = rows.astype(np.int64)[:, None]
+        x = r & e[None, :]
+        while np.any(x):
+            par ^= x & 1
+            x = x >> 1
+        H = (1 - 2 * par).astype(np.float64)  # +-1, rows s_j, columns permuted
+        del par, x
+        re_ph = np.array([1.0, 0.0, -1.0, 0.0])[ph]
+        im_ph = np.array([0.0, 1.0, 0.0, -1.0])[ph]
+        scale = 1.0 / np.sqrt(self.d)  # exact for d = 4^k
+        V = np.empty((self.n, D), np.complex128)
+        V.real = H * (re_ph * scale)
+        V.imag = H * (im_ph * scale)
+        cands = np.empty((self.ncand, D), np.complex128)
+        n_even = (self.ncand + 1) // 2
+        g = rng.standard_normal((n_even, D, 2))
+        cands[0::2].real = g[..., 0]
+        cands[0::2].imag = g[..., 1]
+        n_odd = self.ncand // 2
+        if n_odd:
+            ka = np.rint(rng.standard_normal((n_odd, self.n, 2)) * 1024.0)  # integers, |k| < 2^13
+            # combination / ph = sum_j a_j H[s_j] * scale: integer sums, exact in any order
+            sre = (ka[..., 0] @ H) * (scale / 1024.0)
+            sim = (ka[..., 1] @ H) * (scale / 1024.0)
+            # (sre + i sim) * ph with ph in {1, i, -1, -i}: exact component moves
+            cre = np.where(ph == 0, sre, np.where(ph == 1, -sim, np.where(ph == 2, -sre, sim)))
+            cim = np.where(ph == 0, sim, np.where(ph == 1, sre, np.where(ph == 2, -sim, -sre)))
+            noise = rng.standard_normal((n_odd, D, 2)) * self.noise
+            cands[1::2].real = cre + noise[..., 0]
+            cands[1::2].imag = cim + noise[..., 1]
+        return V, cands
+
+    @staticmethod
+    def digest(V, cands) -> str:
+        import hashlib
+        h = hashlib.sha256()
+        h.update(V.tobytes())
+        h.update(cands.tobytes())
+        return h.hexdigest()[:16]

@@ -95,12 +95,43 @@ def sums_cases():
             save(f"sums_{family}_n{n}_{method}", meta, arrays)
 
 
+def c3_golden():
+    """Config 3's ordered check-and-append (R:src/closure.cpp:142-162 per
+    candidate, accepted residual units appended) on w.Config3Exact: inputs a
+    GPU box regenerates bit for bit with numpy alone (no BLAS or libm rounding
+    in them), so only the reference's outputs are stored."""
+    import time
+    c = w.Config3Exact()
+    V, cands = c.generate_numpy()
+    t0 = time.perf_counter()
+    ind, rn, secs = Ref().check_sequence_dense(V, cands, c.d, tol=c.tol, append=True)
+    meta = {"name": c.name, "d": c.d, "n": c.n, "ncand": c.ncand, "tol": c.tol, "noise": c.noise,
+            "input_digest": c.digest(V, cands), "accepted": int(ind.sum()), "seconds": round(secs, 1),
+            "build": "libliecl_ref.so (liecl_ref_check_sequence_dense, append)"}
+    save(c.name, meta, {"independent": ind, "residual_norm": rn})
+    print(f"c3 golden: {ind.sum()} accepted of {len(ind)} in {time.perf_counter() - t0:.1f} s")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true")
     ap.add_argument("--only-sums", action="store_true")
+    ap.add_argument("--c2-orthonorm", action="store_true",
+                    help="only config 2's growth phase under Alg. 3 (orthonorm, keep_original): ~10 min")
+    ap.add_argument("--c3-golden", action="store_true",
+                    help="only the exact-input config-3 stand-in (ordered check-and-append): ~1 min")
     a = ap.parse_args()
     build()
+    if a.c2_orthonorm:
+        cfg = w.config2()
+        meta, arr = dense_case(Ref(), cfg, "orthonorm", rows=C2_ROWS, threads=os.cpu_count(),
+                               keep_vectors=[0, 1, 2, 64, 512, 2048, 4094])
+        meta["rows"] = C2_ROWS
+        save(f"{cfg.name}_orthonorm_rows{C2_ROWS}", meta, arr)
+        return
+    if a.c3_golden:
+        c3_golden()
+        return
     sums_cases()
     if a.only_sums:
         return

@@ -1,6 +1,7 @@
 """The C++ drop-in: a liecl consumer (reference headers + reference pauli/dense/
 operator/generators objects) linked with closure_b200.cpp instead of
 R:src/closure.cpp, calling liecl::run_closure / project_residual on the GPU."""
+import hashlib
 import json
 import os
 import subprocess
@@ -20,7 +21,14 @@ def demo():
         pytest.skip("drop-in demo not built (needs the reference headers at build time)")
     out = subprocess.run([DEMO], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
-    return json.loads(out.stdout)
+    res = json.loads(out.stdout)
+    # the binary must come from the sources in this tree (build() runs `make dropin`)
+    h = hashlib.sha256()
+    for f in ("closure_b200.cpp", "dropin_demo.cpp"):
+        with open(os.path.join(ROOT, "paper_2506_01120_b200", "csrc", "dropin", f), "rb") as fh:
+            h.update(fh.read())
+    assert res["src_sha"] == h.hexdigest()[:16], "stale drop-in demo: rebuild with `make -C paper_2506_01120_b200/csrc dropin`"
+    return res
 
 
 @pytest.mark.parametrize("method", ["orthonorm-dimonly", "orthonorm"])
