@@ -205,11 +205,63 @@ int liecl_b200_pauli_sums_fetch(liecl_b200_ctx* ctx, int64_t cap, int64_t* basis
                                 uint64_t* basis_z, double* basis_coef, int64_t term_cap, int64_t* ortho_offsets,
                                 uint64_t* ortho_x, uint64_t* ortho_z, double* ortho_coef, int64_t ortho_term_cap);
 
+/* result.gram of the last liecl_b200_closure_pauli_sums call with method
+ * LIECL_B200_METHOD_MATRIX_INVERSION (Alg. 2 over multi-term sums; its
+ * result.basis is the accepted unit brackets): the Gram matrix A and its
+ * maintained inverse, n x n column-major complex (n = stats->dimension). */
+int liecl_b200_pauli_sums_fetch_gram(liecl_b200_ctx* ctx, double* gram_out, double* inverse_out);
+
 /* project_residual (R:include/liecl/closure.hpp:139-140): residual after two
  * projection passes against the orthonormal tuple V (n operators), plus the
  * first-pass coefficients (n complex). Host buffers. */
 int liecl_b200_project_residual_dense(liecl_b200_ctx* ctx, const double* V, int64_t n, const double* h,
                                       int32_t d, double* residual, double* coeffs);
+
+/*
+ * project_residual / linear_combination / check_matrix_inversion over Pauli
+ * sums (R:src/closure.cpp:107-162; R:src/operator.cpp:164-181, the PauliSum
+ * branch), on the device. The tuple is n sums, terms [offsets[l],
+ * offsets[l+1]) of (x, z, coef re/im); h is one sum of h_terms terms; all in
+ * PauliSum form (unique strings sorted by (z, x)); qubits <= 31. A result sum
+ * goes to (rx, rz, rcoef) with room for term_cap terms, *out_terms = its size
+ * (LIECL_B200_CAPACITY "output buffers too small" when it exceeds term_cap;
+ * h_terms + the tuple's total terms always suffices). project_residual and
+ * linear_combination are bit-exact with the reference's PauliSum arithmetic:
+ *   project_residual_pauli : two passes; coeffs = first-pass <V_l, h> (n complex)
+ *   linear_combination_pauli : from_terms(base_coeff * h ++ coeffs[l] * V_l)
+ *   check_matrix_inversion_pauli : beta_l = <B_l, h>, x = A^{-1} beta (inverse
+ *       n x n column-major), independent = ||h - sum_l x_l B_l|| > tol
+ */
+int liecl_b200_project_residual_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                      const uint64_t* z, const double* coef, int64_t n, uint32_t qubits,
+                                      int64_t h_terms, const uint64_t* hx, const uint64_t* hz, const double* hcoef,
+                                      uint64_t* rx, uint64_t* rz, double* rcoef, int64_t term_cap,
+                                      int64_t* out_terms, double* coeffs);
+int liecl_b200_linear_combination_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                        const uint64_t* z, const double* coef, int64_t n, uint32_t qubits,
+                                        int64_t h_terms, const uint64_t* hx, const uint64_t* hz, const double* hcoef,
+                                        double base_re, double base_im, const double* coeffs, uint64_t* rx,
+                                        uint64_t* rz, double* rcoef, int64_t term_cap, int64_t* out_terms);
+/* inner_product(V_l, h) for every tuple element (sum_inner_product,
+ * R:src/pauli.cpp:202-220) -> beta_out (n complex), and norm(h) (sum_norm,
+ * :222-228); bit-exact */
+int liecl_b200_overlaps_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x, const uint64_t* z,
+                              const double* coef, int64_t n, uint32_t qubits, int64_t h_terms, const uint64_t* hx,
+                              const uint64_t* hz, const double* hcoef, double* beta_out);
+/* PauliSum::from_terms (R:src/pauli.cpp:78-115) of n raw terms (duplicates
+ * merged in input order, |c| <= 1e-14 max |c| dropped, sorted by (z, x)), and
+ * PauliSum::operator*(Complex) (:166-177) on a coefficient array; bit-exact */
+int liecl_b200_pauli_from_terms(liecl_b200_ctx* ctx, int64_t n, const uint64_t* x, const uint64_t* z,
+                                const double* coef, uint32_t qubits, uint64_t* rx, uint64_t* rz, double* rcoef,
+                                int64_t term_cap, int64_t* out_terms);
+int liecl_b200_scale_terms(liecl_b200_ctx* ctx, int64_t n, const double* coef, double re, double im, double* out);
+int liecl_b200_norm_pauli(liecl_b200_ctx* ctx, int64_t h_terms, const uint64_t* hx, const uint64_t* hz,
+                          const double* hcoef, uint32_t qubits, double* out);
+int liecl_b200_check_matrix_inversion_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                            const uint64_t* z, const double* coef, int64_t n, uint32_t qubits,
+                                            const double* inverse, int64_t h_terms, const uint64_t* hx,
+                                            const uint64_t* hz, const double* hcoef, double tol,
+                                            int32_t* independent, double* beta_out, double* residual_norm);
 
 /* commutator / inner_product / norm of dense operators
  * (R:include/liecl/operator.hpp:54-60). Host buffers. */
@@ -318,6 +370,48 @@ int liecl_b200_nccl_unique_id(uint8_t* id_out);
 int liecl_b200_shard_range(int32_t d, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi);
 int liecl_b200_session_set_shards(liecl_b200_session* s, int32_t nranks, int32_t rank, const uint8_t* nccl_id,
                                   liecl_b200_reduce_fn reduce, void* user);
+
+/*
+ * The last liecl_b200_closure_dense / liecl_b200_closure_dense_gram result of a
+ * context stays on the device until the next dense closure on that context.
+ * Passing basis_out = NULL to either call skips the copy (stats, warnings and
+ * the log are still written; stats->dimension sizes the fetch), and
+ *   what = 0 : result.basis elements [first, first+count) (d*d complex each)
+ *   what = 1 : result.orthonormal_basis elements (orthonormalization methods)
+ *   what = 2 : result.gram's Gram matrix A, n x n (matrix inversion; first and
+ *              count ignored)
+ *   what = 3 : its maintained inverse, n x n
+ * copies them into `out` (host). A caller can size its buffers from the result
+ * instead of the worst case d^2 (R:src/closure.cpp:368-370 uses d^2 only as a cap).
+ */
+int liecl_b200_dense_fetch(liecl_b200_ctx* ctx, int32_t what, int64_t first, int64_t count, double* out);
+
+/*
+ * GramState (R:include/liecl/closure.hpp:28-55; R:src/closure.cpp:44-105) and
+ * check_matrix_inversion (R:include/liecl/closure.hpp:132-134,
+ * R:src/closure.cpp:107-140) on the device, for callers that keep their own
+ * Gram state. Matrices are n x n column-major complex (Eigen::MatrixXcd
+ * storage), vectors n complex; host buffers.
+ *   schur_complement : s = Re(1 - beta^H A^{-1} beta); n = 0 gives 1
+ *   expand           : bordered A and A^{-1} ((n+1) x (n+1) outputs);
+ *                      LIECL_B200_DEGENERACY with the reference's message when
+ *                      s <= conditioning_floor
+ *   refresh          : A^{-1} from A (Cholesky; LU when A is not positive definite)
+ *   inverse_error    : max |(A A^{-1} - I)_ij|
+ *   check_matrix_inversion_dense : beta_l = <B_l, h>, x = A^{-1} beta,
+ *                      independent = ||h - sum_l x_l B_l|| > tol (basis: n dense
+ *                      operators; n = 0: ||h|| > tol)
+ */
+int liecl_b200_gram_schur_complement(liecl_b200_ctx* ctx, const double* inverse, int64_t n, const double* beta,
+                                     double* s_out);
+int liecl_b200_gram_expand(liecl_b200_ctx* ctx, const double* gram, const double* inverse, int64_t n,
+                           const double* beta, double conditioning_floor, double* gram_out, double* inverse_out);
+int liecl_b200_gram_refresh(liecl_b200_ctx* ctx, const double* gram, int64_t n, double* inverse_out);
+int liecl_b200_gram_inverse_error(liecl_b200_ctx* ctx, const double* gram, const double* inverse, int64_t n,
+                                  double* err_out);
+int liecl_b200_check_matrix_inversion_dense(liecl_b200_ctx* ctx, const double* basis, int64_t n,
+                                            const double* inverse, const double* h, int32_t d, double tol,
+                                            int32_t* independent, double* beta_out, double* residual_norm);
 
 #ifdef __cplusplus
 }

@@ -198,6 +198,87 @@ class Ref:
             C.byref(done), C.byref(nulls), C.byref(ind), C.byref(secs)))
         return {"pairs": done.value, "nulls": nulls.value, "independent": ind.value, "seconds": secs.value}
 
+    # -- Alg. 2 pieces (ref_harness.cpp) ---------------------------------------
+    def last_gram(self, n):
+        """result.gram (A, A^-1) of the last closure_* call (matrix inversion)."""
+        A = np.zeros(max(n * n, 1), np.complex128)
+        Ai = np.zeros(max(n * n, 1), np.complex128)
+        self._check(self.lib.liecl_ref_last_gram(C.c_int64(n), _p(A.view(np.float64)), _p(Ai.view(np.float64))))
+        return A[: n * n].reshape(n, n, order="F"), Ai[: n * n].reshape(n, n, order="F")
+
+    def gram_state_dense(self, basis, d, floor=1e-12):
+        """GramState built by expand over the dense tuple: (schur before each
+        expand, A, A^-1, refreshed A^-1, inverse_error before the refresh)."""
+        basis = _c128(basis)
+        n = len(basis)
+        schur = np.zeros(max(n, 1))
+        A = np.zeros(max(n * n, 1), np.complex128)
+        Ai = np.zeros(max(n * n, 1), np.complex128)
+        Ar = np.zeros(max(n * n, 1), np.complex128)
+        err = C.c_double()
+        self._check(self.lib.liecl_ref_gram_state_dense(
+            _p(basis.view(np.float64)), C.c_int64(n), C.c_int(d), C.c_double(floor), _p(schur),
+            _p(A.view(np.float64)), _p(Ai.view(np.float64)), _p(Ar.view(np.float64)), C.byref(err)))
+        f = lambda m: m[: n * n].reshape(n, n, order="F")
+        return schur[:n], f(A), f(Ai), f(Ar), err.value
+
+    def check_matrix_inversion_dense(self, basis, d, h, tol=1e-10, floor=1e-12):
+        basis = _c128(basis)
+        n = len(basis)
+        ind = C.c_int()
+        beta = np.zeros(max(n, 1), np.complex128)
+        self._check(self.lib.liecl_ref_check_matrix_inversion_dense(
+            _p(basis.view(np.float64)), C.c_int64(n), C.c_int(d), _p(_c128(h).view(np.float64)), C.c_double(tol),
+            C.c_double(floor), C.byref(ind), _p(beta.view(np.float64))))
+        return bool(ind.value), beta[:n]
+
+    def check_matrix_inversion_pauli(self, offsets, x, z, coef, n, qubits, tol=1e-10, floor=1e-12):
+        """Tuple = sums 0..n-1, h = sum n: (independent, beta, A, A^-1)."""
+        ind = C.c_int()
+        beta = np.zeros(max(n, 1), np.complex128)
+        A = np.zeros(max(n * n, 1), np.complex128)
+        Ai = np.zeros(max(n * n, 1), np.complex128)
+        self._check(self.lib.liecl_ref_check_matrix_inversion_pauli(
+            _p(np.ascontiguousarray(offsets, np.int64), I64P), _p(np.ascontiguousarray(x, np.uint64), U64P),
+            _p(np.ascontiguousarray(z, np.uint64), U64P), _p(np.ascontiguousarray(coef, np.float64)), C.c_int64(n),
+            C.c_uint(qubits), C.c_double(tol), C.c_double(floor), _p(A.view(np.float64)), _p(Ai.view(np.float64)),
+            C.byref(ind), _p(beta.view(np.float64))))
+        f = lambda m: m[: n * n].reshape(n, n, order="F")
+        return bool(ind.value), beta[:n], f(A), f(Ai)
+
+    def project_residual_pauli(self, offsets, x, z, coef, n, qubits, term_cap=1 << 16):
+        """Tuple = sums 0..n-1, h = sum n: ((x, z, coef) of the residual, coeffs)."""
+        oo = np.zeros(2, np.int64)
+        ox = np.zeros(term_cap, np.uint64)
+        oz = np.zeros(term_cap, np.uint64)
+        oc = np.zeros((term_cap, 2))
+        coeffs = np.zeros(max(n, 1), np.complex128)
+        self._check(self.lib.liecl_ref_project_residual_pauli(
+            _p(np.ascontiguousarray(offsets, np.int64), I64P), _p(np.ascontiguousarray(x, np.uint64), U64P),
+            _p(np.ascontiguousarray(z, np.uint64), U64P), _p(np.ascontiguousarray(coef, np.float64)), C.c_int64(n),
+            C.c_uint(qubits), _p(oo, I64P), _p(ox, U64P), _p(oz, U64P), _p(oc), C.c_int64(term_cap),
+            _p(coeffs.view(np.float64))))
+        t = int(oo[1])
+        return (ox[:t].copy(), oz[:t].copy(), oc[:t].copy()), coeffs[:n]
+
+    def bracket_window_log_dense(self, basis, d, row_begin, row_end, tol=1e-10, max_pairs=0, threads=1):
+        """Per-pair (null, independent, residual_norm) of a window of rows
+        against the fixed basis (the saturated phase; ref_harness.cpp)."""
+        basis = _c128(basis)
+        total = sum(min(l, len(basis)) for l in range(row_begin, min(row_end, len(basis))))
+        if max_pairs > 0:
+            total = min(total, max_pairs)
+        nul = np.zeros(max(total, 1), np.int32)
+        ind = np.zeros(max(total, 1), np.int32)
+        rn = np.zeros(max(total, 1))
+        done = C.c_int64()
+        self._check(self.lib.liecl_ref_bracket_window_log_dense(
+            _p(basis.view(np.float64)), C.c_int64(len(basis)), C.c_int(d), C.c_double(tol),
+            C.c_int64(row_begin), C.c_int64(row_end), C.c_int64(max_pairs), C.c_uint(threads),
+            _p(nul, I32P), _p(ind, I32P), _p(rn), C.byref(done)))
+        k = done.value
+        return nul[:k], ind[:k], rn[:k]
+
     def check_sequence_dense(self, basis, cands, d, tol=1e-10, append=True, threads=1):
         basis = _c128(basis)
         cands = _c128(cands)

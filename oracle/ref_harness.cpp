@@ -135,6 +135,7 @@ std::int64_t pauli_out(const OperatorTuple& ops, std::int64_t* offsets, std::uin
 }
 
 double g_rank_tolerance = 0.0;  // ClosureConfig::rank_tolerance for the next calls (test knob)
+thread_local std::optional<liecl::GramState> g_last_gram;  // result.gram of the last closure
 
 liecl::ClosureConfig make_config(double tol, unsigned threads, std::uint64_t max_dim) {
   liecl::ClosureConfig cfg;
@@ -196,6 +197,7 @@ int liecl_ref_closure_dense(const double* gens, int ngens, int d, int method, do
     const OperatorTuple g = dense_tuple(gens, ngens, d);
     const auto res = liecl::run_closure(g, static_cast<liecl::Method>(method),
                                         make_config(tol, threads, max_dim));
+    g_last_gram = res.gram;
     stats->commutators_evaluated = res.stats.commutators_evaluated;
     stats->independence_checks = res.stats.independence_checks;
     stats->accepted = res.stats.accepted;
@@ -227,6 +229,7 @@ int liecl_ref_closure_pauli(const std::int64_t* offsets, const std::uint64_t* x,
     const OperatorTuple g = pauli_tuple(offsets, x, z, coef, ngens, qubits);
     const auto res = liecl::run_closure(g, static_cast<liecl::Method>(method),
                                         make_config(tol, threads, max_dim));
+    g_last_gram = res.gram;
     stats->commutators_evaluated = res.stats.commutators_evaluated;
     stats->independence_checks = res.stats.independence_checks;
     stats->accepted = res.stats.accepted;
@@ -426,6 +429,43 @@ int liecl_ref_bracket_window_dense(const double* basis, std::int64_t n, int d, d
   });
 }
 
+/// Per-pair verdicts of a window of cursor rows against a fixed basis (the
+/// saturated phase of run_engine, R:src/closure.cpp:412-460, where nothing is
+/// accepted so every row's speculation is final): for each pair (l, m) in
+/// order, null flag (||[B_l, B_m]|| <= tol, :419-420), verdict and CGS2
+/// residual norm (OrthonormStrategy::check, :276-286). Arrays hold
+/// min(max_pairs, window) entries.
+int liecl_ref_bracket_window_log_dense(const double* basis, std::int64_t n, int d, double tol,
+                                       std::int64_t row_begin, std::int64_t row_end, std::int64_t max_pairs,
+                                       unsigned threads, std::int32_t* null_out, std::int32_t* indep_out,
+                                       double* rn_out, std::int64_t* pairs_done) {
+  return guarded([&] {
+    const OperatorTuple v = dense_tuple(basis, n, d);
+    std::int64_t done = 0;
+    for (std::int64_t l = row_begin; l < row_end && l < n; ++l) {
+      std::int64_t cnt = l;
+      if (max_pairs > 0) cnt = std::min<std::int64_t>(cnt, max_pairs - done);
+      if (cnt <= 0) break;
+      const std::int64_t base = done;
+      liecl::detail::parallel_for(static_cast<std::size_t>(cnt), threads ? threads : 1, [&](std::size_t m) {
+        const Operator h = liecl::commutator(v[static_cast<std::size_t>(l)], v[m]);
+        const double hn = liecl::norm(h);
+        const std::int64_t k = base + static_cast<std::int64_t>(m);
+        null_out[k] = hn > tol ? 0 : 1;
+        indep_out[k] = 0;
+        rn_out[k] = 0.0;
+        if (hn > tol) {
+          const Outcome o = ortho_check(v, Complex{1.0 / hn, 0.0} * h, tol);
+          indep_out[k] = o.independent;
+          rn_out[k] = o.residual_norm;
+        }
+      });
+      done += cnt;
+    }
+    *pairs_done = done;
+  });
+}
+
 /// Ordered independence check of unit-normalised candidates against an
 /// orthonormal basis (config 3): each candidate is normalised as run_engine
 /// does (R:src/closure.cpp:388), checked with project_residual
@@ -567,6 +607,104 @@ int liecl_ref_linear_combination_pauli(const std::int64_t* offsets, const std::u
     *out_null = r.is_null() ? 1 : 0;
     if (pauli_out(OperatorTuple{r}, out_offsets, out_x, out_z, out_coef, term_cap) < 0)
       throw liecl::CapacityError("harness: term output capacity too small");
+  });
+}
+
+// ---- Alg. 2 pieces: GramState, check_matrix_inversion (R:src/closure.cpp:44-140)
+
+namespace {
+// a GramState built like close_matrix_inversion builds it: element k expands
+// with beta_l = <B_l, B_k> (l < k)
+liecl::GramState gram_of(const OperatorTuple& b, double floor) {
+  liecl::GramState st;
+  for (std::size_t k = 0; k < b.size(); ++k) {
+    Eigen::VectorXcd beta(static_cast<Eigen::Index>(k));
+    for (std::size_t l = 0; l < k; ++l) beta(static_cast<Eigen::Index>(l)) = liecl::inner_product(b[l], b[k]);
+    st.expand(beta, floor);
+  }
+  return st;
+}
+void mat_out(const Eigen::MatrixXcd& m, double* out) {
+  std::memcpy(out, m.data(), sizeof(double) * 2 * static_cast<std::size_t>(m.size()));
+}
+} // namespace
+
+/// GramState through its public API: built from the dense tuple B (n
+/// operators) by successive expand calls (schur_complement recorded before
+/// each), then A, A^{-1}, refresh()'s inverse and inverse_error().
+int liecl_ref_gram_state_dense(const double* basis, std::int64_t n, int d, double floor, double* schur_out,
+                               double* gram_out, double* inverse_out, double* refreshed_out, double* err_out) {
+  return guarded([&] {
+    const OperatorTuple b = dense_tuple(basis, n, d);
+    liecl::GramState st;
+    for (std::int64_t k = 0; k < n; ++k) {
+      Eigen::VectorXcd beta(static_cast<Eigen::Index>(k));
+      for (std::int64_t l = 0; l < k; ++l)
+        beta(static_cast<Eigen::Index>(l)) =
+            liecl::inner_product(b[static_cast<std::size_t>(l)], b[static_cast<std::size_t>(k)]);
+      schur_out[k] = st.schur_complement(beta);
+      st.expand(beta, floor);
+    }
+    mat_out(st.gram(), gram_out);
+    mat_out(st.inverse(), inverse_out);
+    *err_out = st.inverse_error();
+    st.refresh();
+    mat_out(st.inverse(), refreshed_out);
+  });
+}
+
+/// check_matrix_inversion(state built from B, B, h, tol), dense or Pauli tuple
+int liecl_ref_check_matrix_inversion_dense(const double* basis, std::int64_t n, int d, const double* h, double tol,
+                                           double floor, int* independent, double* beta_out) {
+  return guarded([&] {
+    const OperatorTuple b = dense_tuple(basis, n, d);
+    const liecl::GramState st = gram_of(b, floor);
+    auto [ind, beta] = liecl::check_matrix_inversion(st, b, dense_from(h, d), tol);
+    *independent = ind ? 1 : 0;
+    std::memcpy(beta_out, beta.data(), sizeof(double) * 2 * beta.size());
+  });
+}
+
+int liecl_ref_check_matrix_inversion_pauli(const std::int64_t* offsets, const std::uint64_t* x,
+                                           const std::uint64_t* z, const double* coef, std::int64_t n,
+                                           unsigned qubits, double tol, double floor, double* gram_out,
+                                           double* inverse_out, int* independent, double* beta_out) {
+  return guarded([&] {
+    const OperatorTuple all = pauli_tuple(offsets, x, z, coef, static_cast<int>(n + 1), qubits);  // B..., h
+    const OperatorTuple b(all.begin(), all.begin() + n);
+    const liecl::GramState st = gram_of(b, floor);
+    mat_out(st.gram(), gram_out);
+    mat_out(st.inverse(), inverse_out);
+    auto [ind, beta] = liecl::check_matrix_inversion(st, b, all[static_cast<std::size_t>(n)], tol);
+    *independent = ind ? 1 : 0;
+    std::memcpy(beta_out, beta.data(), sizeof(double) * 2 * beta.size());
+  });
+}
+
+/// project_residual over Pauli sums: tuple = sums 0..n-1, h = sum n
+int liecl_ref_project_residual_pauli(const std::int64_t* offsets, const std::uint64_t* x, const std::uint64_t* z,
+                                     const double* coef, std::int64_t n, unsigned qubits, std::int64_t* out_offsets,
+                                     std::uint64_t* out_x, std::uint64_t* out_z, double* out_coef,
+                                     std::int64_t term_cap, double* coeffs_out) {
+  return guarded([&] {
+    const OperatorTuple all = pauli_tuple(offsets, x, z, coef, static_cast<int>(n + 1), qubits);
+    const OperatorTuple v(all.begin(), all.begin() + n);
+    auto [r, coeffs] = liecl::project_residual(v, all[static_cast<std::size_t>(n)]);
+    for (std::size_t l = 0; l < coeffs.size(); ++l) {
+      coeffs_out[2 * l] = coeffs[l].real();
+      coeffs_out[2 * l + 1] = coeffs[l].imag();
+    }
+    if (pauli_out(OperatorTuple{r}, out_offsets, out_x, out_z, out_coef, term_cap) < 0)
+      throw liecl::CapacityError("harness: term output capacity too small");
+  });
+}
+
+/// result.gram of the last closure run through liecl_ref_closure_* on this thread
+int liecl_ref_last_gram(std::int64_t n, double* gram_out, double* inverse_out) {
+  return guarded([&] {
+    if (!g_last_gram || g_last_gram->size() != n) throw liecl::InvalidInputError("harness: no Gram state of that size");
+    mat_out(g_last_gram->gram(), gram_out);
+    mat_out(g_last_gram->inverse(), inverse_out);
   });
 }
 

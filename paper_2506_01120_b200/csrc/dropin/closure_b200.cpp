@@ -8,12 +8,15 @@
 //
 //   run_closure                (R:include/liecl/closure.hpp:125-126) -> GPU for
 //   close_orthonormalization   (:119-121)  orthonorm / orthonorm-dimonly
-//   close_matrix_inversion     (:112-113)  matrix-inversion (dense), with result.gram
-//   project_residual           (:139-140)  -> GPU (dense operators)
+//   close_matrix_inversion     (:112-113)  matrix-inversion, with result.gram
+//                                          (dense, Pauli strings, multi-term sums)
+//   project_residual           (:139-140)  -> GPU (dense operators and Pauli sums)
+//   check_matrix_inversion     (:132-134)  -> GPU (dense and Pauli)
+//   GramState methods          (:28-55)    -> GPU (liecl_b200_gram_*)
 //   to_string / method_from_string (:22-23), basis_listing (:143)
-//   GramState methods, check_matrix_inversion -- host utilities on the
-//       caller's own state (the closure builds its state on the GPU)
 //   close_standard             (:108-109)  rank method (Alg. 1) -> GPU (dense)
+// No closure arithmetic runs here: results are marshalled into the reference's
+// types (PauliSum::from_terms / DenseOperator) and nothing else.
 //
 // Status codes of the C-ABI map back onto the reference's exception types
 // (R:include/liecl/errors.hpp:10-61).
@@ -124,38 +127,53 @@ void fill_stats(ClosureResult& r, const liecl_b200_stats& st, const std::vector<
   r.stats.warnings = parse_warnings(wbuf);
 }
 
-ClosureResult close_dense(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
-  Eigen::Index d = 0;
-  for (const Operator& g : generators)
-    if (!g.is_null()) d = g.dim();
-  const size_t D = static_cast<size_t>(d) * d;
+// n result vectors (what 0: result.basis, 1: result.orthonormal_basis) from
+// the device-resident result straight into DenseOperators, through a bounded
+// staging block: no host buffer is sized by the d^2 cap (R:src/closure.cpp:368-370
+// uses d^2 only as a cap)
+OperatorTuple fetch_dense(int32_t what, size_t n, Eigen::Index d) {
+  OperatorTuple t;
+  t.reserve(n);
+  const size_t D = static_cast<size_t>(d) * static_cast<size_t>(d);
+  const size_t block = std::max<size_t>(1, (size_t{32} << 20) / (16 * D));  // ~32 MB per copy
+  std::vector<double> stage(2 * D * std::min(block, std::max<size_t>(n, 1)));
+  for (size_t k0 = 0; k0 < n; k0 += block) {
+    const size_t cnt = std::min(block, n - k0);
+    check(liecl_b200_dense_fetch(context(), what, static_cast<int64_t>(k0), static_cast<int64_t>(cnt), stage.data()));
+    for (size_t k = 0; k < cnt; ++k) {
+      Eigen::MatrixXcd m(d, d);
+      std::memcpy(static_cast<void*>(m.data()), stage.data() + 2 * D * k, sizeof(double) * 2 * D);
+      t.emplace_back(DenseOperator(std::move(m)));
+    }
+  }
+  return t;
+}
+
+std::vector<double> dense_generators(std::span<const Operator> generators, Eigen::Index d) {
+  const size_t D = static_cast<size_t>(d) * static_cast<size_t>(d);
   std::vector<double> gens(2 * D * generators.size(), 0.0);
   for (size_t i = 0; i < generators.size(); ++i)
     if (!generators[i].is_null())
       std::memcpy(gens.data() + 2 * D * i, generators[i].dense().matrix().data(), sizeof(double) * 2 * D);
-  const size_t cap = config.max_dim ? config.max_dim : D;
-  std::vector<double> basis(2 * D * cap), ortho(keep ? 2 * D * cap : 0);
+  return gens;
+}
+
+ClosureResult close_dense(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
+  Eigen::Index d = 0;
+  for (const Operator& g : generators)
+    if (!g.is_null()) d = g.dim();
+  const std::vector<double> gens = dense_generators(generators, d);
   liecl_b200_stats st{};
   std::vector<char> wbuf(1 << 20);
   const liecl_b200_config cfg = to_native(config);
   check(liecl_b200_closure_dense(context(), gens.data(), static_cast<int32_t>(generators.size()),
                                  static_cast<int32_t>(d), keep ? LIECL_B200_METHOD_ORTHONORM
                                                                : LIECL_B200_METHOD_ORTHONORM_DIMONLY,
-                                 &cfg, basis.data(), keep ? ortho.data() : nullptr, static_cast<int64_t>(cap), &st,
-                                 wbuf.data(), static_cast<int64_t>(wbuf.size()), nullptr, 0, nullptr));
-  auto unpack = [&](const std::vector<double>& src) {
-    OperatorTuple t;
-    t.reserve(st.dimension);
-    for (size_t k = 0; k < st.dimension; ++k) {
-      Eigen::MatrixXcd m(d, d);
-      std::memcpy(static_cast<void*>(m.data()), src.data() + 2 * D * k, sizeof(double) * 2 * D);
-      t.emplace_back(DenseOperator(std::move(m)));
-    }
-    return t;
-  };
+                                 &cfg, nullptr, nullptr, 0, &st, wbuf.data(), static_cast<int64_t>(wbuf.size()),
+                                 nullptr, 0, nullptr));
   ClosureResult r;
-  r.basis = unpack(basis);
-  r.orthonormal_basis = keep ? unpack(ortho) : r.basis;
+  r.basis = fetch_dense(0, st.dimension, d);
+  r.orthonormal_basis = keep ? fetch_dense(1, st.dimension, d) : r.basis;
   r.dimension = st.dimension;
   r.method = keep ? Method::orthonorm : Method::orthonorm_dimonly;
   r.backend = Backend::dense;
@@ -164,8 +182,19 @@ ClosureResult close_dense(std::span<const Operator> generators, const ClosureCon
   return r;
 }
 
-// general (multi-term) sums: liecl_b200_closure_pauli_sums, bit-exact
-ClosureResult close_pauli_sums(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
+// a device-built Gram state is installed through GramState::refresh() (a
+// member, so it may set the private matrices) while it is staged here
+thread_local const Eigen::MatrixXcd* g_pending_gram = nullptr;
+thread_local const Eigen::MatrixXcd* g_pending_inverse = nullptr;
+double* dp(Eigen::MatrixXcd& m) { return reinterpret_cast<double*>(m.data()); }
+const double* dp(const Eigen::MatrixXcd& m) { return reinterpret_cast<const double*>(m.data()); }
+const double* dp(const Eigen::VectorXcd& v) { return reinterpret_cast<const double*>(v.data()); }
+
+// general (multi-term) sums: liecl_b200_closure_pauli_sums (orthonormal
+// methods bit-exact; Alg. 2 with result.gram)
+ClosureResult close_pauli_sums(std::span<const Operator> generators, const ClosureConfig& config, Method method) {
+  const bool keep = method == Method::orthonorm;
+  const bool gram = method == Method::matrix_inversion;
   std::uint32_t qubits = 0;
   std::vector<std::int64_t> off(1, 0);
   std::vector<std::uint64_t> x, z;
@@ -192,9 +221,12 @@ ClosureResult close_pauli_sums(std::span<const Operator> generators, const Closu
     std::vector<double> bc(2 * tcap), ocf(2 * tcap);
     liecl_b200_stats st{};
     std::vector<char> wbuf(1 << 20);
+    const int32_t m = gram ? LIECL_B200_METHOD_MATRIX_INVERSION
+                      : keep ? LIECL_B200_METHOD_ORTHONORM
+                             : LIECL_B200_METHOD_ORTHONORM_DIMONLY;
     const int s = liecl_b200_closure_pauli_sums(
         context(), off.data(), x.data(), z.data(), c.data(), static_cast<int32_t>(generators.size()), qubits,
-        keep ? LIECL_B200_METHOD_ORTHONORM : LIECL_B200_METHOD_ORTHONORM_DIMONLY, &cfg, cap, bo.data(), bx.data(),
+        m, &cfg, cap, bo.data(), bx.data(),
         bz.data(), bc.data(), tcap, oo.data(), ox.data(), oz.data(), ocf.data(), tcap, need.data(), &st, wbuf.data(),
         static_cast<std::int64_t>(wbuf.size()), nullptr, 0, nullptr);
     if (s == LIECL_B200_CAPACITY && std::string(liecl_b200_last_error()) == "output buffers too small") {
@@ -226,19 +258,31 @@ ClosureResult close_pauli_sums(std::span<const Operator> generators, const Closu
     };
     ClosureResult r;
     r.basis = unpack(bo, bx, bz, bc);
-    r.orthonormal_basis = unpack(oo, ox, oz, ocf);
+    if (!gram) r.orthonormal_basis = unpack(oo, ox, oz, ocf);
     r.dimension = st.dimension;
-    r.method = keep ? Method::orthonorm : Method::orthonorm_dimonly;
+    r.method = method;
     r.backend = Backend::pauli;
+    if (gram) {  // the device Gram state (A, A^{-1}) as result.gram
+      const Eigen::Index n = static_cast<Eigen::Index>(st.dimension);
+      Eigen::MatrixXcd A(n, n), Ai(n, n);
+      if (n > 0) check(liecl_b200_pauli_sums_fetch_gram(context(), dp(A), dp(Ai)));
+      GramState state;
+      g_pending_gram = &A;
+      g_pending_inverse = &Ai;
+      state.refresh();
+      g_pending_gram = g_pending_inverse = nullptr;
+      r.gram = std::move(state);
+    }
     r.tolerance = config.tolerance;
     fill_stats(r, st, wbuf);
     return r;
   }
 }
 
-ClosureResult close_pauli(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
-  for (const Operator& g : generators)
-    if (!g.is_null() && g.pauli().size() > 1) return close_pauli_sums(generators, config, keep);
+// single strings (every closure element stays one string); Alg. 2 here keeps
+// an identity Gram state (see liecl_b200_closure_pauli)
+ClosureResult close_pauli_single(std::span<const Operator> generators, const ClosureConfig& config, Method method) {
+  const bool keep = method != Method::orthonorm_dimonly;
   std::uint32_t qubits = 0;
   std::vector<std::uint64_t> x, z;
   std::vector<double> c;
@@ -263,8 +307,10 @@ ClosureResult close_pauli(std::span<const Operator> generators, const ClosureCon
   liecl_b200_stats st{};
   std::vector<char> wbuf(1 << 20);
   const liecl_b200_config cfg = to_native(config);
-  check(liecl_b200_closure_pauli(context(), x.data(), z.data(), c.data(), static_cast<int32_t>(x.size()), qubits,
-                                 keep ? LIECL_B200_METHOD_ORTHONORM : LIECL_B200_METHOD_ORTHONORM_DIMONLY, &cfg,
+  const int32_t m = method == Method::matrix_inversion ? LIECL_B200_METHOD_MATRIX_INVERSION
+                    : keep                             ? LIECL_B200_METHOD_ORTHONORM
+                                                       : LIECL_B200_METHOD_ORTHONORM_DIMONLY;
+  check(liecl_b200_closure_pauli(context(), x.data(), z.data(), c.data(), static_cast<int32_t>(x.size()), qubits, m, &cfg,
                                  bx.data(), bz.data(), bc.data(), oc.data(), static_cast<int64_t>(cap), &st,
                                  wbuf.data(), static_cast<int64_t>(wbuf.size()), nullptr, 0, nullptr));
   // the engine hands back the exact coefficient bits of the reference's
@@ -280,19 +326,51 @@ ClosureResult close_pauli(std::span<const Operator> generators, const ClosureCon
   };
   ClosureResult r;
   r.basis = unpack(bc);
-  r.orthonormal_basis = unpack(oc);
+  if (method != Method::matrix_inversion) r.orthonormal_basis = unpack(oc);
   r.dimension = st.dimension;
-  r.method = keep ? Method::orthonorm : Method::orthonorm_dimonly;
+  r.method = method;
   r.backend = Backend::pauli;
   r.tolerance = config.tolerance;
   fill_stats(r, st, wbuf);
   return r;
 }
 
-[[noreturn]] void off_path(const char* what) {
-  throw InvalidInputError(std::string(what) +
-                          ": not on the B200 hot path (the B200 build serves the orthonormalization methods)");
+ClosureResult close_pauli(std::span<const Operator> generators, const ClosureConfig& config, bool keep) {
+  for (const Operator& g : generators)
+    if (!g.is_null() && g.pauli().size() > 1)
+      return close_pauli_sums(generators, config, keep ? Method::orthonorm : Method::orthonorm_dimonly);
+  return close_pauli_single(generators, config, keep ? Method::orthonorm : Method::orthonorm_dimonly);
 }
+
+// the tuple of Pauli sums as (offsets, x, z, coef) arrays (null elements: no terms)
+struct PauliTuple {
+  std::uint32_t qubits = 0;
+  std::vector<std::int64_t> off{0};
+  std::vector<std::uint64_t> x, z;
+  std::vector<double> c;
+  void add(const Operator& op) {
+    if (!op.is_null()) {
+      qubits = op.pauli().qubits();
+      for (const auto& t : op.pauli().terms()) {
+        x.push_back(t.string.x);
+        z.push_back(t.string.z);
+        c.push_back(t.coefficient.real());
+        c.push_back(t.coefficient.imag());
+      }
+    }
+    off.push_back(static_cast<std::int64_t>(x.size()));
+  }
+};
+
+// a device result sum back into a PauliSum (unique sorted terms, exact bits)
+Operator pauli_result(std::uint32_t qubits, const std::vector<std::uint64_t>& x, const std::vector<std::uint64_t>& z,
+                      const std::vector<double>& c, std::int64_t nt) {
+  std::vector<PauliSum::Term> terms;
+  terms.reserve(static_cast<size_t>(nt));
+  for (std::int64_t t = 0; t < nt; ++t) terms.push_back({PauliString{x[t], z[t], qubits}, Complex{c[2 * t], c[2 * t + 1]}});
+  return Operator(PauliSum::from_terms(qubits, terms));
+}
+
 
 } // namespace
 
@@ -315,44 +393,28 @@ Method method_from_string(const std::string& name) {
                           "' (expected standard-rank, matrix-inversion, orthonorm or orthonorm-dimonly)");
 }
 
-// ---- GramState (R:include/liecl/closure.hpp:28-55): the closure's own state
-// is built on the GPU; these host methods serve callers that use GramState
-// directly. The device result is installed through refresh() (a member, so it
-// may set the private matrices) while a pending state is staged.
-namespace {
-thread_local const Eigen::MatrixXcd* g_pending_gram = nullptr;
-thread_local const Eigen::MatrixXcd* g_pending_inverse = nullptr;
-} // namespace
+// ---- GramState (R:include/liecl/closure.hpp:28-55; R:src/closure.cpp:44-105)
+// on the device: the member functions ship the caller's n x n matrices to the
+// C-ABI's Gram operations (liecl_b200_gram_*). A device-built state
+// (close_matrix_inversion) is installed through refresh() (a member, so it may
+// set the private matrices) while a pending state is staged.
 
 double GramState::schur_complement(const Eigen::VectorXcd& beta) const {
   if (beta.size() != gram_.rows()) throw InvalidInputError("GramState: beta length does not match basis size");
-  if (beta.size() == 0) return 1.0;
-  const Eigen::VectorXcd u = inverse_ * beta;
-  return (Complex{1.0, 0.0} - beta.dot(u)).real();
+  double s = 1.0;
+  check(liecl_b200_gram_schur_complement(context(), dp(inverse_), beta.size(), dp(beta), &s));
+  return s;
 }
 
 void GramState::expand(const Eigen::VectorXcd& beta, double conditioning_floor) {
-  const double s = schur_complement(beta);
+  if (beta.size() != gram_.rows()) throw InvalidInputError("GramState: beta length does not match basis size");
   const Eigen::Index n = gram_.rows();
-  if (s <= conditioning_floor)
-    throw DegeneracyError("Gram expansion is numerically degenerate for element " + std::to_string(n) +
-                              " (Schur complement " + std::to_string(s) +
-                              "); the element should have been rejected as dependent",
-                          static_cast<std::size_t>(n));
   Eigen::MatrixXcd a(n + 1, n + 1), ai(n + 1, n + 1);
-  const Eigen::VectorXcd u = n > 0 ? Eigen::VectorXcd(inverse_ * beta) : Eigen::VectorXcd(0);
-  for (Eigen::Index k = 0; k < n; ++k) {
-    for (Eigen::Index i = 0; i < n; ++i) {
-      a(i, k) = gram_(i, k);
-      ai(i, k) = inverse_(i, k) + u(i) * std::conj(u(k)) / s;
-    }
-    a(k, n) = beta(k);
-    a(n, k) = std::conj(beta(k));
-    ai(k, n) = -u(k) / s;
-    ai(n, k) = std::conj(ai(k, n));
-  }
-  a(n, n) = 1.0;
-  ai(n, n) = n == 0 ? 1.0 : 1.0 / s;
+  const int st = liecl_b200_gram_expand(context(), dp(gram_), dp(inverse_), n, dp(beta), conditioning_floor, dp(a),
+                                        dp(ai));
+  if (st == LIECL_B200_DEGENERACY)  // the reference's message and element index (R:src/closure.cpp:58-64)
+    throw DegeneracyError(liecl_b200_last_error(), static_cast<std::size_t>(n));
+  check(st);
   gram_ = std::move(a);
   inverse_ = std::move(ai);
 }
@@ -364,12 +426,15 @@ void GramState::refresh() {
     return;
   }
   if (gram_.rows() == 0) return;
-  inverse_ = gram_.ldlt().solve(Eigen::MatrixXcd::Identity(gram_.rows(), gram_.cols()));
+  Eigen::MatrixXcd ai(gram_.rows(), gram_.cols());
+  check(liecl_b200_gram_refresh(context(), dp(gram_), gram_.rows(), dp(ai)));
+  inverse_ = std::move(ai);
 }
 
 double GramState::inverse_error() const {
-  if (gram_.rows() == 0) return 0.0;
-  return ((gram_ * inverse_) - Eigen::MatrixXcd::Identity(gram_.rows(), gram_.cols())).cwiseAbs().maxCoeff();
+  double err = 0.0;
+  check(liecl_b200_gram_inverse_error(context(), dp(gram_), dp(inverse_), gram_.rows(), &err));
+  return err;
 }
 
 // Alg. 1, the rank method (R:src/closure.cpp:500-517) on the GPU: rank of
@@ -393,25 +458,14 @@ ClosureResult close_standard(std::span<const Operator> generators, const Closure
                                   0.0});
     return r;
   }
-  const size_t D = static_cast<size_t>(d) * d;
-  std::vector<double> gens(2 * D * generators.size(), 0.0);
-  for (size_t i = 0; i < generators.size(); ++i)
-    if (!generators[i].is_null())
-      std::memcpy(gens.data() + 2 * D * i, generators[i].dense().matrix().data(), sizeof(double) * 2 * D);
-  const size_t cap = config.max_dim ? config.max_dim : D;
-  std::vector<double> basis(2 * D * cap);
+  const std::vector<double> gens = dense_generators(generators, d);
   liecl_b200_stats st{};
   std::vector<char> wbuf(1 << 20);
   const liecl_b200_config cfg = to_native(config);
   check(liecl_b200_closure_dense(context(), gens.data(), static_cast<int32_t>(generators.size()),
-                                 static_cast<int32_t>(d), LIECL_B200_METHOD_STANDARD_RANK, &cfg, basis.data(), nullptr,
-                                 static_cast<int64_t>(cap), &st, wbuf.data(), static_cast<int64_t>(wbuf.size()),
-                                 nullptr, 0, nullptr));
-  for (size_t k = 0; k < st.dimension; ++k) {
-    Eigen::MatrixXcd m(d, d);
-    std::memcpy(static_cast<void*>(m.data()), basis.data() + 2 * D * k, sizeof(double) * 2 * D);
-    r.basis.emplace_back(DenseOperator(std::move(m)));
-  }
+                                 static_cast<int32_t>(d), LIECL_B200_METHOD_STANDARD_RANK, &cfg, nullptr, nullptr, 0,
+                                 &st, wbuf.data(), static_cast<int64_t>(wbuf.size()), nullptr, 0, nullptr));
+  r.basis = fetch_dense(0, st.dimension, d);
   r.dimension = st.dimension;
   fill_stats(r, st, wbuf);
   return r;
@@ -420,8 +474,22 @@ ClosureResult close_standard(std::span<const Operator> generators, const Closure
 // Alg. 2 (R:src/closure.cpp:519-527) on the GPU for dense generators
 ClosureResult close_matrix_inversion(std::span<const Operator> generators, const ClosureConfig& config) {
   const std::optional<Backend> backend = validate(generators);
-  if (backend && *backend != Backend::dense)
-    off_path("close_matrix_inversion on Pauli generators");
+  if (backend && *backend != Backend::dense) {
+    bool single = true;
+    for (const Operator& g : generators) single = single && (g.is_null() || g.pauli().size() <= 1);
+    if (!single) return close_pauli_sums(generators, config, Method::matrix_inversion);
+    ClosureResult r = close_pauli_single(generators, config, Method::matrix_inversion);
+    // distinct strings: A = I and A^{-1} = I exactly (GramState::expand with beta = 0, s = 1)
+    const Eigen::Index n = static_cast<Eigen::Index>(r.dimension);
+    const Eigen::MatrixXcd eye = Eigen::MatrixXcd::Identity(n, n);
+    GramState state;
+    g_pending_gram = &eye;
+    g_pending_inverse = &eye;
+    state.refresh();
+    g_pending_gram = g_pending_inverse = nullptr;
+    r.gram = std::move(state);
+    return r;
+  }
   Eigen::Index d = 0;
   for (const Operator& g : generators)
     if (!g.is_null()) d = g.dim();
@@ -433,31 +501,22 @@ ClosureResult close_matrix_inversion(std::span<const Operator> generators, const
     r.gram = GramState{};
     return r;
   }
-  const size_t D = static_cast<size_t>(d) * d;
-  std::vector<double> gens(2 * D * generators.size(), 0.0);
-  for (size_t i = 0; i < generators.size(); ++i)
-    if (!generators[i].is_null())
-      std::memcpy(gens.data() + 2 * D * i, generators[i].dense().matrix().data(), sizeof(double) * 2 * D);
-  const size_t cap = config.max_dim ? config.max_dim : D;
-  std::vector<double> basis(2 * D * cap), A(2 * cap * cap), Ai(2 * cap * cap);
+  const std::vector<double> gens = dense_generators(generators, d);
   liecl_b200_stats st{};
   std::vector<char> wbuf(1 << 20);
   liecl_b200_config cfg = to_native(config);
   cfg.conditioning_floor = config.conditioning_floor;
   cfg.gram_refresh_interval = config.gram_refresh_interval;
   check(liecl_b200_closure_dense_gram(context(), gens.data(), static_cast<int32_t>(generators.size()),
-                                      static_cast<int32_t>(d), &cfg, basis.data(), static_cast<int64_t>(cap),
-                                      A.data(), Ai.data(), &st, wbuf.data(), static_cast<int64_t>(wbuf.size()),
-                                      nullptr, 0, nullptr));
+                                      static_cast<int32_t>(d), &cfg, nullptr, 0, nullptr, nullptr, &st, wbuf.data(),
+                                      static_cast<int64_t>(wbuf.size()), nullptr, 0, nullptr));
   const Eigen::Index n = static_cast<Eigen::Index>(st.dimension);
-  for (Eigen::Index k = 0; k < n; ++k) {
-    Eigen::MatrixXcd m(d, d);
-    std::memcpy(static_cast<void*>(m.data()), basis.data() + 2 * D * k, sizeof(double) * 2 * D);
-    r.basis.emplace_back(DenseOperator(std::move(m)));
-  }
+  r.basis = fetch_dense(0, st.dimension, d);
   Eigen::MatrixXcd gram(n, n), inverse(n, n);
-  std::memcpy(static_cast<void*>(gram.data()), A.data(), sizeof(double) * 2 * n * n);
-  std::memcpy(static_cast<void*>(inverse.data()), Ai.data(), sizeof(double) * 2 * n * n);
+  if (n > 0) {
+    check(liecl_b200_dense_fetch(context(), 2, 0, n, reinterpret_cast<double*>(gram.data())));
+    check(liecl_b200_dense_fetch(context(), 3, 0, n, reinterpret_cast<double*>(inverse.data())));
+  }
   GramState state;
   g_pending_gram = &gram;
   g_pending_inverse = &inverse;
@@ -469,20 +528,44 @@ ClosureResult close_matrix_inversion(std::span<const Operator> generators, const
   return r;
 }
 
-// the single Alg. 2 query (R:src/closure.cpp:135-140): the reference's own
-// operations on the caller's host-side state (no GPU batch to amortise)
+// the single Alg. 2 query (R:src/closure.cpp:107-140) on the caller's state:
+// beta GEMM, x = A^{-1} beta, residual and norm on the device
 std::pair<bool, CoefficientVector> check_matrix_inversion(const GramState& state, std::span<const Operator> basis,
                                                           const Operator& h, double tol) {
   if (static_cast<std::size_t>(state.size()) != basis.size())
     throw InvalidInputError("check_matrix_inversion: state size does not match basis size");
+  for (const Operator& b : basis)
+    if (!b.is_null() && !h.is_null() && (b.backend() != h.backend() || b.dim() != h.dim()))
+      throw InvalidInputError("inner_product: operators have mismatched backends or dimensions");
   CoefficientVector beta(basis.size());
-  for (std::size_t l = 0; l < basis.size(); ++l) beta[l] = inner_product(basis[l], h);
-  if (basis.empty()) return {norm(h) > tol, beta};
-  const Eigen::VectorXcd x =
-      state.inverse() * Eigen::VectorXcd(Eigen::Map<const Eigen::VectorXcd>(beta.data(), static_cast<Eigen::Index>(beta.size())));
-  CoefficientVector neg(beta.size());
-  for (std::size_t l = 0; l < neg.size(); ++l) neg[l] = -x(static_cast<Eigen::Index>(l));
-  return {norm(linear_combination(h, Complex{1.0, 0.0}, basis, neg)) > tol, std::move(beta)};
+  std::int32_t ind = 0;
+  const auto* inv = reinterpret_cast<const double*>(state.inverse().data());
+  if (h.is_null()) {
+    // beta = 0 and the residual is a zero operator (R:src/operator.cpp:66-70, 147-154)
+    std::fill(beta.begin(), beta.end(), Complex{0.0, 0.0});
+    return {0.0 > tol, std::move(beta)};
+  }
+  if (h.is_dense()) {
+    const Eigen::Index d = h.dim();
+    const size_t D = static_cast<size_t>(d) * static_cast<size_t>(d);
+    std::vector<double> B(2 * D * basis.size(), 0.0);
+    for (size_t l = 0; l < basis.size(); ++l)
+      if (!basis[l].is_null()) std::memcpy(B.data() + 2 * D * l, basis[l].dense().matrix().data(), sizeof(double) * 2 * D);
+    check(liecl_b200_check_matrix_inversion_dense(context(), B.data(), static_cast<int64_t>(basis.size()), inv,
+                                                  reinterpret_cast<const double*>(h.dense().matrix().data()),
+                                                  static_cast<int32_t>(d), tol, &ind,
+                                                  reinterpret_cast<double*>(beta.data()), nullptr));
+  } else {
+    PauliTuple t;
+    for (const Operator& b : basis) t.add(b);
+    PauliTuple hh;
+    hh.add(h);
+    check(liecl_b200_check_matrix_inversion_pauli(context(), t.off.data(), t.x.data(), t.z.data(), t.c.data(),
+                                                  static_cast<int64_t>(basis.size()), h.pauli().qubits(), inv,
+                                                  hh.off[1], hh.x.data(), hh.z.data(), hh.c.data(), tol, &ind,
+                                                  reinterpret_cast<double*>(beta.data()), nullptr));
+  }
+  return {ind != 0, std::move(beta)};
 }
 
 ClosureResult close_orthonormalization(std::span<const Operator> generators, const ClosureConfig& config,
@@ -519,8 +602,37 @@ ClosureResult run_closure(std::span<const Operator> generators, Method method, c
 
 std::pair<Operator, CoefficientVector> project_residual(std::span<const Operator> orthonormal, const Operator& h) {
   if (orthonormal.empty()) return {h, {}};
-  if (h.is_null() || !h.is_dense())
-    off_path("project_residual on non-dense operators");
+  for (const Operator& v : orthonormal)
+    if (!v.is_null() && !h.is_null() && (v.backend() != h.backend() || v.dim() != h.dim()))
+      throw InvalidInputError("inner_product: operators have mismatched backends or dimensions");
+  if (h.is_null()) {
+    // every coefficient is <V_l, null> = 0 and the residual is the chained sum
+    // null + 0 * V_0 + ... (R:src/operator.cpp:147-154): a zero operator of V's backend
+    CoefficientVector zeros(orthonormal.size(), Complex{0.0, 0.0});
+    for (const Operator& v : orthonormal)
+      if (!v.is_null())
+        return {v.is_dense() ? Operator(DenseOperator(Eigen::MatrixXcd::Zero(v.dim(), v.dim())))
+                             : Operator(PauliSum::from_terms(v.pauli().qubits(), {})),
+                std::move(zeros)};
+    return {h, std::move(zeros)};
+  }
+  if (h.is_pauli()) {  // PauliSum backend on the device (SumEngine passes), bit-exact
+    PauliTuple t;
+    for (const Operator& v : orthonormal) t.add(v);
+    PauliTuple hh;
+    hh.add(h);
+    const std::int64_t bound = hh.off[1] + t.off.back();  // no result has more terms
+    std::vector<std::uint64_t> rx(static_cast<size_t>(std::max<std::int64_t>(bound, 1))),
+        rz(static_cast<size_t>(std::max<std::int64_t>(bound, 1)));
+    std::vector<double> rc(2 * static_cast<size_t>(std::max<std::int64_t>(bound, 1)));
+    CoefficientVector coeffs(orthonormal.size());
+    std::int64_t nt = 0;
+    check(liecl_b200_project_residual_pauli(context(), t.off.data(), t.x.data(), t.z.data(), t.c.data(),
+                                            static_cast<int64_t>(orthonormal.size()), h.pauli().qubits(), hh.off[1],
+                                            hh.x.data(), hh.z.data(), hh.c.data(), rx.data(), rz.data(), rc.data(),
+                                            bound, &nt, reinterpret_cast<double*>(coeffs.data())));
+    return {pauli_result(h.pauli().qubits(), rx, rz, rc, nt), std::move(coeffs)};
+  }
   const Eigen::Index d = h.dim();
   const size_t D = static_cast<size_t>(d) * d;
   std::vector<double> V(2 * D * orthonormal.size(), 0.0);

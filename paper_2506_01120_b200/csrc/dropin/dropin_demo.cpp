@@ -2,6 +2,7 @@
 // of R:src/closure.cpp): builds configs 0 and 4 with the reference's own
 // Pauli/dense API and runs liecl::run_closure. Prints one JSON object; the GPU
 // test (tests/test_gpu_dropin.py) compares it with the golden fixtures.
+#include <bit>
 #include <complex>
 #include <cstdio>
 #include <cstring>
@@ -129,6 +130,77 @@ int main() {
       threw = true;
     }
     std::printf("\"capacity_error\": %s, ", threw ? "true" : "false");
+  }
+  // round 2: what the drop-in used to refuse -- Alg. 2 on Pauli generators
+  // (single strings and multi-term sums), project_residual and
+  // check_matrix_inversion on Pauli sums, GramState on the caller's state,
+  // and a d = 128 dense closure sized from the result (not the d^2 cap)
+  {
+    AnsatzSpec hea;
+    hea.family = AnsatzFamily::hea;
+    hea.qubits = 3;
+    std::vector<Operator> gens;
+    for (auto& g : build_generators(hea)) gens.emplace_back(std::move(g));
+    const ClosureResult r = close_matrix_inversion(gens, cfg);
+    std::printf("\"hea3_matrix-inversion\": ");
+    print_stats(r);
+    std::printf(", \"gram_size\": %td, \"inverse_error\": %.3g}, ", static_cast<std::ptrdiff_t>(r.gram->size()),
+                r.gram->inverse_error());
+    AnsatzSpec tf;
+    tf.family = AnsatzFamily::tfim_hva_open;
+    tf.qubits = 4;
+    std::vector<Operator> sums;
+    for (auto& g : build_generators(tf)) sums.emplace_back(std::move(g));
+    const ClosureResult rs = close_matrix_inversion(sums, cfg);
+    std::printf("\"tfim4_matrix-inversion\": ");
+    print_stats(rs);
+    std::printf(", \"gram_size\": %td, \"inverse_error\": %.3g, \"sums\": [",
+                static_cast<std::ptrdiff_t>(rs.gram->size()), rs.gram->inverse_error());
+    for (size_t k = 0; k < rs.basis.size(); ++k) {
+      std::printf("%s[", k ? "," : "");
+      const auto terms = rs.basis[k].pauli().terms();
+      for (size_t i = 0; i < terms.size(); ++i)
+        std::printf("%s[%llu,%llu,%.17g,%.17g]", i ? "," : "", static_cast<unsigned long long>(terms[i].string.x),
+                    static_cast<unsigned long long>(terms[i].string.z), terms[i].coefficient.real(),
+                    terms[i].coefficient.imag());
+      std::printf("]");
+    }
+    std::printf("]}, ");
+    // project_residual of a bracket against the first orthonormal elements of the TFIM closure
+    const ClosureResult o = close_orthonormalization(sums, cfg, false);
+    const std::vector<Operator> V(o.basis.begin(), o.basis.begin() + 6);
+    const Operator h = commutator(sums[0], o.basis[7]);
+    const auto [res, coeffs] = project_residual(V, h);
+    std::printf("\"pauli_project_residual\": {\"terms\": %zu, \"norm_bits\": \"%016llx\", \"coeff0\": [%.17g, %.17g]}, ",
+                res.pauli().size(), static_cast<unsigned long long>(std::bit_cast<std::uint64_t>(norm(res))),
+                coeffs[0].real(), coeffs[0].imag());
+    // check_matrix_inversion with the Alg. 2 state: an accepted element is dependent, a new bracket is not
+    const OperatorTuple& B = rs.basis;
+    const auto [dep, b1] = check_matrix_inversion(*rs.gram, B, B[2], 1e-10);
+    std::printf("\"pauli_check_matrix_inversion\": {\"member_independent\": %s, \"beta2\": [%.17g, %.17g]}, ",
+                dep ? "true" : "false", b1[2].real(), b1[2].imag());
+    // GramState driven by hand: expand twice, refresh
+    GramState gs;
+    gs.expand(Eigen::VectorXcd(0), 1e-12);
+    Eigen::VectorXcd beta(1);
+    beta(0) = Complex{0.5, 0.0};
+    const double s = gs.schur_complement(beta);
+    gs.expand(beta, 1e-12);
+    gs.refresh();
+    std::printf("\"gram_state\": {\"schur\": %.17g, \"inv01\": %.17g, \"err\": %.3g}, ", s,
+                gs.inverse()(0, 1).real(), gs.inverse_error());
+  }
+  {
+    // d = 128 (7 qubits): X0 and Z0 close to su(2) (dimension 3); the drop-in
+    // sizes its output from the result, not from the 16384-element cap
+    const std::uint32_t n = 7;
+    std::vector<PauliSum::Term> xs{{PauliString{1, 0, n}, I}}, zs{{PauliString{0, 1, n}, I}};
+    const std::vector<Operator> gens{Operator(from_pauli(PauliSum::from_terms(n, xs))),
+                                     Operator(from_pauli(PauliSum::from_terms(n, zs)))};
+    const ClosureResult r = run_closure(gens, Method::orthonorm, cfg);
+    std::printf("\"d128\": ");
+    print_stats(r);
+    std::printf("}, ");
   }
   // concurrent callers (the reference's entry points are reentrant): four
   // threads, each closing config 0 densely and a 6-qubit HEA as Pauli strings;

@@ -145,6 +145,9 @@ struct liecl_b200_ctx {
   DevBuf<double2> comm_scratch;  // ... and unpacked operands / result (packed field)
   std::shared_ptr<void> dense_cache, pauli_cache;  // workspaces of the last one-shot closure
   std::shared_ptr<void> sum_cache;                  // the last multi-term Pauli closure (fetch)
+  std::shared_ptr<void> gram_ops;                   // GramState / check_matrix_inversion workspaces
+  std::shared_ptr<void> result;                     // the last dense closure (liecl_b200_dense_fetch)
+  int result_kind = 0;                              // 1 DenseEngine, 2 GramEngine, 3 RankEngine
   // per-kernel-class event timing (liecl_b200_ctx_set_timing)
   bool timing = false;
   struct Timed {
@@ -937,12 +940,17 @@ void use_device(liecl_b200_ctx* ctx) { CU(cudaSetDevice(ctx->device)); }
 void run_rank_closure(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, int32_t d, const liecl_b200_config& cfg,
                       double* basis_out, int64_t cap, liecl_b200_stats* stats, char* warnings, int64_t warnings_len,
                       liecl_b200_decision* log, int64_t log_cap, int64_t* log_len) {
-  RankEngine eng(ctx, d, cfg);
+  ctx->result.reset();
+  auto holder = std::make_shared<RankEngine>(ctx, d, cfg);
+  RankEngine& eng = *holder;
   eng.run_generators(reinterpret_cast<const double2*>(gens), ngens);
   eng.run_closure_pairs();
   *stats = eng.stats();
   write_warnings(eng.warnings(), warnings, warnings_len);
   copy_log(eng.log(), log, log_cap, log_len);
+  ctx->result = holder;  // liecl_b200_dense_fetch
+  ctx->result_kind = 3;
+  if (!basis_out) return;
   if (eng.size() > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
   eng.download_basis(basis_out);
 }
@@ -952,18 +960,69 @@ void run_gram_closure(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, in
                       double* basis_out, int64_t cap, double* gram_out, double* inverse_out, liecl_b200_stats* stats,
                       char* warnings, int64_t warnings_len, liecl_b200_decision* log, int64_t log_cap,
                       int64_t* log_len) {
-  GramEngine eng(ctx, d, cfg);
+  ctx->result.reset();
+  auto holder = std::make_shared<GramEngine>(ctx, d, cfg);
+  GramEngine& eng = *holder;
   eng.run_generators(reinterpret_cast<const double2*>(gens), ngens);
   eng.run_closure_pairs();
   *stats = eng.stats();
   write_warnings(eng.warnings(), warnings, warnings_len);
   copy_log(eng.log(), log, log_cap, log_len);
+  ctx->result = holder;  // liecl_b200_dense_fetch
+  ctx->result_kind = 2;
+  if (!basis_out) return;
   if (eng.size() > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
   eng.download_basis(basis_out);
   eng.download_gram(gram_out, inverse_out);
 }
 
 #include "sum_engine.cuh"
+
+// GramState (R:src/closure.cpp:44-105) and check_matrix_inversion (:107-140)
+// on the device for callers that hold their own state (the drop-in's
+// GramState methods): n x n column-major complex matrices, host in and out.
+struct GramOps {
+  HermInverse inverse;
+  DevBuf<double2> a, ai, beta, u, basis, h, r;
+  DevBuf<double> s, partial, rn;
+};
+
+GramOps& gram_ops(liecl_b200_ctx* ctx) {
+  if (!ctx->gram_ops) ctx->gram_ops = std::make_shared<GramOps>();
+  return *std::static_pointer_cast<GramOps>(ctx->gram_ops);
+}
+
+// s = Re(1 - beta^H A^{-1} beta) (GramState::schur_complement, :44-53); u = A^{-1} beta stays in g.u
+double gram_schur(liecl_b200_ctx* ctx, GramOps& g, const double2* inverse_dev, int64_t ld, int64_t n) {
+  if (n == 0) return 1.0;
+  g.u.ensure(static_cast<size_t>(n));
+  g.s.ensure(1);
+  gemm_mc_store(ctx, inverse_dev, ld, n, n, g.beta.p, n, 1, g.u.p, n, 1.0);
+  schur_kernel<<<1, 256, 0, ctx->stream>>>(g.beta.p, g.u.p, n, g.s.p);
+  launched(ctx);
+  double s = 0.0;
+  CU(cudaMemcpyAsync(&s, g.s.p, sizeof s, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return s;
+}
+
+__global__ void eye_diff_max_kernel(const double2* __restrict__ P, int64_t n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int64_t e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int64_t i = e % n, k = e / n;
+    const double2 v = P[e];
+    m = fmax(m, hypot(v.x - (i == k ? 1.0 : 0.0), v.y));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+    *out = t;
+  }
+}
 
 } // namespace
 
@@ -1045,7 +1104,7 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
                              liecl_b200_stats* stats, char* warnings, int64_t warnings_len, liecl_b200_decision* log,
                              int64_t log_cap, int64_t* log_len) {
   return guarded([&] {
-    if (!ctx || !gens || !basis_out || !stats) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (!ctx || !gens || !stats) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     if (ngens <= 0) throw Error(LIECL_B200_INVALID_INPUT, "closure requires a non-empty generator tuple");
     use_device(ctx);
     const auto t0 = Clock::now();
@@ -1068,6 +1127,7 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
       cached->reset(cfg);
     } else {
       ctx->dense_cache.reset();
+      if (ctx->result_kind == 1) ctx->result.reset();
       cached = std::make_shared<DenseEngine>(ctx, d, keep, cfg);
       ctx->dense_cache = cached;
     }
@@ -1085,6 +1145,9 @@ int liecl_b200_closure_dense(liecl_b200_ctx* ctx, const double* gens, int32_t ng
     stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
     write_warnings(eng.warnings(), warnings, warnings_len);
     copy_log(eng.log(), log, log_cap, log_len);
+    ctx->result = cached;  // liecl_b200_dense_fetch
+    ctx->result_kind = 1;
+    if (!basis_out) return;  // the result stays on the device
     if (n > cap) throw Error(LIECL_B200_CAPACITY, "basis output buffer too small");
     eng.download(false, basis_out);
     if (ortho_out) eng.download(true, ortho_out);
@@ -1096,7 +1159,7 @@ int liecl_b200_closure_dense_gram(liecl_b200_ctx* ctx, const double* gens, int32
                                   double* inverse_out, liecl_b200_stats* stats, char* warnings, int64_t warnings_len,
                                   liecl_b200_decision* log, int64_t log_cap, int64_t* log_len) {
   return guarded([&] {
-    if (!ctx || !gens || !basis_out || !stats) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (!ctx || !gens || !stats) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     if (ngens <= 0) throw Error(LIECL_B200_INVALID_INPUT, "closure requires a non-empty generator tuple");
     use_device(ctx);
     const auto t0 = Clock::now();
@@ -1122,7 +1185,13 @@ int liecl_b200_closure_pauli(liecl_b200_ctx* ctx, const uint64_t* x, const uint6
     const auto t0 = Clock::now();
     const liecl_b200_config cfg = default_config(cfg_in);
     const uint64_t k0 = ctx->kernels;
-    const bool keep = keep_for(method);
+    // Alg. 2 on single strings (close_matrix_inversion, R:src/closure.cpp:214-265):
+    // distinct strings are orthonormal, so beta of a new string is exactly 0,
+    // every accept has Schur complement 1 and the Gram state stays the identity;
+    // a member's residual h - x_l B_l has the same zero / rounding-level norm as
+    // the orthonormal check. The basis is the accepted unit brackets = Alg. 3's
+    // commutator basis (keep_original).
+    const bool keep = method == LIECL_B200_METHOD_MATRIX_INVERSION ? true : keep_for(method);
     auto cached = std::static_pointer_cast<PauliEngine>(ctx->pauli_cache);
     if (cached && cached->compatible(qubits, keep, cfg)) {
       cached->reset(cfg);
@@ -1168,7 +1237,8 @@ int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, c
     const auto t0 = Clock::now();
     const liecl_b200_config cfg = default_config(cfg_in);
     const uint64_t k0 = ctx->kernels;
-    auto holder = std::make_shared<SumEngine>(ctx, qubits, keep_for(method), cfg);
+    const bool gram = method == LIECL_B200_METHOD_MATRIX_INVERSION;
+    auto holder = std::make_shared<SumEngine>(ctx, qubits, gram ? false : keep_for(method), cfg, gram);
     SumEngine& eng = *holder;
     eng.run(offsets, x, z, coef, ngens);
     ctx->sum_cache = holder;  // liecl_b200_pauli_sums_fetch copies from it without recomputing
@@ -1202,6 +1272,16 @@ int liecl_b200_pauli_sums_fetch(liecl_b200_ctx* ctx, int64_t cap, int64_t* basis
       throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     eng->download(false, basis_offsets, basis_x, basis_z, basis_coef);
     if (ortho_offsets) eng->download(true, ortho_offsets, ortho_x, ortho_z, ortho_coef);
+  });
+}
+
+int liecl_b200_pauli_sums_fetch_gram(liecl_b200_ctx* ctx, double* gram_out, double* inverse_out) {
+  return guarded([&] {
+    if (!ctx) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    auto eng = std::static_pointer_cast<SumEngine>(ctx->sum_cache);
+    if (!eng || !eng->is_gram()) throw Error(LIECL_B200_INVALID_INPUT, "no matrix-inversion Pauli closure on this context");
+    use_device(ctx);
+    eng->download_gram(gram_out, inverse_out);
   });
 }
 
@@ -1533,6 +1613,327 @@ int liecl_b200_session_set_shards(liecl_b200_session* s, int32_t nranks, int32_t
     if (nccl_id) red = std::make_unique<NcclReducer>(nccl_id, nranks, rank);
     else red = std::make_unique<HostReducer>(reduce, user);
     s->eng->set_shards(nranks, rank, std::move(red));
+  });
+}
+
+int liecl_b200_dense_fetch(liecl_b200_ctx* ctx, int32_t what, int64_t first, int64_t count, double* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (!ctx->result) throw Error(LIECL_B200_INVALID_INPUT, "no dense closure result to fetch on this context");
+    use_device(ctx);
+    switch (ctx->result_kind) {
+    case 1: {
+      auto& e = *std::static_pointer_cast<DenseEngine>(ctx->result);
+      if (what > 1) throw Error(LIECL_B200_INVALID_INPUT, "an orthonormalization result has no Gram state");
+      e.copy_vectors(first, count, out, false, what == 1);
+      return;
+    }
+    case 2: {
+      auto& e = *std::static_pointer_cast<GramEngine>(ctx->result);
+      if (what == 0) e.copy_basis(first, count, out);
+      else if (what == 2) e.download_gram(out, nullptr);
+      else if (what == 3) e.download_gram(nullptr, out);
+      else throw Error(LIECL_B200_INVALID_INPUT, "matrix inversion keeps no orthonormal tuple");
+      return;
+    }
+    case 3: {
+      auto& e = *std::static_pointer_cast<RankEngine>(ctx->result);
+      if (what != 0) throw Error(LIECL_B200_INVALID_INPUT, "the rank method keeps only result.basis");
+      e.copy_basis(first, count, out);
+      return;
+    }
+    default: throw Error(LIECL_B200_INTERNAL, "unknown result kind");
+    }
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// a one-shot SumEngine holding `n` tuple sums (the Pauli single queries)
+std::unique_ptr<SumEngine> pauli_tuple(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                       const uint64_t* z, const double* coef, int64_t n, uint32_t qubits) {
+  if (n < 0 || (n > 0 && !offsets)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+  if (qubits < 1 || qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..31 qubits");
+  if (n > 0 && offsets[0] != 0) throw Error(LIECL_B200_INVALID_INPUT, "offsets[0] must be 0");
+  for (int64_t l = 0; l < n; ++l)
+    if (offsets[l + 1] < offsets[l]) throw Error(LIECL_B200_INVALID_INPUT, "offsets must be non-decreasing");
+  if (n > 0 && offsets[n] > 0 && (!x || !z || !coef)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+  liecl_b200_config cfg = default_config(nullptr);
+  cfg.max_dim = static_cast<uint64_t>(std::max<int64_t>(n, 1));
+  auto e = std::make_unique<SumEngine>(ctx, qubits, false, cfg);
+  if (n > 0) e->load_basis(offsets, x, z, coef, n);
+  return e;
+}
+void check_sum_args(int64_t h_terms, const uint64_t* hx, const uint64_t* hz, const double* hcoef) {
+  if (h_terms < 0 || (h_terms > 0 && (!hx || !hz || !hcoef))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+}
+}  // namespace
+
+extern "C" {
+
+int liecl_b200_project_residual_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                      const uint64_t* z, const double* coef, int64_t n, uint32_t qubits,
+                                      int64_t h_terms, const uint64_t* hx, const uint64_t* hz, const double* hcoef,
+                                      uint64_t* rx, uint64_t* rz, double* rcoef, int64_t term_cap,
+                                      int64_t* out_terms, double* coeffs) {
+  return guarded([&] {
+    if (!ctx || !out_terms || (n > 0 && !coeffs)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    check_sum_args(h_terms, hx, hz, hcoef);
+    use_device(ctx);
+    auto e = pauli_tuple(ctx, offsets, x, z, coef, n, qubits);
+    SumEngine::Segs r;
+    e->project_one(h_terms, hx, hz, hcoef, r, coeffs);
+    *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
+    if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+  });
+}
+
+int liecl_b200_linear_combination_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                        const uint64_t* z, const double* coef, int64_t n, uint32_t qubits,
+                                        int64_t h_terms, const uint64_t* hx, const uint64_t* hz, const double* hcoef,
+                                        double base_re, double base_im, const double* coeffs, uint64_t* rx,
+                                        uint64_t* rz, double* rcoef, int64_t term_cap, int64_t* out_terms) {
+  return guarded([&] {
+    if (!ctx || !out_terms || (n > 0 && !coeffs)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    check_sum_args(h_terms, hx, hz, hcoef);
+    use_device(ctx);
+    auto e = pauli_tuple(ctx, offsets, x, z, coef, n, qubits);
+    SumEngine::Segs r;
+    e->combine_one(h_terms, hx, hz, hcoef, base_re, base_im, coeffs, false, r);
+    *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
+    if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+  });
+}
+
+int liecl_b200_overlaps_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x, const uint64_t* z,
+                              const double* coef, int64_t n, uint32_t qubits, int64_t h_terms, const uint64_t* hx,
+                              const uint64_t* hz, const double* hcoef, double* beta_out) {
+  return guarded([&] {
+    if (!ctx || (n > 0 && !beta_out)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    check_sum_args(h_terms, hx, hz, hcoef);
+    use_device(ctx);
+    auto e = pauli_tuple(ctx, offsets, x, z, coef, n, qubits);
+    e->overlaps_one(h_terms, hx, hz, hcoef, beta_out);
+  });
+}
+
+int liecl_b200_pauli_from_terms(liecl_b200_ctx* ctx, int64_t n, const uint64_t* x, const uint64_t* z,
+                                const double* coef, uint32_t qubits, uint64_t* rx, uint64_t* rz, double* rcoef,
+                                int64_t term_cap, int64_t* out_terms) {
+  return guarded([&] {
+    if (!ctx || !out_terms) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    check_sum_args(n, x, z, coef);
+    use_device(ctx);
+    auto e = pauli_tuple(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
+    SumEngine::Segs r;
+    e->from_terms_one(n, x, z, coef, r);
+    *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
+    if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+  });
+}
+
+int liecl_b200_scale_terms(liecl_b200_ctx* ctx, int64_t n, const double* coef, double re, double im, double* out) {
+  return guarded([&] {
+    if (!ctx || n < 0 || (n > 0 && (!coef || !out))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (n == 0) return;
+    use_device(ctx);
+    DevBuf<psum::C2> buf;
+    buf.ensure(static_cast<size_t>(n));
+    CU(cudaMemcpyAsync(buf.p, coef, static_cast<size_t>(n) * sizeof(psum::C2), cudaMemcpyHostToDevice, ctx->stream));
+    psum::scale_terms_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, ctx->stream>>>(
+        buf.p, n, psum::C2{re, im});
+    launched(ctx);
+    CU(cudaMemcpyAsync(out, buf.p, static_cast<size_t>(n) * sizeof(psum::C2), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int liecl_b200_norm_pauli(liecl_b200_ctx* ctx, int64_t h_terms, const uint64_t* hx, const uint64_t* hz,
+                          const double* hcoef, uint32_t qubits, double* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    check_sum_args(h_terms, hx, hz, hcoef);
+    use_device(ctx);
+    auto e = pauli_tuple(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
+    *out = e->norm_one(h_terms, hx, hz, hcoef);
+  });
+}
+
+int liecl_b200_check_matrix_inversion_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                            const uint64_t* z, const double* coef, int64_t n, uint32_t qubits,
+                                            const double* inverse, int64_t h_terms, const uint64_t* hx,
+                                            const uint64_t* hz, const double* hcoef, double tol,
+                                            int32_t* independent, double* beta_out, double* residual_norm) {
+  return guarded([&] {
+    if (!ctx || !independent || (n > 0 && (!inverse || !beta_out))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    check_sum_args(h_terms, hx, hz, hcoef);
+    use_device(ctx);
+    auto e = pauli_tuple(ctx, offsets, x, z, coef, n, qubits);
+    SumEngine::Segs r;
+    double rn = 0.0;
+    if (n == 0) {  // norm(h) (R:src/closure.cpp:121-123)
+      rn = e->norm_one(h_terms, hx, hz, hcoef);
+    } else {
+      // beta_l = <B_l, h>; x = A^{-1} beta (device GEMM); residual = h - sum_l x_l B_l
+      e->overlaps_one(h_terms, hx, hz, hcoef, beta_out);
+      GramOps& g = gram_ops(ctx);
+      g.ai.ensure(static_cast<size_t>(n * n));
+      g.beta.ensure(static_cast<size_t>(n));
+      g.u.ensure(static_cast<size_t>(n));
+      CU(cudaMemcpyAsync(g.ai.p, inverse, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      CU(cudaMemcpyAsync(g.beta.p, beta_out, static_cast<size_t>(n) * sizeof(double2), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      gemm_mc_store(ctx, g.ai.p, n, n, n, g.beta.p, n, 1, g.u.p, n, 1.0);
+      std::vector<double> xs(static_cast<size_t>(2 * n));
+      CU(cudaMemcpyAsync(xs.data(), g.u.p, static_cast<size_t>(n) * sizeof(double2), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      e->combine_one(h_terms, hx, hz, hcoef, 1.0, 0.0, xs.data(), true, r);  // coefficients -x_l
+      rn = e->norm_of(r);
+    }
+    *independent = rn > tol ? 1 : 0;
+    if (residual_norm) *residual_norm = rn;
+  });
+}
+
+int liecl_b200_gram_schur_complement(liecl_b200_ctx* ctx, const double* inverse, int64_t n, const double* beta,
+                                     double* s_out) {
+  return guarded([&] {
+    if (!ctx || !s_out || n < 0 || (n > 0 && (!inverse || !beta))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    use_device(ctx);
+    GramOps& g = gram_ops(ctx);
+    if (n == 0) {
+      *s_out = 1.0;  // R:src/closure.cpp:48-50
+      return;
+    }
+    g.ai.ensure(static_cast<size_t>(n * n));
+    g.beta.ensure(static_cast<size_t>(n));
+    CU(cudaMemcpyAsync(g.ai.p, inverse, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(g.beta.p, beta, static_cast<size_t>(n) * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    *s_out = gram_schur(ctx, g, g.ai.p, n, n);
+  });
+}
+
+int liecl_b200_gram_expand(liecl_b200_ctx* ctx, const double* gram, const double* inverse, int64_t n,
+                           const double* beta, double conditioning_floor, double* gram_out, double* inverse_out) {
+  return guarded([&] {
+    if (!ctx || !gram_out || !inverse_out || n < 0 || (n > 0 && (!gram || !inverse || !beta)))
+      throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    use_device(ctx);
+    GramOps& g = gram_ops(ctx);
+    const int64_t m = n + 1;
+    g.a.ensure(static_cast<size_t>(m * m));
+    g.ai.ensure(static_cast<size_t>(m * m));
+    g.beta.ensure(static_cast<size_t>(m));
+    g.u.ensure(static_cast<size_t>(m));
+    if (n > 0) {
+      const size_t w = static_cast<size_t>(n) * sizeof(double2), pitch = static_cast<size_t>(m) * sizeof(double2);
+      CU(cudaMemcpy2DAsync(g.a.p, pitch, gram, w, w, n, cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpy2DAsync(g.ai.p, pitch, inverse, w, w, n, cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(g.beta.p, beta, w, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    const double s = gram_schur(ctx, g, g.ai.p, m, n);  // GramState::expand (R:src/closure.cpp:55-87)
+    if (s <= conditioning_floor)
+      throw Error(LIECL_B200_DEGENERACY, "Gram expansion is numerically degenerate for element " + std::to_string(n) +
+                                             " (Schur complement " + std::to_string(s) +
+                                             "); the element should have been rejected as dependent");
+    bordered_update_kernel<<<static_cast<unsigned>(std::min<int64_t>((m * m + 255) / 256, 4096)), 256, 0,
+                             ctx->stream>>>(g.ai.p, g.a.p, m, n, g.u.p, g.beta.p, s);
+    launched(ctx);
+    CU(cudaMemcpyAsync(gram_out, g.a.p, static_cast<size_t>(m * m) * sizeof(double2), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(inverse_out, g.ai.p, static_cast<size_t>(m * m) * sizeof(double2), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int liecl_b200_gram_refresh(liecl_b200_ctx* ctx, const double* gram, int64_t n, double* inverse_out) {
+  return guarded([&] {
+    if (!ctx || n < 0 || (n > 0 && (!gram || !inverse_out))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (n == 0) return;
+    use_device(ctx);
+    GramOps& g = gram_ops(ctx);
+    g.a.ensure(static_cast<size_t>(n * n));
+    g.ai.ensure(static_cast<size_t>(n * n));
+    CU(cudaMemcpyAsync(g.a.p, gram, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    g.inverse(ctx, g.a.p, n, n, g.ai.p, n);
+    CU(cudaMemcpyAsync(inverse_out, g.ai.p, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int liecl_b200_gram_inverse_error(liecl_b200_ctx* ctx, const double* gram, const double* inverse, int64_t n,
+                                  double* err_out) {
+  return guarded([&] {
+    if (!ctx || !err_out || n < 0 || (n > 0 && (!gram || !inverse))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    *err_out = 0.0;  // R:src/closure.cpp:97-100
+    if (n == 0) return;
+    use_device(ctx);
+    GramOps& g = gram_ops(ctx);
+    g.a.ensure(static_cast<size_t>(n * n));
+    g.ai.ensure(static_cast<size_t>(n * n));
+    g.r.ensure(static_cast<size_t>(n * n));
+    g.s.ensure(1);
+    CU(cudaMemcpyAsync(g.a.p, gram, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(g.ai.p, inverse, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    gemm_mc_store(ctx, g.a.p, n, n, n, g.ai.p, n, static_cast<int>(n), g.r.p, n, 1.0);  // A A^{-1}
+    eye_diff_max_kernel<<<1, 1024, 0, ctx->stream>>>(g.r.p, n, g.s.p);
+    launched(ctx);
+    CU(cudaMemcpyAsync(err_out, g.s.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int liecl_b200_check_matrix_inversion_dense(liecl_b200_ctx* ctx, const double* basis, int64_t n,
+                                            const double* inverse, const double* h, int32_t d, double tol,
+                                            int32_t* independent, double* beta_out, double* residual_norm) {
+  return guarded([&] {
+    if (!ctx || !h || !independent || n < 0 || (n > 0 && (!basis || !inverse || !beta_out)))
+      throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (d < 1 || d > 4096) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 4096]");
+    use_device(ctx);
+    GramOps& g = gram_ops(ctx);
+    const int64_t D = static_cast<int64_t>(d) * d;
+    const double sqrt_d = std::sqrt(static_cast<double>(d));
+    g.h.ensure(static_cast<size_t>(D));
+    g.r.ensure(static_cast<size_t>(D));
+    g.rn.ensure(1);
+    CU(cudaMemcpyAsync(g.h.p, h, static_cast<size_t>(D) * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    if (n == 0) {  // matrix_inversion_residual of an empty basis: norm(h) (R:src/closure.cpp:121-123)
+      column_norm_kernel<<<1, 256, 0, ctx->stream>>>(g.h.p, D, sqrt_d, g.rn.p);
+      launched(ctx);
+    } else {
+      g.basis.ensure(static_cast<size_t>(n * D));
+      g.ai.ensure(static_cast<size_t>(n * n));
+      g.beta.ensure(static_cast<size_t>(n));
+      g.u.ensure(static_cast<size_t>(n));
+      const int64_t mtiles = (D + zg::BM - 1) / zg::BM;
+      g.partial.ensure(static_cast<size_t>(mtiles));
+      CU(cudaMemcpyAsync(g.basis.p, basis, static_cast<size_t>(n * D) * sizeof(double2), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      CU(cudaMemcpyAsync(g.ai.p, inverse, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      gemm_project(ctx, g.basis.p, n, D, g.h.p, 1, g.beta.p, 1.0 / d);  // beta_l = <B_l, h>
+      gemm_mc_store(ctx, g.ai.p, n, n, n, g.beta.p, n, 1, g.u.p, n, 1.0);  // x = A^{-1} beta
+      gemm_subtract(ctx, g.basis.p, n, D, g.u.p, g.h.p, 1, g.r.p, g.partial.p);  // h - B x, ||.||^2 partials
+      norm_finalize_kernel<<<1, 256, 0, ctx->stream>>>(g.partial.p, static_cast<int>(mtiles), 1, sqrt_d, g.rn.p);
+      launched(ctx);
+      CU(cudaMemcpyAsync(beta_out, g.beta.p, static_cast<size_t>(n) * sizeof(double2), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    }
+    double rn = 0.0;
+    CU(cudaMemcpyAsync(&rn, g.rn.p, sizeof rn, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *independent = rn > tol ? 1 : 0;
+    if (residual_norm) *residual_norm = rn;
   });
 }
 

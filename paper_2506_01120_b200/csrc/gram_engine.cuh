@@ -11,7 +11,8 @@
 // Accept (R:src/closure.cpp:238-249): Schur complement s = Re(1 - beta^H u),
 // u = A^{-1} beta (= x); degeneracy below the conditioning floor; bordered
 // inverse update (GramState::expand, :55-87); full refresh from A (Cholesky,
-// cuSOLVER) when s < 1e-4 or every `gram_refresh_interval` accepts (:89-95).
+// LU when A is not numerically positive definite; cuSOLVER) when s < 1e-4 or
+// every `gram_refresh_interval` accepts (:89-95).
 // The speculative rule of :440-444 is kept: a "dependent" verdict against the
 // batch-start state stands; an "independent" one after an in-batch accept is
 // recomputed against the current state.
@@ -65,6 +66,75 @@ __global__ void identity_kernel(double2* __restrict__ M, int64_t ld, int64_t n) 
   }
 }
 
+// GramState::refresh's inverse (R:src/closure.cpp:89-95: A.ldlt().solve(I)) on
+// the device: Cholesky (zpotrf / zpotrs) for the Hermitian positive definite
+// Gram matrix of an independent basis; a matrix that is not numerically
+// positive definite takes LU with partial pivoting (zgetrf / zgetrs) and, like
+// the reference's LDL^T, still returns an inverse instead of failing.
+// A (lda) is read only; Ainv (ldi) receives A^{-1}.
+struct HermInverse {
+  cusolverDnHandle_t solver = nullptr;
+  DevBuf<double2> tmp, work;
+  DevBuf<int> info, piv;
+  HermInverse() = default;
+  HermInverse(const HermInverse&) = delete;
+  HermInverse& operator=(const HermInverse&) = delete;
+  ~HermInverse() {
+    if (solver) cusolverDnDestroy(solver);
+  }
+  void operator()(liecl_b200_ctx* ctx, const double2* A, int64_t lda, int64_t n, double2* Ainv, int64_t ldi) {
+    if (n == 0) return;
+    if (!solver && cusolverDnCreate(&solver) != CUSOLVER_STATUS_SUCCESS) throw Error(LIECL_B200_CUDA, "cusolverDnCreate");
+    cusolverDnSetStream(solver, ctx->stream);
+    const int N = static_cast<int>(n);
+    tmp.ensure(static_cast<size_t>(n * n));
+    info.ensure(1);
+    auto* a = reinterpret_cast<cuDoubleComplex*>(tmp.p);
+    auto* b = reinterpret_cast<cuDoubleComplex*>(Ainv);
+    auto load = [&] {
+      CU(cudaMemcpy2DAsync(tmp.p, n * sizeof(double2), A, lda * sizeof(double2), n * sizeof(double2), n,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+      identity_kernel<<<static_cast<unsigned>(std::min<int64_t>((n * n + 255) / 256, 4096)), 256, 0, ctx->stream>>>(
+          Ainv, ldi, n);
+      launched(ctx);
+    };
+    auto read_info = [&] {
+      int v = 0;
+      CU(cudaMemcpyAsync(&v, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      return v;
+    };
+    load();
+    int lwork = 0;
+    if (cusolverDnZpotrf_bufferSize(solver, CUBLAS_FILL_MODE_LOWER, N, a, N, &lwork) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(LIECL_B200_CUDA, "cusolverDnZpotrf_bufferSize");
+    work.ensure(static_cast<size_t>(std::max(lwork, 1)));
+    if (cusolverDnZpotrf(solver, CUBLAS_FILL_MODE_LOWER, N, a, N, reinterpret_cast<cuDoubleComplex*>(work.p), lwork,
+                         info.p) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(LIECL_B200_CUDA, "cusolverDnZpotrf");
+    ctx->kernels += 1;
+    if (read_info() == 0) {
+      if (cusolverDnZpotrs(solver, CUBLAS_FILL_MODE_LOWER, N, N, a, N, b, static_cast<int>(ldi), info.p) !=
+          CUSOLVER_STATUS_SUCCESS)
+        throw Error(LIECL_B200_CUDA, "cusolverDnZpotrs");
+      ctx->kernels += 1;
+      return;
+    }
+    load();  // not positive definite: LU
+    if (cusolverDnZgetrf_bufferSize(solver, N, N, a, N, &lwork) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(LIECL_B200_CUDA, "cusolverDnZgetrf_bufferSize");
+    work.ensure(static_cast<size_t>(std::max(lwork, 1)));
+    piv.ensure(static_cast<size_t>(n));
+    if (cusolverDnZgetrf(solver, N, N, a, N, reinterpret_cast<cuDoubleComplex*>(work.p), piv.p, info.p) !=
+            CUSOLVER_STATUS_SUCCESS ||
+        cusolverDnZgetrs(solver, CUBLAS_OP_N, N, N, a, N, piv.p, b, static_cast<int>(ldi), info.p) !=
+            CUSOLVER_STATUS_SUCCESS)
+      throw Error(LIECL_B200_CUDA, "cuSOLVER LU refresh failed");
+    ctx->kernels += 2;
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+};
+
 class GramEngine {
 public:
   GramEngine(liecl_b200_ctx* ctx, int d, const liecl_b200_config& cfg)
@@ -87,9 +157,6 @@ public:
     partial_.ensure(static_cast<size_t>(((D_ + zg::BM - 1) / zg::BM) * bmax_));
     rn_.ensure(bmax_); hn_.ensure(bmax_); nul_.ensure(bmax_); yn_.ensure(1); s_.ensure(1);
     h_rn_.ensure(bmax_); h_hn_.ensure(bmax_); h_nul_.ensure(bmax_); h_one_.ensure(2);
-  }
-  ~GramEngine() {
-    if (solver_) cusolverDnDestroy(solver_);
   }
 
   int64_t size() const { return n_; }
@@ -149,10 +216,13 @@ public:
     }
   }
 
-  void download_basis(double* out) {
-    if (n_ == 0) return;
-    CU(cudaMemcpyAsync(out, B_.p, static_cast<size_t>(n_ * D_) * sizeof(double2), cudaMemcpyDeviceToHost,
-                       ctx_->stream));
+  void download_basis(double* out) { copy_basis(0, n_, out); }
+  // basis elements [first, first+count) -> host
+  void copy_basis(int64_t first, int64_t count, double* out) {
+    if (first < 0 || count < 0 || first + count > n_) throw Error(LIECL_B200_INVALID_INPUT, "vector range out of bounds");
+    if (count == 0) return;
+    CU(cudaMemcpyAsync(out, B_.p + first * D_, static_cast<size_t>(count * D_) * sizeof(double2),
+                       cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
   }
   // A and A^{-1} as n x n column-major (ld n)
@@ -304,39 +374,7 @@ private:
 
   // GramState::refresh (R:src/closure.cpp:89-95): A^{-1} recomputed from A
   // (Cholesky; A is Hermitian positive definite while the basis is independent)
-  void refresh() {
-    if (n_ == 0) return;
-    if (!solver_) {
-      if (cusolverDnCreate(&solver_) != CUSOLVER_STATUS_SUCCESS) throw Error(LIECL_B200_CUDA, "cusolverDnCreate");
-    }
-    cusolverDnSetStream(solver_, ctx_->stream);
-    Atmp_.ensure(static_cast<size_t>(ld() * ld()));
-    const size_t pitch = static_cast<size_t>(ld()) * sizeof(double2), w = static_cast<size_t>(n_) * sizeof(double2);
-    CU(cudaMemcpy2DAsync(Atmp_.p, pitch, A_.p, pitch, w, n_, cudaMemcpyDeviceToDevice, ctx_->stream));
-    identity_kernel<<<static_cast<unsigned>(std::min<int64_t>((n_ * n_ + 255) / 256, 4096)), 256, 0, ctx_->stream>>>(
-        Ainv_.p, ld(), n_);
-    launched(ctx_);
-    auto* a = reinterpret_cast<cuDoubleComplex*>(Atmp_.p);
-    auto* b = reinterpret_cast<cuDoubleComplex*>(Ainv_.p);
-    int lwork = 0;
-    if (cusolverDnZpotrf_bufferSize(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n_), a, static_cast<int>(ld()),
-                                    &lwork) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(LIECL_B200_CUDA, "cusolverDnZpotrf_bufferSize");
-    work_.ensure(static_cast<size_t>(std::max(lwork, 1)));
-    info_.ensure(1);
-    if (cusolverDnZpotrf(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n_), a, static_cast<int>(ld()),
-                         reinterpret_cast<cuDoubleComplex*>(work_.p), lwork, info_.p) != CUSOLVER_STATUS_SUCCESS ||
-        cusolverDnZpotrs(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n_), static_cast<int>(n_), a,
-                         static_cast<int>(ld()), b, static_cast<int>(ld()), info_.p) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(LIECL_B200_CUDA, "cuSOLVER Cholesky refresh failed");
-    int info = 0;
-    CU(cudaMemcpyAsync(&info, info_.p, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaStreamSynchronize(ctx_->stream));
-    if (info != 0)
-      throw Error(LIECL_B200_DEGENERACY, "Gram matrix is not positive definite at refresh (minor " +
-                                             std::to_string(info) + ")");
-    ctx_->kernels += 2;
-  }
+  void refresh() { inverse_(ctx_, A_.p, ld(), n_, Ainv_.p, ld()); }
 
   liecl_b200_ctx* ctx_;
   int d_;
@@ -352,11 +390,11 @@ private:
   liecl_b200_stats st_{};
   std::vector<Warning> warns_;
   std::vector<liecl_b200_decision> log_;
-  cusolverDnHandle_t solver_ = nullptr;
-  DevBuf<double2> B_, A_, Ainv_, Atmp_, C_, R_, beta_, x_, Y_, bre_, xre_, work_;
+  HermInverse inverse_;
+  DevBuf<double2> B_, A_, Ainv_, C_, R_, beta_, x_, Y_, bre_, xre_;
   int64_t vcap_ = 0;  // basis slots allocated (ld of A and A^{-1})
   DevBuf<double> partial_, rn_, hn_, yn_, s_;
-  DevBuf<int> nul_, info_;
+  DevBuf<int> nul_;
   HostBuf<double> h_rn_, h_hn_, h_one_;
   HostBuf<int> h_nul_;
 };

@@ -322,23 +322,24 @@ struct Chunk {
   int64_t src;
   C2 mult;
 };
-__global__ void chunk_base_kernel(const int* __restrict__ hoff, const int* __restrict__ broff, int nseg,
+__global__ void chunk_base_kernel(const int* __restrict__ hoff, const int* __restrict__ broff, int nseg, C2 base,
                                   Chunk* __restrict__ ch, long long* __restrict__ clen) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nseg; p += gridDim.x * blockDim.x) {
     const int k = p + broff[p];
-    ch[k] = {hoff[p + 1] - hoff[p], 0, hoff[p], {1.0, 0.0}};
+    ch[k] = {hoff[p + 1] - hoff[p], 0, hoff[p], base};
     clen[k] = ch[k].len;
   }
 }
 __global__ void chunk_basis_kernel(const unsigned long long* __restrict__ bl, const C2* __restrict__ beta,
                                    const int* __restrict__ rseg, int nruns, const int64_t* __restrict__ voff,
-                                   Chunk* __restrict__ ch, long long* __restrict__ clen) {
+                                   bool negate, Chunk* __restrict__ ch, long long* __restrict__ clen) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nruns; r += gridDim.x * blockDim.x) {
     const int k = r + rseg[r] + 1;
     const int64_t l = static_cast<int64_t>(bl[r]);
     const C2 b = beta[r];
     const bool zero = b.re == 0.0 && b.im == 0.0;
-    ch[k] = {zero ? 0 : static_cast<int>(voff[l + 1] - voff[l]), 1, voff[l], {-b.re, -b.im}};
+    ch[k] = {zero ? 0 : static_cast<int>(voff[l + 1] - voff[l]), 1, voff[l],
+             negate ? C2{-b.re, -b.im} : b};
     clen[k] = ch[k].len;
   }
 }
@@ -385,6 +386,35 @@ __global__ void append_scaled_kernel(const unsigned long long* __restrict__ key,
     okey[t] = key[t];
     oval[t] = cmul(val[t], s);
   }
+}
+
+// PauliSum::operator*(Complex) (R:src/pauli.cpp:166-177): t.coefficient * scalar
+__global__ void scale_terms_kernel(C2* __restrict__ v, int64_t n, C2 s) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    v[t] = cmul(v[t], s);
+}
+
+// Alg. 2 on sums: per-segment overlap runs (l, beta) -> dense column-major
+// n x nseg (zeroed first), and a dense n x nseg coefficient block -> runs
+// (every l of every segment; chunk_basis_kernel skips exact zeros)
+__global__ void scatter_runs_kernel(const unsigned long long* __restrict__ key, const C2* __restrict__ val,
+                                    const int* __restrict__ rseg, int nruns, int64_t ld, C2* __restrict__ out) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nruns; r += gridDim.x * blockDim.x)
+    out[static_cast<int64_t>(rseg[r]) * ld + static_cast<int64_t>(key[r])] = val[r];
+}
+__global__ void dense_runs_kernel(const C2* __restrict__ X, int n, int nseg, unsigned long long* __restrict__ key,
+                                  C2* __restrict__ val, int* __restrict__ rseg, int* __restrict__ off) {
+  const int64_t total = static_cast<int64_t>(n) * nseg;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    key[e] = static_cast<unsigned long long>(e % n);
+    val[e] = X[e];
+    rseg[e] = static_cast<int>(e / n);
+  }
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p <= nseg;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    off[p] = static_cast<int>(p * n);
 }
 
 } // namespace psum

@@ -226,10 +226,13 @@ public:
     }
   }
 
-  void download_basis(double* out) {
-    if (n_ == 0) return;
-    CU(cudaMemcpyAsync(out, B_.p, static_cast<size_t>(n_ * D_) * sizeof(double2), cudaMemcpyDeviceToHost,
-                       ctx_->stream));
+  void download_basis(double* out) { copy_basis(0, n_, out); }
+  // basis elements [first, first+count) -> host
+  void copy_basis(int64_t first, int64_t count, double* out) {
+    if (first < 0 || count < 0 || first + count > n_) throw Error(LIECL_B200_INVALID_INPUT, "vector range out of bounds");
+    if (count == 0) return;
+    CU(cudaMemcpyAsync(out, B_.p + first * D_, static_cast<size_t>(count * D_) * sizeof(double2),
+                       cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
   }
 

@@ -22,8 +22,14 @@
 
 class SumEngine {
 public:
-  SumEngine(liecl_b200_ctx* ctx, unsigned qubits, bool keep_original, const liecl_b200_config& cfg)
-      : ctx_(ctx), q_(qubits), keep_(keep_original), tol_(cfg.tolerance), record_(cfg.record_log != 0) {
+  // gram = true: Alg. 2 (matrix inversion, R:src/closure.cpp:214-265) -- the
+  // pool holds the accepted unit brackets B, a check is beta = <B_l, h>,
+  // x = A^{-1} beta (device GEMM against the maintained inverse), residual
+  // from_terms(h ++ -x_l B_l) (R:src/closure.cpp:107-131) in one pass, and an
+  // accept expands A and A^{-1} (bordered update, refresh as GramEngine)
+  SumEngine(liecl_b200_ctx* ctx, unsigned qubits, bool keep_original, const liecl_b200_config& cfg, bool gram = false)
+      : ctx_(ctx), q_(qubits), keep_(keep_original && !gram), gram_(gram), tol_(cfg.tolerance),
+        floor_(cfg.conditioning_floor), interval_(cfg.gram_refresh_interval), record_(cfg.record_log != 0) {
     if (qubits < 1 || qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..31 qubits");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
     const uint64_t full = 1ull << (2 * qubits);
@@ -140,6 +146,7 @@ public:
         log_decision(gi, -1, 0, ind ? 1 : 0, 0, rn[k]);
         if (ind) {
           accept(res, k, rn[k], sub, k);
+          if (gram_) gram_note(gi, -1, rn[k]);
           next = gi + 1;  // later generators see the new basis
           break;
         }
@@ -201,6 +208,7 @@ private:
   template <class T> static void need(DevBuf<T>& b, size_t n) {
     if (n > b.n) b.ensure(std::max(n, b.n + b.n / 2));
   }
+public:
   struct Segs {  // nseg sums on the device: terms [off[p], off[p+1])
     int nseg = 0, total = 0;
     DevBuf<int> off;
@@ -221,6 +229,8 @@ private:
       std::swap(val.p, o.val.p), std::swap(val.n, o.val.n);
     }
   };
+
+private:
   static unsigned grid(int64_t n) { return static_cast<unsigned>(std::clamp<int64_t>((n + 255) / 256, 1, 8192)); }
   static constexpr int64_t kMaxItems = int64_t(1) << 30;
 
@@ -380,12 +390,57 @@ private:
     launched(ctx_);
   }
 
+  // nseg host sums (terms [off[p], off[p+1]) relative to off[0]) -> device
+  void upload(const int64_t* off, const uint64_t* x, const uint64_t* z, const double* coef, int nseg, Segs& out) {
+    const int64_t t0 = off[0], nt = off[nseg] - off[0];
+    if (nt > kMaxItems) throw Error(LIECL_B200_CAPACITY, "sums exceed 2^30 terms");
+    const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
+    std::vector<int> ho(static_cast<size_t>(nseg) + 1);
+    for (int p = 0; p <= nseg; ++p) ho[p] = static_cast<int>(off[p] - t0);
+    std::vector<unsigned long long> hk(static_cast<size_t>(std::max<int64_t>(nt, 1)));
+    for (int p = 0; p < nseg; ++p)
+      for (int64_t t = off[p]; t < off[p + 1]; ++t) {
+        if ((x[t] & ~kmask) || (z[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
+        if (t > off[p] && pauli::pack(x[t], z[t]) <= pauli::pack(x[t - 1], z[t - 1]))
+          throw Error(LIECL_B200_INVALID_INPUT, "sum terms must be unique and sorted by (z, x)");
+        hk[t - t0] = pauli::pack(x[t], z[t]);
+      }
+    out.shape(nseg, static_cast<int>(nt));
+    CU(cudaMemcpyAsync(out.off.p, ho.data(), ho.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+    if (nt > 0) {
+      CU(cudaMemcpyAsync(out.key.p, hk.data(), nt * sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx_->stream));
+      CU(cudaMemcpyAsync(out.val.p, coef + 2 * t0, nt * sizeof(C2), cudaMemcpyHostToDevice, ctx_->stream));
+    }
+    CU(cudaStreamSynchronize(ctx_->stream));  // host staging vectors
+  }
+  // the beta runs of the last pass over ONE segment -> dense host vector (n_ complex)
+  void beta_to_host(double* beta) {
+    const int nr = beta_.total;
+    if (nr == 0) return;
+    std::vector<unsigned long long> l(static_cast<size_t>(nr));
+    std::vector<C2> v(static_cast<size_t>(nr));
+    CU(cudaMemcpyAsync(l.data(), beta_.key.p, nr * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(v.data(), beta_.val.p, nr * sizeof(C2), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    for (int r = 0; r < nr; ++r) {
+      beta[2 * l[r]] = v[r].re;
+      beta[2 * l[r] + 1] = v[r].im;
+    }
+  }
+
   // One linear_combination pass (project_residual, R:src/closure.cpp:142-162):
   // out = from_terms(in * (1,0) ++ V_l * (-beta_l)), beta_l = <V_l, in>, for
   // basis elements l < n_limit. Returns false when the batch is too large
   // (the caller splits it).
   bool pass(const Segs& in, int n_limit, Segs& out) {
     Stage st_pass(this, "pass");
+    if (!overlap_runs(in, n_limit)) return false;
+    return combine(in, C2{1.0, 0.0}, true, out);
+  }
+
+  // beta runs of every segment of `in` against V_0..V_{n_limit-1}: beta_
+  // (per segment, ascending l; run_seg_ = each run's segment). False when too large.
+  bool overlap_runs(const Segs& in, int n_limit) {
     const int n = in.total, nseg = in.nseg;
     need(cnt_, std::max(n, 1));
     need(cpos_, std::max(n, 1));
@@ -409,16 +464,25 @@ private:
     int lbits = 1;
     while ((1ll << lbits) < n_limit) ++lbits;
     merge(nseg, boff_.p, bl_.p, bv_.p, static_cast<int>(nb), false, beta_, 0, lbits);  // beta runs, ascending l
+    return true;
+  }
+
+  // out = from_terms(base * in ++ coefficient_r * V_l(r) over the runs r of
+  // beta_ (per segment, ascending l; run_seg_ = each run's segment)), with
+  // coefficient_r = -beta_r (negate: a projection pass) or beta_r as given
+  bool combine(const Segs& in, C2 base, bool negate, Segs& out) {
+    const int nseg = in.nseg;
     const int nruns = beta_.total;
     const int nch = nseg + nruns;
     need(chunks_, std::max(nch, 1));
     need(clen_, std::max(nch, 1));
     need(chpos_, std::max(nch, 1));
-    psum::chunk_base_kernel<<<grid(nseg), 256, 0, ctx_->stream>>>(in.off.p, beta_.off.p, nseg, chunks_.p, clen_.p);
+    psum::chunk_base_kernel<<<grid(nseg), 256, 0, ctx_->stream>>>(in.off.p, beta_.off.p, nseg, base, chunks_.p,
+                                                                 clen_.p);
     launched(ctx_);
     if (nruns > 0) {
       psum::chunk_basis_kernel<<<grid(nruns), 256, 0, ctx_->stream>>>(beta_.key.p, beta_.val.p, run_seg_.p, nruns,
-                                                                      dvoff_.p, chunks_.p, clen_.p);
+                                                                      dvoff_.p, negate, chunks_.p, clen_.p);
       launched(ctx_);
     }
     const long long nt = scan_counts(clen_.p, chpos_.p, nch);
@@ -499,7 +563,7 @@ private:
   void check_screened(const Segs& h, int n_limit, Segs& res, std::vector<double>& rn, std::vector<int>& index) {
     index.resize(static_cast<size_t>(h.nseg));
     for (int p = 0; p < h.nseg; ++p) index[p] = p;
-    if (record_ || n_limit == 0 || h.nseg <= kFusedMaxBatch) {
+    if (gram_ || record_ || n_limit == 0 || h.nseg <= kFusedMaxBatch) {
       check(h, n_limit, res, rn);
       return;
     }
@@ -568,6 +632,10 @@ private:
   void check(const Segs& h, int n_limit, Segs& res, std::vector<double>& rn) {
     rn.assign(static_cast<size_t>(h.nseg), 0.0);
     if (h.nseg == 0) return;
+    if (gram_) {
+      gram_check(h, n_limit, res, rn);
+      return;
+    }
     if (fused_check(h, n_limit, res, rn)) return;
     if (n_limit == 0) {  // project_residual of an empty tuple returns h itself
       copy_segs(h, res);
@@ -597,6 +665,108 @@ private:
     launched(ctx_);
     CU(cudaMemcpyAsync(rn.data(), rn_dev_.p, h.nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
+  }
+
+  // ---- Alg. 2 (gram_) ----------------------------------------------------
+  // matrix_inversion_residual (R:src/closure.cpp:107-131) for every segment of
+  // h against B_0..B_{n_limit-1}: beta and x kept in gb_ / gx_ (column p =
+  // segment p) for the accept that may follow
+  void gram_check(const Segs& h, int n_limit, Segs& res, std::vector<double>& rn) {
+    Stage st_g(this, "gram_check");
+    const int nseg = h.nseg;
+    if (n_limit == 0) {  // empty basis: residual norm = ||h|| (R:src/closure.cpp:121-123)
+      copy_segs(h, res);
+    } else {
+      const int64_t pool_terms = voff_[n_limit];
+      if (static_cast<int64_t>(nseg) * pool_terms + h.total > kMaxItems)
+        throw Error(LIECL_B200_CAPACITY, "one Alg. 2 batch exceeds 2^30 terms");
+      // beta runs (the first half of a projection pass)
+      Segs r1;
+      overlap_runs(h, n_limit);
+      const int64_t ld = n_limit;
+      gld_ = ld;
+      need(gb_, static_cast<size_t>(ld * nseg));
+      need(gx_, static_cast<size_t>(ld * nseg));
+      CU(cudaMemsetAsync(gb_.p, 0, static_cast<size_t>(ld * nseg) * sizeof(double2), ctx_->stream));
+      if (beta_.total > 0) {
+        psum::scatter_runs_kernel<<<grid(beta_.total), 256, 0, ctx_->stream>>>(
+            beta_.key.p, beta_.val.p, run_seg_.p, beta_.total, ld, reinterpret_cast<C2*>(gb_.p));
+        launched(ctx_);
+      }
+      // x = A^{-1} beta
+      gemm_mc_store(ctx_, Ainv_.p, gcap_, n_limit, n_limit, gb_.p, ld, nseg, gx_.p, ld, 1.0);
+      // runs (l, x_l) for every l, then h - sum_l x_l B_l
+      const int64_t nr = ld * nseg;
+      beta_.shape(nseg, static_cast<int>(nr));
+      need(run_seg_, static_cast<size_t>(nr));
+      psum::dense_runs_kernel<<<grid(nr), 256, 0, ctx_->stream>>>(reinterpret_cast<const C2*>(gx_.p), n_limit, nseg,
+                                                                   beta_.key.p, beta_.val.p, run_seg_.p, beta_.off.p);
+      launched(ctx_);
+      if (!combine(h, C2{1.0, 0.0}, true, res)) throw Error(LIECL_B200_CAPACITY, "one Alg. 2 batch exceeds 2^30 terms");
+    }
+    need(rn_dev_, nseg);
+    psum::seg_norm_kernel<<<grid(nseg), 256, 0, ctx_->stream>>>(res.off.p, nseg, res.val.p, rn_dev_.p);
+    launched(ctx_);
+    CU(cudaMemcpyAsync(rn.data(), rn_dev_.p, nseg * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+  }
+
+  // MatrixInversionStrategy::accept (R:src/closure.cpp:238-249) of segment hk of
+  // h, whose beta / x are column hk of gb_ / gx_ (from the gram_check that
+  // produced the verdict)
+  void gram_accept(const Segs& h, int hk) {
+    const int64_t n = n_;
+    double s = 1.0;  // schur_complement of an empty basis
+    if (n > 0) {
+      if (gld_ != n) throw Error(LIECL_B200_INTERNAL, "Alg. 2 accept without a current check");
+      need(gs_, 1);
+      schur_kernel<<<1, 256, 0, ctx_->stream>>>(gb_.p + hk * gld_, gx_.p + hk * gld_, n, gs_.p);
+      launched(ctx_);
+      CU(cudaMemcpyAsync(&s, gs_.p, sizeof s, cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+    }
+    if (s <= floor_)
+      throw Error(LIECL_B200_DEGENERACY, "Gram expansion is numerically degenerate for element " + std::to_string(n) +
+                                             " (Schur complement " + std::to_string(s) +
+                                             "); the element should have been rejected as dependent");
+    if (n + 1 > gcap_) {  // A, A^{-1} grow geometrically, re-pitched
+      const int64_t nc = std::max<int64_t>(n + 1, std::max<int64_t>(64, 2 * gcap_));
+      auto grow = [&](DevBuf<double2>& b) {
+        DevBuf<double2> nb;
+        nb.ensure(static_cast<size_t>(nc * nc));
+        if (n > 0)
+          CU(cudaMemcpy2DAsync(nb.p, nc * sizeof(double2), b.p, gcap_ * sizeof(double2), n * sizeof(double2), n,
+                               cudaMemcpyDeviceToDevice, ctx_->stream));
+        CU(cudaStreamSynchronize(ctx_->stream));
+        std::swap(b.p, nb.p);
+        std::swap(b.n, nb.n);
+      };
+      grow(A_);
+      grow(Ainv_);
+      gcap_ = nc;
+    }
+    const int64_t total = (n + 1) * (n + 1);
+    bordered_update_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 4096)), 256, 0,
+                             ctx_->stream>>>(Ainv_.p, A_.p, gcap_, n, n > 0 ? gx_.p + hk * gld_ : nullptr,
+                                             n > 0 ? gb_.p + hk * gld_ : nullptr, s);
+    launched(ctx_);
+    int h0 = 0, h1 = 0;
+    CU(cudaMemcpyAsync(&h0, h.off.p + hk, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(&h1, h.off.p + hk + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    append_pool(h.key.p + h0, h.val.p + h0, h1 - h0, 0.0);  // B gains the unit bracket itself
+    ++n_;
+    ++st_.accepted;
+    gld_ = -1;  // the kept beta / x no longer match the basis
+    if (++since_refresh_, s < 1e-4 || (interval_ > 0 && since_refresh_ >= interval_)) {
+      inverse_(ctx_, A_.p, gcap_, n_, Ainv_.p, gcap_);  // GramState::refresh (R:src/closure.cpp:89-95)
+      since_refresh_ = 0;
+    }
+  }
+  void gram_note(int64_t l, int64_t m, double rn) {  // R:src/closure.cpp:451-457
+    if (rn * rn <= 1e4 * floor_)
+      warns_.push_back({"schur_conditioning", where_str(l, m) + " accepted with near-degenerate Schur complement",
+                        rn * rn});
   }
 
   void copy_segs(const Segs& a, Segs& b) {
@@ -675,25 +845,19 @@ private:
     ix_.e_l = el_.p, ix_.e_v = ev_.p, ix_.e_next = enext_.p;
   }
 
-  // accept residual segment k (norm rn) of res; the candidate h_unit is
-  // segment hk of h (the original kept by Alg. 3)
-  void accept(const Segs& res, int k, double rn, const Segs& h, int hk) {
-    Stage st_acc(this, "accept");
-    if (n_ >= cap_)
-      throw Error(LIECL_B200_CAPACITY,
-                  "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
-    int r0 = 0, r1 = 0;
-    CU(cudaMemcpyAsync(&r0, res.off.p + k, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaMemcpyAsync(&r1, res.off.p + k + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaStreamSynchronize(ctx_->stream));
-    const int T = r1 - r0;
+  // V pool + index: append one element (device terms), scaled by 1/rn (rn = 0: as given)
+  void append_pool(const unsigned long long* key, const C2* val, int T, double rn) {
     const int64_t vt = voff_.back();
     grow_keep(vkey_, static_cast<size_t>(vt), static_cast<size_t>(vt + T));
     grow_keep(vval_, static_cast<size_t>(vt), static_cast<size_t>(vt + T));
     if (T > 0) {
-      psum::append_scaled_kernel<<<grid(T), 256, 0, ctx_->stream>>>(res.key.p + r0, res.val.p + r0, T, rn,
-                                                                    vkey_.p + vt, vval_.p + vt);
-      launched(ctx_);
+      if (rn > 0.0) {
+        psum::append_scaled_kernel<<<grid(T), 256, 0, ctx_->stream>>>(key, val, T, rn, vkey_.p + vt, vval_.p + vt);
+        launched(ctx_);
+      } else {
+        CU(cudaMemcpyAsync(vkey_.p + vt, key, T * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, ctx_->stream));
+        CU(cudaMemcpyAsync(vval_.p + vt, val, T * sizeof(C2), cudaMemcpyDeviceToDevice, ctx_->stream));
+      }
     }
     // index: keys of one element are distinct; keep the load factor <= 1/2
     keys_upper_ += static_cast<uint64_t>(T);
@@ -715,6 +879,25 @@ private:
     voff_.push_back(vt + T);
     grow_keep(dvoff_, voff_.size() - 1, voff_.size());
     CU(cudaMemcpyAsync(dvoff_.p + n_ + 1, &voff_.back(), sizeof(int64_t), cudaMemcpyHostToDevice, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));  // voff_.back() is a vector slot
+  }
+
+  // accept residual segment k (norm rn) of res; the candidate h_unit is
+  // segment hk of h (the original kept by Alg. 3)
+  void accept(const Segs& res, int k, double rn, const Segs& h, int hk) {
+    Stage st_acc(this, "accept");
+    if (n_ >= cap_)
+      throw Error(LIECL_B200_CAPACITY,
+                  "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
+    if (gram_) {
+      gram_accept(h, hk);
+      return;
+    }
+    int r0 = 0, r1 = 0;
+    CU(cudaMemcpyAsync(&r0, res.off.p + k, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(&r1, res.off.p + k + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    append_pool(res.key.p + r0, res.val.p + r0, r1 - r0, rn);
     if (keep_) {
       int h0 = 0, h1 = 0;
       CU(cudaMemcpyAsync(&h0, h.off.p + hk, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
@@ -764,6 +947,8 @@ private:
           if (ll >= n_ || n_ != row_start_n) break;  // next row: only if it exists and nothing grew
         }
         if (static_cast<int64_t>(poff.size()) > (int64_t(1) << 20)) break;
+        // Alg. 2 combines every basis element into every candidate: bound the batch's chunk terms
+        if (gram_ && static_cast<int64_t>(poff.size()) * voff_[n_] > (int64_t(1) << 28)) break;
       }
       const int cnt = static_cast<int>(poff.size()) - 1;
       // commutators -> merged sums -> norms -> units (K1, R:src/closure.cpp:419-423)
@@ -827,12 +1012,14 @@ private:
           note(pl, pm, r, ind);
           log_decision(pl, pm, 0, ind ? 1 : 0, rc, r);
           if (ind) accept(rres, 0, r, one, 0);
+          if (ind && gram_) gram_note(pl, pm, r);
           continue;
         }
         const bool ind = r > tol_;
         note(pl, pm, r, ind);
         log_decision(pl, pm, 0, ind ? 1 : 0, rc, r);
         if (ind) accept(res, res_index_[j], r, h, j);  // independent => a pass-2 survivor
+        if (ind && gram_) gram_note(pl, pm, r);
       }
       const int64_t g_next = g0 + j;
       pair_from_index(g_next, l, m);
@@ -842,8 +1029,18 @@ private:
   liecl_b200_ctx* ctx_;
   unsigned q_;
   bool keep_;
+  bool gram_;
   double tol_;
+  double floor_;
+  uint64_t interval_;
   bool record_;
+  // Alg. 2 state: A and A^{-1} (ld gcap_), the last check's dense beta / x
+  // (n_limit x nseg, ld gld_)
+  DevBuf<double2> A_, Ainv_, gb_, gx_;
+  DevBuf<double> gs_;
+  int64_t gcap_ = 0, gld_ = 0;
+  uint64_t since_refresh_ = 0;
+  HermInverse inverse_;
   int64_t cap_ = 0, budget_ = 0;
   bool has_deadline_ = false;
   Clock::time_point deadline_{};
@@ -895,4 +1092,151 @@ private:
     spill_.push_back(std::make_unique<Segs>());
     return spill_.back().get();
   }
+public:
+  // ---- single queries over Pauli sums (the drop-in's project_residual /
+  // check_matrix_inversion / linear_combination on the Pauli backend) --------
+  // The tuple is loaded into the basis pool + index with its coefficients as
+  // given; h is one sum (PauliSum form: unique terms sorted by (z, x)).
+
+  // n sums, terms [off[l], off[l+1]) of (x, z, coef re/im)
+  void load_basis(const int64_t* off, const uint64_t* x, const uint64_t* z, const double* coef, int64_t n) {
+    if (n_ != 0) throw Error(LIECL_B200_INTERNAL, "load_basis needs an empty engine");
+    if (n > cap_) throw Error(LIECL_B200_CAPACITY, "basis larger than the engine capacity");
+    Segs all;
+    upload(off, x, z, coef, static_cast<int>(n), all);
+    std::vector<int> ho(static_cast<size_t>(n) + 1);
+    for (int64_t l = 0; l <= n; ++l) ho[l] = static_cast<int>(off[l] - off[0]);
+    for (int64_t l = 0; l < n; ++l) {
+      append_pool(all.key.p + ho[l], all.val.p + ho[l], ho[l + 1] - ho[l], 0.0);
+      ++n_;  // element l of the pool (index entries carry l)
+    }
+  }
+
+  // project_residual (R:src/closure.cpp:142-162) of h against the loaded
+  // tuple: residual after two passes -> out, first-pass coefficients
+  // beta_l = <V_l, h> -> coeffs (n complex; 0 where no string is shared)
+  void project_one(const int64_t nterms, const uint64_t* x, const uint64_t* z, const double* coef, Segs& out,
+                   double* coeffs) {
+    Segs h;
+    const int64_t off[2] = {0, nterms};
+    upload(off, x, z, coef, 1, h);
+    std::fill(coeffs, coeffs + 2 * n_, 0.0);
+    if (n_ == 0) {
+      copy_segs(h, out);
+      return;
+    }
+    Segs r1;
+    if (!pass(h, static_cast<int>(n_), r1)) throw Error(LIECL_B200_CAPACITY, "one projection exceeds 2^30 terms");
+    beta_to_host(coeffs);
+    if (!pass(r1, static_cast<int>(n_), out)) throw Error(LIECL_B200_CAPACITY, "one projection exceeds 2^30 terms");
+  }
+
+  // beta_l = <V_l, h> for the loaded tuple (inner_product, R:src/operator.cpp:66-75)
+  void overlaps_one(const int64_t nterms, const uint64_t* x, const uint64_t* z, const double* coef, double* beta) {
+    Segs h, r1;
+    const int64_t off[2] = {0, nterms};
+    upload(off, x, z, coef, 1, h);
+    std::fill(beta, beta + 2 * n_, 0.0);
+    if (n_ == 0) return;
+    if (!pass(h, static_cast<int>(n_), r1)) throw Error(LIECL_B200_CAPACITY, "one projection exceeds 2^30 terms");
+    beta_to_host(beta);
+  }
+
+  // linear_combination (R:src/operator.cpp:164-181): from_terms(base_coeff * h
+  // ++ coeffs[l] * V_l for l ascending); zero coefficients add only signed
+  // zeros, which never change a slot that starts at +0, so they are skipped
+  void combine_one(const int64_t nterms, const uint64_t* x, const uint64_t* z, const double* coef, double base_re,
+                   double base_im, const double* coeffs, bool negate, Segs& out) {
+    Segs h;
+    const int64_t off[2] = {0, nterms};
+    upload(off, x, z, coef, 1, h);
+    std::vector<unsigned long long> lk;
+    std::vector<C2> lv;
+    for (int64_t l = 0; l < n_; ++l)
+      if (coeffs[2 * l] != 0.0 || coeffs[2 * l + 1] != 0.0) {
+        lk.push_back(static_cast<unsigned long long>(l));
+        lv.push_back({coeffs[2 * l], coeffs[2 * l + 1]});
+      }
+    beta_.shape(1, static_cast<int>(lk.size()));
+    const int bo[2] = {0, static_cast<int>(lk.size())};
+    CU(cudaMemcpyAsync(beta_.off.p, bo, sizeof bo, cudaMemcpyHostToDevice, ctx_->stream));
+    if (!lk.empty()) {
+      CU(cudaMemcpyAsync(beta_.key.p, lk.data(), lk.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                         ctx_->stream));
+      CU(cudaMemcpyAsync(beta_.val.p, lv.data(), lv.size() * sizeof(C2), cudaMemcpyHostToDevice, ctx_->stream));
+    }
+    need(run_seg_, std::max<size_t>(lk.size(), 1));
+    CU(cudaMemsetAsync(run_seg_.p, 0, std::max<size_t>(lk.size(), 1) * sizeof(int), ctx_->stream));
+    if (!combine(h, C2{base_re, base_im}, negate, out))
+      throw Error(LIECL_B200_CAPACITY, "linear combination exceeds 2^30 terms");
+    CU(cudaStreamSynchronize(ctx_->stream));  // host staging vectors above
+  }
+
+  // PauliSum::from_terms (R:src/pauli.cpp:78-115) of n raw terms (any order,
+  // duplicates merged in input order from +0, drop rule, sorted by (z, x))
+  void from_terms_one(int64_t n, const uint64_t* x, const uint64_t* z, const double* coef, Segs& out) {
+    if (n > kMaxItems) throw Error(LIECL_B200_CAPACITY, "terms exceed 2^30");
+    const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
+    std::vector<unsigned long long> hk(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    for (int64_t t = 0; t < n; ++t) {
+      if ((x[t] & ~kmask) || (z[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
+      hk[t] = pauli::pack(x[t], z[t]);
+    }
+    Segs raw;
+    raw.shape(1, static_cast<int>(n));
+    const int o[2] = {0, static_cast<int>(n)};
+    CU(cudaMemcpyAsync(raw.off.p, o, sizeof o, cudaMemcpyHostToDevice, ctx_->stream));
+    if (n > 0) {
+      CU(cudaMemcpyAsync(raw.key.p, hk.data(), n * sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx_->stream));
+      CU(cudaMemcpyAsync(raw.val.p, coef, n * sizeof(C2), cudaMemcpyHostToDevice, ctx_->stream));
+    }
+    merge(1, raw.off.p, raw.key.p, raw.val.p, static_cast<int>(n), true, out, static_cast<int>(q_),
+          2 * static_cast<int>(q_));
+    CU(cudaStreamSynchronize(ctx_->stream));  // host staging
+  }
+
+  bool is_gram() const { return gram_; }
+  // result.gram of an Alg. 2 closure: A and A^{-1}, n x n column-major (host)
+  void download_gram(double* a_out, double* ainv_out) {
+    if (n_ == 0) return;
+    const size_t pitch = static_cast<size_t>(gcap_) * sizeof(double2), w = static_cast<size_t>(n_) * sizeof(double2);
+    if (a_out) CU(cudaMemcpy2DAsync(a_out, w, A_.p, pitch, w, n_, cudaMemcpyDeviceToHost, ctx_->stream));
+    if (ainv_out) CU(cudaMemcpy2DAsync(ainv_out, w, Ainv_.p, pitch, w, n_, cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+  }
+
+  // ||h|| of one host sum (norm, R:src/operator.cpp:77-82 -> sum_norm)
+  double norm_one(const int64_t nterms, const uint64_t* x, const uint64_t* z, const double* coef) {
+    Segs h;
+    const int64_t off[2] = {0, nterms};
+    upload(off, x, z, coef, 1, h);
+    return norm_of(h);
+  }
+
+  // ||sum|| of segment 0 (sum_norm, R:src/pauli.cpp:202-228)
+  double norm_of(const Segs& a) {
+    need(rn_dev_, 1);
+    psum::seg_norm_kernel<<<1, 1, 0, ctx_->stream>>>(a.off.p, 1, a.val.p, rn_dev_.p);
+    launched(ctx_);
+    double v = 0.0;
+    CU(cudaMemcpyAsync(&v, rn_dev_.p, sizeof v, cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    return v;
+  }
+  // segment 0 of `a` -> host (x, z, coef); returns the term count (writes
+  // nothing when it exceeds cap)
+  int64_t download_one(const Segs& a, uint64_t* x, uint64_t* z, double* coef, int64_t cap) {
+    const int64_t nt = a.total;
+    if (nt > cap || nt == 0) return nt;
+    std::vector<unsigned long long> k(static_cast<size_t>(nt));
+    CU(cudaMemcpyAsync(k.data(), a.key.p, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(coef, a.val.p, nt * sizeof(C2), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    for (int64_t t = 0; t < nt; ++t) {
+      x[t] = k[t] & 0xffffffffull;
+      z[t] = k[t] >> 32;
+    }
+    return nt;
+  }
+
 };

@@ -265,11 +265,9 @@ def closure_dense_arrays(gens: np.ndarray, d: int, method: Method = Method.ortho
     gens = np.ascontiguousarray(gens, dtype=np.complex128)
     lib = native.load()
     cap = int(config.max_dim or d * d)
-    basis = np.zeros((cap, d * d), np.complex128)
     if method == Method.matrix_inversion:
-        return _closure_dense_gram(gens, d, config, device, cap, basis)
+        return _closure_dense_gram(gens, d, config, device, cap)
     keep = method == Method.orthonorm
-    ortho = np.zeros((cap, d * d), np.complex128) if keep else None
     st = native.Stats()
     wbuf = C.create_string_buffer(1 << 20)
     log_cap = (cap * cap // 2 + 64 + len(gens)) if config.record_log else 0
@@ -278,11 +276,13 @@ def closure_dense_arrays(gens: np.ndarray, d: int, method: Method = Method.ortho
     cfg = config.native()
     _check(lib.liecl_b200_closure_dense(
         native.context(device), _dp(gens.view(np.float64)), C.c_int32(len(gens)), C.c_int32(d),
-        C.c_int32(method.value), C.byref(cfg), _dp(basis.view(np.float64)),
-        _dp(ortho.view(np.float64)) if ortho is not None else None, C.c_int64(cap), C.byref(st), wbuf,
+        C.c_int32(method.value), C.byref(cfg), None, None, C.c_int64(0), C.byref(st), wbuf,
         C.c_int64(len(wbuf)), log.ctypes.data_as(C.c_void_p) if config.record_log else None, C.c_int64(log_cap),
         C.byref(log_len)))
     n = int(st.dimension)
+    # the result stays on the device: fetch exactly n elements (not the d^2 cap)
+    basis = _dense_fetch(device, 0, n, d)
+    ortho = _dense_fetch(device, 1, n, d) if keep else None
     warnings = _parse_warnings(wbuf.value)
     stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds, warnings,
                          {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
@@ -293,7 +293,24 @@ def closure_dense_arrays(gens: np.ndarray, d: int, method: Method = Method.ortho
                          log[: log_len.value].copy() if config.record_log else None, b, o)
 
 
-def _closure_dense_gram(gens, d, config, device, cap, basis) -> ClosureResult:
+def _dense_fetch(device: int, what: int, n: int, d: int) -> np.ndarray:
+    """liecl_b200_dense_fetch: the last dense closure's vectors (what 0 / 1, n x d*d)
+    or Gram matrices (what 2 / 3, n x n column-major)."""
+    lib = native.load()
+    if what >= 2:
+        out = np.zeros(n * n, np.complex128)
+        if n:
+            _check(lib.liecl_b200_dense_fetch(native.context(device), C.c_int32(what), C.c_int64(0), C.c_int64(n),
+                                              _dp(out.view(np.float64))))
+        return out.reshape(n, n, order="F")
+    out = np.zeros((n, d * d), np.complex128)
+    if n:
+        _check(lib.liecl_b200_dense_fetch(native.context(device), C.c_int32(what), C.c_int64(0), C.c_int64(n),
+                                          _dp(out.view(np.float64))))
+    return out
+
+
+def _closure_dense_gram(gens, d, config, device, cap) -> ClosureResult:
     """close_matrix_inversion (Alg. 2): basis = accepted unit candidates, gram = (A, A^{-1})."""
     lib = native.load()
     st = native.Stats()
@@ -301,22 +318,20 @@ def _closure_dense_gram(gens, d, config, device, cap, basis) -> ClosureResult:
     log_cap = (cap * cap // 2 + 64 + len(gens)) if config.record_log else 0
     log = np.zeros(max(log_cap, 1), DECISION_DTYPE)
     log_len = C.c_int64()
-    gram = np.zeros((cap, cap), np.complex128)
-    inv = np.zeros((cap, cap), np.complex128)
     cfg = config.native()
     _check(lib.liecl_b200_closure_dense_gram(
         native.context(device), _dp(gens.view(np.float64)), C.c_int32(len(gens)), C.c_int32(d), C.byref(cfg),
-        _dp(basis.view(np.float64)), C.c_int64(cap), _dp(gram.view(np.float64)), _dp(inv.view(np.float64)),
+        None, C.c_int64(0), None, None,
         C.byref(st), wbuf, C.c_int64(len(wbuf)), log.ctypes.data_as(C.c_void_p) if config.record_log else None,
         C.c_int64(log_cap), C.byref(log_len)))
     n = int(st.dimension)
+    basis = _dense_fetch(device, 0, n, d)
     stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds,
                          _parse_warnings(wbuf.value),
                          {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
     b = basis[:n]
-    # n x n column-major blocks written with leading dimension n
-    A = gram.ravel()[: n * n].reshape(n, n, order="F").copy()
-    Ai = inv.ravel()[: n * n].reshape(n, n, order="F").copy()
+    A = _dense_fetch(device, 2, n, d)
+    Ai = _dense_fetch(device, 3, n, d)
     res = ClosureResult([DenseOperator.from_vec(v, d) for v in b], None, n, Method.matrix_inversion, Backend.dense,
                         config.tolerance, stats, log[: log_len.value].copy() if config.record_log else None, b, None)
     res.gram = (A, Ai)
@@ -356,9 +371,13 @@ def closure_pauli_arrays(x, z, coef, qubits: int, method: Method = Method.orthon
     def sums(cs):
         return [PauliSum.single(PauliString(int(bx[i]), int(bz[i]), qubits), complex(cs[i, 0], cs[i, 1]))
                 for i in range(n)]
-    return ClosureResult(sums(bc), sums(oc), n, method, Backend.pauli, config.tolerance, stats,
-                         log[: log_len.value].copy() if config.record_log else None,
-                         (bx[:n].copy(), bz[:n].copy(), bc[:n].copy()), oc[:n].copy())
+    gram = method == Method.matrix_inversion
+    res = ClosureResult(sums(bc), None if gram else sums(oc), n, method, Backend.pauli, config.tolerance, stats,
+                        log[: log_len.value].copy() if config.record_log else None,
+                        (bx[:n].copy(), bz[:n].copy(), bc[:n].copy()), None if gram else oc[:n].copy())
+    if gram:  # distinct strings: A = A^{-1} = I exactly (see liecl_b200_closure_pauli)
+        res.gram = (np.eye(n, dtype=np.complex128), np.eye(n, dtype=np.complex128))
+    return res
 
 
 def closure_pauli_sums_arrays(offsets, x, z, coef, qubits: int, method: Method = Method.orthonorm_dimonly,
@@ -421,19 +440,29 @@ def closure_pauli_sums_arrays(offsets, x, z, coef, qubits: int, method: Method =
     def arrays(off, xs, zs, cs):
         t = int(off[n])
         return off[: n + 1].copy(), xs[:t].copy(), zs[:t].copy(), cs[:t].copy()
-    return ClosureResult(sums(bo, bx, bz, bc), sums(oo, ox, oz, ocf), n, method, Backend.pauli, config.tolerance,
-                         stats, log[: log_len.value].copy() if config.record_log else None,
-                         arrays(bo, bx, bz, bc), arrays(oo, ox, oz, ocf))
+    gram = method == Method.matrix_inversion
+    res = ClosureResult(sums(bo, bx, bz, bc), None if gram else sums(oo, ox, oz, ocf), n, method, Backend.pauli,
+                        config.tolerance, stats, log[: log_len.value].copy() if config.record_log else None,
+                        arrays(bo, bx, bz, bc), None if gram else arrays(oo, ox, oz, ocf))
+    if gram:  # result.gram from the device (liecl_b200_pauli_sums_fetch_gram)
+        A = np.zeros(n * n, np.complex128)
+        Ai = np.zeros(n * n, np.complex128)
+        if n:
+            _check(lib.liecl_b200_pauli_sums_fetch_gram(native.context(device), _dp(A.view(np.float64)),
+                                                        _dp(Ai.view(np.float64))))
+        res.gram = (A.reshape(n, n, order="F"), Ai.reshape(n, n, order="F"))
+    return res
 
 
 def run_closure(generators, method: Method, config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
-    """R:src/closure.cpp:541-564: orthonormal methods (dense, single-string
-    and multi-term Pauli) and matrix inversion (dense)."""
+    """R:src/closure.cpp:541-564: every method on dense generators; orthonormal
+    methods and matrix inversion on single-string and multi-term Pauli
+    generators (the rank method expands Pauli generators to dense, as the
+    reference does, R:src/closure.cpp:545-553)."""
     backend, dim = _validate(generators)
     if method == Method.standard_rank and backend != Backend.dense:
-        raise InvalidInputError("close_standard requires the dense backend; the rank check vectorizes operators")
-    if method == Method.matrix_inversion and backend != Backend.dense:
-        raise InvalidInputError("matrix-inversion on the B200 path takes dense generators")
+        dense = [None if g is None else from_pauli([g], device)[0] for g in generators]
+        return run_closure(dense, method, config, device)
     if backend == Backend.dense:
         gens = np.stack([g.vec() if g is not None else np.zeros(dim * dim, np.complex128) for g in generators])
         return closure_dense_arrays(gens, dim, method, config, device)
@@ -470,7 +499,12 @@ def close_matrix_inversion(generators, config: ClosureConfig | None = None, devi
 
 
 def close_standard(generators, config: ClosureConfig | None = None, device: int = 0) -> ClosureResult:
-    """R:include/liecl/closure.hpp:107-108 (Alg. 1, the rank method; dense generators)."""
+    """R:include/liecl/closure.hpp:107-108 (Alg. 1, the rank method; dense
+    generators -- run_closure expands Pauli generators first, close_standard
+    refuses them, R:src/closure.cpp:500-506)."""
+    backend, _ = _validate(generators)
+    if backend != Backend.dense and any(g is not None for g in generators):
+        raise InvalidInputError("close_standard requires the dense backend; the rank check vectorizes operators")
     return run_closure(generators, Method.standard_rank, config, device)
 
 
@@ -478,18 +512,24 @@ def close_standard(generators, config: ClosureConfig | None = None, device: int 
 
 
 def pauli_sum_from_terms(qubits: int, terms) -> PauliSum:
-    """PauliSum::from_terms (R:src/pauli.cpp:78-115): merge duplicate strings
-    in input order, drop |c| <= 1e-14 * max|c|, sort by (z, x)."""
-    acc: dict = {}
-    for s, c in terms:
+    """PauliSum::from_terms (R:src/pauli.cpp:78-115) on the device: merge
+    duplicate strings in input order, drop |c| <= 1e-14 * max|c|, sort by (z, x)."""
+    terms = list(terms)
+    for s, _ in terms:
         if s.qubits != qubits:
             raise InvalidInputError("PauliSum::from_terms: term qubit count mismatch")
-        key = (s.z, s.x)
-        a = acc.get(key, complex(0.0, 0.0))
-        acc[key] = complex(a.real + complex(c).real, a.imag + complex(c).imag)
-    floor = 1e-14 * max((abs(c) for c in acc.values()), default=0.0)
-    keys = sorted(k for k, c in acc.items() if abs(c) > floor)
-    return PauliSum(qubits, [(PauliString(k[1], k[0], qubits), acc[k]) for k in keys])
+    n = len(terms)
+    x = np.array([s.x for s, _ in terms], np.uint64)
+    z = np.array([s.z for s, _ in terms], np.uint64)
+    cf = np.array([(complex(c).real, complex(c).imag) for _, c in terms], np.float64).reshape(-1, 2)
+    m = max(n, 1)
+    rx, rz, rc = np.zeros(m, np.uint64), np.zeros(m, np.uint64), np.zeros((m, 2))
+    nt = C.c_int64()
+    u64 = C.POINTER(C.c_uint64)
+    _check(native.load().liecl_b200_pauli_from_terms(
+        native.context(0), C.c_int64(n), x.ctypes.data_as(u64), z.ctypes.data_as(u64), _dp(cf), C.c_uint32(qubits),
+        rx.ctypes.data_as(u64), rz.ctypes.data_as(u64), _dp(rc), C.c_int64(m), C.byref(nt)))
+    return _sum_from_arrays(qubits, rx, rz, rc, nt.value)
 
 
 def from_pauli(sums, device: int = 0):
@@ -567,8 +607,164 @@ def basis_listing(result: ClosureResult) -> str:
 # ------------------------------------------------------------ primitives ----
 
 
-def project_residual(orthonormal, h: DenseOperator, device: int = 0):
-    """(residual, first-pass coefficients), R:src/closure.cpp:142-162."""
+def _sums_arrays(sums):
+    """A tuple of PauliSums (None = null: no terms) -> (offsets, x, z, coef (t, 2))."""
+    offs, xs, zs, cs = [0], [], [], []
+    for g in sums:
+        for s_, c in (g.terms if g is not None else []):
+            c = complex(c)
+            xs.append(s_.x); zs.append(s_.z); cs.append((c.real, c.imag))
+        offs.append(len(xs))
+    return (np.array(offs, np.int64), np.array(xs, np.uint64), np.array(zs, np.uint64),
+            np.array(cs, np.float64).reshape(-1, 2))
+
+
+def _sum_args(sums, h, qubits):
+    o, x, z, c = _sums_arrays(sums)
+    ho, hx, hz, hc = _sums_arrays([h])
+    u64, i64 = C.POINTER(C.c_uint64), C.POINTER(C.c_int64)
+    keep = (o, x, z, c, hx, hz, hc)
+    args = [o.ctypes.data_as(i64), x.ctypes.data_as(u64), z.ctypes.data_as(u64), _dp(c), C.c_int64(len(sums)),
+            C.c_uint32(qubits), C.c_int64(len(hx)), hx.ctypes.data_as(u64), hz.ctypes.data_as(u64), _dp(hc)]
+    return args, keep, int(ho[-1] + o[-1])
+
+
+def _sum_from_arrays(qubits, x, z, c, nt) -> PauliSum:
+    return PauliSum(qubits, [(PauliString(int(x[t]), int(z[t]), qubits), complex(c[t, 0], c[t, 1]))
+                             for t in range(nt)])
+
+
+def _pauli_project_residual(orthonormal, h: PauliSum, device: int):
+    """project_residual over Pauli sums on the device (SumEngine passes), bit-exact."""
+    args, keep, bound = _sum_args(orthonormal, h, h.qubits)
+    bound = max(bound, 1)
+    rx, rz, rc = np.zeros(bound, np.uint64), np.zeros(bound, np.uint64), np.zeros((bound, 2))
+    nt = C.c_int64()
+    coeffs = np.zeros(max(len(orthonormal), 1), np.complex128)
+    u64 = C.POINTER(C.c_uint64)
+    _check(native.load().liecl_b200_project_residual_pauli(
+        native.context(device), *args, rx.ctypes.data_as(u64), rz.ctypes.data_as(u64), _dp(rc), C.c_int64(bound),
+        C.byref(nt), _dp(coeffs.view(np.float64))))
+    return _sum_from_arrays(h.qubits, rx, rz, rc, nt.value), list(coeffs[: len(orthonormal)])
+
+
+def _pauli_linear_combination(base: PauliSum, base_coeff: complex, tuple_, coeffs, device: int) -> PauliSum:
+    """from_terms(base_coeff * base ++ coeffs[l] * tuple_[l]) on the device."""
+    args, keep, bound = _sum_args(tuple_, base, base.qubits)
+    bound = max(bound, 1)
+    cf = np.array([[complex(c).real, complex(c).imag] for c in coeffs] or [[0.0, 0.0]], np.float64)
+    rx, rz, rc = np.zeros(bound, np.uint64), np.zeros(bound, np.uint64), np.zeros((bound, 2))
+    nt = C.c_int64()
+    u64 = C.POINTER(C.c_uint64)
+    _check(native.load().liecl_b200_linear_combination_pauli(
+        native.context(device), *args, C.c_double(complex(base_coeff).real), C.c_double(complex(base_coeff).imag),
+        _dp(cf), rx.ctypes.data_as(u64), rz.ctypes.data_as(u64), _dp(rc), C.c_int64(bound), C.byref(nt)))
+    return _sum_from_arrays(base.qubits, rx, rz, rc, nt.value)
+
+
+def check_matrix_inversion(gram: tuple, basis, h, tol: float, device: int = 0):
+    """check_matrix_inversion (R:src/closure.cpp:107-140) on the device:
+    (independent, beta). gram = (A, A^{-1}) n x n; basis = n operators."""
+    A, Ai = gram
+    n = len(basis)
+    if Ai.shape != (n, n):
+        raise InvalidInputError("check_matrix_inversion: state size does not match basis size")
+    if h is None:
+        return 0.0 > tol, [0j] * n
+    ind = C.c_int32()
+    beta = np.zeros(max(n, 1), np.complex128)
+    inv = np.asfortranarray(Ai, np.complex128).ravel(order="F")
+    if isinstance(h, PauliSum):
+        args, keep, _ = _sum_args(basis, h, h.qubits)
+        ao = args[:6]
+        _check(native.load().liecl_b200_check_matrix_inversion_pauli(
+            native.context(device), *ao, _dp(inv.view(np.float64)), *args[6:], C.c_double(tol), C.byref(ind),
+            _dp(beta.view(np.float64)), None))
+    else:
+        d = h.dim
+        B = np.ascontiguousarray(np.stack([b.vec() if b is not None else np.zeros(d * d, np.complex128)
+                                           for b in basis]) if n else np.zeros((1, d * d), np.complex128))
+        hv = np.ascontiguousarray(h.vec())
+        _check(native.load().liecl_b200_check_matrix_inversion_dense(
+            native.context(device), _dp(B.view(np.float64)), C.c_int64(n), _dp(inv.view(np.float64)),
+            _dp(hv.view(np.float64)), C.c_int32(d), C.c_double(tol), C.byref(ind), _dp(beta.view(np.float64)), None))
+    return bool(ind.value), list(beta[:n])
+
+
+class GramState:
+    """GramState (R:include/liecl/closure.hpp:28-55; R:src/closure.cpp:44-105)
+    with its operations on the device (liecl_b200_gram_*)."""
+
+    def __init__(self, gram=None, inverse=None, device: int = 0):
+        self.gram = np.zeros((0, 0), np.complex128) if gram is None else np.asarray(gram, np.complex128)
+        self.inverse = np.zeros((0, 0), np.complex128) if inverse is None else np.asarray(inverse, np.complex128)
+        self.device = device
+
+    def size(self) -> int:
+        return self.gram.shape[0]
+
+    @staticmethod
+    def _f(m):
+        return np.ascontiguousarray(np.asarray(m, np.complex128).ravel(order="F"))
+
+    def schur_complement(self, beta) -> float:
+        beta = np.ascontiguousarray(beta, np.complex128)
+        if len(beta) != self.size():
+            raise InvalidInputError("GramState: beta length does not match basis size")
+        s = C.c_double()
+        inv = self._f(self.inverse)
+        _check(native.load().liecl_b200_gram_schur_complement(native.context(self.device), _dp(inv.view(np.float64)),
+                                                              C.c_int64(len(beta)), _dp(beta.view(np.float64)),
+                                                              C.byref(s)))
+        return s.value
+
+    def expand(self, beta, conditioning_floor: float) -> None:
+        beta = np.ascontiguousarray(beta, np.complex128)
+        n = self.size()
+        if len(beta) != n:
+            raise InvalidInputError("GramState: beta length does not match basis size")
+        a = np.zeros((n + 1) ** 2, np.complex128)
+        ai = np.zeros((n + 1) ** 2, np.complex128)
+        g, inv = self._f(self.gram), self._f(self.inverse)
+        st = native.load().liecl_b200_gram_expand(
+            native.context(self.device), _dp(g.view(np.float64)), _dp(inv.view(np.float64)), C.c_int64(n),
+            _dp(beta.view(np.float64)), C.c_double(conditioning_floor), _dp(a.view(np.float64)),
+            _dp(ai.view(np.float64)))
+        if st == native.DEGENERACY:
+            raise DegeneracyError(native.last_error(), n)
+        _check(st)
+        self.gram = a.reshape(n + 1, n + 1, order="F")
+        self.inverse = ai.reshape(n + 1, n + 1, order="F")
+
+    def refresh(self) -> None:
+        n = self.size()
+        if n == 0:
+            return
+        ai = np.zeros(n * n, np.complex128)
+        g = self._f(self.gram)
+        _check(native.load().liecl_b200_gram_refresh(native.context(self.device), _dp(g.view(np.float64)),
+                                                     C.c_int64(n), _dp(ai.view(np.float64))))
+        self.inverse = ai.reshape(n, n, order="F")
+
+    def inverse_error(self) -> float:
+        e = C.c_double()
+        g, inv = self._f(self.gram), self._f(self.inverse)
+        _check(native.load().liecl_b200_gram_inverse_error(native.context(self.device), _dp(g.view(np.float64)),
+                                                           _dp(inv.view(np.float64)), C.c_int64(self.size()),
+                                                           C.byref(e)))
+        return e.value
+
+
+def project_residual(orthonormal, h, device: int = 0):
+    """(residual, first-pass coefficients), R:src/closure.cpp:142-162; dense
+    operators or Pauli sums, on the device."""
+    orthonormal = list(orthonormal)
+    if not orthonormal:
+        return h, []
+    if isinstance(h, PauliSum):
+        if any(not isinstance(v, PauliSum) or v.qubits != h.qubits for v in orthonormal if v is not None):
+            raise InvalidInputError("inner_product: operators have mismatched backends or dimensions")
+        return _pauli_project_residual(orthonormal, h, device)
     d = h.dim
     V = np.ascontiguousarray(np.stack([v.vec() for v in orthonormal]) if len(orthonormal) else
                              np.zeros((0, d * d), np.complex128))
@@ -601,16 +797,10 @@ def inner_product(a, b, device: int = 0) -> complex:
     if isinstance(a, PauliSum) or isinstance(b, PauliSum):
         if not (isinstance(a, PauliSum) and isinstance(b, PauliSum)) or a.qubits != b.qubits:
             raise InvalidInputError("inner_product: operators have mismatched backends or dimensions")
-        kb = {(s.z, s.x): c for s, c in b.terms}
-        re = im = 0.0
-        for s, ca in a.terms:  # both sorted by (z, x): the merge visits matches in this order
-            cb = kb.get((s.z, s.x))
-            if cb is None:
-                continue
-            ca, cb = complex(ca), complex(cb)
-            re += ca.real * cb.real + ca.imag * cb.imag
-            im += ca.real * cb.imag - ca.imag * cb.real
-        return complex(re, im)
+        args, keep, _ = _sum_args([a], b, a.qubits)
+        out = np.zeros(1, np.complex128)
+        _check(native.load().liecl_b200_overlaps_pauli(native.context(device), *args, _dp(out.view(np.float64))))
+        return complex(out[0])
     if a.dim != b.dim:
         raise InvalidInputError("inner_product: operators have mismatched backends or dimensions")
     out = np.zeros(2)
@@ -627,11 +817,13 @@ def norm(a, device: int = 0) -> float:
     if a is None:
         return 0.0
     if isinstance(a, PauliSum):
-        acc = 0.0
-        for _, c in a.terms:
-            c = complex(c)
-            acc += c.real * c.real + c.imag * c.imag
-        return float(np.sqrt(acc))
+        _, hx, hz, hc = _sums_arrays([a])
+        out = C.c_double()
+        u64 = C.POINTER(C.c_uint64)
+        _check(native.load().liecl_b200_norm_pauli(native.context(device), C.c_int64(len(hx)),
+                                                   hx.ctypes.data_as(u64), hz.ctypes.data_as(u64), _dp(hc),
+                                                   C.c_uint32(a.qubits), C.byref(out)))
+        return out.value
     out = C.c_double()
     av = np.ascontiguousarray(a.vec())
     _check(native.load().liecl_b200_norm_dense(native.context(device), _dp(av.view(np.float64)), C.c_int32(a.dim),
@@ -664,34 +856,30 @@ def normalized(a, device: int = 0):
         raise InvalidInputError("normalized: null operator")
     s = complex(1.0 / n, 0.0)
     if isinstance(a, PauliSum):
-        return _pauli_scale(a, s)
+        return _pauli_scale(a, s, device)
     return _linear_combination_dense(a, s, [], [], device)
 
 
-def _pauli_add(a: PauliSum, b: PauliSum) -> PauliSum:
-    """PauliSum::operator+ (R:src/pauli.cpp:128-159): sorted merge, equal
-    strings add (a + b), then |c| <= 1e-14 * max|c| is dropped."""
+def _pauli_add(a: PauliSum, b: PauliSum, device: int = 0) -> PauliSum:
+    """PauliSum::operator+ (R:src/pauli.cpp:128-159) on the device: the sorted
+    merge a + b with the drop rule is from_terms(1 * a ++ 1 * b) (slots start at
+    +0, so the sums are the same)."""
     if a.qubits != b.qubits:
         raise InvalidInputError("PauliSum::operator+: qubit counts differ")
-    ka = {(s.z, s.x): (s, c) for s, c in a.terms}
-    kb = {(s.z, s.x): (s, c) for s, c in b.terms}
-    merged = []
-    for k in sorted(set(ka) | set(kb)):
-        if k in ka and k in kb:
-            ca, cb = ka[k][1], kb[k][1]
-            merged.append((ka[k][0], complex(ca.real + cb.real, ca.imag + cb.imag)))
-        else:
-            merged.append(ka[k] if k in ka else kb[k])
-    floor = 1e-14 * max((abs(c) for _, c in merged), default=0.0)
-    return PauliSum(a.qubits, [(s, c) for s, c in merged if abs(c) > floor])
+    return _pauli_linear_combination(a, 1.0, [b], [1.0], device)
 
 
-def _pauli_scale(a: PauliSum, c: complex) -> PauliSum:
-    """PauliSum::operator*(Complex) (R:src/pauli.cpp:166-177)."""
+def _pauli_scale(a: PauliSum, c: complex, device: int = 0) -> PauliSum:
+    """PauliSum::operator*(Complex) (R:src/pauli.cpp:166-177): every term times
+    c, no merge or drop (a sum's strings are already unique)."""
     c = complex(c)
     if c == 0:
         return PauliSum(a.qubits, [])
-    return PauliSum(a.qubits, [(s, complex(t) * c) for s, t in a.terms])
+    _, x, z, cf = _sums_arrays([a])
+    out = np.zeros((max(len(x), 1), 2))
+    _check(native.load().liecl_b200_scale_terms(native.context(device), C.c_int64(len(x)), _dp(cf),
+                                                C.c_double(c.real), C.c_double(c.imag), _dp(out)))
+    return PauliSum(a.qubits, [(s, complex(out[t, 0], out[t, 1])) for t, (s, _) in enumerate(a.terms)])
 
 
 def linear_combination(base, base_coeff: complex, tuple_, coeffs, device: int = 0):
@@ -717,16 +905,14 @@ def linear_combination(base, base_coeff: complex, tuple_, coeffs, device: int = 
         for op, c in zip(tuple_, coeffs):
             if op is None:
                 continue
-            term = _pauli_scale(op, c)
-            acc = term if acc is None else _pauli_add(acc, term)
+            term = _pauli_scale(op, c, device)
+            acc = term if acc is None else _pauli_add(acc, term, device)
         return acc
     if isinstance(base, DenseOperator):
         return _linear_combination_dense(base, complex(base_coeff), tuple_, coeffs, device)
-    terms = [(s, complex(t) * complex(base_coeff)) for s, t in base.terms]
-    for op, c in zip(tuple_, coeffs):
-        if op is not None:
-            terms += [(s, complex(t) * c) for s, t in op.terms]
-    return pauli_sum_from_terms(base.qubits, terms)
+    # the PauliSum branch (R:src/operator.cpp:164-181) on the device
+    keep = [(op, c) for op, c in zip(tuple_, coeffs) if op is not None]
+    return _pauli_linear_combination(base, base_coeff, [o for o, _ in keep], [c for _, c in keep], device)
 
 
 def _linear_combination_dense(base, base_coeff, tuple_, coeffs, device):
@@ -894,10 +1080,16 @@ class ClosureSession:
         _check(self.lib.liecl_b200_session_field(self.ptr, C.byref(f)))
         return {0: "unset", 1: "complex", 2: "antihermitian_packed"}[f.value]
 
-    def basis(self) -> np.ndarray:
+    def basis(self, ortho: bool = False) -> np.ndarray:
+        """The commutator basis (host copy); ortho=True: the orthonormal tuple
+        (they differ for Alg. 3 sessions, keep_original)."""
         n = self.size()
         out = np.zeros((n, self.width), np.complex128)
-        _check(self.lib.liecl_b200_session_get_basis(self.ptr, _dp(out.view(np.float64)), C.c_int64(n)))
+        if ortho:
+            _check(self.lib.liecl_b200_session_get_vectors(self.ptr, C.c_int64(0), C.c_int64(n),
+                                                           _dp(out.view(np.float64)), C.c_int32(0), C.c_int32(1)))
+        else:
+            _check(self.lib.liecl_b200_session_get_basis(self.ptr, _dp(out.view(np.float64)), C.c_int64(n)))
         return out
 
     def vectors_to(self, first: int, count: int, out_ptr: int, on_device: bool = True, ortho: bool = False):

@@ -30,6 +30,13 @@ EXPORTED = [
     "liecl_b200_session_get_log",
     "liecl_b200_session_check_candidates",
     "liecl_b200_nccl_unique_id", "liecl_b200_shard_range", "liecl_b200_session_set_shards",
+    # round 2: device-resident results, GramState / check_matrix_inversion, Pauli-sum single queries
+    "liecl_b200_dense_fetch", "liecl_b200_pauli_sums_fetch_gram",
+    "liecl_b200_gram_schur_complement", "liecl_b200_gram_expand", "liecl_b200_gram_refresh",
+    "liecl_b200_gram_inverse_error", "liecl_b200_check_matrix_inversion_dense",
+    "liecl_b200_project_residual_pauli", "liecl_b200_linear_combination_pauli", "liecl_b200_overlaps_pauli",
+    "liecl_b200_pauli_from_terms", "liecl_b200_scale_terms", "liecl_b200_norm_pauli",
+    "liecl_b200_check_matrix_inversion_pauli",
 ]
 
 # int (*liecl_b200_reduce_fn)(double* values, int64_t count, void* user)

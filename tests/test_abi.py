@@ -61,8 +61,8 @@ def test_validation_errors_before_device():
     b = liecl.DenseOperator(np.eye(4))
     with pytest.raises(liecl.InvalidInputError):
         liecl.run_closure([a, b], liecl.Method.orthonorm_dimonly)
-    with pytest.raises(liecl.InvalidInputError):  # the rank method vectorizes dense operators only
-        liecl.run_closure([liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)], liecl.Method.standard_rank)
+    with pytest.raises(liecl.InvalidInputError):  # close_standard vectorizes dense operators only
+        liecl.close_standard([liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)])
 
 
 def test_pair_index_roundtrip():

@@ -108,3 +108,74 @@ def test_dropin_concurrent_callers(demo):
     """liecl::run_closure from four threads at once (one device context per
     calling thread): every result bit-identical to the serial run."""
     assert demo["concurrent_identical"] is True
+
+
+def _sum_arrays(sums):
+    offs, xs, zs, cs = [0], [], [], []
+    for s_ in sums:
+        for x, z, c in s_:
+            xs.append(x); zs.append(z); cs.append(c)
+        offs.append(len(xs))
+    return (np.array(offs, np.int64), np.array(xs, np.uint64), np.array(zs, np.uint64),
+            np.array(cs, np.float64).reshape(-1, 2))
+
+
+def _split(off, x, z, c):
+    return [[(int(x[t]), int(z[t]), (c[t, 0], c[t, 1])) for t in range(off[i], off[i + 1])]
+            for i in range(len(off) - 1)]
+
+
+def test_dropin_pauli_matrix_inversion(demo, ref_exact):
+    """close_matrix_inversion on Pauli generators through the drop-in (single
+    strings: HEA n = 3; multi-term sums: TFIM HVA n = 4) against the reference."""
+    off, x, z, c = ref_exact.build_generators("hea", 3)
+    o = ref_exact.closure_pauli(off, x, z, c, 3, method="matrix-inversion", tol=1e-10)
+    r = demo["hea3_matrix-inversion"]
+    assert r["dimension"] == o.dimension == 63 and r["gram_size"] == 63 and r["inverse_error"] == 0.0
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert r[k] == o.stats[k]
+    off, x, z, c = ref_exact.build_generators("tfim_hva_open", 4)
+    o = ref_exact.closure_pauli(off, x, z, c, 4, method="matrix-inversion", tol=1e-10)
+    r = demo["tfim4_matrix-inversion"]
+    assert r["dimension"] == o.dimension and r["gram_size"] == o.dimension and r["inverse_error"] < 1e-10
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert r[k] == o.stats[k]
+    ro, rx, rz, rc = o.basis
+    allt = np.concatenate([np.array(s_) for s_ in r["sums"]])
+    assert np.array_equal(allt[:, 0].astype(np.uint64), rx) and np.array_equal(allt[:, 1].astype(np.uint64), rz)
+    assert np.array_equal(allt[:, 2:], rc)
+
+
+def test_dropin_pauli_project_residual_and_check(demo, ref_exact):
+    import ctypes as C
+    off, x, z, c = ref_exact.build_generators("tfim_hva_open", 4)
+    gens = _split(off, x, z, c)
+    o = ref_exact.closure_pauli(off, x, z, c, 4, method="orthonorm-dimonly", tol=1e-10)
+    basis = _split(*o.basis)
+    # h = [gens[0], basis[7]] through the reference
+    ao, ax, az, ac = _sum_arrays([gens[0], basis[7]])
+    cap = 1 << 12
+    ho, hx, hz, hc = np.zeros(2, np.int64), np.zeros(cap, np.uint64), np.zeros(cap, np.uint64), np.zeros((cap, 2))
+    i64, u64, dp = C.POINTER(C.c_int64), C.POINTER(C.c_uint64), C.POINTER(C.c_double)
+    assert ref_exact.lib.liecl_ref_sum_commutator(
+        ao.ctypes.data_as(i64), ax.ctypes.data_as(u64), az.ctypes.data_as(u64), ac.ctypes.data_as(dp), C.c_uint(4),
+        ho.ctypes.data_as(i64), hx.ctypes.data_as(u64), hz.ctypes.data_as(u64), hc.ctypes.data_as(dp),
+        C.c_int64(cap)) == 0
+    h = [(int(hx[t]), int(hz[t]), (hc[t, 0], hc[t, 1])) for t in range(int(ho[1]))]
+    po, px, pz, pc = _sum_arrays(basis[:6] + [h])
+    (rx, rz, rcf), coeffs = ref_exact.project_residual_pauli(po, px, pz, pc, 6, 4)
+    acc = 0.0
+    for re, im in rcf:
+        acc += re * re + im * im
+    pr = demo["pauli_project_residual"]
+    assert pr["terms"] == len(rx)
+    assert pr["norm_bits"] == format(np.float64(np.sqrt(acc)).view(np.uint64), "016x")
+    assert pr["coeff0"] == [coeffs[0].real, coeffs[0].imag]
+    ck = demo["pauli_check_matrix_inversion"]
+    assert ck["member_independent"] is False and abs(ck["beta2"][0] - 1.0) < 1e-14 and ck["beta2"][1] == 0.0
+
+
+def test_dropin_gram_state_and_large_dense(demo):
+    g = demo["gram_state"]
+    assert g["schur"] == 0.75 and abs(g["inv01"] + 2.0 / 3.0) < 1e-15 and g["err"] < 1e-15
+    assert demo["d128"]["dimension"] == 3

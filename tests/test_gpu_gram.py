@@ -76,6 +76,121 @@ def test_expand_gram_spec_example():
     assert np.abs(Ai - np.array([[4 / 3, -2 / 3], [-2 / 3, 4 / 3]])).max() < 1e-14
 
 
-def test_pauli_matrix_inversion_is_rejected():
-    with pytest.raises(liecl.InvalidInputError):
-        liecl.run_closure([liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)], MI)
+def _pauli_ops(off, x, z, c, n):
+    return [liecl.PauliSum(n, [(liecl.PauliString(int(x[t]), int(z[t]), n), complex(c[t, 0], c[t, 1]))
+                               for t in range(off[i], off[i + 1])]) for i in range(len(off) - 1)]
+
+
+def _terms_bits(res_arrays, theirs_basis):
+    mo, mx, mz, mc = res_arrays
+    to, tx, tz, tc = theirs_basis
+    return (np.array_equal(mo, to) and np.array_equal(mx, tx) and np.array_equal(mz, tz)
+            and np.array_equal(mc, tc))
+
+
+@pytest.mark.parametrize("family,n,dim", [("hea", 2, 15), ("hea", 3, 63), ("hea", 4, 255)])
+def test_pauli_single_string_matrix_inversion_matches_reference(ref_exact, family, n, dim):
+    """close_matrix_inversion on single-string Pauli generators (was refused in
+    round 1; R:src/closure.cpp:519-527 accepts them): same dimension, stats and
+    accepted strings / coefficient bits as the reference build; A = A^-1 = I."""
+    off, x, z, c = ref_exact.build_generators(family, n)
+    assert (np.diff(off) == 1).all()
+    res = liecl.run_closure(_pauli_ops(off, x, z, c, n), MI, liecl.ClosureConfig(tolerance=1e-10))
+    theirs = ref_exact.closure_pauli(off, x, z, c, n, method="matrix-inversion", tol=1e-10)
+    assert res.dimension == theirs.dimension == dim
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(res.stats, k) == theirs.stats[k]
+    bx, bz, bc = res.basis_array
+    to, tx, tz, tc = theirs.basis
+    assert np.array_equal(bx, tx) and np.array_equal(bz, tz) and np.array_equal(bc, tc)
+    A, Ai = ref_exact.last_gram(dim)
+    assert np.array_equal(res.gram[0], A) and np.array_equal(res.gram[1], Ai)  # both the identity
+    assert np.array_equal(A, np.eye(dim))
+
+
+@pytest.mark.parametrize("family,n", [("tfim_hva_open", 4), ("tfim_hva_open", 6), ("xxz_hva", 4)])
+def test_pauli_sums_matrix_inversion_matches_reference(ref_exact, family, n):
+    """Alg. 2 over multi-term sums (SumEngine gram mode: beta from the sparse
+    overlaps, x = A^-1 beta on the device, residual = from_terms(h ++ -x_l B_l)):
+    the accept sequence and the accepted unit brackets bit for bit (they are
+    commutators of earlier elements, computed exactly as the reference does),
+    the Gram state within 1e-10."""
+    off, x, z, c = ref_exact.build_generators(family, n)
+    cfg = liecl.ClosureConfig(tolerance=1e-10)
+    res = liecl.closure_pauli_sums_arrays(off, x, z, c, n, MI, cfg)
+    theirs = ref_exact.closure_pauli(off, x, z, c, n, method="matrix-inversion", tol=1e-10)
+    assert res.dimension == theirs.dimension
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(res.stats, k) == theirs.stats[k]
+    assert _terms_bits(res.basis_array, theirs.basis)
+    A, Ai = ref_exact.last_gram(res.dimension)
+    assert np.abs(res.gram[0] - A).max() < 1e-12
+    assert np.abs(res.gram[1] - Ai).max() < 1e-10 * max(1.0, np.abs(Ai).max())
+    kinds = sorted(line.split("\t")[0] for line in theirs.warnings.splitlines() if line)
+    assert sorted(wr.kind for wr in res.stats.warnings) == kinds
+
+
+def test_gram_state_operations_match_reference(ref):
+    """GramState (R:src/closure.cpp:44-105) through the device operations: the
+    same expand sequence, Schur complements, bordered inverse, refresh and
+    inverse_error as the reference's own GramState."""
+    rng = np.random.default_rng(11)
+    d, n = 8, 12
+    B = rng.standard_normal((n, d * d)) + 1j * rng.standard_normal((n, d * d))
+    B /= (np.linalg.norm(B, axis=1) / np.sqrt(d))[:, None]  # unit under <a,b> = vdot/d
+    schur, A, Ai, Ar, err = ref.gram_state_dense(B, d)
+    st = liecl.GramState()
+    for k in range(n):
+        beta = np.array([ref.inner_product_dense(B[l], B[k], d) for l in range(k)], np.complex128)
+        assert abs(st.schur_complement(beta) - schur[k]) < 1e-12
+        st.expand(beta, 1e-12)
+    assert np.abs(st.gram - A).max() == 0.0  # the same betas placed the same way
+    assert np.abs(st.inverse - Ai).max() < 1e-12 * np.abs(Ai).max()
+    assert abs(st.inverse_error() - err) < 1e-12
+    st.refresh()
+    assert np.abs(st.inverse - Ar).max() < 1e-12 * np.abs(Ar).max()
+    with pytest.raises(liecl.DegeneracyError):  # an element in the span: Schur complement ~ 0
+        st.expand(np.array([ref.inner_product_dense(B[l], B[0], d) for l in range(n)]), 1e-12)
+
+
+def test_check_matrix_inversion_dense_and_pauli(ref, ref_exact):
+    rng = np.random.default_rng(12)
+    d, n = 8, 6
+    B = rng.standard_normal((n, d * d)) + 1j * rng.standard_normal((n, d * d))
+    B /= (np.linalg.norm(B, axis=1) / np.sqrt(d))[:, None]
+    _, A, Ai, _, _ = ref.gram_state_dense(B, d)
+    ops = [liecl.DenseOperator.from_vec(b, d) for b in B]
+    inside = 0.3 * B[1] - 0.7j * B[4]
+    for h in (rng.standard_normal(d * d) + 1j * rng.standard_normal(d * d), inside):
+        ind, beta = liecl.check_matrix_inversion((A, Ai), ops, liecl.DenseOperator.from_vec(h, d), 1e-10)
+        rind, rbeta = ref.check_matrix_inversion_dense(B, d, h)
+        assert ind == rind and np.abs(np.array(beta) - rbeta).max() < 1e-13
+    assert liecl.check_matrix_inversion((A, Ai), ops, liecl.DenseOperator.from_vec(inside, d), 1e-10)[0] is False
+    # Pauli: tuple of TFIM sums, h = another sum / a combination
+    off, x, z, c = ref_exact.build_generators("tfim_hva_open", 4)
+    sums = _pauli_ops(off, x, z, c, 4)
+    from paper_2506_01120_b200.liecl import _sums_arrays
+    for h in (sums[-1], liecl.linear_combination(sums[0], 0.5, [sums[1]], [2.0])):
+        tup = sums[:-1] if h is sums[-1] else sums[:2]
+        o, xx, zz, cc = _sums_arrays(tup + [h])
+        rind, rbeta, rA, rAi = ref_exact.check_matrix_inversion_pauli(o, xx, zz, cc, len(tup), 4)
+        ind, beta = liecl.check_matrix_inversion((rA, rAi), tup, h, 1e-10)
+        assert ind == rind and np.array_equal(np.array(beta, np.complex128), rbeta)
+
+
+def test_project_residual_pauli_bit_exact(ref_exact):
+    from paper_2506_01120_b200.liecl import _sums_arrays
+    off, x, z, c = ref_exact.build_generators("xxz_hva", 4)
+    sums = _pauli_ops(off, x, z, c, 4)
+    # an orthonormal tuple (the reference's own closure) and a bracket to project
+    o = ref_exact.closure_pauli(off, x, z, c, 4, method="orthonorm-dimonly", tol=1e-10)
+    bo, bx, bz, bc = o.basis
+    V = _pauli_ops(bo, bx, bz, bc, 4)[:10]
+    for h in (sums[0], V[3], liecl.linear_combination(V[2], 1.0, [sums[1]], [0.25j])):
+        r, coeffs = liecl.project_residual(V, h)
+        oo, xx, zz, cc = _sums_arrays(V + [h])
+        (rx, rz, rc), rco = ref_exact.project_residual_pauli(oo, xx, zz, cc, len(V), 4)
+        assert [(t.x, t.z) for t, _ in r.terms] == list(zip(rx.tolist(), rz.tolist()))
+        got = np.array([[v.real, v.imag] for _, v in r.terms]).reshape(-1, 2)
+        assert np.array_equal(got.view(np.uint64), rc.view(np.uint64))
+        assert np.array_equal(np.array(coeffs, np.complex128).view(np.uint64), rco.view(np.uint64))

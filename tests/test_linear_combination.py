@@ -1,6 +1,7 @@
 """linear_combination (R:src/operator.cpp:137-182) against the reference
-build: the Pauli branch (host, from_terms) on CPU, the dense branch (GPU
-kernel) on the GPU; null / empty-base fallbacks and errors."""
+build: the Pauli branch (SumEngine merges) and the dense branch (GPU kernel),
+bit for bit; null / empty-base fallbacks; argument errors (raised before any
+device work, so they run on CPU)."""
 import ctypes as C
 
 import numpy as np
@@ -10,8 +11,12 @@ from paper_2506_01120_b200 import liecl
 
 
 def _rand_sum(rng, n, k):
-    return liecl.pauli_sum_from_terms(n, [(liecl.PauliString(int(rng.integers(0, 1 << n)), int(rng.integers(0, 1 << n)), n),
-                                          complex(*rng.standard_normal(2))) for _ in range(k)])
+    # built with the host recipe (test infrastructure); the product's from_terms runs on the device
+    from paper_2506_01120_b200 import workloads as w
+    raw = [((int(rng.integers(0, 1 << n)), int(rng.integers(0, 1 << n))), complex(*rng.standard_normal(2)))
+           for _ in range(k)]
+    b = w.PauliSumSpec.from_terms(n, raw)
+    return liecl.PauliSum(n, [(liecl.PauliString(int(x), int(z), n), c) for x, z, c in zip(b.x, b.z, b.coef)])
 
 
 def _ref_lc_pauli(ref, base, bc, tup, coeffs, n):
@@ -49,6 +54,7 @@ def _bits(v):
     return None if v is None else [(a, b, np.float64(c).view(np.uint64), np.float64(d).view(np.uint64)) for a, b, c, d in v]
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("seed", range(6))
 def test_pauli_branch_bit_exact(ref_exact, seed):
     rng = np.random.default_rng(50 + seed)
@@ -69,10 +75,10 @@ def test_pauli_branch_bit_exact(ref_exact, seed):
 
 
 def test_errors():
-    a = liecl.pauli_sum_from_terms(1, [(liecl.PauliString(1, 0, 1), 1.0)])
+    a = liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)
     with pytest.raises(liecl.InvalidInputError, match="lengths differ"):
         liecl.linear_combination(a, 1.0, [a], [])
-    b = liecl.pauli_sum_from_terms(2, [(liecl.PauliString(1, 0, 2), 1.0)])
+    b = liecl.PauliSum.single(liecl.PauliString(1, 0, 2), 1.0)
     with pytest.raises(liecl.InvalidInputError):
         liecl.linear_combination(a, 1.0, [b], [1.0])
 
@@ -115,6 +121,7 @@ def test_dense_branch_matches_reference(ref_exact, case):
     assert np.array_equal(got.vec().view(np.uint64), out.view(np.uint64))
 
 
+@pytest.mark.gpu
 def test_pauli_norm_inner_product_axpy_dot_and_helpers():
     rng = np.random.default_rng(9)
     a, b = _rand_sum(rng, 3, 5), _rand_sum(rng, 3, 5)
