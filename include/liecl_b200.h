@@ -16,6 +16,11 @@
  *   Pauli string    (x, z) masks (bit j = X / Z factor on qubit j), one
  *                   complex coefficient as (re, im) doubles
  *                   (R:include/liecl/pauli.hpp:24-38,67-70).
+ *
+ * Streams: a context launches on its own non-blocking stream unless
+ * liecl_b200_ctx_set_stream gives it the caller's. Device input produced on
+ * another stream must be complete before the call (synchronise, or share the
+ * stream); every call returns with its host outputs written.
  */
 #ifndef LIECL_B200_H
 #define LIECL_B200_H

@@ -22,11 +22,14 @@ public:
   DenseEngine(liecl_b200_ctx* ctx, int d, bool keep_original, const liecl_b200_config& cfg)
       : ctx_(ctx), d_(d), D_(static_cast<int64_t>(d) * d), keep_(keep_original), tol_(cfg.tolerance),
         record_(cfg.record_log != 0), force_complex_(cfg.field == 1), stop_complete_(cfg.stop_when_complete != 0) {
-    if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
+    if (d < 1 || d > 4096)  // 12 qubits: the reference's dense expansion limit (R:include/liecl/dense.hpp:45)
+      throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 4096]");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
     cap_ = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : D_;
     const int64_t budget = int64_t(16) << 30;  // bytes for the three D x B candidate slabs (complex)
-    bmax_ = cfg.batch_max > 0 ? cfg.batch_max : std::clamp<int64_t>(budget / (3 * D_ * 16), 64, 8192);
+    // at d >= 2048 (D = 4M..16.7M elements) fewer than 64 candidates fit the budget
+    bmax_ = cfg.batch_max > 0 ? cfg.batch_max
+                              : std::clamp<int64_t>(budget / (3 * D_ * 16), D_ > (int64_t(1) << 20) ? 8 : 64, 8192);
     set_deadline(cfg);
     sqrt_d_ = std::sqrt(static_cast<double>(d));
     B_cur_ = std::min<int64_t>(bmax_, 512);
@@ -504,7 +507,8 @@ private:
       field_ = (n_o_ == 0) ? f : Field::kComplex;
       const bool reuse = layout_slabs();
       alloc_batch();
-      ensure_capacity(std::min<int64_t>(cap_ + 1, std::max<int64_t>(64, (int64_t(1) << 30) / (D_ * 16))));
+      ensure_capacity(std::min<int64_t>(cap_ + 1, std::max<int64_t>(D_ > (int64_t(1) << 20) ? 8 : 64,
+                                                                    (int64_t(1) << 30) / (D_ * 16))));
       if (reuse && vcap_ > 0) {  // a previous closure's vectors: restore the zero tail invariant
         CU(cudaMemsetAsync(V_.p, 0, static_cast<size_t>(vcap_ * vw()) * sizeof(double), ctx_->stream));
         if (Vw_.p) CU(cudaMemsetAsync(Vw_.p, 0, static_cast<size_t>(vcap_ * vw()) * sizeof(double), ctx_->stream));

@@ -1303,7 +1303,8 @@ int liecl_b200_project_residual_dense(liecl_b200_ctx* ctx, const double* V, int6
 int liecl_b200_commutator_dense(liecl_b200_ctx* ctx, const double* a, const double* b, int32_t d, double* out) {
   return guarded([&] {
     if (!ctx || !a || !b || !out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-    if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
+    if (d < 1 || d > 4096)  // 12 qubits: the reference's dense expansion limit (R:include/liecl/dense.hpp:45)
+      throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 4096]");
     use_device(ctx);
     const int64_t D = static_cast<int64_t>(d) * d;
     DevBuf<double2> basis, o;
@@ -1417,7 +1418,7 @@ int liecl_b200_linear_combination_dense(liecl_b200_ctx* ctx, const double* base,
                                         const double* tuple, const double* coeffs, const int32_t* is_null,
                                         int64_t n, int32_t d, double* out, int32_t* out_null) {
   return guarded([&] {
-    if (!ctx || !out || n < 0 || (n > 0 && (!tuple || !coeffs)) || d < 1 || d > 1024)
+    if (!ctx || !out || n < 0 || (n > 0 && (!tuple || !coeffs)) || d < 1 || d > 4096)
       throw Error(LIECL_B200_INVALID_INPUT, "linear_combination: bad arguments");
     use_device(ctx);
     const int64_t D = static_cast<int64_t>(d) * d;

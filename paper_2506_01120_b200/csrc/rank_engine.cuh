@@ -157,10 +157,13 @@ public:
   RankEngine(liecl_b200_ctx* ctx, int d, const liecl_b200_config& cfg)
       : ctx_(ctx), d_(d), D_(static_cast<int64_t>(d) * d), tol_(cfg.tolerance), rank_tol_(cfg.rank_tolerance),
         record_(cfg.record_log != 0) {
-    if (d < 1 || d > 1024) throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 1024]");
+    if (d < 1 || d > 4096)  // 12 qubits: the reference's dense expansion limit (R:include/liecl/dense.hpp:45)
+      throw Error(LIECL_B200_INVALID_INPUT, "dense dimension must be in [1, 4096]");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
     cap_ = cfg.max_dim ? static_cast<int64_t>(cfg.max_dim) : D_;
-    bmax_ = cfg.batch_max > 0 ? cfg.batch_max : std::clamp<int64_t>((int64_t(4) << 30) / (3 * D_ * 16), 16, 1024);
+    bmax_ = cfg.batch_max > 0 ? cfg.batch_max
+                              : std::clamp<int64_t>((int64_t(4) << 30) / (3 * D_ * 16), D_ > (int64_t(1) << 20) ? 4 : 16,
+                                                    1024);
     if (cfg.deadline_seconds > 0) {
       has_deadline_ = true;
       deadline_ = Clock::now() + std::chrono::duration_cast<Clock::duration>(
@@ -169,7 +172,7 @@ public:
     sqrt_d_ = std::sqrt(static_cast<double>(d));
     C_.ensure(static_cast<size_t>(bmax_ * D_));
     X_.ensure(static_cast<size_t>(bmax_ * D_));
-    reserve(std::min<int64_t>(cap_ + 1, 64));  // basis slabs grow with the closure
+    reserve(std::min<int64_t>(cap_ + 1, D_ > (int64_t(1) << 20) ? 8 : 64));  // basis slabs grow with the closure
     partial_.ensure(static_cast<size_t>(((D_ + zg::BM - 1) / zg::BM) * bmax_));
     rn_.ensure(bmax_); hn_.ensure(bmax_); nul_.ensure(bmax_); ind_.ensure(bmax_); smin_.ensure(bmax_);
     smax_.ensure(bmax_);

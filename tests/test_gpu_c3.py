@@ -18,6 +18,7 @@ def c3_run():
     dev = torch.device("cuda", 0)
     c3 = w.Config3()
     V, cands = c3.generate(torch, dev)
+    torch.cuda.synchronize(dev)  # the context's stream does not order against torch's
     s = liecl.ClosureSession(c3.d, config=liecl.ClosureConfig(tolerance=c3.tol, max_dim=c3.n + c3.ncand))
     s.set_basis(V.data_ptr(), on_device=True, n=c3.n)
     ind, rn, st = s.check_candidates(cands.data_ptr(), on_device=True, n=c3.ncand)

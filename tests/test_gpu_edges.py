@@ -210,3 +210,25 @@ def test_stop_when_complete_keeps_the_basis(field):
     b = liecl.closure_dense_arrays(tf, 16, liecl.Method.orthonorm_dimonly,
                                    liecl.ClosureConfig(tolerance=1e-10, field=field, stop_when_complete=True))
     assert a.dimension == b.dimension and a.stats.commutators_evaluated == b.stats.commutators_evaluated
+
+
+@pytest.mark.parametrize("d,method", [(2048, "orthonorm-dimonly"), (2048, "orthonorm"), (2048, "matrix-inversion"),
+                                      (2048, "standard-rank"), (4096, "orthonorm-dimonly")])
+def test_dense_up_to_twelve_qubits(d, method):
+    """Dense operators up to d = 4096 (the reference's 12-qubit expansion
+    limit, R:include/liecl/dense.hpp:45; round 1 refused d > 1024): i X_0 and
+    i Z_0 close to su(2), dimension 3, with the reference's counters."""
+    n = d.bit_length() - 1
+    xs = liecl.PauliSum.single(liecl.PauliString(1, 0, n), 1j)
+    zs = liecl.PauliSum.single(liecl.PauliString(0, 1, n), 1j)
+    X, Z = liecl.from_pauli([xs, zs])
+    m = liecl.method_from_string(method)
+    res = liecl.run_closure([X, Z], m, liecl.ClosureConfig(tolerance=1e-10))
+    assert res.dimension == 3
+    assert res.stats.commutators_evaluated == 3 and res.stats.independence_checks == 5
+    assert res.stats.accepted == 3
+    # the third element is +-i Y_0 (unit norm under <a,b> = tr(a^H b)/d)
+    ys = liecl.from_pauli([liecl.PauliSum.single(liecl.PauliString(1, 1, n), 1j)])[0]
+    v = res.basis[2].vec()
+    ov = np.vdot(ys.vec(), v) / d
+    assert abs(abs(ov) - 1.0) < 1e-12

@@ -70,6 +70,7 @@ def test_c3_full_size_first_64_candidates_same_bytes_as_reference(ref):
     dev = torch.device("cuda", 0)
     c3 = w.Config3()
     V, cands = c3.generate(torch, dev)
+    torch.cuda.synchronize(dev)  # the context's stream does not order against torch's
     k = 64
     s = liecl.ClosureSession(c3.d, config=liecl.ClosureConfig(tolerance=c3.tol, max_dim=c3.n + 1))
     ind = np.zeros(k, np.int32)

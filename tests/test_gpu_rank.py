@@ -60,7 +60,10 @@ def test_rank_tolerance_knob(ref):
 
 def test_rank_method_rejects_pauli_and_honours_capacity():
     with pytest.raises(liecl.InvalidInputError, match="dense backend"):
-        liecl.run_closure([liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)], RANK)
+        liecl.close_standard([liecl.PauliSum.single(liecl.PauliString(1, 0, 1), 1.0)])
+    # run_closure expands Pauli generators to dense first (R:src/closure.cpp:545-553)
+    xz = [liecl.PauliSum.single(liecl.PauliString(1, 0, 2), 1j), liecl.PauliSum.single(liecl.PauliString(0, 1, 2), 1j)]
+    assert liecl.run_closure(xz, RANK, liecl.ClosureConfig(tolerance=1e-10)).dimension == 3
     cfg = w.config0()
     with pytest.raises(liecl.CapacityError):
         liecl.closure_dense_arrays(cfg.generators, cfg.d, RANK, liecl.ClosureConfig(tolerance=cfg.tol, max_dim=4))
