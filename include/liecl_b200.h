@@ -418,6 +418,30 @@ int liecl_b200_check_matrix_inversion_dense(liecl_b200_ctx* ctx, const double* b
                                             const double* inverse, const double* h, int32_t d, double tol,
                                             int32_t* independent, double* beta_out, double* residual_norm);
 
+/*
+ * D-sharded closure loop (the north star's "basis rows sharded per
+ * GPU; only per-candidate partial overlap sums are all-reduced"): on a fresh
+ * session, rank r of P keeps WHOLE operators (set_basis / run_closure take
+ * full operators, get_basis returns them) and computes every commutator, null
+ * test and normalisation itself; the projection GEMMs run on elements [lo, hi)
+ * = liecl_b200_loop_shard_range(d, P, r) only, and the partial overlaps beta,
+ * the partial squared residual norms and each accepted vector's slices are
+ * summed over ranks (NCCL via nccl_id, or the host callback as in set_shards).
+ * Every rank reaches the same verdicts, basis and statistics; a per-batch
+ * digest all-reduce raises LIECL_B200_INTERNAL if ranks ever diverge.
+ * run_pairs / run_rows / run_closure all work on such a session.
+ */
+int liecl_b200_session_set_loop_shards(liecl_b200_session* s, int32_t nranks, int32_t rank, const uint8_t* nccl_id,
+                                       liecl_b200_reduce_fn reduce, void* user);
+int liecl_b200_loop_shard_range(int32_t d, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi);
+/* The whole closure on a session (run_closure's engine, R:src/closure.cpp:356-473):
+ * the generator loop over `ngens` full operators (normalise, check, append;
+ * null-generator warnings), then every cursor pair until exhausted. The
+ * basis, log and warnings stay in the session (get_basis / get_log /
+ * session_warnings, lines "kind\tvalue\tdetail\n"). */
+int liecl_b200_session_run_closure(liecl_b200_session* s, const double* gens, int32_t ngens, liecl_b200_stats* stats);
+int liecl_b200_session_warnings(liecl_b200_session* s, char* buf, int64_t len);
+
 #ifdef __cplusplus
 }
 #endif

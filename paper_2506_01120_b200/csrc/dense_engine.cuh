@@ -143,9 +143,41 @@ public:
     shard_range(Dfull, nranks, rank, lo, hi);
     D_ = hi - lo;
     red_ = std::move(red);
+    nranks_ = nranks;
     force_complex_ = true;
   }
   bool sharded() const { return static_cast<bool>(red_); }
+
+  // D-sharded closure loop (the north star's "basis rows sharded
+  // per GPU"): every rank keeps the whole operators (the commutators need
+  // them; c2's basis is 134-268 MB) and computes the same commutators, null
+  // tests and normalisations bit for bit; the projection GEMMs run on this
+  // rank's element slice [lo, hi) only (1/P of the flops), and the partial
+  // overlaps and squared residual norms are summed over ranks by `red` -- the
+  // only data that crosses GPUs besides one all-reduce per accepted vector
+  // (each rank contributes its slice of the new basis vector, the sum rebuilds
+  // it everywhere). Slice bounds are multiples of 2(d+1) elements: even (16-byte
+  // aligned packed rows) and aligned to the diagonal period of the packed
+  // weights, so the GEMM epilogues weight a slice exactly as the whole vector.
+  void set_loop_shards(int nranks, int rank, std::unique_ptr<Reducer> red) {
+    if (n_o_ != 0 || field_ != Field::kUnset || vcap_ != 0 || red_)
+      throw Error(LIECL_B200_INVALID_INPUT, "set_shards needs a fresh session (before set_basis / check_candidates)");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(LIECL_B200_INVALID_INPUT, "bad shard rank / count");
+    loop_shard_range(D_, d_, nranks, rank, lo_, hi_);
+    red_ = std::move(red);
+    loop_shard_ = true;
+    nranks_ = nranks;
+  }
+  static void loop_shard_range(int64_t D, int d, int nranks, int rank, int64_t& lo, int64_t& hi) {
+    const int64_t unit = 2 * (static_cast<int64_t>(d) + 1);
+    auto bound = [&](int r) {
+      if (r <= 0) return int64_t(0);
+      if (r >= nranks) return D;
+      return std::min(D, (D * r / nranks) / unit * unit);
+    };
+    lo = bound(rank);
+    hi = bound(rank + 1);
+  }
 
   // ---- state / results ----------------------------------------------------
   Field field() const { return field_; }
@@ -308,9 +340,10 @@ public:
         scale_columns_ah_kernel<<<g2, 256, 0, ctx_->stream>>>(R_.p, hn_.p, tol_, D_, C_.p);
         launched(ctx_);
       } else {
-        column_norm_kernel<<<cnt, 256, 0, ctx_->stream>>>(stage_.p, D_, red_ ? 0.0 : sqrt_d_, hn_.p);
+        const bool partial_norms = red_ && !loop_shard_;  // slice storage: norms are sums over ranks
+        column_norm_kernel<<<cnt, 256, 0, ctx_->stream>>>(stage_.p, D_, partial_norms ? 0.0 : sqrt_d_, hn_.p);
         launched(ctx_);
-        if (red_) sharded_norms(hn_.p, cnt);
+        if (partial_norms) sharded_norms(hn_.p, cnt);
         dim3 g2(static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 64)), cnt);
         scale_columns_kernel<<<g2, 256, 0, ctx_->stream>>>(stage_.p, hn_.p, tol_, D_, cplx(C_.p));
         launched(ctx_);
@@ -477,7 +510,7 @@ private:
       throw Error(LIECL_B200_TIMEOUT, "closure computation exceeded its deadline");
   }
   void whole_operators(const char* what) const {
-    if (red_)
+    if (red_ && !loop_shard_)
       throw Error(LIECL_B200_INVALID_INPUT,
                   std::string(what) + " needs whole operators; a D-sharded session only checks candidates");
   }
@@ -603,18 +636,35 @@ private:
   // copy Vwb on the packed path): Rout = X - Vb beta, beta = <Vb, X>,
   // rn = ||Rout|| (Rout may alias X).
   void project(const double* Vb, const double* Vwb, int64_t n, const double* X, int count, double* Rout, double* rn) {
-    int mtiles;
+    int mtiles = 0;
+    // loop shards: the GEMMs cover elements [lo, hi) of full-length columns
+    const int64_t off = loop_shard_ ? lo_ * ew() : 0;
+    const int64_t len = loop_shard_ ? hi_ - lo_ : D_;
     if (field_ == Field::kAntiHerm) {
       const int64_t ldp = (n + 1) & ~int64_t(1);  // even: 16-byte aligned P columns
-      rgemm_project(ctx_, Vwb, n, D_, X, count, P_.p, ldp, 1.0 / d_);
-      rgemm_subtract(ctx_, Vb, n, D_, P_.p, ldp, X, count, Rout, partial_.p, d_);
-      mtiles = static_cast<int>((D_ + rg::BM - 1) / rg::BM);
+      if (len > 0) {
+        rgemm_project(ctx_, Vwb + off, n, len, X + off, count, P_.p, ldp, 1.0 / d_, D_, D_);
+      } else if (n > 0) {
+        CU(cudaMemsetAsync(P_.p, 0, static_cast<size_t>(ldp * count) * sizeof(double), ctx_->stream));
+      }
+      if (red_ && n > 0) red_->sum(P_.p, ldp * count, ctx_->stream);  // partial overlaps over ranks
+      if (len > 0) {
+        rgemm_subtract(ctx_, Vb + off, n, len, P_.p, ldp, X + off, count, Rout + off, partial_.p, d_, D_, D_);
+        mtiles = static_cast<int>((len + rg::BM - 1) / rg::BM);
+      }
     } else {
-      gemm_project(ctx_, cplx(Vb), n, D_, cplx(X), count, cplx(P_.p), 1.0 / d_);
+      if (len > 0) {
+        gemm_project(ctx_, cplx(Vb) + off / 2, n, len, cplx(X) + off / 2, count, cplx(P_.p), 1.0 / d_, D_, D_);
+      } else if (n > 0) {
+        CU(cudaMemsetAsync(P_.p, 0, static_cast<size_t>(2 * n * count) * sizeof(double), ctx_->stream));
+      }
       // D-shard: this rank's beta is a partial sum over its slice
       if (red_ && n > 0) red_->sum(P_.p, 2 * n * count, ctx_->stream);
-      gemm_subtract(ctx_, cplx(Vb), n, D_, cplx(P_.p), cplx(X), count, cplx(Rout), partial_.p);
-      mtiles = static_cast<int>((D_ + zg::BM - 1) / zg::BM);
+      if (len > 0) {
+        gemm_subtract(ctx_, cplx(Vb) + off / 2, n, len, cplx(P_.p), cplx(X) + off / 2, count, cplx(Rout) + off / 2,
+                      partial_.p, D_, D_);
+        mtiles = static_cast<int>((len + zg::BM - 1) / zg::BM);
+      }
     }
     norm_finalize_kernel<<<(count + 255) / 256, 256, 0, ctx_->stream>>>(partial_.p, mtiles, count,
                                                                        red_ ? 0.0 : sqrt_d_, rn);
@@ -742,6 +792,11 @@ private:
     for (int j = 0; j < cnt; ++j)
       if (!h_nul_.p[j] && h_rn1_.p[j] > screen) h_idx_.p[nsurv++] = j;
     st_.survivors += static_cast<uint64_t>(nsurv);
+    if (red_) {  // every rank must take the same survivors (see verdict_guard)
+      uint64_t h = static_cast<uint64_t>(nsurv);
+      for (int q = 0; q < nsurv; ++q) h = h * 1000003u + static_cast<uint64_t>(h_idx_.p[q]);
+      verdict_guard(h, "survivor set");
+    }
     if (nsurv > 0) {
       CU(cudaMemcpyAsync(idx_.p, h_idx_.p, nsurv * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
       dim3 gg(static_cast<unsigned>(std::min<int64_t>((W + 255) / 256, 64)), nsurv);
@@ -867,11 +922,46 @@ private:
             keep_ ? cplx(vp(O_, n_b_)) : nullptr);
       }
       launched(ctx_);
+      if (loop_shard_) {  // only this rank's slice of the residual is valid: rebuild the vector over ranks
+        gather_slices(vp(V_, n_o_));
+        if (field_ == Field::kAntiHerm) gather_slices(vp(Vw_, n_o_));
+      }
       ++n_o_;
       if (keep_) ++n_b_;
       ++st_.accepted;
     }
     if (!keep_) n_b_ = n_o_;
+    if (red_) verdict_guard(static_cast<uint64_t>(n_o_) * 1000003u + static_cast<uint64_t>(n_bs), "accepts");
+  }
+
+  // Ranks agree on every verdict because each reduced value is bit-identical
+  // on every rank (NCCL's all-reduce reduces each element once and hands the
+  // same bits to all ranks; so does the host callback by contract). If that
+  // ever failed, ranks would issue different collective sequences; this check
+  // (one 2-double all-reduce) turns the divergence into an error instead: it
+  // sums h and h^2 of a 20-bit digest over ranks, exact in doubles, and all
+  // ranks agree iff P * sum(h^2) == sum(h)^2.
+  void verdict_guard(uint64_t h, const char* what) {
+    h = (h ^ (h >> 29) ^ (h >> 47)) & 0xFFFFF;
+    double v[2] = {static_cast<double>(h), static_cast<double>(h) * static_cast<double>(h)};
+    guard_.ensure(2);
+    CU(cudaMemcpyAsync(guard_.p, v, sizeof v, cudaMemcpyHostToDevice, ctx_->stream));
+    red_->sum(guard_.p, 2, ctx_->stream);
+    CU(cudaMemcpyAsync(v, guard_.p, sizeof v, cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    if (static_cast<double>(nranks_) * v[1] != v[0] * v[0])
+      throw Error(LIECL_B200_INTERNAL, std::string("D-sharded ranks diverged (") + what +
+                                           "): the cross-rank sums were not bit-identical on every rank");
+  }
+
+  // loop shards: a freshly appended vector holds this rank's slice [lo, hi);
+  // zero the rest and sum over ranks (exact: every element has one non-zero
+  // contribution), leaving the whole vector on every rank
+  void gather_slices(double* v) {
+    const int64_t W = vw(), a = lo_ * ew(), b = hi_ * ew();
+    if (a > 0) CU(cudaMemsetAsync(v, 0, static_cast<size_t>(a) * sizeof(double), ctx_->stream));
+    if (b < W) CU(cudaMemsetAsync(v + b, 0, static_cast<size_t>(W - b) * sizeof(double), ctx_->stream));
+    red_->sum(v, W, ctx_->stream);
   }
 
   // device-resident block decisions (block_gs.cuh): either field, not
@@ -960,7 +1050,11 @@ private:
   uint64_t cseq_ = 0;
   int64_t complete_n_ = -1;
   bool complete_ = false;
-  std::unique_ptr<Reducer> red_;  // set: D-sharded (D_ is this rank's slice)
+  std::unique_ptr<Reducer> red_;  // set: D-sharded (D_ is this rank's slice, or loop_shard_)
+  bool loop_shard_ = false;       // D-sharded closure loop: whole operators, GEMMs on [lo_, hi_)
+  int64_t lo_ = 0, hi_ = 0;
+  int nranks_ = 1;
+  DevBuf<double> guard_;
   Field field_ = Field::kUnset;
   Field slab_field_ = Field::kUnset;  // layout the basis slabs are allocated for
   DevBuf<double2> unpack_;            // packed -> complex output staging

@@ -255,17 +255,18 @@ __global__ void rsplitk_reduce_scale_kernel(const double* __restrict__ ws, int s
 // one CTA of rg::BM threads per (row tile, column); partial layout as the GEMM's
 __global__ void rsplitk_reduce_subtract_kernel(const double* __restrict__ ws, int slices, int64_t stride, int M,
                                                int N, const double* __restrict__ X, double* __restrict__ R,
-                                               double* __restrict__ partial, int dim) {
+                                               double* __restrict__ partial, int dim, int64_t ldx) {
   __shared__ double red[rg::BM / 32];
   const int mt = blockIdx.x, b = blockIdx.y;
   const int m = mt * rg::BM + threadIdx.x;
   double s = 0.0;
   if (m < M) {
-    const int64_t i = static_cast<int64_t>(b) * M + m;
+    const int64_t i = static_cast<int64_t>(b) * M + m;  // the workspace is packed (ld M)
+    const int64_t ix = static_cast<int64_t>(b) * ldx + m;
     double acc = 0.0;
     for (int z = 0; z < slices; ++z) acc += ws[z * stride + i];
-    const double r = X[i] - acc;
-    R[i] = r;
+    const double r = X[ix] - acc;
+    R[ix] = r;
     s = packed_weight(m, dim) * r * r;
   }
   s = warp_sum(s);

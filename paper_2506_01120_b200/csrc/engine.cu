@@ -313,16 +313,20 @@ int split_slices(int64_t tiles, int64_t K) {
 }
 
 // P[n x count] = (1/d) V[:, 0:n]^H X      (ldc = n)
+// (ldv / ldx: element strides of V's and X's columns when they are slices of
+// longer vectors -- the D-sharded closure loop; default D)
 void gemm_project(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, const double2* X, int count,
-                  double2* P, double alpha) {
+                  double2* P, double alpha, int64_t ldv = -1, int64_t ldx = -1) {
   if (n == 0 || count == 0) return;
+  if (ldv < 0) ldv = D;
+  if (ldx < 0) ldx = D;
   gemm_attr_once<true, true, Epilogue::kStoreScaled>();
   dim3 grid((n + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
   Timer t(ctx, 0, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
   int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, D);
   if (slices <= 1) {
     zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
-        static_cast<int>(n), count, static_cast<int>(D), V, D, X, D, P, n, alpha, nullptr, 0, nullptr, 0, 0);
+        static_cast<int>(n), count, static_cast<int>(D), V, ldv, X, ldx, P, n, alpha, nullptr, 0, nullptr, 0, 0);
     launched(ctx);
   } else {
     const int chunk = static_cast<int>(((D + slices - 1) / slices + zg::BK - 1) / zg::BK * zg::BK);
@@ -331,7 +335,7 @@ void gemm_project(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, c
     ctx->splitk_ws.ensure(static_cast<size_t>(slices * stride));
     grid.z = slices;
     zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
-        static_cast<int>(n), count, static_cast<int>(D), V, D, X, D, ctx->splitk_ws.p, n, 1.0, nullptr, 0, nullptr,
+        static_cast<int>(n), count, static_cast<int>(D), V, ldv, X, ldx, ctx->splitk_ws.p, n, 1.0, nullptr, 0, nullptr,
         chunk, stride);
     launched(ctx);
     splitk_reduce_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>((stride + 255) / 256, 1024)), 256, 0,
@@ -343,7 +347,9 @@ void gemm_project(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, c
 
 // R = X - V[:, 0:n] P ; partial[mt][b] = sum_rows |R|^2
 void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, const double2* P, const double2* X,
-                   int count, double2* R, double* partial) {
+                   int count, double2* R, double* partial, int64_t ldv = -1, int64_t ldx = -1) {
+  if (ldv < 0) ldv = D;
+  if (ldx < 0) ldx = D;  // X and R
   gemm_attr_once<false, false, Epilogue::kSubtractNorm>();
   dim3 grid((D + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
   Timer t(ctx, 1, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
@@ -351,7 +357,7 @@ void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, 
   if (slices <= 1) {
     zgemm_dmma_kernel<false, false, Epilogue::kSubtractNorm>
         <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n),
-                                                                       V, D, P, n, R, D, 1.0, X, D, partial, 0, 0);
+                                                                       V, ldv, P, n, R, ldx, 1.0, X, ldx, partial, 0, 0);
     launched(ctx);
   } else {
     gemm_attr_once<false, false, Epilogue::kStoreScaled>();
@@ -362,12 +368,12 @@ void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, 
     grid.z = slices;
     zgemm_dmma_kernel<false, false, Epilogue::kStoreScaled>
         <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n),
-                                                                       V, D, P, n, ctx->splitk_ws.p, D, 1.0, nullptr,
+                                                                       V, ldv, P, n, ctx->splitk_ws.p, D, 1.0, nullptr,
                                                                        0, nullptr, chunk, stride);
     launched(ctx);
     splitk_reduce_subtract_kernel<<<dim3(static_cast<unsigned>((D + zg::BM - 1) / zg::BM), count), zg::BM, 0,
                                     ctx->stream>>>(ctx->splitk_ws.p, slices, stride, static_cast<int>(D), count, X, R,
-                                                   partial);
+                                                   partial, ldx);
     launched(ctx);
   }
   t.stop();
@@ -383,15 +389,17 @@ template <bool KC, REpi E> void rgemm_attr_once() {
 
 // P[n x count] (ld ldp) = alpha * Vw[:, 0:n]^T X   -- beta on the packed path
 void rgemm_project(liecl_b200_ctx* ctx, const double* Vw, int64_t n, int64_t D, const double* X, int count,
-                   double* P, int64_t ldp, double alpha) {
+                   double* P, int64_t ldp, double alpha, int64_t ldv = -1, int64_t ldx = -1) {
   if (n == 0 || count == 0) return;
+  if (ldv < 0) ldv = D;
+  if (ldx < 0) ldx = D;
   rgemm_attr_once<true, REpi::kStoreScaled>();
   dim3 grid((n + rg::BM - 1) / rg::BM, (count + rg::BN - 1) / rg::BN);
   Timer t(ctx, 0, 2.0 * static_cast<double>(n) * static_cast<double>(D) * count);
   int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, D);
   if (slices <= 1) {
     dgemm_dmma_kernel<true, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<true>(), ctx->stream>>>(
-        static_cast<int>(n), count, static_cast<int>(D), Vw, D, X, D, P, ldp, alpha, nullptr, 0, nullptr, 0, 0, 0);
+        static_cast<int>(n), count, static_cast<int>(D), Vw, ldv, X, ldx, P, ldp, alpha, nullptr, 0, nullptr, 0, 0, 0);
     launched(ctx);
   } else {
     const int chunk = static_cast<int>(((D + slices - 1) / slices + rg::BK - 1) / rg::BK * rg::BK);
@@ -401,7 +409,7 @@ void rgemm_project(liecl_b200_ctx* ctx, const double* Vw, int64_t n, int64_t D, 
     double* ws = reinterpret_cast<double*>(ctx->splitk_ws.p);
     grid.z = slices;
     dgemm_dmma_kernel<true, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<true>(), ctx->stream>>>(
-        static_cast<int>(n), count, static_cast<int>(D), Vw, D, X, D, ws, ldp, 1.0, nullptr, 0, nullptr, 0, chunk,
+        static_cast<int>(n), count, static_cast<int>(D), Vw, ldv, X, ldx, ws, ldp, 1.0, nullptr, 0, nullptr, 0, chunk,
         stride);
     launched(ctx);
     rsplitk_reduce_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>((stride + 255) / 256, 1024)), 256, 0,
@@ -413,7 +421,10 @@ void rgemm_project(liecl_b200_ctx* ctx, const double* Vw, int64_t n, int64_t D, 
 
 // R = X - V[:, 0:n] P (P ld ldp); partial[mt][b] = sum_rows w R^2
 void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, const double* P, int64_t ldp,
-                    const double* X, int count, double* R, double* partial, int d) {
+                    const double* X, int count, double* R, double* partial, int d, int64_t ldv = -1,
+                    int64_t ldx = -1) {
+  if (ldv < 0) ldv = D;
+  if (ldx < 0) ldx = D;  // X and R
   rgemm_attr_once<false, REpi::kSubtractNorm>();
   dim3 grid((D + rg::BM - 1) / rg::BM, (count + rg::BN - 1) / rg::BN);
   Timer t(ctx, 1, 2.0 * static_cast<double>(n) * static_cast<double>(D) * count);
@@ -421,7 +432,7 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
   int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, kpad);
   if (slices <= 1) {
     dgemm_dmma_kernel<false, REpi::kSubtractNorm><<<grid, rg::THREADS, rg::smem_bytes<false>(), ctx->stream>>>(
-        static_cast<int>(D), count, static_cast<int>(kpad), V, D, P, ldp, R, D, 1.0, X, D, partial, d, 0, 0);
+        static_cast<int>(D), count, static_cast<int>(kpad), V, ldv, P, ldp, R, ldx, 1.0, X, ldx, partial, d, 0, 0);
     launched(ctx);
   } else {
     rgemm_attr_once<false, REpi::kStoreScaled>();
@@ -432,11 +443,12 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
     double* ws = reinterpret_cast<double*>(ctx->splitk_ws.p);
     grid.z = slices;
     dgemm_dmma_kernel<false, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<false>(), ctx->stream>>>(
-        static_cast<int>(D), count, static_cast<int>(kpad), V, D, P, ldp, ws, D, 1.0, nullptr, 0, nullptr, d, chunk,
+        static_cast<int>(D), count, static_cast<int>(kpad), V, ldv, P, ldp, ws, D, 1.0, nullptr, 0, nullptr, d, chunk,
         stride);
     launched(ctx);
     rsplitk_reduce_subtract_kernel<<<dim3(static_cast<unsigned>((D + rg::BM - 1) / rg::BM), count), rg::BM, 0,
-                                     ctx->stream>>>(ws, slices, stride, static_cast<int>(D), count, X, R, partial, d);
+                                     ctx->stream>>>(ws, slices, stride, static_cast<int>(D), count, X, R, partial, d,
+                                                    ldx);
     launched(ctx);
   }
   t.stop();
@@ -1614,6 +1626,48 @@ int liecl_b200_session_set_shards(liecl_b200_session* s, int32_t nranks, int32_t
     if (nccl_id) red = std::make_unique<NcclReducer>(nccl_id, nranks, rank);
     else red = std::make_unique<HostReducer>(reduce, user);
     s->eng->set_shards(nranks, rank, std::move(red));
+  });
+}
+
+int liecl_b200_session_set_loop_shards(liecl_b200_session* s, int32_t nranks, int32_t rank, const uint8_t* nccl_id,
+                                       liecl_b200_reduce_fn reduce, void* user) {
+  return guarded([&] {
+    if (!s || (!nccl_id && !reduce)) throw Error(LIECL_B200_INVALID_INPUT, "need a session and an NCCL id or a reduce callback");
+    use_device(s->ctx);
+    std::unique_ptr<Reducer> red;
+    if (nccl_id) red = std::make_unique<NcclReducer>(nccl_id, nranks, rank);
+    else red = std::make_unique<HostReducer>(reduce, user);
+    s->eng->set_loop_shards(nranks, rank, std::move(red));
+  });
+}
+
+int liecl_b200_loop_shard_range(int32_t d, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi) {
+  return guarded([&] {
+    if (!lo || !hi || d < 1 || nranks < 1 || rank < 0 || rank >= nranks)
+      throw Error(LIECL_B200_INVALID_INPUT, "bad shard arguments");
+    DenseEngine::loop_shard_range(static_cast<int64_t>(d) * d, d, nranks, rank, *lo, *hi);
+  });
+}
+
+int liecl_b200_session_run_closure(liecl_b200_session* s, const double* gens, int32_t ngens, liecl_b200_stats* stats) {
+  return guarded([&] {
+    if (!s || !gens || !stats) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (ngens <= 0) throw Error(LIECL_B200_INVALID_INPUT, "closure requires a non-empty generator tuple");
+    use_device(s->ctx);
+    const auto t0 = Clock::now();
+    DenseEngine& eng = *s->eng;
+    eng.reset_stats();
+    eng.run_candidates(reinterpret_cast<const double2*>(gens), ngens, false, nullptr, nullptr, true);
+    eng.run_closure_pairs();
+    *stats = eng.stats();
+    stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  });
+}
+
+int liecl_b200_session_warnings(liecl_b200_session* s, char* buf, int64_t len) {
+  return guarded([&] {
+    if (!s || !buf) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    write_warnings(s->eng->warnings(), buf, len);
   });
 }
 

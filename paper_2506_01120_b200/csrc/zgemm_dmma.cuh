@@ -251,22 +251,23 @@ __global__ void splitk_reduce_scale_kernel(const double2* __restrict__ ws, int s
 // its rows, the layout norm_finalize_kernel expects.
 __global__ void splitk_reduce_subtract_kernel(const double2* __restrict__ ws, int slices, int64_t stride, int M,
                                               int N, const double2* __restrict__ X, double2* __restrict__ R,
-                                              double* __restrict__ partial) {
+                                              double* __restrict__ partial, int64_t ldx) {
   __shared__ double red[zg::BM / 32];
   const int mt = blockIdx.x, b = blockIdx.y;
   const int m = mt * zg::BM + threadIdx.x;
   double s = 0.0;
   if (m < M) {
-    const int64_t i = static_cast<int64_t>(b) * M + m;
+    const int64_t i = static_cast<int64_t>(b) * M + m;  // the workspace is packed (ld M)
+    const int64_t ix = static_cast<int64_t>(b) * ldx + m;
     double re = 0.0, im = 0.0;
     for (int z = 0; z < slices; ++z) {
       const double2 v = ws[z * stride + i];
       re += v.x;
       im += v.y;
     }
-    const double2 x = X[i];
+    const double2 x = X[ix];
     const double2 r = make_double2(x.x - re, x.y - im);
-    R[i] = r;
+    R[ix] = r;
     s = r.x * r.x + r.y * r.y;
   }
   s = warp_sum(s);

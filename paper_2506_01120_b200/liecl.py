@@ -948,6 +948,15 @@ def shard_range(d: int, nranks: int, rank: int) -> tuple[int, int]:
     return lo.value, hi.value
 
 
+def loop_shard_range(d: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Elements [lo, hi) whose projections rank `rank` of a D-sharded closure
+    loop computes (multiples of 2(d+1); liecl_b200_loop_shard_range)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(native.load().liecl_b200_loop_shard_range(C.c_int32(d), C.c_int32(nranks), C.c_int32(rank), C.byref(lo),
+                                                     C.byref(hi)))
+    return lo.value, hi.value
+
+
 def _resident_nccl() -> None:
     """Make torch's NCCL the process's libnccl.so.2 before the engine dlopens
     one: a later `import torch` would otherwise bind libtorch_cuda to whichever
@@ -984,7 +993,33 @@ class ClosureSession:
                                                         C.c_int32(d), C.c_int32(int(keep_original)), C.byref(cfg),
                                                         C.byref(self.ptr)))
 
+    def set_loop_shards(self, nranks: int, rank: int, nccl_id: bytes | None = None, reduce=None):
+        """D-shard the closure loop of this (fresh) session: operators stay whole
+        on every rank, the projection GEMMs cover loop_shard_range(d, nranks,
+        rank) only and their partial sums (and each accepted vector's slices)
+        are summed over ranks through NCCL or `reduce` (as set_shards)."""
+        self._set_shards(self.lib.liecl_b200_session_set_loop_shards, nranks, rank, nccl_id, reduce)
+
+    def run_closure(self, gens) -> dict:
+        """The whole closure from `gens` ((ngens, d*d) complex128, full operators):
+        generator loop, then every cursor pair (liecl_b200_session_run_closure)."""
+        gens = np.ascontiguousarray(gens, np.complex128)
+        st = native.Stats()
+        _check(self.lib.liecl_b200_session_run_closure(self.ptr, _dp(gens.view(np.float64)), C.c_int32(len(gens)),
+                                                       C.byref(st)))
+        return st.as_dict()
+
+    def warnings(self) -> list:
+        buf = C.create_string_buffer(1 << 20)
+        _check(self.lib.liecl_b200_session_warnings(self.ptr, buf, C.c_int64(len(buf))))
+        return _parse_warnings(buf.value)
+
     def set_shards(self, nranks: int, rank: int, nccl_id: bytes | None = None, reduce=None):
+        self._set_shards(self.lib.liecl_b200_session_set_shards, nranks, rank, nccl_id, reduce)
+        lo, hi = shard_range(self.d, nranks, rank)
+        self.width = hi - lo
+
+    def _set_shards(self, fn, nranks: int, rank: int, nccl_id: bytes | None = None, reduce=None):
         """D-shard this (fresh) session: it then holds elements shard_range(d, nranks, rank)
         of every operator; overlaps and squared norms are summed over ranks through
         NCCL (`nccl_id` from nccl_unique_id(), shared by the caller) or through
@@ -995,8 +1030,7 @@ class ClosureSession:
                 raise InvalidInputError("an NCCL unique id is 128 bytes")
             _resident_nccl()
             buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
-            _check(self.lib.liecl_b200_session_set_shards(self.ptr, C.c_int32(nranks), C.c_int32(rank), buf,
-                                                          native.ReduceFn(), None))
+            _check(fn(self.ptr, C.c_int32(nranks), C.c_int32(rank), buf, native.ReduceFn(), None))
         elif reduce is not None:
             def trampoline(values, count, _user):
                 try:
@@ -1005,12 +1039,9 @@ class ClosureSession:
                 except Exception:  # reported as a failed reduction by the engine
                     return 1
             self._reduce = native.ReduceFn(trampoline)  # keep alive as long as the session
-            _check(self.lib.liecl_b200_session_set_shards(self.ptr, C.c_int32(nranks), C.c_int32(rank), None,
-                                                          self._reduce, None))
+            _check(fn(self.ptr, C.c_int32(nranks), C.c_int32(rank), None, self._reduce, None))
         else:
             raise InvalidInputError("set_shards needs nccl_id or reduce")
-        lo, hi = shard_range(self.d, nranks, rank)
-        self.width = hi - lo
 
     def close(self):
         if self.ptr:

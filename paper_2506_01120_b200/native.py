@@ -37,6 +37,8 @@ EXPORTED = [
     "liecl_b200_project_residual_pauli", "liecl_b200_linear_combination_pauli", "liecl_b200_overlaps_pauli",
     "liecl_b200_pauli_from_terms", "liecl_b200_scale_terms", "liecl_b200_norm_pauli",
     "liecl_b200_check_matrix_inversion_pauli",
+    "liecl_b200_session_set_loop_shards", "liecl_b200_loop_shard_range", "liecl_b200_session_run_closure",
+    "liecl_b200_session_warnings",
 ]
 
 # int (*liecl_b200_reduce_fn)(double* values, int64_t count, void* user)
