@@ -23,8 +23,14 @@ growth phase on the GPU.
   cpu_baseline: the reference itself (oracle/_ref: unmodified liecl sources +
            Eigen-subset shim) on the same window bytes, all host cores
 
-Multi-GPU (torchrun): weak scaling, each rank checks its own disjoint rows
-against a replicated basis; no collective on the data path.
+Multi-GPU (torchrun, N > 1): the north star's layout -- the D-sharded closure
+loop (liecl_b200_session_set_loop_shards): every rank runs the SAME windows
+with whole operators, the projection GEMMs on 1/N of every vector, and NCCL
+all-reduces of the partial overlaps / squared norms (strong scaling; value =
+the window's brackets / max-over-ranks time). `--c2-mode replicas` instead
+gives each rank its own disjoint rows against a replicated basis (weak
+scaling, no collective); `--c2-mode sharded` runs the sharded engine at N = 1
+too (a one-rank NCCL communicator: the multi-rank code path on one GPU).
 
 `--impl reference` times the reference's own CPU path instead (rank 0 only).
 """
@@ -62,6 +68,8 @@ def parse():
     ap.add_argument("--c3-mode", choices=["auto", "sharded", "replicas"], default="auto",
                     help="c3: one instance D-sharded over the ranks (auto: when N>1; 'sharded' also at N=1, "
                          "through a one-rank NCCL communicator), or one instance per rank")
+    ap.add_argument("--c2-mode", choices=["auto", "sharded", "replicas"], default="auto",
+                    help="c2 over N ranks: the D-sharded closure loop (auto: when N>1), or disjoint rows per rank")
     ap.add_argument("--rows-per-step", type=int, default=8)
     ap.add_argument("--row0", type=int, default=1024)
     ap.add_argument("--cpu-pairs", type=int, default=1024, help="bracket sample for the CPU baseline")
@@ -405,9 +413,27 @@ def run_b200_arm(a):
     def sum_over_ranks(x):
         return reduce_over_ranks(x, "sum", device)
 
+    sharded = a.c2_mode == "sharded" or (a.c2_mode == "auto" and world > 1)
+    if sharded and not launched_by_torchrun:
+        raise SystemExit("--c2-mode sharded needs torchrun (a process group for the NCCL id)")
+    # sharded: every rank runs the same windows (strong scaling); replicas: disjoint rows per rank
+    w_rank, w_world = (0, 1) if sharded else (rank, world)
+
+    def nccl_id():
+        import torch.distributed as dist
+        box = [liecl.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        return box[0]
+
+    def new_session(field):
+        s = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol, field=field), device=local)
+        if sharded:
+            s.set_loop_shards(world, rank, nccl_id=nccl_id())
+        return s
+
     def grown_session(field):
         """Setup (untimed): generator loop + growth phase on the GPU."""
-        s = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol, field=field), device=local)
+        s = new_session(field)
         s.check_candidates(cfg.generators)
         t0 = time.perf_counter()
         g = s.run_rows(1, GROWTH_ROWS)
@@ -418,9 +444,9 @@ def run_b200_arm(a):
     def measure(s, first_step, steps, profile=False):
         """Warm-up + `steps` timed windows; CUDA events on the launching stream."""
         for i in range(a.warmup):
-            s.run_rows(*window_rows(first_step + i, rank, world, a.row0, a.rows_per_step))
+            s.run_rows(*window_rows(first_step + i, w_rank, w_world, a.row0, a.rows_per_step))
         first_step += a.warmup
-        windows = [window_rows(first_step + i, rank, world, a.row0, a.rows_per_step) for i in range(steps)]
+        windows = [window_rows(first_step + i, w_rank, w_world, a.row0, a.rows_per_step) for i in range(steps)]
         native.kernel_times(local)  # reset
         native.set_timing(True, local)
         barrier()
@@ -462,8 +488,18 @@ def run_b200_arm(a):
     peak = fp64_peak_tflops(torch, device)
     windows, my_ms, max_ms, kt, launches, clocks = measure(sess, 0, a.steps, profile=True)
     my_brackets = sum(brackets_in(*wnd) for wnd in windows)
-    total_brackets = sum_over_ranks(my_brackets)
+    # sharded: all ranks checked the same brackets together; replicas: disjoint rows
+    total_brackets = my_brackets if sharded else sum_over_ranks(my_brackets)
     value = total_brackets / (max_ms / 1e3)
+    comm = None
+    if sharded:
+        per_rank_ms = [None] * world
+        import torch.distributed as dist
+        dist.all_gather_object(per_rank_ms, my_ms)
+        comm = {"allreduce_bytes_per_step": sess.comm_bytes() / (a.steps + a.warmup),
+                "per_rank_ms_per_step": [t / a.steps for t in per_rank_ms],
+                "what": "NCCL all-reduce of partial overlaps (8 n B bytes per pass, packed field), partial "
+                        "squared norms (8 B), one 16-byte verdict digest per batch"}
     roof = gemm_roofline(kt, my_ms, peak)
     field = sess.field()
     traffic = load_traffic()
@@ -473,7 +509,7 @@ def run_b200_arm(a):
     if not a.no_e2e:
         host_V = torch.empty((4095, DIM * DIM), dtype=torch.complex128, pin_memory=True)
         host_V.numpy()[:] = sess.basis()
-        sess2 = liecl.ClosureSession(DIM, config=liecl.ClosureConfig(tolerance=cfg.tol), device=local)
+        sess2 = new_session("auto")
         vptr = host_V.data_ptr()
 
         def e2e_step(r0, r1, prefetch_next):
@@ -489,7 +525,7 @@ def run_b200_arm(a):
                 sess2.prefetch_basis(vptr, 4095)
             return sess2.run_rows(r0, r1)
         for s in range(a.warmup):
-            e2e_step(*window_rows(s, rank, world, a.row0, a.rows_per_step), prefetch_next=s + 1 < a.warmup)
+            e2e_step(*window_rows(s, w_rank, w_world, a.row0, a.rows_per_step), prefetch_next=s + 1 < a.warmup)
         barrier()
         torch.cuda.synchronize(device)
         f0 = torch.cuda.Event(enable_timing=True)
@@ -512,10 +548,25 @@ def run_b200_arm(a):
     if not a.no_general:
         gsess, _, _ = grown_session("complex")
         gw, g_my_ms, g_max_ms, gkt, _, _ = measure(gsess, 0, max(2, a.steps // 2))
-        gb = sum_over_ranks(sum(brackets_in(*wnd) for wnd in gw))
+        gb = sum(brackets_in(*wnd) for wnd in gw)
+        gb = gb if sharded else sum_over_ranks(gb)
         general = {"value": gb / (g_max_ms / 1e3), "unit": UNIT, **gemm_roofline(gkt, g_my_ms, peak),
                    "flops_per_unit": "8*N*D per candidate per complex GEMM; commutator 16 d^3"}
         gsess.close()
+
+    # the whole config-2 closure through the sharded engine (every rank takes part)
+    sharded_full = None
+    if sharded and not a.no_secondary:
+        fs = new_session("auto")
+        barrier()
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        st = fs.run_closure(cfg.generators)
+        torch.cuda.synchronize(device)
+        secs = max_over_ranks(time.perf_counter() - t0)
+        sharded_full = {"dimension": st["dimension"], "brackets": st["commutators_evaluated"], "seconds": secs,
+                        "brackets_per_s": st["commutators_evaluated"] / secs, "ranks": world}
+        fs.close()
 
     if rank != 0:
         return
@@ -529,17 +580,22 @@ def run_b200_arm(a):
         cpu = {"value": pairs / secs, "unit": UNIT, "cores": threads, "kind": kind,
                "sample": f"first {pairs} brackets of rows >= {r0} of the same window, same basis bytes "
                          f"({secs:.1f} s)"}
-    secondary = None if a.no_secondary else secondary_closures()
+    secondary = None if (a.no_secondary or sharded) else secondary_closures()
+    if sharded_full is not None:
+        secondary = {"c2_full_closure_sharded": sharded_full}
     packed = field == "antihermitian_packed"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": max_ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": max_ms / a.steps, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None,
         "dtype": "f64" if packed else "c128", "data": "synthetic (seeded SplitMix64 recipe, SURVEY.md §8d)",
         "config": {"workload": "c2_saturated_window", "qubits": D_QUBITS, "d": DIM, "D": DIM * DIM, "basis": 4095,
                    "tol": 1e-10, "rows_per_step": a.rows_per_step, "brackets_per_step_per_gpu": my_brackets / a.steps,
                    "row0": a.row0, "field": field,
                    "l2": "inputs > L2 (basis 134-268 MB + candidate slabs per step)",
-                   "parallelism": f"dp{world}: disjoint closure rows per GPU, basis replicated, no collective",
+                   "parallelism": (f"D-sharded closure loop x{world}: same rows on every GPU, projections on 1/{world} "
+                                   f"of each vector, NCCL all-reduce of partial overlaps and norms" if sharded else
+                                   f"dp{world}: disjoint closure rows per GPU, basis replicated, no collective"),
                    "growth_setup_s": round(growth_s, 3), "growth_batches": grow["batches"]},
         "roofline": {"bound": "tensor",
                      "kernel": ("dgemm_dmma (K2a_r beta=Vw^T C/d + K2b_r R=C-V beta, packed anti-Hermitian, "
@@ -557,6 +613,7 @@ def run_b200_arm(a):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
+        "comm": comm,
         "clocks": clocks,
         "secondary": secondary,
     }

@@ -441,6 +441,8 @@ int liecl_b200_loop_shard_range(int32_t d, int32_t nranks, int32_t rank, int64_t
  * session_warnings, lines "kind\tvalue\tdetail\n"). */
 int liecl_b200_session_run_closure(liecl_b200_session* s, const double* gens, int32_t ngens, liecl_b200_stats* stats);
 int liecl_b200_session_warnings(liecl_b200_session* s, char* buf, int64_t len);
+/* bytes this rank has summed over ranks so far (D-sharded sessions; 0 otherwise) */
+int liecl_b200_session_comm_bytes(const liecl_b200_session* s, uint64_t* bytes);
 
 #ifdef __cplusplus
 }

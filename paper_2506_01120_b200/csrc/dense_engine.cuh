@@ -147,6 +147,7 @@ public:
     force_complex_ = true;
   }
   bool sharded() const { return static_cast<bool>(red_); }
+  uint64_t comm_bytes() const { return red_ ? red_->bytes : 0; }
 
   // D-sharded closure loop (the north star's "basis rows sharded
   // per GPU"): every rank keeps the whole operators (the commutators need

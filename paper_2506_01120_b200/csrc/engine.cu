@@ -1664,6 +1664,13 @@ int liecl_b200_session_run_closure(liecl_b200_session* s, const double* gens, in
   });
 }
 
+int liecl_b200_session_comm_bytes(const liecl_b200_session* s, uint64_t* bytes) {
+  return guarded([&] {
+    if (!s || !bytes) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    *bytes = s->eng->comm_bytes();
+  });
+}
+
 int liecl_b200_session_warnings(liecl_b200_session* s, char* buf, int64_t len) {
   return guarded([&] {
     if (!s || !buf) throw Error(LIECL_B200_INVALID_INPUT, "null argument");

@@ -21,7 +21,14 @@
 struct Reducer {
   virtual ~Reducer() = default;
   // sum `count` doubles of device memory over ranks, in place, ordered on `s`
-  virtual void sum(double* dev, int64_t count, cudaStream_t s) = 0;
+  void sum(double* dev, int64_t count, cudaStream_t s) {
+    if (count > 0) bytes += static_cast<uint64_t>(count) * sizeof(double);
+    do_sum(dev, count, s);
+  }
+  uint64_t bytes = 0;  // payload summed so far (the bench's communication figure)
+
+protected:
+  virtual void do_sum(double* dev, int64_t count, cudaStream_t s) = 0;
 };
 
 struct NcclApi {
@@ -72,7 +79,7 @@ struct NcclReducer final : Reducer {
   ~NcclReducer() override {
     if (comm) nccl_api().comm_destroy(comm);
   }
-  void sum(double* dev, int64_t count, cudaStream_t s) override {
+  void do_sum(double* dev, int64_t count, cudaStream_t s) override {
     if (count <= 0) return;
     nccl_check(nccl_api().all_reduce(dev, dev, static_cast<size_t>(count), ncclFloat64, ncclSum, comm, s),
                "ncclAllReduce");
@@ -86,7 +93,7 @@ struct HostReducer final : Reducer {
   void* user;
   HostBuf<double> h;
   HostReducer(liecl_b200_reduce_fn f, void* u) : fn(f), user(u) {}
-  void sum(double* dev, int64_t count, cudaStream_t s) override {
+  void do_sum(double* dev, int64_t count, cudaStream_t s) override {
     if (count <= 0) return;
     h.ensure(static_cast<size_t>(count));
     CU(cudaMemcpyAsync(h.p, dev, static_cast<size_t>(count) * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -1009,6 +1009,12 @@ class ClosureSession:
                                                        C.byref(st)))
         return st.as_dict()
 
+    def comm_bytes(self) -> int:
+        """Bytes this rank has summed over ranks so far (D-sharded sessions)."""
+        b = C.c_uint64()
+        _check(self.lib.liecl_b200_session_comm_bytes(self.ptr, C.byref(b)))
+        return b.value
+
     def warnings(self) -> list:
         buf = C.create_string_buffer(1 << 20)
         _check(self.lib.liecl_b200_session_warnings(self.ptr, buf, C.c_int64(len(buf))))

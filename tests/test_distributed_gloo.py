@@ -225,3 +225,93 @@ def test_two_d_shards_match_unsharded(tmp_path):
         np.testing.assert_allclose(g["B"], B0[:, int(g["lo"]):int(g["hi"])], atol=1e-13)
         assert bytes(g["token"]) == bytes(range(128))
     assert int(got[0]["hi"]) == int(got[1]["lo"]) and int(got[1]["hi"]) == d * d
+
+
+# ---- D-sharded closure loop (ShardedClosure / set_loop_shards protocol) ----
+
+def loop_shard_model(gens, d, tol, lo, hi, reduce):
+    """numpy model of the engine's D-sharded closure loop: whole operators on
+    every rank (commutators, norms and normalisation computed locally, same
+    bits everywhere); inner products and residual norms over the slice
+    [lo, hi) completed by `reduce`; an accepted vector rebuilt from the
+    ranks' slices by a sum. Cursor order as R:src/closure.cpp:412-460."""
+    V = []
+
+    def ip_slice(a, b):
+        return np.vdot(a[lo:hi], b[lo:hi]) / d
+
+    def project(r):
+        if not V:
+            return r
+        b = np.array([ip_slice(v, r) for v in V]).view(np.float64).copy()
+        reduce(b)
+        return r - np.tensordot(b.view(np.complex128), np.array(V), axes=1)
+
+    def rnorm(r):
+        s = np.array([np.vdot(r[lo:hi], r[lo:hi]).real])
+        reduce(s)
+        return np.sqrt(s[0]) / np.sqrt(d)
+
+    def check_append(h):
+        r = project(project(h))
+        rn = rnorm(r)
+        if rn > tol:
+            full = np.zeros_like(r)
+            full[lo:hi] = r[lo:hi] / rn
+            fv = full.view(np.float64).copy()
+            reduce(fv)  # the other ranks' slices
+            V.append(fv.view(np.complex128))
+        return int(rn > tol)
+
+    log = []
+    for g in gens:
+        n = np.linalg.norm(g) / np.sqrt(d)
+        log.append(check_append(g / n) if n > tol else -1)
+    l = 1
+    while l < len(V):
+        row_start = len(V)
+        for m in range(l):
+            A = V[l].reshape(d, d, order="F")
+            B = V[m].reshape(d, d, order="F")
+            h = (A @ B - B @ A).ravel(order="F")
+            hn = np.linalg.norm(h) / np.sqrt(d)
+            log.append(check_append(h / hn) if hn > tol else -1)
+        assert len(V) >= row_start
+        l += 1
+    return np.array(log), np.array(V)
+
+
+def _loop_problem():
+    rng = np.random.default_rng(9)
+    d = 4
+    mats = []
+    for _ in range(2):
+        H = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+        mats.append((1j * (H + H.conj().T)).ravel(order="F"))
+    return d, np.array(mats)
+
+
+def _loop_worker(rank, world, port, out_dir):
+    from paper_2506_01120_b200 import liecl
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    comm = TorchComm()
+    d, gens = _loop_problem()
+    lo, hi = liecl.loop_shard_range(d, world, rank)  # the engine's bounds (no device call)
+    log, V = loop_shard_model(gens, d, 1e-10, lo, hi, comm.sum_doubles)
+    np.savez(os.path.join(out_dir, f"loop{rank}.npz"), log=log, V=V, lo=lo, hi=hi)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_loop_matches_unsharded(tmp_path):
+    d, gens = _loop_problem()
+    log0, V0 = loop_shard_model(gens, d, 1e-10, 0, d * d, lambda v: None)
+    assert len(V0) == d * d  # two random i*H generate u(4)
+    mp.spawn(_loop_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    got = [np.load(tmp_path / f"loop{r}.npz") for r in range(2)]
+    assert int(got[0]["lo"]) == 0 and int(got[0]["hi"]) == int(got[1]["lo"]) and int(got[1]["hi"]) == d * d
+    assert int(got[0]["hi"]) % (2 * (d + 1)) == 0
+    for g in got:
+        assert np.array_equal(g["log"], log0)  # same verdict sequence
+        np.testing.assert_allclose(g["V"], V0, atol=1e-12)
+    assert np.array_equal(got[0]["V"].view(np.uint64), got[1]["V"].view(np.uint64))  # identical replicas

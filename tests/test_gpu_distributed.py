@@ -62,3 +62,18 @@ def test_bench_under_torchrun():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["gpu_launches"] > 0
+
+
+def test_bench_sharded_loop_under_torchrun():
+    """bench.py's N > 1 path (the D-sharded closure loop over NCCL) at one
+    rank: same windows, strong scaling, the sharded whole closure as secondary."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"), "--gpus", "1",
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-general", "--c2-mode", "sharded"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["scaling"] == "strong" and line["value"] > 0 and line["comm"]["allreduce_bytes_per_step"] > 0
+    full = line["secondary"]["c2_full_closure_sharded"]
+    assert full["dimension"] == 4095 and full["brackets"] == 8382465
+    assert line["e2e"]["value"] > 0
