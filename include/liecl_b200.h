@@ -259,6 +259,14 @@ int liecl_b200_overlaps_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const
 int liecl_b200_pauli_from_terms(liecl_b200_ctx* ctx, int64_t n, const uint64_t* x, const uint64_t* z,
                                 const double* coef, uint32_t qubits, uint64_t* rx, uint64_t* rz, double* rcoef,
                                 int64_t term_cap, int64_t* out_terms);
+/* parse_pauli_sum (R:include/liecl/pauli.hpp, R:src/pauli.cpp:230-395): the
+ * reference's text grammar ("1.5 XIZ - (0,2) YYI + ..."), letter j on qubit
+ * j; the terms are merged by from_terms on the device. LIECL_B200_PARSE with
+ * the reference's message and the 1-based position in *err_line / *err_col
+ * (either may be NULL) on malformed text; qubits <= 31 on this path. */
+int liecl_b200_parse_pauli_sum(liecl_b200_ctx* ctx, const char* text, int64_t len, uint32_t qubits, uint64_t* x,
+                               uint64_t* z, double* coef, int64_t term_cap, int64_t* out_terms, int64_t* err_line,
+                               int64_t* err_col);
 int liecl_b200_scale_terms(liecl_b200_ctx* ctx, int64_t n, const double* coef, double re, double im, double* out);
 int liecl_b200_norm_pauli(liecl_b200_ctx* ctx, int64_t h_terms, const uint64_t* hx, const uint64_t* hz,
                           const double* hcoef, uint32_t qubits, double* out);

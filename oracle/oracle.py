@@ -198,6 +198,19 @@ class Ref:
             C.byref(done), C.byref(nulls), C.byref(ind), C.byref(secs)))
         return {"pairs": done.value, "nulls": nulls.value, "independent": ind.value, "seconds": secs.value}
 
+    def parse_pauli_sum(self, text, qubits, cap=4096):
+        """(x, z, coef) of parse_pauli_sum, or ("error", message, line, column)."""
+        b = text.encode()
+        x, z, c = np.zeros(cap, np.uint64), np.zeros(cap, np.uint64), np.zeros((cap, 2))
+        n, line, col = C.c_int64(), C.c_int64(), C.c_int64()
+        st = self.lib.liecl_ref_parse_pauli_sum(b, C.c_int64(len(b)), C.c_uint(qubits), _p(x, U64P), _p(z, U64P),
+                                                _p(c), C.c_int64(cap), C.byref(n), C.byref(line), C.byref(col))
+        if st == 5:
+            return ("error", self.lib.liecl_ref_last_error().decode(), line.value, col.value)
+        self._check(st)
+        k = n.value
+        return x[:k].copy(), z[:k].copy(), c[:k].copy()
+
     # -- Alg. 2 pieces (ref_harness.cpp) ---------------------------------------
     def last_gram(self, n):
         """result.gram (A, A^-1) of the last closure_* call (matrix inversion)."""

@@ -708,6 +708,28 @@ int liecl_ref_last_gram(std::int64_t n, double* gram_out, double* inverse_out) {
   });
 }
 
+/// parse_pauli_sum (R:src/pauli.cpp:230-395): terms, or the ParseError's
+/// message / line / column (status 5)
+int liecl_ref_parse_pauli_sum(const char* text, std::int64_t len, unsigned qubits, std::uint64_t* x, std::uint64_t* z,
+                              double* coef, std::int64_t cap, std::int64_t* nterms, std::int64_t* line,
+                              std::int64_t* col) {
+  try {
+    const PauliSum s = liecl::parse_pauli_sum(std::string_view(text, static_cast<std::size_t>(len)), qubits);
+    std::int64_t offs[2];
+    *nterms = pauli_out(OperatorTuple{Operator(s)}, offs, x, z, coef, cap);
+    if (*nterms < 0) throw liecl::CapacityError("harness: term output capacity too small");
+    return 0;
+  } catch (const liecl::ParseError& e) {
+    *line = static_cast<std::int64_t>(e.line());
+    *col = static_cast<std::int64_t>(e.column());
+    g_last_error = e.what();
+    return 5;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 1;
+  }
+}
+
 /// Generator catalog (R:src/generators.cpp:132-148) as Pauli term arrays.
 int liecl_ref_build_generators(int family, unsigned qubits, std::uint64_t seed, double delta,
                                std::int64_t* out_offsets, std::uint64_t* out_x,

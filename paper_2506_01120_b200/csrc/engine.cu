@@ -30,6 +30,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <charconv>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -989,6 +990,7 @@ void run_gram_closure(liecl_b200_ctx* ctx, const double* gens, int32_t ngens, in
 }
 
 #include "sum_engine.cuh"
+#include "pauli_text.cuh"
 
 // GramState (R:src/closure.cpp:44-105) and check_matrix_inversion (:107-140)
 // on the device for callers that hold their own state (the drop-in's
@@ -1791,6 +1793,37 @@ int liecl_b200_pauli_from_terms(liecl_b200_ctx* ctx, int64_t n, const uint64_t* 
     SumEngine::Segs r;
     e->from_terms_one(n, x, z, coef, r);
     *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
+    if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+  });
+}
+
+int liecl_b200_parse_pauli_sum(liecl_b200_ctx* ctx, const char* text, int64_t len, uint32_t qubits, uint64_t* x,
+                               uint64_t* z, double* coef, int64_t term_cap, int64_t* out_terms, int64_t* err_line,
+                               int64_t* err_col) {
+  return guarded([&] {
+    if (!ctx || !out_terms || (len > 0 && !text)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (qubits < 1 || qubits > 64)  // R:src/pauli.cpp:383-385
+      throw Error(LIECL_B200_INVALID_INPUT, "parse_pauli_sum: qubit count must be in 1..64");
+    std::vector<PauliTerm> terms;
+    try {
+      terms = PauliTextReader(text, static_cast<size_t>(std::max<int64_t>(len, 0)), qubits).terms();
+    } catch (const PauliTextError& e) {
+      if (err_line) *err_line = e.line;
+      if (err_col) *err_col = e.col;
+      throw Error(LIECL_B200_PARSE, e.msg);
+    }
+    if (qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "the device PauliSum path supports 1..31 qubits");
+    use_device(ctx);
+    const int64_t n = static_cast<int64_t>(terms.size());
+    std::vector<uint64_t> tx(static_cast<size_t>(n)), tz(static_cast<size_t>(n));
+    std::vector<double> tc(static_cast<size_t>(2 * n));
+    for (int64_t t = 0; t < n; ++t) {
+      tx[t] = terms[t].x, tz[t] = terms[t].z, tc[2 * t] = terms[t].re, tc[2 * t + 1] = terms[t].im;
+    }
+    auto e = pauli_tuple(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
+    SumEngine::Segs r;
+    e->from_terms_one(n, tx.data(), tz.data(), tc.data(), r);  // PauliSum::from_terms (R:src/pauli.cpp:78-115)
+    *out_terms = e->download_one(r, x, z, coef, term_cap);
     if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
   });
 }

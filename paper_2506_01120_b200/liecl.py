@@ -532,6 +532,26 @@ def pauli_sum_from_terms(qubits: int, terms) -> PauliSum:
     return _sum_from_arrays(qubits, rx, rz, rc, nt.value)
 
 
+def parse_pauli_sum(text: str, qubits: int, device: int = 0) -> PauliSum:
+    """parse_pauli_sum (R:src/pauli.cpp:230-395): the reference's grammar, e.g.
+    "1.5 XIZ - (0,2) YYI"; letter j acts on qubit j. Malformed text raises
+    ParseError with the reference's message and .line / .column."""
+    b = text.encode()
+    cap = max(1, b.count(b"X") + b.count(b"Y") + b.count(b"Z") + b.count(b"I"))
+    x, z, c = np.zeros(cap, np.uint64), np.zeros(cap, np.uint64), np.zeros((cap, 2))
+    n, line, col = C.c_int64(), C.c_int64(), C.c_int64()
+    u64 = C.POINTER(C.c_uint64)
+    st = native.load().liecl_b200_parse_pauli_sum(native.context(device), b, C.c_int64(len(b)), C.c_uint32(qubits),
+                                                  x.ctypes.data_as(u64), z.ctypes.data_as(u64), _dp(c),
+                                                  C.c_int64(cap), C.byref(n), C.byref(line), C.byref(col))
+    if st == native.PARSE:
+        e = ParseError(f"{native.last_error()} (line {line.value}, column {col.value})")
+        e.line, e.column = line.value, col.value
+        raise e
+    _check(st)
+    return _sum_from_arrays(qubits, x, z, c, n.value)
+
+
 def from_pauli(sums, device: int = 0):
     """Dense expansion on the GPU, bit-exact with R:src/dense.cpp:70-98. Takes
     one PauliSum or a list (terms in PauliSum order); returns DenseOperator(s)."""

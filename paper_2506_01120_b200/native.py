@@ -38,7 +38,7 @@ EXPORTED = [
     "liecl_b200_pauli_from_terms", "liecl_b200_scale_terms", "liecl_b200_norm_pauli",
     "liecl_b200_check_matrix_inversion_pauli",
     "liecl_b200_session_set_loop_shards", "liecl_b200_loop_shard_range", "liecl_b200_session_run_closure",
-    "liecl_b200_session_warnings", "liecl_b200_session_comm_bytes",
+    "liecl_b200_session_warnings", "liecl_b200_session_comm_bytes", "liecl_b200_parse_pauli_sum",
 ]
 
 # int (*liecl_b200_reduce_fn)(double* values, int64_t count, void* user)

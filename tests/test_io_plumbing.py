@@ -73,3 +73,33 @@ def test_device_from_pauli_bit_exact(ref):
         assert np.array_equal(got.view(np.uint64), cfg.generators.view(np.uint64))
     with pytest.raises(liecl.CapacityError):
         liecl.from_pauli(liecl.PauliSum(13, [(liecl.PauliString(1, 0, 13), 1.0)]))
+
+
+PARSE_CASES = [
+    ("1.5 XIZ - (0,2) YYI + 0.25 XIZ", 3),
+    ("  -2e-3 ZZ\n+ (1e2, -3.5E+1)   XY - 1 II ", 2),
+    ("3 X", 1),
+    ("(0.5,0.5) IXYZ - (0.5,0.5) IXYZ + 1 ZZZZ", 4),  # an exact cancellation drops the term
+    ("1e-20 XX + 1 ZZ", 2),  # below the 1e-14 relative drop floor
+    ("", 2), ("   ", 2), ("1.5", 2), ("1.5XX", 2), ("1.5 XQ", 2), ("1.5 XXX", 2), ("1.5 X", 2),
+    ("1 XX * 2 ZZ", 2), ("(1 2) XX", 2), ("(1,2 XX", 2), ("1..2 XX", 2), ("1 XX +", 2), ("1 XX\n - e ZZ", 2),
+    ("+ 1 XX", 2), ("1 XX - - 2 ZZ", 2),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("text,qubits", PARSE_CASES)
+def test_parse_pauli_sum_matches_reference(ref_exact, text, qubits):
+    """parse_pauli_sum (R:src/pauli.cpp:230-395): the same terms, bit for bit,
+    or the same ParseError (message, line, column)."""
+    want = ref_exact.parse_pauli_sum(text, qubits)
+    if isinstance(want, tuple) and want and want[0] == "error":
+        with pytest.raises(liecl.ParseError) as e:
+            liecl.parse_pauli_sum(text, qubits)
+        assert str(e.value) == want[1] and (e.value.line, e.value.column) == (want[2], want[3])
+        return
+    got = liecl.parse_pauli_sum(text, qubits)
+    x, z, c = want
+    assert [(s.x, s.z) for s, _ in got.terms] == list(zip(x.tolist(), z.tolist()))
+    mine = np.array([[v.real, v.imag] for _, v in got.terms]).reshape(-1, 2)
+    assert np.array_equal(mine.view(np.uint64), c.view(np.uint64))
