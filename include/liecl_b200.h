@@ -267,6 +267,19 @@ int liecl_b200_pauli_from_terms(liecl_b200_ctx* ctx, int64_t n, const uint64_t* 
 int liecl_b200_parse_pauli_sum(liecl_b200_ctx* ctx, const char* text, int64_t len, uint32_t qubits, uint64_t* x,
                                uint64_t* z, double* coef, int64_t term_cap, int64_t* out_terms, int64_t* err_line,
                                int64_t* err_col);
+/* realize_generators (R:include/liecl/generators.hpp; R:src/generators.cpp:
+ * 9-110, 171-194): the catalog family (0 hea, 1 spin_glass_hva, 2 xxz_hva,
+ * 3 tfim_hva_open; seed for spin_glass_hva, delta for xxz_hva) as *count
+ * generators. dense = 0: Pauli sums (PauliSum form, merged on the device) in
+ * offsets (count + 1 entries) / x / z / coef (term_cap terms); dense = 1 or
+ * restrict_zero_magnetization (xxz_hva only): from_pauli on the device, then
+ * the C(n, n/2) zero-magnetization submatrix, as *dim x *dim complex
+ * operators in dense_out (dense_cap doubles). Bit-exact with the reference;
+ * Pauli qubits <= 31, dense <= 12. */
+int liecl_b200_realize_generators(liecl_b200_ctx* ctx, int32_t family, uint32_t qubits, uint64_t seed, double delta,
+                                  int32_t restrict_zero_magnetization, int32_t dense, int32_t* count,
+                                  int64_t* offsets, uint64_t* x, uint64_t* z, double* coef, int64_t term_cap,
+                                  int32_t* dim, double* dense_out, int64_t dense_cap);
 int liecl_b200_scale_terms(liecl_b200_ctx* ctx, int64_t n, const double* coef, double re, double im, double* out);
 int liecl_b200_norm_pauli(liecl_b200_ctx* ctx, int64_t h_terms, const uint64_t* hx, const uint64_t* hz,
                           const double* hcoef, uint32_t qubits, double* out);

@@ -198,6 +198,16 @@ class Ref:
             C.byref(done), C.byref(nulls), C.byref(ind), C.byref(secs)))
         return {"pairs": done.value, "nulls": nulls.value, "independent": ind.value, "seconds": secs.value}
 
+    def realize_generators_dense(self, family, qubits, seed=0, delta=1.5, restrict=False):
+        cap = 1 << 26
+        out = np.zeros(cap // 2, np.complex128)
+        cnt, dim = C.c_int64(), C.c_int64()
+        self._check(self.lib.liecl_ref_realize_generators_dense(
+            C.c_int(FAMILIES[family]), C.c_uint(qubits), C.c_uint64(seed), C.c_double(delta), C.c_int(int(restrict)),
+            _p(out.view(np.float64)), C.c_int64(cap), C.byref(cnt), C.byref(dim)))
+        k, m = cnt.value, dim.value
+        return out[: k * m * m].reshape(k, m * m).copy(), m
+
     def parse_pauli_sum(self, text, qubits, cap=4096):
         """(x, z, coef) of parse_pauli_sum, or ("error", message, line, column)."""
         b = text.encode()

@@ -749,6 +749,27 @@ int liecl_ref_build_generators(int family, unsigned qubits, std::uint64_t seed, 
   });
 }
 
+/// realize_generators on the dense backend (R:src/generators.cpp:171-194),
+/// with or without the zero-magnetization restriction
+int liecl_ref_realize_generators_dense(int family, unsigned qubits, std::uint64_t seed, double delta, int restrict_zm,
+                                       double* out, std::int64_t cap, std::int64_t* count, std::int64_t* dim) {
+  return guarded([&] {
+    liecl::AnsatzSpec spec;
+    spec.family = static_cast<liecl::AnsatzFamily>(family);
+    spec.qubits = qubits;
+    spec.seed = seed;
+    spec.delta = delta;
+    spec.restrict_zero_magnetization = restrict_zm != 0;
+    const OperatorTuple ops = liecl::realize_generators(spec, liecl::Backend::dense);
+    *count = static_cast<std::int64_t>(ops.size());
+    const int d = static_cast<int>(ops[0].dim());
+    *dim = d;
+    if (static_cast<std::int64_t>(ops.size()) * 2 * d * d > cap)
+      throw liecl::CapacityError("harness: output capacity too small");
+    for (std::size_t i = 0; i < ops.size(); ++i) dense_to(ops[i], out + i * 2 * static_cast<std::size_t>(d) * d, d);
+  });
+}
+
 /// format_pauli_sum / parse round trip helper (R:src/pauli.cpp:390-422).
 int liecl_ref_format_pauli(const std::uint64_t* x, const std::uint64_t* z, const double* coef,
                            std::int64_t nterms, unsigned qubits, char* buf, std::int64_t len) {

@@ -1828,6 +1828,95 @@ int liecl_b200_parse_pauli_sum(liecl_b200_ctx* ctx, const char* text, int64_t le
   });
 }
 
+int liecl_b200_realize_generators(liecl_b200_ctx* ctx, int32_t family, uint32_t qubits, uint64_t seed, double delta,
+                                  int32_t restrict_zero_magnetization, int32_t dense, int32_t* count,
+                                  int64_t* offsets, uint64_t* x, uint64_t* z, double* coef, int64_t term_cap,
+                                  int32_t* dim, double* dense_out, int64_t dense_cap) {
+  return guarded([&] {
+    if (!ctx || !count) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (restrict_zero_magnetization && family != 2)  // R:src/generators.cpp:172-175
+      throw Error(LIECL_B200_INVALID_INPUT, "zero-magnetization restriction is an xxz_hva option");
+    const auto gens = catalog_terms(family, qubits, seed, delta);
+    if (qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "the device PauliSum path supports 1..31 qubits");
+    use_device(ctx);
+    const int32_t ng = static_cast<int32_t>(gens.size());
+    *count = ng;
+    // PauliSum::from_terms of every generator (device)
+    auto e = pauli_tuple(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
+    std::vector<int64_t> off(1, 0);
+    std::vector<uint64_t> sx, sz;
+    std::vector<double> sc;
+    for (const auto& g : gens) {
+      const int64_t n = static_cast<int64_t>(g.size());
+      std::vector<uint64_t> tx(n), tz(n);
+      std::vector<double> tc(2 * n);
+      for (int64_t t = 0; t < n; ++t) tx[t] = g[t].x, tz[t] = g[t].z, tc[2 * t] = g[t].re, tc[2 * t + 1] = g[t].im;
+      SumEngine::Segs r;
+      e->from_terms_one(n, tx.data(), tz.data(), tc.data(), r);
+      const int64_t base = off.back();
+      sx.resize(base + r.total), sz.resize(base + r.total), sc.resize(2 * (base + r.total));
+      e->download_one(r, sx.data() + base, sz.data() + base, sc.data() + 2 * base, r.total);
+      off.push_back(base + r.total);
+    }
+    if (!dense && !restrict_zero_magnetization) {
+      if (!offsets) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+      std::copy(off.begin(), off.end(), offsets);
+      if (off.back() > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+      if (off.back() > 0 && (!x || !z || !coef)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+      std::copy(sx.begin(), sx.end(), x);
+      std::copy(sz.begin(), sz.end(), z);
+      std::copy(sc.begin(), sc.end(), coef);
+      return;
+    }
+    // dense: from_pauli (R:src/dense.cpp:70-98) on the device, then the
+    // zero-magnetization restriction when asked (R:src/dense.cpp:167-199)
+    if (qubits > 12)
+      throw Error(LIECL_B200_CAPACITY, "from_pauli: " + std::to_string(qubits) +
+                                           " qubits exceeds the expansion limit of 12");
+    const int64_t d = int64_t(1) << qubits;
+    std::vector<int64_t> states;
+    if (restrict_zero_magnetization)
+      for (int64_t st = 0; st < d; ++st)
+        if (__builtin_popcountll(static_cast<unsigned long long>(st)) == static_cast<int>(qubits / 2))
+          states.push_back(st);
+    const int64_t m = restrict_zero_magnetization ? static_cast<int64_t>(states.size()) : d;
+    if (dim) *dim = static_cast<int32_t>(m);
+    if (!dense_out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+    if (ng * m * m * 2 > dense_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    DevBuf<int64_t> doff, dst;
+    DevBuf<uint64_t> dx, dz;
+    DevBuf<double2> dc, full, sub;
+    const int64_t terms = off.back();
+    doff.ensure(ng + 1);
+    dx.ensure(std::max<int64_t>(terms, 1));
+    dz.ensure(std::max<int64_t>(terms, 1));
+    dc.ensure(std::max<int64_t>(terms, 1));
+    full.ensure(static_cast<size_t>(ng * d * d));
+    CU(cudaMemcpyAsync(doff.p, off.data(), (ng + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (terms > 0) {
+      CU(cudaMemcpyAsync(dx.p, sx.data(), terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(dz.p, sz.data(), terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(dc.p, sc.data(), terms * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    from_pauli_kernel<<<static_cast<unsigned>(std::min<int64_t>((ng * d + 127) / 128, 4096)), 128, 0, ctx->stream>>>(
+        doff.p, dx.p, dz.p, dc.p, ng, static_cast<int>(qubits), full.p);
+    launched(ctx);
+    const double2* res = full.p;
+    if (restrict_zero_magnetization) {
+      dst.ensure(static_cast<size_t>(m));
+      sub.ensure(static_cast<size_t>(ng * m * m));
+      CU(cudaMemcpyAsync(dst.p, states.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+      restrict_states_kernel<<<static_cast<unsigned>(std::min<int64_t>((ng * m * m + 255) / 256, 4096)), 256, 0,
+                               ctx->stream>>>(full.p, ng, d, dst.p, m, sub.p);
+      launched(ctx);
+      res = sub.p;
+    }
+    CU(cudaMemcpyAsync(dense_out, res, static_cast<size_t>(ng * m * m) * sizeof(double2), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int liecl_b200_scale_terms(liecl_b200_ctx* ctx, int64_t n, const double* coef, double re, double im, double* out) {
   return guarded([&] {
     if (!ctx || n < 0 || (n > 0 && (!coef || !out))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");

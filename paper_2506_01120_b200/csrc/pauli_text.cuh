@@ -130,3 +130,60 @@ private:
   size_t i_ = 0;
   int64_t line_ = 1, col_ = 1;
 };
+
+// ---- the generator catalog (R:src/generators.cpp:9-110, 132-148) -----------
+// Term lists only (strings and real coefficients, in the reference's order);
+// the sums are merged by from_terms and expanded by from_pauli on the device.
+// SplitMix64 and uniform_symmetric as R:include/liecl/rng.hpp:20-39.
+struct CatalogRng {
+  uint64_t state;
+  uint64_t next() {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  double symmetric() { return 2.0 * (static_cast<double>(next() >> 11) * 0x1.0p-53) - 1.0; }
+};
+
+// family: 0 hea, 1 spin_glass_hva, 2 xxz_hva, 3 tfim_hva_open (liecl::AnsatzFamily)
+inline std::vector<std::vector<PauliTerm>> catalog_terms(int family, uint32_t n, uint64_t seed, double delta) {
+  static const char* names[] = {"hea", "spin_glass_hva", "xxz_hva", "tfim_hva_open"};
+  if (family < 0 || family > 3) throw Error(LIECL_B200_INVALID_INPUT, "build_generators: unknown family");
+  if (n < 2) throw Error(LIECL_B200_INVALID_INPUT, std::string(names[family]) + " requires at least 2 qubits");
+  if (family == 2 && n % 2 != 0)
+    throw Error(LIECL_B200_INVALID_INPUT, std::string(names[family]) + " requires an even qubit count");
+  if (n > 64) throw Error(LIECL_B200_INVALID_INPUT, "qubit count above the 64-qubit mask width");
+  auto bit = [](uint32_t q) { return uint64_t(1) << q; };
+  std::vector<std::vector<PauliTerm>> g;
+  if (family == 0) {  // X_i, Z_i, Z_i Z_{i+1}: one term per generator
+    for (uint32_t i = 0; i < n; ++i) g.push_back({{bit(i), 0, 1.0, 0.0}});
+    for (uint32_t i = 0; i < n; ++i) g.push_back({{0, bit(i), 1.0, 0.0}});
+    for (uint32_t i = 0; i + 1 < n; ++i) g.push_back({{0, bit(i) | bit(i + 1), 1.0, 0.0}});
+  } else if (family == 1) {  // a_i Z_i, then J_ij Z_i Z_j (i < j); sum_i X_i
+    CatalogRng rng{seed};
+    std::vector<PauliTerm> h1, h2;
+    for (uint32_t i = 0; i < n; ++i) h1.push_back({0, bit(i), rng.symmetric(), 0.0});
+    for (uint32_t i = 0; i < n; ++i)
+      for (uint32_t j = i + 1; j < n; ++j) h1.push_back({0, bit(i) | bit(j), rng.symmetric(), 0.0});
+    for (uint32_t i = 0; i < n; ++i) h2.push_back({bit(i), 0, 1.0, 0.0});
+    g = {h1, h2};
+  } else if (family == 2) {  // even / odd bonds of XX + YY + delta ZZ, periodic
+    for (uint32_t parity = 0; parity < 2; ++parity) {
+      std::vector<PauliTerm> h;
+      for (uint32_t i = parity; i < n; i += 2) {
+        const uint64_t b = bit(i) | bit((i + 1) % n);
+        h.push_back({b, 0, 1.0, 0.0});
+        h.push_back({b, b, 1.0, 0.0});
+        h.push_back({0, b, delta, 0.0});
+      }
+      g.push_back(h);
+    }
+  } else {  // open ZZ chain; sum_i X_i
+    std::vector<PauliTerm> h1, h2;
+    for (uint32_t i = 0; i + 1 < n; ++i) h1.push_back({0, bit(i) | bit(i + 1), 1.0, 0.0});
+    for (uint32_t i = 0; i < n; ++i) h2.push_back({bit(i), 0, 1.0, 0.0});
+    g = {h1, h2};
+  }
+  return g;
+}

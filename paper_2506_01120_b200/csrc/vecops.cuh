@@ -62,6 +62,20 @@ __global__ void from_pauli_kernel(const int64_t* __restrict__ offsets, const uin
   }
 }
 
+// restrict_to_subspace with the zero-magnetization projector (R:src/dense.cpp:
+// 167-199): B^H A B for a 0/1 column-selection basis B is the submatrix
+// A(s_i, s_j) over the selected basis states s (ascending). count operators,
+// full dimension d, m selected states.
+__global__ void restrict_states_kernel(const double2* __restrict__ A, int64_t count, int64_t d,
+                                       const int64_t* __restrict__ states, int64_t m, double2* __restrict__ out) {
+  const int64_t mm = m * m;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count * mm;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / mm, k = e % mm, i = k % m, j = k / m;
+    out[e] = A[c * d * d + states[j] * d + states[i]];
+  }
+}
+
 // dst[j] = src[idx[j]] for columns of W doubles (either field).
 __global__ void gather_words_kernel(const double* __restrict__ src, const int* __restrict__ idx, int64_t W,
                                     double* __restrict__ dst) {

@@ -532,6 +532,41 @@ def pauli_sum_from_terms(qubits: int, terms) -> PauliSum:
     return _sum_from_arrays(qubits, rx, rz, rc, nt.value)
 
 
+FAMILIES = {"hea": 0, "spin_glass_hva": 1, "xxz_hva": 2, "tfim_hva_open": 3}
+
+
+def realize_generators(family: str, qubits: int, backend: Backend = Backend.pauli, seed: int = 0,
+                       delta: float = 1.5, restrict_zero_magnetization: bool = False, device: int = 0) -> list:
+    """realize_generators (R:src/generators.cpp:171-194) through the C-ABI: the
+    catalog family as PauliSums, or dense operators (from_pauli on the device;
+    the zero-magnetization restriction implies dense)."""
+    if family not in FAMILIES:
+        raise InvalidInputError(f"unknown ansatz family '{family}'")
+    lib = native.load()
+    count = C.c_int32()
+    dense = backend == Backend.dense or restrict_zero_magnetization
+    u64, i64 = C.POINTER(C.c_uint64), C.POINTER(C.c_int64)
+    if not dense:
+        cap = 4 * qubits * qubits + 64
+        off = np.zeros(3 * qubits + 1, np.int64)
+        x, z, c = np.zeros(cap, np.uint64), np.zeros(cap, np.uint64), np.zeros((cap, 2))
+        _check(lib.liecl_b200_realize_generators(
+            native.context(device), C.c_int32(FAMILIES[family]), C.c_uint32(qubits), C.c_uint64(seed),
+            C.c_double(delta), C.c_int32(0), C.c_int32(0), C.byref(count), off.ctypes.data_as(i64),
+            x.ctypes.data_as(u64), z.ctypes.data_as(u64), _dp(c), C.c_int64(cap), None, None, C.c_int64(0)))
+        return [_sum_from_arrays(qubits, x[off[i]:], z[off[i]:], c[off[i]:], int(off[i + 1] - off[i]))
+                for i in range(count.value)]
+    d = 1 << qubits
+    out = np.zeros(max(3 * qubits - 1, 2) * d * d, np.complex128)
+    dim = C.c_int32()
+    _check(lib.liecl_b200_realize_generators(
+        native.context(device), C.c_int32(FAMILIES[family]), C.c_uint32(qubits), C.c_uint64(seed), C.c_double(delta),
+        C.c_int32(int(restrict_zero_magnetization)), C.c_int32(1), C.byref(count), None, None, None, None,
+        C.c_int64(0), C.byref(dim), _dp(out.view(np.float64)), C.c_int64(2 * len(out))))
+    m = dim.value
+    return [DenseOperator.from_vec(out[i * m * m:(i + 1) * m * m], m) for i in range(count.value)]
+
+
 def parse_pauli_sum(text: str, qubits: int, device: int = 0) -> PauliSum:
     """parse_pauli_sum (R:src/pauli.cpp:230-395): the reference's grammar, e.g.
     "1.5 XIZ - (0,2) YYI"; letter j acts on qubit j. Malformed text raises

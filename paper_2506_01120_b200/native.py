@@ -39,6 +39,7 @@ EXPORTED = [
     "liecl_b200_check_matrix_inversion_pauli",
     "liecl_b200_session_set_loop_shards", "liecl_b200_loop_shard_range", "liecl_b200_session_run_closure",
     "liecl_b200_session_warnings", "liecl_b200_session_comm_bytes", "liecl_b200_parse_pauli_sum",
+    "liecl_b200_realize_generators",
 ]
 
 # int (*liecl_b200_reduce_fn)(double* values, int64_t count, void* user)
