@@ -78,6 +78,9 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-general", action="store_true", help="skip the general-complex-path comparison")
+    ap.add_argument("--no-same-bytes", action="store_true",
+                    help="skip timing the reference arm's basis bytes (random su(64)) on the GPU")
+    ap.add_argument("--cpu-pairs-1t", type=int, default=48, help="bracket sample for the threads=1 CPU baseline")
     return ap.parse_args()
 
 
@@ -168,17 +171,39 @@ class ClockSampler:
 # ---------------------------------------------------------- reference arm --
 
 def random_saturated_basis(d=DIM, seed=0):
-    """Seeded orthonormal basis of the traceless d x d matrices (vec layout,
-    orthonormal under <a,b> = vdot(a,b)/d): the same shape and per-bracket work
-    as the config-2 saturated basis (every bracket non-null, every check a
-    reject)."""
+    """Seeded orthonormal basis of su(d) -- anti-Hermitian traceless d x d
+    matrices, orthonormal under <a,b> = vdot(a,b)/d (R:src/dense.cpp:53-59) --
+    in the complex vec layout: the class of basis config 2 saturates to (its
+    d^2 - 1 = 4095 elements span su(64)), with the same per-bracket work
+    (every bracket non-null, every check a reject). Built in the packed real
+    coordinates of an anti-Hermitian matrix (M(i,j) = Re A(i,j), M(j,i) =
+    Im A(i,j) for i < j, M(i,i) = Im A(i,i)), where the inner product is
+    (1/d) sum_k w_k M_A(k) M_B(k), w = 2 off the diagonal, 1 on it: a seeded
+    Gaussian matrix, its trace direction removed, QR in the scaled
+    coordinates y = sqrt(w/d) M."""
     rng = np.random.default_rng(seed)
     D = d * d
-    M = rng.standard_normal((D, D - 1)) + 1j * rng.standard_normal((D, D - 1))
-    ident = np.eye(d).ravel(order="F")
-    M -= np.outer(ident, ident @ M) / d
-    q, _ = np.linalg.qr(M)
-    return np.ascontiguousarray(q.T * np.sqrt(d))
+    k = np.arange(D)
+    diag = (k % (d + 1)) == 0
+    scale = np.sqrt(np.where(diag, 1.0, 2.0) / d)  # y = scale * M
+    G = rng.standard_normal((D, D - 1))
+    u = diag / np.sqrt(d)  # the trace direction (unit) in y coordinates
+    G -= np.outer(u, u @ G)
+    Q, _ = np.linalg.qr(G)
+    M = Q.T / scale  # (D - 1) x D packed matrices, column-major (i, j) = (k % d, k // d)
+    i, j = k % d, k // d
+    up = i < j
+    A = np.zeros((D - 1, D), np.complex128)
+    kt = i * d + j  # element (j, i): row j, column i
+    A[:, k[up]] = M[:, k[up]] + 1j * M[:, kt[up]]
+    A[:, kt[up]] = -M[:, k[up]] + 1j * M[:, kt[up]]
+    A[:, k[diag]] = 1j * M[:, k[diag]]
+    return np.ascontiguousarray(A)
+
+
+def basis_digest(V) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(V).tobytes()).hexdigest()[:16]
 
 
 def cpu_reference(V, pairs, row, threads):
@@ -218,8 +243,11 @@ def run_reference_arm(a):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * total_s / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": "c2_saturated_window", "qubits": D_QUBITS, "d": DIM, "basis": 4095,
-                       "tol": 1e-10, "basis_source": "seeded random orthonormal traceless basis (numpy QR)"},
+            "config": {"workload": "c2_saturated_window", "qubits": D_QUBITS, "d": DIM, "D": DIM * DIM, "basis": 4095,
+                       "tol": 1e-10, "basis_class": "orthonormal basis of su(64) (anti-Hermitian, traceless)",
+                       "basis_source": "random_saturated_basis(seed 0): the bytes the B200 arm also times "
+                                       "(its 'same_bytes_as_reference' line)",
+                       "basis_sha16": basis_digest(V)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                              "sample": f"{a.ref_pairs} brackets per step from rows >= {a.row0}, {a.steps} steps"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -543,6 +571,24 @@ def run_b200_arm(a):
                "path": "liecl_b200_session_set_basis(host pinned) + liecl_b200_session_run_rows; the next "
                        "step's basis H2D (liecl_b200_session_prefetch_basis) overlaps the current window"}
 
+    # ---- the reference arm's basis bytes (random su(64), random_saturated_basis):
+    # the same windows timed on exactly what `--impl reference` times
+    same_bytes = None
+    if not a.no_same_bytes:
+        Vr = random_saturated_basis()
+        rs = new_session("auto")
+        rs.set_basis(Vr)
+        _, r_my_ms, r_max_ms, rkt, _, _ = measure(rs, 0, max(2, a.steps // 2))
+        rb = sum(brackets_in(*wnd) for wnd in
+                 [window_rows(a.warmup + i, w_rank, w_world, a.row0, a.rows_per_step)
+                  for i in range(max(2, a.steps // 2))])
+        rb = rb if sharded else sum_over_ranks(rb)
+        same_bytes = {"value": rb / (r_max_ms / 1e3), "unit": UNIT, "basis_sha16": basis_digest(Vr),
+                      "field": rs.field(), **gemm_roofline(rkt, r_my_ms, peak),
+                      "basis_source": "random_saturated_basis(seed 0), the reference arm's bytes"}
+        rs.close()
+        del Vr
+
     # ---- the general complex path on the same windows (for comparison)
     general = None
     if not a.no_general:
@@ -580,6 +626,11 @@ def run_b200_arm(a):
         cpu = {"value": pairs / secs, "unit": UNIT, "cores": threads, "kind": kind,
                "sample": f"first {pairs} brackets of rows >= {r0} of the same window, same basis bytes "
                          f"({secs:.1f} s)"}
+        # threads = 1 as well ("also run with threads = 1")
+        p1, s1, k1, i1 = cpu_reference(V, a.cpu_pairs_1t, r0, 1)
+        assert i1 == 0
+        cpu["threads_1"] = {"value": p1 / s1, "unit": UNIT, "cores": 1, "kind": k1,
+                            "sample": f"first {p1} brackets of rows >= {r0}, same basis bytes ({s1:.1f} s)"}
     secondary = None if (a.no_secondary or sharded) else secondary_closures()
     if sharded_full is not None:
         secondary = {"c2_full_closure_sharded": sharded_full}
@@ -609,6 +660,7 @@ def run_b200_arm(a):
                      "peak_source": "measured in-run: cuBLAS ZGEMM 4096^3 via torch.matmul complex128 "
                                     "(MEASURED_PEAKS.json has no FP64 entry)",
                      "commutator_ms": roof["commutator_ms"], "commutator_tflops": roof["commutator_tflops"]},
+        "same_bytes_as_reference": same_bytes,
         "general_complex_path": general,
         "cpu_baseline": cpu,
         "e2e": e2e,
