@@ -1,0 +1,242 @@
+// In-block decisions from the Gram matrix of the block (the
+// re-check rule of R:src/closure.cpp:440-444), replacing the per-survivor
+// grid-synchronised walk of block_gs.cuh on the common path.
+//
+// A block holds up to 64 survivors y_0..y_{nb-1} (residuals already
+// re-projected against everything accepted before the block, norms rn2). In
+// cursor order, survivor q is decided from rn2_q when nothing was accepted
+// earlier in the block, else from its CGS2 residual against the block's
+// earlier accepts. With G = <y_i, y_j> (one GEMM) that residual's square is
+// the Schur complement s_q = G_qq - sum_a |Z_aq|^2 of a Cholesky factor grown
+// one accept at a time (Z = R of the QR of the accepted survivors, extended to
+// every later column): O(64^2) work per accept in one CTA.
+//
+// s_q is exact to ~eps * G_qq, so it CERTIFIES an accept when s_q clears
+// 1e-4 G_qq and (100 tol)^2 -- the residual is then far above tol, not
+// borderline, and the accepted set well conditioned. A smaller s_q cannot separate 1e-15 from 1e-9: the survivor is
+// a TENTATIVE reject, confirmed afterwards by its explicit CGS2 residual
+// against exactly the accepts before it (a masked two-pass projection); if
+// any explicit residual exceeds tol, the caller redoes the block with the
+// exact per-survivor kernel. The accepted vectors are formed by CholQR2 --
+// W = Y_A R1^-1, then Q = W R2^-1 with R2 from the Cholesky of W^H W --
+// the same Q as sequential Gram-Schmidt up to eps * cond (orthonormal to
+// eps), and residual norms R2_aa * R1_aa. Included by engine.cu (namespace
+// liecl_b200 helpers; anonymous-namespace users in dense_engine.cuh).
+#pragma once
+
+#include "common.cuh"
+
+namespace liecl_b200 {
+
+constexpr int kBcMax = 64;  // survivors per block (== kBlockGsMax)
+
+// scalar helpers: double (packed anti-Hermitian field: real Gram) or double2
+__device__ __forceinline__ double bc_conj(double a) { return a; }
+__device__ __forceinline__ double2 bc_conj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double bc_mul(double a, double b) { return a * b; }
+__device__ __forceinline__ double2 bc_mul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double bc_sub(double a, double b) { return a - b; }
+__device__ __forceinline__ double2 bc_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double bc_scale(double a, double s) { return a * s; }
+__device__ __forceinline__ double2 bc_scale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double bc_abs2(double a) { return a * a; }
+__device__ __forceinline__ double bc_abs2(double2 a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double bc_re(double a) { return a; }
+__device__ __forceinline__ double bc_re(double2 a) { return a.x; }
+template <class T> __device__ __forceinline__ T bc_zero();
+template <> __device__ __forceinline__ double bc_zero<double>() { return 0.0; }
+template <> __device__ __forceinline__ double2 bc_zero<double2>() { return make_double2(0.0, 0.0); }
+
+struct BcDecision {
+  int nacc;          // accepts in the block
+  int ntent;         // tentative rejects (explicit check pending)
+  int cap_hit;       // survivor whose accept exceeds the cap (-1 none)
+  int acc[kBcMax];   // accepted survivors, in order
+  int tent[kBcMax];  // tentative rejects, in order
+  int tent_before[kBcMax];  // accepts before each tentative reject
+};
+
+// One CTA of kBcMax threads: sequential decisions over the block (thread t
+// owns column t of Z and s). G: nb x nb, G[i + j*ldg] = <y_i, y_j>. Outputs
+// flags (bit 0 independent, 1 re-checked, 2 tentative), rn (decided
+// survivors: rn2, or sqrt(s) for certified accepts -- replaced by the CholQR2
+// norm later), R1 (accepted x accepted upper factor, ld kBcMax) and `dec`.
+template <class T>
+__global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__ G, int ldg, int nb,
+                                                            const double* __restrict__ rn2, double tol,
+                                                            int cap_left, int* __restrict__ flags,
+                                                            double* __restrict__ rn, T* __restrict__ R1,
+                                                            BcDecision* __restrict__ dec) {
+  extern __shared__ __align__(16) unsigned char bc_smem[];
+  // Z(a, q) = Zs[a * kBcMax + q]: kBcMax^2 T (dynamic). Flat indexing: the
+  // 2-D array-pointer form miscompiled here (a loop-entry register read before
+  // its first write in the SASS of nvcc 12.9 / sm_100a; tools/probe/bc_kernels_test.cu)
+  T* Zs = reinterpret_cast<T*>(bc_smem);
+  __shared__ double s[kBcMax];
+  __shared__ int acc_list[kBcMax];
+  __shared__ int s_ind, s_stop;
+  const int t = threadIdx.x;
+  if (t < nb) s[t] = bc_re(G[t + static_cast<int64_t>(t) * ldg]);
+  int acc = 0, tent = 0;
+  if (t == 0) dec->cap_hit = -1;
+  __syncthreads();
+  for (int q = 0; q < nb; ++q) {
+    if (t == 0) {
+      const double r2 = rn2[q];
+      const bool recheck = acc > 0 && r2 > tol;
+      int ind;
+      int fl = recheck ? 2 : 0;
+      double r = r2;
+      if (!recheck) {
+        ind = r2 > tol ? 1 : 0;
+      } else {
+        const double gqq = bc_re(G[q + static_cast<int64_t>(q) * ldg]);
+        const double sq = s[q];
+        // certified: the residual keeps >= 1% of the survivor's norm (so the
+        // accepted set stays well conditioned, cond <= ~100 per step, and
+        // CholQR2 reproduces sequential Gram-Schmidt to ~eps * cond) and is far
+        // above tol; anything else is decided explicitly
+        ind = (sq > 1e-4 * gqq && sq > (100.0 * tol) * (100.0 * tol)) ? 1 : 0;
+        r = sqrt(fmax(sq, 0.0));
+        if (!ind) {  // tentative: confirmed by an explicit residual
+          fl |= 4;
+          dec->tent[tent] = q;
+          dec->tent_before[tent] = acc;
+          ++tent;
+        }
+      }
+      s_stop = 0;
+      if (ind && acc >= cap_left) {
+        dec->cap_hit = q;
+        s_stop = 1;
+      }
+      flags[q] = fl | ind;
+      rn[q] = r;
+      s_ind = ind;
+    }
+    __syncthreads();
+    if (s_stop) break;
+    if (s_ind) {
+      // row `acc` of Z: the new accept's R entries against every later column
+      const double lqq = sqrt(s[q]);  // == rn2_q for the block's first accept
+      if (t == 0) acc_list[acc] = q;
+      if (t > q && t < nb) {
+        T z = G[q + static_cast<int64_t>(t) * ldg];
+        for (int a = 0; a < acc; ++a) z = bc_sub(z, bc_mul(bc_conj(Zs[a * kBcMax + q]), Zs[a * kBcMax + t]));
+        z = bc_scale(z, 1.0 / lqq);
+        Zs[acc * kBcMax + t] = z;
+        s[t] -= bc_abs2(z);
+      }
+      if (t == 0) {  // the diagonal (real, positive); no thread reads row `acc` in this phase
+        if constexpr (sizeof(T) == sizeof(double)) Zs[acc * kBcMax + q] = lqq;
+        else Zs[acc * kBcMax + q] = T{lqq, 0.0};
+      }
+      ++acc;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // R1[a'][a] = Z[a'][q_a] (upper triangular, ld kBcMax)
+  for (int e = t; e < acc * acc; e += blockDim.x) {
+    const int ap = e % acc, a = e / acc;
+    R1[ap + a * kBcMax] = ap <= a ? Zs[ap * kBcMax + acc_list[a]] : bc_zero<T>();
+  }
+  if (t < acc) dec->acc[t] = acc_list[t];
+  if (t == 0) {
+    dec->nacc = acc;
+    dec->ntent = tent;
+  }
+}
+
+// Cholesky G = R^H R (upper R, ld kBcMax) of an a x a Hermitian matrix
+// (a <= 64), one CTA; diag[a] receives R_aa.
+template <class T>
+__global__ void __launch_bounds__(kBcMax) bc_cholesky_kernel(const T* __restrict__ G, int ldg, int a,
+                                                              T* __restrict__ R, double* __restrict__ diag) {
+  extern __shared__ __align__(16) unsigned char bc_smem[];
+  T* Rs = reinterpret_cast<T*>(bc_smem);  // R(i, j) = Rs[i * kBcMax + j]: kBcMax^2 T (dynamic), flat (see above)
+  const int t = threadIdx.x;
+  for (int i = 0; i < a; ++i) {
+    if (t == 0) {
+      double s = bc_re(G[i + static_cast<int64_t>(i) * ldg]);
+      for (int k = 0; k < i; ++k) s -= bc_abs2(Rs[k * kBcMax + i]);
+      const double r = sqrt(fmax(s, 0.0));
+      if constexpr (sizeof(T) == sizeof(double)) Rs[i * kBcMax + i] = r;
+      else Rs[i * kBcMax + i] = T{r, 0.0};
+      diag[i] = r;
+    }
+    __syncthreads();
+    if (t > i && t < a) {
+      T z = G[i + static_cast<int64_t>(t) * ldg];
+      for (int k = 0; k < i; ++k) z = bc_sub(z, bc_mul(bc_conj(Rs[k * kBcMax + i]), Rs[k * kBcMax + t]));
+      Rs[i * kBcMax + t] = bc_scale(z, 1.0 / bc_re(Rs[i * kBcMax + i]));
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < a * a; e += blockDim.x) {
+    const int i = e % a, j = e / a;
+    R[i + j * kBcMax] = i <= j ? Rs[i * kBcMax + j] : bc_zero<T>();
+  }
+}
+
+// W = Y R^-1 for a column set: w_a = (y_{src a} - sum_{a'<a} w_a' R[a'][a]) / R[a][a],
+// element-wise over [lo, hi) of every vector (stride W elements). src: column
+// index of each output in Y (null: identity). One thread per element.
+template <class T>
+__global__ void bc_trsm_kernel(const T* __restrict__ Y, int64_t ldy, const int* __restrict__ src, int a,
+                               const T* __restrict__ R, T* __restrict__ Wout, int64_t ldw, int64_t lo, int64_t hi) {
+  extern __shared__ __align__(16) unsigned char bc_smem[];
+  T* Rs = reinterpret_cast<T*>(bc_smem);  // kBcMax^2 T (dynamic)
+  for (int e = threadIdx.x; e < a * a; e += blockDim.x) Rs[(e % a) + (e / a) * kBcMax] = R[(e % a) + (e / a) * kBcMax];
+  __syncthreads();
+  for (int64_t e = lo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < hi;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    T w[kBcMax];
+#pragma unroll 1
+    for (int j = 0; j < a; ++j) {
+      T v = Y[static_cast<int64_t>(src ? src[j] : j) * ldy + e];
+#pragma unroll 1
+      for (int i = 0; i < j; ++i) v = bc_sub(v, bc_mul(w[i], Rs[i + j * kBcMax]));
+      v = bc_scale(v, 1.0 / bc_re(Rs[j + j * kBcMax]));
+      w[j] = v;
+      Wout[static_cast<int64_t>(j) * ldw + e] = v;
+    }
+  }
+}
+
+// masked overlaps: beta[a][t] = 0 for a >= before[t] (tentative reject t is
+// checked against the accepts that preceded it only); P column-major, ld ldp,
+// `scalars` doubles per entry (1 packed, 2 complex)
+__global__ void bc_mask_kernel(double* __restrict__ P, int64_t ldp, int rows, int cols,
+                               const int* __restrict__ before, int scalars) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int a = e % rows, c = e / rows;
+    if (a >= before[c])
+      for (int k = 0; k < scalars; ++k) P[(static_cast<int64_t>(c) * ldp + a) * scalars + k] = 0.0;
+  }
+}
+
+// accepted survivors that were re-checked report the CGS2 norm R_aa = R2_aa R1_aa
+// (R1_aa = sqrt(s) is already in rn); the block's first accept keeps rn2
+__global__ void bc_rn_kernel(const BcDecision* __restrict__ dec, const double* __restrict__ diag2,
+                             const int* __restrict__ flags, double* __restrict__ rn) {
+  const int a = threadIdx.x;
+  if (a >= dec->nacc) return;
+  const int q = dec->acc[a];
+  if (flags[q] & 2) rn[q] *= diag2[a];
+}
+
+// zero every element outside [lo, hi) (doubles) of n vectors of W doubles
+__global__ void bc_zero_outside_kernel(double* __restrict__ v, int64_t n, int64_t W, int64_t lo, int64_t hi) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * W;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = e % W;
+    if (k < lo || k >= hi) v[e] = 0.0;
+  }
+}
+
+template <class T> constexpr int bc_smem_bytes() { return kBcMax * kBcMax * static_cast<int>(sizeof(T)); }
+
+} // namespace liecl_b200

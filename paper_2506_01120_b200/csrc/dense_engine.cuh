@@ -636,7 +636,10 @@ private:
   // One CGS pass of `count` columns X against basis columns Vb[0:n] (weighted
   // copy Vwb on the packed path): Rout = X - Vb beta, beta = <Vb, X>,
   // rn = ||Rout|| (Rout may alias X).
-  void project(const double* Vb, const double* Vwb, int64_t n, const double* X, int count, double* Rout, double* rn) {
+  // `before` (device, count ints, optional): candidate c projects only against
+  // basis columns a < before[c] (the Gram-block check of tentative rejects)
+  void project(const double* Vb, const double* Vwb, int64_t n, const double* X, int count, double* Rout, double* rn,
+               const int* before = nullptr) {
     int mtiles = 0;
     // loop shards: the GEMMs cover elements [lo, hi) of full-length columns
     const int64_t off = loop_shard_ ? lo_ * ew() : 0;
@@ -648,6 +651,11 @@ private:
       } else if (n > 0) {
         CU(cudaMemsetAsync(P_.p, 0, static_cast<size_t>(ldp * count) * sizeof(double), ctx_->stream));
       }
+      if (before && n > 0) {
+        bc_mask_kernel<<<static_cast<unsigned>(std::min<int64_t>((n * count + 255) / 256, 1024)), 256, 0,
+                         ctx_->stream>>>(P_.p, ldp, static_cast<int>(n), count, before, 1);
+        launched(ctx_);
+      }
       if (red_ && n > 0) red_->sum(P_.p, ldp * count, ctx_->stream);  // partial overlaps over ranks
       if (len > 0) {
         rgemm_subtract(ctx_, Vb + off, n, len, P_.p, ldp, X + off, count, Rout + off, partial_.p, d_, D_, D_);
@@ -658,6 +666,11 @@ private:
         gemm_project(ctx_, cplx(Vb) + off / 2, n, len, cplx(X) + off / 2, count, cplx(P_.p), 1.0 / d_, D_, D_);
       } else if (n > 0) {
         CU(cudaMemsetAsync(P_.p, 0, static_cast<size_t>(2 * n * count) * sizeof(double), ctx_->stream));
+      }
+      if (before && n > 0) {
+        bc_mask_kernel<<<static_cast<unsigned>(std::min<int64_t>((n * count + 255) / 256, 1024)), 256, 0,
+                         ctx_->stream>>>(P_.p, n, static_cast<int>(n), count, before, 2);
+        launched(ctx_);
       }
       // D-shard: this rank's beta is a partial sum over its slice
       if (red_ && n > 0) red_->sum(P_.p, 2 * n * count, ctx_->stream);
@@ -860,7 +873,8 @@ private:
       if (k == blk_start_next) {  // a new block: decide it on the device when that applies
         blk_start = k;
         blk_start_next = blk_end;
-        blk_on_device = use_block_gs(blk_end - k) && run_block_gs(k, blk_end - k);
+        blk_on_device = (use_block_chol(blk_end - k) && run_block_chol(k, blk_end - k)) ||
+                        (use_block_gs(blk_end - k) && run_block_gs(k, blk_end - k));
         blk_refreshed = n_o_ > n_bs;
       }
       if (blk_on_device) {
@@ -963,6 +977,139 @@ private:
     if (a > 0) CU(cudaMemsetAsync(v, 0, static_cast<size_t>(a) * sizeof(double), ctx_->stream));
     if (b < W) CU(cudaMemsetAsync(v + b, 0, static_cast<size_t>(W - b) * sizeof(double), ctx_->stream));
     red_->sum(v, W, ctx_->stream);
+  }
+
+  // Gram-matrix block decisions (block_chol.cuh): either field, sharded or not
+  bool use_block_chol(int nb) const { return field_ != Field::kUnset && nb >= 2 && block_chol_; }
+  template <class T> bool block_chol(int k, int nb) {
+    const bool packed = field_ == Field::kAntiHerm;
+    const int64_t W = vw();
+    const int64_t lo = loop_shard_ ? lo_ : 0, hi = loop_shard_ ? hi_ : D_, len = hi - lo;
+    const int sc = packed ? 1 : 2;  // doubles per element
+    double* Y = X_.p + k * W;
+    auto T_ = [](double* p) { return reinterpret_cast<T*>(p); };
+    if (!bc_attr_) {
+      func_attr_once(bc_decide_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double>());
+      func_attr_once(bc_decide_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double2>());
+      func_attr_once(bc_cholesky_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double>());
+      func_attr_once(bc_cholesky_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                     bc_smem_bytes<double2>());
+      func_attr_once(bc_trsm_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double>());
+      func_attr_once(bc_trsm_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double2>());
+      bgs_flags_.ensure(kBlockGsMax);
+      bgs_rn_.ensure(kBlockGsMax);
+      h_bgs_flags_.ensure(kBlockGsMax);
+      h_bgs_rn_.ensure(kBlockGsMax);
+      h_bgs_status_.ensure(2);
+      bc_dec_.ensure(1);
+      h_bc_dec_.ensure(1);
+      bc_g_.ensure(static_cast<size_t>(2 * kBcMax * kBcMax));
+      bc_r1_.ensure(static_cast<size_t>(2 * kBcMax * kBcMax));
+      bc_r2_.ensure(static_cast<size_t>(2 * kBcMax * kBcMax));
+      bc_diag_.ensure(kBcMax);
+      bc_rnt_.ensure(kBcMax);
+      h_bc_rnt_.ensure(kBcMax);
+      bc_idx_.ensure(kBcMax);
+      h_bc_idx_.ensure(kBcMax);
+      bc_attr_ = true;
+    }
+    bc_w_.ensure(static_cast<size_t>(kBcMax * W));
+    bc_ww_.ensure(static_cast<size_t>(kBcMax * W));
+    // the Gram matrix of the block: G = <y_i, y_j> (packed: against the weighted copy)
+    auto gram = [&](double* A, int n, double* G) -> int {
+      int ldg;
+      if (packed) {
+        ldg = (n + 1) & ~1;
+        weight_ah_kernel<<<grid_for(n * D_), 256, 0, ctx_->stream>>>(A, n, d_, bc_ww_.p);
+        launched(ctx_); dbg_sync("block_chol 1");
+        rgemm_project(ctx_, bc_ww_.p + lo, n, len, A + lo, n, G, ldg, 1.0 / d_, D_, D_);
+        dbg_sync("block_chol gram gemm");
+      } else {
+        ldg = n;
+        gemm_project(ctx_, cplx(A) + lo, n, len, cplx(A) + lo, n, cplx(G), 1.0 / d_, D_, D_);
+      }
+      if (red_) red_->sum(G, static_cast<int64_t>(ldg) * n * sc, ctx_->stream);
+      return ldg;
+    };
+    const int ldg = gram(Y, nb, bc_g_.p);
+    const int cap_left = static_cast<int>(std::min<int64_t>(kBcMax + 1, std::max<int64_t>(0, cap_ - basis_size())));
+    bc_decide_kernel<T><<<1, kBcMax, bc_smem_bytes<T>(), ctx_->stream>>>(
+        T_(bc_g_.p), ldg, nb, rn2_.p + k, tol_, cap_left, bgs_flags_.p, bgs_rn_.p, T_(bc_r1_.p), bc_dec_.p);
+    launched(ctx_); dbg_sync("block_chol 2");
+    CU(cudaMemcpyAsync(h_bc_dec_.p, bc_dec_.p, sizeof(BcDecision), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    const BcDecision& dec = *h_bc_dec_.p;
+    if (dec.cap_hit >= 0) return false;  // the exact kernel raises at the right survivor
+    const int a = dec.nacc, nt = dec.ntent;
+    if (a > 0) {
+      ensure_capacity(std::min<int64_t>(cap_ + 2, n_o_ + a + 2));
+      double* Vn = V_.p + n_o_ * W;
+      const unsigned tb = static_cast<unsigned>(std::min<int64_t>((len + 127) / 128, 1024));
+      // CholQR2: W1 = Y_A R1^-1, G2 = W1^H W1 = R2^H R2, Q = W1 R2^-1 -> the new basis slots
+      if (len > 0)
+        bc_trsm_kernel<T><<<tb, 128, bc_smem_bytes<T>(), ctx_->stream>>>(T_(Y), D_, bc_dec_.p->acc, a,
+                                                                      T_(bc_r1_.p), T_(bc_w_.p), D_, lo, hi);
+      launched(ctx_); dbg_sync("block_chol 3");
+      const int ldg2 = gram(bc_w_.p, a, bc_g_.p);
+      bc_cholesky_kernel<T><<<1, kBcMax, bc_smem_bytes<T>(), ctx_->stream>>>(T_(bc_g_.p), ldg2, a, T_(bc_r2_.p),
+                                                                               bc_diag_.p);
+      launched(ctx_); dbg_sync("block_chol 4");
+      if (len > 0)
+        bc_trsm_kernel<T><<<tb, 128, bc_smem_bytes<T>(), ctx_->stream>>>(T_(bc_w_.p), D_, nullptr, a,
+                                                                      T_(bc_r2_.p), T_(Vn), D_, lo, hi);
+      launched(ctx_); dbg_sync("block_chol 5");
+      bc_rn_kernel<<<1, kBcMax, 0, ctx_->stream>>>(bc_dec_.p, bc_diag_.p, bgs_flags_.p, bgs_rn_.p);
+      launched(ctx_); dbg_sync("block_chol 6");
+      if (loop_shard_) {  // every rank holds its slice of the new vectors: rebuild them everywhere
+        bc_zero_outside_kernel<<<grid_for(a * W), 256, 0, ctx_->stream>>>(Vn, a, W, lo * sc, hi * sc);
+        launched(ctx_); dbg_sync("block_chol 7");
+        red_->sum(Vn, a * W, ctx_->stream);
+      }
+      if (packed) {
+        weight_ah_kernel<<<grid_for(a * D_), 256, 0, ctx_->stream>>>(Vn, a, d_, Vw_.p + n_o_ * W);
+        launched(ctx_); dbg_sync("block_chol 8");
+      }
+      if (keep_) {  // Alg. 3: the accepted candidates themselves into the originals slab
+        for (int i = 0; i < a; ++i) h_bc_idx_.p[i] = h_idx_.p[k + dec.acc[i]];
+        CU(cudaMemcpyAsync(bc_idx_.p, h_bc_idx_.p, a * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+        dim3 gg(static_cast<unsigned>(std::min<int64_t>((W + 255) / 256, 64)), a);
+        gather_words_kernel<<<gg, 256, 0, ctx_->stream>>>(C_.p, bc_idx_.p, W, O_.p + n_b_ * W);
+        launched(ctx_); dbg_sync("block_chol 9");
+      }
+      if (nt > 0) {  // tentative rejects: explicit CGS2 against the accepts before each
+        dim3 gg(static_cast<unsigned>(std::min<int64_t>((W + 255) / 256, 64)), nt);
+        gather_words_kernel<<<gg, 256, 0, ctx_->stream>>>(Y, bc_dec_.p->tent, W, bc_w_.p);
+        launched(ctx_); dbg_sync("block_chol 10");
+        const int* before = bc_dec_.p->tent_before;
+        project(Vn, packed ? Vw_.p + n_o_ * W : nullptr, a, bc_w_.p, nt, bc_w_.p, bc_rnt_.p, before);
+        project(Vn, packed ? Vw_.p + n_o_ * W : nullptr, a, bc_w_.p, nt, bc_w_.p, bc_rnt_.p, before);
+        CU(cudaMemcpyAsync(h_bc_rnt_.p, bc_rnt_.p, nt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      }
+    }
+    CU(cudaMemcpyAsync(h_bgs_flags_.p, bgs_flags_.p, nb * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(h_bgs_rn_.p, bgs_rn_.p, nb * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaStreamSynchronize(ctx_->stream));
+    for (int i = 0; i < nt; ++i) {
+      if (h_bc_rnt_.p[i] > tol_) {  // not the reject the Gram bound suggested: decide the block exactly
+        ++bc_fallbacks_;
+        return false;
+      }
+      h_bgs_rn_.p[dec.tent[i]] = h_bc_rnt_.p[i];
+      h_bgs_flags_.p[dec.tent[i]] &= 3;
+    }
+    h_bgs_status_.p[1] = -1;
+    ++bc_blocks_;
+    return true;
+  }
+  // LIECL_B200_DEBUG_SYNC=1: synchronise after each step of the block path and name the failing one
+  void dbg_sync(const char* what) {
+    static const bool on = std::getenv("LIECL_B200_DEBUG_SYNC") != nullptr;
+    if (!on) return;
+    const cudaError_t e = cudaStreamSynchronize(ctx_->stream);
+    if (e != cudaSuccess) throw Error(LIECL_B200_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  bool run_block_chol(int k, int nb) {
+    return field_ == Field::kAntiHerm ? block_chol<double>(k, nb) : block_chol<double2>(k, nb);
   }
 
   // device-resident block decisions (block_gs.cuh): either field, not
@@ -1072,6 +1219,18 @@ private:
   DevBuf<double> V_, Vw_, O_, C_, R_, X_, Y_, P_;  // element width ew() doubles
   DevBuf<double2> stage_;                          // complex input staging
   DevBuf<double2> basis_stage_;                    // set_basis staging (kept across calls)
+  bool block_chol_ = [] {  // LIECL_B200_BLOCK_CHOL=0: the per-survivor block kernel (diagnostics)
+    const char* e = std::getenv("LIECL_B200_BLOCK_CHOL");
+    return !(e && e[0] == '0');
+  }();
+  bool bc_attr_ = false;
+  uint64_t bc_blocks_ = 0, bc_fallbacks_ = 0;
+  DevBuf<BcDecision> bc_dec_;
+  HostBuf<BcDecision> h_bc_dec_;
+  DevBuf<double> bc_g_, bc_r1_, bc_r2_, bc_diag_, bc_rnt_, bc_w_, bc_ww_;
+  HostBuf<double> h_bc_rnt_;
+  DevBuf<int> bc_idx_;
+  HostBuf<int> h_bc_idx_;
   bool block_gs_ = [] {  // LIECL_B200_BLOCK_GS=0: host-driven re-checks (diagnostics)
     const char* e = std::getenv("LIECL_B200_BLOCK_GS");
     return !(e && e[0] == '0');

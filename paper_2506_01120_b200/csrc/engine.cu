@@ -48,6 +48,7 @@
 
 #include "../../include/liecl_b200.h"
 #include "ah.cuh"
+#include "block_chol.cuh"
 #include "block_gs.cuh"
 #include "commutator.cuh"
 #include "dgemm_dmma.cuh"
