@@ -12,13 +12,14 @@
 // every later column): O(64^2) work per accept in one CTA.
 //
 // s_q is exact to ~eps * G_qq, so it CERTIFIES an accept when s_q clears
-// 1e-4 G_qq and (100 tol)^2 -- the residual is then far above tol, not
+// 1e-2 G_qq and (100 tol)^2 -- the residual is then far above tol, not
 // borderline, and the accepted set well conditioned. A smaller s_q cannot separate 1e-15 from 1e-9: the survivor is
 // a TENTATIVE reject, confirmed afterwards by its explicit CGS2 residual
 // against exactly the accepts before it (a masked two-pass projection); if
 // any explicit residual exceeds tol, the caller redoes the block with the
 // exact per-survivor kernel. The accepted vectors are formed by CholQR2 --
-// W = Y_A R1^-1, then Q = W R2^-1 with R2 from the Cholesky of W^H W --
+// W = Y_A R1^-1, then Q = W R2^-1 with R2 from the Cholesky of W^H W (the
+// triangular inverses in one CTA, the products as DMMA GEMMs) --
 // the same Q as sequential Gram-Schmidt up to eps * cond (orthonormal to
 // eps), and residual norms R2_aa * R1_aa. Included by engine.cu (namespace
 // liecl_b200 helpers; anonymous-namespace users in dense_engine.cuh).
@@ -48,6 +49,9 @@ __device__ __forceinline__ double bc_re(double2 a) { return a.x; }
 template <class T> __device__ __forceinline__ T bc_zero();
 template <> __device__ __forceinline__ double bc_zero<double>() { return 0.0; }
 template <> __device__ __forceinline__ double2 bc_zero<double2>() { return make_double2(0.0, 0.0); }
+template <class T> __device__ __forceinline__ T bc_one();
+template <> __device__ __forceinline__ double bc_one<double>() { return 1.0; }
+template <> __device__ __forceinline__ double2 bc_one<double2>() { return make_double2(1.0, 0.0); }
 
 struct BcDecision {
   int nacc;          // accepts in the block
@@ -70,15 +74,20 @@ __global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__
                                                             double* __restrict__ rn, T* __restrict__ R1,
                                                             BcDecision* __restrict__ dec) {
   extern __shared__ __align__(16) unsigned char bc_smem[];
-  // Z(a, q) = Zs[a * kBcMax + q]: kBcMax^2 T (dynamic). Flat indexing: the
-  // 2-D array-pointer form miscompiled here (a loop-entry register read before
-  // its first write in the SASS of nvcc 12.9 / sm_100a; tools/probe/bc_kernels_test.cu)
+  // Z(a, q) = Zs[a * kBcMax + q] and G(i, j) = Gs[i + j * kBcMax]: 2 kBcMax^2 T
+  // (dynamic; G staged once -- every step then runs out of shared memory).
+  // Flat indexing: the 2-D array-pointer form miscompiled here (a loop-entry
+  // register read before its first write in the SASS of nvcc 12.9 / sm_100a;
+  // tools/probe/bc_kernels_test.cu)
   T* Zs = reinterpret_cast<T*>(bc_smem);
+  T* Gs = Zs + kBcMax * kBcMax;
   __shared__ double s[kBcMax];
   __shared__ int acc_list[kBcMax];
   __shared__ int s_ind, s_stop;
   const int t = threadIdx.x;
-  if (t < nb) s[t] = bc_re(G[t + static_cast<int64_t>(t) * ldg]);
+  for (int e = t; e < nb * nb; e += blockDim.x) Gs[(e % nb) + (e / nb) * kBcMax] = G[(e % nb) + static_cast<int64_t>(e / nb) * ldg];
+  __syncthreads();
+  if (t < nb) s[t] = bc_re(Gs[t + t * kBcMax]);
   int acc = 0, tent = 0;
   if (t == 0) dec->cap_hit = -1;
   __syncthreads();
@@ -92,13 +101,15 @@ __global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__
       if (!recheck) {
         ind = r2 > tol ? 1 : 0;
       } else {
-        const double gqq = bc_re(G[q + static_cast<int64_t>(q) * ldg]);
+        const double gqq = bc_re(Gs[q + q * kBcMax]);
         const double sq = s[q];
-        // certified: the residual keeps >= 1% of the survivor's norm (so the
+        // certified: the residual keeps >= 10% of the survivor's norm (so the
         // accepted set stays well conditioned, cond <= ~100 per step, and
         // CholQR2 reproduces sequential Gram-Schmidt to ~eps * cond) and is far
         // above tol; anything else is decided explicitly
-        ind = (sq > 1e-4 * gqq && sq > (100.0 * tol) * (100.0 * tol)) ? 1 : 0;
+        // (survivors are residuals of unit candidates, G_qq <= ~1: G_qq >= 1e-6
+        // keeps the accepted columns within a few decades of each other)
+        ind = (sq > 1e-2 * gqq && gqq > 1e-6 && sq > (100.0 * tol) * (100.0 * tol)) ? 1 : 0;
         r = sqrt(fmax(sq, 0.0));
         if (!ind) {  // tentative: confirmed by an explicit residual
           fl |= 4;
@@ -123,7 +134,7 @@ __global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__
       const double lqq = sqrt(s[q]);  // == rn2_q for the block's first accept
       if (t == 0) acc_list[acc] = q;
       if (t > q && t < nb) {
-        T z = G[q + static_cast<int64_t>(t) * ldg];
+        T z = Gs[q + t * kBcMax];
         for (int a = 0; a < acc; ++a) z = bc_sub(z, bc_mul(bc_conj(Zs[a * kBcMax + q]), Zs[a * kBcMax + t]));
         z = bc_scale(z, 1.0 / lqq);
         Zs[acc * kBcMax + t] = z;
@@ -157,10 +168,13 @@ __global__ void __launch_bounds__(kBcMax) bc_cholesky_kernel(const T* __restrict
                                                               T* __restrict__ R, double* __restrict__ diag) {
   extern __shared__ __align__(16) unsigned char bc_smem[];
   T* Rs = reinterpret_cast<T*>(bc_smem);  // R(i, j) = Rs[i * kBcMax + j]: kBcMax^2 T (dynamic), flat (see above)
+  T* Gs = Rs + kBcMax * kBcMax;            // G staged in shared memory
   const int t = threadIdx.x;
+  for (int e = t; e < a * a; e += blockDim.x) Gs[(e % a) + (e / a) * kBcMax] = G[(e % a) + static_cast<int64_t>(e / a) * ldg];
+  __syncthreads();
   for (int i = 0; i < a; ++i) {
     if (t == 0) {
-      double s = bc_re(G[i + static_cast<int64_t>(i) * ldg]);
+      double s = bc_re(Gs[i + i * kBcMax]);
       for (int k = 0; k < i; ++k) s -= bc_abs2(Rs[k * kBcMax + i]);
       const double r = sqrt(fmax(s, 0.0));
       if constexpr (sizeof(T) == sizeof(double)) Rs[i * kBcMax + i] = r;
@@ -169,7 +183,7 @@ __global__ void __launch_bounds__(kBcMax) bc_cholesky_kernel(const T* __restrict
     }
     __syncthreads();
     if (t > i && t < a) {
-      T z = G[i + static_cast<int64_t>(t) * ldg];
+      T z = Gs[i + t * kBcMax];
       for (int k = 0; k < i; ++k) z = bc_sub(z, bc_mul(bc_conj(Rs[k * kBcMax + i]), Rs[k * kBcMax + t]));
       Rs[i * kBcMax + t] = bc_scale(z, 1.0 / bc_re(Rs[i * kBcMax + i]));
     }
@@ -178,31 +192,6 @@ __global__ void __launch_bounds__(kBcMax) bc_cholesky_kernel(const T* __restrict
   for (int e = t; e < a * a; e += blockDim.x) {
     const int i = e % a, j = e / a;
     R[i + j * kBcMax] = i <= j ? Rs[i * kBcMax + j] : bc_zero<T>();
-  }
-}
-
-// W = Y R^-1 for a column set: w_a = (y_{src a} - sum_{a'<a} w_a' R[a'][a]) / R[a][a],
-// element-wise over [lo, hi) of every vector (stride W elements). src: column
-// index of each output in Y (null: identity). One thread per element.
-template <class T>
-__global__ void bc_trsm_kernel(const T* __restrict__ Y, int64_t ldy, const int* __restrict__ src, int a,
-                               const T* __restrict__ R, T* __restrict__ Wout, int64_t ldw, int64_t lo, int64_t hi) {
-  extern __shared__ __align__(16) unsigned char bc_smem[];
-  T* Rs = reinterpret_cast<T*>(bc_smem);  // kBcMax^2 T (dynamic)
-  for (int e = threadIdx.x; e < a * a; e += blockDim.x) Rs[(e % a) + (e / a) * kBcMax] = R[(e % a) + (e / a) * kBcMax];
-  __syncthreads();
-  for (int64_t e = lo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < hi;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    T w[kBcMax];
-#pragma unroll 1
-    for (int j = 0; j < a; ++j) {
-      T v = Y[static_cast<int64_t>(src ? src[j] : j) * ldy + e];
-#pragma unroll 1
-      for (int i = 0; i < j; ++i) v = bc_sub(v, bc_mul(w[i], Rs[i + j * kBcMax]));
-      v = bc_scale(v, 1.0 / bc_re(Rs[j + j * kBcMax]));
-      w[j] = v;
-      Wout[static_cast<int64_t>(j) * ldw + e] = v;
-    }
   }
 }
 
@@ -215,6 +204,56 @@ __global__ void bc_mask_kernel(double* __restrict__ P, int64_t ldp, int rows, in
     const int a = e % rows, c = e / rows;
     if (a >= before[c])
       for (int k = 0; k < scalars; ++k) P[(static_cast<int64_t>(c) * ldp + a) * scalars + k] = 0.0;
+  }
+}
+
+// T = R^-1 for an a x a upper-triangular R (ld kBcMax), one CTA: thread j
+// back-substitutes column j. Rows a .. 2*ceil(a/2)-1 of T are zero (the real
+// GEMM reads an even K).
+template <class T>
+__global__ void __launch_bounds__(kBcMax) bc_tri_inverse_kernel(const T* __restrict__ R, int a, T* __restrict__ Tinv) {
+  extern __shared__ __align__(16) unsigned char bc_smem[];
+  T* Rs = reinterpret_cast<T*>(bc_smem);  // R(i, j) = Rs[i + j * kBcMax]
+  T* Ts = Rs + kBcMax * kBcMax;           // T(i, j) = Ts[i + j * kBcMax]
+  const int j = threadIdx.x;
+  for (int e = j; e < a * a; e += blockDim.x) Rs[(e % a) + (e / a) * kBcMax] = R[(e % a) + (e / a) * kBcMax];
+  __syncthreads();
+  if (j < a) {
+    if constexpr (sizeof(T) == sizeof(double)) Ts[j + j * kBcMax] = 1.0 / bc_re(Rs[j + j * kBcMax]);
+    else Ts[j + j * kBcMax] = T{1.0 / bc_re(Rs[j + j * kBcMax]), 0.0};
+    for (int i = j - 1; i >= 0; --i) {
+      T acc = bc_zero<T>();
+      for (int k = i + 1; k <= j; ++k) acc = bc_sub(acc, bc_mul(Rs[i + k * kBcMax], Ts[k + j * kBcMax]));
+      Ts[i + j * kBcMax] = bc_scale(acc, 1.0 / bc_re(Rs[i + i * kBcMax]));
+    }
+  }
+  __syncthreads();
+  const int rows = (a + 1) & ~1;
+  for (int e = threadIdx.x; e < rows * a; e += blockDim.x) {
+    const int i = e % rows, c = e / rows;
+    Tinv[i + c * kBcMax] = (i <= c && i < a) ? Ts[i + c * kBcMax] : bc_zero<T>();
+  }
+}
+
+// max |(Q^H Q)_ij - delta_ij| of the new block (G ld ldg, a x a): the
+// a-posteriori orthogonality check of CholQR2 (the caller falls back to the
+// exact per-survivor kernel above a bound)
+template <class T>
+__global__ void bc_orth_error_kernel(const T* __restrict__ G, int ldg, int a, double* __restrict__ out) {
+  __shared__ double red[kBcMax];
+  double m = 0.0;
+  for (int e = threadIdx.x; e < a * a; e += blockDim.x) {
+    const int i = e % a, j = e / a;
+    T v = G[i + static_cast<int64_t>(j) * ldg];
+    if (i == j) v = bc_sub(v, bc_scale(bc_one<T>(), 1.0));
+    m = fmax(m, sqrt(bc_abs2(v)));
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < static_cast<int>(blockDim.x); ++k) t = fmax(t, red[k]);
+    *out = t;
   }
 }
 
@@ -237,6 +276,6 @@ __global__ void bc_zero_outside_kernel(double* __restrict__ v, int64_t n, int64_
   }
 }
 
-template <class T> constexpr int bc_smem_bytes() { return kBcMax * kBcMax * static_cast<int>(sizeof(T)); }
+template <class T> constexpr int bc_smem_bytes() { return 2 * kBcMax * kBcMax * static_cast<int>(sizeof(T)); }
 
 } // namespace liecl_b200

@@ -37,6 +37,9 @@ public:
   }
 
   ~DenseEngine() {
+    if (std::getenv("LIECL_B200_TRACE") && (bc_blocks_ || bc_fallbacks_))
+      std::fprintf(stderr, "[dense] Gram-block decisions: %llu blocks, %llu exact fallbacks\n",
+                   static_cast<unsigned long long>(bc_blocks_), static_cast<unsigned long long>(bc_fallbacks_));
     if (copy_stream_) {
       cudaStreamSynchronize(copy_stream_);
       cudaStreamDestroy(copy_stream_);
@@ -994,8 +997,10 @@ private:
       func_attr_once(bc_cholesky_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double>());
       func_attr_once(bc_cholesky_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                      bc_smem_bytes<double2>());
-      func_attr_once(bc_trsm_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double>());
-      func_attr_once(bc_trsm_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double2>());
+      func_attr_once(bc_tri_inverse_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                     bc_smem_bytes<double>());
+      func_attr_once(bc_tri_inverse_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                     bc_smem_bytes<double2>());
       bgs_flags_.ensure(kBlockGsMax);
       bgs_rn_.ensure(kBlockGsMax);
       h_bgs_flags_.ensure(kBlockGsMax);
@@ -1013,8 +1018,10 @@ private:
       h_bc_idx_.ensure(kBcMax);
       bc_attr_ = true;
     }
-    bc_w_.ensure(static_cast<size_t>(kBcMax * W));
-    bc_ww_.ensure(static_cast<size_t>(kBcMax * W));
+    bc_w_.ensure(static_cast<size_t>((kBcMax + 1) * W));
+    bc_ww_.ensure(static_cast<size_t>((kBcMax + 1) * W));
+    bc_ya_.ensure(static_cast<size_t>((kBcMax + 1) * W));
+    bc_tinv_.ensure(static_cast<size_t>(2 * kBcMax * kBcMax));
     // the Gram matrix of the block: G = <y_i, y_j> (packed: against the weighted copy)
     auto gram = [&](double* A, int n, double* G) -> int {
       int ldg;
@@ -1044,20 +1051,37 @@ private:
     if (a > 0) {
       ensure_capacity(std::min<int64_t>(cap_ + 2, n_o_ + a + 2));
       double* Vn = V_.p + n_o_ * W;
-      const unsigned tb = static_cast<unsigned>(std::min<int64_t>((len + 127) / 128, 1024));
-      // CholQR2: W1 = Y_A R1^-1, G2 = W1^H W1 = R2^H R2, Q = W1 R2^-1 -> the new basis slots
-      if (len > 0)
-        bc_trsm_kernel<T><<<tb, 128, bc_smem_bytes<T>(), ctx_->stream>>>(T_(Y), D_, bc_dec_.p->acc, a,
-                                                                      T_(bc_r1_.p), T_(bc_w_.p), D_, lo, hi);
-      launched(ctx_); dbg_sync("block_chol 3");
+      // CholQR2: W1 = Y_A R1^-1, G2 = W1^H W1 = R2^H R2, Q = W1 R2^-1 -> the new basis slots.
+      // Each R^-1 is formed in one CTA; the products are DMMA GEMMs over this rank's rows.
+      const int a_even = (a + 1) & ~1;
+      {  // the accepted survivors, contiguous (+ one zero column: the real GEMM reads an even K)
+        dim3 gg(static_cast<unsigned>(std::min<int64_t>((W + 255) / 256, 64)), a);
+        gather_words_kernel<<<gg, 256, 0, ctx_->stream>>>(Y, bc_dec_.p->acc, W, bc_ya_.p);
+        launched(ctx_); dbg_sync("block_chol gather");
+        if (a_even > a) CU(cudaMemsetAsync(bc_ya_.p + a * W, 0, W * sizeof(double), ctx_->stream));
+      }
+      auto times_inverse = [&](const double* A, const double* R, double* out) {
+        bc_tri_inverse_kernel<T><<<1, kBcMax, bc_smem_bytes<T>(), ctx_->stream>>>(T_(const_cast<double*>(R)), a,
+                                                                                   T_(bc_tinv_.p));
+        launched(ctx_); dbg_sync("block_chol inverse");
+        if (len == 0) return;
+        if (packed)
+          rgemm_mc_store(ctx_, A + lo, D_, len, a_even, bc_tinv_.p, kBcMax, a, out + lo, D_, 1.0);
+        else
+          gemm_mc_store(ctx_, cplx(A) + lo, D_, len, a, cplx(bc_tinv_.p), kBcMax, a, cplx(out) + lo, D_, 1.0);
+        dbg_sync("block_chol times_inverse");
+      };
+      times_inverse(bc_ya_.p, bc_r1_.p, bc_w_.p);
+      if (a_even > a) CU(cudaMemsetAsync(bc_w_.p + a * W, 0, W * sizeof(double), ctx_->stream));
       const int ldg2 = gram(bc_w_.p, a, bc_g_.p);
       bc_cholesky_kernel<T><<<1, kBcMax, bc_smem_bytes<T>(), ctx_->stream>>>(T_(bc_g_.p), ldg2, a, T_(bc_r2_.p),
                                                                                bc_diag_.p);
       launched(ctx_); dbg_sync("block_chol 4");
-      if (len > 0)
-        bc_trsm_kernel<T><<<tb, 128, bc_smem_bytes<T>(), ctx_->stream>>>(T_(bc_w_.p), D_, nullptr, a,
-                                                                      T_(bc_r2_.p), T_(Vn), D_, lo, hi);
-      launched(ctx_); dbg_sync("block_chol 5");
+      times_inverse(bc_w_.p, bc_r2_.p, Vn);
+      // a-posteriori: the new block must be orthonormal to CGS2's accuracy
+      const int ldg3 = gram(Vn, a, bc_g_.p);
+      bc_orth_error_kernel<T><<<1, kBcMax, 0, ctx_->stream>>>(T_(bc_g_.p), ldg3, a, bc_rnt_.p + kBcMax - 1);
+      launched(ctx_);
       bc_rn_kernel<<<1, kBcMax, 0, ctx_->stream>>>(bc_dec_.p, bc_diag_.p, bgs_flags_.p, bgs_rn_.p);
       launched(ctx_); dbg_sync("block_chol 6");
       if (loop_shard_) {  // every rank holds its slice of the new vectors: rebuild them everywhere
@@ -1088,7 +1112,14 @@ private:
     }
     CU(cudaMemcpyAsync(h_bgs_flags_.p, bgs_flags_.p, nb * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaMemcpyAsync(h_bgs_rn_.p, bgs_rn_.p, nb * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    if (a > 0)
+      CU(cudaMemcpyAsync(h_bc_rnt_.p + kBcMax - 1, bc_rnt_.p + kBcMax - 1, sizeof(double), cudaMemcpyDeviceToHost,
+                         ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
+    if (a > 0 && !(h_bc_rnt_.p[kBcMax - 1] <= 1e-13)) {  // CholQR2 lost orthogonality: decide exactly
+      ++bc_fallbacks_;
+      return false;
+    }
     for (int i = 0; i < nt; ++i) {
       if (h_bc_rnt_.p[i] > tol_) {  // not the reject the Gram bound suggested: decide the block exactly
         ++bc_fallbacks_;
@@ -1227,7 +1258,7 @@ private:
   uint64_t bc_blocks_ = 0, bc_fallbacks_ = 0;
   DevBuf<BcDecision> bc_dec_;
   HostBuf<BcDecision> h_bc_dec_;
-  DevBuf<double> bc_g_, bc_r1_, bc_r2_, bc_diag_, bc_rnt_, bc_w_, bc_ww_;
+  DevBuf<double> bc_g_, bc_r1_, bc_r2_, bc_diag_, bc_rnt_, bc_w_, bc_ww_, bc_ya_, bc_tinv_;
   HostBuf<double> h_bc_rnt_;
   DevBuf<int> bc_idx_;
   HostBuf<int> h_bc_idx_;

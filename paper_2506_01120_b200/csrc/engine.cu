@@ -421,6 +421,19 @@ void rgemm_project(liecl_b200_ctx* ctx, const double* Vw, int64_t n, int64_t D, 
   t.stop();
 }
 
+// C[m + n*ldc] = alpha * sum_k A(m, k) B(k, n), all real: A M-contiguous
+// (A(m,k) = A[k*lda + m]), B K-contiguous (ld ldb); K even (16-byte B rows).
+// (CholQR in the Gram-block decisions: W = Y_A R^-1.)
+void rgemm_mc_store(liecl_b200_ctx* ctx, const double* A, int64_t lda, int64_t M, int64_t K, const double* B,
+                    int64_t ldb, int count, double* C, int64_t ldc, double alpha) {
+  if (M == 0 || count == 0) return;
+  rgemm_attr_once<false, REpi::kStoreScaled>();
+  dim3 grid((M + rg::BM - 1) / rg::BM, (count + rg::BN - 1) / rg::BN);
+  dgemm_dmma_kernel<false, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<false>(), ctx->stream>>>(
+      static_cast<int>(M), count, static_cast<int>(K), A, lda, B, ldb, C, ldc, alpha, nullptr, 0, nullptr, 0, 0, 0);
+  launched(ctx);
+}
+
 // R = X - V[:, 0:n] P (P ld ldp); partial[mt][b] = sum_rows w R^2
 void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, const double* P, int64_t ldp,
                     const double* X, int count, double* R, double* partial, int d, int64_t ldv = -1,

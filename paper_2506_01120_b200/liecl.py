@@ -20,6 +20,7 @@ is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+from collections.abc import Sequence
 import enum
 import time
 from dataclasses import dataclass, field
@@ -122,8 +123,31 @@ class DenseOperator:
         return np.asfortranarray(self.matrix).ravel(order="F")
 
     @staticmethod
-    def from_vec(v: np.ndarray, d: int) -> "DenseOperator":
-        return DenseOperator(np.asarray(v).reshape(d, d, order="F").copy())
+    def from_vec(v: np.ndarray, d: int, copy: bool = True) -> "DenseOperator":
+        m = np.asarray(v).reshape(d, d, order="F")  # a view of a contiguous vec
+        return DenseOperator(m.copy() if copy else m)
+
+
+class DenseOperatorList(Sequence):
+    """result.basis / orthonormal_basis of a dense closure without copying:
+    element k is a DenseOperator viewing row k of the (n, d*d) result array
+    (column-major d x d), built on access."""
+
+    def __init__(self, arr: np.ndarray, d: int):
+        self.arr, self.d = arr, d
+
+    def __len__(self) -> int:
+        return len(self.arr)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        return DenseOperator.from_vec(self.arr[k], self.d, copy=False)
+
+    def __eq__(self, other):
+        if not isinstance(other, (list, tuple, DenseOperatorList)) or len(other) != len(self):
+            return NotImplemented if not isinstance(other, (list, tuple, DenseOperatorList)) else False
+        return all(np.array_equal(a.matrix, b.matrix) for a, b in zip(self, other))
 
 
 @dataclass(frozen=True)
@@ -288,7 +312,7 @@ def closure_dense_arrays(gens: np.ndarray, d: int, method: Method = Method.ortho
                          {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
     b = basis[:n]
     o = ortho[:n] if ortho is not None else (b[:0] if method == Method.standard_rank else b)
-    return ClosureResult([DenseOperator.from_vec(v, d) for v in b], [DenseOperator.from_vec(v, d) for v in o], n,
+    return ClosureResult(DenseOperatorList(b, d), DenseOperatorList(o, d), n,
                          method, Backend.dense, config.tolerance, stats,
                          log[: log_len.value].copy() if config.record_log else None, b, o)
 
@@ -332,7 +356,7 @@ def _closure_dense_gram(gens, d, config, device, cap) -> ClosureResult:
     b = basis[:n]
     A = _dense_fetch(device, 2, n, d)
     Ai = _dense_fetch(device, 3, n, d)
-    res = ClosureResult([DenseOperator.from_vec(v, d) for v in b], None, n, Method.matrix_inversion, Backend.dense,
+    res = ClosureResult(DenseOperatorList(b, d), None, n, Method.matrix_inversion, Backend.dense,
                         config.tolerance, stats, log[: log_len.value].copy() if config.record_log else None, b, None)
     res.gram = (A, Ai)
     return res
