@@ -170,7 +170,7 @@ int liecl_b200_closure_dense_gram(liecl_b200_ctx* ctx, const double* gens, int32
 /*
  * run_closure for Pauli generators that are single strings (one term each;
  * every closure element then stays a single string). Bit-exact with the
- * reference's PauliSum arithmetic (R:src/pauli.cpp). qubits <= 31.
+ * reference's PauliSum arithmetic (R:src/pauli.cpp). qubits 1..64 (128-bit string keys).
  * Outputs `cap` entries of (x, z, coef) for result.basis and, when
  * ortho_coef != NULL, the coefficients of result.orthonormal_basis.
  */

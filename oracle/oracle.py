@@ -162,12 +162,12 @@ class Ref:
         return ClosureOut(n, basis[:n].copy(), ortho[:n].copy(), {}, log[: min(nlog.value, log_cap)].copy())
 
     def decision_log_pauli(self, offsets, x, z, coef, qubits, keep_original=False, tol=1e-10, threads=1,
-                           term_cap=None):
+                           term_cap=None, basis_cap=None):
         offsets = np.ascontiguousarray(offsets, np.int64)
         x = np.ascontiguousarray(x, np.uint64)
         z = np.ascontiguousarray(z, np.uint64)
         coef = np.ascontiguousarray(coef, np.float64)
-        basis_cap = 4 ** qubits
+        basis_cap = basis_cap or 4 ** qubits
         term_cap = term_cap or max(basis_cap * 4, 1 << 20)
         log_cap = 1 << 22
         log = np.zeros(log_cap, DECISION_DTYPE)

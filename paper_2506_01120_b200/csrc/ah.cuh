@@ -121,8 +121,9 @@ template <int DIM> struct CommAhShape {
   static constexpr int PAIRS_PER_CTA = 8 / WARPS_PER_PAIR;
   static constexpr int ROWS_PER_WARP = TR / WARPS_PER_PAIR;  // tile rows per warp
   static constexpr int LDP = DIM + 4;                // == 4 (mod 16): conflict-free fragment gathers
+  static constexpr int LDQ = DIM + 1;                // P planes: odd stride, row and column reads conflict-free
   static constexpr int PACKED = DIM * LDP;
-  static constexpr int SMEM_PER_PAIR = 2 * PACKED * 8 + WARPS_PER_PAIR * 8;
+  static constexpr int SMEM_PER_PAIR = (2 * PACKED * 8 + WARPS_PER_PAIR * 8 + 15) / 16 * 16;  // 16-byte slots
   static constexpr int SMEM = PAIRS_PER_CTA * SMEM_PER_PAIR;
 };
 
@@ -171,10 +172,9 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
     for (int e = tip; e < D2 / 2; e += NT) {  // 16-byte loads; DIM even
       const int i = (2 * e) % DIM, k = (2 * e) / DIM;
       const double2 va = ga[e], vb = gb[e];
-      pa[i + k * LDP] = va.x;
-      pa[i + 1 + k * LDP] = va.y;
-      pb[i + k * LDP] = vb.x;
-      pb[i + 1 + k * LDP] = vb.y;
+      // i even, LDP even: 16-byte aligned, one conflict-free vector store each
+      *reinterpret_cast<double2*>(pa + i + k * LDP) = va;
+      *reinterpret_cast<double2*>(pb + i + k * LDP) = vb;
     }
   }
   __syncthreads();
@@ -208,7 +208,10 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
     }
   }
   __syncthreads();  // inputs consumed: P planes reuse the packed buffers
-  double* pre = pa;  // P(i, k) re at [i*LDP + k]
+  // P(i, k) re at pre[i*LDQ + k]: the epilogue reads P(k, i) along a row and
+  // P(i, k) down a column; an odd stride keeps both free of bank conflicts
+  constexpr int LDQ = S::LDQ;
+  double* pre = pa;
   double* pim = pb;
   if (active) {
 #pragma unroll
@@ -218,8 +221,8 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
       for (int c = 0; c < S::TR; ++c)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          pre[(ti + g) * LDP + c * 8 + 2 * t + h] = cre[r][c][h];
-          pim[(ti + g) * LDP + c * 8 + 2 * t + h] = cim[r][c][h];
+          pre[(ti + g) * LDQ + c * 8 + 2 * t + h] = cre[r][c][h];
+          pim[(ti + g) * LDQ + c * 8 + 2 * t + h] = cim[r][c][h];
         }
     }
   }
@@ -233,9 +236,9 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
       if (e >= D2) break;
       const int i = e % DIM, k = e / DIM;
       double v;
-      if (i < k) v = pre[i * LDP + k] - pre[k * LDP + i];
-      else if (i > k) v = pim[k * LDP + i] + pim[i * LDP + k];
-      else v = 2.0 * pim[i * LDP + i];
+      if (i < k) v = pre[i * LDQ + k] - pre[k * LDQ + i];
+      else if (i > k) v = pim[k * LDQ + i] + pim[i * LDQ + k];
+      else v = 2.0 * pim[i * LDQ + i];
       hv[q] = v;
       sumsq += (i == k ? 1.0 : 2.0) * v * v;
     }

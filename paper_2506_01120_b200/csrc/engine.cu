@@ -619,59 +619,6 @@ void launch_commutator_complex(liecl_b200_ctx* ctx, const double2* basis, int d,
 
 // --------------------------------------------------------- Pauli engine ---
 
-__global__ void pauli_generators_kernel(int count, const uint64_t* __restrict__ gx, const uint64_t* __restrict__ gz,
-                                        const pauli::C2* __restrict__ gc, const uint64_t* __restrict__ vx,
-                                        const uint64_t* __restrict__ vz, const pauli::C2* __restrict__ vc,
-                                        long long nv, pauli::StringSet vset, double tol, pauli::CandidateOut out,
-                                        int* __restrict__ accept_flag) {
-  // The generator loop is sequential in the reference (R:src/closure.cpp:378-403);
-  // a single thread replays it exactly (generator tuples are short).
-  using namespace pauli;
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  long long accepted = 0;
-  for (int j = 0; j < count; ++j) {
-    const uint64_t x = gx[j], z = gz[j];
-    out.x[j] = x;
-    out.z[j] = z;
-    out.flags[j] = 0;
-    accept_flag[j] = 0;
-    const C2 g = slot(gc[j]);
-    const double gn = is_zero(g) ? 0.0 : single_norm(g);
-    if (!(gn > tol)) {
-      out.verdict[j] = kNull;
-      out.rn[j] = gn;
-      continue;
-    }
-    const C2 h = cmul(g, {__ddiv_rn(1.0, gn), 0.0});
-    out.hunit[j] = h;
-    const unsigned long long key = pack(x, z);
-    long long idx = nv > 0 ? set_find(vset, key) : -1;
-    C2 v = {0.0, 0.0};
-    if (idx >= 0) v = vc[idx];
-    for (int q = 0; q < j && idx < 0; ++q)
-      if (accept_flag[q] && out.x[q] == x && out.z[q] == z) {
-        idx = q;
-        v = out.unit[q];
-      }
-    bool indep;
-    C2 unit = {0.0, 0.0};
-    const double rn = check(nv + accepted == 0, idx >= 0, v, h, tol, indep, unit);
-    out.rn[j] = rn;
-    out.unit[j] = unit;
-    int f = 0;
-    if (rn > 0.0 && rn >= tol / 10.0 && rn <= tol * 10.0) f |= 1;
-    if (idx >= 0 && indep) f |= 2;
-    out.flags[j] = f;
-    if (indep && idx < 0) {
-      out.verdict[j] = kAccepted;
-      accept_flag[j] = 1;
-      ++accepted;
-    } else {
-      out.verdict[j] = kMember;
-    }
-  }
-}
-
 __global__ void pauli_count_kernel(int count, const int* __restrict__ verdict, const int* __restrict__ flags,
                                    unsigned long long* __restrict__ counters) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -684,7 +631,7 @@ __global__ void pauli_count_kernel(int count, const int* __restrict__ verdict, c
 __global__ void pauli_rehash_kernel(long long n, const uint64_t* __restrict__ vx, const uint64_t* __restrict__ vz,
                                     pauli::StringSet vset) {
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (i < n) pauli::set_insert(vset, pauli::pack(vx[i], vz[i]), i);
+  if (i < n) pauli::set_insert(vset, vx[i], vz[i], i);
 }
 
 uint64_t next_pow2(uint64_t v) {
@@ -697,9 +644,10 @@ class PauliEngine {
 public:
   PauliEngine(liecl_b200_ctx* ctx, unsigned qubits, bool keep_original, const liecl_b200_config& cfg)
       : ctx_(ctx), q_(qubits), keep_(keep_original), tol_(cfg.tolerance), record_(cfg.record_log != 0) {
-    if (qubits < 1 || qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..31 qubits");
+    // strings are 128-bit keys: any qubit count the reference accepts (R:src/pauli.cpp:383-391)
+    if (qubits < 1 || qubits > 64) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..64 qubits");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
-    const uint64_t full = qubits >= 32 ? ~0ull : (1ull << (2 * qubits));
+    const uint64_t full = full_dim(qubits);
     cap_ = cfg.max_dim ? static_cast<int64_t>(std::min<uint64_t>(cfg.max_dim, full)) : static_cast<int64_t>(full);
     bmax_ = cfg.batch_max > 0 ? cfg.batch_max : (int64_t(1) << 22);
     if (cfg.deadline_seconds > 0) {
@@ -711,8 +659,10 @@ public:
     counters_.ensure(3);
   }
 
+  static uint64_t full_dim(unsigned qubits) { return qubits >= 32 ? ~0ull : (1ull << (2 * qubits)); }
+
   bool compatible(unsigned qubits, bool keep, const liecl_b200_config& cfg) const {
-    const uint64_t full = 1ull << (2 * qubits);
+    const uint64_t full = full_dim(qubits);
     const int64_t cap = cfg.max_dim ? static_cast<int64_t>(std::min<uint64_t>(cfg.max_dim, full))
                                     : static_cast<int64_t>(full);
     return qubits == q_ && keep == keep_ && cap == cap_ && (cfg.batch_max <= 0 || cfg.batch_max == bmax_);
@@ -729,58 +679,72 @@ public:
     st_ = liecl_b200_stats{};
     warns_.clear();
     log_.clear();
-    const uint64_t tsize = vmask_ + 1;
+    const uint64_t tsize = vmask_ + 2;
     pauli::reset_table_kernel<<<static_cast<unsigned>(std::min<uint64_t>((tsize + 255) / 256, 4096)), 256, 0,
                                 ctx_->stream>>>(vset(), tsize);
     launched(ctx_);
   }
 
+  // run_engine (R:src/closure.cpp:356-473): the persistent frontier kernel
+  // (pauli::frontier_kernel) runs the generator loop and every narrow stretch
+  // of the cursor loop in one CTA; wide frontiers go through the multi-CTA
+  // batch (candidates / resolve / scan / append).
   void run(const uint64_t* gx, const uint64_t* gz, const double* gc, int ngens) {
-    // generator loop
-    ensure_batch(std::max(ngens, 1));
+    const int64_t log_cap = frontier_log_cap();
+    ensure_batch(ngens + log_cap);
+    grow_basis(std::max<int64_t>(n_ + ngens, 1024));
     DevBuf<uint64_t> dgx, dgz;
     DevBuf<pauli::C2> dgc;
-    dgx.ensure(ngens);
-    dgz.ensure(ngens);
-    dgc.ensure(ngens);
     if (ngens > 0) {
+      dgx.ensure(ngens);
+      dgz.ensure(ngens);
+      dgc.ensure(ngens);
       CU(cudaMemcpyAsync(dgx.p, gx, ngens * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx_->stream));
       CU(cudaMemcpyAsync(dgz.p, gz, ngens * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx_->stream));
       CU(cudaMemcpyAsync(dgc.p, gc, ngens * sizeof(pauli::C2), cudaMemcpyHostToDevice, ctx_->stream));
-      pauli_generators_kernel<<<1, 1, 0, ctx_->stream>>>(ngens, dgx.p, dgz.p, dgc.p, vx_.p, vz_.p, vc_.p, n_, vset(),
-                                                          tol_, outs(), acc_.p);
-      launched(ctx_);
-      finish_batch(ngens, -1);
     }
-    // frontier batches over all available cursor pairs
+    fstate_.ensure(1);
+    fstate_host_.ensure(1);
+    const int64_t wide = frontier_wide();
+    int gens_left = ngens;
     int64_t g = 0;
     for (;;) {
-      const int64_t avail = n_ * (n_ - 1) / 2;
-      if (g >= avail) break;
       if (has_deadline_ && Clock::now() > deadline_)
         throw Error(LIECL_B200_TIMEOUT, "closure computation exceeded its deadline");
-      const int cnt = static_cast<int>(std::min<int64_t>(bmax_, avail - g));
-      ensure_batch(cnt);
-      const uint64_t fsize = next_pow2(2ull * cnt + 16);
-      first_keys_.ensure(fsize);
-      first_vals_.ensure(fsize);
-      pauli::StringSet first{first_keys_.p, first_vals_.p, fsize - 1};
-      pauli::reset_table_kernel<<<static_cast<unsigned>(std::min<uint64_t>((fsize + 255) / 256, 4096)), 256, 0,
-                                  ctx_->stream>>>(first, fsize);
+      pauli::FrontierState& hs = *fstate_host_.p;
+      hs = pauli::FrontierState{};
+      hs.n = n_;
+      hs.g = g;
+      CU(cudaMemcpyAsync(fstate_.p, &hs, sizeof hs, cudaMemcpyHostToDevice, ctx_->stream));
+      pauli::frontier_kernel<<<1, pauli::kFrontierThreads, 0, ctx_->stream>>>(
+          gens_left, dgx.p, dgz.p, dgc.p, vx_.p, vz_.p, vc_.p, keep_ ? oc_.p : nullptr, vset(),
+          static_cast<long long>(vx_.n), cap_, tol_, outs(), static_cast<long long>(ngens + log_cap), wide,
+          fstate_.p);
       launched(ctx_);
-      const unsigned blocks = static_cast<unsigned>((cnt + 255) / 256);
-      pauli::candidates_kernel<<<blocks, 256, 0, ctx_->stream>>>(1, g, cnt, nullptr, nullptr, nullptr, vx_.p, vz_.p,
-                                                                  vc_.p, keep_ ? oc_.p : vc_.p, n_, vset(), first,
-                                                                  tol_, outs());
-      launched(ctx_);
-      pauli::resolve_kernel<<<blocks, 256, 0, ctx_->stream>>>(cnt, first, tol_, outs(), acc_.p);
-      launched(ctx_);
-      st_.commutators_evaluated += static_cast<uint64_t>(cnt);
-      finish_batch(cnt, g);
-      g += cnt;
+      CU(cudaMemcpyAsync(&hs, fstate_.p, sizeof hs, cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      const pauli::FrontierState fs = hs;
+      const int64_t base = gens_left;
+      const int64_t pairs = fs.g - g;
+      if (fs.bad > 0) throw_residual_floor();
+      if (gens_left > 0) {
+        ++st_.batches;
+        collect(0, gens_left, -1);
+      }
+      if (pairs > 0 && (fs.border > 0 || record_)) collect(base, pairs, g);
+      st_.batches += fs.chunks;
+      st_.independence_checks += fs.checks;
+      st_.commutators_evaluated += static_cast<uint64_t>(pairs);
+      st_.accepted += static_cast<uint64_t>(fs.n - n_);
+      n_ = fs.n;
+      g = fs.g;
+      gens_left = 0;
+      if (fs.status == pauli::kDone) break;
+      if (fs.status == pauli::kCapacity) throw_capacity();
+      if (fs.status == pauli::kGrow) grow_basis(2 * static_cast<int64_t>(vx_.n));
+      if (fs.status == pauli::kWide) g = wide_batch(g);
     }
   }
-
   liecl_b200_stats stats() {
     liecl_b200_stats s = st_;
     s.dimension = static_cast<uint64_t>(n_);
@@ -801,6 +765,46 @@ public:
   }
 
 private:
+  static int64_t frontier_log_cap() { return int64_t(1) << 18; }
+  // frontier width above which the multi-CTA batch beats the one-CTA loop
+  static int64_t frontier_wide() {
+    const char* e = std::getenv("LIECL_B200_PAULI_WIDE");
+    return e ? std::max<int64_t>(0, std::atoll(e)) : (int64_t(1) << 14);
+  }
+  [[noreturn]] void throw_residual_floor() {
+    throw Error(LIECL_B200_INVALID_INPUT,
+                "tolerance below the residual floor of the Pauli arithmetic: a repeated string would be "
+                "accepted as independent");
+  }
+  [[noreturn]] void throw_capacity() {
+    throw Error(LIECL_B200_CAPACITY,
+                "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
+  }
+
+  // one multi-CTA batch over the whole frontier [g, avail) (at most bmax_ pairs)
+  int64_t wide_batch(int64_t g) {
+    const int64_t avail = n_ * (n_ - 1) / 2;
+    const int cnt = static_cast<int>(std::min<int64_t>(bmax_, avail - g));
+    ensure_batch(cnt);
+    const uint64_t fsize = next_pow2(2ull * cnt + 16);
+    first_keys_.ensure(fsize + 2);
+    first_vals_.ensure(fsize + 2);
+    pauli::StringSet first{first_keys_.p, first_vals_.p, fsize - 1};
+    pauli::reset_table_kernel<<<static_cast<unsigned>(std::min<uint64_t>((fsize + 257) / 256, 4096)), 256, 0,
+                                ctx_->stream>>>(first, fsize + 2);
+    launched(ctx_);
+    const unsigned blocks = static_cast<unsigned>((cnt + 255) / 256);
+    pauli::candidates_kernel<<<blocks, 256, 0, ctx_->stream>>>(1, g, cnt, nullptr, nullptr, nullptr, vx_.p, vz_.p,
+                                                                vc_.p, keep_ ? oc_.p : vc_.p, n_, vset(), first,
+                                                                tol_, outs());
+    launched(ctx_);
+    pauli::resolve_kernel<<<blocks, 256, 0, ctx_->stream>>>(cnt, first, tol_, outs(), acc_.p);
+    launched(ctx_);
+    st_.commutators_evaluated += static_cast<uint64_t>(cnt);
+    finish_batch(cnt, g);
+    return g + cnt;
+  }
+
   pauli::StringSet vset() { return {vkeys_.p, vvals_.p, vmask_}; }
   pauli::CandidateOut outs() { return {cx_.p, cz_.p, ch_.p, cu_.p, crn_.p, cver_.p, cflag_.p}; }
 
@@ -827,11 +831,11 @@ private:
     const uint64_t tsize = next_pow2(4ull * cap);
     vkeys_.release();
     vvals_.release();
-    vkeys_.ensure(tsize);
-    vvals_.ensure(tsize);
+    vkeys_.ensure(tsize + 2);
+    vvals_.ensure(tsize + 2);
     vmask_ = tsize - 1;
-    pauli::reset_table_kernel<<<static_cast<unsigned>(std::min<uint64_t>((tsize + 255) / 256, 4096)), 256, 0,
-                                ctx_->stream>>>(vset(), tsize);
+    pauli::reset_table_kernel<<<static_cast<unsigned>(std::min<uint64_t>((tsize + 257) / 256, 4096)), 256, 0,
+                                ctx_->stream>>>(vset(), tsize + 2);
     launched(ctx_);
     if (n_ > 0) {
       pauli_rehash_kernel<<<static_cast<unsigned>((n_ + 255) / 256), 256, 0, ctx_->stream>>>(n_, vx_.p, vz_.p, vset());
@@ -864,14 +868,9 @@ private:
     const int64_t acc = last[0] + last[1];
     ++st_.batches;
     st_.independence_checks += cnts[0];
-    if (cnts[2] > 0)
-      throw Error(LIECL_B200_INVALID_INPUT,
-                  "tolerance below the residual floor of the Pauli arithmetic: a repeated string would be "
-                  "accepted as independent");
-    if (cnts[1] > 0 || record_ || pair_g0 < 0) collect(cnt, pair_g0);
-    if (n_ + acc > cap_)
-      throw Error(LIECL_B200_CAPACITY,
-                  "basis size cap of " + std::to_string(cap_) + " exceeded; raise the cap to continue");
+    if (cnts[2] > 0) throw_residual_floor();
+    if (cnts[1] > 0 || record_ || pair_g0 < 0) collect(0, cnt, pair_g0);
+    if (n_ + acc > cap_) throw_capacity();
     grow_basis(n_ + acc);
     pauli::append_kernel<<<(cnt + 255) / 256, 256, 0, ctx_->stream>>>(cnt, acc_.p, rank_.p, n_, outs(), vx_.p, vz_.p,
                                                                        vc_.p, keep_ ? oc_.p : nullptr, vset());
@@ -880,14 +879,15 @@ private:
     st_.accepted += static_cast<uint64_t>(acc);
   }
 
-  void collect(int cnt, int64_t pair_g0) {
+  // warnings / decision log of candidates [off, off + cnt) of the output arrays
+  void collect(int64_t off, int64_t cnt, int64_t pair_g0) {
     std::vector<int> ver(cnt), flag(cnt);
     std::vector<double> rn(cnt);
-    CU(cudaMemcpyAsync(ver.data(), cver_.p, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaMemcpyAsync(flag.data(), cflag_.p, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaMemcpyAsync(rn.data(), crn_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(ver.data(), cver_.p + off, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(flag.data(), cflag_.p + off, cnt * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(rn.data(), crn_.p + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
-    for (int j = 0; j < cnt; ++j) {
+    for (int64_t j = 0; j < cnt; ++j) {
       int64_t l, m;
       if (pair_g0 >= 0) pair_from_index(pair_g0 + j, l, m);
       else { l = j; m = -1; }
@@ -923,8 +923,10 @@ private:
   std::vector<liecl_b200_decision> log_;
   DevBuf<uint64_t> vx_, vz_;
   DevBuf<pauli::C2> vc_, oc_;
-  DevBuf<unsigned long long> vkeys_, first_keys_;
+  DevBuf<ulonglong2> vkeys_, first_keys_;
   DevBuf<long long> vvals_, first_vals_;
+  DevBuf<pauli::FrontierState> fstate_;
+  HostBuf<pauli::FrontierState> fstate_host_;
   uint64_t vmask_ = 0;
   DevBuf<uint64_t> cx_, cz_;
   DevBuf<pauli::C2> ch_, cu_;

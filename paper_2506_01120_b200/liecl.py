@@ -177,6 +177,33 @@ class PauliSum:
         return 1 << self.qubits
 
 
+class PauliSingleList(Sequence):
+    """result.basis / orthonormal_basis of a single-string Pauli closure
+    without building n PauliSum objects up front: element k is the one-term
+    sum (x[k], z[k], coef[k]), built on access."""
+
+    def __init__(self, x: np.ndarray, z: np.ndarray, coef: np.ndarray, qubits: int):
+        self.x, self.z, self.coef, self.qubits = x, z, coef, qubits
+
+    def __len__(self) -> int:
+        return len(self.x)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        if k < 0:
+            k += len(self)
+        if not 0 <= k < len(self):
+            raise IndexError(k)
+        return PauliSum.single(PauliString(int(self.x[k]), int(self.z[k]), self.qubits),
+                               complex(self.coef[k, 0], self.coef[k, 1]))
+
+    def __eq__(self, other):
+        if not isinstance(other, (list, tuple, PauliSingleList)):
+            return NotImplemented
+        return len(other) == len(self) and all(a == b for a, b in zip(self, other))
+
+
 @dataclass
 class WarningRecord:
     kind: str
@@ -392,13 +419,12 @@ def closure_pauli_arrays(x, z, coef, qubits: int, method: Method = Method.orthon
     stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds, warnings,
                          {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
 
-    def sums(cs):
-        return [PauliSum.single(PauliString(int(bx[i]), int(bz[i]), qubits), complex(cs[i, 0], cs[i, 1]))
-                for i in range(n)]
     gram = method == Method.matrix_inversion
-    res = ClosureResult(sums(bc), None if gram else sums(oc), n, method, Backend.pauli, config.tolerance, stats,
+    bx, bz, bc, oc = bx[:n].copy(), bz[:n].copy(), bc[:n].copy(), oc[:n].copy()
+    res = ClosureResult(PauliSingleList(bx, bz, bc, qubits), None if gram else PauliSingleList(bx, bz, oc, qubits),
+                        n, method, Backend.pauli, config.tolerance, stats,
                         log[: log_len.value].copy() if config.record_log else None,
-                        (bx[:n].copy(), bz[:n].copy(), bc[:n].copy()), None if gram else oc[:n].copy())
+                        (bx, bz, bc), None if gram else oc)
     if gram:  # distinct strings: A = A^{-1} = I exactly (see liecl_b200_closure_pauli)
         res.gram = (np.eye(n, dtype=np.complex128), np.eye(n, dtype=np.complex128))
     return res

@@ -1,0 +1,145 @@
+"""Single-string Pauli closures on up to 64 qubits (128-bit string keys) and
+the persistent one-CTA frontier loop. Needs a B200.
+
+The reference keeps strings as two uint64 masks and accepts 1..64 qubits
+(R:src/pauli.cpp:383-391, R:src/generators.cpp:32). Its default dimension
+cap (2^q)^2 (R:src/closure.cpp:369-371, R:src/operator.cpp:42-44) overflows
+from q = 32 on, so these cases pass max_dim explicitly, as a reference user
+must.
+"""
+import numpy as np
+import pytest
+
+from paper_2506_01120_b200 import liecl
+from paper_2506_01120_b200 import workloads as w
+
+pytestmark = pytest.mark.gpu
+
+ALL = (1 << 64) - 1
+
+
+def ring_case(pos, all_ones=True, seed=5):
+    """c4-style ring (X X, Y Y, Z) on the qubit positions `pos` of 64, plus Y^64
+    (x = z = all ones: the empty-slot marker of the string tables)."""
+    n = len(pos)
+    xs, zs = [], []
+    for j in range(n):
+        b = (1 << pos[j]) | (1 << pos[(j + 1) % n])
+        xs.append(b), zs.append(0)
+    for j in range(n):
+        b = (1 << pos[j]) | (1 << pos[(j + 1) % n])
+        xs.append(b), zs.append(b)
+    for j in range(n):
+        xs.append(0), zs.append(1 << pos[j])
+    if all_ones:
+        xs.append(ALL), zs.append(ALL)
+    coef = np.random.default_rng(seed).normal(size=(len(xs), 2))
+    return np.array(xs, np.uint64), np.array(zs, np.uint64), coef
+
+
+@pytest.mark.parametrize("method", [liecl.Method.orthonorm_dimonly, liecl.Method.orthonorm],
+                         ids=["dimonly", "orthonorm"])
+def test_64_qubit_closure_matches_reference(ref_exact, method):
+    x, z, c = ring_case([0, 31, 32, 63])
+    keep = method == liecl.Method.orthonorm
+    r = ref_exact.decision_log_pauli(np.arange(len(x) + 1), x, z, c, 64, keep_original=keep, tol=1e-10,
+                                     basis_cap=4096, term_cap=1 << 14)
+    assert r.dimension == 126
+    res = liecl.closure_pauli_arrays(x, z, c, 64, method,
+                                     liecl.ClosureConfig(tolerance=1e-10, record_log=True, max_dim=4096))
+    assert res.dimension == r.dimension
+    off, rx, rz, rc = r.basis
+    assert np.array_equal(off, np.arange(r.dimension + 1))  # single strings stay single strings
+    bx, bz, bc = res.basis_array
+    assert np.array_equal(bx, rx) and np.array_equal(bz, rz)
+    assert np.array_equal(bc.view(np.uint64), rc.view(np.uint64))
+    assert (bx == np.uint64(ALL)).any()  # Y^64 is in the basis (the special slot)
+    log, rl = res.decision_log, r.log
+    assert len(log) == len(rl)
+    for k in ("l", "m", "null_cand", "independent"):
+        assert np.array_equal(log[k], rl[k]), k
+    assert np.array_equal(log["residual_norm"].view(np.uint64), rl["residual_norm"].view(np.uint64))
+
+
+def test_embedded_ring_equals_the_10_qubit_closure():
+    """Config 4's ring relabelled onto qubits spread over all 64 bit positions:
+    the same algebra, so the same verdicts, dimension and coefficient bits."""
+    p = w.config4()
+    pos = [0, 7, 19, 31, 32, 40, 47, 55, 62, 63]
+
+    def embed(m):
+        out = 0
+        for j in range(p.qubits):
+            if (int(m) >> j) & 1:
+                out |= 1 << pos[j]
+        return out
+    ex = np.array([embed(v) for v in p.x], np.uint64)
+    ez = np.array([embed(v) for v in p.z], np.uint64)
+    cfg = liecl.ClosureConfig(tolerance=p.tol, record_log=True, max_dim=4096)
+    small = liecl.closure_pauli_arrays(p.x, p.z, p.coef, p.qubits, config=cfg)
+    big = liecl.closure_pauli_arrays(ex, ez, p.coef, 64, config=cfg)
+    assert small.dimension == big.dimension == 380
+    sx, sz, sc = small.basis_array
+    bx, bz, bc = big.basis_array
+    assert np.array_equal(bx, [embed(v) for v in sx]) and np.array_equal(bz, [embed(v) for v in sz])
+    assert np.array_equal(bc.view(np.uint64), sc.view(np.uint64))
+    for k in ("l", "m", "null_cand", "independent"):
+        assert np.array_equal(small.decision_log[k], big.decision_log[k])
+
+
+@pytest.mark.parametrize("wide", ["0", "1000", "100000000"], ids=["multi_cta", "mixed", "persistent"])
+@pytest.mark.parametrize("method", [liecl.Method.orthonorm_dimonly, liecl.Method.orthonorm],
+                         ids=["dimonly", "orthonorm"])
+def test_frontier_paths_match_golden(golden, wide, method, monkeypatch):
+    """LIECL_B200_PAULI_WIDE moves the hand-over between the one-CTA frontier
+    loop and the multi-CTA batches; every split gives the golden bits."""
+    monkeypatch.setenv("LIECL_B200_PAULI_WIDE", wide)
+    p = w.config4()
+    meta, g = golden(f"{p.name}_{liecl.to_string(method)}")
+    res = liecl.closure_pauli_arrays(p.x, p.z, p.coef, p.qubits, method,
+                                     liecl.ClosureConfig(tolerance=p.tol, record_log=True))
+    assert res.dimension == meta["dimension"] == 380
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(res.stats, k) == meta["stats"][k]
+    bx, bz, bc = res.basis_array
+    assert np.array_equal(bx, g["x"]) and np.array_equal(bz, g["z"])
+    assert np.array_equal(bc.view(np.uint64), g["coef_bits"])
+    log = res.decision_log
+    assert np.array_equal(log["independent"], g["log_indep"])
+    assert np.array_equal(log["residual_norm"].view(np.uint64), g["log_rn_bits"])
+
+
+def test_frontier_grows_basis_buffers_mid_loop(port, monkeypatch):
+    """HEA n=5 sparse (dim 1023) on the one-CTA loop only: the basis buffers
+    start at 1024 slots and the table at 4096, so growth and relaunch happen
+    inside the loop; the result equals the C restatement bit for bit."""
+    monkeypatch.setenv("LIECL_B200_PAULI_WIDE", "100000000")
+    n = 5
+    x = np.array([1 << i for i in range(n)] + [0] * n + [0] * (n - 1), np.uint64)
+    z = np.array([0] * n + [1 << i for i in range(n)] + [(1 << i) | (1 << (i + 1)) for i in range(n - 1)], np.uint64)
+    c = np.tile([1.0, 0.0], (3 * n - 1, 1))
+    res = liecl.closure_pauli_arrays(x, z, c, n, config=liecl.ClosureConfig(tolerance=1e-10, record_log=True))
+    assert res.stats.engine["batches"] > 1
+    po = port.closure_pauli_single(x, z, c, n, tol=1e-10)
+    assert res.dimension == po.dimension == 1023
+    bx, bz, bc = res.basis_array
+    assert np.array_equal(bx, po.basis[0]) and np.array_equal(bz, po.basis[1])
+    assert np.array_equal(bc.view(np.uint64), po.basis[2].view(np.uint64))
+
+
+def test_capacity_error_inside_the_frontier_loop():
+    p = w.config4()
+    with pytest.raises(liecl.CapacityError):
+        liecl.closure_pauli_arrays(p.x, p.z, p.coef, p.qubits,
+                                   config=liecl.ClosureConfig(tolerance=p.tol, max_dim=200))
+
+
+def test_qubit_range():
+    x = np.array([1], np.uint64)
+    z = np.array([0], np.uint64)
+    c = np.array([[0.0, 1.0]])
+    with pytest.raises(liecl.InvalidInputError):
+        liecl.closure_pauli_arrays(x, z, c, 65, config=liecl.ClosureConfig(max_dim=8))
+    r = liecl.closure_pauli_arrays(np.array([ALL], np.uint64), np.array([ALL], np.uint64), c, 64,
+                                   config=liecl.ClosureConfig(max_dim=8))
+    assert r.dimension == 1 and int(r.basis_array[0][0]) == ALL
