@@ -115,11 +115,17 @@ __global__ void weight_ah_kernel(const double* __restrict__ v, int64_t count, in
     vw[e] = (((e % D2) % (d + 1)) == 0 ? 1.0 : 2.0) * v[e];
 }
 
-template <int DIM> struct CommAhShape {
+// Warp layout of one pair's product P = A B (TR x TR tiles of 8 x 8): a warp
+// owns WR x WC tiles (WR row tiles sharing A fragments, WC column tiles
+// sharing B fragments). d < 64: one row of tiles per warp, several pairs per
+// CTA; d = 64: eight warps per pair, WR x WC per warp (default 2 x 4: 12
+// fragment loads per 32 DMMAs, 64 accumulator registers).
+template <int DIM, int WR_ = (DIM == 64 ? 2 : 1), int WC_ = (DIM == 64 ? 4 : DIM / 8)> struct CommAhShape {
   static constexpr int TR = DIM / 8;                 // tile rows (and columns)
-  static constexpr int WARPS_PER_PAIR = TR < 8 ? TR : 8;
+  static constexpr int WR = WR_, WC = WC_;
+  static constexpr int WARPS_PER_PAIR = (TR / WR) * (TR / WC);
+  static_assert(WARPS_PER_PAIR <= 8 && 8 % WARPS_PER_PAIR == 0, "warp layout");
   static constexpr int PAIRS_PER_CTA = 8 / WARPS_PER_PAIR;
-  static constexpr int ROWS_PER_WARP = TR / WARPS_PER_PAIR;  // tile rows per warp
   static constexpr int LDP = DIM + 4;                // == 4 (mod 16): conflict-free fragment gathers
   static constexpr int LDQ = DIM + 1;                // P planes: odd stride, row and column reads conflict-free
   static constexpr int PACKED = DIM * LDP;
@@ -138,16 +144,15 @@ __device__ __forceinline__ void ah_elem(const double* p, int i, int k, double& r
 
 // K1 on the packed path: pairs [g0, g0+count) of the packed commutator basis;
 // writes packed h_unit, ||h||, null flag. One DMMA product P = A B per pair,
-// fragments gathered straight from the packed inputs in shared memory; each
-// warp owns whole tile rows of P (A fragments reused across the row); P is
-// written back over the consumed inputs and h = P - P^dagger is read out in
-// the packed layout. ~70 KB per pair at d = 64: three CTAs per SM (80
-// registers, full carveout) overlap their load and compute phases.
-template <int DIM>
-__global__ void __launch_bounds__(256, 3)
+// fragments gathered straight from the packed inputs in shared memory (A
+// fragments reused across a warp's WC column tiles, B fragments across its WR
+// row tiles); P is written back over the consumed inputs and h = P - P^dagger
+// is read out in the packed layout. ~70 KB per pair at d = 64.
+template <int DIM, int MINB = 2, int WR = CommAhShape<DIM>::WR, int WC = CommAhShape<DIM>::WC>
+__global__ void __launch_bounds__(256, MINB)
 commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, double tol, bool normalize,
                      double* __restrict__ out, double* __restrict__ hnorm, int* __restrict__ is_null) {
-  using S = CommAhShape<DIM>;
+  using S = CommAhShape<DIM, WR, WC>;
   constexpr int D2 = DIM * DIM;
   constexpr int LDP = S::LDP;
   constexpr int NT = S::WARPS_PER_PAIR * 32;
@@ -156,6 +161,8 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
   const int g = lane >> 2, t = lane & 3;
   const int slot = warp / S::WARPS_PER_PAIR;
   const int wip = warp % S::WARPS_PER_PAIR;
+  const int wr0 = (wip / (S::TR / WC)) * WR;  // first row tile of this warp
+  const int wc0 = (wip % (S::TR / WC)) * WC;  // first column tile
   const int j = blockIdx.x * S::PAIRS_PER_CTA + slot;
   const bool active = j < count;
   const int tip = threadIdx.x - slot * NT;
@@ -179,30 +186,29 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
   }
   __syncthreads();
 
-  double cre[S::ROWS_PER_WARP][S::TR][2], cim[S::ROWS_PER_WARP][S::TR][2];
+  double cre[WR][WC][2], cim[WR][WC][2];
 #pragma unroll
-  for (int r = 0; r < S::ROWS_PER_WARP; ++r)
+  for (int r = 0; r < WR; ++r)
 #pragma unroll
-    for (int c = 0; c < S::TR; ++c) cre[r][c][0] = cre[r][c][1] = cim[r][c][0] = cim[r][c][1] = 0.0;
+    for (int c = 0; c < WC; ++c) cre[r][c][0] = cre[r][c][1] = cim[r][c][0] = cim[r][c][1] = 0.0;
   if (active) {
 #pragma unroll 2
     for (int k0 = 0; k0 < DIM; k0 += 4) {
       const int k = k0 + t;
-      double br[S::TR], bi[S::TR];
+      double br[WC], bi[WC], ar[WR], ai[WR];
 #pragma unroll
-      for (int c = 0; c < S::TR; ++c) ah_elem<LDP>(pb, k, c * 8 + g, br[c], bi[c]);  // B(k, tj + g)
+      for (int c = 0; c < WC; ++c) ah_elem<LDP>(pb, k, (wc0 + c) * 8 + g, br[c], bi[c]);  // B(k, tj + g)
 #pragma unroll
-      for (int r = 0; r < S::ROWS_PER_WARP; ++r) {
-        const int ti = (wip * S::ROWS_PER_WARP + r) * 8;
-        double ar, ai;
-        ah_elem<LDP>(pa, ti + g, k, ar, ai);  // A(ti + g, k)
-        const double nai = -ai;
+      for (int r = 0; r < WR; ++r) ah_elem<LDP>(pa, (wr0 + r) * 8 + g, k, ar[r], ai[r]);  // A(ti + g, k)
 #pragma unroll
-        for (int c = 0; c < S::TR; ++c) {
-          dmma_8x8x4(cre[r][c][0], cre[r][c][1], ar, br[c]);
+      for (int r = 0; r < WR; ++r) {
+        const double nai = -ai[r];
+#pragma unroll
+        for (int c = 0; c < WC; ++c) {
+          dmma_8x8x4(cre[r][c][0], cre[r][c][1], ar[r], br[c]);
           dmma_8x8x4(cre[r][c][0], cre[r][c][1], nai, bi[c]);
-          dmma_8x8x4(cim[r][c][0], cim[r][c][1], ar, bi[c]);
-          dmma_8x8x4(cim[r][c][0], cim[r][c][1], ai, br[c]);
+          dmma_8x8x4(cim[r][c][0], cim[r][c][1], ar[r], bi[c]);
+          dmma_8x8x4(cim[r][c][0], cim[r][c][1], ai[r], br[c]);
         }
       }
     }
@@ -215,14 +221,14 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
   double* pim = pb;
   if (active) {
 #pragma unroll
-    for (int r = 0; r < S::ROWS_PER_WARP; ++r) {
-      const int ti = (wip * S::ROWS_PER_WARP + r) * 8;
+    for (int r = 0; r < WR; ++r) {
+      const int ti = (wr0 + r) * 8;
 #pragma unroll
-      for (int c = 0; c < S::TR; ++c)
+      for (int c = 0; c < WC; ++c)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          pre[(ti + g) * LDQ + c * 8 + 2 * t + h] = cre[r][c][h];
-          pim[(ti + g) * LDQ + c * 8 + 2 * t + h] = cim[r][c][h];
+          pre[(ti + g) * LDQ + (wc0 + c) * 8 + 2 * t + h] = cre[r][c][h];
+          pim[(ti + g) * LDQ + (wc0 + c) * 8 + 2 * t + h] = cim[r][c][h];
         }
     }
   }
