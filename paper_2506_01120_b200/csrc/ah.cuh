@@ -127,11 +127,20 @@ template <int DIM, int WR_ = (DIM == 64 ? 2 : 1), int WC_ = (DIM == 64 ? 4 : DIM
   static_assert(WARPS_PER_PAIR <= 8 && 8 % WARPS_PER_PAIR == 0, "warp layout");
   static constexpr int PAIRS_PER_CTA = 8 / WARPS_PER_PAIR;
   static constexpr int LDP = DIM + 4;                // == 4 (mod 16): conflict-free fragment gathers
-  static constexpr int LDQ = DIM + 1;                // P planes: odd stride, row and column reads conflict-free
   static constexpr int PACKED = DIM * LDP;
   static constexpr int SMEM_PER_PAIR = (2 * PACKED * 8 + WARPS_PER_PAIR * 8 + 15) / 16 * 16;  // 16-byte slots
   static constexpr int SMEM = PAIRS_PER_CTA * SMEM_PER_PAIR;
 };
+
+// P-plane offset of (r, c): the fragment writes (rows g, columns 2t + h), the
+// row reads and the column reads of the epilogue are all conflict-free with
+// the XOR swizzle c ^ sw(r), sw(r) = r & 7 | ((r >> 1 ^ r >> 3) & 1) << 3 on the
+// low four column bits (found by exhaustive search over GF(2) row maps; a
+// plain padded stride leaves the writes 3-4-way conflicted). d < 16: padded.
+template <int DIM> __device__ __forceinline__ int p_at(int r, int c) {
+  if constexpr (DIM >= 16) return r * DIM + (c ^ ((r & 7) | ((((r >> 1) ^ (r >> 3)) & 1) << 3)));
+  else return r * (DIM + 1) + c;
+}
 
 // complex element (i, k) of the anti-Hermitian matrix stored packed at p (stride LDP)
 template <int LDP>
@@ -148,7 +157,7 @@ __device__ __forceinline__ void ah_elem(const double* p, int i, int k, double& r
 // fragments reused across a warp's WC column tiles, B fragments across its WR
 // row tiles); P is written back over the consumed inputs and h = P - P^dagger
 // is read out in the packed layout. ~70 KB per pair at d = 64.
-template <int DIM, int MINB = 2, int WR = CommAhShape<DIM>::WR, int WC = CommAhShape<DIM>::WC>
+template <int DIM, int MINB = 2, int WR = CommAhShape<DIM>::WR, int WC = CommAhShape<DIM>::WC, bool ASYNC = true>
 __global__ void __launch_bounds__(256, MINB)
 commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, double tol, bool normalize,
                      double* __restrict__ out, double* __restrict__ hnorm, int* __restrict__ is_null) {
@@ -176,12 +185,24 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
     pair_from_index(g0 + j, l, m);
     const double2* ga = reinterpret_cast<const double2*>(basis + l * D2);
     const double2* gb = reinterpret_cast<const double2*>(basis + m * D2);
-    for (int e = tip; e < D2 / 2; e += NT) {  // 16-byte loads; DIM even
+    // 16-byte pieces (DIM even); i even and LDP even keep them 16-byte
+    // aligned in shared memory. cp.async issues every piece before waiting:
+    // one memory latency per pair instead of one per loop trip.
+#pragma unroll
+    for (int e = tip; e < D2 / 2; e += NT) {
       const int i = (2 * e) % DIM, k = (2 * e) / DIM;
-      const double2 va = ga[e], vb = gb[e];
-      // i even, LDP even: 16-byte aligned, one conflict-free vector store each
-      *reinterpret_cast<double2*>(pa + i + k * LDP) = va;
-      *reinterpret_cast<double2*>(pb + i + k * LDP) = vb;
+      if constexpr (ASYNC) {
+        cp_async16(pa + i + k * LDP, ga + e, 16);
+        cp_async16(pb + i + k * LDP, gb + e, 16);
+      } else {
+        const double2 va = ga[e], vb = gb[e];
+        *reinterpret_cast<double2*>(pa + i + k * LDP) = va;
+        *reinterpret_cast<double2*>(pb + i + k * LDP) = vb;
+      }
+    }
+    if constexpr (ASYNC) {
+      cp_async_commit();
+      cp_async_wait<0>();
     }
   }
   __syncthreads();
@@ -214,9 +235,8 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
     }
   }
   __syncthreads();  // inputs consumed: P planes reuse the packed buffers
-  // P(i, k) re at pre[i*LDQ + k]: the epilogue reads P(k, i) along a row and
-  // P(i, k) down a column; an odd stride keeps both free of bank conflicts
-  constexpr int LDQ = S::LDQ;
+  // P(i, k) re at pre[p_at(i, k)]: the epilogue reads P(k, i) along a row and
+  // P(i, k) down a column
   double* pre = pa;
   double* pim = pb;
   if (active) {
@@ -227,8 +247,8 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
       for (int c = 0; c < WC; ++c)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          pre[(ti + g) * LDQ + (wc0 + c) * 8 + 2 * t + h] = cre[r][c][h];
-          pim[(ti + g) * LDQ + (wc0 + c) * 8 + 2 * t + h] = cim[r][c][h];
+          pre[p_at<DIM>(ti + g, (wc0 + c) * 8 + 2 * t + h)] = cre[r][c][h];
+          pim[p_at<DIM>(ti + g, (wc0 + c) * 8 + 2 * t + h)] = cim[r][c][h];
         }
     }
   }
@@ -242,9 +262,9 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
       if (e >= D2) break;
       const int i = e % DIM, k = e / DIM;
       double v;
-      if (i < k) v = pre[i * LDQ + k] - pre[k * LDQ + i];
-      else if (i > k) v = pim[k * LDQ + i] + pim[i * LDQ + k];
-      else v = 2.0 * pim[i * LDQ + i];
+      if (i < k) v = pre[p_at<DIM>(i, k)] - pre[p_at<DIM>(k, i)];
+      else if (i > k) v = pim[p_at<DIM>(k, i)] + pim[p_at<DIM>(i, k)];
+      else v = 2.0 * pim[p_at<DIM>(i, i)];
       hv[q] = v;
       sumsq += (i == k ? 1.0 : 2.0) * v * v;
     }

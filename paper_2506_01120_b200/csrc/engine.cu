@@ -27,6 +27,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <cudaTypedefs.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -52,6 +53,7 @@
 #include "block_gs.cuh"
 #include "commutator.cuh"
 #include "dgemm_dmma.cuh"
+#include "dgemm_tma.cuh"
 #include "pauli.cuh"
 #include "pauli_sum.cuh"
 #include "tiny.cuh"
@@ -389,6 +391,45 @@ template <bool KC, REpi E> void rgemm_attr_once() {
   func_attr_once(dgemm_dmma_kernel<KC, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, rg::smem_bytes<KC>());
 }
 
+// ---- TMA tensor maps for the packed-real projection GEMMs (dgemm_tma.cuh) ----
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+// LIECL_B200_TMA=0 selects the cp.async kernels (A/B comparisons).
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+bool tma_enabled() {
+  const char* e = std::getenv("LIECL_B200_TMA");
+  return !(e && e[0] == '0') && tma_encoder() != nullptr;
+}
+// rows x len doubles, row stride ld (K-contiguous operand): box {16, box_rows}
+bool tma_map_kc(CUtensorMap* m, const double* p, int64_t len, int64_t rows, int64_t ld, int box_rows) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) || (ld & 1) || len <= 0 || rows <= 0) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(len), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+  cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_rows)}, es[2] = {1, 1};
+  return tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// A(m, k) = p[k*ld + m] (M-contiguous operand), M a multiple of 16: 3-D {16, K, M/16}, box {16, 16, 8}
+bool tma_map_mc(CUtensorMap* m, const double* p, int64_t M, int64_t K, int64_t ld) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) || (ld & 1) || (M % 16) || M <= 0 || K <= 0) return false;
+  cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M / 16)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8, 128};
+  cuuint32_t box[3] = {16, 16, 8}, es[3] = {1, 1, 1};
+  return tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // P[n x count] (ld ldp) = alpha * Vw[:, 0:n]^T X   -- beta on the packed path
 void rgemm_project(liecl_b200_ctx* ctx, const double* Vw, int64_t n, int64_t D, const double* X, int count,
                    double* P, int64_t ldp, double alpha, int64_t ldv = -1, int64_t ldx = -1) {
@@ -399,7 +440,14 @@ void rgemm_project(liecl_b200_ctx* ctx, const double* Vw, int64_t n, int64_t D, 
   dim3 grid((n + rg::BM - 1) / rg::BM, (count + rg::BN - 1) / rg::BN);
   Timer t(ctx, 0, 2.0 * static_cast<double>(n) * static_cast<double>(D) * count);
   int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, D);
-  if (slices <= 1) {
+  CUtensorMap ma, mb;
+  if (slices <= 1 && tma_enabled() && (ldp & 1) == 0 && tma_map_kc(&ma, Vw, D, n, ldv, tg::BM) &&
+      tma_map_kc(&mb, X, D, count, ldx, tg::BN)) {
+    func_attr_once(dgemm_tma_kernel<true, REpi::kStoreScaled>, cudaFuncAttributeMaxDynamicSharedMemorySize, tg::SMEM);
+    dgemm_tma_kernel<true, REpi::kStoreScaled><<<grid, tg::THREADS, tg::SMEM, ctx->stream>>>(
+        ma, mb, static_cast<int>(n), count, static_cast<int>(D), P, ldp, alpha, nullptr, 0, nullptr, 0);
+    launched(ctx);
+  } else if (slices <= 1) {
     dgemm_dmma_kernel<true, REpi::kStoreScaled><<<grid, rg::THREADS, rg::smem_bytes<true>(), ctx->stream>>>(
         static_cast<int>(n), count, static_cast<int>(D), Vw, ldv, X, ldx, P, ldp, alpha, nullptr, 0, nullptr, 0, 0, 0);
     launched(ctx);
@@ -445,7 +493,15 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
   Timer t(ctx, 1, 2.0 * static_cast<double>(n) * static_cast<double>(D) * count);
   const int64_t kpad = (n + 1) & ~int64_t(1);  // even K: reads one zero row of V past an odd n
   int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, kpad);
-  if (slices <= 1) {
+  CUtensorMap ma, mb;
+  if (slices <= 1 && tma_enabled() && tma_map_mc(&ma, V, D, n, ldv) && tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
+    // K = n exactly: rows past the basis read as zeros (TMA out-of-bounds fill)
+    func_attr_once(dgemm_tma_kernel<false, REpi::kSubtractNorm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                   tg::SMEM);
+    dgemm_tma_kernel<false, REpi::kSubtractNorm><<<grid, tg::THREADS, tg::SMEM, ctx->stream>>>(
+        ma, mb, static_cast<int>(D), count, static_cast<int>(n), R, ldx, 1.0, X, ldx, partial, d);
+    launched(ctx);
+  } else if (slices <= 1) {
     dgemm_dmma_kernel<false, REpi::kSubtractNorm><<<grid, rg::THREADS, rg::smem_bytes<false>(), ctx->stream>>>(
         static_cast<int>(D), count, static_cast<int>(kpad), V, ldv, P, ldp, R, ldx, 1.0, X, ldx, partial, d, 0, 0);
     launched(ctx);

@@ -428,3 +428,20 @@ def test_candidate_prefetch_matches_direct_checks():
         got = ses.check_candidates(bufs[k % 2].data_ptr(), n=30)
         assert np.array_equal(got[0], want[0])
         assert np.allclose(got[1], want[1], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("make", [w.config0, w.config1], ids=["c0", "c1"])
+def test_reject_norms_are_pass1_bounds(golden, make):
+    """A certified reject (pass-1 residual <= tol/20) reports its pass-1 norm,
+    not the reference's second-pass norm (R:src/closure.cpp:277-280): an upper
+    bound of it up to O(eps), and both are far below tol."""
+    cfg = make()
+    method = liecl.Method.orthonorm_dimonly
+    meta, g = golden(f"{cfg.name}_{liecl.to_string(method)}")
+    res = liecl.closure_dense_arrays(cfg.generators, cfg.d, method,
+                                     liecl.ClosureConfig(tolerance=cfg.tol, record_log=True))
+    rej = (g["log_indep"] == 0) & (g["log_null"] == 0)
+    assert rej.any()
+    rn, ref = res.decision_log["residual_norm"][rej], g["log_rn"][rej]
+    assert (rn <= cfg.tol / 20 + 1e-14).all() and (ref <= cfg.tol / 20 + 1e-14).all()
+    assert (rn >= ref - 1e-14).all()

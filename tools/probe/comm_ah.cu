@@ -16,11 +16,11 @@ using namespace liecl_b200;
 
 constexpr int DIM = 64, D2 = DIM * DIM, NB = 4095, CNT = 8192;
 
-template <int MINB, int WR, int WC>
+template <int MINB, int WR, int WC, bool ASYNC = true>
 double run(const char* name, const double* basis, int64_t g0, double* out, double* hn, int* nul,
            std::vector<double>& h_out, std::vector<double>& h_hn) {
   using S = CommAhShape<DIM, WR, WC>;
-  auto k = commutator_ah_kernel<DIM, MINB, WR, WC>;
+  auto k = commutator_ah_kernel<DIM, MINB, WR, WC, ASYNC>;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
   CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   cudaFuncAttributes fa;
@@ -67,12 +67,14 @@ int main() {
   CK(cudaMemcpy(basis, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice));
   const int64_t g0 = pair_index(1024, 0);
   std::vector<double> ro, rh, o, h;
-  run<3, 1, 8>("row_strip_minb3", basis, g0, out, hn, nul, ro, rh);
+  run<3, 1, 8, false>("row_strip_minb3_sync", basis, g0, out, hn, nul, ro, rh);
   auto same = [&](const char* n) {
     const bool eq = !std::memcmp(o.data(), ro.data(), o.size() * 8) && !std::memcmp(h.data(), rh.data(), h.size() * 8);
     printf("  %s bit-identical: %s\n", n, eq ? "yes" : "NO");
   };
+  run<3, 1, 8>("row_strip_minb3", basis, g0, out, hn, nul, o, h); same("row_strip_minb3");
   run<2, 1, 8>("row_strip_minb2", basis, g0, out, hn, nul, o, h); same("row_strip_minb2");
+  run<2, 2, 4, false>("2x4_minb2_sync", basis, g0, out, hn, nul, o, h); same("2x4_minb2_sync");
   run<2, 2, 4>("2x4_minb2", basis, g0, out, hn, nul, o, h); same("2x4_minb2");
   run<3, 2, 4>("2x4_minb3", basis, g0, out, hn, nul, o, h); same("2x4_minb3");
   run<2, 4, 2>("4x2_minb2", basis, g0, out, hn, nul, o, h); same("4x2_minb2");
