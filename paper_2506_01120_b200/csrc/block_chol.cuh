@@ -53,6 +53,20 @@ template <class T> __device__ __forceinline__ T bc_one();
 template <> __device__ __forceinline__ double bc_one<double>() { return 1.0; }
 template <> __device__ __forceinline__ double2 bc_one<double2>() { return make_double2(1.0, 0.0); }
 
+// The one-CTA kernels below give every column four lanes (kBcThreads =
+// 4 kBcMax): a column's dot products are split over its lanes (k = sub, sub+4,
+// ...) and summed with two shuffles, so a sequential step costs ~a/4 dependent
+// multiply-adds instead of ~a.
+constexpr int kBcLanes = 4, kBcThreads = kBcLanes * kBcMax;
+// (groups take branches as a whole; the shuffles name only the group's lanes)
+__device__ __forceinline__ unsigned bc_group_mask() { return 0xFu << (threadIdx.x & 28); }
+__device__ __forceinline__ double bc_group_sum(double v) {
+  const unsigned m = bc_group_mask();
+  v += __shfl_xor_sync(m, v, 1);
+  return v + __shfl_xor_sync(m, v, 2);
+}
+__device__ __forceinline__ double2 bc_group_sum(double2 v) { return make_double2(bc_group_sum(v.x), bc_group_sum(v.y)); }
+
 struct BcDecision {
   int nacc;          // accepts in the block
   int ntent;         // tentative rejects (explicit check pending)
@@ -68,7 +82,7 @@ struct BcDecision {
 // survivors: rn2, or sqrt(s) for certified accepts -- replaced by the CholQR2
 // norm later), R1 (accepted x accepted upper factor, ld kBcMax) and `dec`.
 template <class T>
-__global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__ G, int ldg, int nb,
+__global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restrict__ G, int ldg, int nb,
                                                             const double* __restrict__ rn2, double tol,
                                                             int cap_left, int* __restrict__ flags,
                                                             double* __restrict__ rn, T* __restrict__ R1,
@@ -84,15 +98,16 @@ __global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__
   __shared__ double s[kBcMax];
   __shared__ int acc_list[kBcMax];
   __shared__ int s_ind, s_stop;
-  const int t = threadIdx.x;
-  for (int e = t; e < nb * nb; e += blockDim.x) Gs[(e % nb) + (e / nb) * kBcMax] = G[(e % nb) + static_cast<int64_t>(e / nb) * ldg];
+  const int tid = threadIdx.x;
+  const int t = tid >> 2, sub = tid & 3;  // column t, lane sub of its group
+  for (int e = tid; e < nb * nb; e += blockDim.x) Gs[(e % nb) + (e / nb) * kBcMax] = G[(e % nb) + static_cast<int64_t>(e / nb) * ldg];
   __syncthreads();
-  if (t < nb) s[t] = bc_re(Gs[t + t * kBcMax]);
+  if (sub == 0 && t < nb) s[t] = bc_re(Gs[t + t * kBcMax]);
   int acc = 0, tent = 0;
-  if (t == 0) dec->cap_hit = -1;
+  if (tid == 0) dec->cap_hit = -1;
   __syncthreads();
   for (int q = 0; q < nb; ++q) {
-    if (t == 0) {
+    if (tid == 0) {
       const double r2 = rn2[q];
       const bool recheck = acc > 0 && r2 > tol;
       int ind;
@@ -132,15 +147,18 @@ __global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__
     if (s_ind) {
       // row `acc` of Z: the new accept's R entries against every later column
       const double lqq = sqrt(s[q]);  // == rn2_q for the block's first accept
-      if (t == 0) acc_list[acc] = q;
-      if (t > q && t < nb) {
-        T z = Gs[q + t * kBcMax];
-        for (int a = 0; a < acc; ++a) z = bc_sub(z, bc_mul(bc_conj(Zs[a * kBcMax + q]), Zs[a * kBcMax + t]));
-        z = bc_scale(z, 1.0 / lqq);
-        Zs[acc * kBcMax + t] = z;
-        s[t] -= bc_abs2(z);
+      if (tid == 0) acc_list[acc] = q;
+      if (t > q && t < nb) {  // whole 4-lane groups: the shuffles stay inside active lanes
+        T part = bc_zero<T>();
+        for (int a = sub; a < acc; a += kBcLanes) part = bc_sub(part, bc_mul(bc_conj(Zs[a * kBcMax + q]), Zs[a * kBcMax + t]));
+        part = bc_group_sum(part);
+        if (sub == 0) {
+          const T z = bc_scale(bc_sub(Gs[q + t * kBcMax], bc_scale(part, -1.0)), 1.0 / lqq);
+          Zs[acc * kBcMax + t] = z;
+          s[t] -= bc_abs2(z);
+        }
       }
-      if (t == 0) {  // the diagonal (real, positive); no thread reads row `acc` in this phase
+      if (tid == 0) {  // the diagonal (real, positive); no thread reads row `acc` in this phase
         if constexpr (sizeof(T) == sizeof(double)) Zs[acc * kBcMax + q] = lqq;
         else Zs[acc * kBcMax + q] = T{lqq, 0.0};
       }
@@ -150,12 +168,12 @@ __global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__
   }
   __syncthreads();
   // R1[a'][a] = Z[a'][q_a] (upper triangular, ld kBcMax)
-  for (int e = t; e < acc * acc; e += blockDim.x) {
+  for (int e = tid; e < acc * acc; e += blockDim.x) {
     const int ap = e % acc, a = e / acc;
     R1[ap + a * kBcMax] = ap <= a ? Zs[ap * kBcMax + acc_list[a]] : bc_zero<T>();
   }
-  if (t < acc) dec->acc[t] = acc_list[t];
-  if (t == 0) {
+  if (tid < acc) dec->acc[tid] = acc_list[tid];
+  if (tid == 0) {
     dec->nacc = acc;
     dec->ntent = tent;
   }
@@ -164,32 +182,38 @@ __global__ void __launch_bounds__(kBcMax) bc_decide_kernel(const T* __restrict__
 // Cholesky G = R^H R (upper R, ld kBcMax) of an a x a Hermitian matrix
 // (a <= 64), one CTA; diag[a] receives R_aa.
 template <class T>
-__global__ void __launch_bounds__(kBcMax) bc_cholesky_kernel(const T* __restrict__ G, int ldg, int a,
-                                                              T* __restrict__ R, double* __restrict__ diag) {
+__global__ void __launch_bounds__(kBcThreads) bc_cholesky_kernel(const T* __restrict__ G, int ldg, int a,
+                                                                  T* __restrict__ R, double* __restrict__ diag) {
   extern __shared__ __align__(16) unsigned char bc_smem[];
   T* Rs = reinterpret_cast<T*>(bc_smem);  // R(i, j) = Rs[i * kBcMax + j]: kBcMax^2 T (dynamic), flat (see above)
   T* Gs = Rs + kBcMax * kBcMax;            // G staged in shared memory
-  const int t = threadIdx.x;
-  for (int e = t; e < a * a; e += blockDim.x) Gs[(e % a) + (e / a) * kBcMax] = G[(e % a) + static_cast<int64_t>(e / a) * ldg];
+  const int tid = threadIdx.x;
+  const int t = tid >> 2, sub = tid & 3;
+  for (int e = tid; e < a * a; e += blockDim.x) Gs[(e % a) + (e / a) * kBcMax] = G[(e % a) + static_cast<int64_t>(e / a) * ldg];
   __syncthreads();
   for (int i = 0; i < a; ++i) {
-    if (t == 0) {
-      double s = bc_re(Gs[i + i * kBcMax]);
-      for (int k = 0; k < i; ++k) s -= bc_abs2(Rs[k * kBcMax + i]);
-      const double r = sqrt(fmax(s, 0.0));
-      if constexpr (sizeof(T) == sizeof(double)) Rs[i * kBcMax + i] = r;
-      else Rs[i * kBcMax + i] = T{r, 0.0};
-      diag[i] = r;
+    if (t == i) {  // one 4-lane group: the diagonal
+      double part = 0.0;
+      for (int k = sub; k < i; k += kBcLanes) part += bc_abs2(Rs[k * kBcMax + i]);
+      part = bc_group_sum(part);
+      if (sub == 0) {
+        const double r = sqrt(fmax(bc_re(Gs[i + i * kBcMax]) - part, 0.0));
+        if constexpr (sizeof(T) == sizeof(double)) Rs[i * kBcMax + i] = r;
+        else Rs[i * kBcMax + i] = T{r, 0.0};
+        diag[i] = r;
+      }
     }
     __syncthreads();
     if (t > i && t < a) {
-      T z = Gs[i + t * kBcMax];
-      for (int k = 0; k < i; ++k) z = bc_sub(z, bc_mul(bc_conj(Rs[k * kBcMax + i]), Rs[k * kBcMax + t]));
-      Rs[i * kBcMax + t] = bc_scale(z, 1.0 / bc_re(Rs[i * kBcMax + i]));
+      T part = bc_zero<T>();
+      for (int k = sub; k < i; k += kBcLanes) part = bc_sub(part, bc_mul(bc_conj(Rs[k * kBcMax + i]), Rs[k * kBcMax + t]));
+      part = bc_group_sum(part);
+      if (sub == 0)
+        Rs[i * kBcMax + t] = bc_scale(bc_sub(Gs[i + t * kBcMax], bc_scale(part, -1.0)), 1.0 / bc_re(Rs[i * kBcMax + i]));
     }
     __syncthreads();
   }
-  for (int e = t; e < a * a; e += blockDim.x) {
+  for (int e = tid; e < a * a; e += blockDim.x) {
     const int i = e % a, j = e / a;
     R[i + j * kBcMax] = i <= j ? Rs[i * kBcMax + j] : bc_zero<T>();
   }
@@ -211,20 +235,26 @@ __global__ void bc_mask_kernel(double* __restrict__ P, int64_t ldp, int rows, in
 // back-substitutes column j. Rows a .. 2*ceil(a/2)-1 of T are zero (the real
 // GEMM reads an even K).
 template <class T>
-__global__ void __launch_bounds__(kBcMax) bc_tri_inverse_kernel(const T* __restrict__ R, int a, T* __restrict__ Tinv) {
+__global__ void __launch_bounds__(kBcThreads) bc_tri_inverse_kernel(const T* __restrict__ R, int a, T* __restrict__ Tinv) {
   extern __shared__ __align__(16) unsigned char bc_smem[];
   T* Rs = reinterpret_cast<T*>(bc_smem);  // R(i, j) = Rs[i + j * kBcMax]
   T* Ts = Rs + kBcMax * kBcMax;           // T(i, j) = Ts[i + j * kBcMax]
-  const int j = threadIdx.x;
-  for (int e = j; e < a * a; e += blockDim.x) Rs[(e % a) + (e / a) * kBcMax] = R[(e % a) + (e / a) * kBcMax];
+  const int tid = threadIdx.x;
+  const int j = tid >> 2, sub = tid & 3;  // column j back-substituted by one 4-lane group
+  for (int e = tid; e < a * a; e += blockDim.x) Rs[(e % a) + (e / a) * kBcMax] = R[(e % a) + (e / a) * kBcMax];
   __syncthreads();
   if (j < a) {
-    if constexpr (sizeof(T) == sizeof(double)) Ts[j + j * kBcMax] = 1.0 / bc_re(Rs[j + j * kBcMax]);
-    else Ts[j + j * kBcMax] = T{1.0 / bc_re(Rs[j + j * kBcMax]), 0.0};
+    if (sub == 0) {
+      if constexpr (sizeof(T) == sizeof(double)) Ts[j + j * kBcMax] = 1.0 / bc_re(Rs[j + j * kBcMax]);
+      else Ts[j + j * kBcMax] = T{1.0 / bc_re(Rs[j + j * kBcMax]), 0.0};
+    }
+    __syncwarp(bc_group_mask());
     for (int i = j - 1; i >= 0; --i) {
-      T acc = bc_zero<T>();
-      for (int k = i + 1; k <= j; ++k) acc = bc_sub(acc, bc_mul(Rs[i + k * kBcMax], Ts[k + j * kBcMax]));
-      Ts[i + j * kBcMax] = bc_scale(acc, 1.0 / bc_re(Rs[i + i * kBcMax]));
+      T part = bc_zero<T>();
+      for (int k = i + 1 + sub; k <= j; k += kBcLanes) part = bc_sub(part, bc_mul(Rs[i + k * kBcMax], Ts[k + j * kBcMax]));
+      part = bc_group_sum(part);
+      if (sub == 0) Ts[i + j * kBcMax] = bc_scale(part, 1.0 / bc_re(Rs[i + i * kBcMax]));
+      __syncwarp(bc_group_mask());
     }
   }
   __syncthreads();

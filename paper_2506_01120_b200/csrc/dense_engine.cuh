@@ -1040,7 +1040,7 @@ private:
     };
     const int ldg = gram(Y, nb, bc_g_.p);
     const int cap_left = static_cast<int>(std::min<int64_t>(kBcMax + 1, std::max<int64_t>(0, cap_ - basis_size())));
-    bc_decide_kernel<T><<<1, kBcMax, bc_smem_bytes<T>(), ctx_->stream>>>(
+    bc_decide_kernel<T><<<1, kBcThreads, bc_smem_bytes<T>(), ctx_->stream>>>(
         T_(bc_g_.p), ldg, nb, rn2_.p + k, tol_, cap_left, bgs_flags_.p, bgs_rn_.p, T_(bc_r1_.p), bc_dec_.p);
     launched(ctx_); dbg_sync("block_chol 2");
     CU(cudaMemcpyAsync(h_bc_dec_.p, bc_dec_.p, sizeof(BcDecision), cudaMemcpyDeviceToHost, ctx_->stream));
@@ -1061,7 +1061,7 @@ private:
         if (a_even > a) CU(cudaMemsetAsync(bc_ya_.p + a * W, 0, W * sizeof(double), ctx_->stream));
       }
       auto times_inverse = [&](const double* A, const double* R, double* out) {
-        bc_tri_inverse_kernel<T><<<1, kBcMax, bc_smem_bytes<T>(), ctx_->stream>>>(T_(const_cast<double*>(R)), a,
+        bc_tri_inverse_kernel<T><<<1, kBcThreads, bc_smem_bytes<T>(), ctx_->stream>>>(T_(const_cast<double*>(R)), a,
                                                                                    T_(bc_tinv_.p));
         launched(ctx_); dbg_sync("block_chol inverse");
         if (len == 0) return;
@@ -1074,7 +1074,7 @@ private:
       times_inverse(bc_ya_.p, bc_r1_.p, bc_w_.p);
       if (a_even > a) CU(cudaMemsetAsync(bc_w_.p + a * W, 0, W * sizeof(double), ctx_->stream));
       const int ldg2 = gram(bc_w_.p, a, bc_g_.p);
-      bc_cholesky_kernel<T><<<1, kBcMax, bc_smem_bytes<T>(), ctx_->stream>>>(T_(bc_g_.p), ldg2, a, T_(bc_r2_.p),
+      bc_cholesky_kernel<T><<<1, kBcThreads, bc_smem_bytes<T>(), ctx_->stream>>>(T_(bc_g_.p), ldg2, a, T_(bc_r2_.p),
                                                                                bc_diag_.p);
       launched(ctx_); dbg_sync("block_chol 4");
       times_inverse(bc_w_.p, bc_r2_.p, Vn);

@@ -54,6 +54,7 @@
 #include "commutator.cuh"
 #include "dgemm_dmma.cuh"
 #include "dgemm_tma.cuh"
+#include "zgemm_tma.cuh"
 #include "pauli.cuh"
 #include "pauli_sum.cuh"
 #include "tiny.cuh"
@@ -316,82 +317,7 @@ int split_slices(int64_t tiles, int64_t K) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, K / 256)));
 }
 
-// P[n x count] = (1/d) V[:, 0:n]^H X      (ldc = n)
-// (ldv / ldx: element strides of V's and X's columns when they are slices of
-// longer vectors -- the D-sharded closure loop; default D)
-void gemm_project(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, const double2* X, int count,
-                  double2* P, double alpha, int64_t ldv = -1, int64_t ldx = -1) {
-  if (n == 0 || count == 0) return;
-  if (ldv < 0) ldv = D;
-  if (ldx < 0) ldx = D;
-  gemm_attr_once<true, true, Epilogue::kStoreScaled>();
-  dim3 grid((n + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
-  Timer t(ctx, 0, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
-  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, D);
-  if (slices <= 1) {
-    zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
-        static_cast<int>(n), count, static_cast<int>(D), V, ldv, X, ldx, P, n, alpha, nullptr, 0, nullptr, 0, 0);
-    launched(ctx);
-  } else {
-    const int chunk = static_cast<int>(((D + slices - 1) / slices + zg::BK - 1) / zg::BK * zg::BK);
-    slices = static_cast<int>((D + chunk - 1) / chunk);
-    const int64_t stride = n * count;
-    ctx->splitk_ws.ensure(static_cast<size_t>(slices * stride));
-    grid.z = slices;
-    zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
-        static_cast<int>(n), count, static_cast<int>(D), V, ldv, X, ldx, ctx->splitk_ws.p, n, 1.0, nullptr, 0, nullptr,
-        chunk, stride);
-    launched(ctx);
-    splitk_reduce_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>((stride + 255) / 256, 1024)), 256, 0,
-                                 ctx->stream>>>(ctx->splitk_ws.p, slices, stride, stride, alpha, P);
-    launched(ctx);
-  }
-  t.stop();
-}
-
-// R = X - V[:, 0:n] P ; partial[mt][b] = sum_rows |R|^2
-void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, const double2* P, const double2* X,
-                   int count, double2* R, double* partial, int64_t ldv = -1, int64_t ldx = -1) {
-  if (ldv < 0) ldv = D;
-  if (ldx < 0) ldx = D;  // X and R
-  gemm_attr_once<false, false, Epilogue::kSubtractNorm>();
-  dim3 grid((D + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
-  Timer t(ctx, 1, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
-  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, n);
-  if (slices <= 1) {
-    zgemm_dmma_kernel<false, false, Epilogue::kSubtractNorm>
-        <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n),
-                                                                       V, ldv, P, n, R, ldx, 1.0, X, ldx, partial, 0, 0);
-    launched(ctx);
-  } else {
-    gemm_attr_once<false, false, Epilogue::kStoreScaled>();
-    const int chunk = static_cast<int>(((n + slices - 1) / slices + zg::BK - 1) / zg::BK * zg::BK);
-    slices = static_cast<int>((n + chunk - 1) / chunk);
-    const int64_t stride = D * count;
-    ctx->splitk_ws.ensure(static_cast<size_t>(slices * stride));
-    grid.z = slices;
-    zgemm_dmma_kernel<false, false, Epilogue::kStoreScaled>
-        <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n),
-                                                                       V, ldv, P, n, ctx->splitk_ws.p, D, 1.0, nullptr,
-                                                                       0, nullptr, chunk, stride);
-    launched(ctx);
-    splitk_reduce_subtract_kernel<<<dim3(static_cast<unsigned>((D + zg::BM - 1) / zg::BM), count), zg::BM, 0,
-                                    ctx->stream>>>(ctx->splitk_ws.p, slices, stride, static_cast<int>(D), count, X, R,
-                                                   partial, ldx);
-    launched(ctx);
-  }
-  t.stop();
-}
-
-// --------------------------------------------------------- dense engine ---
-
-// ------------------------------------------------ packed-real GEMM launch ---
-
-template <bool KC, REpi E> void rgemm_attr_once() {
-  func_attr_once(dgemm_dmma_kernel<KC, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, rg::smem_bytes<KC>());
-}
-
-// ---- TMA tensor maps for the packed-real projection GEMMs (dgemm_tma.cuh) ----
+// ---- TMA tensor maps for the projection GEMMs (dgemm_tma.cuh, zgemm_tma.cuh) ----
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 // LIECL_B200_TMA=0 selects the cp.async kernels (A/B comparisons).
 PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
@@ -428,6 +354,110 @@ bool tma_map_mc(CUtensorMap* m, const double* p, int64_t M, int64_t K, int64_t l
   return tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// complex operands as doubles: rows x len complex, row stride ld complex: box {16 doubles, 64}
+bool tma_zmap_kc(CUtensorMap* m, const double2* p, int64_t len, int64_t rows, int64_t ld) {
+  return tma_map_kc(m, reinterpret_cast<const double*>(p), 2 * len, rows, 2 * ld, 64);
+}
+// A(m, k) = p[k*ld + m] complex, M a multiple of 8: 3-D {16, K, M/8} doubles, box {16, 8, 8}
+bool tma_zmap_mc(CUtensorMap* m, const double2* p, int64_t M, int64_t K, int64_t ld) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) || (M % 8) || M <= 0 || K <= 0) return false;
+  cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M / 8)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 16, 128};
+  cuuint32_t box[3] = {16, 8, 8}, es[3] = {1, 1, 1};
+  return tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(p), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// P[n x count] = (1/d) V[:, 0:n]^H X      (ldc = n)
+// (ldv / ldx: element strides of V's and X's columns when they are slices of
+// longer vectors -- the D-sharded closure loop; default D)
+void gemm_project(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, const double2* X, int count,
+                  double2* P, double alpha, int64_t ldv = -1, int64_t ldx = -1) {
+  if (n == 0 || count == 0) return;
+  if (ldv < 0) ldv = D;
+  if (ldx < 0) ldx = D;
+  gemm_attr_once<true, true, Epilogue::kStoreScaled>();
+  dim3 grid((n + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
+  Timer t(ctx, 0, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, D);
+  CUtensorMap ma, mb;
+  if (slices <= 1 && tma_enabled() && tma_zmap_kc(&ma, V, D, n, ldv) && tma_zmap_kc(&mb, X, D, count, ldx)) {
+    func_attr_once(zgemm_tma_kernel<true, true, Epilogue::kStoreScaled>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                   ztg::SMEM);
+    zgemm_tma_kernel<true, true, Epilogue::kStoreScaled><<<grid, ztg::THREADS, ztg::SMEM, ctx->stream>>>(
+        ma, mb, static_cast<int>(n), count, static_cast<int>(D), P, n, alpha, nullptr, 0, nullptr);
+    launched(ctx);
+  } else if (slices <= 1) {
+    zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
+        static_cast<int>(n), count, static_cast<int>(D), V, ldv, X, ldx, P, n, alpha, nullptr, 0, nullptr, 0, 0);
+    launched(ctx);
+  } else {
+    const int chunk = static_cast<int>(((D + slices - 1) / slices + zg::BK - 1) / zg::BK * zg::BK);
+    slices = static_cast<int>((D + chunk - 1) / chunk);
+    const int64_t stride = n * count;
+    ctx->splitk_ws.ensure(static_cast<size_t>(slices * stride));
+    grid.z = slices;
+    zgemm_dmma_kernel<true, true, Epilogue::kStoreScaled><<<grid, zg::THREADS, zg::smem_bytes<true>(), ctx->stream>>>(
+        static_cast<int>(n), count, static_cast<int>(D), V, ldv, X, ldx, ctx->splitk_ws.p, n, 1.0, nullptr, 0, nullptr,
+        chunk, stride);
+    launched(ctx);
+    splitk_reduce_scale_kernel<<<static_cast<unsigned>(std::min<int64_t>((stride + 255) / 256, 1024)), 256, 0,
+                                 ctx->stream>>>(ctx->splitk_ws.p, slices, stride, stride, alpha, P);
+    launched(ctx);
+  }
+  t.stop();
+}
+
+// R = X - V[:, 0:n] P ; partial[mt][b] = sum_rows |R|^2
+void gemm_subtract(liecl_b200_ctx* ctx, const double2* V, int64_t n, int64_t D, const double2* P, const double2* X,
+                   int count, double2* R, double* partial, int64_t ldv = -1, int64_t ldx = -1) {
+  if (ldv < 0) ldv = D;
+  if (ldx < 0) ldx = D;  // X and R
+  gemm_attr_once<false, false, Epilogue::kSubtractNorm>();
+  dim3 grid((D + zg::BM - 1) / zg::BM, (count + zg::BN - 1) / zg::BN);
+  Timer t(ctx, 1, 8.0 * static_cast<double>(n) * static_cast<double>(D) * count);
+  int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, n);
+  CUtensorMap ma, mb;
+  if (slices <= 1 && tma_enabled() && tma_zmap_mc(&ma, V, D, n, ldv) && tma_zmap_kc(&mb, P, n, count, n)) {
+    func_attr_once(zgemm_tma_kernel<false, false, Epilogue::kSubtractNorm>,
+                   cudaFuncAttributeMaxDynamicSharedMemorySize, ztg::SMEM);
+    zgemm_tma_kernel<false, false, Epilogue::kSubtractNorm><<<grid, ztg::THREADS, ztg::SMEM, ctx->stream>>>(
+        ma, mb, static_cast<int>(D), count, static_cast<int>(n), R, ldx, 1.0, X, ldx, partial);
+    launched(ctx);
+  } else if (slices <= 1) {
+    zgemm_dmma_kernel<false, false, Epilogue::kSubtractNorm>
+        <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n),
+                                                                       V, ldv, P, n, R, ldx, 1.0, X, ldx, partial, 0, 0);
+    launched(ctx);
+  } else {
+    gemm_attr_once<false, false, Epilogue::kStoreScaled>();
+    const int chunk = static_cast<int>(((n + slices - 1) / slices + zg::BK - 1) / zg::BK * zg::BK);
+    slices = static_cast<int>((n + chunk - 1) / chunk);
+    const int64_t stride = D * count;
+    ctx->splitk_ws.ensure(static_cast<size_t>(slices * stride));
+    grid.z = slices;
+    zgemm_dmma_kernel<false, false, Epilogue::kStoreScaled>
+        <<<grid, zg::THREADS, zg::smem_bytes<false>(), ctx->stream>>>(static_cast<int>(D), count, static_cast<int>(n),
+                                                                       V, ldv, P, n, ctx->splitk_ws.p, D, 1.0, nullptr,
+                                                                       0, nullptr, chunk, stride);
+    launched(ctx);
+    splitk_reduce_subtract_kernel<<<dim3(static_cast<unsigned>((D + zg::BM - 1) / zg::BM), count), zg::BM, 0,
+                                    ctx->stream>>>(ctx->splitk_ws.p, slices, stride, static_cast<int>(D), count, X, R,
+                                                   partial, ldx);
+    launched(ctx);
+  }
+  t.stop();
+}
+
+// --------------------------------------------------------- dense engine ---
+
+// ------------------------------------------------ packed-real GEMM launch ---
+
+template <bool KC, REpi E> void rgemm_attr_once() {
+  func_attr_once(dgemm_dmma_kernel<KC, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, rg::smem_bytes<KC>());
 }
 
 // P[n x count] (ld ldp) = alpha * Vw[:, 0:n]^T X   -- beta on the packed path

@@ -49,7 +49,7 @@ int main() {
     CK(cudaMemcpy(dG, G.data(), 64 * 64 * 8, cudaMemcpyHostToDevice));
     CK(cudaFuncSetAttribute(bc_cholesky_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bc_smem_bytes<double>()));
     if (getenv("DBG")) chol_dbg<<<1, kBcMax, 32768>>>(dG, a, a, dR, dd);
-    else bc_cholesky_kernel<double><<<1, kBcMax, bc_smem_bytes<double>()>>>(dG, a, a, dR, dd);
+    else bc_cholesky_kernel<double><<<1, kBcThreads, bc_smem_bytes<double>()>>>(dG, a, a, dR, dd);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     std::vector<double> R(64 * 64);
