@@ -35,17 +35,69 @@ namespace psum {
 using pauli::C2;
 using pauli::cadd;
 using pauli::cmul;
-constexpr unsigned long long kInvalid = ~0ull;  // commuting product (sorts last)
-constexpr double kDropTolerance = 1e-14;       // R:include/liecl/pauli.hpp:73
+constexpr double kDropTolerance = 1e-14;  // R:include/liecl/pauli.hpp:73
 
-__device__ __forceinline__ uint64_t key_x(unsigned long long k) { return k & 0xffffffffull; }
-__device__ __forceinline__ uint64_t key_z(unsigned long long k) { return k >> 32; }
+// ---- string keys -------------------------------------------------------------
+// Every kernel below is a template over the key type K:
+//  * narrow (1..31 qubits): unsigned long long x | z << 32, whose numeric
+//    order is the reference's (z, x) order (PauliStringLess);
+//  * wide (32..63 qubits): WKey {x, z}, ordered by (z, x).
+// Both reserve all ones as the marker of a commuting product (sorts last) and
+// of a free hash slot; no string of <= 63 qubits reaches it. Index keys (basis
+// element l, the beta merges) live in the same arrays (kfrom_index / kindex).
+struct __align__(16) WKey {
+  unsigned long long x, z;
+};
+
+__host__ __device__ __forceinline__ uint64_t kx(unsigned long long k) { return k & 0xffffffffull; }
+__host__ __device__ __forceinline__ uint64_t kz(unsigned long long k) { return k >> 32; }
+__host__ __device__ __forceinline__ uint64_t kx(const WKey& k) { return k.x; }
+__host__ __device__ __forceinline__ uint64_t kz(const WKey& k) { return k.z; }
+__host__ __device__ __forceinline__ bool keq(unsigned long long a, unsigned long long b) { return a == b; }
+__host__ __device__ __forceinline__ bool keq(const WKey& a, const WKey& b) { return a.x == b.x && a.z == b.z; }
+__host__ __device__ __forceinline__ bool kless(unsigned long long a, unsigned long long b) { return a < b; }
+__host__ __device__ __forceinline__ bool kless(const WKey& a, const WKey& b) {
+  return a.z < b.z || (a.z == b.z && a.x < b.x);
+}
+__host__ __device__ __forceinline__ unsigned long long kxor(unsigned long long a, unsigned long long b) { return a ^ b; }
+__host__ __device__ __forceinline__ WKey kxor(const WKey& a, const WKey& b) { return {a.x ^ b.x, a.z ^ b.z}; }
+__host__ __device__ __forceinline__ bool kmarked(unsigned long long k) { return k == ~0ull; }
+__host__ __device__ __forceinline__ bool kmarked(const WKey& k) { return (k.x & k.z) == ~0ull; }
+__host__ __device__ __forceinline__ int64_t kindex(unsigned long long k) { return static_cast<int64_t>(k); }
+__host__ __device__ __forceinline__ int64_t kindex(const WKey& k) { return static_cast<int64_t>(k.x); }
+__device__ __forceinline__ uint64_t khash(unsigned long long k) { return pauli::mix(k); }
+__device__ __forceinline__ uint64_t khash(const WKey& k) { return pauli::mix2(k.x, k.z); }
+__device__ __forceinline__ unsigned long long kcas(unsigned long long* p, unsigned long long cmp,
+                                                   unsigned long long v) {
+  return atomicCAS(p, cmp, v);
+}
+__device__ __forceinline__ WKey kcas(WKey* p, WKey cmp, WKey v) {
+  const unsigned __int128 c = (static_cast<unsigned __int128>(cmp.z) << 64) | cmp.x;
+  const unsigned __int128 w = (static_cast<unsigned __int128>(v.z) << 64) | v.x;
+  const unsigned __int128 r = atomicCAS(reinterpret_cast<unsigned __int128*>(p), c, w);
+  return {static_cast<unsigned long long>(r), static_cast<unsigned long long>(r >> 64)};
+}
+template <class K> __host__ __device__ __forceinline__ K kpack(uint64_t x, uint64_t z);
+template <> __host__ __device__ __forceinline__ unsigned long long kpack<unsigned long long>(uint64_t x, uint64_t z) {
+  return static_cast<unsigned long long>(x) | (static_cast<unsigned long long>(z) << 32);
+}
+template <> __host__ __device__ __forceinline__ WKey kpack<WKey>(uint64_t x, uint64_t z) { return {x, z}; }
+template <class K> __host__ __device__ __forceinline__ K kmarker() { return kpack<K>(~0ull, ~0ull) ; }
+template <> __host__ __device__ __forceinline__ unsigned long long kmarker<unsigned long long>() { return ~0ull; }
+template <class K> __host__ __device__ __forceinline__ K kfrom_index(int64_t l);
+template <> __host__ __device__ __forceinline__ unsigned long long kfrom_index<unsigned long long>(int64_t l) {
+  return static_cast<unsigned long long>(l);
+}
+template <> __host__ __device__ __forceinline__ WKey kfrom_index<WKey>(int64_t l) {
+  return {static_cast<unsigned long long>(l), 0ull};
+}
 
 // Bracket products of cursor pairs [g0, g0 + cnt): one block per pair,
 // product q = ia * |b| + ib at off[p] + q (a = basis[l], b = basis[m]).
+template <class K>
 __global__ void products_kernel(int64_t g0, int cnt, const int* __restrict__ off, const int64_t* __restrict__ boff,
-                                const unsigned long long* __restrict__ bkey, const C2* __restrict__ bval,
-                                unsigned long long* __restrict__ out_key, C2* __restrict__ out_val) {
+                                const K* __restrict__ bkey, const C2* __restrict__ bval, K* __restrict__ out_key,
+                                C2* __restrict__ out_val) {
   const int p = blockIdx.x;
   if (p >= cnt) return;
   int64_t l, m;
@@ -55,14 +107,14 @@ __global__ void products_kernel(int64_t g0, int cnt, const int* __restrict__ off
   const int base = off[p];
   for (int64_t q = threadIdx.x; q < na * nb; q += blockDim.x) {
     const int64_t ia = q / nb, ib = q - ia * nb;
-    const unsigned long long ka = bkey[a0 + ia], kb = bkey[b0 + ib];
-    const uint64_t xa = key_x(ka), za = key_z(ka), xb = key_x(kb), zb = key_z(kb);
-    unsigned long long key = kInvalid;
+    const K ka = bkey[a0 + ia], kb = bkey[b0 + ib];
+    const uint64_t xa = kx(ka), za = kz(ka), xb = kx(kb), zb = kz(kb);
+    K key = kmarker<K>();
     C2 w{0.0, 0.0};
     if (!pauli::commute(xa, za, xb, zb)) {
       w = cmul(bval[a0 + ia], bval[b0 + ib]);
       w = pauli::apply_phase(cadd(w, w), pauli::phase_exponent(xa, za, xb, zb));
-      key = ka ^ kb;
+      key = kxor(ka, kb);
     }
     out_key[base + q] = key;
     out_val[base + q] = w;
@@ -89,8 +141,9 @@ __global__ void seg_of_kernel(const int* __restrict__ off, int nseg, int n, int*
 // Combined sort key (segment | invalid | key) for one stable LSD radix sort of
 // the whole batch over only its live bits: Pauli keys compact to 2q bits
 // x | z << q (the (z, x) order is kept), index keys (basis l) use kbits bits.
-__global__ void combine_kernel(const int* __restrict__ off, int nseg, int n, const unsigned long long* __restrict__ key,
-                               int pauli_q, int kbits, unsigned long long* __restrict__ ck) {
+template <class K>
+__global__ void combine_kernel(const int* __restrict__ off, int nseg, int n, const K* __restrict__ key, int pauli_q,
+                               int kbits, unsigned long long* __restrict__ ck) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int lo = 0, hi = nseg - 1;
     while (lo < hi) {
@@ -98,51 +151,52 @@ __global__ void combine_kernel(const int* __restrict__ off, int nseg, int n, con
       if (off[mid] <= i) lo = mid;
       else hi = mid - 1;
     }
-    const unsigned long long k = key[i];
+    const K k = key[i];
     unsigned long long c;
     if (pauli_q > 0) {
-      const bool inv = k == kInvalid;
-      c = inv ? (1ull << kbits) : (key_x(k) | (key_z(k) << pauli_q));
+      c = kmarked(k) ? (1ull << kbits) : (kx(k) | (kz(k) << pauli_q));
     } else {
-      c = k;
+      c = static_cast<unsigned long long>(kindex(k));
     }
     ck[i] = (static_cast<unsigned long long>(lo) << (kbits + 1)) | c;
   }
 }
+template <class K>
 __global__ void split_kernel(const unsigned long long* __restrict__ ck, int n, int pauli_q, int kbits,
-                             unsigned long long* __restrict__ ks, int* __restrict__ seg) {
+                             K* __restrict__ ks, int* __restrict__ seg) {
   const unsigned long long kmask = (1ull << kbits) - 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const unsigned long long c = ck[i];
     seg[i] = static_cast<int>(c >> (kbits + 1));
     if ((c >> kbits) & 1ull) {
-      ks[i] = kInvalid;
+      ks[i] = kmarker<K>();
     } else if (pauli_q > 0) {
       const unsigned long long k = c & kmask, qm = (1ull << pauli_q) - 1;
-      ks[i] = pauli::pack(k & qm, k >> pauli_q);
+      ks[i] = kpack<K>(k & qm, k >> pauli_q);
     } else {
-      ks[i] = c & kmask;
+      ks[i] = kfrom_index<K>(static_cast<int64_t>(c & kmask));
     }
   }
 }
 
 // first element of each (segment, key) run of the sorted keys
-__global__ void heads_kernel(const unsigned long long* __restrict__ ks, const int* __restrict__ seg, int n,
-                             int* __restrict__ flag) {
+template <class K>
+__global__ void heads_kernel(const K* __restrict__ ks, const int* __restrict__ seg, int n, int* __restrict__ flag) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    flag[i] = ks[i] != kInvalid && (i == 0 || seg[i] != seg[i - 1] || ks[i] != ks[i - 1]);
+    flag[i] = !kmarked(ks[i]) && (i == 0 || seg[i] != seg[i - 1] || !keq(ks[i], ks[i - 1]));
 }
 
 // from_terms accumulation: each run summed in input order from +0
-__global__ void run_sum_kernel(const unsigned long long* __restrict__ ks, const unsigned* __restrict__ is,
-                               const C2* __restrict__ val, const int* __restrict__ seg, const int* __restrict__ flag,
-                               const int* __restrict__ pos, int n, unsigned long long* __restrict__ rkey,
-                               C2* __restrict__ rval, double* __restrict__ rmag, int* __restrict__ rseg) {
+template <class K>
+__global__ void run_sum_kernel(const K* __restrict__ ks, const unsigned* __restrict__ is, const C2* __restrict__ val,
+                               const int* __restrict__ seg, const int* __restrict__ flag, const int* __restrict__ pos,
+                               int n, K* __restrict__ rkey, C2* __restrict__ rval, double* __restrict__ rmag,
+                               int* __restrict__ rseg) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (!flag[i]) continue;
-    const unsigned long long k = ks[i];
+    const K k = ks[i];
     C2 acc = pauli::slot(val[is[i]]);
-    for (int j = i + 1; j < n && ks[j] == k && seg[j] == seg[i]; ++j) acc = cadd(acc, val[is[j]]);
+    for (int j = i + 1; j < n && keq(ks[j], k) && seg[j] == seg[i]; ++j) acc = cadd(acc, val[is[j]]);
     const int r = pos[i];
     rkey[r] = k;
     rval[r] = acc;
@@ -182,9 +236,10 @@ __global__ void floor_keep_kernel(const int* __restrict__ roff, int nseg, const 
   for (int r = b + lane; r < e; r += 32) keep[r] = rmag[r] > floor;
 }
 
+template <class K>
 __global__ void compact_kernel(const int* __restrict__ keep, const int* __restrict__ kpos, int n,
-                               const unsigned long long* __restrict__ rkey, const C2* __restrict__ rval,
-                               unsigned long long* __restrict__ okey, C2* __restrict__ oval) {
+                               const K* __restrict__ rkey, const C2* __restrict__ rval, K* __restrict__ okey,
+                               C2* __restrict__ oval) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     if (keep[r]) {
       okey[kpos[r]] = rkey[r];
@@ -215,8 +270,8 @@ __global__ void seg_scale_kernel(const int* __restrict__ off, int nseg, const do
 
 // ---- key -> (basis index, coefficient) lists, ascending basis index -------
 
-struct Index {
-  unsigned long long* key;  // open-addressed slots (pauli::kEmpty = free)
+template <class K> struct Index {
+  K* key;  // open-addressed slots (kmarker = free)
   int* head;
   int* tail;
   int* count;
@@ -226,32 +281,33 @@ struct Index {
   int* e_next;
 };
 
-__device__ __forceinline__ int index_find(const Index& ix, unsigned long long key) {
-  for (uint64_t p = pauli::mix(key) & ix.mask;; p = (p + 1) & ix.mask) {
-    const unsigned long long k = ix.key[p];
-    if (k == pauli::kEmpty) return -1;
-    if (k == key) return static_cast<int>(p);
+template <class K> __device__ __forceinline__ int index_find(const Index<K>& ix, const K& key) {
+  for (uint64_t p = khash(key) & ix.mask;; p = (p + 1) & ix.mask) {
+    const K k = ix.key[p];
+    if (keq(k, key)) return static_cast<int>(p);
+    if (kmarked(k)) return -1;
   }
 }
 
 // Append the n terms (distinct keys) of accepted element l as entries e0...
-__global__ void index_insert_kernel(Index ix, const unsigned long long* __restrict__ key, const C2* __restrict__ val,
-                                    int n, int l, int e0) {
+template <class K>
+__global__ void index_insert_kernel(Index<K> ix, const K* __restrict__ key, const C2* __restrict__ val, int n, int l,
+                                    int e0) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int e = e0 + t;
     ix.e_l[e] = l;
     ix.e_v[e] = val[t];
     ix.e_next[e] = -1;
-    const unsigned long long k = key[t];
-    for (uint64_t p = pauli::mix(k) & ix.mask;; p = (p + 1) & ix.mask) {
-      const unsigned long long prev = atomicCAS(&ix.key[p], pauli::kEmpty, k);
-      if (prev == pauli::kEmpty) {
+    const K k = key[t];
+    for (uint64_t p = khash(k) & ix.mask;; p = (p + 1) & ix.mask) {
+      const K prev = kcas(&ix.key[p], kmarker<K>(), k);
+      if (kmarked(prev)) {
         ix.head[p] = e;
         ix.tail[p] = e;
         ix.count[p] = 1;
         break;
       }
-      if (prev == k) {  // one thread per key in this launch
+      if (keq(prev, k)) {  // one thread per key in this launch
         ix.e_next[ix.tail[p]] = e;
         ix.tail[p] = e;
         ix.count[p] += 1;
@@ -262,13 +318,13 @@ __global__ void index_insert_kernel(Index ix, const unsigned long long* __restri
 }
 
 // move every occupied slot of `from` into `to` (lists unchanged)
-__global__ void index_rehash_kernel(Index from, uint64_t from_slots, Index to) {
+template <class K> __global__ void index_rehash_kernel(Index<K> from, uint64_t from_slots, Index<K> to) {
   for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < from_slots;
        s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long k = from.key[s];
-    if (k == pauli::kEmpty) continue;
-    for (uint64_t p = pauli::mix(k) & to.mask;; p = (p + 1) & to.mask) {
-      if (atomicCAS(&to.key[p], pauli::kEmpty, k) == pauli::kEmpty) {
+    const K k = from.key[s];
+    if (kmarked(k)) continue;
+    for (uint64_t p = khash(k) & to.mask;; p = (p + 1) & to.mask) {
+      if (kmarked(kcas(&to.key[p], kmarker<K>(), k))) {
         to.head[p] = from.head[s];
         to.tail[p] = from.tail[s];
         to.count[p] = from.count[s];
@@ -278,15 +334,16 @@ __global__ void index_rehash_kernel(Index from, uint64_t from_slots, Index to) {
   }
 }
 
-__global__ void index_reset_kernel(Index ix, uint64_t slots) {
+template <class K> __global__ void index_reset_kernel(Index<K> ix, uint64_t slots) {
   for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < slots;
        s += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    ix.key[s] = pauli::kEmpty;
+    ix.key[s] = kmarker<K>();
 }
 
 // overlap contributions of each term: one per basis element l < n_limit that
 // holds the term's string
-__global__ void beta_count_kernel(Index ix, const unsigned long long* __restrict__ key, int n, int n_limit,
+template <class K>
+__global__ void beta_count_kernel(Index<K> ix, const K* __restrict__ key, int n, int n_limit,
                                   long long* __restrict__ cnt) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int s = index_find(ix, key[t]);
@@ -299,8 +356,9 @@ __global__ void beta_count_kernel(Index ix, const unsigned long long* __restrict
 // (l, conj(v_l) * h_t) at pos[t].. in ascending l; the segment's terms are in
 // sorted key order, so a stable sort by l leaves each l's contributions in
 // the order sum_inner_product adds them
-__global__ void beta_fill_kernel(Index ix, const unsigned long long* __restrict__ key, const C2* __restrict__ val,
-                                 int n, int n_limit, const long long* __restrict__ pos, unsigned long long* __restrict__ out_l,
+template <class K>
+__global__ void beta_fill_kernel(Index<K> ix, const K* __restrict__ key, const C2* __restrict__ val, int n,
+                                 int n_limit, const long long* __restrict__ pos, K* __restrict__ out_l,
                                  C2* __restrict__ out_v) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int s = index_find(ix, key[t]);
@@ -308,7 +366,7 @@ __global__ void beta_fill_kernel(Index ix, const unsigned long long* __restrict_
     long long w = pos[t];
     for (int e = ix.head[s]; e >= 0 && ix.e_l[e] < n_limit; e = ix.e_next[e], ++w) {
       const C2 v = ix.e_v[e];
-      out_l[w] = static_cast<unsigned long long>(ix.e_l[e]);
+      out_l[w] = kfrom_index<K>(ix.e_l[e]);
       out_v[w] = cmul({v.re, -v.im}, val[t]);
     }
   }
@@ -330,12 +388,13 @@ __global__ void chunk_base_kernel(const int* __restrict__ hoff, const int* __res
     clen[k] = ch[k].len;
   }
 }
-__global__ void chunk_basis_kernel(const unsigned long long* __restrict__ bl, const C2* __restrict__ beta,
+template <class K>
+__global__ void chunk_basis_kernel(const K* __restrict__ bl, const C2* __restrict__ beta,
                                    const int* __restrict__ rseg, int nruns, const int64_t* __restrict__ voff,
                                    bool negate, Chunk* __restrict__ ch, long long* __restrict__ clen) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nruns; r += gridDim.x * blockDim.x) {
     const int k = r + rseg[r] + 1;
-    const int64_t l = static_cast<int64_t>(bl[r]);
+    const int64_t l = kindex(bl[r]);
     const C2 b = beta[r];
     const bool zero = b.re == 0.0 && b.im == 0.0;
     ch[k] = {zero ? 0 : static_cast<int>(voff[l + 1] - voff[l]), 1, voff[l],
@@ -344,13 +403,13 @@ __global__ void chunk_basis_kernel(const unsigned long long* __restrict__ bl, co
   }
 }
 // one block per chunk: coefficient = mult * term (base_coeff * t, coeffs[l] * t)
+template <class K>
 __global__ void chunk_fill_kernel(const Chunk* __restrict__ ch, const long long* __restrict__ cpos, int nchunks,
-                                  const unsigned long long* __restrict__ hkey, const C2* __restrict__ hval,
-                                  const unsigned long long* __restrict__ vkey, const C2* __restrict__ vval,
-                                  unsigned long long* __restrict__ out_key, C2* __restrict__ out_val) {
+                                  const K* __restrict__ hkey, const C2* __restrict__ hval, const K* __restrict__ vkey,
+                                  const C2* __restrict__ vval, K* __restrict__ out_key, C2* __restrict__ out_val) {
   for (int k = blockIdx.x; k < nchunks; k += gridDim.x) {
     const Chunk c = ch[k];
-    const unsigned long long* sk = (c.kind == 0 ? hkey : vkey) + c.src;
+    const K* sk = (c.kind == 0 ? hkey : vkey) + c.src;
     const C2* sv = (c.kind == 0 ? hval : vval) + c.src;
     for (int t = threadIdx.x; t < c.len; t += blockDim.x) {
       out_key[cpos[k] + t] = sk[t];
@@ -379,8 +438,9 @@ __global__ void rebase_kernel(const int* __restrict__ off, int a, int nseg, int*
 }
 
 // accept: Complex{1/rn, 0} * residual -> pool (R:src/closure.cpp:287-290)
-__global__ void append_scaled_kernel(const unsigned long long* __restrict__ key, const C2* __restrict__ val, int n,
-                                     double rn, unsigned long long* __restrict__ okey, C2* __restrict__ oval) {
+template <class K>
+__global__ void append_scaled_kernel(const K* __restrict__ key, const C2* __restrict__ val, int n, double rn,
+                                     K* __restrict__ okey, C2* __restrict__ oval) {
   const C2 s{__ddiv_rn(1.0, rn), 0.0};
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     okey[t] = key[t];
@@ -398,17 +458,19 @@ __global__ void scale_terms_kernel(C2* __restrict__ v, int64_t n, C2 s) {
 // Alg. 2 on sums: per-segment overlap runs (l, beta) -> dense column-major
 // n x nseg (zeroed first), and a dense n x nseg coefficient block -> runs
 // (every l of every segment; chunk_basis_kernel skips exact zeros)
-__global__ void scatter_runs_kernel(const unsigned long long* __restrict__ key, const C2* __restrict__ val,
-                                    const int* __restrict__ rseg, int nruns, int64_t ld, C2* __restrict__ out) {
+template <class K>
+__global__ void scatter_runs_kernel(const K* __restrict__ key, const C2* __restrict__ val, const int* __restrict__ rseg,
+                                    int nruns, int64_t ld, C2* __restrict__ out) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nruns; r += gridDim.x * blockDim.x)
-    out[static_cast<int64_t>(rseg[r]) * ld + static_cast<int64_t>(key[r])] = val[r];
+    out[static_cast<int64_t>(rseg[r]) * ld + kindex(key[r])] = val[r];
 }
-__global__ void dense_runs_kernel(const C2* __restrict__ X, int n, int nseg, unsigned long long* __restrict__ key,
-                                  C2* __restrict__ val, int* __restrict__ rseg, int* __restrict__ off) {
+template <class K>
+__global__ void dense_runs_kernel(const C2* __restrict__ X, int n, int nseg, K* __restrict__ key, C2* __restrict__ val,
+                                  int* __restrict__ rseg, int* __restrict__ off) {
   const int64_t total = static_cast<int64_t>(n) * nseg;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    key[e] = static_cast<unsigned long long>(e % n);
+    key[e] = kfrom_index<K>(e % n);
     val[e] = X[e];
     rseg[e] = static_cast<int>(e / n);
   }
@@ -441,19 +503,19 @@ namespace psum {
 // engine re-runs the batch through the general merges.
 constexpr int kFusedThreads = 256;
 
-struct FusedSmem {
-  unsigned long long* hkey;  // open-addressed accumulation slots [hc]
+template <class K> struct FusedSmem {
+  K* hkey;  // open-addressed accumulation slots [hc]
   C2* hval;
-  unsigned long long* skey;  // sorted pass input / output [hc]
+  K* skey;  // sorted pass input / output [hc]
   C2* sval;
-  unsigned long long* ckey;  // beta contributions: basis index [hc]
+  K* ckey;  // beta contributions: basis index [hc]
   C2* cval;
   C2* beta;                  // [nb]
   unsigned* touched;         // [nb / 32 + 1]
 };
 
-__device__ __forceinline__ void fused_bitonic(unsigned long long* key, C2* val, int count, int npow2) {
-  for (int i = count + threadIdx.x; i < npow2; i += blockDim.x) key[i] = ~0ull;
+template <class K> __device__ __forceinline__ void fused_bitonic(K* key, C2* val, int count, int npow2) {
+  for (int i = count + threadIdx.x; i < npow2; i += blockDim.x) key[i] = kmarker<K>();
   __syncthreads();
   for (int k = 2; k <= npow2; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
@@ -461,8 +523,8 @@ __device__ __forceinline__ void fused_bitonic(unsigned long long* key, C2* val, 
         const int p = i ^ j;
         if (p > i) {
           const bool up = (i & k) == 0;
-          if ((key[i] > key[p]) == up) {
-            const unsigned long long tk = key[i];
+          if (kless(key[p], key[i]) == up) {
+            const K tk = key[i];
             key[i] = key[p];
             key[p] = tk;
             const C2 tv = val[i];
@@ -477,14 +539,15 @@ __device__ __forceinline__ void fused_bitonic(unsigned long long* key, C2* val, 
 
 // one pass: input = (s.skey, s.sval, n_in) sorted; output replaces it; returns
 // the output count or -1 on overflow
-__device__ int fused_pass(const FusedSmem& s, int hc, int n_in, const Index& ix, int n_limit,
-                          const int64_t* __restrict__ voff, const unsigned long long* __restrict__ vkey,
-                          const C2* __restrict__ vval, int* s_scratch) {
+template <class K>
+__device__ int fused_pass(const FusedSmem<K>& s, int hc, int n_in, const Index<K>& ix, int n_limit,
+                          const int64_t* __restrict__ voff, const K* __restrict__ vkey, const C2* __restrict__ vval,
+                          int* s_scratch) {
   int* s_count = s_scratch;      // [0] contributions, [1] distinct keys, [2] kept, [3] overflow
   int* s_pos = s_scratch + 4;    // per-term contribution offsets [kFusedThreads + 1] chunk scan
   for (int l = threadIdx.x; l < n_limit; l += blockDim.x) s.beta[l] = {0.0, 0.0};
   for (int w = threadIdx.x; w < n_limit / 32 + 1; w += blockDim.x) s.touched[w] = 0u;
-  for (int i = threadIdx.x; i < hc; i += blockDim.x) s.hkey[i] = pauli::kEmpty;
+  for (int i = threadIdx.x; i < hc; i += blockDim.x) s.hkey[i] = kmarker<K>();
   if (threadIdx.x < 4) s_count[threadIdx.x] = 0;
   __syncthreads();
   // (a) contributions, term-major: chunks of blockDim terms, each chunk
@@ -516,7 +579,7 @@ __device__ int fused_pass(const FusedSmem& s, int hc, int n_in, const Index& ix,
       const C2 h = s.sval[t];
       for (int e = ix.head[sl]; e >= 0 && ix.e_l[e] < n_limit; e = ix.e_next[e], ++w) {
         const C2 v = ix.e_v[e];
-        s.ckey[w] = static_cast<unsigned long long>(ix.e_l[e]);
+        s.ckey[w] = kfrom_index<K>(ix.e_l[e]);
         s.cval[w] = cmul({v.re, -v.im}, h);
       }
     }
@@ -525,7 +588,7 @@ __device__ int fused_pass(const FusedSmem& s, int hc, int n_in, const Index& ix,
   // (b) beta_l += contributions in list order, from +0
   if (threadIdx.x == 0) {
     for (int i = 0; i < s_count[0]; ++i) {
-      const int l = static_cast<int>(s.ckey[i]);
+      const int l = static_cast<int>(kindex(s.ckey[i]));
       s.beta[l] = cadd(s.beta[l], s.cval[i]);
       s.touched[l >> 5] |= 1u << (l & 31);
     }
@@ -536,24 +599,24 @@ __device__ int fused_pass(const FusedSmem& s, int hc, int n_in, const Index& ix,
   // source; a new key first reserves capacity (<= 3/4 of the table, the
   // spare quarter >= one CTA of in-flight claims), so probing always ends
   const int limit = (hc * 3) / 4;
-  auto merge_source = [&](const unsigned long long* key, const C2* val, int n, C2 mult) {
+  auto merge_source = [&](const K* key, const C2* val, int n, C2 mult) {
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
-      const unsigned long long k = key[t];
+      const K k = key[t];
       const C2 v = cmul(mult, val[t]);
-      for (uint64_t p = pauli::mix(k) & static_cast<uint64_t>(hc - 1);; p = (p + 1) & static_cast<uint64_t>(hc - 1)) {
-        const unsigned long long cur = s.hkey[p];
-        if (cur == k) {
+      for (uint64_t p = khash(k) & static_cast<uint64_t>(hc - 1);; p = (p + 1) & static_cast<uint64_t>(hc - 1)) {
+        const K cur = s.hkey[p];
+        if (keq(cur, k)) {
           s.hval[p] = cadd(s.hval[p], v);
           break;
         }
-        if (cur != pauli::kEmpty) continue;
-        const unsigned long long prev = atomicCAS(&s.hkey[p], pauli::kEmpty, k);
-        if (prev == pauli::kEmpty) {
+        if (!kmarked(cur)) continue;
+        const K prev = kcas(&s.hkey[p], kmarker<K>(), k);
+        if (kmarked(prev)) {
           if (atomicAdd(&s_count[1], 1) >= limit) s_count[3] = 1;
           s.hval[p] = pauli::slot(v);
           break;
         }
-        if (prev == k) {  // cannot happen within one source; kept for safety
+        if (keq(prev, k)) {  // cannot happen within one source; kept for safety
           s.hval[p] = cadd(s.hval[p], v);
           break;
         }
@@ -578,7 +641,7 @@ __device__ int fused_pass(const FusedSmem& s, int hc, int n_in, const Index& ix,
   __shared__ double s_max[kFusedThreads / 32];
   double mx = 0.0;
   for (int i = threadIdx.x; i < hc; i += blockDim.x)
-    if (s.hkey[i] != pauli::kEmpty) mx = fmax(mx, hypot(s.hval[i].re, s.hval[i].im));
+    if (!kmarked(s.hkey[i])) mx = fmax(mx, hypot(s.hval[i].re, s.hval[i].im));
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
   __syncthreads();
@@ -590,7 +653,7 @@ __device__ int fused_pass(const FusedSmem& s, int hc, int n_in, const Index& ix,
   __syncthreads();
   const double floor = __dmul_rn(kDropTolerance, s_max[0]);
   for (int i = threadIdx.x; i < hc; i += blockDim.x)
-    if (s.hkey[i] != pauli::kEmpty && hypot(s.hval[i].re, s.hval[i].im) > floor) {
+    if (!kmarked(s.hkey[i]) && hypot(s.hval[i].re, s.hval[i].im) > floor) {
       const int w = atomicAdd(&s_count[2], 1);
       s.skey[w] = s.hkey[i];
       s.sval[w] = s.hval[i];
@@ -604,16 +667,16 @@ __device__ int fused_pass(const FusedSmem& s, int hc, int n_in, const Index& ix,
 }
 
 // OrthonormStrategy::check of segment p of h against basis elements l < n_limit
+template <class K>
 __global__ void __launch_bounds__(kFusedThreads)
-fused_check_kernel(const int* __restrict__ off, int nseg, const unsigned long long* __restrict__ hkey,
-                   const C2* __restrict__ hval, Index ix, int n_limit, const int64_t* __restrict__ voff,
-                   const unsigned long long* __restrict__ vkey, const C2* __restrict__ vval, int hc,
-                   unsigned long long* __restrict__ okey, C2* __restrict__ oval, int* __restrict__ olen,
-                   double* __restrict__ rn, int* __restrict__ status) {
-  extern __shared__ unsigned char s_raw[];
+fused_check_kernel(const int* __restrict__ off, int nseg, const K* __restrict__ hkey, const C2* __restrict__ hval,
+                   Index<K> ix, int n_limit, const int64_t* __restrict__ voff, const K* __restrict__ vkey,
+                   const C2* __restrict__ vval, int hc, K* __restrict__ okey, C2* __restrict__ oval,
+                   int* __restrict__ olen, double* __restrict__ rn, int* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
   __shared__ int s_scratch[4 + kFusedThreads];
-  FusedSmem s;
-  s.hkey = reinterpret_cast<unsigned long long*>(s_raw);
+  FusedSmem<K> s;
+  s.hkey = reinterpret_cast<K*>(s_raw);
   s.skey = s.hkey + hc;
   s.ckey = s.skey + hc;
   s.hval = reinterpret_cast<C2*>(s.ckey + hc);
@@ -659,9 +722,9 @@ fused_check_kernel(const int* __restrict__ off, int nseg, const unsigned long lo
 }
 
 // segments starting at src[q] (lengths from off) -> contiguous batch
-__global__ void gather_segs_kernel(const unsigned long long* __restrict__ key, const C2* __restrict__ val,
-                                   const int* __restrict__ src, const int* __restrict__ off, int nseg,
-                                   unsigned long long* __restrict__ okey, C2* __restrict__ oval) {
+template <class K>
+__global__ void gather_segs_kernel(const K* __restrict__ key, const C2* __restrict__ val, const int* __restrict__ src,
+                                   const int* __restrict__ off, int nseg, K* __restrict__ okey, C2* __restrict__ oval) {
   for (int q = blockIdx.x; q < nseg; q += gridDim.x)
     for (int t = threadIdx.x; t < off[q + 1] - off[q]; t += blockDim.x) {
       okey[off[q] + t] = key[src[q] + t];
@@ -670,9 +733,9 @@ __global__ void gather_segs_kernel(const unsigned long long* __restrict__ key, c
 }
 
 // strided fused outputs (row p at p * hc) -> contiguous segments
-__global__ void strided_to_segs_kernel(const unsigned long long* __restrict__ sk, const C2* __restrict__ sv, int hc,
-                                       const int* __restrict__ off, int nseg, unsigned long long* __restrict__ ok,
-                                       C2* __restrict__ ov) {
+template <class K>
+__global__ void strided_to_segs_kernel(const K* __restrict__ sk, const C2* __restrict__ sv, int hc,
+                                       const int* __restrict__ off, int nseg, K* __restrict__ ok, C2* __restrict__ ov) {
   for (int p = blockIdx.x; p < nseg; p += gridDim.x)
     for (int t = threadIdx.x; t < off[p + 1] - off[p]; t += blockDim.x) {
       ok[off[p] + t] = sk[static_cast<int64_t>(p) * hc + t];
@@ -680,9 +743,30 @@ __global__ void strided_to_segs_kernel(const unsigned long long* __restrict__ sk
     }
 }
 
-inline size_t fused_smem_bytes(int hc, int n_limit) {
-  return static_cast<size_t>(hc) * 3 * (sizeof(unsigned long long) + sizeof(C2)) +
+template <class K> inline size_t fused_smem_bytes(int hc, int n_limit) {
+  return static_cast<size_t>(hc) * 3 * (sizeof(K) + sizeof(C2)) +
          static_cast<size_t>(n_limit) * sizeof(C2) + (static_cast<size_t>(n_limit) / 32 + 1) * sizeof(unsigned);
+}
+
+} // namespace psum
+} // namespace liecl_b200
+
+namespace liecl_b200 {
+namespace psum {
+
+// wide keys: the (z, x) order by two stable LSD passes over the 64-bit words;
+// out[i] = word (0: x, 1: z) of key[perm[i]] (perm null: identity)
+__global__ void wide_words_kernel(const WKey* __restrict__ key, const unsigned* __restrict__ perm, int n, int word,
+                                  unsigned long long* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const WKey k = key[perm ? perm[i] : i];
+    out[i] = word ? k.z : k.x;
+  }
+}
+template <class K>
+__global__ void gather_keys_kernel(const K* __restrict__ key, const unsigned* __restrict__ perm, int n,
+                                   K* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = key[perm[i]];
 }
 
 } // namespace psum

@@ -16,7 +16,7 @@ python bench.py $ARGS > gpurun_out/${TAG}_plain.json 2> gpurun_out/${TAG}_plain.
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py $ARGS > gpurun_out/${TAG}_ncu_launches.log 2>&1 || exit 2
 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:'dgemm|commutator_ah' --launch-count 3 \
+    -k regex:'dgemm|commutator_ah' --launch-count 4 \
     -o gpurun_out/${TAG}_full python bench.py $ARGS > gpurun_out/${TAG}_full.log 2>&1 || exit 3
 ncu --set full --clock-control none --import-source on -k regex:'bc_' --launch-skip 30 --launch-count 7 \
     -o gpurun_out/${TAG}_growth python bench.py $ARGS > gpurun_out/${TAG}_growth.log 2>&1 || exit 4
