@@ -14,9 +14,9 @@
 // load conflict-free:
 //   K-contiguous tile (rows of 16 k): lane (g, t) reads the 16-byte chunk
 //     (2t + p) ^ (row & 7): rows g and g^1 of a quarter-warp hit disjoint chunks;
-//   M-contiguous A (K2b: A(m, k) = V[k][m]): a 3-D box [m / 16][k][m % 16],
-//     rows r = (m / 16) * 16 + k, chunk ((m % 16) / 2) ^ (k & 7): two lanes per
-//     bank, the minimum for 8-byte loads.
+//   M-contiguous A (K2b: A(m, k) = V[k][m]): a 5-D box that orders k's bits so
+//     that a lane's t lands in the swizzle row (sw_mc below): each half-warp
+//     of 8-byte loads on 16 distinct banks.
 // Tile: BM x BN = 128 x 64 per CTA (4 warps of 64 x 32), BK = 16, two CTAs per
 // SM (96 KB of stages each).
 #pragma once
@@ -76,17 +76,32 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
 
 // swizzled element offsets (doubles) inside a stage tile
 __device__ __forceinline__ int sw_kc(int r, int k) { return r * 16 + ((((k >> 1) ^ r) & 7) << 1) + (k & 1); }
+// M-contiguous tile as the 5-D box [m/16][p][t][q][m%16] of k = 4t + 2p + q:
+// line (m/16)*16 + 8p + 2t + q, so line & 7 = 2t + q and the swizzled chunk
+// ((m%16)/2) ^ (2t + q) spreads each half-warp's fragment loads over 16 banks
+// (a [m/16][k][m%16] box leaves t's high bit out of line & 7: 2-way conflicts)
 __device__ __forceinline__ int sw_mc(int m, int k) {
-  return ((m >> 4) * 16 + k) * 16 + ((((m & 15) >> 1) ^ k) & 7) * 2 + (m & 1);
+  const int line = (m >> 4) * 16 + ((k >> 1) & 1) * 8 + (k >> 2) * 2 + (k & 1);
+  return line * 16 + ((((m & 15) >> 1) ^ line) & 7) * 2 + (m & 1);
 }
 
 // Same contract as dgemm_dmma_kernel without split-K: C(m, n) = epi(sum_k
-// A(m, k) B(k, n)). mapA: A_KCONTIG -- 2-D {K, M} box {16, 128}; else 3-D
-// {16, K, M / 16} box {16, 16, 8} (M a multiple of 16). mapB: 2-D {K, N} box
-// {16, 64}. All 128-byte swizzled, out-of-bounds elements read as zeros.
+// A(m, k) B(k, n)). mapA: A_KCONTIG -- 2-D {K, M} box {16, 128}; else 5-D
+// {16 (m%16), 2 (q), ceil(K/4) (t), 2 (p), M/16} box {16, 2, 4, 2, 8} (M a
+// multiple of 16; rows up to 4 ceil(K/4) are read and must be zero past K).
+// mapB: 2-D {K, N} box {16, 64}. All 128-byte swizzled, out-of-bounds
+// elements read as zeros.
 template <bool A_KCONTIG, REpi EPI>
 __global__ void __launch_bounds__(tg::THREADS, 2)
 dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
@@ -120,7 +135,7 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     unsigned char* a = tsm + s * STAGE_BYTES;
     mbar_expect_tx(&full[s], STAGE_BYTES);
     if (A_KCONTIG) tma_load_2d(a, &mapA, kt * BK, m0, &full[s]);
-    else tma_load_3d(a, &mapA, 0, kt * BK, m0 / 16, &full[s]);
+    else tma_load_5d(a, &mapA, 0, 0, kt * (BK / 4), 0, m0 / 16, &full[s]);
     tma_load_2d(a + A_BYTES, &mapB, kt * BK, n0, &full[s]);
   };
   if (tid == 0)

@@ -150,6 +150,7 @@ struct liecl_b200_ctx {
   DevBuf<double2> comm_scratch;  // ... and unpacked operands / result (packed field)
   std::shared_ptr<void> dense_cache, pauli_cache;  // workspaces of the last one-shot closure
   std::shared_ptr<void> sum_cache;                  // the last multi-term Pauli closure (fetch)
+  bool sum_cache_wide = false;                      // ... a SumEngineWide (32..63 qubits)
   std::shared_ptr<void> gram_ops;                   // GramState / check_matrix_inversion workspaces
   std::shared_ptr<void> result;                     // the last dense closure (liecl_b200_dense_fetch)
   int result_kind = 0;                              // 1 DenseEngine, 2 GramEngine, 3 RankEngine
@@ -345,13 +346,19 @@ bool tma_map_kc(CUtensorMap* m, const double* p, int64_t len, int64_t rows, int6
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// A(m, k) = p[k*ld + m] (M-contiguous operand), M a multiple of 16: 3-D {16, K, M/16}, box {16, 16, 8}
-bool tma_map_mc(CUtensorMap* m, const double* p, int64_t M, int64_t K, int64_t ld) {
+// A(m, k) = p[k*ld + m] (M-contiguous operand), M a multiple of 16, k = 4t + 2p + q:
+// 5-D {16 (m%16), 2 (q), ceil(K/4) (t), 2 (p), M/16}, box {16, 2, 4, 2, 8}
+// (dgemm_tma.cuh sw_mc). Rows K .. 4 ceil(K/4) - 1 are read as in-bounds:
+// the caller guarantees they exist and are zero (rows_zeroed).
+bool tma_map_mc(CUtensorMap* m, const double* p, int64_t M, int64_t K, int64_t ld, int64_t rows_zeroed) {
   if ((reinterpret_cast<uintptr_t>(p) & 15) || (ld & 1) || (M % 16) || M <= 0 || K <= 0) return false;
-  cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M / 16)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8, 128};
-  cuuint32_t box[3] = {16, 16, 8}, es[3] = {1, 1, 1};
-  return tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, es,
+  const int64_t kq = (K + 3) / 4;
+  if (4 * kq > rows_zeroed) return false;
+  cuuint64_t dims[5] = {16, 2, static_cast<cuuint64_t>(kq), 2, static_cast<cuuint64_t>(M / 16)};
+  cuuint64_t strides[4] = {static_cast<cuuint64_t>(ld) * 8, static_cast<cuuint64_t>(ld) * 32,
+                           static_cast<cuuint64_t>(ld) * 16, 128};
+  cuuint32_t box[5] = {16, 2, 4, 2, 8}, es[5] = {1, 1, 1, 1, 1};
+  return tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(p), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -513,9 +520,11 @@ void rgemm_mc_store(liecl_b200_ctx* ctx, const double* A, int64_t lda, int64_t M
 }
 
 // R = X - V[:, 0:n] P (P ld ldp); partial[mt][b] = sum_rows w R^2
+// (v_rows: rows of V that exist and are zero past n -- the TMA path reads up
+// to 4 ceil(n/4); -1 unknown: the cp.async kernel)
 void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, const double* P, int64_t ldp,
                     const double* X, int count, double* R, double* partial, int d, int64_t ldv = -1,
-                    int64_t ldx = -1) {
+                    int64_t ldx = -1, int64_t v_rows = -1) {
   if (ldv < 0) ldv = D;
   if (ldx < 0) ldx = D;  // X and R
   rgemm_attr_once<false, REpi::kSubtractNorm>();
@@ -524,7 +533,8 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
   const int64_t kpad = (n + 1) & ~int64_t(1);  // even K: reads one zero row of V past an odd n
   int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, kpad);
   CUtensorMap ma, mb;
-  if (slices <= 1 && tma_enabled() && tma_map_mc(&ma, V, D, n, ldv) && tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
+  if (slices <= 1 && tma_enabled() && tma_map_mc(&ma, V, D, n, ldv, v_rows) &&
+      tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
     // K = n exactly: rows past the basis read as zeros (TMA out-of-bounds fill)
     func_attr_once(dgemm_tma_kernel<false, REpi::kSubtractNorm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                    tg::SMEM);
@@ -1340,12 +1350,13 @@ int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, c
     if (!ctx || !offsets || !stats || !terms_needed || !basis_offsets)
       throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     if (ngens <= 0) throw Error(LIECL_B200_INVALID_INPUT, "closure requires a non-empty generator tuple");
-    if (qubits < 1 || qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..31 qubits");
+    if (qubits < 1 || qubits > 63)
+      throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..63 qubits");
     if (offsets[0] != 0) throw Error(LIECL_B200_INVALID_INPUT, "offsets[0] must be 0");
     for (int i = 0; i < ngens; ++i) {
       if (offsets[i + 1] < offsets[i]) throw Error(LIECL_B200_INVALID_INPUT, "offsets must be non-decreasing");
       for (int64_t t = offsets[i] + 1; t < offsets[i + 1]; ++t)  // PauliSum form: unique, sorted by (z, x)
-        if (pauli::pack(x[t], z[t]) <= pauli::pack(x[t - 1], z[t - 1]))
+        if (z[t] < z[t - 1] || (z[t] == z[t - 1] && x[t] <= x[t - 1]))
           throw Error(LIECL_B200_INVALID_INPUT, "generator terms must be unique and sorted by (z, x)");
     }
     if (offsets[ngens] > 0 && (!x || !z || !coef)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
@@ -1354,23 +1365,29 @@ int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, c
     const liecl_b200_config cfg = default_config(cfg_in);
     const uint64_t k0 = ctx->kernels;
     const bool gram = method == LIECL_B200_METHOD_MATRIX_INVERSION;
-    auto holder = std::make_shared<SumEngine>(ctx, qubits, gram ? false : keep_for(method), cfg, gram);
-    SumEngine& eng = *holder;
-    eng.run(offsets, x, z, coef, ngens);
-    ctx->sum_cache = holder;  // liecl_b200_pauli_sums_fetch copies from it without recomputing
-    *stats = eng.stats();
-    stats->kernels = ctx->kernels - k0;
-    stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
-    write_warnings(eng.warnings(), warnings, warnings_len);
-    copy_log(eng.log(), log, log_cap, log_len);
-    terms_needed[0] = eng.terms(false);
-    terms_needed[1] = eng.terms(true);
-    if (eng.size() > cap || terms_needed[0] > term_cap || (ortho_offsets && terms_needed[1] > ortho_term_cap))
-      throw Error(LIECL_B200_CAPACITY, "output buffers too small");
-    if (terms_needed[0] > 0 && (!basis_x || !basis_z || !basis_coef))
-      throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-    eng.download(false, basis_offsets, basis_x, basis_z, basis_coef);
-    if (ortho_offsets) eng.download(true, ortho_offsets, ortho_x, ortho_z, ortho_coef);
+    auto go = [&](auto tag) {
+      using E = SumEngineT<decltype(tag)>;
+      auto holder = std::make_shared<E>(ctx, qubits, gram ? false : keep_for(method), cfg, gram);
+      E& eng = *holder;
+      eng.run(offsets, x, z, coef, ngens);
+      ctx->sum_cache = holder;  // liecl_b200_pauli_sums_fetch copies from it without recomputing
+      ctx->sum_cache_wide = std::is_same_v<E, SumEngineWide>;
+      *stats = eng.stats();
+      stats->kernels = ctx->kernels - k0;
+      stats->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+      write_warnings(eng.warnings(), warnings, warnings_len);
+      copy_log(eng.log(), log, log_cap, log_len);
+      terms_needed[0] = eng.terms(false);
+      terms_needed[1] = eng.terms(true);
+      if (eng.size() > cap || terms_needed[0] > term_cap || (ortho_offsets && terms_needed[1] > ortho_term_cap))
+        throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+      if (terms_needed[0] > 0 && (!basis_x || !basis_z || !basis_coef))
+        throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+      eng.download(false, basis_offsets, basis_x, basis_z, basis_coef);
+      if (ortho_offsets) eng.download(true, ortho_offsets, ortho_x, ortho_z, ortho_coef);
+    };
+    if (qubits <= 31) go(0ull);
+    else go(psum::WKey{});
   });
 }
 
@@ -1379,25 +1396,34 @@ int liecl_b200_pauli_sums_fetch(liecl_b200_ctx* ctx, int64_t cap, int64_t* basis
                                 uint64_t* ortho_x, uint64_t* ortho_z, double* ortho_coef, int64_t ortho_term_cap) {
   return guarded([&] {
     if (!ctx || !basis_offsets) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-    auto eng = std::static_pointer_cast<SumEngine>(ctx->sum_cache);
-    if (!eng) throw Error(LIECL_B200_INVALID_INPUT, "no multi-term Pauli closure to fetch on this context");
+    if (!ctx->sum_cache) throw Error(LIECL_B200_INVALID_INPUT, "no multi-term Pauli closure to fetch on this context");
     use_device(ctx);
-    if (eng->size() > cap || eng->terms(false) > term_cap || (ortho_offsets && eng->terms(true) > ortho_term_cap))
-      throw Error(LIECL_B200_CAPACITY, "output buffers too small");
-    if (eng->terms(false) > 0 && (!basis_x || !basis_z || !basis_coef))
-      throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-    eng->download(false, basis_offsets, basis_x, basis_z, basis_coef);
-    if (ortho_offsets) eng->download(true, ortho_offsets, ortho_x, ortho_z, ortho_coef);
+    auto go = [&](auto* tag) {
+      auto eng = std::static_pointer_cast<std::remove_pointer_t<decltype(tag)>>(ctx->sum_cache);
+      if (eng->size() > cap || eng->terms(false) > term_cap || (ortho_offsets && eng->terms(true) > ortho_term_cap))
+        throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+      if (eng->terms(false) > 0 && (!basis_x || !basis_z || !basis_coef))
+        throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+      eng->download(false, basis_offsets, basis_x, basis_z, basis_coef);
+      if (ortho_offsets) eng->download(true, ortho_offsets, ortho_x, ortho_z, ortho_coef);
+    };
+    if (ctx->sum_cache_wide) go(static_cast<SumEngineWide*>(nullptr));
+    else go(static_cast<SumEngine*>(nullptr));
   });
 }
 
 int liecl_b200_pauli_sums_fetch_gram(liecl_b200_ctx* ctx, double* gram_out, double* inverse_out) {
   return guarded([&] {
     if (!ctx) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-    auto eng = std::static_pointer_cast<SumEngine>(ctx->sum_cache);
-    if (!eng || !eng->is_gram()) throw Error(LIECL_B200_INVALID_INPUT, "no matrix-inversion Pauli closure on this context");
-    use_device(ctx);
-    eng->download_gram(gram_out, inverse_out);
+    auto go = [&](auto* tag) {
+      auto eng = std::static_pointer_cast<std::remove_pointer_t<decltype(tag)>>(ctx->sum_cache);
+      if (!eng || !eng->is_gram())
+        throw Error(LIECL_B200_INVALID_INPUT, "no matrix-inversion Pauli closure on this context");
+      use_device(ctx);
+      eng->download_gram(gram_out, inverse_out);
+    };
+    if (ctx->sum_cache_wide) go(static_cast<SumEngineWide*>(nullptr));
+    else go(static_cast<SumEngine*>(nullptr));
   });
 }
 
@@ -1817,19 +1843,26 @@ int liecl_b200_dense_fetch(liecl_b200_ctx* ctx, int32_t what, int64_t first, int
 
 namespace {
 // a one-shot SumEngine holding `n` tuple sums (the Pauli single queries)
-std::unique_ptr<SumEngine> pauli_tuple(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
-                                       const uint64_t* z, const double* coef, int64_t n, uint32_t qubits) {
+template <class K>
+std::unique_ptr<SumEngineT<K>> pauli_tuple(liecl_b200_ctx* ctx, const int64_t* offsets, const uint64_t* x,
+                                           const uint64_t* z, const double* coef, int64_t n, uint32_t qubits) {
   if (n < 0 || (n > 0 && !offsets)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-  if (qubits < 1 || qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..31 qubits");
   if (n > 0 && offsets[0] != 0) throw Error(LIECL_B200_INVALID_INPUT, "offsets[0] must be 0");
   for (int64_t l = 0; l < n; ++l)
     if (offsets[l + 1] < offsets[l]) throw Error(LIECL_B200_INVALID_INPUT, "offsets must be non-decreasing");
   if (n > 0 && offsets[n] > 0 && (!x || !z || !coef)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
   liecl_b200_config cfg = default_config(nullptr);
   cfg.max_dim = static_cast<uint64_t>(std::max<int64_t>(n, 1));
-  auto e = std::make_unique<SumEngine>(ctx, qubits, false, cfg);
+  auto e = std::make_unique<SumEngineT<K>>(ctx, qubits, false, cfg);
   if (n > 0) e->load_basis(offsets, x, z, coef, n);
   return e;
+}
+// runs f(K{}) with the key type for `qubits`: narrow 1..31, wide 32..63
+template <class F> void with_keys(uint32_t qubits, F&& f) {
+  if (qubits < 1 || qubits > 63)
+    throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..63 qubits");
+  if (qubits <= 31) f(0ull);
+  else f(psum::WKey{});
 }
 void check_sum_args(int64_t h_terms, const uint64_t* hx, const uint64_t* hz, const double* hcoef) {
   if (h_terms < 0 || (h_terms > 0 && (!hx || !hz || !hcoef))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
@@ -1847,11 +1880,14 @@ int liecl_b200_project_residual_pauli(liecl_b200_ctx* ctx, const int64_t* offset
     if (!ctx || !out_terms || (n > 0 && !coeffs)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     check_sum_args(h_terms, hx, hz, hcoef);
     use_device(ctx);
-    auto e = pauli_tuple(ctx, offsets, x, z, coef, n, qubits);
-    SumEngine::Segs r;
-    e->project_one(h_terms, hx, hz, hcoef, r, coeffs);
-    *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
-    if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    with_keys(qubits, [&](auto tag) {
+      using K = decltype(tag);
+      auto e = pauli_tuple<K>(ctx, offsets, x, z, coef, n, qubits);
+      typename SumEngineT<K>::Segs r;
+      e->project_one(h_terms, hx, hz, hcoef, r, coeffs);
+      *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
+      if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    });
   });
 }
 
@@ -1864,11 +1900,14 @@ int liecl_b200_linear_combination_pauli(liecl_b200_ctx* ctx, const int64_t* offs
     if (!ctx || !out_terms || (n > 0 && !coeffs)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     check_sum_args(h_terms, hx, hz, hcoef);
     use_device(ctx);
-    auto e = pauli_tuple(ctx, offsets, x, z, coef, n, qubits);
-    SumEngine::Segs r;
-    e->combine_one(h_terms, hx, hz, hcoef, base_re, base_im, coeffs, false, r);
-    *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
-    if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    with_keys(qubits, [&](auto tag) {
+      using K = decltype(tag);
+      auto e = pauli_tuple<K>(ctx, offsets, x, z, coef, n, qubits);
+      typename SumEngineT<K>::Segs r;
+      e->combine_one(h_terms, hx, hz, hcoef, base_re, base_im, coeffs, false, r);
+      *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
+      if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    });
   });
 }
 
@@ -1879,8 +1918,11 @@ int liecl_b200_overlaps_pauli(liecl_b200_ctx* ctx, const int64_t* offsets, const
     if (!ctx || (n > 0 && !beta_out)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     check_sum_args(h_terms, hx, hz, hcoef);
     use_device(ctx);
-    auto e = pauli_tuple(ctx, offsets, x, z, coef, n, qubits);
-    e->overlaps_one(h_terms, hx, hz, hcoef, beta_out);
+    with_keys(qubits, [&](auto tag) {
+      using K = decltype(tag);
+      auto e = pauli_tuple<K>(ctx, offsets, x, z, coef, n, qubits);
+      e->overlaps_one(h_terms, hx, hz, hcoef, beta_out);
+    });
   });
 }
 
@@ -1891,11 +1933,14 @@ int liecl_b200_pauli_from_terms(liecl_b200_ctx* ctx, int64_t n, const uint64_t* 
     if (!ctx || !out_terms) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     check_sum_args(n, x, z, coef);
     use_device(ctx);
-    auto e = pauli_tuple(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
-    SumEngine::Segs r;
-    e->from_terms_one(n, x, z, coef, r);
-    *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
-    if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    with_keys(qubits, [&](auto tag) {
+      using K = decltype(tag);
+      auto e = pauli_tuple<K>(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
+      typename SumEngineT<K>::Segs r;
+      e->from_terms_one(n, x, z, coef, r);
+      *out_terms = e->download_one(r, rx, rz, rcoef, term_cap);
+      if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    });
   });
 }
 
@@ -1914,7 +1959,6 @@ int liecl_b200_parse_pauli_sum(liecl_b200_ctx* ctx, const char* text, int64_t le
       if (err_col) *err_col = e.col;
       throw Error(LIECL_B200_PARSE, e.msg);
     }
-    if (qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "the device PauliSum path supports 1..31 qubits");
     use_device(ctx);
     const int64_t n = static_cast<int64_t>(terms.size());
     std::vector<uint64_t> tx(static_cast<size_t>(n)), tz(static_cast<size_t>(n));
@@ -1922,11 +1966,14 @@ int liecl_b200_parse_pauli_sum(liecl_b200_ctx* ctx, const char* text, int64_t le
     for (int64_t t = 0; t < n; ++t) {
       tx[t] = terms[t].x, tz[t] = terms[t].z, tc[2 * t] = terms[t].re, tc[2 * t + 1] = terms[t].im;
     }
-    auto e = pauli_tuple(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
-    SumEngine::Segs r;
-    e->from_terms_one(n, tx.data(), tz.data(), tc.data(), r);  // PauliSum::from_terms (R:src/pauli.cpp:78-115)
-    *out_terms = e->download_one(r, x, z, coef, term_cap);
-    if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    with_keys(qubits, [&](auto tag) {
+      using K = decltype(tag);
+      auto e = pauli_tuple<K>(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
+      typename SumEngineT<K>::Segs r;
+      e->from_terms_one(n, tx.data(), tz.data(), tc.data(), r);  // PauliSum::from_terms (R:src/pauli.cpp:78-115)
+      *out_terms = e->download_one(r, x, z, coef, term_cap);
+      if (*out_terms > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+    });
   });
 }
 
@@ -1939,83 +1986,85 @@ int liecl_b200_realize_generators(liecl_b200_ctx* ctx, int32_t family, uint32_t 
     if (restrict_zero_magnetization && family != 2)  // R:src/generators.cpp:172-175
       throw Error(LIECL_B200_INVALID_INPUT, "zero-magnetization restriction is an xxz_hva option");
     const auto gens = catalog_terms(family, qubits, seed, delta);
-    if (qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "the device PauliSum path supports 1..31 qubits");
     use_device(ctx);
     const int32_t ng = static_cast<int32_t>(gens.size());
     *count = ng;
     // PauliSum::from_terms of every generator (device)
-    auto e = pauli_tuple(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
-    std::vector<int64_t> off(1, 0);
-    std::vector<uint64_t> sx, sz;
-    std::vector<double> sc;
-    for (const auto& g : gens) {
-      const int64_t n = static_cast<int64_t>(g.size());
-      std::vector<uint64_t> tx(n), tz(n);
-      std::vector<double> tc(2 * n);
-      for (int64_t t = 0; t < n; ++t) tx[t] = g[t].x, tz[t] = g[t].z, tc[2 * t] = g[t].re, tc[2 * t + 1] = g[t].im;
-      SumEngine::Segs r;
-      e->from_terms_one(n, tx.data(), tz.data(), tc.data(), r);
-      const int64_t base = off.back();
-      sx.resize(base + r.total), sz.resize(base + r.total), sc.resize(2 * (base + r.total));
-      e->download_one(r, sx.data() + base, sz.data() + base, sc.data() + 2 * base, r.total);
-      off.push_back(base + r.total);
-    }
-    if (!dense && !restrict_zero_magnetization) {
-      if (!offsets) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-      std::copy(off.begin(), off.end(), offsets);
-      if (off.back() > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
-      if (off.back() > 0 && (!x || !z || !coef)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-      std::copy(sx.begin(), sx.end(), x);
-      std::copy(sz.begin(), sz.end(), z);
-      std::copy(sc.begin(), sc.end(), coef);
-      return;
-    }
-    // dense: from_pauli (R:src/dense.cpp:70-98) on the device, then the
-    // zero-magnetization restriction when asked (R:src/dense.cpp:167-199)
-    if (qubits > 12)
-      throw Error(LIECL_B200_CAPACITY, "from_pauli: " + std::to_string(qubits) +
-                                           " qubits exceeds the expansion limit of 12");
-    const int64_t d = int64_t(1) << qubits;
-    std::vector<int64_t> states;
-    if (restrict_zero_magnetization)
-      for (int64_t st = 0; st < d; ++st)
-        if (__builtin_popcountll(static_cast<unsigned long long>(st)) == static_cast<int>(qubits / 2))
-          states.push_back(st);
-    const int64_t m = restrict_zero_magnetization ? static_cast<int64_t>(states.size()) : d;
-    if (dim) *dim = static_cast<int32_t>(m);
-    if (!dense_out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
-    if (ng * m * m * 2 > dense_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
-    DevBuf<int64_t> doff, dst;
-    DevBuf<uint64_t> dx, dz;
-    DevBuf<double2> dc, full, sub;
-    const int64_t terms = off.back();
-    doff.ensure(ng + 1);
-    dx.ensure(std::max<int64_t>(terms, 1));
-    dz.ensure(std::max<int64_t>(terms, 1));
-    dc.ensure(std::max<int64_t>(terms, 1));
-    full.ensure(static_cast<size_t>(ng * d * d));
-    CU(cudaMemcpyAsync(doff.p, off.data(), (ng + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-    if (terms > 0) {
-      CU(cudaMemcpyAsync(dx.p, sx.data(), terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-      CU(cudaMemcpyAsync(dz.p, sz.data(), terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-      CU(cudaMemcpyAsync(dc.p, sc.data(), terms * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
-    }
-    from_pauli_kernel<<<static_cast<unsigned>(std::min<int64_t>((ng * d + 127) / 128, 4096)), 128, 0, ctx->stream>>>(
-        doff.p, dx.p, dz.p, dc.p, ng, static_cast<int>(qubits), full.p);
-    launched(ctx);
-    const double2* res = full.p;
-    if (restrict_zero_magnetization) {
-      dst.ensure(static_cast<size_t>(m));
-      sub.ensure(static_cast<size_t>(ng * m * m));
-      CU(cudaMemcpyAsync(dst.p, states.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-      restrict_states_kernel<<<static_cast<unsigned>(std::min<int64_t>((ng * m * m + 255) / 256, 4096)), 256, 0,
-                               ctx->stream>>>(full.p, ng, d, dst.p, m, sub.p);
+    with_keys(qubits, [&](auto tag) {
+      using K = decltype(tag);
+      auto e = pauli_tuple<K>(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
+      std::vector<int64_t> off(1, 0);
+      std::vector<uint64_t> sx, sz;
+      std::vector<double> sc;
+      for (const auto& g : gens) {
+        const int64_t n = static_cast<int64_t>(g.size());
+        std::vector<uint64_t> tx(n), tz(n);
+        std::vector<double> tc(2 * n);
+        for (int64_t t = 0; t < n; ++t) tx[t] = g[t].x, tz[t] = g[t].z, tc[2 * t] = g[t].re, tc[2 * t + 1] = g[t].im;
+        typename SumEngineT<K>::Segs r;
+        e->from_terms_one(n, tx.data(), tz.data(), tc.data(), r);
+        const int64_t base = off.back();
+        sx.resize(base + r.total), sz.resize(base + r.total), sc.resize(2 * (base + r.total));
+        e->download_one(r, sx.data() + base, sz.data() + base, sc.data() + 2 * base, r.total);
+        off.push_back(base + r.total);
+      }
+      if (!dense && !restrict_zero_magnetization) {
+        if (!offsets) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+        std::copy(off.begin(), off.end(), offsets);
+        if (off.back() > term_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+        if (off.back() > 0 && (!x || !z || !coef)) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+        std::copy(sx.begin(), sx.end(), x);
+        std::copy(sz.begin(), sz.end(), z);
+        std::copy(sc.begin(), sc.end(), coef);
+        return;
+      }
+      // dense: from_pauli (R:src/dense.cpp:70-98) on the device, then the
+      // zero-magnetization restriction when asked (R:src/dense.cpp:167-199)
+      if (qubits > 12)
+        throw Error(LIECL_B200_CAPACITY, "from_pauli: " + std::to_string(qubits) +
+                                             " qubits exceeds the expansion limit of 12");
+      const int64_t d = int64_t(1) << qubits;
+      std::vector<int64_t> states;
+      if (restrict_zero_magnetization)
+        for (int64_t st = 0; st < d; ++st)
+          if (__builtin_popcountll(static_cast<unsigned long long>(st)) == static_cast<int>(qubits / 2))
+            states.push_back(st);
+      const int64_t m = restrict_zero_magnetization ? static_cast<int64_t>(states.size()) : d;
+      if (dim) *dim = static_cast<int32_t>(m);
+      if (!dense_out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
+      if (ng * m * m * 2 > dense_cap) throw Error(LIECL_B200_CAPACITY, "output buffers too small");
+      DevBuf<int64_t> doff, dst;
+      DevBuf<uint64_t> dx, dz;
+      DevBuf<double2> dc, full, sub;
+      const int64_t terms = off.back();
+      doff.ensure(ng + 1);
+      dx.ensure(std::max<int64_t>(terms, 1));
+      dz.ensure(std::max<int64_t>(terms, 1));
+      dc.ensure(std::max<int64_t>(terms, 1));
+      full.ensure(static_cast<size_t>(ng * d * d));
+      CU(cudaMemcpyAsync(doff.p, off.data(), (ng + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+      if (terms > 0) {
+        CU(cudaMemcpyAsync(dx.p, sx.data(), terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(dz.p, sz.data(), terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(dc.p, sc.data(), terms * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+      }
+      from_pauli_kernel<<<static_cast<unsigned>(std::min<int64_t>((ng * d + 127) / 128, 4096)), 128, 0, ctx->stream>>>(
+          doff.p, dx.p, dz.p, dc.p, ng, static_cast<int>(qubits), full.p);
       launched(ctx);
-      res = sub.p;
-    }
-    CU(cudaMemcpyAsync(dense_out, res, static_cast<size_t>(ng * m * m) * sizeof(double2), cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+      const double2* res = full.p;
+      if (restrict_zero_magnetization) {
+        dst.ensure(static_cast<size_t>(m));
+        sub.ensure(static_cast<size_t>(ng * m * m));
+        CU(cudaMemcpyAsync(dst.p, states.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+        restrict_states_kernel<<<static_cast<unsigned>(std::min<int64_t>((ng * m * m + 255) / 256, 4096)), 256, 0,
+                                 ctx->stream>>>(full.p, ng, d, dst.p, m, sub.p);
+        launched(ctx);
+        res = sub.p;
+      }
+      CU(cudaMemcpyAsync(dense_out, res, static_cast<size_t>(ng * m * m) * sizeof(double2), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    });
   });
 }
 
@@ -2041,8 +2090,11 @@ int liecl_b200_norm_pauli(liecl_b200_ctx* ctx, int64_t h_terms, const uint64_t* 
     if (!ctx || !out) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     check_sum_args(h_terms, hx, hz, hcoef);
     use_device(ctx);
-    auto e = pauli_tuple(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
-    *out = e->norm_one(h_terms, hx, hz, hcoef);
+    with_keys(qubits, [&](auto tag) {
+      using K = decltype(tag);
+      auto e = pauli_tuple<K>(ctx, nullptr, nullptr, nullptr, nullptr, 0, qubits);
+      *out = e->norm_one(h_terms, hx, hz, hcoef);
+    });
   });
 }
 
@@ -2055,32 +2107,35 @@ int liecl_b200_check_matrix_inversion_pauli(liecl_b200_ctx* ctx, const int64_t* 
     if (!ctx || !independent || (n > 0 && (!inverse || !beta_out))) throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     check_sum_args(h_terms, hx, hz, hcoef);
     use_device(ctx);
-    auto e = pauli_tuple(ctx, offsets, x, z, coef, n, qubits);
-    SumEngine::Segs r;
-    double rn = 0.0;
-    if (n == 0) {  // norm(h) (R:src/closure.cpp:121-123)
-      rn = e->norm_one(h_terms, hx, hz, hcoef);
-    } else {
-      // beta_l = <B_l, h>; x = A^{-1} beta (device GEMM); residual = h - sum_l x_l B_l
-      e->overlaps_one(h_terms, hx, hz, hcoef, beta_out);
-      GramOps& g = gram_ops(ctx);
-      g.ai.ensure(static_cast<size_t>(n * n));
-      g.beta.ensure(static_cast<size_t>(n));
-      g.u.ensure(static_cast<size_t>(n));
-      CU(cudaMemcpyAsync(g.ai.p, inverse, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyHostToDevice,
-                         ctx->stream));
-      CU(cudaMemcpyAsync(g.beta.p, beta_out, static_cast<size_t>(n) * sizeof(double2), cudaMemcpyHostToDevice,
-                         ctx->stream));
-      gemm_mc_store(ctx, g.ai.p, n, n, n, g.beta.p, n, 1, g.u.p, n, 1.0);
-      std::vector<double> xs(static_cast<size_t>(2 * n));
-      CU(cudaMemcpyAsync(xs.data(), g.u.p, static_cast<size_t>(n) * sizeof(double2), cudaMemcpyDeviceToHost,
-                         ctx->stream));
-      CU(cudaStreamSynchronize(ctx->stream));
-      e->combine_one(h_terms, hx, hz, hcoef, 1.0, 0.0, xs.data(), true, r);  // coefficients -x_l
-      rn = e->norm_of(r);
-    }
-    *independent = rn > tol ? 1 : 0;
-    if (residual_norm) *residual_norm = rn;
+    with_keys(qubits, [&](auto tag) {
+      using K = decltype(tag);
+      auto e = pauli_tuple<K>(ctx, offsets, x, z, coef, n, qubits);
+      typename SumEngineT<K>::Segs r;
+      double rn = 0.0;
+      if (n == 0) {  // norm(h) (R:src/closure.cpp:121-123)
+        rn = e->norm_one(h_terms, hx, hz, hcoef);
+      } else {
+        // beta_l = <B_l, h>; x = A^{-1} beta (device GEMM); residual = h - sum_l x_l B_l
+        e->overlaps_one(h_terms, hx, hz, hcoef, beta_out);
+        GramOps& g = gram_ops(ctx);
+        g.ai.ensure(static_cast<size_t>(n * n));
+        g.beta.ensure(static_cast<size_t>(n));
+        g.u.ensure(static_cast<size_t>(n));
+        CU(cudaMemcpyAsync(g.ai.p, inverse, static_cast<size_t>(n * n) * sizeof(double2), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CU(cudaMemcpyAsync(g.beta.p, beta_out, static_cast<size_t>(n) * sizeof(double2), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        gemm_mc_store(ctx, g.ai.p, n, n, n, g.beta.p, n, 1, g.u.p, n, 1.0);
+        std::vector<double> xs(static_cast<size_t>(2 * n));
+        CU(cudaMemcpyAsync(xs.data(), g.u.p, static_cast<size_t>(n) * sizeof(double2), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        e->combine_one(h_terms, hx, hz, hcoef, 1.0, 0.0, xs.data(), true, r);  // coefficients -x_l
+        rn = e->norm_of(r);
+      }
+      *independent = rn > tol ? 1 : 0;
+      if (residual_norm) *residual_norm = rn;
+    });
   });
 }
 

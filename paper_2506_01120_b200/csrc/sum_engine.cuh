@@ -20,19 +20,24 @@
 // element l = [off[l], off[l+1])); a key -> (l, coefficient) index with
 // per-key lists in ascending l serves sum_inner_product's merge join.
 
-class SumEngine {
+template <class K> class SumEngineT {
 public:
+  // 1..31 qubits with narrow keys (x | z << 32), 32..63 with WKey {x, z}
+  // (pauli_sum.cuh); all ones is the key arrays' marker, so 64-qubit sums
+  // (where Y^64 is all ones) are refused
+  static constexpr unsigned kMaxQubits = std::is_same_v<K, psum::WKey> ? 63 : 31;
   // gram = true: Alg. 2 (matrix inversion, R:src/closure.cpp:214-265) -- the
   // pool holds the accepted unit brackets B, a check is beta = <B_l, h>,
   // x = A^{-1} beta (device GEMM against the maintained inverse), residual
   // from_terms(h ++ -x_l B_l) (R:src/closure.cpp:107-131) in one pass, and an
   // accept expands A and A^{-1} (bordered update, refresh as GramEngine)
-  SumEngine(liecl_b200_ctx* ctx, unsigned qubits, bool keep_original, const liecl_b200_config& cfg, bool gram = false)
+  SumEngineT(liecl_b200_ctx* ctx, unsigned qubits, bool keep_original, const liecl_b200_config& cfg, bool gram = false)
       : ctx_(ctx), q_(qubits), keep_(keep_original && !gram), gram_(gram), tol_(cfg.tolerance),
         floor_(cfg.conditioning_floor), interval_(cfg.gram_refresh_interval), record_(cfg.record_log != 0) {
-    if (qubits < 1 || qubits > 31) throw Error(LIECL_B200_INVALID_INPUT, "Pauli path supports 1..31 qubits");
+    if (qubits < 1 || qubits > kMaxQubits)
+      throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..63 qubits");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
-    const uint64_t full = 1ull << (2 * qubits);
+    const uint64_t full = qubits >= 32 ? ~0ull : (1ull << (2 * qubits));
     cap_ = cfg.max_dim ? static_cast<int64_t>(std::min<uint64_t>(cfg.max_dim, full)) : static_cast<int64_t>(full);
     budget_ = cfg.batch_max > 0 ? cfg.batch_max : (int64_t(1) << 24);
     if (cfg.deadline_seconds > 0) {
@@ -95,17 +100,17 @@ public:
     const int64_t nt = ngens > 0 ? goff[ngens] : 0;
     if (nt > (int64_t(1) << 30)) throw Error(LIECL_B200_CAPACITY, "generator terms exceed 2^30");
     std::vector<int> hoff(static_cast<size_t>(ngens) + 1);
-    std::vector<unsigned long long> hkey(static_cast<size_t>(std::max<int64_t>(nt, 1)));
+    std::vector<K> hkey(static_cast<size_t>(std::max<int64_t>(nt, 1)));
     for (int i = 0; i <= ngens; ++i) hoff[i] = static_cast<int>(goff[i]);
     for (int64_t t = 0; t < nt; ++t) {
       if ((gx[t] & ~kmask) || (gz[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
-      hkey[t] = pauli::pack(gx[t], gz[t]);
+      hkey[t] = psum::kpack<K>(gx[t], gz[t]);
     }
     Segs g;
     g.shape(ngens, static_cast<int>(nt));
     CU(cudaMemcpyAsync(g.off.p, hoff.data(), hoff.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
     if (nt > 0) {
-      CU(cudaMemcpyAsync(g.key.p, hkey.data(), nt * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+      CU(cudaMemcpyAsync(g.key.p, hkey.data(), nt * sizeof(K), cudaMemcpyHostToDevice,
                          ctx_->stream));
       CU(cudaMemcpyAsync(g.val.p, gc, nt * sizeof(psum::C2), cudaMemcpyHostToDevice, ctx_->stream));
     }
@@ -168,14 +173,13 @@ public:
     const int64_t nt = o.back();
     for (int64_t l = 0; l <= n_; ++l) off[l] = o[l];
     if (nt == 0) return;
-    std::vector<unsigned long long> k(static_cast<size_t>(nt));
-    CU(cudaMemcpyAsync(k.data(), (v ? vkey_ : okey_).p, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                       ctx_->stream));
+    std::vector<K> k(static_cast<size_t>(nt));
+    CU(cudaMemcpyAsync(k.data(), (v ? vkey_ : okey_).p, nt * sizeof(K), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaMemcpyAsync(coef, (v ? vval_ : oval_).p, nt * sizeof(psum::C2), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
     for (int64_t t = 0; t < nt; ++t) {
-      x[t] = k[t] & 0xffffffffull;
-      z[t] = k[t] >> 32;
+      x[t] = psum::kx(k[t]);
+      z[t] = psum::kz(k[t]);
     }
   }
 
@@ -185,10 +189,10 @@ private:
   bool trace_ = std::getenv("LIECL_B200_TRACE") != nullptr;
   std::map<std::string, std::pair<double, uint64_t>> tsum_;
   struct Stage {
-    SumEngine* e;
+    SumEngineT* e;
     const char* name;
     Clock::time_point t0;
-    Stage(SumEngine* eng, const char* n) : e(eng), name(n) {
+    Stage(SumEngineT* eng, const char* n) : e(eng), name(n) {
       if (e->trace_) {
         cudaStreamSynchronize(e->ctx_->stream);
         t0 = Clock::now();
@@ -212,7 +216,7 @@ public:
   struct Segs {  // nseg sums on the device: terms [off[p], off[p+1])
     int nseg = 0, total = 0;
     DevBuf<int> off;
-    DevBuf<unsigned long long> key;
+    DevBuf<K> key;
     DevBuf<C2> val;
     void shape(int ns, int tot) {
       nseg = ns;
@@ -306,8 +310,8 @@ private:
   // run_seg_ = each run's segment)
   // pauli_q > 0: keys are packed Pauli strings (kbits = 2q); 0: basis indices
   // below 2^kbits
-  void merge(int nseg, const int* off, const unsigned long long* key, const C2* val, int n, bool drop, Segs& out,
-             int pauli_q, int kbits) {
+  void merge(int nseg, const int* off, const K* key, const C2* val, int n, bool drop, Segs& out, int pauli_q,
+             int kbits) {
     Stage st_merge(this, drop ? "merge" : "merge_beta");
     if (n == 0) {
       out.shape(nseg, 0);
@@ -340,6 +344,34 @@ private:
                                            ctx_->stream));
       }
       psum::split_kernel<<<grid(n), 256, 0, ctx_->stream>>>(cks_.p, n, pauli_q, kbits, ks_.p, seg_.p);
+      launched(ctx_), launched(ctx_);
+    } else if constexpr (std::is_same_v<K, psum::WKey>) {
+      // wide keys: the (z, x) order within segments by two stable passes,
+      // x first; index keys (pauli_q == 0) sort by x alone
+      need(ck_, n);
+      need(cks_, n);
+      need(is1_, n);
+      const int passes = pauli_q > 0 ? 2 : 1;
+      const unsigned* perm = nullptr;
+      unsigned* dst[2] = {passes == 2 ? is1_.p : is_.p, is_.p};
+      const unsigned* src[2] = {idx_.p, is1_.p};
+      for (int w = 0; w < passes; ++w) {
+        psum::wide_words_kernel<<<grid(n), 256, 0, ctx_->stream>>>(key, perm, n, w, ck_.p);
+        launched(ctx_);
+        bytes = 0;
+        CU(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, ck_.p, cks_.p, src[w], dst[w], n, nseg, off,
+                                                     off + 1, ctx_->stream));
+        ensure_temp(bytes);
+        {
+          Stage st_s(this, "segsort");
+          CU(cub::DeviceSegmentedSort::StableSortPairs(temp_.p, bytes, ck_.p, cks_.p, src[w], dst[w], n, nseg, off,
+                                                       off + 1, ctx_->stream));
+        }
+        launched(ctx_);
+        perm = dst[w];
+      }
+      psum::gather_keys_kernel<<<grid(n), 256, 0, ctx_->stream>>>(key, is_.p, n, ks_.p);
+      psum::seg_of_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, n, seg_.p);
       launched(ctx_), launched(ctx_);
     } else {
       CU(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off, off + 1,
@@ -397,18 +429,18 @@ private:
     const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
     std::vector<int> ho(static_cast<size_t>(nseg) + 1);
     for (int p = 0; p <= nseg; ++p) ho[p] = static_cast<int>(off[p] - t0);
-    std::vector<unsigned long long> hk(static_cast<size_t>(std::max<int64_t>(nt, 1)));
+    std::vector<K> hk(static_cast<size_t>(std::max<int64_t>(nt, 1)));
     for (int p = 0; p < nseg; ++p)
       for (int64_t t = off[p]; t < off[p + 1]; ++t) {
         if ((x[t] & ~kmask) || (z[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
-        if (t > off[p] && pauli::pack(x[t], z[t]) <= pauli::pack(x[t - 1], z[t - 1]))
+        hk[t - t0] = psum::kpack<K>(x[t], z[t]);
+        if (t > off[p] && !psum::kless(hk[t - 1 - t0], hk[t - t0]))
           throw Error(LIECL_B200_INVALID_INPUT, "sum terms must be unique and sorted by (z, x)");
-        hk[t - t0] = pauli::pack(x[t], z[t]);
       }
     out.shape(nseg, static_cast<int>(nt));
     CU(cudaMemcpyAsync(out.off.p, ho.data(), ho.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
     if (nt > 0) {
-      CU(cudaMemcpyAsync(out.key.p, hk.data(), nt * sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx_->stream));
+      CU(cudaMemcpyAsync(out.key.p, hk.data(), nt * sizeof(K), cudaMemcpyHostToDevice, ctx_->stream));
       CU(cudaMemcpyAsync(out.val.p, coef + 2 * t0, nt * sizeof(C2), cudaMemcpyHostToDevice, ctx_->stream));
     }
     CU(cudaStreamSynchronize(ctx_->stream));  // host staging vectors
@@ -417,14 +449,15 @@ private:
   void beta_to_host(double* beta) {
     const int nr = beta_.total;
     if (nr == 0) return;
-    std::vector<unsigned long long> l(static_cast<size_t>(nr));
+    std::vector<K> l(static_cast<size_t>(nr));
     std::vector<C2> v(static_cast<size_t>(nr));
-    CU(cudaMemcpyAsync(l.data(), beta_.key.p, nr * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(l.data(), beta_.key.p, nr * sizeof(K), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaMemcpyAsync(v.data(), beta_.val.p, nr * sizeof(C2), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
     for (int r = 0; r < nr; ++r) {
-      beta[2 * l[r]] = v[r].re;
-      beta[2 * l[r] + 1] = v[r].im;
+      const int64_t li = psum::kindex(l[r]);
+      beta[2 * li] = v[r].re;
+      beta[2 * li + 1] = v[r].im;
     }
   }
 
@@ -513,10 +546,10 @@ private:
     if (!fused_ || h.nseg > kFusedMaxBatch || fused_fallbacks_ > fused_batches_ + 8) return false;
     const int hc = n_limit <= 4096 ? 2048 : (n_limit <= 8192 ? 1024 : 0);
     if (hc == 0) return false;
-    const size_t smem = psum::fused_smem_bytes(hc, n_limit);
+    const size_t smem = psum::fused_smem_bytes<K>(hc, n_limit);
     if (smem > kFusedSmemMax) return false;
     if (!fused_attr_) {
-      CU(cudaFuncSetAttribute(psum::fused_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CU(cudaFuncSetAttribute(psum::fused_check_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(kFusedSmemMax)));
       fused_attr_ = true;
     }
@@ -773,7 +806,7 @@ private:
     b.shape(a.nseg, a.total);
     CU(cudaMemcpyAsync(b.off.p, a.off.p, (a.nseg + 1) * sizeof(int), cudaMemcpyDeviceToDevice, ctx_->stream));
     if (a.total > 0) {
-      CU(cudaMemcpyAsync(b.key.p, a.key.p, a.total * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+      CU(cudaMemcpyAsync(b.key.p, a.key.p, a.total * sizeof(K), cudaMemcpyDeviceToDevice,
                          ctx_->stream));
       CU(cudaMemcpyAsync(b.val.p, a.val.p, a.total * sizeof(C2), cudaMemcpyDeviceToDevice, ctx_->stream));
     }
@@ -788,7 +821,7 @@ private:
     psum::rebase_kernel<<<grid(b - a + 1), 256, 0, ctx_->stream>>>(src.off.p, a, b - a, dst.off.p);
     launched(ctx_);
     if (hi > lo) {
-      CU(cudaMemcpyAsync(dst.key.p, src.key.p + lo, (hi - lo) * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+      CU(cudaMemcpyAsync(dst.key.p, src.key.p + lo, (hi - lo) * sizeof(K), cudaMemcpyDeviceToDevice,
                          ctx_->stream));
       CU(cudaMemcpyAsync(dst.val.p, src.val.p + lo, (hi - lo) * sizeof(C2), cudaMemcpyDeviceToDevice, ctx_->stream));
     }
@@ -803,12 +836,12 @@ private:
     for (int p = a.nseg; p <= a.nseg + b.nseg; ++p) ho[p] += a.total;
     CU(cudaMemcpyAsync(out.off.p, ho.data(), ho.size() * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
     if (a.total) {
-      CU(cudaMemcpyAsync(out.key.p, a.key.p, a.total * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+      CU(cudaMemcpyAsync(out.key.p, a.key.p, a.total * sizeof(K), cudaMemcpyDeviceToDevice,
                          ctx_->stream));
       CU(cudaMemcpyAsync(out.val.p, a.val.p, a.total * sizeof(C2), cudaMemcpyDeviceToDevice, ctx_->stream));
     }
     if (b.total) {
-      CU(cudaMemcpyAsync(out.key.p + a.total, b.key.p, b.total * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+      CU(cudaMemcpyAsync(out.key.p + a.total, b.key.p, b.total * sizeof(K), cudaMemcpyDeviceToDevice,
                          ctx_->stream));
       CU(cudaMemcpyAsync(out.val.p + a.total, b.val.p, b.total * sizeof(C2), cudaMemcpyDeviceToDevice,
                          ctx_->stream));
@@ -818,13 +851,13 @@ private:
 
   // ---- basis pools + index ----------------------------------------------
   void grow_index(uint64_t slots) {
-    DevBuf<unsigned long long> k;
+    DevBuf<K> k;
     DevBuf<int> h, t, c;
     k.ensure(slots);
     h.ensure(slots);
     t.ensure(slots);
     c.ensure(slots);
-    psum::Index nx = ix_;
+    psum::Index<K> nx = ix_;
     nx.key = k.p, nx.head = h.p, nx.tail = t.p, nx.count = c.p, nx.mask = slots - 1;
     psum::index_reset_kernel<<<grid(static_cast<int64_t>(slots)), 256, 0, ctx_->stream>>>(nx, slots);
     launched(ctx_);
@@ -846,7 +879,7 @@ private:
   }
 
   // V pool + index: append one element (device terms), scaled by 1/rn (rn = 0: as given)
-  void append_pool(const unsigned long long* key, const C2* val, int T, double rn) {
+  void append_pool(const K* key, const C2* val, int T, double rn) {
     const int64_t vt = voff_.back();
     grow_keep(vkey_, static_cast<size_t>(vt), static_cast<size_t>(vt + T));
     grow_keep(vval_, static_cast<size_t>(vt), static_cast<size_t>(vt + T));
@@ -855,7 +888,7 @@ private:
         psum::append_scaled_kernel<<<grid(T), 256, 0, ctx_->stream>>>(key, val, T, rn, vkey_.p + vt, vval_.p + vt);
         launched(ctx_);
       } else {
-        CU(cudaMemcpyAsync(vkey_.p + vt, key, T * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, ctx_->stream));
+        CU(cudaMemcpyAsync(vkey_.p + vt, key, T * sizeof(K), cudaMemcpyDeviceToDevice, ctx_->stream));
         CU(cudaMemcpyAsync(vval_.p + vt, val, T * sizeof(C2), cudaMemcpyDeviceToDevice, ctx_->stream));
       }
     }
@@ -907,7 +940,7 @@ private:
       grow_keep(okey_, static_cast<size_t>(ot), static_cast<size_t>(ot + h1 - h0));
       grow_keep(oval_, static_cast<size_t>(ot), static_cast<size_t>(ot + h1 - h0));
       if (h1 > h0) {
-        CU(cudaMemcpyAsync(okey_.p + ot, h.key.p + h0, (h1 - h0) * sizeof(unsigned long long),
+        CU(cudaMemcpyAsync(okey_.p + ot, h.key.p + h0, (h1 - h0) * sizeof(K),
                            cudaMemcpyDeviceToDevice, ctx_->stream));
         CU(cudaMemcpyAsync(oval_.p + ot, h.val.p + h0, (h1 - h0) * sizeof(C2), cudaMemcpyDeviceToDevice,
                            ctx_->stream));
@@ -957,7 +990,7 @@ private:
       need(pk_, std::max<int64_t>(prods, 1));
       need(pv_, std::max<int64_t>(prods, 1));
       const int64_t* bdoff = keep_ ? dooff_.p : dvoff_.p;
-      const unsigned long long* bkey = keep_ ? okey_.p : vkey_.p;
+      const K* bkey = keep_ ? okey_.p : vkey_.p;
       const C2* bval = keep_ ? oval_.p : vval_.p;
       Stage st_p(this, "products");
       psum::products_kernel<<<cnt, 256, 0, ctx_->stream>>>(g0, cnt, poff_.p, bdoff, bkey, bval, pk_.p, pv_.p);
@@ -1051,21 +1084,22 @@ private:
   // basis pools: orthonormal tuple V; originals O (Alg. 3, commutator basis)
   std::vector<int64_t> voff_, ooff_;
   DevBuf<int64_t> dvoff_, dooff_;
-  DevBuf<unsigned long long> vkey_, okey_;
+  DevBuf<K> vkey_, okey_;
   DevBuf<C2> vval_, oval_;
   // index
-  psum::Index ix_{};
+  psum::Index<K> ix_{};
   uint64_t slots_ = 0, keys_upper_ = 0;
   int64_t entries_ = 0;
-  DevBuf<unsigned long long> skey_;
+  DevBuf<K> skey_;
   DevBuf<int> shead_, stail_, scount_, el_, enext_;
   DevBuf<C2> ev_;
   // batch scratch
   DevBuf<unsigned char> temp_;
   DevBuf<int> small_, poff_, seg_, flag_, pos_, run_seg_, roff_, keep_flag_, kpos_, boff_;
   DevBuf<long long> cnt_, cpos_, clen_, chpos_, total_ll_;
-  DevBuf<unsigned> idx_, is_;
-  DevBuf<unsigned long long> ks_, rkey_, pk_, bl_, ck_, cks_;
+  DevBuf<unsigned> idx_, is_, is1_;
+  DevBuf<K> ks_, rkey_, pk_, bl_;
+  DevBuf<unsigned long long> ck_, cks_;  // composite sort keys
   DevBuf<C2> rval_, pv_, bv_;
   DevBuf<double> rmag_, hn_, rn_dev_;
   DevBuf<psum::Chunk> chunks_;
@@ -1082,7 +1116,7 @@ private:
   }();
   bool fused_attr_ = false;
   uint64_t fused_batches_ = 0, fused_fallbacks_ = 0;
-  DevBuf<unsigned long long> fk_;
+  DevBuf<K> fk_;
   DevBuf<C2> fv_;
   DevBuf<int> flen_, fst_;
   DevBuf<double> frn_;
@@ -1150,18 +1184,18 @@ public:
     Segs h;
     const int64_t off[2] = {0, nterms};
     upload(off, x, z, coef, 1, h);
-    std::vector<unsigned long long> lk;
+    std::vector<K> lk;
     std::vector<C2> lv;
     for (int64_t l = 0; l < n_; ++l)
       if (coeffs[2 * l] != 0.0 || coeffs[2 * l + 1] != 0.0) {
-        lk.push_back(static_cast<unsigned long long>(l));
+        lk.push_back(psum::kfrom_index<K>(l));
         lv.push_back({coeffs[2 * l], coeffs[2 * l + 1]});
       }
     beta_.shape(1, static_cast<int>(lk.size()));
     const int bo[2] = {0, static_cast<int>(lk.size())};
     CU(cudaMemcpyAsync(beta_.off.p, bo, sizeof bo, cudaMemcpyHostToDevice, ctx_->stream));
     if (!lk.empty()) {
-      CU(cudaMemcpyAsync(beta_.key.p, lk.data(), lk.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+      CU(cudaMemcpyAsync(beta_.key.p, lk.data(), lk.size() * sizeof(K), cudaMemcpyHostToDevice,
                          ctx_->stream));
       CU(cudaMemcpyAsync(beta_.val.p, lv.data(), lv.size() * sizeof(C2), cudaMemcpyHostToDevice, ctx_->stream));
     }
@@ -1177,17 +1211,17 @@ public:
   void from_terms_one(int64_t n, const uint64_t* x, const uint64_t* z, const double* coef, Segs& out) {
     if (n > kMaxItems) throw Error(LIECL_B200_CAPACITY, "terms exceed 2^30");
     const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
-    std::vector<unsigned long long> hk(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    std::vector<K> hk(static_cast<size_t>(std::max<int64_t>(n, 1)));
     for (int64_t t = 0; t < n; ++t) {
       if ((x[t] & ~kmask) || (z[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
-      hk[t] = pauli::pack(x[t], z[t]);
+      hk[t] = psum::kpack<K>(x[t], z[t]);
     }
     Segs raw;
     raw.shape(1, static_cast<int>(n));
     const int o[2] = {0, static_cast<int>(n)};
     CU(cudaMemcpyAsync(raw.off.p, o, sizeof o, cudaMemcpyHostToDevice, ctx_->stream));
     if (n > 0) {
-      CU(cudaMemcpyAsync(raw.key.p, hk.data(), n * sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx_->stream));
+      CU(cudaMemcpyAsync(raw.key.p, hk.data(), n * sizeof(K), cudaMemcpyHostToDevice, ctx_->stream));
       CU(cudaMemcpyAsync(raw.val.p, coef, n * sizeof(C2), cudaMemcpyHostToDevice, ctx_->stream));
     }
     merge(1, raw.off.p, raw.key.p, raw.val.p, static_cast<int>(n), true, out, static_cast<int>(q_),
@@ -1228,15 +1262,18 @@ public:
   int64_t download_one(const Segs& a, uint64_t* x, uint64_t* z, double* coef, int64_t cap) {
     const int64_t nt = a.total;
     if (nt > cap || nt == 0) return nt;
-    std::vector<unsigned long long> k(static_cast<size_t>(nt));
-    CU(cudaMemcpyAsync(k.data(), a.key.p, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx_->stream));
+    std::vector<K> k(static_cast<size_t>(nt));
+    CU(cudaMemcpyAsync(k.data(), a.key.p, nt * sizeof(K), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaMemcpyAsync(coef, a.val.p, nt * sizeof(C2), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
     for (int64_t t = 0; t < nt; ++t) {
-      x[t] = k[t] & 0xffffffffull;
-      z[t] = k[t] >> 32;
+      x[t] = psum::kx(k[t]);
+      z[t] = psum::kz(k[t]);
     }
     return nt;
   }
 
 };
+
+using SumEngine = SumEngineT<unsigned long long>;      // 1..31 qubits
+using SumEngineWide = SumEngineT<psum::WKey>;          // 32..63 qubits

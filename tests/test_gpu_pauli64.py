@@ -143,3 +143,83 @@ def test_qubit_range():
     r = liecl.closure_pauli_arrays(np.array([ALL], np.uint64), np.array([ALL], np.uint64), c, 64,
                                    config=liecl.ClosureConfig(max_dim=8))
     assert r.dimension == 1 and int(r.basis_array[0][0]) == ALL
+
+
+# ---- multi-term sums on 32..63 qubits (SumEngineT<WKey>: 128-bit keys) ------
+
+def embed_masks(a, pos):
+    out = np.zeros(len(a), np.uint64)
+    for i, m in enumerate(a):
+        v = 0
+        for j, p in enumerate(pos):
+            if (int(m) >> j) & 1:
+                v |= 1 << p
+        out[i] = v
+    return out
+
+
+WIDE = [("tfim_hva_open", 4, 16, 48, [3, 31, 40, 47]), ("xxz_hva", 4, 10, 63, [0, 33, 34, 62]),
+        ("spin_glass_hva", 3, 63, 40, [5, 32, 39])]
+
+
+@pytest.mark.parametrize("method", [liecl.Method.orthonorm_dimonly, liecl.Method.orthonorm],
+                         ids=["dimonly", "orthonorm"])
+@pytest.mark.parametrize("family,n,dim,q,pos", WIDE, ids=[w_[0] for w_ in WIDE])
+def test_wide_sums_match_reference(ref_exact, family, n, dim, q, pos, method):
+    """The reference's catalog generators relabelled onto qubits past 31: the
+    wide-key engine against the reference build, bit for bit (basis terms,
+    coefficient bits, statistics, decision log residual bits)."""
+    off, x, z, c = ref_exact.build_generators(family, n)
+    ex, ez = embed_masks(x, pos), embed_masks(z, pos)
+    keep = method == liecl.Method.orthonorm
+    res = liecl.closure_pauli_sums_arrays(off, ex, ez, c, q, method,
+                                          liecl.ClosureConfig(tolerance=1e-10, record_log=True, max_dim=4096))
+    o = ref_exact.closure_pauli(off, ex, ez, c, q, method=liecl.to_string(method), tol=1e-10, threads=4,
+                                max_dim=4096, basis_cap=4096)
+    assert res.dimension == o.dimension == dim
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(res.stats, k) == o.stats[k], k
+    bo, bx, bz, bc = res.basis_array
+    ro, rx, rz, rc = o.basis
+    assert np.array_equal(bo, ro) and np.array_equal(bx, rx) and np.array_equal(bz, rz)
+    assert np.array_equal(bc.view(np.uint64), rc.view(np.uint64))
+    assert int(max(bx.max(), bz.max())) >> 32  # genuinely past 32 bits
+    lg = ref_exact.decision_log_pauli(off, ex, ez, c, q, keep_original=keep, tol=1e-10, basis_cap=4096)
+    mine = res.decision_log
+    assert len(mine) == len(lg.log)
+    for f in ("l", "m", "null_cand", "independent"):
+        assert np.array_equal(mine[f], lg.log[f]), f
+    assert np.array_equal(mine["residual_norm"].view(np.uint64), lg.log["residual_norm"].view(np.uint64))
+
+
+def test_wide_sums_equal_narrow_relabelled(ref_exact, monkeypatch):
+    """Narrow (31-qubit) and wide keys on the same algebra: identical bits
+    once relabelled; also with the fused single-CTA check switched off."""
+    off, x, z, c = ref_exact.build_generators("tfim_hva_open", 6)
+    pos = [1, 20, 32, 44, 50, 61]
+    cfg = liecl.ClosureConfig(tolerance=1e-10, record_log=True, max_dim=4096)
+    small = liecl.closure_pauli_sums_arrays(off, x, z, c, 6, config=cfg)
+    for fused in ("1", "0"):
+        monkeypatch.setenv("LIECL_B200_SUMS_FUSED", fused)
+        big = liecl.closure_pauli_sums_arrays(off, embed_masks(x, pos), embed_masks(z, pos), c, 62, config=cfg)
+        so, sx, sz, sc = small.basis_array
+        bo, bx, bz, bc = big.basis_array
+        assert big.dimension == small.dimension == 36
+        assert np.array_equal(bo, so)
+        assert np.array_equal(bx, embed_masks(sx, pos)) and np.array_equal(bz, embed_masks(sz, pos))
+        assert np.array_equal(bc.view(np.uint64), sc.view(np.uint64))
+        assert np.array_equal(big.decision_log["residual_norm"].view(np.uint64),
+                              small.decision_log["residual_norm"].view(np.uint64))
+
+
+def test_wide_parse_matches_reference(ref_exact):
+    """parse_pauli_sum (the reference grammar; from_terms on the device, wide
+    keys) on 40 qubits against the reference build."""
+    q = 40
+    text = "1.5 " + "X" * 33 + "Z" + "I" * 6 + " - (0,2) " + "I" * 39 + "Y" + " + 0.25 " + "X" * 33 + "Z" + "I" * 6
+    got = liecl.parse_pauli_sum(text, q)
+    rx, rz, rc = ref_exact.parse_pauli_sum(text, q)
+    assert [(t[0].x, t[0].z) for t in got.terms] == list(zip(map(int, rx), map(int, rz)))
+    assert np.array_equal(np.array([[t[1].real, t[1].imag] for t in got.terms]).view(np.uint64), rc.view(np.uint64))
+    with pytest.raises(liecl.InvalidInputError):
+        liecl.parse_pauli_sum("1.0 " + "X" * 64, 64)  # 64-qubit sums: the key marker (DESIGN §9)

@@ -35,13 +35,15 @@ static CUtensorMap map_kc(const double* p, int64_t len, int64_t rows, int64_t ld
   if (r != CUDA_SUCCESS) { printf("encode kc failed %d\n", r); exit(1); }
   return m;
 }
-// A(m, k) = p[k*ld + m], M a multiple of 16: 3-D {16, K, M/16} box {16, 16, 8}
+// A(m, k) = p[k*ld + m], M a multiple of 16, k = 4t + 2p + q: 5-D {16, 2, ceil(K/4), 2, M/16}
 static CUtensorMap map_mc(const double* p, int64_t M, int64_t K, int64_t ld) {
   CUtensorMap m;
-  cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M / 16)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 8), 128};
-  cuuint32_t box[3] = {16, 16, 8}, es[3] = {1, 1, 1};
-  CUresult r = encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, es,
+  const int64_t kq = (K + 3) / 4;
+  cuuint64_t dims[5] = {16, 2, static_cast<cuuint64_t>(kq), 2, static_cast<cuuint64_t>(M / 16)};
+  cuuint64_t strides[4] = {static_cast<cuuint64_t>(ld * 8), static_cast<cuuint64_t>(ld * 32),
+                           static_cast<cuuint64_t>(ld * 16), 128};
+  cuuint32_t box[5] = {16, 2, 4, 2, 8}, es[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(p), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { printf("encode mc failed %d\n", r); exit(1); }
