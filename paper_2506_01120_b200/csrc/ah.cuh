@@ -221,17 +221,26 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
       for (int c = 0; c < WC; ++c) ah_elem<LDP>(pb, k, (wc0 + c) * 8 + g, br[c], bi[c]);  // B(k, tj + g)
 #pragma unroll
       for (int r = 0; r < WR; ++r) ah_elem<LDP>(pa, (wr0 + r) * 8 + g, k, ar[r], ai[r]);  // A(ti + g, k)
+      // four sweeps over the warp's tiles: two DMMAs into the same
+      // accumulator are WR*WC*2 - 1 instructions apart (no back-to-back
+      // dependency on the DMMA latency); each accumulator still adds its
+      // terms in the same order (re: ar br, then -ai bi; im: ar bi, then ai br)
 #pragma unroll
-      for (int r = 0; r < WR; ++r) {
-        const double nai = -ai[r];
+      for (int r = 0; r < WR; ++r)
 #pragma unroll
-        for (int c = 0; c < WC; ++c) {
-          dmma_8x8x4(cre[r][c][0], cre[r][c][1], ar[r], br[c]);
-          dmma_8x8x4(cre[r][c][0], cre[r][c][1], nai, bi[c]);
-          dmma_8x8x4(cim[r][c][0], cim[r][c][1], ar[r], bi[c]);
-          dmma_8x8x4(cim[r][c][0], cim[r][c][1], ai[r], br[c]);
-        }
-      }
+        for (int c = 0; c < WC; ++c) dmma_8x8x4(cre[r][c][0], cre[r][c][1], ar[r], br[c]);
+#pragma unroll
+      for (int r = 0; r < WR; ++r)
+#pragma unroll
+        for (int c = 0; c < WC; ++c) dmma_8x8x4(cim[r][c][0], cim[r][c][1], ar[r], bi[c]);
+#pragma unroll
+      for (int r = 0; r < WR; ++r)
+#pragma unroll
+        for (int c = 0; c < WC; ++c) dmma_8x8x4(cre[r][c][0], cre[r][c][1], -ai[r], bi[c]);
+#pragma unroll
+      for (int r = 0; r < WR; ++r)
+#pragma unroll
+        for (int c = 0; c < WC; ++c) dmma_8x8x4(cim[r][c][0], cim[r][c][1], ai[r], br[c]);
     }
   }
   __syncthreads();  // inputs consumed: P planes reuse the packed buffers

@@ -755,7 +755,10 @@ public:
     counters_.ensure(3);
   }
 
-  static uint64_t full_dim(unsigned qubits) { return qubits >= 32 ? ~0ull : (1ull << (2 * qubits)); }
+  // 4^q, saturated at INT64_MAX (31+ qubits: no cap beyond max_dim)
+  static uint64_t full_dim(unsigned qubits) {
+    return qubits >= 31 ? static_cast<uint64_t>(INT64_MAX) : (1ull << (2 * qubits));
+  }
 
   bool compatible(unsigned qubits, bool keep, const liecl_b200_config& cfg) const {
     const uint64_t full = full_dim(qubits);

@@ -37,7 +37,7 @@ public:
     if (qubits < 1 || qubits > kMaxQubits)
       throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..63 qubits");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
-    const uint64_t full = qubits >= 32 ? ~0ull : (1ull << (2 * qubits));
+    const uint64_t full = qubits >= 31 ? static_cast<uint64_t>(INT64_MAX) : (1ull << (2 * qubits));
     cap_ = cfg.max_dim ? static_cast<int64_t>(std::min<uint64_t>(cfg.max_dim, full)) : static_cast<int64_t>(full);
     budget_ = cfg.batch_max > 0 ? cfg.batch_max : (int64_t(1) << 24);
     if (cfg.deadline_seconds > 0) {

@@ -143,6 +143,11 @@ def test_qubit_range():
     r = liecl.closure_pauli_arrays(np.array([ALL], np.uint64), np.array([ALL], np.uint64), c, 64,
                                    config=liecl.ClosureConfig(max_dim=8))
     assert r.dimension == 1 and int(r.basis_array[0][0]) == ALL
+    # max_dim = 0 on 40 qubits: no cap (the reference's d^2 default overflows)
+    p = w.config4()
+    r = liecl.closure_pauli_arrays(p.x << np.uint64(30), p.z << np.uint64(30), p.coef, 40,
+                                   config=liecl.ClosureConfig(tolerance=p.tol))
+    assert r.dimension == 380
 
 
 # ---- multi-term sums on 32..63 qubits (SumEngineT<WKey>: 128-bit keys) ------
