@@ -96,19 +96,23 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
   T* Zs = reinterpret_cast<T*>(bc_smem);
   T* Gs = Zs + kBcMax * kBcMax;
   __shared__ double s[kBcMax];
+  __shared__ double s_rn2[kBcMax];  // rn2 staged: thread 0's serial decisions read shared memory only
   __shared__ int acc_list[kBcMax];
   __shared__ int s_ind, s_stop;
   const int tid = threadIdx.x;
   const int t = tid >> 2, sub = tid & 3;  // column t, lane sub of its group
   for (int e = tid; e < nb * nb; e += blockDim.x) Gs[(e % nb) + (e / nb) * kBcMax] = G[(e % nb) + static_cast<int64_t>(e / nb) * ldg];
   __syncthreads();
-  if (sub == 0 && t < nb) s[t] = bc_re(Gs[t + t * kBcMax]);
+  if (sub == 0 && t < nb) {
+    s[t] = bc_re(Gs[t + t * kBcMax]);
+    s_rn2[t] = rn2[t];
+  }
   int acc = 0, tent = 0;
   if (tid == 0) dec->cap_hit = -1;
   __syncthreads();
   for (int q = 0; q < nb; ++q) {
     if (tid == 0) {
-      const double r2 = rn2[q];
+      const double r2 = s_rn2[q];
       const bool recheck = acc > 0 && r2 > tol;
       int ind;
       int fl = recheck ? 2 : 0;
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(kBcThreads) bc_tri_inverse_kernel(const T* __r
 // exact per-survivor kernel above a bound)
 template <class T>
 __global__ void bc_orth_error_kernel(const T* __restrict__ G, int ldg, int a, double* __restrict__ out) {
-  __shared__ double red[kBcMax];
+  __shared__ double red[32];
   double m = 0.0;
   for (int e = threadIdx.x; e < a * a; e += blockDim.x) {
     const int i = e % a, j = e / a;
@@ -278,12 +282,13 @@ __global__ void bc_orth_error_kernel(const T* __restrict__ G, int ldg, int a, do
     if (i == j) v = bc_sub(v, bc_scale(bc_one<T>(), 1.0));
     m = fmax(m, sqrt(bc_abs2(v)));
   }
-  red[threadIdx.x] = m;
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int k = 0; k < static_cast<int>(blockDim.x); ++k) t = fmax(t, red[k]);
-    *out = t;
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) *out = m;
   }
 }
 

@@ -1082,7 +1082,7 @@ private:
       times_inverse(bc_w_.p, bc_r2_.p, Vn);
       // a-posteriori: the new block must be orthonormal to CGS2's accuracy
       const int ldg3 = gram(Vn, a, bc_g_.p);
-      bc_orth_error_kernel<T><<<1, kBcMax, 0, ctx_->stream>>>(T_(bc_g_.p), ldg3, a, bc_rnt_.p + kBcMax - 1);
+      bc_orth_error_kernel<T><<<1, kBcThreads, 0, ctx_->stream>>>(T_(bc_g_.p), ldg3, a, bc_rnt_.p + kBcMax - 1);
       launched(ctx_);
       bc_rn_kernel<<<1, kBcMax, 0, ctx_->stream>>>(bc_dec_.p, bc_diag_.p, bgs_flags_.p, bgs_rn_.p);
       launched(ctx_); dbg_sync("block_chol 6");
