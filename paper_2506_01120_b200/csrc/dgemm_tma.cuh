@@ -95,6 +95,10 @@ __device__ __forceinline__ int sw_mc(int m, int k) {
   const int line = (m >> 4) * 16 + ((k >> 1) & 1) * 8 + (k >> 2) * 2 + (k & 1);
   return line * 16 + ((((m & 15) >> 1) ^ line) & 7) * 2 + (m & 1);
 }
+// the 3-D box [m/16][k][m%16] (line (m/16)*16 + k): half-warps 2-way conflicted
+__device__ __forceinline__ int sw_mc3(int m, int k) {
+  return ((m >> 4) * 16 + k) * 16 + ((((m & 15) >> 1) ^ k) & 7) * 2 + (m & 1);
+}
 
 // Same contract as dgemm_dmma_kernel without split-K: C(m, n) = epi(sum_k
 // A(m, k) B(k, n)). mapA: A_KCONTIG -- 2-D {K, M} box {16, 128}; else 5-D
@@ -102,7 +106,7 @@ __device__ __forceinline__ int sw_mc(int m, int k) {
 // multiple of 16; rows up to 4 ceil(K/4) are read and must be zero past K).
 // mapB: 2-D {K, N} box {16, 64}. All 128-byte swizzled, out-of-bounds
 // elements read as zeros.
-template <bool A_KCONTIG, REpi EPI>
+template <bool A_KCONTIG, REpi EPI, int MC_BOX = 5>
 __global__ void __launch_bounds__(tg::THREADS, 2)
 dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                  int K, double* __restrict__ Cout, int64_t ldc, double alpha, const double* __restrict__ X,
@@ -135,7 +139,8 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     unsigned char* a = tsm + s * STAGE_BYTES;
     mbar_expect_tx(&full[s], STAGE_BYTES);
     if (A_KCONTIG) tma_load_2d(a, &mapA, kt * BK, m0, &full[s]);
-    else tma_load_5d(a, &mapA, 0, 0, kt * (BK / 4), 0, m0 / 16, &full[s]);
+    else if (MC_BOX == 5) tma_load_5d(a, &mapA, 0, 0, kt * (BK / 4), 0, m0 / 16, &full[s]);
+    else tma_load_3d(a, &mapA, 0, kt * BK, m0 / 16, &full[s]);
     tma_load_2d(a + A_BYTES, &mapB, kt * BK, n0, &full[s]);
   };
   if (tid == 0)
@@ -162,8 +167,8 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         if (A_KCONTIG) {
           a[i] = *reinterpret_cast<const double2*>(as + sw_kc(mr, kc));
         } else {
-          a[i].x = as[sw_mc(mr, kc)];
-          a[i].y = as[sw_mc(mr, kc + 1)];
+          a[i].x = as[MC_BOX == 5 ? sw_mc(mr, kc) : sw_mc3(mr, kc)];
+          a[i].y = as[MC_BOX == 5 ? sw_mc(mr, kc + 1) : sw_mc3(mr, kc + 1)];
         }
       }
 #pragma unroll
