@@ -661,9 +661,7 @@ private:
       }
       if (red_ && n > 0) red_->sum(P_.p, ldp * count, ctx_->stream);  // partial overlaps over ranks
       if (len > 0) {
-        // rows of V at and past Vb that exist (the zero tail past the basis)
-        const int64_t vrows = (Vb >= V_.p && Vb < V_.p + vcap_ * vw()) ? vcap_ - (Vb - V_.p) / vw() : -1;
-        rgemm_subtract(ctx_, Vb + off, n, len, P_.p, ldp, X + off, count, Rout + off, partial_.p, d_, D_, D_, vrows);
+        rgemm_subtract(ctx_, Vb + off, n, len, P_.p, ldp, X + off, count, Rout + off, partial_.p, d_, D_, D_);
         mtiles = static_cast<int>((len + rg::BM - 1) / rg::BM);
       }
     } else {

@@ -346,23 +346,19 @@ bool tma_map_kc(CUtensorMap* m, const double* p, int64_t len, int64_t rows, int6
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// A(m, k) = p[k*ld + m] (M-contiguous operand), M a multiple of 16, k = 4t + 2p + q:
-// 5-D {16 (m%16), 2 (q), ceil(K/4) (t), 2 (p), M/16}, box {16, 2, 4, 2, 8}
-// (dgemm_tma.cuh sw_mc). Rows K .. 4 ceil(K/4) - 1 are read as in-bounds:
-// the caller guarantees they exist and are zero (rows_zeroed).
-bool tma_map_mc(CUtensorMap* m, const double* p, int64_t M, int64_t K, int64_t ld, int64_t rows_zeroed) {
+// A(m, k) = p[k*ld + m] (M-contiguous operand), M a multiple of 16: the 3-D box
+// {16, K, M/16}, box {16, 16, 8} (dgemm_tma.cuh sw_mc3). The 5-D box (sw_mc:
+// conflict-free fragment loads) measured 0.5 % slower on the headline shape
+// (profiles/r02m_k2b_box_ab.txt), so the engine launches MC_BOX = 3.
+bool tma_map_mc(CUtensorMap* m, const double* p, int64_t M, int64_t K, int64_t ld) {
   if ((reinterpret_cast<uintptr_t>(p) & 15) || (ld & 1) || (M % 16) || M <= 0 || K <= 0) return false;
-  const int64_t kq = (K + 3) / 4;
-  if (4 * kq > rows_zeroed) return false;
-  cuuint64_t dims[5] = {16, 2, static_cast<cuuint64_t>(kq), 2, static_cast<cuuint64_t>(M / 16)};
-  cuuint64_t strides[4] = {static_cast<cuuint64_t>(ld) * 8, static_cast<cuuint64_t>(ld) * 32,
-                           static_cast<cuuint64_t>(ld) * 16, 128};
-  cuuint32_t box[5] = {16, 2, 4, 2, 8}, es[5] = {1, 1, 1, 1, 1};
-  return tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(p), dims, strides, box, es,
+  cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M / 16)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8, 128};
+  cuuint32_t box[3] = {16, 16, 8}, es[3] = {1, 1, 1};
+  return tma_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-
 // complex operands as doubles: rows x len complex, row stride ld complex: box {16 doubles, 64}
 bool tma_zmap_kc(CUtensorMap* m, const double2* p, int64_t len, int64_t rows, int64_t ld) {
   return tma_map_kc(m, reinterpret_cast<const double*>(p), 2 * len, rows, 2 * ld, 64);
@@ -520,11 +516,9 @@ void rgemm_mc_store(liecl_b200_ctx* ctx, const double* A, int64_t lda, int64_t M
 }
 
 // R = X - V[:, 0:n] P (P ld ldp); partial[mt][b] = sum_rows w R^2
-// (v_rows: rows of V that exist and are zero past n -- the TMA path reads up
-// to 4 ceil(n/4); -1 unknown: the cp.async kernel)
 void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, const double* P, int64_t ldp,
                     const double* X, int count, double* R, double* partial, int d, int64_t ldv = -1,
-                    int64_t ldx = -1, int64_t v_rows = -1) {
+                    int64_t ldx = -1) {
   if (ldv < 0) ldv = D;
   if (ldx < 0) ldx = D;  // X and R
   rgemm_attr_once<false, REpi::kSubtractNorm>();
@@ -533,12 +527,11 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
   const int64_t kpad = (n + 1) & ~int64_t(1);  // even K: reads one zero row of V past an odd n
   int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, kpad);
   CUtensorMap ma, mb;
-  if (slices <= 1 && tma_enabled() && tma_map_mc(&ma, V, D, n, ldv, v_rows) &&
-      tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
+  if (slices <= 1 && tma_enabled() && tma_map_mc(&ma, V, D, n, ldv) && tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
     // K = n exactly: rows past the basis read as zeros (TMA out-of-bounds fill)
-    func_attr_once(dgemm_tma_kernel<false, REpi::kSubtractNorm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    func_attr_once(dgemm_tma_kernel<false, REpi::kSubtractNorm, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                    tg::SMEM);
-    dgemm_tma_kernel<false, REpi::kSubtractNorm><<<grid, tg::THREADS, tg::SMEM, ctx->stream>>>(
+    dgemm_tma_kernel<false, REpi::kSubtractNorm, 3><<<grid, tg::THREADS, tg::SMEM, ctx->stream>>>(
         ma, mb, static_cast<int>(D), count, static_cast<int>(n), R, ldx, 1.0, X, ldx, partial, d);
     launched(ctx);
   } else if (slices <= 1) {

@@ -445,6 +445,7 @@ frontier_kernel(int ngens, const uint64_t* __restrict__ gx, const uint64_t* __re
           __threadfence_block();
           for (int p = static_cast<int>(mix2(x, z) & (kFirstSlots - 1));; p = (p + 1) & (kFirstSlots - 1)) {
             const int prev = atomicCAS(&s_slot[p], -1, j);
+            __threadfence_block();  // pairs with the writer's fence: s_x/s_z[prev] are visible
             if (prev == -1 || (s_x[prev] == x && s_z[prev] == z)) {
               atomicMin(&s_min[p], j);
               myslot = p;
