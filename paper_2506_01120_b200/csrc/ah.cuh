@@ -115,6 +115,24 @@ __global__ void weight_ah_kernel(const double* __restrict__ v, int64_t count, in
     vw[e] = (((e % D2) % (d + 1)) == 0 ? 1.0 : 2.0) * v[e];
 }
 
+// VT[m * ldvt + k] = V[k * D + m] for basis rows k in [k0, k1): the transposed
+// (K-contiguous) copy K2b reads through TMA (dense_engine.cuh ensure_vt).
+// 32 x 32 tiles through shared memory, both sides coalesced.
+__global__ void transpose_rows_kernel(const double* __restrict__ V, int64_t D, int64_t k0, int64_t k1,
+                                      double* __restrict__ VT, int64_t ldvt) {
+  __shared__ double tile[32][33];
+  const int64_t kb = k0 + static_cast<int64_t>(blockIdx.y) * 32, mb = static_cast<int64_t>(blockIdx.x) * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t k = kb + r, m = mb + threadIdx.x;
+    tile[r][threadIdx.x] = (k < k1 && m < D) ? V[k * D + m] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t m = mb + r, k = kb + threadIdx.x;
+    if (m < D && k < k1) VT[m * ldvt + k] = tile[threadIdx.x][r];
+  }
+}
+
 // Warp layout of one pair's product P = A B (TR x TR tiles of 8 x 8): a warp
 // owns WR x WC tiles (WR row tiles sharing A fragments, WC column tiles
 // sharing B fragments). d < 64: one row of tiles per warp, several pairs per

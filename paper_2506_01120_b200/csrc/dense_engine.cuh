@@ -126,6 +126,7 @@ public:
     record_ = cfg.record_log != 0;
     set_deadline(cfg);
     n_o_ = n_b_ = 0;
+    n_vt_ = 0;
     field_ = Field::kUnset;
     B_cur_ = std::min<int64_t>(bmax_, 512);
     reset_stats();
@@ -225,6 +226,7 @@ public:
       CU(cudaMemcpyAsync(tmp_o, orig, static_cast<size_t>(n_orig * D_) * sizeof(double2), kind, ctx_->stream));
     const Field f = classify(tmp, n + (orig ? n_orig : 0));
     n_o_ = n_b_ = 0;
+    n_vt_ = 0;          // the transposed copy belongs to the old basis
     complete_n_ = -1;  // the completeness certificate belongs to the old basis
     field_ = f;
     layout_slabs();
@@ -636,6 +638,31 @@ private:
     vcap_ = nc;
   }
 
+  // Transposed packed basis for K2b's TMA path: VT_[m * ldvt_ + k] = V_[k][m]
+  // for k < n_vt_, extended by the rows appended since (basis rows are only
+  // ever appended between resets). Only for unsplit grids (the path that reads
+  // it) and within a memory budget.
+  bool ensure_vt(int64_t n, int count) {
+    if (field_ != Field::kAntiHerm || red_ || n == 0 || !tma_enabled()) return false;
+    const int64_t tiles = ((D_ + rg::BM - 1) / rg::BM) * ((count + rg::BN - 1) / rg::BN);
+    if (split_slices(tiles, (n + 1) & ~int64_t(1)) > 1) return false;  // split-K: cp.async, no reader
+    const int64_t ld = (vcap_ + 1) & ~int64_t(1);
+    if (static_cast<double>(D_) * ld * 8.0 > 4e9) return false;
+    if (ld > ldvt_ || !VT_.p) {
+      VT_.release();
+      VT_.ensure(static_cast<size_t>(D_ * ld));
+      ldvt_ = ld;
+      n_vt_ = 0;
+    }
+    if (n > n_vt_) {
+      const dim3 grid(static_cast<unsigned>((D_ + 31) / 32), static_cast<unsigned>((n - n_vt_ + 31) / 32));
+      transpose_rows_kernel<<<grid, dim3(32, 8), 0, ctx_->stream>>>(V_.p, D_, n_vt_, n, VT_.p, ldvt_);
+      launched(ctx_);
+      n_vt_ = n;
+    }
+    return true;
+  }
+
   // One CGS pass of `count` columns X against basis columns Vb[0:n] (weighted
   // copy Vwb on the packed path): Rout = X - Vb beta, beta = <Vb, X>,
   // rn = ||Rout|| (Rout may alias X).
@@ -661,7 +688,9 @@ private:
       }
       if (red_ && n > 0) red_->sum(P_.p, ldp * count, ctx_->stream);  // partial overlaps over ranks
       if (len > 0) {
-        rgemm_subtract(ctx_, Vb + off, n, len, P_.p, ldp, X + off, count, Rout + off, partial_.p, d_, D_, D_);
+        const bool vt = Vb == V_.p && off == 0 && ensure_vt(n, count);
+        rgemm_subtract(ctx_, Vb + off, n, len, P_.p, ldp, X + off, count, Rout + off, partial_.p, d_, D_, D_,
+                       vt ? VT_.p : nullptr, ldvt_);
         mtiles = static_cast<int>((len + rg::BM - 1) / rg::BM);
       }
     } else {
@@ -1248,6 +1277,8 @@ private:
   std::vector<Warning> warns_;
   std::vector<liecl_b200_decision> log_;
   DevBuf<double> V_, Vw_, O_, C_, R_, X_, Y_, P_;  // element width ew() doubles
+  DevBuf<double> VT_;                               // transposed packed basis (ensure_vt)
+  int64_t ldvt_ = 0, n_vt_ = 0;
   DevBuf<double2> stage_;                          // complex input staging
   DevBuf<double2> basis_stage_;                    // set_basis staging (kept across calls)
   bool block_chol_ = [] {  // LIECL_B200_BLOCK_CHOL=0: the per-survivor block kernel (diagnostics)

@@ -516,9 +516,12 @@ void rgemm_mc_store(liecl_b200_ctx* ctx, const double* A, int64_t lda, int64_t M
 }
 
 // R = X - V[:, 0:n] P (P ld ldp); partial[mt][b] = sum_rows w R^2
+// (VT: optional transposed basis, VT[m * ldvt + k] = V[k * ldv + m] for k < n:
+// K2b then reads a K-contiguous operand like K2a -- conflict-free 128-bit
+// fragment loads through the 2-D TMA box)
 void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, const double* P, int64_t ldp,
                     const double* X, int count, double* R, double* partial, int d, int64_t ldv = -1,
-                    int64_t ldx = -1) {
+                    int64_t ldx = -1, const double* VT = nullptr, int64_t ldvt = 0) {
   if (ldv < 0) ldv = D;
   if (ldx < 0) ldx = D;  // X and R
   rgemm_attr_once<false, REpi::kSubtractNorm>();
@@ -527,7 +530,15 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
   const int64_t kpad = (n + 1) & ~int64_t(1);  // even K: reads one zero row of V past an odd n
   int slices = split_slices(static_cast<int64_t>(grid.x) * grid.y, kpad);
   CUtensorMap ma, mb;
-  if (slices <= 1 && tma_enabled() && tma_map_mc(&ma, V, D, n, ldv) && tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
+  if (slices <= 1 && VT && tma_enabled() && tma_map_kc(&ma, VT, n, D, ldvt, tg::BM) &&
+      tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
+    func_attr_once(dgemm_tma_kernel<true, REpi::kSubtractNorm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                   tg::SMEM);
+    dgemm_tma_kernel<true, REpi::kSubtractNorm><<<grid, tg::THREADS, tg::SMEM, ctx->stream>>>(
+        ma, mb, static_cast<int>(D), count, static_cast<int>(n), R, ldx, 1.0, X, ldx, partial, d);
+    launched(ctx);
+  } else if (slices <= 1 && tma_enabled() && tma_map_mc(&ma, V, D, n, ldv) &&
+             tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
     // K = n exactly: rows past the basis read as zeros (TMA out-of-bounds fill)
     func_attr_once(dgemm_tma_kernel<false, REpi::kSubtractNorm, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                    tg::SMEM);
