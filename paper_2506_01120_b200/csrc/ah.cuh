@@ -142,8 +142,10 @@ template <int DIM, int WR_ = (DIM == 64 ? 2 : 1), int WC_ = (DIM == 64 ? 4 : DIM
   static constexpr int TR = DIM / 8;                 // tile rows (and columns)
   static constexpr int WR = WR_, WC = WC_;
   static constexpr int WARPS_PER_PAIR = (TR / WR) * (TR / WC);
-  static_assert(WARPS_PER_PAIR <= 8 && 8 % WARPS_PER_PAIR == 0, "warp layout");
-  static constexpr int PAIRS_PER_CTA = 8 / WARPS_PER_PAIR;
+  static constexpr int CTA_WARPS = WARPS_PER_PAIR > 8 ? WARPS_PER_PAIR : 8;  // 256 threads, or one pair
+  static constexpr int THREADS = 32 * CTA_WARPS;
+  static_assert(CTA_WARPS % WARPS_PER_PAIR == 0, "warp layout");
+  static constexpr int PAIRS_PER_CTA = CTA_WARPS / WARPS_PER_PAIR;
   static constexpr int LDP = DIM + 4;                // == 4 (mod 16): conflict-free fragment gathers
   static constexpr int PACKED = DIM * LDP;
   static constexpr int SMEM_PER_PAIR = (2 * PACKED * 8 + WARPS_PER_PAIR * 8 + 15) / 16 * 16;  // 16-byte slots
@@ -176,7 +178,7 @@ __device__ __forceinline__ void ah_elem(const double* p, int i, int k, double& r
 // row tiles); P is written back over the consumed inputs and h = P - P^dagger
 // is read out in the packed layout. ~70 KB per pair at d = 64.
 template <int DIM, int MINB = 2, int WR = CommAhShape<DIM>::WR, int WC = CommAhShape<DIM>::WC, bool ASYNC = true>
-__global__ void __launch_bounds__(256, MINB)
+__global__ void __launch_bounds__(CommAhShape<DIM, WR, WC>::THREADS, MINB)
 commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, double tol, bool normalize,
                      double* __restrict__ out, double* __restrict__ hnorm, int* __restrict__ is_null) {
   using S = CommAhShape<DIM, WR, WC>;

@@ -775,7 +775,7 @@ private:
     func_attr_once(commutator_ah_kernel<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     const int blocks = (cnt + SA::PAIRS_PER_CTA - 1) / SA::PAIRS_PER_CTA;
     Timer t(ctx_, 2, 8.0 * DIM * DIM * static_cast<double>(DIM) * cnt);
-    commutator_ah_kernel<DIM><<<blocks, 256, SA::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, C_.p, hn_.p,
+    commutator_ah_kernel<DIM><<<blocks, SA::THREADS, SA::SMEM, ctx_->stream>>>(basis, g0, cnt, tol_, true, C_.p, hn_.p,
                                                                         nul_.p);
     launched(ctx_);
     t.stop();

@@ -53,3 +53,28 @@ def test_tma_and_cpasync_gemms_agree(monkeypatch, n, field):
     assert np.abs(rn1[acc] - rn0[acc]).max(initial=0.0) < 1e-10
     assert np.abs(rn1[~acc] - rn0[~acc]).max(initial=0.0) < 1e-12
     assert rn1[~acc].max(initial=0.0) < 1e-11
+
+
+def test_transposed_basis_follows_appends_and_replacements(monkeypatch):
+    """K2b reads VT, a transposed copy of the packed basis extended by the rows
+    appended since its last use and discarded when the basis is replaced:
+    batches after appends and after set_basis must equal the cp.async path."""
+    V = su16_basis()
+    rng = np.random.default_rng(3)
+    b1 = np.concatenate([antiherm(rng, 8, 16), (rng.standard_normal((8184, 200)) @ V[:200])])
+    b2 = antiherm(rng, 8192, 16)
+    b3 = np.concatenate([antiherm(rng, 4, 16), (rng.standard_normal((8188, 120)) @ V[100:220])])
+
+    def go(tma):
+        monkeypatch.setenv("LIECL_B200_TMA", tma)
+        s = liecl.ClosureSession(16, config=liecl.ClosureConfig(tolerance=1e-10))
+        out = []
+        s.set_basis(V[:200])
+        out.append(s.check_candidates(b1)[:2])  # 8 accepts: rows 200..207 appended
+        out.append(s.check_candidates(b2)[:2])  # VT extended by those rows first
+        s.set_basis(V[100:220])                 # replaced: VT rebuilt, not reused
+        out.append(s.check_candidates(b3)[:2])
+        return out
+    for (i1, r1), (i0, r0) in zip(go("1"), go("0")):
+        assert np.array_equal(i1, i0)
+        assert np.abs(r1 - r0).max() < 1e-10

@@ -26,7 +26,7 @@ double run(const char* name, const double* basis, int64_t g0, double* out, doubl
   cudaFuncAttributes fa;
   CK(cudaFuncGetAttributes(&fa, k));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, S::SMEM));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, S::THREADS, S::SMEM));
   const int blocks = (CNT + S::PAIRS_PER_CTA - 1) / S::PAIRS_PER_CTA;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -34,7 +34,7 @@ double run(const char* name, const double* basis, int64_t g0, double* out, doubl
   float best = 1e30f;
   for (int it = 0; it < 12; ++it) {
     cudaEventRecord(e0);
-    k<<<blocks, 256, S::SMEM>>>(basis, g0, CNT, 1e-10, true, out, hn, nul);
+    k<<<blocks, S::THREADS, S::SMEM>>>(basis, g0, CNT, 1e-10, true, out, hn, nul);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -80,5 +80,8 @@ int main() {
   run<2, 4, 2>("4x2_minb2", basis, g0, out, hn, nul, o, h); same("4x2_minb2");
   run<1, 2, 4>("2x4_minb1", basis, g0, out, hn, nul, o, h); same("2x4_minb1");
   run<2, 8, 1>("8x1_minb2", basis, g0, out, hn, nul, o, h); same("8x1_minb2");
+  run<2, 1, 4>("1x4_16warps_minb2", basis, g0, out, hn, nul, o, h); same("1x4_16warps_minb2");
+  run<2, 2, 2>("2x2_16warps_minb2", basis, g0, out, hn, nul, o, h); same("2x2_16warps_minb2");
+  run<3, 2, 2>("2x2_16warps_minb3", basis, g0, out, hn, nul, o, h); same("2x2_16warps_minb3");
   return 0;
 }
