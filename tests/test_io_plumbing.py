@@ -127,3 +127,23 @@ def test_realize_generators_matches_reference(ref_exact, family, n):
         sub = liecl.realize_generators(family, n, restrict_zero_magnetization=True)
         want, m = ref_exact.realize_generators_dense(family, n, restrict=True)
         assert m == 6 and all(np.array_equal(a.vec(), b) for a, b in zip(sub, want))
+
+
+def test_pauli_single_list_is_a_lazy_sequence():
+    """result.basis of a single-string closure (liecl.PauliSingleList): built on
+    access from the (x, z, coef) arrays, equal to the eager list of sums."""
+    import numpy as np
+    x = np.array([1, 2, 3], np.uint64)
+    z = np.array([0, 2, 1], np.uint64)
+    c = np.array([[0.0, 1.0], [0.5, -0.5], [-1.0, 0.0]])
+    lst = liecl.PauliSingleList(x, z, c, 2)
+    eager = [liecl.PauliSum.single(liecl.PauliString(int(x[i]), int(z[i]), 2), complex(c[i, 0], c[i, 1]))
+             for i in range(3)]
+    assert len(lst) == 3 and lst == eager and list(lst) == eager
+    assert lst[-1] == eager[-1] and lst[0:2] == eager[0:2]
+    assert liecl.format_pauli_sum(lst[1]) == liecl.format_pauli_sum(eager[1])
+    try:
+        lst[3]
+        raise AssertionError("index past the end must raise")
+    except IndexError:
+        pass
