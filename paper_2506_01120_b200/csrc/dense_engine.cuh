@@ -45,6 +45,14 @@ public:
       cudaStreamDestroy(copy_stream_);
       cudaEventDestroy(prefetch_done_);
     }
+    if (comm_stream_) {
+      cudaStreamSynchronize(comm_stream_);
+      cudaStreamDestroy(comm_stream_);
+      for (int c = 0; c < kMaxShardChunks; ++c) {
+        cudaEventDestroy(ev_gemm_[c]);
+        cudaEventDestroy(ev_red_[c]);
+      }
+    }
     for (auto& sl : cslot_) {
       if (sl.ready) cudaEventDestroy(sl.ready);
       if (sl.free) cudaEventDestroy(sl.free);
@@ -663,6 +671,55 @@ private:
     return true;
   }
 
+  // D-sharded packed pass over a large batch: the candidates in `nch` chunks;
+  // chunk c's partial overlaps are all-reduced on comm_stream_ as soon as its
+  // K2a lands, while the engine stream runs K2a of the next chunks, and K2b of
+  // chunk c waits only for its own reduction -- the NVLink transfer overlaps
+  // the GEMMs (one collective at a time on the communicator: the engine
+  // stream's later reductions wait for the last chunk). Same arithmetic per
+  // candidate as one unchunked pass.
+  static constexpr int kMaxShardChunks = 4;
+  int shard_chunks(int64_t n, int count, int64_t len, const int* before) const {
+    if (!red_ || !loop_shard_ || n == 0 || len == 0 || before) return 1;
+    const char* e = std::getenv("LIECL_B200_SHARD_CHUNKS");
+    const int want = e ? std::max(1, std::atoi(e)) : kMaxShardChunks;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, kMaxShardChunks, count / 2048})));
+  }
+  void project_pipelined(const double* Vb, const double* Vwb, int64_t n, const double* X, int count, double* Rout,
+                         double* rn, int64_t off, int64_t len, int64_t ldp, int nch) {
+    if (!comm_stream_) {
+      CU(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
+      for (int c = 0; c < kMaxShardChunks; ++c) {
+        CU(cudaEventCreateWithFlags(&ev_gemm_[c], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ev_red_[c], cudaEventDisableTiming));
+      }
+    }
+    const int cs = ((count + nch - 1) / nch + 63) / 64 * 64;
+    const int mt = static_cast<int>((len + rg::BM - 1) / rg::BM);
+    int c = 0;
+    for (int c0 = 0; c0 < count; c0 += cs, ++c) {
+      const int cc = std::min(cs, count - c0);
+      rgemm_project(ctx_, Vwb + off, n, len, X + off + static_cast<int64_t>(c0) * D_, cc, P_.p + c0 * ldp, ldp,
+                    1.0 / d_, D_, D_);
+      CU(cudaEventRecord(ev_gemm_[c], ctx_->stream));
+      CU(cudaStreamWaitEvent(comm_stream_, ev_gemm_[c], 0));
+      red_->sum(P_.p + c0 * ldp, ldp * cc, comm_stream_);  // partial overlaps of chunk c over ranks
+      CU(cudaEventRecord(ev_red_[c], comm_stream_));
+    }
+    c = 0;
+    for (int c0 = 0; c0 < count; c0 += cs, ++c) {
+      const int cc = std::min(cs, count - c0);
+      CU(cudaStreamWaitEvent(ctx_->stream, ev_red_[c], 0));
+      rgemm_subtract(ctx_, Vb + off, n, len, P_.p + c0 * ldp, ldp, X + off + static_cast<int64_t>(c0) * D_, cc,
+                     Rout + off + static_cast<int64_t>(c0) * D_, partial_.p + static_cast<int64_t>(c0) * mt, d_, D_,
+                     D_);
+      norm_finalize_kernel<<<(cc + 255) / 256, 256, 0, ctx_->stream>>>(partial_.p + static_cast<int64_t>(c0) * mt,
+                                                                        mt, cc, 0.0, rn + c0);
+      launched(ctx_);
+    }
+    sharded_norms(rn, count);
+  }
+
   // One CGS pass of `count` columns X against basis columns Vb[0:n] (weighted
   // copy Vwb on the packed path): Rout = X - Vb beta, beta = <Vb, X>,
   // rn = ||Rout|| (Rout may alias X).
@@ -676,6 +733,11 @@ private:
     const int64_t len = loop_shard_ ? hi_ - lo_ : D_;
     if (field_ == Field::kAntiHerm) {
       const int64_t ldp = (n + 1) & ~int64_t(1);  // even: 16-byte aligned P columns
+      const int nch = shard_chunks(n, count, len, before);
+      if (nch > 1) {
+        project_pipelined(Vb, Vwb, n, X, count, Rout, rn, off, len, ldp, nch);
+        return;
+      }
       if (len > 0) {
         rgemm_project(ctx_, Vwb + off, n, len, X + off, count, P_.p, ldp, 1.0 / d_, D_, D_);
       } else if (n > 0) {
@@ -1278,6 +1340,8 @@ private:
   std::vector<liecl_b200_decision> log_;
   DevBuf<double> V_, Vw_, O_, C_, R_, X_, Y_, P_;  // element width ew() doubles
   DevBuf<double> VT_;                               // transposed packed basis (ensure_vt)
+  cudaStream_t comm_stream_ = nullptr;              // chunked shard reductions (project_pipelined)
+  cudaEvent_t ev_gemm_[kMaxShardChunks] = {}, ev_red_[kMaxShardChunks] = {};
   int64_t ldvt_ = 0, n_vt_ = 0;
   DevBuf<double2> stage_;                          // complex input staging
   DevBuf<double2> basis_stage_;                    // set_basis staging (kept across calls)

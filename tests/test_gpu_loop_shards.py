@@ -180,3 +180,31 @@ def test_two_processes_over_gloo_match_golden(golden):
         assert comms == meta["stats"]["commutators_evaluated"] and checks == meta["stats"]["independence_checks"]
         assert indep == g["log_indep"].tolist()
     assert res[0][5] == res[1][5]  # bit-identical replicas
+
+
+@pytest.mark.parametrize("chunks", ["1", "4"])
+def test_sharded_saturated_window_chunked_reductions(chunks, monkeypatch):
+    """A saturated-window batch of 8,192 pairs on P = 2 thread ranks: with
+    LIECL_B200_SHARD_CHUNKS = 4 the partial overlaps are reduced chunk by chunk
+    on a side stream while the next chunks' GEMMs run; verdicts and norms equal
+    the unsharded session's (and the unchunked sharded run's)."""
+    from bench import random_saturated_basis
+    monkeypatch.setenv("LIECL_B200_SHARD_CHUNKS", chunks)
+    V = random_saturated_basis(64, 0)
+    d = 64
+    rows = (1024, 1032)  # ~8,200 pairs: full 8,192-pair batches
+
+    def job(s):
+        s.set_basis(V)
+        st = s.run_rows(*rows)
+        return st, s.log()
+    out, sums = run_threads(2, d, job)
+    solo = liecl.ClosureSession(d, config=liecl.ClosureConfig(tolerance=1e-10, record_log=True))
+    solo.set_basis(V)
+    st0 = solo.run_rows(*rows)
+    log0 = solo.log()
+    for st, log in out:
+        assert st["accepted"] == st0["accepted"] == 0
+        assert np.array_equal(log["independent"], log0["independent"])
+        assert np.abs(log["residual_norm"] - log0["residual_norm"]).max() < 1e-12
+    assert sums.calls[0] == sums.calls[1]
