@@ -269,6 +269,36 @@ __global__ void __launch_bounds__(kBcThreads) bc_tri_inverse_kernel(const T* __r
   }
 }
 
+// out = A R^-1 for the real (packed) field, one thread per row i of A: row i
+// (A[q * lda + i], q < a) solved against the upper-triangular R (ld kBcMax) by
+// forward substitution, w_j = (y_j - sum_{k<j} w_k R_kj) / R_jj, w in
+// registers (the loops unroll to the block's 64 columns; R in shared memory,
+// read as broadcasts). Replaces "R^-1 in one CTA, then a GEMM" in CholQR2:
+// one launch, no 64-step sequential inverse.
+__global__ void __launch_bounds__(128) bc_trsm_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
+                                                           const double* __restrict__ R, int a,
+                                                           double* __restrict__ out, int64_t ldo) {
+  __shared__ double Rs[kBcMax * kBcMax];
+  __shared__ double rinv[kBcMax];
+  for (int e = threadIdx.x; e < a * a; e += blockDim.x) Rs[(e % a) + (e / a) * kBcMax] = R[(e % a) + (e / a) * kBcMax];
+  __syncthreads();
+  if (threadIdx.x < a) rinv[threadIdx.x] = 1.0 / Rs[threadIdx.x + threadIdx.x * kBcMax];
+  __syncthreads();
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= M) return;
+  double w[kBcMax];
+#pragma unroll
+  for (int j = 0; j < kBcMax; ++j) {
+    if (j < a) {
+      double acc = A[j * lda + i];
+#pragma unroll
+      for (int k = 0; k < j; ++k) acc -= w[k] * Rs[k + j * kBcMax];
+      w[j] = acc * rinv[j];
+      out[j * ldo + i] = w[j];
+    }
+  }
+}
+
 // max |(Q^H Q)_ij - delta_ij| of the new block (G ld ldg, a x a): the
 // a-posteriori orthogonality check of CholQR2 (the caller falls back to the
 // exact per-survivor kernel above a bound)

@@ -678,12 +678,17 @@ private:
   // the GEMMs (one collective at a time on the communicator: the engine
   // stream's later reductions wait for the last chunk). Same arithmetic per
   // candidate as one unchunked pass.
+  // Two chunks of >= 4,096 candidates by default, only when there is a
+  // transfer to hide (nranks > 1): a 2,048-candidate K2a grid is 1,024 CTAs,
+  // 3.5 waves on 296 slots (measured 13 % slower at one rank), a 4,096 one
+  // 6.9 waves. LIECL_B200_SHARD_CHUNKS forces a count (tests: one rank too).
   static constexpr int kMaxShardChunks = 4;
   int shard_chunks(int64_t n, int count, int64_t len, const int* before) const {
     if (!red_ || !loop_shard_ || n == 0 || len == 0 || before) return 1;
     const char* e = std::getenv("LIECL_B200_SHARD_CHUNKS");
-    const int want = e ? std::max(1, std::atoi(e)) : kMaxShardChunks;
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, kMaxShardChunks, count / 2048})));
+    if (e) return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({std::atoi(e), kMaxShardChunks, count / 2048})));
+    if (nranks_ < 2) return 1;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(2, count / 4096)));
   }
   void project_pipelined(const double* Vb, const double* Vwb, int64_t n, const double* X, int count, double* Rout,
                          double* rn, int64_t off, int64_t len, int64_t ldp, int nch) {
@@ -1152,6 +1157,13 @@ private:
         if (a_even > a) CU(cudaMemsetAsync(bc_ya_.p + a * W, 0, W * sizeof(double), ctx_->stream));
       }
       auto times_inverse = [&](const double* A, const double* R, double* out) {
+        if (packed) {  // real field: one row-wise forward substitution (bc_trsm_rows_kernel)
+          if (len == 0) return;
+          bc_trsm_rows_kernel<<<static_cast<unsigned>((len + 127) / 128), 128, 0, ctx_->stream>>>(
+              A + lo, D_, len, R, a, out + lo, D_);
+          launched(ctx_); dbg_sync("block_chol trsm");
+          return;
+        }
         bc_tri_inverse_kernel<T><<<1, kBcThreads, bc_smem_bytes<T>(), ctx_->stream>>>(T_(const_cast<double*>(R)), a,
                                                                                    T_(bc_tinv_.p));
         launched(ctx_); dbg_sync("block_chol inverse");
