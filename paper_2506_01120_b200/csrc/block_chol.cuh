@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
   T* Gs = Zs + kBcMax * kBcMax;
   __shared__ double s[kBcMax];
   __shared__ double s_rn2[kBcMax];  // rn2 staged: thread 0's serial decisions read shared memory only
+  __shared__ double g0[kBcMax];
   __shared__ int acc_list[kBcMax];
   __shared__ int s_ind, s_stop;
   const int tid = threadIdx.x;
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
   __syncthreads();
   if (sub == 0 && t < nb) {
     s[t] = bc_re(Gs[t + t * kBcMax]);
+    g0[t] = s[t];  // original diagonal (Gs becomes the Schur complement)
     s_rn2[t] = rn2[t];
   }
   int acc = 0, tent = 0;
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
       if (!recheck) {
         ind = r2 > tol ? 1 : 0;
       } else {
-        const double gqq = bc_re(Gs[q + q * kBcMax]);
+        const double gqq = g0[q];
         const double sq = s[q];
         // certified: the residual keeps >= 10% of the survivor's norm (so the
         // accepted set stays well conditioned, cond <= ~100 per step, and
@@ -149,23 +151,27 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
     __syncthreads();
     if (s_stop) break;
     if (s_ind) {
-      // row `acc` of Z: the new accept's R entries against every later column
+      // Right-looking: Gs holds the Schur complement of the accepts so far
+      // (rows / columns > q still live). Row `acc` of Z is z_t = Gs(q, t) / l,
+      // l = sqrt(Gs(q, q)); then the trailing block loses conj(z_u) z_v --
+      // every thread updates its own elements, no dot-product chains.
       const double lqq = sqrt(s[q]);  // == rn2_q for the block's first accept
+      const double il = 1.0 / lqq;
       if (tid == 0) acc_list[acc] = q;
-      if (t > q && t < nb) {  // whole 4-lane groups: the shuffles stay inside active lanes
-        T part = bc_zero<T>();
-        for (int a = sub; a < acc; a += kBcLanes) part = bc_sub(part, bc_mul(bc_conj(Zs[a * kBcMax + q]), Zs[a * kBcMax + t]));
-        part = bc_group_sum(part);
-        if (sub == 0) {
-          const T z = bc_scale(bc_sub(Gs[q + t * kBcMax], bc_scale(part, -1.0)), 1.0 / lqq);
-          Zs[acc * kBcMax + t] = z;
-          s[t] -= bc_abs2(z);
-        }
-      }
-      if (tid == 0) {  // the diagonal (real, positive); no thread reads row `acc` in this phase
+      for (int v = q + 1 + tid; v < nb; v += blockDim.x) Zs[acc * kBcMax + v] = bc_scale(Gs[q + v * kBcMax], il);
+      if (tid == 0) {  // the diagonal (real, positive)
         if constexpr (sizeof(T) == sizeof(double)) Zs[acc * kBcMax + q] = lqq;
         else Zs[acc * kBcMax + q] = T{lqq, 0.0};
       }
+      const int m = nb - q - 1;  // trailing block (u, v) in (q, nb)^2, upper triangle u <= v
+      for (int e = tid; e < m * m; e += blockDim.x) {
+        const int u = q + 1 + e % m, v = q + 1 + e / m;
+        if (u > v) continue;
+        const T zu = bc_scale(Gs[q + u * kBcMax], il), zv = bc_scale(Gs[q + v * kBcMax], il);
+        Gs[u + v * kBcMax] = bc_sub(Gs[u + v * kBcMax], bc_mul(bc_conj(zu), zv));
+      }
+      __syncthreads();
+      if (tid > q && tid < nb) s[tid] = bc_re(Gs[tid + tid * kBcMax]);
       ++acc;
       __syncthreads();
     }
@@ -184,36 +190,37 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
 }
 
 // Cholesky G = R^H R (upper R, ld kBcMax) of an a x a Hermitian matrix
-// (a <= 64), one CTA; diag[a] receives R_aa.
+// (a <= 64), one CTA; diag[a] receives R_aa. Right-looking: step i reads row i
+// of the current Schur complement (every thread recomputes R_ii), writes R's
+// row i and takes conj(R_iu) R_iv off the trailing upper triangle -- one
+// barrier per step, every thread's work independent.
 template <class T>
 __global__ void __launch_bounds__(kBcThreads) bc_cholesky_kernel(const T* __restrict__ G, int ldg, int a,
                                                                   T* __restrict__ R, double* __restrict__ diag) {
   extern __shared__ __align__(16) unsigned char bc_smem[];
   T* Rs = reinterpret_cast<T*>(bc_smem);  // R(i, j) = Rs[i * kBcMax + j]: kBcMax^2 T (dynamic), flat (see above)
-  T* Gs = Rs + kBcMax * kBcMax;            // G staged in shared memory
+  T* Gs = Rs + kBcMax * kBcMax;            // G staged in shared memory, then its Schur complements
   const int tid = threadIdx.x;
-  const int t = tid >> 2, sub = tid & 3;
   for (int e = tid; e < a * a; e += blockDim.x) Gs[(e % a) + (e / a) * kBcMax] = G[(e % a) + static_cast<int64_t>(e / a) * ldg];
   __syncthreads();
   for (int i = 0; i < a; ++i) {
-    if (t == i) {  // one 4-lane group: the diagonal
-      double part = 0.0;
-      for (int k = sub; k < i; k += kBcLanes) part += bc_abs2(Rs[k * kBcMax + i]);
-      part = bc_group_sum(part);
-      if (sub == 0) {
-        const double r = sqrt(fmax(bc_re(Gs[i + i * kBcMax]) - part, 0.0));
+    const double r = sqrt(fmax(bc_re(Gs[i + i * kBcMax]), 0.0));
+    const double ir = 1.0 / r;
+    for (int j = i + tid; j < a; j += blockDim.x) {
+      if (j == i) {
         if constexpr (sizeof(T) == sizeof(double)) Rs[i * kBcMax + i] = r;
         else Rs[i * kBcMax + i] = T{r, 0.0};
         diag[i] = r;
+      } else {
+        Rs[i * kBcMax + j] = bc_scale(Gs[i + j * kBcMax], ir);
       }
     }
-    __syncthreads();
-    if (t > i && t < a) {
-      T part = bc_zero<T>();
-      for (int k = sub; k < i; k += kBcLanes) part = bc_sub(part, bc_mul(bc_conj(Rs[k * kBcMax + i]), Rs[k * kBcMax + t]));
-      part = bc_group_sum(part);
-      if (sub == 0)
-        Rs[i * kBcMax + t] = bc_scale(bc_sub(Gs[i + t * kBcMax], bc_scale(part, -1.0)), 1.0 / bc_re(Rs[i * kBcMax + i]));
+    const int m = a - i - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int u = i + 1 + e % m, v = i + 1 + e / m;
+      if (u > v) continue;
+      const T ru = bc_scale(Gs[i + u * kBcMax], ir), rv = bc_scale(Gs[i + v * kBcMax], ir);
+      Gs[u + v * kBcMax] = bc_sub(Gs[u + v * kBcMax], bc_mul(bc_conj(ru), rv));
     }
     __syncthreads();
   }
@@ -235,67 +242,40 @@ __global__ void bc_mask_kernel(double* __restrict__ P, int64_t ldp, int rows, in
   }
 }
 
-// T = R^-1 for an a x a upper-triangular R (ld kBcMax), one CTA: thread j
-// back-substitutes column j. Rows a .. 2*ceil(a/2)-1 of T are zero (the real
-// GEMM reads an even K).
+// T = R^-1 for an a x a upper-triangular R (ld kBcMax), one CTA, right-looking
+// from the bottom row: B starts as I; step i (a-1 down to 0) fixes row i,
+// T(i, j) = B(i, j) / R_ii, and takes R(u, i) T(i, j) off every row u < i --
+// one barrier per step, every thread's updates independent (no dot-product
+// chains). Rows a .. 2*ceil(a/2)-1 of T are zero (the real GEMM reads an even K).
 template <class T>
 __global__ void __launch_bounds__(kBcThreads) bc_tri_inverse_kernel(const T* __restrict__ R, int a, T* __restrict__ Tinv) {
   extern __shared__ __align__(16) unsigned char bc_smem[];
   T* Rs = reinterpret_cast<T*>(bc_smem);  // R(i, j) = Rs[i + j * kBcMax]
-  T* Ts = Rs + kBcMax * kBcMax;           // T(i, j) = Ts[i + j * kBcMax]
+  T* Bs = Rs + kBcMax * kBcMax;           // B(i, j) = Bs[i + j * kBcMax]; T written back in place per row
   const int tid = threadIdx.x;
-  const int j = tid >> 2, sub = tid & 3;  // column j back-substituted by one 4-lane group
-  for (int e = tid; e < a * a; e += blockDim.x) Rs[(e % a) + (e / a) * kBcMax] = R[(e % a) + (e / a) * kBcMax];
+  for (int e = tid; e < a * a; e += blockDim.x) {
+    const int i = e % a, j = e / a;
+    Rs[i + j * kBcMax] = R[i + j * kBcMax];
+    Bs[i + j * kBcMax] = i == j ? bc_one<T>() : bc_zero<T>();
+  }
   __syncthreads();
-  if (j < a) {
-    if (sub == 0) {
-      if constexpr (sizeof(T) == sizeof(double)) Ts[j + j * kBcMax] = 1.0 / bc_re(Rs[j + j * kBcMax]);
-      else Ts[j + j * kBcMax] = T{1.0 / bc_re(Rs[j + j * kBcMax]), 0.0};
+  for (int i = a - 1; i >= 0; --i) {
+    const double ir = 1.0 / bc_re(Rs[i + i * kBcMax]);
+    // rows u < i, columns j >= i: B(u, j) -= R(u, i) B(i, j) / R_ii (row i is final)
+    const int w = a - i;
+    for (int e = tid; e < i * w; e += blockDim.x) {
+      const int u = e % i, j = i + e / i;
+      Bs[u + j * kBcMax] = bc_sub(Bs[u + j * kBcMax], bc_mul(Rs[u + i * kBcMax], bc_scale(Bs[i + j * kBcMax], ir)));
     }
-    __syncwarp(bc_group_mask());
-    for (int i = j - 1; i >= 0; --i) {
-      T part = bc_zero<T>();
-      for (int k = i + 1 + sub; k <= j; k += kBcLanes) part = bc_sub(part, bc_mul(Rs[i + k * kBcMax], Ts[k + j * kBcMax]));
-      part = bc_group_sum(part);
-      if (sub == 0) Ts[i + j * kBcMax] = bc_scale(part, 1.0 / bc_re(Rs[i + i * kBcMax]));
-      __syncwarp(bc_group_mask());
-    }
+    __syncthreads();
+    for (int j = i + tid; j < a; j += blockDim.x) Bs[i + j * kBcMax] = bc_scale(Bs[i + j * kBcMax], ir);
+    // (row i is read again only by steps < i, after the next barrier)
   }
   __syncthreads();
   const int rows = (a + 1) & ~1;
   for (int e = threadIdx.x; e < rows * a; e += blockDim.x) {
     const int i = e % rows, c = e / rows;
-    Tinv[i + c * kBcMax] = (i <= c && i < a) ? Ts[i + c * kBcMax] : bc_zero<T>();
-  }
-}
-
-// out = A R^-1 for the real (packed) field, one thread per row i of A: row i
-// (A[q * lda + i], q < a) solved against the upper-triangular R (ld kBcMax) by
-// forward substitution, w_j = (y_j - sum_{k<j} w_k R_kj) / R_jj, w in
-// registers (the loops unroll to the block's 64 columns; R in shared memory,
-// read as broadcasts). Replaces "R^-1 in one CTA, then a GEMM" in CholQR2:
-// one launch, no 64-step sequential inverse.
-__global__ void __launch_bounds__(128) bc_trsm_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
-                                                           const double* __restrict__ R, int a,
-                                                           double* __restrict__ out, int64_t ldo) {
-  __shared__ double Rs[kBcMax * kBcMax];
-  __shared__ double rinv[kBcMax];
-  for (int e = threadIdx.x; e < a * a; e += blockDim.x) Rs[(e % a) + (e / a) * kBcMax] = R[(e % a) + (e / a) * kBcMax];
-  __syncthreads();
-  if (threadIdx.x < a) rinv[threadIdx.x] = 1.0 / Rs[threadIdx.x + threadIdx.x * kBcMax];
-  __syncthreads();
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= M) return;
-  double w[kBcMax];
-#pragma unroll
-  for (int j = 0; j < kBcMax; ++j) {
-    if (j < a) {
-      double acc = A[j * lda + i];
-#pragma unroll
-      for (int k = 0; k < j; ++k) acc -= w[k] * Rs[k + j * kBcMax];
-      w[j] = acc * rinv[j];
-      out[j * ldo + i] = w[j];
-    }
+    Tinv[i + c * kBcMax] = (i <= c && i < a) ? Bs[i + c * kBcMax] : bc_zero<T>();
   }
 }
 

@@ -1157,13 +1157,6 @@ private:
         if (a_even > a) CU(cudaMemsetAsync(bc_ya_.p + a * W, 0, W * sizeof(double), ctx_->stream));
       }
       auto times_inverse = [&](const double* A, const double* R, double* out) {
-        if (packed) {  // real field: one row-wise forward substitution (bc_trsm_rows_kernel)
-          if (len == 0) return;
-          bc_trsm_rows_kernel<<<static_cast<unsigned>((len + 127) / 128), 128, 0, ctx_->stream>>>(
-              A + lo, D_, len, R, a, out + lo, D_);
-          launched(ctx_); dbg_sync("block_chol trsm");
-          return;
-        }
         bc_tri_inverse_kernel<T><<<1, kBcThreads, bc_smem_bytes<T>(), ctx_->stream>>>(T_(const_cast<double*>(R)), a,
                                                                                    T_(bc_tinv_.p));
         launched(ctx_); dbg_sync("block_chol inverse");
