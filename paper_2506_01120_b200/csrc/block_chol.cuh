@@ -97,7 +97,6 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
   T* Gs = Zs + kBcMax * kBcMax;
   __shared__ double s[kBcMax];
   __shared__ double s_rn2[kBcMax];  // rn2 staged: thread 0's serial decisions read shared memory only
-  __shared__ double g0[kBcMax];
   __shared__ int acc_list[kBcMax];
   __shared__ int s_ind, s_stop;
   const int tid = threadIdx.x;
@@ -106,7 +105,6 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
   __syncthreads();
   if (sub == 0 && t < nb) {
     s[t] = bc_re(Gs[t + t * kBcMax]);
-    g0[t] = s[t];  // original diagonal (Gs becomes the Schur complement)
     s_rn2[t] = rn2[t];
   }
   int acc = 0, tent = 0;
@@ -122,7 +120,7 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
       if (!recheck) {
         ind = r2 > tol ? 1 : 0;
       } else {
-        const double gqq = g0[q];
+        const double gqq = bc_re(Gs[q + q * kBcMax]);
         const double sq = s[q];
         // certified: the residual keeps >= 10% of the survivor's norm (so the
         // accepted set stays well conditioned, cond <= ~100 per step, and
@@ -151,27 +149,23 @@ __global__ void __launch_bounds__(kBcThreads) bc_decide_kernel(const T* __restri
     __syncthreads();
     if (s_stop) break;
     if (s_ind) {
-      // Right-looking: Gs holds the Schur complement of the accepts so far
-      // (rows / columns > q still live). Row `acc` of Z is z_t = Gs(q, t) / l,
-      // l = sqrt(Gs(q, q)); then the trailing block loses conj(z_u) z_v --
-      // every thread updates its own elements, no dot-product chains.
+      // row `acc` of Z: the new accept's R entries against every later column
       const double lqq = sqrt(s[q]);  // == rn2_q for the block's first accept
-      const double il = 1.0 / lqq;
       if (tid == 0) acc_list[acc] = q;
-      for (int v = q + 1 + tid; v < nb; v += blockDim.x) Zs[acc * kBcMax + v] = bc_scale(Gs[q + v * kBcMax], il);
-      if (tid == 0) {  // the diagonal (real, positive)
+      if (t > q && t < nb) {  // whole 4-lane groups: the shuffles stay inside active lanes
+        T part = bc_zero<T>();
+        for (int a = sub; a < acc; a += kBcLanes) part = bc_sub(part, bc_mul(bc_conj(Zs[a * kBcMax + q]), Zs[a * kBcMax + t]));
+        part = bc_group_sum(part);
+        if (sub == 0) {
+          const T z = bc_scale(bc_sub(Gs[q + t * kBcMax], bc_scale(part, -1.0)), 1.0 / lqq);
+          Zs[acc * kBcMax + t] = z;
+          s[t] -= bc_abs2(z);
+        }
+      }
+      if (tid == 0) {  // the diagonal (real, positive); no thread reads row `acc` in this phase
         if constexpr (sizeof(T) == sizeof(double)) Zs[acc * kBcMax + q] = lqq;
         else Zs[acc * kBcMax + q] = T{lqq, 0.0};
       }
-      const int m = nb - q - 1;  // trailing block (u, v) in (q, nb)^2, upper triangle u <= v
-      for (int e = tid; e < m * m; e += blockDim.x) {
-        const int u = q + 1 + e % m, v = q + 1 + e / m;
-        if (u > v) continue;
-        const T zu = bc_scale(Gs[q + u * kBcMax], il), zv = bc_scale(Gs[q + v * kBcMax], il);
-        Gs[u + v * kBcMax] = bc_sub(Gs[u + v * kBcMax], bc_mul(bc_conj(zu), zv));
-      }
-      __syncthreads();
-      if (tid > q && tid < nb) s[tid] = bc_re(Gs[tid + tid * kBcMax]);
       ++acc;
       __syncthreads();
     }
