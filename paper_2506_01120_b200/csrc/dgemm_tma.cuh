@@ -108,7 +108,7 @@ __device__ __forceinline__ int sw_mc3(int m, int k) {
 // multiple of 16; rows up to 4 ceil(K/4) are read and must be zero past K).
 // mapB: 2-D {K, N} box {16, 64}. All 128-byte swizzled, out-of-bounds
 // elements read as zeros.
-template <bool A_KCONTIG, REpi EPI, int MC_BOX = 5>
+template <bool A_KCONTIG, REpi EPI, int MC_BOX = 5, int GROUP = rg::GROUP>
 __global__ void __launch_bounds__(tg::THREADS, 2)
 dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                  int K, double* __restrict__ Cout, int64_t ldc, double alpha, const double* __restrict__ X,
@@ -122,7 +122,7 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % WM, wn = warp / WM;
   int m_tile, n_tile;
-  grouped_tile<rg::GROUP>(blockIdx.x + blockIdx.y * gridDim.x, gridDim.x, gridDim.y, m_tile, n_tile);
+  grouped_tile<GROUP>(blockIdx.x + blockIdx.y * gridDim.x, gridDim.x, gridDim.y, m_tile, n_tile);
   const int m0 = m_tile * BM, n0 = n_tile * BN;
   const int KT = K > 0 ? (K + BK - 1) / BK : 0;
 
