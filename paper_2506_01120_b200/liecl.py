@@ -204,6 +204,33 @@ class PauliSingleList(Sequence):
         return len(other) == len(self) and all(a == b for a, b in zip(self, other))
 
 
+class PauliSumList(Sequence):
+    """result.basis / orthonormal_basis of a multi-term Pauli closure: element
+    k is the sum of terms [off[k], off[k+1]) of the (x, z, coef) arrays,
+    built on access (a closure can hold 10^5 terms)."""
+
+    def __init__(self, off: np.ndarray, x: np.ndarray, z: np.ndarray, coef: np.ndarray, qubits: int):
+        self.off, self.x, self.z, self.coef, self.qubits = off, x, z, coef, qubits
+
+    def __len__(self) -> int:
+        return len(self.off) - 1
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        if k < 0:
+            k += len(self)
+        if not 0 <= k < len(self):
+            raise IndexError(k)
+        return _sum_from_arrays(self.qubits, self.x[self.off[k]:], self.z[self.off[k]:], self.coef[self.off[k]:],
+                                int(self.off[k + 1] - self.off[k]))
+
+    def __eq__(self, other):
+        if not isinstance(other, (list, tuple, PauliSumList)):
+            return NotImplemented
+        return len(other) == len(self) and all(a == b for a, b in zip(self, other))
+
+
 @dataclass
 class WarningRecord:
     kind: str
@@ -483,17 +510,15 @@ def closure_pauli_sums_arrays(offsets, x, z, coef, qubits: int, method: Method =
     stats = ClosureStats(st.commutators_evaluated, st.independence_checks, st.accepted, st.wall_seconds, warnings,
                          {k: v for k, v in st.as_dict().items() if k in ("batches", "survivors", "rechecks", "kernels")})
 
-    def sums(off, xs, zs, cs):
-        return [PauliSum(qubits, [(PauliString(int(xs[t]), int(zs[t]), qubits), complex(cs[t, 0], cs[t, 1]))
-                                  for t in range(off[i], off[i + 1])]) for i in range(n)]
-
     def arrays(off, xs, zs, cs):
         t = int(off[n])
         return off[: n + 1].copy(), xs[:t].copy(), zs[:t].copy(), cs[:t].copy()
     gram = method == Method.matrix_inversion
-    res = ClosureResult(sums(bo, bx, bz, bc), None if gram else sums(oo, ox, oz, ocf), n, method, Backend.pauli,
-                        config.tolerance, stats, log[: log_len.value].copy() if config.record_log else None,
-                        arrays(bo, bx, bz, bc), None if gram else arrays(oo, ox, oz, ocf))
+    ba = arrays(bo, bx, bz, bc)
+    oa = None if gram else arrays(oo, ox, oz, ocf)
+    res = ClosureResult(PauliSumList(*ba, qubits), None if gram else PauliSumList(*oa, qubits), n, method,
+                        Backend.pauli, config.tolerance, stats,
+                        log[: log_len.value].copy() if config.record_log else None, ba, oa)
     if gram:  # result.gram from the device (liecl_b200_pauli_sums_fetch_gram)
         A = np.zeros(n * n, np.complex128)
         Ai = np.zeros(n * n, np.complex128)

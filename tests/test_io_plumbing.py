@@ -147,3 +147,17 @@ def test_pauli_single_list_is_a_lazy_sequence():
         raise AssertionError("index past the end must raise")
     except IndexError:
         pass
+
+
+def test_pauli_sum_list_is_a_lazy_sequence():
+    """result.basis of a multi-term closure (liecl.PauliSumList) built on access."""
+    import numpy as np
+    off = np.array([0, 2, 2, 3], np.int64)
+    x = np.array([1, 2, 3], np.uint64)
+    z = np.array([0, 2, 1], np.uint64)
+    c = np.array([[0.0, 1.0], [0.5, -0.5], [-1.0, 0.0]])
+    lst = liecl.PauliSumList(off, x, z, c, 2)
+    assert len(lst) == 3
+    assert [len(s.terms) for s in lst] == [2, 0, 1]
+    assert lst[0].terms[1] == (liecl.PauliString(2, 2, 2), complex(0.5, -0.5))
+    assert lst[-1] == lst[2] and lst[0:2] == [lst[0], lst[1]]
