@@ -1109,7 +1109,12 @@ private:
   // fused check (LIECL_B200_SUMS_FUSED=0 disables it, e.g. to exercise the
   // general merges)
   static constexpr size_t kFusedSmemMax = 220 * 1024;
-  static constexpr int kFusedMaxBatch = 16;
+  // batches of at most this many candidates take the fused single-CTA check
+  // (LIECL_B200_SUMS_FUSED_BATCH overrides; larger batches run the merges)
+  const int kFusedMaxBatch = [] {
+    const char* e = std::getenv("LIECL_B200_SUMS_FUSED_BATCH");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
   bool fused_ = [] {
     const char* e = std::getenv("LIECL_B200_SUMS_FUSED");
     return !(e && e[0] == '0');
