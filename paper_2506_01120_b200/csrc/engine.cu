@@ -949,26 +949,27 @@ private:
   void ensure_batch(int64_t cnt) {
     cx_.ensure(cnt); cz_.ensure(cnt); ch_.ensure(cnt); cu_.ensure(cnt); crn_.ensure(cnt);
     cver_.ensure(cnt); cflag_.ensure(cnt); acc_.ensure(cnt); rank_.ensure(cnt);
-    size_t tmp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp, acc_.p, rank_.p, static_cast<int>(cnt), ctx_->stream);
-    scan_tmp_.ensure(tmp);
+    scan_sums_.ensure(static_cast<size_t>((cnt + pauli::kScanBlock - 1) / pauli::kScanBlock + 1));
   }
 
   // scan, bookkeeping, warnings, append
   void finish_batch(int cnt, int64_t pair_g0) {
-    size_t tmp = scan_tmp_.n;
-    CU(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tmp, acc_.p, rank_.p, cnt, ctx_->stream));
-    launched(ctx_);
+    // append ranks: exclusive scan of the accept flags (pauli.cuh scan_*)
+    const int nb = (cnt + pauli::kScanBlock - 1) / pauli::kScanBlock;
+    if (nb > 4 * pauli::kScanBlock) throw Error(LIECL_B200_INTERNAL, "Pauli batch exceeds the scan's 4M pairs");
+    pauli::scan_blocks_kernel<<<nb, pauli::kScanBlock, 0, ctx_->stream>>>(acc_.p, cnt, rank_.p, scan_sums_.p);
+    pauli::scan_sums_kernel<<<1, pauli::kScanBlock, 0, ctx_->stream>>>(scan_sums_.p, nb);
+    pauli::scan_add_kernel<<<(cnt + 255) / 256, 256, 0, ctx_->stream>>>(rank_.p, cnt, scan_sums_.p);
+    launched(ctx_), launched(ctx_), launched(ctx_);
     CU(cudaMemsetAsync(counters_.p, 0, 3 * sizeof(unsigned long long), ctx_->stream));
     pauli_count_kernel<<<(cnt + 255) / 256, 256, 0, ctx_->stream>>>(cnt, cver_.p, cflag_.p, counters_.p);
     launched(ctx_);
-    int last[2];
+    int total = 0;
     unsigned long long cnts[3];
-    CU(cudaMemcpyAsync(&last[0], rank_.p + cnt - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
-    CU(cudaMemcpyAsync(&last[1], acc_.p + cnt - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+    CU(cudaMemcpyAsync(&total, scan_sums_.p + nb, sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaMemcpyAsync(cnts, counters_.p, sizeof cnts, cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
-    const int64_t acc = last[0] + last[1];
+    const int64_t acc = total;
     ++st_.batches;
     st_.independence_checks += cnts[0];
     if (cnts[2] > 0) throw_residual_floor();
@@ -1035,7 +1036,7 @@ private:
   DevBuf<pauli::C2> ch_, cu_;
   DevBuf<double> crn_;
   DevBuf<int> cver_, cflag_, acc_, rank_;
-  DevBuf<unsigned char> scan_tmp_;
+  DevBuf<int> scan_sums_;
   DevBuf<unsigned long long> counters_;
 };
 

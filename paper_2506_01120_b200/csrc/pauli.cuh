@@ -525,6 +525,68 @@ frontier_kernel(int ngens, const uint64_t* __restrict__ gx, const uint64_t* __re
   }
 }
 
+// ---- exclusive scan of accept flags (the wide batches' append ranks) -------
+// Three launches: per-1024 block scans with their totals, one block scanning
+// the (<= 4096) totals, block offsets added back. Batches hold <= 4M pairs.
+constexpr int kScanBlock = 1024;
+__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < static_cast<int>(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    s_warp[lane] = w;  // inclusive prefix of warp totals
+  }
+  __syncthreads();
+  total = s_warp[(blockDim.x >> 5) - 1];
+  return (warp > 0 ? s_warp[warp - 1] : 0) + x - v;
+}
+__global__ void __launch_bounds__(kScanBlock) scan_blocks_kernel(const int* __restrict__ in, int n,
+                                                                 int* __restrict__ out, int* __restrict__ sums) {
+  __shared__ int s_warp[32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  int total;
+  const int e = block_exclusive_scan(i < n ? in[i] : 0, s_warp, total);
+  if (i < n) out[i] = e;
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+// one block of kScanBlock threads: exclusive scan of nb <= 4 kScanBlock totals, grand total at sums[nb]
+__global__ void __launch_bounds__(kScanBlock) scan_sums_kernel(int* __restrict__ sums, int nb) {
+  __shared__ int s_warp[32];
+  int v[4], t = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = threadIdx.x * 4 + k;
+    v[k] = i < nb ? sums[i] : 0;
+    t += v[k];
+  }
+  int total;
+  int run = block_exclusive_scan(t, s_warp, total);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = threadIdx.x * 4 + k;
+    if (i < nb) sums[i] = run;
+    run += v[k];
+  }
+  if (threadIdx.x == 0) sums[nb] = total;
+}
+__global__ void scan_add_kernel(int* __restrict__ out, int n, const int* __restrict__ sums) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += sums[i / kScanBlock];
+}
+
 // n = mask + 2 slots
 __global__ void reset_table_kernel(StringSet s, uint64_t n) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
