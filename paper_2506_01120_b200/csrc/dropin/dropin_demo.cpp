@@ -88,6 +88,66 @@ int main() {
     }
     std::printf("]}, ");
   }
+  // past 32 qubits (128-bit string keys): config 4's ring and the reference's
+  // TFIM-open n = 4 generators relabelled onto 48 qubits (the reference's
+  // default cap d^2 overflows there, so max_dim is explicit, as a caller must)
+  {
+    const std::uint32_t q = 48;
+    const std::uint32_t ring[10] = {0, 5, 11, 17, 23, 29, 35, 41, 44, 47};
+    auto relabel = [](std::uint64_t m, const std::uint32_t* pos, int n) {
+      std::uint64_t out = 0;
+      for (int j = 0; j < n; ++j)
+        if ((m >> j) & 1u) out |= 1ull << pos[j];
+      return out;
+    };
+    ClosureConfig wide = cfg;
+    wide.max_dim = 4096;
+    std::vector<Operator> gens;
+    for (std::uint32_t j = 0; j < 10; ++j) {
+      const std::uint64_t b = relabel((1ull << j) | (1ull << ((j + 1) % 10)), ring, 10);
+      gens.emplace_back(PauliSum::single(PauliString{b, 0, q}, I));
+    }
+    for (std::uint32_t j = 0; j < 10; ++j) {
+      const std::uint64_t b = relabel((1ull << j) | (1ull << ((j + 1) % 10)), ring, 10);
+      gens.emplace_back(PauliSum::single(PauliString{b, b, q}, I));
+    }
+    for (std::uint32_t j = 0; j < 10; ++j) gens.emplace_back(PauliSum::single(PauliString{0, 1ull << ring[j], q}, I));
+    const ClosureResult r = run_closure(gens, Method::orthonorm_dimonly, wide);
+    std::printf("\"c4_q48\": ");
+    print_stats(r);
+    std::printf(", \"strings\": [");
+    for (size_t k = 0; k < r.basis.size(); ++k) {
+      const auto& t = r.basis[k].pauli().terms()[0];
+      std::printf("%s[\"%llu\",\"%llu\",%.17g,%.17g]", k ? "," : "", static_cast<unsigned long long>(t.string.x),
+                  static_cast<unsigned long long>(t.string.z), t.coefficient.real(), t.coefficient.imag());
+    }
+    std::printf("]}, ");
+    AnsatzSpec spec;
+    spec.family = AnsatzFamily::tfim_hva_open;
+    spec.qubits = 4;
+    const std::uint32_t tf[4] = {3, 31, 40, 47};
+    std::vector<Operator> sums;
+    for (auto& s : build_generators(spec)) {
+      std::vector<PauliSum::Term> terms;
+      for (const auto& t : s.terms())
+        terms.push_back({PauliString{relabel(t.string.x, tf, 4), relabel(t.string.z, tf, 4), q}, t.coefficient});
+      sums.emplace_back(PauliSum::from_terms(q, terms));
+    }
+    const ClosureResult rs = run_closure(sums, Method::orthonorm_dimonly, wide);
+    std::printf("\"tfim4_q48\": ");
+    print_stats(rs);
+    std::printf(", \"sums\": [");
+    for (size_t k = 0; k < rs.basis.size(); ++k) {
+      std::printf("%s[", k ? "," : "");
+      const auto terms = rs.basis[k].pauli().terms();
+      for (size_t i = 0; i < terms.size(); ++i)
+        std::printf("%s[\"%llu\",\"%llu\",%.17g,%.17g]", i ? "," : "",
+                    static_cast<unsigned long long>(terms[i].string.x), static_cast<unsigned long long>(terms[i].string.z),
+                    terms[i].coefficient.real(), terms[i].coefficient.imag());
+      std::printf("]");
+    }
+    std::printf("]}, ");
+  }
   // multi-term Pauli sums: the reference's TFIM-open HVA generators, n = 6
   for (const Method m : {Method::orthonorm_dimonly, Method::orthonorm}) {
     AnsatzSpec spec;

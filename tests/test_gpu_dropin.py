@@ -179,3 +179,50 @@ def test_dropin_gram_state_and_large_dense(demo):
     g = demo["gram_state"]
     assert g["schur"] == 0.75 and abs(g["inv01"] + 2.0 / 3.0) < 1e-15 and g["err"] < 1e-15
     assert demo["d128"]["dimension"] == 3
+
+
+def _relabel(a, pos):
+    out = np.zeros(len(a), np.uint64)
+    for i, m in enumerate(a):
+        v = 0
+        for j, p in enumerate(pos):
+            if (int(m) >> j) & 1:
+                v |= 1 << p
+        out[i] = v
+    return out
+
+
+def test_dropin_48_qubit_strings(demo, golden):
+    """Config 4's ring relabelled onto 48 qubits through the C++ drop-in (the
+    128-bit string keys): config 4's golden strings relabelled, same bits."""
+    meta, g = golden("c4_pauli_ring_n10_orthonorm-dimonly")
+    r = demo["c4_q48"]
+    assert r["dimension"] == 380
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert r[k] == meta["stats"][k]
+    pos = [0, 5, 11, 17, 23, 29, 35, 41, 44, 47]
+    xs = np.array([int(t[0]) for t in r["strings"]], np.uint64)
+    zs = np.array([int(t[1]) for t in r["strings"]], np.uint64)
+    assert np.array_equal(xs, _relabel(g["x"], pos)) and np.array_equal(zs, _relabel(g["z"], pos))
+    coef = np.array([t[2:] for t in r["strings"]])
+    assert np.array_equal(coef, g["coef_bits"].view(np.float64))
+
+
+def test_dropin_48_qubit_sums(demo, ref_exact):
+    """The reference's TFIM-open n = 4 generators on 48 qubits through the C++
+    drop-in (SumEngineT<WKey>) against the reference build on the same input."""
+    off, x, z, c = ref_exact.build_generators("tfim_hva_open", 4)
+    pos = [3, 31, 40, 47]
+    ex, ez = _relabel(x, pos), _relabel(z, pos)
+    o = ref_exact.closure_pauli(off, ex, ez, c, 48, method="orthonorm-dimonly", tol=1e-10, max_dim=4096,
+                                basis_cap=4096)
+    r = demo["tfim4_q48"]
+    assert r["dimension"] == o.dimension == 16
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert r[k] == o.stats[k]
+    ro, rx, rz, rc = o.basis
+    allt = [t for s_ in r["sums"] for t in s_]
+    assert [len(s_) for s_ in r["sums"]] == np.diff(ro).tolist()
+    assert np.array_equal(np.array([int(t[0]) for t in allt], np.uint64), rx)
+    assert np.array_equal(np.array([int(t[1]) for t in allt], np.uint64), rz)
+    assert np.array_equal(np.array([t[2:] for t in allt]), rc)
