@@ -243,3 +243,22 @@ def test_dense_up_to_twelve_qubits(d, method):
     v = res.basis[2].vec()
     ov = np.vdot(ys.vec(), v) / d
     assert abs(abs(ov) - 1.0) < 1e-12
+
+
+@pytest.mark.parametrize("d", [3, 5, 6, 12])
+@pytest.mark.parametrize("field", ["auto", "complex"])
+def test_non_power_of_two_dimensions_match_reference(ref, d, field):
+    """The reference takes any dense d (R:include/liecl/dense.hpp); odd d has no
+    packed field (complex path), even non-power-of-two d packs; neither has
+    the 16-element alignment some TMA boxes need, so the cp.async kernels
+    take over. Random traceless generators close to su(d)."""
+    rng = np.random.default_rng(d)
+    mats = [g.reshape(d, d, order="F") for g in _random_ah(rng, d, 2)]
+    gens = np.stack([(m - np.trace(m) / d * np.eye(d)).ravel(order="F") for m in mats])  # traceless
+    res = liecl.closure_dense_arrays(gens, d, liecl.Method.orthonorm_dimonly,
+                                     liecl.ClosureConfig(tolerance=1e-10, field=field, record_log=True))
+    o = ref.decision_log_dense(gens, d, keep_original=False, tol=1e-10, threads=8)
+    assert res.dimension == o.dimension == d * d - 1
+    log = res.decision_log
+    assert np.array_equal(log["independent"], o.log["independent"])
+    assert np.abs(res.basis_array - o.basis).max() < 1e-10
