@@ -171,12 +171,142 @@ __device__ __forceinline__ void ah_elem(const double* p, int i, int k, double& r
   else { re = 0.0; im = u; }
 }
 
+// One pair's pieces, shared by the kernels below (same arithmetic in the same
+// order, so every variant gives bit-identical h and norms).
+//
+// Operands of pair `pair` into pa / pb (stride LDP): 16-byte pieces (DIM
+// even; i even and LDP even keep them 16-byte aligned in shared memory).
+// cp.async issues every piece before waiting: one memory latency per pair.
+template <int DIM, int LDP, int NT, bool ASYNC>
+__device__ __forceinline__ void ah_load_pair(const double* __restrict__ basis, int64_t pair, double* pa, double* pb,
+                                             int tip) {
+  constexpr int D2 = DIM * DIM;
+  int64_t l, m;
+  pair_from_index(pair, l, m);
+  const double2* ga = reinterpret_cast<const double2*>(basis + l * D2);
+  const double2* gb = reinterpret_cast<const double2*>(basis + m * D2);
+#pragma unroll
+  for (int e = tip; e < D2 / 2; e += NT) {
+    const int i = (2 * e) % DIM, k = (2 * e) / DIM;
+    if constexpr (ASYNC) {
+      cp_async16(pa + i + k * LDP, ga + e, 16);
+      cp_async16(pb + i + k * LDP, gb + e, 16);
+    } else {
+      const double2 va = ga[e], vb = gb[e];
+      *reinterpret_cast<double2*>(pa + i + k * LDP) = va;
+      *reinterpret_cast<double2*>(pb + i + k * LDP) = vb;
+    }
+  }
+  if constexpr (ASYNC) {
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+}
+
+// This warp's WR x WC tiles of P = A B, fragments gathered straight from the
+// packed inputs (A fragments reused across the WC column tiles, B fragments
+// across the WR row tiles).
+template <int DIM, int LDP, int WR, int WC>
+__device__ __forceinline__ void ah_product(const double* pa, const double* pb, int wr0, int wc0, int g, int t,
+                                           double (&cre)[WR][WC][2], double (&cim)[WR][WC][2]) {
+#pragma unroll 2
+  for (int k0 = 0; k0 < DIM; k0 += 4) {
+    const int k = k0 + t;
+    double br[WC], bi[WC], ar[WR], ai[WR];
+#pragma unroll
+    for (int c = 0; c < WC; ++c) ah_elem<LDP>(pb, k, (wc0 + c) * 8 + g, br[c], bi[c]);  // B(k, tj + g)
+#pragma unroll
+    for (int r = 0; r < WR; ++r) ah_elem<LDP>(pa, (wr0 + r) * 8 + g, k, ar[r], ai[r]);  // A(ti + g, k)
+    // four sweeps over the warp's tiles: two DMMAs into the same
+    // accumulator are WR*WC*2 - 1 instructions apart (no back-to-back
+    // dependency on the DMMA latency); each accumulator still adds its
+    // terms in the same order (re: ar br, then -ai bi; im: ar bi, then ai br)
+#pragma unroll
+    for (int r = 0; r < WR; ++r)
+#pragma unroll
+      for (int c = 0; c < WC; ++c) dmma_8x8x4(cre[r][c][0], cre[r][c][1], ar[r], br[c]);
+#pragma unroll
+    for (int r = 0; r < WR; ++r)
+#pragma unroll
+      for (int c = 0; c < WC; ++c) dmma_8x8x4(cim[r][c][0], cim[r][c][1], ar[r], bi[c]);
+#pragma unroll
+    for (int r = 0; r < WR; ++r)
+#pragma unroll
+      for (int c = 0; c < WC; ++c) dmma_8x8x4(cre[r][c][0], cre[r][c][1], -ai[r], bi[c]);
+#pragma unroll
+    for (int r = 0; r < WR; ++r)
+#pragma unroll
+      for (int c = 0; c < WC; ++c) dmma_8x8x4(cim[r][c][0], cim[r][c][1], ai[r], br[c]);
+  }
+}
+
+// P(i, k) re at pre[p_at(i, k)]: the epilogue reads P(k, i) along a row and
+// P(i, k) down a column
+template <int DIM, int WR, int WC>
+__device__ __forceinline__ void ah_store_p(double* pre, double* pim, int wr0, int wc0, int g, int t,
+                                           const double (&cre)[WR][WC][2], const double (&cim)[WR][WC][2]) {
+#pragma unroll
+  for (int r = 0; r < WR; ++r) {
+    const int ti = (wr0 + r) * 8;
+#pragma unroll
+    for (int c = 0; c < WC; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        pre[p_at<DIM>(ti + g, (wc0 + c) * 8 + 2 * t + h)] = cre[r][c][h];
+        pim[p_at<DIM>(ti + g, (wc0 + c) * 8 + 2 * t + h)] = cim[r][c][h];
+      }
+  }
+}
+
+// packed h = P - P^dagger for this thread's elements; returns its part of sum w h^2
+template <int DIM, int NT>
+__device__ __forceinline__ double ah_h_values(const double* pre, const double* pim, int tip,
+                                              double (&hv)[(DIM * DIM + NT - 1) / NT]) {
+  constexpr int D2 = DIM * DIM;
+  double sumsq = 0.0;
+#pragma unroll
+  for (int q = 0; q < (D2 + NT - 1) / NT; ++q) {
+    const int e = tip + q * NT;
+    if (e >= D2) break;
+    const int i = e % DIM, k = e / DIM;
+    double v;
+    if (i < k) v = pre[p_at<DIM>(i, k)] - pre[p_at<DIM>(k, i)];
+    else if (i > k) v = pim[p_at<DIM>(k, i)] + pim[p_at<DIM>(i, k)];
+    else v = 2.0 * pim[p_at<DIM>(i, i)];
+    hv[q] = v;
+    sumsq += (i == k ? 1.0 : 2.0) * v * v;
+  }
+  return sumsq;
+}
+
+// norm, null flag and the (normalised) packed h of pair j from the warps' partial sums
+template <int DIM, int NT, int WARPS>
+__device__ __forceinline__ void ah_finish(const double* red, const double (&hv)[(DIM * DIM + NT - 1) / NT], int j,
+                                          int tip, double tol, bool normalize, double* __restrict__ out,
+                                          double* __restrict__ hnorm, int* __restrict__ is_null) {
+  constexpr int D2 = DIM * DIM;
+  double total = 0.0;
+#pragma unroll
+  for (int w = 0; w < WARPS; ++w) total += red[w];
+  const double hn = sqrt(total) / sqrt(static_cast<double>(DIM));
+  const bool nul = !(hn > tol);
+  if (tip == 0) {
+    hnorm[j] = hn;
+    is_null[j] = nul ? 1 : 0;
+  }
+  const double sc = !normalize ? 1.0 : (nul ? 0.0 : 1.0 / hn);
+  double* o = out + static_cast<int64_t>(j) * D2;
+#pragma unroll
+  for (int q = 0; q < (D2 + NT - 1) / NT; ++q) {
+    const int e = tip + q * NT;
+    if (e < D2) o[e] = hv[q] * sc;
+  }
+}
+
 // K1 on the packed path: pairs [g0, g0+count) of the packed commutator basis;
-// writes packed h_unit, ||h||, null flag. One DMMA product P = A B per pair,
-// fragments gathered straight from the packed inputs in shared memory (A
-// fragments reused across a warp's WC column tiles, B fragments across its WR
-// row tiles); P is written back over the consumed inputs and h = P - P^dagger
-// is read out in the packed layout. ~70 KB per pair at d = 64.
+// writes packed h_unit, ||h||, null flag. One DMMA product P = A B per pair;
+// P is written back over the consumed inputs and h = P - P^dagger is read out
+// in the packed layout. ~70 KB per pair at d = 64.
 template <int DIM, int MINB = 2, int WR = CommAhShape<DIM>::WR, int WC = CommAhShape<DIM>::WC, bool ASYNC = true>
 __global__ void __launch_bounds__(CommAhShape<DIM, WR, WC>::THREADS, MINB)
 commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, double tol, bool normalize,
@@ -200,31 +330,7 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
   double* pb = pa + S::PACKED;
   double* red = pb + S::PACKED;
 
-  if (active) {
-    int64_t l, m;
-    pair_from_index(g0 + j, l, m);
-    const double2* ga = reinterpret_cast<const double2*>(basis + l * D2);
-    const double2* gb = reinterpret_cast<const double2*>(basis + m * D2);
-    // 16-byte pieces (DIM even); i even and LDP even keep them 16-byte
-    // aligned in shared memory. cp.async issues every piece before waiting:
-    // one memory latency per pair instead of one per loop trip.
-#pragma unroll
-    for (int e = tip; e < D2 / 2; e += NT) {
-      const int i = (2 * e) % DIM, k = (2 * e) / DIM;
-      if constexpr (ASYNC) {
-        cp_async16(pa + i + k * LDP, ga + e, 16);
-        cp_async16(pb + i + k * LDP, gb + e, 16);
-      } else {
-        const double2 va = ga[e], vb = gb[e];
-        *reinterpret_cast<double2*>(pa + i + k * LDP) = va;
-        *reinterpret_cast<double2*>(pb + i + k * LDP) = vb;
-      }
-    }
-    if constexpr (ASYNC) {
-      cp_async_commit();
-      cp_async_wait<0>();
-    }
-  }
+  if (active) ah_load_pair<DIM, LDP, NT, ASYNC>(basis, g0 + j, pa, pb, tip);
   __syncthreads();
 
   double cre[WR][WC][2], cim[WR][WC][2];
@@ -232,92 +338,17 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
   for (int r = 0; r < WR; ++r)
 #pragma unroll
     for (int c = 0; c < WC; ++c) cre[r][c][0] = cre[r][c][1] = cim[r][c][0] = cim[r][c][1] = 0.0;
-  if (active) {
-#pragma unroll 2
-    for (int k0 = 0; k0 < DIM; k0 += 4) {
-      const int k = k0 + t;
-      double br[WC], bi[WC], ar[WR], ai[WR];
-#pragma unroll
-      for (int c = 0; c < WC; ++c) ah_elem<LDP>(pb, k, (wc0 + c) * 8 + g, br[c], bi[c]);  // B(k, tj + g)
-#pragma unroll
-      for (int r = 0; r < WR; ++r) ah_elem<LDP>(pa, (wr0 + r) * 8 + g, k, ar[r], ai[r]);  // A(ti + g, k)
-      // four sweeps over the warp's tiles: two DMMAs into the same
-      // accumulator are WR*WC*2 - 1 instructions apart (no back-to-back
-      // dependency on the DMMA latency); each accumulator still adds its
-      // terms in the same order (re: ar br, then -ai bi; im: ar bi, then ai br)
-#pragma unroll
-      for (int r = 0; r < WR; ++r)
-#pragma unroll
-        for (int c = 0; c < WC; ++c) dmma_8x8x4(cre[r][c][0], cre[r][c][1], ar[r], br[c]);
-#pragma unroll
-      for (int r = 0; r < WR; ++r)
-#pragma unroll
-        for (int c = 0; c < WC; ++c) dmma_8x8x4(cim[r][c][0], cim[r][c][1], ar[r], bi[c]);
-#pragma unroll
-      for (int r = 0; r < WR; ++r)
-#pragma unroll
-        for (int c = 0; c < WC; ++c) dmma_8x8x4(cre[r][c][0], cre[r][c][1], -ai[r], bi[c]);
-#pragma unroll
-      for (int r = 0; r < WR; ++r)
-#pragma unroll
-        for (int c = 0; c < WC; ++c) dmma_8x8x4(cim[r][c][0], cim[r][c][1], ai[r], br[c]);
-    }
-  }
+  if (active) ah_product<DIM, LDP, WR, WC>(pa, pb, wr0, wc0, g, t, cre, cim);
   __syncthreads();  // inputs consumed: P planes reuse the packed buffers
-  // P(i, k) re at pre[p_at(i, k)]: the epilogue reads P(k, i) along a row and
-  // P(i, k) down a column
-  double* pre = pa;
-  double* pim = pb;
-  if (active) {
-#pragma unroll
-    for (int r = 0; r < WR; ++r) {
-      const int ti = (wr0 + r) * 8;
-#pragma unroll
-      for (int c = 0; c < WC; ++c)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          pre[p_at<DIM>(ti + g, (wc0 + c) * 8 + 2 * t + h)] = cre[r][c][h];
-          pim[p_at<DIM>(ti + g, (wc0 + c) * 8 + 2 * t + h)] = cim[r][c][h];
-        }
-    }
-  }
+  if (active) ah_store_p<DIM, WR, WC>(pa, pb, wr0, wc0, g, t, cre, cim);
   __syncthreads();
-  double sumsq = 0.0;
   double hv[(D2 + NT - 1) / NT];
-  if (active) {
-#pragma unroll
-    for (int q = 0; q < (D2 + NT - 1) / NT; ++q) {
-      const int e = tip + q * NT;
-      if (e >= D2) break;
-      const int i = e % DIM, k = e / DIM;
-      double v;
-      if (i < k) v = pre[p_at<DIM>(i, k)] - pre[p_at<DIM>(k, i)];
-      else if (i > k) v = pim[p_at<DIM>(k, i)] + pim[p_at<DIM>(i, k)];
-      else v = 2.0 * pim[p_at<DIM>(i, i)];
-      hv[q] = v;
-      sumsq += (i == k ? 1.0 : 2.0) * v * v;
-    }
-  }
+  double sumsq = active ? ah_h_values<DIM, NT>(pa, pb, tip, hv) : 0.0;
   sumsq = warp_sum(sumsq);
   if (lane == 0) red[wip] = sumsq;
   __syncthreads();
   if (!active) return;
-  double total = 0.0;
-#pragma unroll
-  for (int w = 0; w < S::WARPS_PER_PAIR; ++w) total += red[w];
-  const double hn = sqrt(total) / sqrt(static_cast<double>(DIM));
-  const bool nul = !(hn > tol);
-  if (wip == 0 && lane == 0) {
-    hnorm[j] = hn;
-    is_null[j] = nul ? 1 : 0;
-  }
-  const double sc = !normalize ? 1.0 : (nul ? 0.0 : 1.0 / hn);
-  double* o = out + static_cast<int64_t>(j) * D2;
-#pragma unroll
-  for (int q = 0; q < (D2 + NT - 1) / NT; ++q) {
-    const int e = tip + q * NT;
-    if (e < D2) o[e] = hv[q] * sc;
-  }
+  ah_finish<DIM, NT, S::WARPS_PER_PAIR>(red, hv, j, tip, tol, normalize, out, hnorm, is_null);
 }
 
 // packed path, any even d: one CTA per pair, operands through L1/L2
