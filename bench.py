@@ -276,6 +276,12 @@ def fp64_peak_tflops(torch, device):
     return 8.0 * n ** 3 / (best / 1e3) / 1e12
 
 
+def gemm_name(field: str) -> str:
+    """The projection GEMM kernel the engine launches: TMA-staged unless
+    LIECL_B200_TMA=0 (then the cp.async kernels; split-K grids use those too)."""
+    return f"{field}gemm_dmma (cp.async)" if os.environ.get("LIECL_B200_TMA", "1") == "0" else f"{field}gemm_tma"
+
+
 def load_traffic():
     """dram bytes per launch of the projection GEMMs from the committed ncu
     capture summary (profiles/), if present."""
@@ -679,9 +685,9 @@ def run_b200_arm(a):
                                    f"dp{world}: disjoint closure rows per GPU, basis replicated, no collective"),
                    "growth_setup_s": round(growth_s, 3), "growth_batches": grow["batches"]},
         "roofline": {"bound": "tensor",
-                     "kernel": ("dgemm_dmma (K2a_r beta=Vw^T C/d + K2b_r R=C-V beta, packed anti-Hermitian, "
-                                "DMMA.8x8x4)") if packed else
-                               "zgemm_dmma (K2a beta=V^H C/d + K2b R=C-V beta, DMMA.8x8x4)",
+                     "kernel": (f"{gemm_name('d')} (K2a_r beta=Vw^T C/d + K2b_r R=C-V beta, packed "
+                                "anti-Hermitian, DMMA.8x8x4)") if packed else
+                               f"{gemm_name('z')} (K2a beta=V^H C/d + K2b R=C-V beta, DMMA.8x8x4)",
                      "achieved": roof["achieved"], "peak": peak, "unit": "TFLOP/s", "frac": roof["frac"],
                      "traffic": traffic, "launches": roof["launches"], "avg_launch_ms": roof["avg_launch_ms"],
                      "share_of_step": roof["share_of_step"],
@@ -846,7 +852,7 @@ def run_c3(a):
                        "parallelism": (f"D-sharded x{world} (NCCL all-reduce of beta and squared norms)" if sharded
                                        else f"replicas x{world}"),
                        "l2": "inputs larger than L2 (basis 17 GB / N per rank)"},
-            "roofline": {"bound": "tensor", "kernel": "zgemm_dmma (K2a + K2b)", "achieved": gfl / (gms / 1e3) / 1e12,
+            "roofline": {"bound": "tensor", "kernel": f"{gemm_name('z')} (K2a + K2b)", "achieved": gfl / (gms / 1e3) / 1e12,
                          "peak": peak, "unit": "TFLOP/s", "frac": gfl / (gms / 1e3) / 1e12 / peak,
                          "share_of_step": gms / sum(times), "traffic": None,
                          "peak_source": "measured in-run: cuBLAS ZGEMM 4096^3 (torch.matmul complex128)"},

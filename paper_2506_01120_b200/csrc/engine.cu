@@ -25,7 +25,6 @@
 // batches of all available pairs.
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cudaTypedefs.h>
 #include <cusolverDn.h>
@@ -57,6 +56,7 @@
 #include "zgemm_tma.cuh"
 #include "pauli.cuh"
 #include "pauli_sum.cuh"
+#include "scan.cuh"
 #include "tiny.cuh"
 #include "vecops.cuh"
 #include "zgemm_dmma.cuh"

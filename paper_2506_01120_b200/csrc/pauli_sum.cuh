@@ -212,17 +212,6 @@ __global__ void seg_positions_kernel(const int* __restrict__ off, int nseg, int 
     out[p] = (p < nseg && off[p] < n) ? pos[off[p]] : total;
 }
 
-// exclusive-scan total: pos[n-1] + flag[n-1]
-__global__ void scan_total_kernel(const int* __restrict__ pos, const int* __restrict__ flag, int n,
-                                  int* __restrict__ out) {
-  *out = n > 0 ? pos[n - 1] + flag[n - 1] : 0;
-}
-
-__global__ void scan_total64_kernel(const long long* __restrict__ pos, const long long* __restrict__ cnt, int n,
-                                    long long* __restrict__ out) {
-  *out = n > 0 ? pos[n - 1] + cnt[n - 1] : 0;
-}
-
 // drop rule per segment: keep |c| > 1e-14 * max |c| (one warp per segment)
 __global__ void floor_keep_kernel(const int* __restrict__ roff, int nseg, const double* __restrict__ rmag,
                                   int* __restrict__ keep) {

@@ -282,27 +282,26 @@ private:
     need(temp_, bytes);
   }
 
-  // int exclusive sum of n flags -> pos; returns the total
+  // int exclusive sum of n flags -> pos (hand-written scan, scan.cuh); returns the total
   int scan_flags(const int* flag, int* pos, int n) {
     Stage st_sc(this, "scan");
-    size_t bytes = 0;
-    CU(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag, pos, n, ctx_->stream));
-    ensure_temp(bytes);
-    CU(cub::DeviceScan::ExclusiveSum(temp_.p, bytes, flag, pos, n, ctx_->stream));
-    psum::scan_total_kernel<<<1, 1, 0, ctx_->stream>>>(pos, flag, n, small_.p);
-    launched(ctx_);
-    return read_int(small_.p);
+    if (n <= 0) return 0;
+    need(scan_ws_, static_cast<size_t>(scan::workspace(n)));
+    int k = 0;
+    const int* total = scan::exclusive<int>(flag, pos, n, scan_ws_.p, ctx_->stream, k);
+    ctx_->kernels += k;
+    CU(cudaGetLastError());
+    return read_int(total);
   }
   // 64-bit exclusive sum of n counts -> pos; returns the total
   long long scan_counts(const long long* cnt, long long* pos, int n) {
-    size_t bytes = 0;
-    CU(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, pos, n, ctx_->stream));
-    ensure_temp(bytes);
-    CU(cub::DeviceScan::ExclusiveSum(temp_.p, bytes, cnt, pos, n, ctx_->stream));
-    need(total_ll_, 1);
-    psum::scan_total64_kernel<<<1, 1, 0, ctx_->stream>>>(pos, cnt, n, total_ll_.p);
-    launched(ctx_);
-    return read_ll(total_ll_.p);
+    if (n <= 0) return 0;
+    need(scan_ws_ll_, static_cast<size_t>(scan::workspace(n)));
+    int k = 0;
+    const long long* total = scan::exclusive<long long>(cnt, pos, n, scan_ws_ll_.p, ctx_->stream, k);
+    ctx_->kernels += k;
+    CU(cudaGetLastError());
+    return read_ll(total);
   }
 
   // PauliSum::from_terms on every segment of (off, key, val), n items:
@@ -1096,7 +1095,8 @@ private:
   // batch scratch
   DevBuf<unsigned char> temp_;
   DevBuf<int> small_, poff_, seg_, flag_, pos_, run_seg_, roff_, keep_flag_, kpos_, boff_;
-  DevBuf<long long> cnt_, cpos_, clen_, chpos_, total_ll_;
+  DevBuf<long long> cnt_, cpos_, clen_, chpos_, scan_ws_ll_;
+  DevBuf<int> scan_ws_;
   DevBuf<unsigned> idx_, is_, is1_;
   DevBuf<K> ks_, rkey_, pk_, bl_;
   DevBuf<unsigned long long> ck_, cks_;  // composite sort keys
