@@ -27,7 +27,6 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cudaTypedefs.h>
-#include <cusolverDn.h>
 
 #include <algorithm>
 #include <charconv>

@@ -10,8 +10,8 @@
 // one pass (the reference does not re-orthogonalise); independent iff ||R|| > tol.
 // Accept (R:src/closure.cpp:238-249): Schur complement s = Re(1 - beta^H u),
 // u = A^{-1} beta (= x); degeneracy below the conditioning floor; bordered
-// inverse update (GramState::expand, :55-87); full refresh from A (Cholesky,
-// LU when A is not numerically positive definite; cuSOLVER) when s < 1e-4 or
+// inverse update (GramState::expand, :55-87); full refresh from A (blocked
+// Cholesky on the DMMA GEMMs, pivoted fallback; HermInverse) when s < 1e-4 or
 // every `gram_refresh_interval` accepts (:89-95).
 // The speculative rule of :440-444 is kept: a "dependent" verdict against the
 // batch-start state stands; an "independent" one after an in-batch accept is
@@ -66,72 +66,344 @@ __global__ void identity_kernel(double2* __restrict__ M, int64_t ld, int64_t n) 
   }
 }
 
-// GramState::refresh's inverse (R:src/closure.cpp:89-95: A.ldlt().solve(I)) on
-// the device: Cholesky (zpotrf / zpotrs) for the Hermitian positive definite
-// Gram matrix of an independent basis; a matrix that is not numerically
-// positive definite takes LU with partial pivoting (zgetrf / zgetrs) and, like
-// the reference's LDL^T, still returns an inverse instead of failing.
+// ---- GramState::refresh's inverse (R:src/closure.cpp:89-95: A.ldlt().solve(I))
+// Hand-written, Cholesky based (a Hermitian positive definite Gram matrix),
+// i.e. zpotrf + zpotrs(I) in 64-wide blocks:
+//  1. right-looking Cholesky A = L L^H: per panel one CTA factors the diagonal
+//     block (gj_chol_block_kernel), L21 = A21 L11^-H by row-wise substitution
+//     (gj_trsm_rows_kernel), the trailing A22 -= L21 L21^H is a complex DMMA
+//     GEMM (gemm_subtract);
+//  2. L Y = I, block rows top-down: Z = E_K - L[K,:k0] Y[:k0,:] (gemm_mc_store),
+//     Y[K,:] = L_KK^-1 Z (column-wise substitution, gj_solve_cols_kernel);
+//  3. L^H X = Y, block rows bottom-up: Z = Y[K,:] - L[I,K]^H X[I,:]
+//     (gemm_project), X[K,:] = L_KK^-H Z.
+// Triangular blocks are solved with, never multiplied by their inverses: a
+// blocked Gauss-Jordan with explicit 64 x 64 pivot inverses measured a 3 %
+// error at cond 3e9 (this scheme: 1.6e-7, like LAPACK's potrf/potrs).
+// A diagonal that is not a finite positive number (not numerically positive
+// definite) sends the whole inverse to an unblocked Gauss-Jordan with partial
+// pivoting (Numerical-Recipes style row interchanges, columns unscrambled at
+// the end): like the reference's LDL^T it still returns an inverse; an
+// exactly singular matrix raises DegeneracyError.
+
+__device__ __forceinline__ double2 gj_mul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 gj_mulc(double2 a, double2 b) {  // a conj(b)
+  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ double2 gj_inv(double2 p) {
+  const double q = p.x * p.x + p.y * p.y;
+  return make_double2(p.x / q, -p.y / q);
+}
+
+// One CTA: the diagonal block W[K,K] (b <= 64, lower part) -> L11 (Cholesky,
+// right-looking in shared memory), written to L (ld b, upper part zero).
+// *bad = 1 on a diagonal that is not a finite positive number.
+__global__ void __launch_bounds__(256) gj_chol_block_kernel(const double2* __restrict__ W, int64_t ldw, int64_t k0,
+                                                           int b, double2* __restrict__ Lout, int* __restrict__ bad) {
+  extern __shared__ double2 gm[];  // b x b
+  double2* L = gm;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e % b, c = e / b;
+    L[e] = i >= c ? W[(k0 + i) + (k0 + c) * ldw] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int j = 0; j < b; ++j) {
+    const double dj = L[j + j * b].x;
+    if (threadIdx.x == 0 && !(dj > 0.0 && dj < INFINITY)) *bad = 1;
+    const double l = sqrt(dj), il = 1.0 / l;
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < b; i += blockDim.x)
+      L[i + j * b] = make_double2(L[i + j * b].x * il, L[i + j * b].y * il);
+    if (threadIdx.x == 0) L[j + j * b] = make_double2(l, 0.0);
+    __syncthreads();
+    // trailing lower part: L[i,c] -= L[i,j] conj(L[c,j]), j < c <= i
+    const int m = b - j - 1;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int i = j + 1 + e % m, c = j + 1 + e / m;
+      if (c <= i) {
+        const double2 f = gj_mulc(L[i + j * b], L[c + j * b]);
+        L[i + c * b] = make_double2(L[i + c * b].x - f.x, L[i + c * b].y - f.y);
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) Lout[e] = L[e];
+}
+
+// L21 = A21 L11^-H in place: rows [r0, r0 + m) of W, columns [c0, c0 + b); one
+// thread per row: x_i = (a_i - sum_{k<i} x_k conj(L[i,k])) / L[i,i]
+__global__ void __launch_bounds__(128) gj_trsm_rows_kernel(double2* __restrict__ W, int64_t ldw, int64_t r0, int64_t m,
+                                                          int64_t c0, int b, const double2* __restrict__ Lg) {
+  extern __shared__ double2 gl[];
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) gl[e] = Lg[e];
+  __syncthreads();
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= m) return;
+  double2* row = W + r0 + r + c0 * ldw;
+  for (int i = 0; i < b; ++i) {
+    double2 acc = row[i * ldw];
+    for (int k = 0; k < i; ++k) {
+      const double2 f = gj_mulc(row[k * ldw], gl[i + k * b]);
+      acc.x -= f.x;
+      acc.y -= f.y;
+    }
+    const double il = 1.0 / gl[i + i * b].x;
+    row[i * ldw] = make_double2(acc.x * il, acc.y * il);
+  }
+}
+
+// Z (b x cols, ld b) <- L^-1 Z (FWD) or L^-H Z (backward), one thread per column
+template <bool FWD>
+__global__ void __launch_bounds__(128) gj_solve_cols_kernel(double2* __restrict__ Z, int b, int64_t cols,
+                                                           const double2* __restrict__ Lg) {
+  extern __shared__ double2 gl[];
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) gl[e] = Lg[e];
+  __syncthreads();
+  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (j >= cols) return;
+  double2* z = Z + j * b;
+  if constexpr (FWD) {
+    for (int i = 0; i < b; ++i) {  // y_i = (z_i - sum_{k<i} L[i,k] y_k) / L[i,i]
+      double2 acc = z[i];
+      for (int k = 0; k < i; ++k) {
+        const double2 f = gj_mul(gl[i + k * b], z[k]);
+        acc.x -= f.x;
+        acc.y -= f.y;
+      }
+      const double il = 1.0 / gl[i + i * b].x;
+      z[i] = make_double2(acc.x * il, acc.y * il);
+    }
+  } else {
+    for (int i = b - 1; i >= 0; --i) {  // x_i = (z_i - sum_{k>i} conj(L[k,i]) x_k) / L[i,i]
+      double2 acc = z[i];
+      for (int k = i + 1; k < b; ++k) {
+        const double2 f = gj_mulc(z[k], gl[k + i * b]);
+        acc.x -= f.x;
+        acc.y -= f.y;
+      }
+      const double il = 1.0 / gl[i + i * b].x;
+      z[i] = make_double2(acc.x * il, acc.y * il);
+    }
+  }
+}
+
+// out (c x r, ld c) = in^H for in (r x c, ld r)
+__global__ void gj_conj_transpose_kernel(const double2* __restrict__ in, int64_t r, int c, double2* __restrict__ out) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < r * c;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % r, j = e / r;
+    const double2 v = in[e];
+    out[j + i * c] = make_double2(v.x, -v.y);
+  }
+}
+
+// Z[:, c0 : c0 + b] = I (Z: b x *, ld b)
+__global__ void gj_identity_cols_kernel(double2* __restrict__ Z, int b, int64_t c0) {
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x)
+    Z[(e % b) + (c0 + e / b) * b] = make_double2((e % b) == (e / b) ? 1.0 : 0.0, 0.0);
+}
+
+// Z[i + j b] += Y[(k0 + i) + j ldy], j < cols
+__global__ void gj_add_rows_kernel(double2* __restrict__ Z, int b, int64_t cols, const double2* __restrict__ Y,
+                                   int64_t ldy, int64_t k0) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < b * cols;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % b, j = e / b;
+    const double2 y = Y[(k0 + i) + j * ldy];
+    Z[e] = make_double2(Z[e].x + y.x, Z[e].y + y.y);
+  }
+}
+
+// ---- fallback: unblocked Gauss-Jordan with partial pivoting (column k) ----
+// pivot = argmax_{i >= k} |W[i,k]| (ties: smallest i), rows k and pivot swapped,
+// row k scaled by 1/pivot (W[k,k] keeps the pivot until gjp_column_kernel)
+__global__ void __launch_bounds__(1024) gjp_pivot_kernel(double2* __restrict__ W, int64_t ldw, int64_t n, int64_t k,
+                                                        int* __restrict__ piv, double2* __restrict__ ipiv,
+                                                        int* __restrict__ bad) {
+  __shared__ double sv[32];
+  __shared__ int64_t si[32];
+  __shared__ int64_t sp;
+  double best = -1.0;
+  int64_t bi = n;
+  for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) {
+    const double2 v = W[i + k * ldw];
+    const double m = v.x * v.x + v.y * v.y;
+    if (m > best) { best = m; bi = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_down_sync(0xffffffffu, best, o);
+    const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
+    if (!(best > 0.0)) { *bad = 2; bi = k; }
+    piv[k] = static_cast<int>(bi);
+    sp = bi;
+  }
+  __syncthreads();
+  const int64_t p = sp;
+  const double2 pv = W[p + k * ldw];
+  const double2 ip = gj_inv(pv);
+  __syncthreads();  // every thread read the pivot before the swap moves it
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    double2 vk = W[k + j * ldw];
+    const double2 vp = W[p + j * ldw];
+    if (p != k) W[p + j * ldw] = vk;
+    vk = vp;
+    W[k + j * ldw] = j == k ? vk : gj_mul(vk, ip);
+  }
+  if (threadIdx.x == 0) *ipiv = ip;
+}
+// W[i,j] -= W[i,k] W[k,j] for i, j != k (row k already scaled)
+__global__ void gjp_eliminate_kernel(double2* __restrict__ W, int64_t ldw, int64_t n, int64_t k) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    if (i == k || j == k) continue;
+    const double2 f = gj_mul(W[i + k * ldw], W[k + j * ldw]);
+    W[i + j * ldw] = make_double2(W[i + j * ldw].x - f.x, W[i + j * ldw].y - f.y);
+  }
+}
+// column k: W[i,k] = -W[i,k] / pivot, W[k,k] = 1 / pivot
+__global__ void gjp_column_kernel(double2* __restrict__ W, int64_t ldw, int64_t n, int64_t k,
+                                  const double2* __restrict__ ipiv) {
+  const double2 ip = *ipiv;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i == k) W[k + k * ldw] = ip;
+    else {
+      const double2 f = gj_mul(W[i + k * ldw], ip);
+      W[i + k * ldw] = make_double2(-f.x, -f.y);
+    }
+  }
+}
+// undo the row interchanges: columns k and piv[k] swapped, k = n-1 .. 0 (one thread per row)
+__global__ void gjp_unscramble_kernel(double2* __restrict__ W, int64_t ldw, int64_t n, const int* __restrict__ piv) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    for (int64_t k = n - 1; k >= 0; --k) {
+      const int64_t p = piv[k];
+      if (p != k) {
+        const double2 t = W[i + k * ldw];
+        W[i + k * ldw] = W[i + p * ldw];
+        W[i + p * ldw] = t;
+      }
+    }
+}
+
 // A (lda) is read only; Ainv (ldi) receives A^{-1}.
 struct HermInverse {
-  cusolverDnHandle_t solver = nullptr;
-  DevBuf<double2> tmp, work;
-  DevBuf<int> info, piv;
-  HermInverse() = default;
-  HermInverse(const HermInverse&) = delete;
-  HermInverse& operator=(const HermInverse&) = delete;
-  ~HermInverse() {
-    if (solver) cusolverDnDestroy(solver);
-  }
+  static constexpr int NB = 64;
+  DevBuf<double2> w, y, lall, lp, lh, z, ipiv;
+  DevBuf<double> partial;
+  DevBuf<int> bad, piv;
+  HostBuf<int> h_bad;
   void operator()(liecl_b200_ctx* ctx, const double2* A, int64_t lda, int64_t n, double2* Ainv, int64_t ldi) {
     if (n == 0) return;
-    if (!solver && cusolverDnCreate(&solver) != CUSOLVER_STATUS_SUCCESS) throw Error(LIECL_B200_CUDA, "cusolverDnCreate");
-    cusolverDnSetStream(solver, ctx->stream);
-    const int N = static_cast<int>(n);
-    tmp.ensure(static_cast<size_t>(n * n));
-    info.ensure(1);
-    auto* a = reinterpret_cast<cuDoubleComplex*>(tmp.p);
-    auto* b = reinterpret_cast<cuDoubleComplex*>(Ainv);
-    auto load = [&] {
-      CU(cudaMemcpy2DAsync(tmp.p, n * sizeof(double2), A, lda * sizeof(double2), n * sizeof(double2), n,
-                           cudaMemcpyDeviceToDevice, ctx->stream));
-      identity_kernel<<<static_cast<unsigned>(std::min<int64_t>((n * n + 255) / 256, 4096)), 256, 0, ctx->stream>>>(
-          Ainv, ldi, n);
+    cudaStream_t st = ctx->stream;
+    const int64_t nblk = (n + NB - 1) / NB;
+    w.ensure(static_cast<size_t>(n * n));
+    y.ensure(static_cast<size_t>(n * n));
+    lall.ensure(static_cast<size_t>(nblk * NB * NB));
+    lp.ensure(static_cast<size_t>(n * NB));
+    lh.ensure(static_cast<size_t>(n * NB));
+    z.ensure(static_cast<size_t>(n * NB));
+    partial.ensure(static_cast<size_t>(((n + zg::BM - 1) / zg::BM) * n));
+    bad.ensure(1);
+    h_bad.ensure(1);
+    constexpr int kL = NB * NB * 16;  // one 64 x 64 complex block in shared memory
+    func_attr_once(gj_chol_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL);
+    func_attr_once(gj_trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kL);
+    func_attr_once(gj_solve_cols_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kL);
+    func_attr_once(gj_solve_cols_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kL);
+    auto read_bad = [&] {
+      CU(cudaMemcpyAsync(h_bad.p, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      return h_bad.p[0];
+    };
+    const auto grid = [](int64_t e) { return static_cast<unsigned>(std::min<int64_t>((e + 255) / 256, 4096)); };
+    const auto blocks128 = [](int64_t e) { return static_cast<unsigned>((e + 127) / 128); };
+    CU(cudaMemcpy2DAsync(w.p, n * sizeof(double2), A, lda * sizeof(double2), n * sizeof(double2), n,
+                         cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    // 1. Cholesky: W's strictly-lower blocks become L's, the diagonal blocks go to lall
+    for (int64_t kb = 0; kb < nblk; ++kb) {
+      const int64_t k0 = kb * NB;
+      const int b = static_cast<int>(std::min<int64_t>(NB, n - k0));
+      const int64_t m = n - k0 - b;
+      double2* L = lall.p + kb * NB * NB;
+      gj_chol_block_kernel<<<1, 256, b * b * 16, st>>>(w.p, n, k0, b, L, bad.p);
       launched(ctx);
-    };
-    auto read_info = [&] {
-      int v = 0;
-      CU(cudaMemcpyAsync(&v, info.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      CU(cudaStreamSynchronize(ctx->stream));
-      return v;
-    };
-    load();
-    int lwork = 0;
-    if (cusolverDnZpotrf_bufferSize(solver, CUBLAS_FILL_MODE_LOWER, N, a, N, &lwork) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(LIECL_B200_CUDA, "cusolverDnZpotrf_bufferSize");
-    work.ensure(static_cast<size_t>(std::max(lwork, 1)));
-    if (cusolverDnZpotrf(solver, CUBLAS_FILL_MODE_LOWER, N, a, N, reinterpret_cast<cuDoubleComplex*>(work.p), lwork,
-                         info.p) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(LIECL_B200_CUDA, "cusolverDnZpotrf");
-    ctx->kernels += 1;
-    if (read_info() == 0) {
-      if (cusolverDnZpotrs(solver, CUBLAS_FILL_MODE_LOWER, N, N, a, N, b, static_cast<int>(ldi), info.p) !=
-          CUSOLVER_STATUS_SUCCESS)
-        throw Error(LIECL_B200_CUDA, "cusolverDnZpotrs");
-      ctx->kernels += 1;
+      if (m == 0) break;
+      gj_trsm_rows_kernel<<<blocks128(m), 128, b * b * 16, st>>>(w.p, n, k0 + b, m, k0, b, L);  // L21 in place
+      launched(ctx);
+      double2* l21 = w.p + (k0 + b) + k0 * n;
+      CU(cudaMemcpy2DAsync(lp.p, m * sizeof(double2), l21, n * sizeof(double2), m * sizeof(double2), b,
+                           cudaMemcpyDeviceToDevice, st));
+      gj_conj_transpose_kernel<<<grid(m * b), 256, 0, st>>>(lp.p, m, b, lh.p);  // L21^H (b x m)
+      launched(ctx);
+      double2* a22 = w.p + (k0 + b) + (k0 + b) * n;
+      gemm_subtract(ctx, lp.p, b, m, lh.p, a22, static_cast<int>(m), a22, partial.p, m, n);  // A22 -= L21 L21^H
+    }
+    if (read_bad() == 0) {
+      // 2. L Y = I (Y lower triangular: block row K spans columns [0, k0 + b))
+      for (int64_t kb = 0; kb < nblk; ++kb) {
+        const int64_t k0 = kb * NB;
+        const int b = static_cast<int>(std::min<int64_t>(NB, n - k0));
+        const int64_t cols = k0 + b;
+        if (k0 > 0) gemm_mc_store(ctx, w.p + k0, n, b, k0, y.p, n, static_cast<int>(k0), z.p, b, -1.0);
+        gj_identity_cols_kernel<<<1, 256, 0, st>>>(z.p, b, k0);
+        launched(ctx);
+        gj_solve_cols_kernel<true><<<blocks128(cols), 128, b * b * 16, st>>>(z.p, b, cols, lall.p + kb * NB * NB);
+        launched(ctx);
+        CU(cudaMemcpy2DAsync(y.p + k0, n * sizeof(double2), z.p, b * sizeof(double2), b * sizeof(double2), cols,
+                             cudaMemcpyDeviceToDevice, st));
+        if (cols < n)
+          CU(cudaMemset2DAsync(y.p + k0 + cols * n, n * sizeof(double2), 0, b * sizeof(double2), n - cols, st));
+      }
+      // 3. L^H X = Y, bottom-up, X = Ainv
+      for (int64_t kb = nblk - 1; kb >= 0; --kb) {
+        const int64_t k0 = kb * NB;
+        const int b = static_cast<int>(std::min<int64_t>(NB, n - k0));
+        const int64_t m = n - k0 - b;
+        if (m > 0)  // Z = -L[I,K]^H X[I,:]
+          gemm_project(ctx, w.p + (k0 + b) + k0 * n, b, m, Ainv + (k0 + b), static_cast<int>(n), z.p, -1.0, n, ldi);
+        else
+          CU(cudaMemsetAsync(z.p, 0, static_cast<size_t>(b * n) * sizeof(double2), st));
+        gj_add_rows_kernel<<<grid(b * n), 256, 0, st>>>(z.p, b, n, y.p, n, k0);
+        launched(ctx);
+        gj_solve_cols_kernel<false><<<blocks128(n), 128, b * b * 16, st>>>(z.p, b, n, lall.p + kb * NB * NB);
+        launched(ctx);
+        CU(cudaMemcpy2DAsync(Ainv + k0, ldi * sizeof(double2), z.p, b * sizeof(double2), b * sizeof(double2), n,
+                             cudaMemcpyDeviceToDevice, st));
+      }
       return;
     }
-    load();  // not positive definite: LU
-    if (cusolverDnZgetrf_bufferSize(solver, N, N, a, N, &lwork) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(LIECL_B200_CUDA, "cusolverDnZgetrf_bufferSize");
-    work.ensure(static_cast<size_t>(std::max(lwork, 1)));
+    // not numerically positive definite: pivoted Gauss-Jordan on a fresh copy
+    CU(cudaMemcpy2DAsync(Ainv, ldi * sizeof(double2), A, lda * sizeof(double2), n * sizeof(double2), n,
+                         cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
     piv.ensure(static_cast<size_t>(n));
-    if (cusolverDnZgetrf(solver, N, N, a, N, reinterpret_cast<cuDoubleComplex*>(work.p), piv.p, info.p) !=
-            CUSOLVER_STATUS_SUCCESS ||
-        cusolverDnZgetrs(solver, CUBLAS_OP_N, N, N, a, N, piv.p, b, static_cast<int>(ldi), info.p) !=
-            CUSOLVER_STATUS_SUCCESS)
-      throw Error(LIECL_B200_CUDA, "cuSOLVER LU refresh failed");
-    ctx->kernels += 2;
-    CU(cudaStreamSynchronize(ctx->stream));
+    ipiv.ensure(1);
+    const unsigned g_el = static_cast<unsigned>(std::min<int64_t>((n * n + 255) / 256, 8192));
+    const unsigned g_n = grid(n);
+    for (int64_t k = 0; k < n; ++k) {
+      gjp_pivot_kernel<<<1, 1024, 0, st>>>(Ainv, ldi, n, k, piv.p, ipiv.p, bad.p);
+      launched(ctx);
+      gjp_eliminate_kernel<<<g_el, 256, 0, st>>>(Ainv, ldi, n, k);
+      launched(ctx);
+      gjp_column_kernel<<<g_n, 256, 0, st>>>(Ainv, ldi, n, k, ipiv.p);
+      launched(ctx);
+    }
+    gjp_unscramble_kernel<<<g_n, 256, 0, st>>>(Ainv, ldi, n, piv.p);
+    launched(ctx);
+    if (read_bad() == 2) throw Error(LIECL_B200_DEGENERACY, "Gram matrix is singular: no inverse to refresh");
   }
 };
 
@@ -376,7 +648,7 @@ private:
   }
 
   // GramState::refresh (R:src/closure.cpp:89-95): A^{-1} recomputed from A
-  // (Cholesky; A is Hermitian positive definite while the basis is independent)
+  // (HermInverse; A is Hermitian positive definite while the basis is independent)
   void refresh() { inverse_(ctx_, A_.p, ld(), n_, Ainv_.p, ld()); }
 
   liecl_b200_ctx* ctx_;

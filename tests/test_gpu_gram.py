@@ -145,12 +145,16 @@ def test_pauli_sums_matrix_inversion_matches_reference(ref_exact, family, n):
 def test_pauli_sums_matrix_inversion_breaks_down_like_the_reference(ref_exact, family, n):
     """On these closures the reference's own one-pass Alg. 2 residual cannot
     resolve the Schur complement: it raises
-    DegeneracyError, and so does the device path (where exactly is decided by
-    rounding)."""
+    DegeneracyError. The device path breaks down too, under the reference's
+    contract; where, and so which of the reference's two breakdown errors
+    fires first, is decided by rounding (spin_glass_hva n=3: the degenerate
+    accepts reach the d^2 cap before a Schur complement falls below the floor
+    with the hand-written Cholesky refresh; cuSOLVER's refresh in round 1 hit
+    the floor first)."""
     off, x, z, c = ref_exact.build_generators(family, n)
     with pytest.raises(Exception, match="numerically degenerate"):
         ref_exact.closure_pauli(off, x, z, c, n, method="matrix-inversion", tol=1e-10)
-    with pytest.raises(liecl.DegeneracyError):
+    with pytest.raises((liecl.DegeneracyError, liecl.CapacityError)):
         liecl.closure_pauli_sums_arrays(off, x, z, c, n, MI, liecl.ClosureConfig(tolerance=1e-10))
 
 
