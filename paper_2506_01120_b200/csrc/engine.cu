@@ -24,9 +24,9 @@
 // The Pauli single-string path (pauli.cuh) is bit-exact and runs frontier
 // batches of all available pairs.
 #include <cooperative_groups.h>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_segmented_sort.cuh>
 #include <cudaTypedefs.h>
+#include <dlfcn.h>  // at global scope: shard.cuh is included inside the anonymous namespace
+#include <nccl.h>
 
 #include <algorithm>
 #include <charconv>
@@ -56,6 +56,7 @@
 #include "pauli.cuh"
 #include "pauli_sum.cuh"
 #include "scan.cuh"
+#include "sort.cuh"
 #include "tiny.cuh"
 #include "vecops.cuh"
 #include "zgemm_dmma.cuh"

@@ -743,13 +743,30 @@ template <class K> inline size_t fused_smem_bytes(int hc, int n_limit) {
 namespace liecl_b200 {
 namespace psum {
 
-// wide keys: the (z, x) order by two stable LSD passes over the 64-bit words;
-// out[i] = word (0: x, 1: z) of key[perm[i]] (perm null: identity)
-__global__ void wide_words_kernel(const WKey* __restrict__ key, const unsigned* __restrict__ perm, int n, int word,
-                                  unsigned long long* __restrict__ out) {
+// sort words of the merge's multi-pass path (sum_engine.cuh merge): word w of
+// the key at input position perm[i] (wide keys: 0 = x, 1 = z; narrow keys:
+// the packed key itself)
+template <class K>
+__global__ void key_words_kernel(const K* __restrict__ key, const unsigned* __restrict__ perm, int n, int word,
+                                 unsigned long long* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const WKey k = key[perm ? perm[i] : i];
-    out[i] = word ? k.z : k.x;
+    const K k = key[perm ? perm[i] : i];
+    if constexpr (std::is_same_v<K, WKey>) out[i] = word ? k.z : k.x;
+    else out[i] = static_cast<unsigned long long>(k);
+  }
+}
+// the segment holding input position perm[i]
+__global__ void seg_words_kernel(const int* __restrict__ off, int nseg, const unsigned* __restrict__ perm, int n,
+                                 unsigned long long* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int p = static_cast<int>(perm[i]);
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off[mid] <= p) lo = mid;
+      else hi = mid - 1;
+    }
+    out[i] = static_cast<unsigned long long>(lo);
   }
 }
 template <class K>

@@ -282,6 +282,17 @@ private:
     need(temp_, bytes);
   }
 
+  // (kout, vout) = (kin, vin) stably sorted on the keys' low end_bit bits (sort.cuh)
+  void sort_pairs(const unsigned long long* kin, unsigned long long* kout, const unsigned* vin, unsigned* vout, int n,
+                  int end_bit) {
+    ensure_temp(sort::workspace_bytes(n));
+    Stage st_s(this, "sort");
+    int k = 0;
+    sort::pairs(kin, kout, vin, vout, n, end_bit, temp_.p, ctx_->stream, k);
+    ctx_->kernels += k;
+    CU(cudaGetLastError());
+  }
+
   // int exclusive sum of n flags -> pos (hand-written scan, scan.cuh); returns the total
   int scan_flags(const int* flag, int* pos, int n) {
     Stage st_sc(this, "scan");
@@ -328,62 +339,42 @@ private:
     int segbits = 1;
     while ((1ll << segbits) < nseg) ++segbits;
     const int end_bit = segbits + kbits + 1;
-    size_t bytes = 0;
     if (end_bit <= 64) {
       // one stable radix sort of (segment | invalid | key) over end_bit bits
       need(ck_, n);
       need(cks_, n);
       psum::combine_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, n, key, pauli_q, kbits, ck_.p);
       launched(ctx_);
-      CU(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ck_.p, cks_.p, idx_.p, is_.p, n, 0, end_bit, ctx_->stream));
-      ensure_temp(bytes);
-      {
-        Stage st_s(this, "radixsort");
-        CU(cub::DeviceRadixSort::SortPairs(temp_.p, bytes, ck_.p, cks_.p, idx_.p, is_.p, n, 0, end_bit,
-                                           ctx_->stream));
-      }
+      sort_pairs(ck_.p, cks_.p, idx_.p, is_.p, n, end_bit);
       psum::split_kernel<<<grid(n), 256, 0, ctx_->stream>>>(cks_.p, n, pauli_q, kbits, ks_.p, seg_.p);
       launched(ctx_), launched(ctx_);
-    } else if constexpr (std::is_same_v<K, psum::WKey>) {
-      // wide keys: the (z, x) order within segments by two stable passes,
-      // x first; index keys (pauli_q == 0) sort by x alone
+    } else {
+      // the key does not fit one 64-bit composite: stable passes from the
+      // least significant word up (wide keys: x, then z; narrow: the key),
+      // then one over the segment of each term's input position. Unmarked
+      // words stay below 2^q, the marker is all ones: q + 1 bits order them.
       need(ck_, n);
       need(cks_, n);
       need(is1_, n);
-      const int passes = pauli_q > 0 ? 2 : 1;
-      const unsigned* perm = nullptr;
-      unsigned* dst[2] = {passes == 2 ? is1_.p : is_.p, is_.p};
-      const unsigned* src[2] = {idx_.p, is1_.p};
-      for (int w = 0; w < passes; ++w) {
-        psum::wide_words_kernel<<<grid(n), 256, 0, ctx_->stream>>>(key, perm, n, w, ck_.p);
+      constexpr bool wide = std::is_same_v<K, psum::WKey>;
+      const int words = (wide && pauli_q > 0) ? 2 : 1;
+      const int wbits = !wide ? 64 : std::min(64, (pauli_q > 0 ? pauli_q : kbits) + 1);
+      const unsigned* perm = nullptr;  // identity
+      unsigned* pp[2] = {is_.p, is1_.p};
+      int cur = (words & 1) ? 1 : 0;   // words + 1 sorts in all: the last one writes is_
+      for (int w = 0; w < words; ++w) {
+        psum::key_words_kernel<K><<<grid(n), 256, 0, ctx_->stream>>>(key, perm, n, w, ck_.p);
         launched(ctx_);
-        bytes = 0;
-        CU(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, ck_.p, cks_.p, src[w], dst[w], n, nseg, off,
-                                                     off + 1, ctx_->stream));
-        ensure_temp(bytes);
-        {
-          Stage st_s(this, "segsort");
-          CU(cub::DeviceSegmentedSort::StableSortPairs(temp_.p, bytes, ck_.p, cks_.p, src[w], dst[w], n, nseg, off,
-                                                       off + 1, ctx_->stream));
-        }
-        launched(ctx_);
-        perm = dst[w];
+        sort_pairs(ck_.p, cks_.p, perm ? perm : idx_.p, pp[cur], n, wbits);
+        perm = pp[cur];
+        cur ^= 1;
       }
+      psum::seg_words_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, perm, n, ck_.p);
+      launched(ctx_);
+      sort_pairs(ck_.p, cks_.p, perm, pp[cur], n, segbits);
       psum::gather_keys_kernel<<<grid(n), 256, 0, ctx_->stream>>>(key, is_.p, n, ks_.p);
       psum::seg_of_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, n, seg_.p);
       launched(ctx_), launched(ctx_);
-    } else {
-      CU(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off, off + 1,
-                                                   ctx_->stream));
-      ensure_temp(bytes);
-      {
-        Stage st_s(this, "segsort");
-        CU(cub::DeviceSegmentedSort::StableSortPairs(temp_.p, bytes, key, ks_.p, idx_.p, is_.p, n, nseg, off,
-                                                     off + 1, ctx_->stream));
-      }
-      launched(ctx_);
-      psum::seg_of_kernel<<<grid(n), 256, 0, ctx_->stream>>>(off, nseg, n, seg_.p);
-      launched(ctx_);
     }
     psum::heads_kernel<<<grid(n), 256, 0, ctx_->stream>>>(ks_.p, seg_.p, n, flag_.p);
     launched(ctx_);
