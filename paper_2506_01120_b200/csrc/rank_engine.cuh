@@ -21,8 +21,8 @@
 // sqrt(n+1); the last row of T is rho e_n, so sigma_min(T) <= rho; and with
 // T^{-1} = [[R^{-1}, -R^{-1} beta / rho], [0, 1/rho]] and |beta| <= 1,
 //   sigma_min(T) >= 1 / sqrt(F + (F + 1) / rho^2),   F = ||R^{-1}||_F^2,
-// where F is kept exactly up to rounding on the host (an O(n^2)
-// back-substitution per accept). A candidate is dependent if rho < thr / 8,
+// where F is kept exactly up to rounding (an O(n^2) back-substitution per
+// accept, rank_backsolve_kernel). A candidate is dependent if rho < thr / 8,
 // independent if that lower bound >= 8 thr sqrt(n+1) -- both a factor 8
 // clear of the threshold, where the Jacobi SVD's rounding (~m eps sigma_max)
 // cannot reach -- and otherwise goes to the Jacobi kernel as before.
@@ -152,6 +152,86 @@ __global__ void rank_append_r_kernel(double2* __restrict__ R, int64_t ldr, int n
     R[i + static_cast<int64_t>(n) * ldr] = i < n ? beta[i] : make_double2(*rho, 0.0);
 }
 
+// xx[slot] = ||R^{-1} beta_j||^2, j = sel ? sel[slot] : slot: back-substitution
+// on the upper-triangular R (column-major, ld ldr), one CTA per column of
+// beta, x in xs (n per slot). Block rows of 32 from the bottom: the diagonal
+// block is solved by one warp out of shared memory (one shuffle per step),
+// the rows above take x_k -= sum_c R[k, i0 + c] x_c with R read down its
+// columns (coalesced).
+__global__ void __launch_bounds__(256)
+rank_backsolve_kernel(const double2* __restrict__ R, int64_t ldr, int n, const double2* __restrict__ beta, int64_t ldb,
+                      const int* __restrict__ sel, double2* __restrict__ xs, double* __restrict__ xx) {
+  __shared__ double2 s_blk[32][33];
+  __shared__ double2 s_x[32];
+  __shared__ double s_red[8];
+  const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int j = sel ? sel[slot] : slot;
+  double2* x = xs + static_cast<int64_t>(slot) * n;
+  for (int i = tid; i < n; i += blockDim.x) x[i] = beta[static_cast<int64_t>(j) * ldb + i];
+  __syncthreads();
+  for (int i1 = n; i1 > 0; i1 -= 32) {
+    const int i0 = i1 > 32 ? i1 - 32 : 0, w = i1 - i0;
+    for (int e = tid; e < w * w; e += blockDim.x) {
+      const int r = e % w, c = e / w;
+      s_blk[r][c] = R[(i0 + r) + static_cast<int64_t>(i0 + c) * ldr];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double2 v = lane < w ? x[i0 + lane] : make_double2(0.0, 0.0);
+      for (int c = w - 1; c >= 0; --c) {
+        if (lane == c) {  // v / R[c, c]
+          const double2 dg = s_blk[c][c];
+          const double den = dg.x * dg.x + dg.y * dg.y;
+          v = make_double2((v.x * dg.x + v.y * dg.y) / den, (v.y * dg.x - v.x * dg.y) / den);
+        }
+        const double xr = __shfl_sync(0xffffffffu, v.x, c), xi = __shfl_sync(0xffffffffu, v.y, c);
+        if (lane < c) {
+          const double2 a = s_blk[lane][c];
+          v.x -= a.x * xr - a.y * xi;
+          v.y -= a.x * xi + a.y * xr;
+        }
+      }
+      if (lane < w) {
+        x[i0 + lane] = v;
+        s_x[lane] = v;
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < i0; k += blockDim.x) {
+      double2 acc = x[k];
+      for (int c = 0; c < w; ++c) {
+        const double2 a = R[k + static_cast<int64_t>(i0 + c) * ldr], b = s_x[c];
+        acc.x -= a.x * b.x - a.y * b.y;
+        acc.y -= a.x * b.y + a.y * b.x;
+      }
+      x[k] = acc;
+    }
+    __syncthreads();
+  }
+  double part = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) part += x[i].x * x[i].x + x[i].y * x[i].y;
+  part = warp_sum(part);
+  if (lane == 0) s_red[warp] = part;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) t += s_red[q];
+    xx[slot] = t;
+  }
+}
+
+// squared row norms of R after the column (beta, rho) joins: rows2[i] +=
+// |beta_i|^2, rows2[n] = rho^2; *rmax2 = the largest so far (non-negative
+// doubles order like their bit patterns)
+__global__ void rank_rows2_kernel(const double2* __restrict__ beta, const double* __restrict__ rho, int n,
+                                  double* __restrict__ rows2, unsigned long long* __restrict__ rmax2) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+    const double v = i < n ? rows2[i] + beta[i].x * beta[i].x + beta[i].y * beta[i].y : rho[0] * rho[0];
+    rows2[i] = v;
+    atomicMax(rmax2, static_cast<unsigned long long>(__double_as_longlong(v)));
+  }
+}
+
 class RankEngine {
 public:
   RankEngine(liecl_b200_ctx* ctx, int d, const liecl_b200_config& cfg)
@@ -176,7 +256,7 @@ public:
     partial_.ensure(static_cast<size_t>(((D_ + zg::BM - 1) / zg::BM) * bmax_));
     rn_.ensure(bmax_); hn_.ensure(bmax_); nul_.ensure(bmax_); ind_.ensure(bmax_); smin_.ensure(bmax_);
     smax_.ensure(bmax_);
-    h_hn_.ensure(bmax_); h_nul_.ensure(bmax_); h_ind_.ensure(bmax_); h_one_.ensure(2);
+    h_hn_.ensure(bmax_); h_nul_.ensure(bmax_); h_ind_.ensure(bmax_); h_one_.ensure(4);
   }
 
   int64_t size() const { return n_; }
@@ -271,6 +351,14 @@ private:
       std::swap(R_.p, nb.p);
       std::swap(R_.n, nb.n);
     }
+    {  // squared row norms of R: n_ live entries
+      DevBuf<double> nb;
+      nb.ensure(static_cast<size_t>(nc + 1));
+      if (n_ > 0) CU(cudaMemcpyAsync(nb.p, rows2_.p, n_ * sizeof(double), cudaMemcpyDeviceToDevice, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));
+      std::swap(rows2_.p, nb.p);
+      std::swap(rows2_.n, nb.n);
+    }
     grow1(P1_, static_cast<size_t>(nc * bmax_), P1_.n);
     grow1(P2_, static_cast<size_t>(nc * bmax_), 0);
     vcap_ = nc;
@@ -328,21 +416,18 @@ private:
         amb.push_back(j);
       }
     }
-    // second stage for the few left: x = R^{-1} beta exactly (host
-    // back-substitution, O(n^2)) gives ||T^{-1}||_F^2 = F + (|x|^2 + 1) / rho^2
+    // second stage for the few left: x = R^{-1} beta exactly (back-substitution
+    // on the device, rank_backsolve_kernel, one CTA per candidate) gives ||T^{-1}||_F^2 = F + (|x|^2 + 1) / rho^2
     // and ||T^{-1} e_n|| = sqrt(|x|^2 + 1) / rho, i.e.
     //   1 / sqrt(F + (|x|^2 + 1) / rho^2) <= sigma_min(T) <= rho / sqrt(|x|^2 + 1)
     if (screen_ && !amb.empty() && n_ > 0) {
-      h_bcol_.ensure(static_cast<size_t>(n_) * amb.size());
-      for (size_t q = 0; q < amb.size(); ++q)
-        CU(cudaMemcpyAsync(h_bcol_.p + q * n_, Pacc + static_cast<int64_t>(amb[q]) * n_, n_ * sizeof(double2),
-                           cudaMemcpyDeviceToHost, ctx_->stream));
-      CU(cudaStreamSynchronize(ctx_->stream));
+      h_xx_.ensure(amb.size());
+      solve_norm2(Pacc, n_, amb.data(), static_cast<int>(amb.size()), h_xx_.p);
       std::vector<int> rest;
       for (size_t q = 0; q < amb.size(); ++q) {
         const int j = amb[q];
         const double r = h_rho_.p[j];
-        const double xx = solve_norm2(h_bcol_.p + q * n_);
+        const double xx = h_xx_.p[q];
         if (r / std::sqrt(xx + 1.0) < thr * smax_lo / 8.0) h_ind_.p[j] = 0;
         else if (r > 0.0 && 1.0 / std::sqrt(finv_ + (xx + 1.0) / (r * r)) >= 8.0 * thr * smax_hi) h_ind_.p[j] = 1;
         else rest.push_back(j);
@@ -475,13 +560,26 @@ private:
   // with the CGS2 residual (rho = 0 cannot be accepted: sigma_min <= rho)
   void accept(const double2* h, const double2* resid, const double2* beta, const double* rho) {
     CU(cudaMemcpyAsync(B_.p + n_ * D_, h, D_ * sizeof(double2), cudaMemcpyDeviceToDevice, ctx_->stream));
-    CU(cudaMemcpyAsync(h_one_.p, rho, sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
-    h_beta_.ensure(static_cast<size_t>(std::max<int64_t>(n_, 1)));
-    if (n_ > 0)
-      CU(cudaMemcpyAsync(h_beta_.p, beta, n_ * sizeof(double2), cudaMemcpyDeviceToHost, ctx_->stream));
+    // F = ||R^{-1}||_F^2 after the column (beta, rho) joins R:
+    // F += (||R^{-1} beta||^2 + 1) / rho^2; the largest row norm of R bounds
+    // sigma_max(R) from below. Both on the device; three doubles come back.
+    acc_.ensure(4);
+    if (n_ == 0) CU(cudaMemsetAsync(acc_.p, 0, 4 * sizeof(double), ctx_->stream));
+    if (n_ > 0) {
+      xs_.ensure(static_cast<size_t>(n_));
+      rank_backsolve_kernel<<<1, 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), beta, n_, nullptr, xs_.p,
+                                                         acc_.p);
+      launched(ctx_);
+    }
+    rank_rows2_kernel<<<grid_for(n_ + 1), 256, 0, ctx_->stream>>>(
+        beta, rho, static_cast<int>(n_), rows2_.p, reinterpret_cast<unsigned long long*>(acc_.p + 1));
+    launched(ctx_);
+    CU(cudaMemcpyAsync(acc_.p + 2, rho, sizeof(double), cudaMemcpyDeviceToDevice, ctx_->stream));
+    CU(cudaMemcpyAsync(h_one_.p, acc_.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
     CU(cudaStreamSynchronize(ctx_->stream));
-    const double r = h_one_.p[0];
-    update_finv(h_beta_.p, r);
+    const double r = h_one_.p[2];
+    finv_ += ((n_ > 0 ? h_one_.p[0] : 0.0) + 1.0) / (r * r);
+    smax_row_ = std::sqrt(h_one_.p[1]);
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((D_ + 255) / 256, 256));
     append_scaled_kernel<<<blocks, 256, 0, ctx_->stream>>>(resid, 1.0 / r, D_, V_.p + n_ * D_, nullptr, nullptr);
     rank_append_r_kernel<<<grid_for(n_ + 1), 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), beta, rho);
@@ -490,39 +588,21 @@ private:
     ++st_.accepted;
   }
 
-  // |R^{-1} beta|^2 by back-substitution on the host copy of R
-  double solve_norm2(const double2* beta) const {
-    using cd = std::complex<double>;
-    const int64_t n = n_;
-    std::vector<cd> x(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i) x[i] = cd(beta[i].x, beta[i].y);
-    for (int64_t i = n - 1; i >= 0; --i) {
-      cd acc = x[i];
-      for (int64_t k = i + 1; k < n; ++k) acc -= hR_[k][i] * x[k];
-      x[i] = acc / hR_[i][i];
+  // ||R^{-1} beta_j||^2 for the columns j = sel[0..count) of beta (ld ldb) -> out (host)
+  void solve_norm2(const double2* beta, int64_t ldb, const int* sel, int count, double* out) {
+    constexpr int kChunk = 256;  // columns per launch: bounds the x scratch
+    xs_.ensure(static_cast<size_t>(std::min(count, kChunk)) * n_);
+    sel_.ensure(kChunk);
+    xx_.ensure(kChunk);
+    for (int c0 = 0; c0 < count; c0 += kChunk) {
+      const int c = std::min(kChunk, count - c0);
+      CU(cudaMemcpyAsync(sel_.p, sel + c0, c * sizeof(int), cudaMemcpyHostToDevice, ctx_->stream));
+      rank_backsolve_kernel<<<c, 256, 0, ctx_->stream>>>(R_.p, ldr(), static_cast<int>(n_), beta, ldb, sel_.p, xs_.p,
+                                                         xx_.p);
+      launched(ctx_);
+      CU(cudaMemcpyAsync(out + c0, xx_.p, c * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream));
+      CU(cudaStreamSynchronize(ctx_->stream));  // sel (pageable) and out are reused per chunk
     }
-    double xx = 0.0;
-    for (const cd& v : x) xx += std::norm(v);
-    return xx;
-  }
-
-  // F = ||R^{-1}||_F^2 after appending the column (beta, rho) to R:
-  // F += (||R^{-1} beta||^2 + 1) / rho^2 (back-substitution on the host copy
-  // hR_ of the upper-triangular R, one vector per column)
-  void update_finv(const double2* beta, double rho) {
-    using cd = std::complex<double>;
-    const int64_t n = n_;
-    finv_ += (solve_norm2(beta) + 1.0) / (rho * rho);  // hR_[k] = column k, rows 0..k
-    std::vector<cd> col(static_cast<size_t>(n + 1));
-    for (int64_t i = 0; i < n; ++i) col[i] = cd(beta[i].x, beta[i].y);
-    col[n] = cd(rho, 0.0);
-    // row norms of R (lower bounds on sigma_max(R)): the new column adds
-    // |beta_i|^2 to row i, and row n starts at rho^2
-    rows2_.resize(static_cast<size_t>(n + 1), 0.0);
-    for (int64_t i = 0; i < n; ++i) rows2_[i] += std::norm(col[i]);
-    hR_.push_back(std::move(col));
-    rows2_[n] = rho * rho;
-    for (double v : rows2_) smax_row_ = std::max(smax_row_, std::sqrt(v));
   }
 
   liecl_b200_ctx* ctx_;
@@ -535,9 +615,7 @@ private:
   }();
   double finv_ = 0.0;  // ||R^{-1}||_F^2
   double smax_row_ = 0.0;  // largest row norm of R
-  std::vector<double> rows2_;
   bool trace_ = std::getenv("LIECL_B200_TRACE") != nullptr;
-  std::vector<std::vector<std::complex<double>>> hR_;
   int64_t vcap_ = 0;  // basis slots allocated (ld of R)
   bool record_;
   int64_t cap_ = 0, bmax_ = 0, n_ = 0;
@@ -549,9 +627,9 @@ private:
   std::vector<Warning> warns_;
   std::vector<liecl_b200_decision> log_;
   DevBuf<double2> B_, V_, R_, C_, X_, Y_, Yb_, P1_, P2_, W_, Xr_, Pr_;
-  DevBuf<double> partial_, rn_, hn_, smin_, smax_, rnr_;
+  DevBuf<double> partial_, rn_, hn_, smin_, smax_, rnr_, rows2_, acc_, xx_;
+  DevBuf<double2> xs_;
   DevBuf<int> nul_, ind_, indr_, idx_, sel_, jind_;
-  HostBuf<double> h_hn_, h_one_, h_rho_;
-  HostBuf<double2> h_beta_, h_bcol_;
+  HostBuf<double> h_hn_, h_one_, h_rho_, h_xx_;
   HostBuf<int> h_nul_, h_ind_, h_jind_;
 };
