@@ -217,6 +217,35 @@ def test_wide_sums_equal_narrow_relabelled(ref_exact, monkeypatch):
                               small.decision_log["residual_norm"].view(np.uint64))
 
 
+@pytest.mark.parametrize("q,pos", [(30, [0, 7, 13, 21, 26, 29]), (31, [2, 9, 16, 23, 28, 30]), (29, [1, 5, 11, 19, 24, 28])],
+                         ids=["q30", "q31", "q29"])
+def test_narrow_sums_past_64_composite_bits(ref_exact, q, pos, monkeypatch):
+    """Narrow 64-bit keys on 29..31 qubits: segment | marker | 2q string bits no
+    longer fit one 64-bit sort word, so the merge sorts by the key and then by
+    the segment (sum_engine.cuh merge, sort.cuh). Against the 6-qubit closure
+    relabelled (identical bits) and, for the decisions, the reference build."""
+    monkeypatch.setenv("LIECL_B200_SUMS_FUSED", "0")  # every check through the merge pipelines
+    off, x, z, c = ref_exact.build_generators("tfim_hva_open", 6)
+    cfg = liecl.ClosureConfig(tolerance=1e-10, record_log=True, max_dim=4096)
+    small = liecl.closure_pauli_sums_arrays(off, x, z, c, 6, config=cfg)
+    ex, ez = embed_masks(x, pos), embed_masks(z, pos)
+    big = liecl.closure_pauli_sums_arrays(off, ex, ez, c, q, config=cfg)
+    so, sx, sz, sc = small.basis_array
+    bo, bx, bz, bc = big.basis_array
+    assert big.dimension == small.dimension == 36
+    assert np.array_equal(bo, so)
+    assert np.array_equal(bx, embed_masks(sx, pos)) and np.array_equal(bz, embed_masks(sz, pos))
+    assert np.array_equal(bc.view(np.uint64), sc.view(np.uint64))
+    assert np.array_equal(big.decision_log["residual_norm"].view(np.uint64),
+                          small.decision_log["residual_norm"].view(np.uint64))
+    o = ref_exact.closure_pauli(off, ex, ez, c, q, method="orthonorm-dimonly", tol=1e-10, threads=4, max_dim=4096,
+                                basis_cap=4096)
+    assert o.dimension == 36
+    ro, rx, rz, rc = o.basis
+    assert np.array_equal(bo, ro) and np.array_equal(bx, rx) and np.array_equal(bz, rz)
+    assert np.array_equal(bc.view(np.uint64), rc.view(np.uint64))
+
+
 def test_wide_parse_matches_reference(ref_exact):
     """parse_pauli_sum (the reference grammar; from_terms on the device, wide
     keys) on 40 qubits against the reference build."""
