@@ -46,6 +46,22 @@ def test_kernels_use_fp64_tensor_pipe():
     assert "DMMA" in sass  # mma.sync f64 -> DMMA.8x8x4 (no tcgen05 kind::f64 exists)
 
 
+def test_library_is_self_contained():
+    """Every kernel is this repository's: no CUB / cuBLAS / cuSOLVER kernels in
+    the fatbin and no CUDA math library among the dynamic dependencies (the
+    runtime is linked statically, NCCL is resolved with dlopen)."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump") or not shutil.which("readelf"):
+        pytest.skip("cuobjdump / readelf missing")
+    names = subprocess.run(["cuobjdump", "--dump-elf-symbols", native.LIB_PATH], capture_output=True, text=True).stdout
+    for lib in ("cub", "cublas", "cusolver", "thrust"):
+        assert f"N{len(lib)}{lib}" not in names and f"{lib}::" not in names, lib
+    needed = subprocess.run(["readelf", "-d", native.LIB_PATH], capture_output=True, text=True).stdout
+    for lib in ("cublas", "cusolver", "cusparse", "nccl", "cudart"):
+        assert f"lib{lib}" not in needed, lib
+
+
 def test_method_strings_roundtrip():
     for m in liecl.Method:
         assert liecl.method_from_string(liecl.to_string(m)) == m
