@@ -244,12 +244,24 @@ onesweep_kernel(const u64* __restrict__ kin, const unsigned* __restrict__ vin, i
     unsigned before = 0;  // keys of earlier tiles with digit d
     if (tile > 0) {
       st[tile * kBins + d] = kFlagAgg | static_cast<unsigned>(total);
-      for (int64_t t = tile - 1; t >= 0; --t) {
-        unsigned v;
-        do v = st[t * kBins + d];
-        while ((v >> 30) == 0);
-        before += v & kValueMask;
-        if (v & kFlagPrefix) break;
+      // look back kLook tiles per trip: the loads are independent, so a walk
+      // over many still-running predecessors costs one memory latency per
+      // kLook tiles instead of one per tile
+      constexpr int kLook = 8;
+      bool done = false;
+      for (int64_t t = tile - 1; !done; t -= kLook) {
+        unsigned v[kLook];
+#pragma unroll
+        for (int u = 0; u < kLook; ++u) v[u] = t - u >= 0 ? st[(t - u) * kBins + d] : (2u << 30);  // before tile 0: an inclusive prefix of 0
+#pragma unroll
+        for (int u = 0; u < kLook; ++u) {
+          if (!done) {
+            unsigned x = v[u];
+            while ((x >> 30) == 0) x = st[(t - u) * kBins + d];
+            before += x & kValueMask;
+            done = (x & kFlagPrefix) != 0;
+          }
+        }
       }
     }
     st[tile * kBins + d] = kFlagPrefix | (before + static_cast<unsigned>(total));
