@@ -187,7 +187,8 @@ int liecl_b200_closure_pauli(liecl_b200_ctx* ctx, const uint64_t* x, const uint6
  * bit-exact with the reference: same verdicts, decision log, warnings and
  * coefficient bits. Generator i = terms [offsets[i], offsets[i+1]) of
  * (x, z, coef re/im) in PauliSum form (unique strings sorted by (z, x));
- * qubits 1..63 (64-bit keys to 31, 128-bit keys past). Outputs result.basis as basis_offsets (dimension + 1 entries,
+ * qubits 1..64 (64-bit keys to 31, 128-bit keys past; on 64 qubits the single string Y^64 -- the key marker --
+ * raises LIECL_B200_INVALID_INPUT if it occurs as an input term or as a bracket's product). Outputs result.basis as basis_offsets (dimension + 1 entries,
  * dimension <= cap) and its terms (term_cap entries), and, when ortho_offsets
  * != NULL, result.orthonormal_basis likewise. terms_needed[0..1] (basis,
  * orthonormal) and *stats are always written; LIECL_B200_CAPACITY ("output
@@ -227,7 +228,7 @@ int liecl_b200_project_residual_dense(liecl_b200_ctx* ctx, const double* V, int6
  * sums (R:src/closure.cpp:107-162; R:src/operator.cpp:164-181, the PauliSum
  * branch), on the device. The tuple is n sums, terms [offsets[l],
  * offsets[l+1]) of (x, z, coef re/im); h is one sum of h_terms terms; all in
- * PauliSum form (unique strings sorted by (z, x)); qubits 1..63. A result sum
+ * PauliSum form (unique strings sorted by (z, x)); qubits 1..64 (Y^64 refused). A result sum
  * goes to (rx, rz, rcoef) with room for term_cap terms, *out_terms = its size
  * (LIECL_B200_CAPACITY "output buffers too small" when it exceeds term_cap;
  * h_terms + the tuple's total terms always suffices). project_residual and
@@ -263,7 +264,7 @@ int liecl_b200_pauli_from_terms(liecl_b200_ctx* ctx, int64_t n, const uint64_t* 
  * reference's text grammar ("1.5 XIZ - (0,2) YYI + ..."), letter j on qubit
  * j; the terms are merged by from_terms on the device. LIECL_B200_PARSE with
  * the reference's message and the 1-based position in *err_line / *err_col
- * (either may be NULL) on malformed text; the device from_terms takes 1..63 qubits. */
+ * (either may be NULL) on malformed text; the device from_terms takes 1..64 qubits (Y^64 refused). */
 int liecl_b200_parse_pauli_sum(liecl_b200_ctx* ctx, const char* text, int64_t len, uint32_t qubits, uint64_t* x,
                                uint64_t* z, double* coef, int64_t term_cap, int64_t* out_terms, int64_t* err_line,
                                int64_t* err_col);
@@ -275,7 +276,7 @@ int liecl_b200_parse_pauli_sum(liecl_b200_ctx* ctx, const char* text, int64_t le
  * restrict_zero_magnetization (xxz_hva only): from_pauli on the device, then
  * the C(n, n/2) zero-magnetization submatrix, as *dim x *dim complex
  * operators in dense_out (dense_cap doubles). Bit-exact with the reference;
- * Pauli qubits 1..63, dense <= 12. */
+ * Pauli qubits 1..64, dense <= 12. */
 int liecl_b200_realize_generators(liecl_b200_ctx* ctx, int32_t family, uint32_t qubits, uint64_t seed, double delta,
                                   int32_t restrict_zero_magnetization, int32_t dense, int32_t* count,
                                   int64_t* offsets, uint64_t* x, uint64_t* z, double* coef, int64_t term_cap,

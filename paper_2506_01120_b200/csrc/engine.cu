@@ -150,7 +150,7 @@ struct liecl_b200_ctx {
   DevBuf<double2> comm_scratch;  // ... and unpacked operands / result (packed field)
   std::shared_ptr<void> dense_cache, pauli_cache;  // workspaces of the last one-shot closure
   std::shared_ptr<void> sum_cache;                  // the last multi-term Pauli closure (fetch)
-  bool sum_cache_wide = false;                      // ... a SumEngineWide (32..63 qubits)
+  bool sum_cache_wide = false;                      // ... a SumEngineWide (32..64 qubits)
   std::shared_ptr<void> gram_ops;                   // GramState / check_matrix_inversion workspaces
   std::shared_ptr<void> result;                     // the last dense closure (liecl_b200_dense_fetch)
   int result_kind = 0;                              // 1 DenseEngine, 2 GramEngine, 3 RankEngine
@@ -1358,8 +1358,8 @@ int liecl_b200_closure_pauli_sums(liecl_b200_ctx* ctx, const int64_t* offsets, c
     if (!ctx || !offsets || !stats || !terms_needed || !basis_offsets)
       throw Error(LIECL_B200_INVALID_INPUT, "null argument");
     if (ngens <= 0) throw Error(LIECL_B200_INVALID_INPUT, "closure requires a non-empty generator tuple");
-    if (qubits < 1 || qubits > 63)
-      throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..63 qubits");
+    if (qubits < 1 || qubits > 64)
+      throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..64 qubits");
     if (offsets[0] != 0) throw Error(LIECL_B200_INVALID_INPUT, "offsets[0] must be 0");
     for (int i = 0; i < ngens; ++i) {
       if (offsets[i + 1] < offsets[i]) throw Error(LIECL_B200_INVALID_INPUT, "offsets must be non-decreasing");
@@ -1865,10 +1865,10 @@ std::unique_ptr<SumEngineT<K>> pauli_tuple(liecl_b200_ctx* ctx, const int64_t* o
   if (n > 0) e->load_basis(offsets, x, z, coef, n);
   return e;
 }
-// runs f(K{}) with the key type for `qubits`: narrow 1..31, wide 32..63
+// runs f(K{}) with the key type for `qubits`: narrow 1..31, wide 32..64
 template <class F> void with_keys(uint32_t qubits, F&& f) {
-  if (qubits < 1 || qubits > 63)
-    throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..63 qubits");
+  if (qubits < 1 || qubits > 64)
+    throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..64 qubits");
   if (qubits <= 31) f(0ull);
   else f(psum::WKey{});
 }

@@ -41,7 +41,7 @@ constexpr double kDropTolerance = 1e-14;  // R:include/liecl/pauli.hpp:73
 // Every kernel below is a template over the key type K:
 //  * narrow (1..31 qubits): unsigned long long x | z << 32, whose numeric
 //    order is the reference's (z, x) order (PauliStringLess);
-//  * wide (32..63 qubits): WKey {x, z}, ordered by (z, x).
+//  * wide (32..64 qubits): WKey {x, z}, ordered by (z, x).
 // Both reserve all ones as the marker of a commuting product (sorts last) and
 // of a free hash slot; no string of <= 63 qubits reaches it. Index keys (basis
 // element l, the beta merges) live in the same arrays (kfrom_index / kindex).
@@ -97,7 +97,7 @@ template <> __host__ __device__ __forceinline__ WKey kfrom_index<WKey>(int64_t l
 template <class K>
 __global__ void products_kernel(int64_t g0, int cnt, const int* __restrict__ off, const int64_t* __restrict__ boff,
                                 const K* __restrict__ bkey, const C2* __restrict__ bval, K* __restrict__ out_key,
-                                C2* __restrict__ out_val) {
+                                C2* __restrict__ out_val, int* __restrict__ marker_flag) {
   const int p = blockIdx.x;
   if (p >= cnt) return;
   int64_t l, m;
@@ -115,6 +115,7 @@ __global__ void products_kernel(int64_t g0, int cnt, const int* __restrict__ off
       w = cmul(bval[a0 + ia], bval[b0 + ib]);
       w = pauli::apply_phase(cadd(w, w), pauli::phase_exponent(xa, za, xb, zb));
       key = kxor(ka, kb);
+      if (marker_flag && kmarked(key)) *marker_flag = 1;  // 64 qubits: the product is Y^64 (sum_engine.cuh)
     }
     out_key[base + q] = key;
     out_val[base + q] = w;

@@ -22,10 +22,12 @@
 
 template <class K> class SumEngineT {
 public:
-  // 1..31 qubits with narrow keys (x | z << 32), 32..63 with WKey {x, z}
-  // (pauli_sum.cuh); all ones is the key arrays' marker, so 64-qubit sums
-  // (where Y^64 is all ones) are refused
-  static constexpr unsigned kMaxQubits = std::is_same_v<K, psum::WKey> ? 63 : 31;
+  // 1..31 qubits with narrow keys (x | z << 32), 32..64 with WKey {x, z}
+  // (pauli_sum.cuh). All ones is the key arrays' marker: on 64 qubits that is
+  // the string Y^64, so a 64-qubit closure runs unless Y^64 itself turns up
+  // (in an input term or as a bracket's product), which raises
+  // InvalidInputError instead of a wrong answer
+  static constexpr unsigned kMaxQubits = std::is_same_v<K, psum::WKey> ? 64 : 31;
   // gram = true: Alg. 2 (matrix inversion, R:src/closure.cpp:214-265) -- the
   // pool holds the accepted unit brackets B, a check is beta = <B_l, h>,
   // x = A^{-1} beta (device GEMM against the maintained inverse), residual
@@ -35,7 +37,7 @@ public:
       : ctx_(ctx), q_(qubits), keep_(keep_original && !gram), gram_(gram), tol_(cfg.tolerance),
         floor_(cfg.conditioning_floor), interval_(cfg.gram_refresh_interval), record_(cfg.record_log != 0) {
     if (qubits < 1 || qubits > kMaxQubits)
-      throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..63 qubits");
+      throw Error(LIECL_B200_INVALID_INPUT, "the multi-term PauliSum path supports 1..64 qubits");
     if (!(tol_ >= 0.0)) throw Error(LIECL_B200_INVALID_INPUT, "tolerance must be non-negative");
     const uint64_t full = qubits >= 31 ? static_cast<uint64_t>(INT64_MAX) : (1ull << (2 * qubits));
     cap_ = cfg.max_dim ? static_cast<int64_t>(std::min<uint64_t>(cfg.max_dim, full)) : static_cast<int64_t>(full);
@@ -55,6 +57,8 @@ public:
     }
     grow_index(1 << 12);
     need(small_, 4);
+    need(marker_flag_, 1);
+    CU(cudaMemsetAsync(marker_flag_.p, 0, sizeof(int), ctx_->stream));
   }
 
   void print_trace() const {
@@ -96,7 +100,7 @@ public:
 
   void run_impl(const int64_t* goff, const uint64_t* gx, const uint64_t* gz, const double* gc, int ngens) {
     Stage st_run(this, "run");
-    const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
+    const uint64_t kmask = (q_ >= 64) ? ~0ull : ((1ull << q_) - 1);
     const int64_t nt = ngens > 0 ? goff[ngens] : 0;
     if (nt > (int64_t(1) << 30)) throw Error(LIECL_B200_CAPACITY, "generator terms exceed 2^30");
     std::vector<int> hoff(static_cast<size_t>(ngens) + 1);
@@ -105,6 +109,7 @@ public:
     for (int64_t t = 0; t < nt; ++t) {
       if ((gx[t] & ~kmask) || (gz[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
       hkey[t] = psum::kpack<K>(gx[t], gz[t]);
+      refuse_marker(hkey[t]);
     }
     Segs g;
     g.shape(ngens, static_cast<int>(nt));
@@ -277,6 +282,20 @@ private:
     std::swap(b.p, nb.p);
     std::swap(b.n, nb.n);
   }
+  // 64 qubits: Y^64 (x = z = all ones) is the key arrays' marker
+  static void refuse_marker(const K& k) {
+    if (psum::kmarked(k))
+      throw Error(LIECL_B200_INVALID_INPUT,
+                  "the 64-qubit string Y^64 cannot be a term of the multi-term PauliSum path (it is the key marker)");
+  }
+  // a bracket's product was Y^64 (products_kernel raised the flag)
+  void check_marker_flag() {
+    if (q_ < 64) return;
+    if (read_int(marker_flag_.p))
+      throw Error(LIECL_B200_INVALID_INPUT,
+                  "a bracket produced the 64-qubit string Y^64, which the multi-term PauliSum path cannot hold "
+                  "(it is the key marker)");
+  }
   void ensure_temp(size_t bytes) {
     Stage st_t(this, "temp");
     need(temp_, bytes);
@@ -416,7 +435,7 @@ private:
   void upload(const int64_t* off, const uint64_t* x, const uint64_t* z, const double* coef, int nseg, Segs& out) {
     const int64_t t0 = off[0], nt = off[nseg] - off[0];
     if (nt > kMaxItems) throw Error(LIECL_B200_CAPACITY, "sums exceed 2^30 terms");
-    const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
+    const uint64_t kmask = (q_ >= 64) ? ~0ull : ((1ull << q_) - 1);
     std::vector<int> ho(static_cast<size_t>(nseg) + 1);
     for (int p = 0; p <= nseg; ++p) ho[p] = static_cast<int>(off[p] - t0);
     std::vector<K> hk(static_cast<size_t>(std::max<int64_t>(nt, 1)));
@@ -424,6 +443,7 @@ private:
       for (int64_t t = off[p]; t < off[p + 1]; ++t) {
         if ((x[t] & ~kmask) || (z[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
         hk[t - t0] = psum::kpack<K>(x[t], z[t]);
+        refuse_marker(hk[t - t0]);
         if (t > off[p] && !psum::kless(hk[t - 1 - t0], hk[t - t0]))
           throw Error(LIECL_B200_INVALID_INPUT, "sum terms must be unique and sorted by (z, x)");
       }
@@ -983,8 +1003,10 @@ private:
       const K* bkey = keep_ ? okey_.p : vkey_.p;
       const C2* bval = keep_ ? oval_.p : vval_.p;
       Stage st_p(this, "products");
-      psum::products_kernel<<<cnt, 256, 0, ctx_->stream>>>(g0, cnt, poff_.p, bdoff, bkey, bval, pk_.p, pv_.p);
+      psum::products_kernel<<<cnt, 256, 0, ctx_->stream>>>(g0, cnt, poff_.p, bdoff, bkey, bval, pk_.p, pv_.p,
+                                                           q_ >= 64 ? marker_flag_.p : nullptr);
       launched(ctx_);
+      check_marker_flag();
       Segs& h = h_;
       {
         Stage st_c(this, "commutator");
@@ -1085,7 +1107,7 @@ private:
   DevBuf<C2> ev_;
   // batch scratch
   DevBuf<unsigned char> temp_;
-  DevBuf<int> small_, poff_, seg_, flag_, pos_, run_seg_, roff_, keep_flag_, kpos_, boff_;
+  DevBuf<int> marker_flag_, small_, poff_, seg_, flag_, pos_, run_seg_, roff_, keep_flag_, kpos_, boff_;
   DevBuf<long long> cnt_, cpos_, clen_, chpos_, scan_ws_ll_;
   DevBuf<int> scan_ws_;
   DevBuf<unsigned> idx_, is_, is1_;
@@ -1206,11 +1228,12 @@ public:
   // duplicates merged in input order from +0, drop rule, sorted by (z, x))
   void from_terms_one(int64_t n, const uint64_t* x, const uint64_t* z, const double* coef, Segs& out) {
     if (n > kMaxItems) throw Error(LIECL_B200_CAPACITY, "terms exceed 2^30");
-    const uint64_t kmask = (q_ >= 32) ? ~0ull : ((1ull << q_) - 1);
+    const uint64_t kmask = (q_ >= 64) ? ~0ull : ((1ull << q_) - 1);
     std::vector<K> hk(static_cast<size_t>(std::max<int64_t>(n, 1)));
     for (int64_t t = 0; t < n; ++t) {
       if ((x[t] & ~kmask) || (z[t] & ~kmask)) throw Error(LIECL_B200_INVALID_INPUT, "string mask exceeds qubits");
       hk[t] = psum::kpack<K>(x[t], z[t]);
+      refuse_marker(hk[t]);
     }
     Segs raw;
     raw.shape(1, static_cast<int>(n));

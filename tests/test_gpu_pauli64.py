@@ -255,5 +255,55 @@ def test_wide_parse_matches_reference(ref_exact):
     rx, rz, rc = ref_exact.parse_pauli_sum(text, q)
     assert [(t[0].x, t[0].z) for t in got.terms] == list(zip(map(int, rx), map(int, rz)))
     assert np.array_equal(np.array([[t[1].real, t[1].imag] for t in got.terms]).view(np.uint64), rc.view(np.uint64))
+    # 64 qubits parse too; only the string Y^64 (all ones: the key marker) is refused
+    got = liecl.parse_pauli_sum("1.0 " + "X" * 64 + " + 2 " + "Y" * 63 + "Z", 64)
+    rx, rz, rc = ref_exact.parse_pauli_sum("1.0 " + "X" * 64 + " + 2 " + "Y" * 63 + "Z", 64)
+    assert [(t[0].x, t[0].z) for t in got.terms] == list(zip(map(int, rx), map(int, rz)))
     with pytest.raises(liecl.InvalidInputError):
-        liecl.parse_pauli_sum("1.0 " + "X" * 64, 64)  # 64-qubit sums: the key marker
+        liecl.parse_pauli_sum("1.0 " + "Y" * 64, 64)
+
+
+def test_64_qubit_sums_match_reference(ref_exact):
+    """Multi-term sums on all 64 qubits (the reference's limit, R:src/pauli.cpp:391):
+    the catalog's spin-glass generators relabelled onto qubits 0, 31, 63, against
+    the reference build bit for bit."""
+    off, x, z, c = ref_exact.build_generators("spin_glass_hva", 3)
+    pos = [0, 31, 63]
+    ex, ez = embed_masks(x, pos), embed_masks(z, pos)
+    res = liecl.closure_pauli_sums_arrays(off, ex, ez, c, 64, liecl.Method.orthonorm_dimonly,
+                                          liecl.ClosureConfig(tolerance=1e-10, record_log=True, max_dim=4096))
+    o = ref_exact.closure_pauli(off, ex, ez, c, 64, method="orthonorm-dimonly", tol=1e-10, threads=4, max_dim=4096,
+                                basis_cap=4096)
+    assert res.dimension == o.dimension == 63
+    for k in ("commutators_evaluated", "independence_checks", "accepted"):
+        assert getattr(res.stats, k) == o.stats[k], k
+    bo, bx, bz, bc = res.basis_array
+    ro, rx, rz, rc = o.basis
+    assert np.array_equal(bo, ro) and np.array_equal(bx, rx) and np.array_equal(bz, rz)
+    assert np.array_equal(bc.view(np.uint64), rc.view(np.uint64))
+    assert int(bx.max()) >> 63 or int(bz.max()) >> 63  # bit 63 is in use
+
+
+def test_64_qubit_sums_refuse_only_y64():
+    """Y^64 is the key arrays' marker: as an input term, or as the product of a
+    bracket, it raises InvalidInputError instead of giving a wrong result."""
+    one = np.array([1.0, 0.0])
+    off = np.array([0, 1], np.int64)
+    with pytest.raises(liecl.InvalidInputError):  # an input term
+        liecl.closure_pauli_sums_arrays(off, np.array([ALL], np.uint64), np.array([ALL], np.uint64), one.reshape(1, 2),
+                                        64, liecl.Method.orthonorm_dimonly, liecl.ClosureConfig(max_dim=16))
+    # a product: P = X on every qubit with Z on qubit 0 too (Y_0 X_1..X_63), Q = Z on qubits 1..63:
+    # P Q has x = all ones, z = all ones, and they anticommute (63 positions with X against Z)
+    px, pz = ALL, 1
+    qx, qz = 0, ALL & ~1
+    off2 = np.array([0, 1, 2], np.int64)
+    with pytest.raises(liecl.InvalidInputError):
+        liecl.closure_pauli_sums_arrays(off2, np.array([px, qx], np.uint64), np.array([pz, qz], np.uint64),
+                                        np.array([[1.0, 0.0], [1.0, 0.0]]), 64, liecl.Method.orthonorm_dimonly,
+                                        liecl.ClosureConfig(max_dim=16))
+    # an anticommuting pair one qubit narrower closes normally: dimension 3
+    m63 = (1 << 63) - 1
+    r = liecl.closure_pauli_sums_arrays(off2, np.array([m63, 0], np.uint64), np.array([1, m63], np.uint64),
+                                        np.array([[1.0, 0.0], [1.0, 0.0]]), 63, liecl.Method.orthonorm_dimonly,
+                                        liecl.ClosureConfig(max_dim=16))
+    assert r.dimension == 3
