@@ -177,6 +177,12 @@ public:
       throw Error(LIECL_B200_INVALID_INPUT, "set_shards needs a fresh session (before set_basis / check_candidates)");
     if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(LIECL_B200_INVALID_INPUT, "bad shard rank / count");
     loop_shard_range(D_, d_, nranks, rank, lo_, hi_);
+    max_slice_ = 0;  // the widest slice of any rank: batch sizes derived from it agree on every rank
+    for (int r = 0; r < nranks; ++r) {
+      int64_t a, b;
+      loop_shard_range(D_, d_, nranks, r, a, b);
+      max_slice_ = std::max(max_slice_, b - a);
+    }
     red_ = std::move(red);
     loop_shard_ = true;
     nranks_ = nranks;
@@ -186,7 +192,10 @@ public:
     auto bound = [&](int r) {
       if (r <= 0) return int64_t(0);
       if (r >= nranks) return D;
-      return std::min(D, (D * r / nranks) / unit * unit);
+      // the multiple of `unit` nearest to D r / P: the largest slice is at most
+      // half a unit above D / P (rounding down instead left the last rank with
+      // up to a whole extra unit per earlier rank: 586 of 4096 elements at P = 8)
+      return std::min(D / unit * unit, (2 * D * r + nranks * unit) / (2 * nranks * unit) * unit);
     };
     lo = bound(rank);
     hi = bound(rank + 1);
@@ -683,12 +692,26 @@ private:
   // 3.5 waves on 296 slots (measured 13 % slower at one rank), a 4,096 one
   // 6.9 waves. LIECL_B200_SHARD_CHUNKS forces a count (tests: one rank too).
   static constexpr int kMaxShardChunks = 4;
+  // Largest batch of the saturated phase. D-sharded packed loop with a narrow
+  // slice (8 ranks at d = 64: 520 elements = 5 row tiles of K2b): 64 column
+  // tiles make 320 CTAs, two waves on the 296 resident slots for 1.08 waves of
+  // work (measured: K2b no faster at 8 ranks than at 4). A chunk of
+  // floor(296 / row tiles) column tiles runs K2b in one wave, so the batch is
+  // two such chunks (7,552 candidates instead of 8,192).
+  int64_t batch_cap() const {
+    if (!red_ || !loop_shard_ || nranks_ < 2 || field_ != Field::kAntiHerm) return bmax_;
+    const int64_t mt = (max_slice_ + rg::BM - 1) / rg::BM;  // identical on every rank
+    constexpr int64_t kSlots = 2 * 148;  // two CTAs of the projection GEMMs per SM
+    if (mt < 1 || mt > 8 || mt * 64 <= kSlots) return bmax_;
+    const int64_t chunk = kSlots / mt * rg::BN;
+    return chunk >= 2048 ? std::min<int64_t>(bmax_, 2 * chunk) : bmax_;
+  }
   int shard_chunks(int64_t n, int count, int64_t len, const int* before) const {
     if (!red_ || !loop_shard_ || n == 0 || len == 0 || before) return 1;
     const char* e = std::getenv("LIECL_B200_SHARD_CHUNKS");
     if (e) return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({std::atoi(e), kMaxShardChunks, count / 2048})));
     if (nranks_ < 2) return 1;
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(2, count / 4096)));
+    return count >= std::min<int64_t>(8192, batch_cap()) ? 2 : 1;
   }
   void project_pipelined(const double* Vb, const double* Vwb, int64_t n, const double* X, int count, double* Rout,
                          double* rn, int64_t off, int64_t len, int64_t ldp, int nch) {
@@ -855,7 +878,7 @@ private:
     const uint64_t before = st_.accepted;
     run_pair_batch(g, static_cast<int>(cnt));
     const uint64_t acc = st_.accepted - before;
-    if (acc == 0) B_cur_ = std::min<int64_t>(2 * B_cur_, bmax_);
+    if (acc == 0) B_cur_ = std::min<int64_t>(2 * B_cur_, batch_cap());
     else if (acc * 4 > static_cast<uint64_t>(cnt))  // floor 64, never above the cap the buffers are sized for
       B_cur_ = std::max<int64_t>(std::min<int64_t>(64, bmax_), B_cur_ / 2);
   }
@@ -1327,7 +1350,7 @@ private:
   bool complete_ = false;
   std::unique_ptr<Reducer> red_;  // set: D-sharded (D_ is this rank's slice, or loop_shard_)
   bool loop_shard_ = false;       // D-sharded closure loop: whole operators, GEMMs on [lo_, hi_)
-  int64_t lo_ = 0, hi_ = 0;
+  int64_t lo_ = 0, hi_ = 0, max_slice_ = 0;
   int nranks_ = 1;
   DevBuf<double> guard_;
   Field field_ = Field::kUnset;
