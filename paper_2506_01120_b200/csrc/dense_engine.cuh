@@ -169,9 +169,10 @@ public:
   // overlaps and squared residual norms are summed over ranks by `red` -- the
   // only data that crosses GPUs besides one all-reduce per accepted vector
   // (each rank contributes its slice of the new basis vector, the sum rebuilds
-  // it everywhere). Slice bounds are multiples of 2(d+1) elements: even (16-byte
-  // aligned packed rows) and aligned to the diagonal period of the packed
-  // weights, so the GEMM epilogues weight a slice exactly as the whole vector.
+  // it everywhere). Slice bounds are even (16-byte aligned packed rows) and,
+  // where the slices are wide enough, multiples of the GEMM row tile
+  // (loop_shard_range); K2b's epilogue weights a slice like the whole vector
+  // from the slice's first index mod (d + 1).
   void set_loop_shards(int nranks, int rank, std::unique_ptr<Reducer> red) {
     if (n_o_ != 0 || field_ != Field::kUnset || vcap_ != 0 || red_)
       throw Error(LIECL_B200_INVALID_INPUT, "set_shards needs a fresh session (before set_basis / check_candidates)");
@@ -187,14 +188,18 @@ public:
     loop_shard_ = true;
     nranks_ = nranks;
   }
+  // Slice bounds: the multiple of `unit` nearest to D r / P. unit = 128 packed
+  // elements (a row tile of the K2b GEMM, so no rank pays for a mostly empty
+  // tile: 8 ranks at d = 64 hold 512 elements = 4 tiles each) when every rank
+  // gets at least two of them, else 2 (16-byte aligned rows). The weighted
+  // norm in K2b's epilogue takes the slice's first index mod (d + 1), so the
+  // bounds need not follow the diagonal period of the packed weights.
   static void loop_shard_range(int64_t D, int d, int nranks, int rank, int64_t& lo, int64_t& hi) {
-    const int64_t unit = 2 * (static_cast<int64_t>(d) + 1);
+    (void)d;
+    const int64_t unit = D / nranks >= 2 * rg::BM ? rg::BM : 2;
     auto bound = [&](int r) {
       if (r <= 0) return int64_t(0);
       if (r >= nranks) return D;
-      // the multiple of `unit` nearest to D r / P: the largest slice is at most
-      // half a unit above D / P (rounding down instead left the last rank with
-      // up to a whole extra unit per earlier rank: 586 of 4096 elements at P = 8)
       return std::min(D / unit * unit, (2 * D * r + nranks * unit) / (2 * nranks * unit) * unit);
     };
     lo = bound(rank);
@@ -740,7 +745,7 @@ private:
       CU(cudaStreamWaitEvent(ctx_->stream, ev_red_[c], 0));
       rgemm_subtract(ctx_, Vb + off, n, len, P_.p + c0 * ldp, ldp, X + off + static_cast<int64_t>(c0) * D_, cc,
                      Rout + off + static_cast<int64_t>(c0) * D_, partial_.p + static_cast<int64_t>(c0) * mt, d_, D_,
-                     D_);
+                     D_, nullptr, 0, static_cast<int>(off % (d_ + 1)));
       norm_finalize_kernel<<<(cc + 255) / 256, 256, 0, ctx_->stream>>>(partial_.p + static_cast<int64_t>(c0) * mt,
                                                                         mt, cc, 0.0, rn + c0);
       launched(ctx_);
@@ -780,7 +785,7 @@ private:
       if (len > 0) {
         const bool vt = Vb == V_.p && off == 0 && ensure_vt(n, count);
         rgemm_subtract(ctx_, Vb + off, n, len, P_.p, ldp, X + off, count, Rout + off, partial_.p, d_, D_, D_,
-                       vt ? VT_.p : nullptr, ldvt_);
+                       vt ? VT_.p : nullptr, ldvt_, static_cast<int>(off % (d_ + 1)));
         mtiles = static_cast<int>((len + rg::BM - 1) / rg::BM);
       }
     } else {

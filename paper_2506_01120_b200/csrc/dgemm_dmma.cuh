@@ -36,7 +36,9 @@ template <bool KC> constexpr int a_elems() { return KC ? A_KC : A_MC; }
 template <bool KC> constexpr int smem_bytes() { return STAGES * (a_elems<KC>() + B_KC) * 8; }
 } // namespace rg
 
-// weight of packed element k of a d x d matrix: 1 on the diagonal, 2 elsewhere
+// weight of packed element k of a d x d matrix: 1 on the diagonal, 2 elsewhere.
+// Kernels working on a slice [lo, hi) of the packed vector pass k = local row +
+// wofs, wofs = lo mod (d + 1).
 __device__ __forceinline__ double packed_weight(int64_t k, int d) {
   return (k % (d + 1)) == 0 ? 1.0 : 2.0;
 }
@@ -53,7 +55,8 @@ template <bool A_KCONTIG, REpi EPI>
 __global__ void __launch_bounds__(rg::THREADS, 2)
 dgemm_dmma_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
                   int64_t ldb, double* __restrict__ Cout, int64_t ldc, double alpha, const double* __restrict__ X,
-                  int64_t ldx, double* __restrict__ partial, int dim, int k_chunk, int64_t split_stride) {
+                  int64_t ldx, double* __restrict__ partial, int dim, int k_chunk, int64_t split_stride,
+                  int wofs = 0) {
   using namespace rg;
   extern __shared__ __align__(16) double rsm[];
   double* As = rsm;
@@ -205,7 +208,7 @@ dgemm_dmma_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda
     for (int i = 0; i < MT; ++i) {
       const int gm = m0 + wm * WTM + i * 8 + g;
       if (gm >= M) continue;
-      const double w = packed_weight(gm, dim);
+      const double w = packed_weight(gm + wofs, dim);
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll
@@ -255,7 +258,8 @@ __global__ void rsplitk_reduce_scale_kernel(const double* __restrict__ ws, int s
 // one CTA of rg::BM threads per (row tile, column); partial layout as the GEMM's
 __global__ void rsplitk_reduce_subtract_kernel(const double* __restrict__ ws, int slices, int64_t stride, int M,
                                                int N, const double* __restrict__ X, double* __restrict__ R,
-                                               double* __restrict__ partial, int dim, int64_t ldx) {
+                                               double* __restrict__ partial, int dim, int64_t ldx,
+                                               int wofs = 0) {
   __shared__ double red[rg::BM / 32];
   const int mt = blockIdx.x, b = blockIdx.y;
   const int m = mt * rg::BM + threadIdx.x;
@@ -267,7 +271,7 @@ __global__ void rsplitk_reduce_subtract_kernel(const double* __restrict__ ws, in
     for (int z = 0; z < slices; ++z) acc += ws[z * stride + i];
     const double r = X[ix] - acc;
     R[ix] = r;
-    s = packed_weight(m, dim) * r * r;
+    s = packed_weight(m + wofs, dim) * r * r;
   }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;

@@ -112,7 +112,7 @@ template <bool A_KCONTIG, REpi EPI, int MC_BOX = 5, int GROUP = rg::GROUP>
 __global__ void __launch_bounds__(tg::THREADS, 2)
 dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                  int K, double* __restrict__ Cout, int64_t ldc, double alpha, const double* __restrict__ X,
-                 int64_t ldx, double* __restrict__ partial, int dim) {
+                 int64_t ldx, double* __restrict__ partial, int dim, int wofs = 0) {
   using namespace tg;
   extern __shared__ __align__(16) unsigned char tsm_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -227,7 +227,7 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     for (int i = 0; i < MT; ++i) {
       const int gm = m0 + wm * WTM + i * 8 + g;
       if (gm >= M) continue;
-      const double w = packed_weight(gm, dim);
+      const double w = packed_weight(gm + wofs, dim);  // wofs: the slice's first packed index mod (d + 1)
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll

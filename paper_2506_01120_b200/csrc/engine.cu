@@ -521,7 +521,7 @@ void rgemm_mc_store(liecl_b200_ctx* ctx, const double* A, int64_t lda, int64_t M
 // fragment loads through the 2-D TMA box)
 void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, const double* P, int64_t ldp,
                     const double* X, int count, double* R, double* partial, int d, int64_t ldv = -1,
-                    int64_t ldx = -1, const double* VT = nullptr, int64_t ldvt = 0) {
+                    int64_t ldx = -1, const double* VT = nullptr, int64_t ldvt = 0, int wofs = 0) {
   if (ldv < 0) ldv = D;
   if (ldx < 0) ldx = D;  // X and R
   rgemm_attr_once<false, REpi::kSubtractNorm>();
@@ -535,7 +535,7 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
     func_attr_once(dgemm_tma_kernel<true, REpi::kSubtractNorm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                    tg::SMEM);
     dgemm_tma_kernel<true, REpi::kSubtractNorm><<<grid, tg::THREADS, tg::SMEM, ctx->stream>>>(
-        ma, mb, static_cast<int>(D), count, static_cast<int>(n), R, ldx, 1.0, X, ldx, partial, d);
+        ma, mb, static_cast<int>(D), count, static_cast<int>(n), R, ldx, 1.0, X, ldx, partial, d, wofs);
     launched(ctx);
   } else if (slices <= 1 && tma_enabled() && tma_map_mc(&ma, V, D, n, ldv) &&
              tma_map_kc(&mb, P, n, count, ldp, tg::BN)) {
@@ -543,11 +543,11 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
     func_attr_once(dgemm_tma_kernel<false, REpi::kSubtractNorm, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                    tg::SMEM);
     dgemm_tma_kernel<false, REpi::kSubtractNorm, 3><<<grid, tg::THREADS, tg::SMEM, ctx->stream>>>(
-        ma, mb, static_cast<int>(D), count, static_cast<int>(n), R, ldx, 1.0, X, ldx, partial, d);
+        ma, mb, static_cast<int>(D), count, static_cast<int>(n), R, ldx, 1.0, X, ldx, partial, d, wofs);
     launched(ctx);
   } else if (slices <= 1) {
     dgemm_dmma_kernel<false, REpi::kSubtractNorm><<<grid, rg::THREADS, rg::smem_bytes<false>(), ctx->stream>>>(
-        static_cast<int>(D), count, static_cast<int>(kpad), V, ldv, P, ldp, R, ldx, 1.0, X, ldx, partial, d, 0, 0);
+        static_cast<int>(D), count, static_cast<int>(kpad), V, ldv, P, ldp, R, ldx, 1.0, X, ldx, partial, d, 0, 0, wofs);
     launched(ctx);
   } else {
     rgemm_attr_once<false, REpi::kStoreScaled>();
@@ -563,7 +563,7 @@ void rgemm_subtract(liecl_b200_ctx* ctx, const double* V, int64_t n, int64_t D, 
     launched(ctx);
     rsplitk_reduce_subtract_kernel<<<dim3(static_cast<unsigned>((D + rg::BM - 1) / rg::BM), count), rg::BM, 0,
                                      ctx->stream>>>(ws, slices, stride, static_cast<int>(D), count, X, R, partial, d,
-                                                    ldx);
+                                                    ldx, wofs);
     launched(ctx);
   }
   t.stop();

@@ -1080,7 +1080,8 @@ def shard_range(d: int, nranks: int, rank: int) -> tuple[int, int]:
 
 def loop_shard_range(d: int, nranks: int, rank: int) -> tuple[int, int]:
     """Elements [lo, hi) whose projections rank `rank` of a D-sharded closure
-    loop computes (multiples of 2(d+1); liecl_b200_loop_shard_range)."""
+    loop computes (even bounds, on the GEMMs' 128-row tiles when the slices are wide
+    enough; liecl_b200_loop_shard_range)."""
     lo, hi = C.c_int64(), C.c_int64()
     _check(native.load().liecl_b200_loop_shard_range(C.c_int32(d), C.c_int32(nranks), C.c_int32(rank), C.byref(lo),
                                                      C.byref(hi)))

@@ -29,14 +29,19 @@ def test_sums_unsorted_or_duplicate_terms_rejected():
 
 
 def test_sums_qubit_limits_and_masks():
-    # 32..63 qubits run on wide keys (max_dim = 0: no cap, unlike the
-    # reference's overflowing d^2 default); 64 is refused
-    r = liecl.closure_pauli_sums_arrays(np.array([0, 2], np.int64), np.array([1, 2], np.uint64),
-                                        np.array([0, 0], np.uint64), np.ones((2, 2)), 32)
-    assert r.dimension == 1
+    # 32..64 qubits run on wide keys (max_dim = 0: no cap, unlike the
+    # reference's overflowing d^2 default); 65 is refused, and on 64 only the
+    # string Y^64 (tests/test_gpu_pauli64.py)
+    for q in (32, 64):
+        r = liecl.closure_pauli_sums_arrays(np.array([0, 2], np.int64), np.array([1, 2], np.uint64),
+                                            np.array([0, 0], np.uint64), np.ones((2, 2)), q)
+        assert r.dimension == 1
     with pytest.raises(liecl.InvalidInputError):
         liecl.closure_pauli_sums_arrays(np.array([0, 2], np.int64), np.array([1, 2], np.uint64),
-                                        np.array([0, 0], np.uint64), np.ones((2, 2)), 64)
+                                        np.array([0, 0], np.uint64), np.ones((2, 2)), 65)
+    with pytest.raises(liecl.InvalidInputError, match="exceeds"):  # wide keys check their masks too
+        liecl.closure_pauli_sums_arrays(np.array([0, 2], np.int64), np.array([1, 1 << 50], np.uint64),
+                                        np.array([0, 0], np.uint64), np.ones((2, 2)), 40)
     with pytest.raises(liecl.InvalidInputError, match="exceeds"):
         liecl.closure_pauli_sums_arrays(np.array([0, 2], np.int64), np.array([1, 8], np.uint64),
                                         np.array([0, 0], np.uint64), np.ones((2, 2)), 2)
