@@ -351,6 +351,132 @@ commutator_ah_kernel(const double* __restrict__ basis, int64_t g0, int count, do
   ah_finish<DIM, NT, S::WARPS_PER_PAIR>(red, hv, j, tip, tol, normalize, out, hnorm, is_null);
 }
 
+// K1 of a D-sharded rank ("GPU p computes only the columns
+// J_p of h"): packed columns [8 tc0, 8 tc1) of h = P - P^dagger, i.e. packed
+// elements [64 * 8 tc0, 64 * 8 tc1) at d = 64. They need P's tile columns
+// [tc0, tc1) and tile rows [tc0, tc1) only: 8w + w(8 - w) of the 64 tiles for
+// w = tc1 - tc0 (15 at eight ranks). Tiles go round-robin over the eight
+// warps, up to six per warp, each accumulating in the engine kernel's order
+// (re: ar br, then -ai bi; im: ar bi, then ai br), so the unnormalised slice
+// has the bits of the whole-operator kernel. Writes the UNNORMALISED slice
+// and this rank's part of sum w h^2; the norm is a sum over ranks
+// (commutator_ah_cols_finish_kernel).
+template <int DIM>
+__global__ void __launch_bounds__(256, 2)
+commutator_ah_cols_kernel(const double* __restrict__ basis, int64_t g0, int count, int tc0, int tc1,
+                          double* __restrict__ out, double* __restrict__ sumsq_out) {
+  static_assert(DIM == 64, "tile bookkeeping below is for 8 x 8 tiles");
+  using S = CommAhShape<DIM, 2, 4>;
+  constexpr int D2 = DIM * DIM, LDP = S::LDP, NT = 256, TR = 8, MAXT = 6;
+  extern __shared__ __align__(16) double csm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int j = blockIdx.x, tip = threadIdx.x;
+  if (j >= count) return;
+  double* pa = csm;
+  double* pb = pa + S::PACKED;
+  double* red = pb + S::PACKED;
+  const int w = tc1 - tc0, ntile = TR * w + w * (TR - w);
+  auto tile_of = [&](int idx, int& r, int& c) {
+    if (idx < TR * w) {  // the tile columns of the slice
+      r = idx % TR;
+      c = tc0 + idx / TR;
+    } else {  // the rest of its tile rows
+      const int u = idx - TR * w, cc = u % (TR - w);
+      r = tc0 + u / (TR - w);
+      c = cc < tc0 ? cc : cc + w;
+    }
+  };
+  ah_load_pair<DIM, LDP, NT, true>(basis, g0 + j, pa, pb, tip);
+  __syncthreads();
+  double cre[MAXT][2], cim[MAXT][2];
+#pragma unroll
+  for (int q = 0; q < MAXT; ++q) cre[q][0] = cre[q][1] = cim[q][0] = cim[q][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < MAXT; q += 2) {  // two tiles at a time: independent accumulators
+    const int i0 = warp + 8 * q, i1 = warp + 8 * (q + 1);
+    if (i0 >= ntile) break;
+    int r0, c0, r1 = 0, c1 = 0;
+    tile_of(i0, r0, c0);
+    const bool two = i1 < ntile;
+    if (two) tile_of(i1, r1, c1);
+    for (int k0 = 0; k0 < DIM; k0 += 4) {
+      const int k = k0 + t;
+      double ar, ai, br, bi;
+      ah_elem<LDP>(pa, r0 * 8 + g, k, ar, ai);
+      ah_elem<LDP>(pb, k, c0 * 8 + g, br, bi);
+      dmma_8x8x4(cre[q][0], cre[q][1], ar, br);
+      dmma_8x8x4(cim[q][0], cim[q][1], ar, bi);
+      dmma_8x8x4(cre[q][0], cre[q][1], -ai, bi);
+      dmma_8x8x4(cim[q][0], cim[q][1], ai, br);
+      if (two) {
+        ah_elem<LDP>(pa, r1 * 8 + g, k, ar, ai);
+        ah_elem<LDP>(pb, k, c1 * 8 + g, br, bi);
+        dmma_8x8x4(cre[q + 1][0], cre[q + 1][1], ar, br);
+        dmma_8x8x4(cim[q + 1][0], cim[q + 1][1], ar, bi);
+        dmma_8x8x4(cre[q + 1][0], cre[q + 1][1], -ai, bi);
+        dmma_8x8x4(cim[q + 1][0], cim[q + 1][1], ai, br);
+      }
+    }
+  }
+  __syncthreads();  // inputs consumed: the P planes reuse the packed buffers
+#pragma unroll
+  for (int q = 0; q < MAXT; ++q) {
+    const int idx = warp + 8 * q;
+    if (idx < ntile) {
+      int r, c;
+      tile_of(idx, r, c);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        pa[p_at<DIM>(r * 8 + g, c * 8 + 2 * t + h)] = cre[q][h];
+        pb[p_at<DIM>(r * 8 + g, c * 8 + 2 * t + h)] = cim[q][h];
+      }
+    }
+  }
+  __syncthreads();
+  // packed elements of columns [8 tc0, 8 tc1): e = i + k * DIM
+  const int e0 = tc0 * 8 * DIM, ne = w * 8 * DIM;
+  double sumsq = 0.0;
+  double* o = out + static_cast<int64_t>(j) * D2 + e0;
+  for (int x = tip; x < ne; x += NT) {
+    const int e = e0 + x, i = e % DIM, k = e / DIM;
+    double v;
+    if (i < k) v = pa[p_at<DIM>(i, k)] - pa[p_at<DIM>(k, i)];
+    else if (i > k) v = pb[p_at<DIM>(k, i)] + pb[p_at<DIM>(i, k)];
+    else v = 2.0 * pb[p_at<DIM>(i, i)];
+    o[x] = v;
+    sumsq += (i == k ? 1.0 : 2.0) * v * v;
+  }
+  sumsq = warp_sum(sumsq);
+  if (lane == 0) red[warp] = sumsq;
+  __syncthreads();
+  if (tip == 0) {
+    double total = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) total += red[q];
+    sumsq_out[j] = total;
+  }
+}
+
+// After the sum of sumsq over ranks: ||h||, the null flag, and the slice
+// [e0, e0 + ne) of every bracket scaled by 1/||h|| (null: zeros), as the
+// whole-operator kernel's epilogue does.
+__global__ void commutator_ah_cols_finish_kernel(const double* __restrict__ sumsq, int d, double tol, int64_t e0,
+                                                 int64_t ne, double* __restrict__ out, double* __restrict__ hnorm,
+                                                 int* __restrict__ is_null) {
+  const int j = blockIdx.y;
+  const double hn = sqrt(sumsq[j]) / sqrt(static_cast<double>(d));
+  const bool nul = !(hn > tol);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    hnorm[j] = hn;
+    is_null[j] = nul ? 1 : 0;
+  }
+  const double sc = nul ? 0.0 : 1.0 / hn;
+  double* o = out + static_cast<int64_t>(j) * d * d + e0;
+  for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < ne;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    o[x] *= sc;
+}
+
 // packed path, any even d: one CTA per pair, operands through L1/L2
 __global__ void __launch_bounds__(256)
 commutator_ah_generic_kernel(const double* __restrict__ basis, int dim, int64_t g0, int count, double tol,

@@ -179,10 +179,12 @@ public:
     if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(LIECL_B200_INVALID_INPUT, "bad shard rank / count");
     loop_shard_range(D_, d_, nranks, rank, lo_, hi_);
     max_slice_ = 0;  // the widest slice of any rank: batch sizes derived from it agree on every rank
+    tile_col_slices_ = true;  // every rank's slice is 1..4 whole tile columns of a 64 x 64 product
     for (int r = 0; r < nranks; ++r) {
       int64_t a, b;
       loop_shard_range(D_, d_, nranks, r, a, b);
       max_slice_ = std::max(max_slice_, b - a);
+      if (b <= a || a % 512 != 0 || b % 512 != 0 || b - a > 2048) tile_col_slices_ = false;
     }
     red_ = std::move(red);
     loop_shard_ = true;
@@ -820,7 +822,10 @@ private:
       case 8: launch_comm_ah<8>(basis, g0, cnt); return;
       case 16: launch_comm_ah<16>(basis, g0, cnt); return;
       case 32: launch_comm_ah<32>(basis, g0, cnt); return;
-      case 64: launch_comm_ah<64>(basis, g0, cnt); return;
+      case 64:
+        if (shard_commutator()) launch_comm_ah_cols(basis, g0, cnt);
+        else launch_comm_ah<64>(basis, g0, cnt);
+        return;
       default: {
         if (use_large_commutator(d_)) {
           commutator_large(ctx_, basis, true, d_, g0, cnt, tol_, C_.p, hn_.p, nul_.p);
@@ -862,6 +867,40 @@ private:
                                                                          hn_.p, nul_.p);
     launched(ctx_);
     t.stop();
+  }
+  // D-sharded loop, packed d = 64, slices on P's tile columns (512 packed
+  // elements): a rank forms only its slice of every bracket -- the tile
+  // columns and rows of P the slice touches (15 of 64 tiles at eight ranks) --
+  // and the brackets' norms are summed over ranks (8 bytes per bracket).
+  // Alg. 4 only: Alg. 3 appends whole brackets to the commutator basis.
+  // LIECL_B200_SHARD_COMM=0 keeps the whole-operator kernel on every rank.
+  bool shard_commutator() const {
+    static const bool enabled = [] {
+      const char* e = std::getenv("LIECL_B200_SHARD_COMM");
+      return !(e && e[0] == '0');
+    }();
+    // tile_col_slices_ looks at every rank's bounds: all ranks take the same branch
+    return enabled && red_ && loop_shard_ && nranks_ > 1 && !keep_ && d_ == 64 && tile_col_slices_;
+  }
+  void launch_comm_ah_cols(const double* basis, int64_t g0, int cnt) {
+    using SA = CommAhShape<64, 2, 4>;
+    func_attr_once(commutator_ah_cols_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, SA::SMEM);
+    func_attr_once(commutator_ah_cols_kernel<64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    const int tc0 = static_cast<int>(lo_ / 512), tc1 = static_cast<int>(hi_ / 512), w = tc1 - tc0;
+    const int ntile = 8 * w + w * (8 - w);
+    comm_sumsq_.ensure(static_cast<size_t>(bmax_));
+    {
+      Timer t(ctx_, 2, 8.0 * 64 * 64 * 64.0 * cnt * ntile / 64.0);
+      commutator_ah_cols_kernel<64><<<cnt, 256, SA::SMEM, ctx_->stream>>>(basis, g0, cnt, tc0, tc1, C_.p,
+                                                                         comm_sumsq_.p);
+      launched(ctx_);
+      t.stop();
+    }
+    red_->sum(comm_sumsq_.p, cnt, ctx_->stream);  // ||h||^2 over the ranks' column slices
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((hi_ - lo_ + 255) / 256, 8)), cnt);
+    commutator_ah_cols_finish_kernel<<<grid, 256, 0, ctx_->stream>>>(comm_sumsq_.p, d_, tol_, lo_, hi_ - lo_, C_.p,
+                                                                     hn_.p, nul_.p);
+    launched(ctx_);
   }
   template <int DIM> void launch_comm_ah(const double* basis, int64_t g0, int cnt) {
     using SA = CommAhShape<DIM>;
@@ -1356,6 +1395,8 @@ private:
   std::unique_ptr<Reducer> red_;  // set: D-sharded (D_ is this rank's slice, or loop_shard_)
   bool loop_shard_ = false;       // D-sharded closure loop: whole operators, GEMMs on [lo_, hi_)
   int64_t lo_ = 0, hi_ = 0, max_slice_ = 0;
+  bool tile_col_slices_ = false;
+  DevBuf<double> comm_sumsq_;  // D-sharded K1: per-bracket partial squared norms
   int nranks_ = 1;
   DevBuf<double> guard_;
   Field field_ = Field::kUnset;
