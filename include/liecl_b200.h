@@ -445,7 +445,9 @@ int liecl_b200_check_matrix_inversion_dense(liecl_b200_ctx* ctx, const double* b
  * GPU; only per-candidate partial overlap sums are all-reduced"): on a fresh
  * session, rank r of P keeps WHOLE operators (set_basis / run_closure take
  * full operators, get_basis returns them) and computes every commutator, null
- * test and normalisation itself; the projection GEMMs run on elements [lo, hi)
+ * test and normalisation itself (at d = 64 on 2, 4 or 8 ranks, dimonly method:
+ * only its own columns of every bracket, the brackets' norms summed over
+ * ranks); the projection GEMMs run on elements [lo, hi)
  * = liecl_b200_loop_shard_range(d, P, r) only, and the partial overlaps beta,
  * the partial squared residual norms and each accepted vector's slices are
  * summed over ranks (NCCL via nccl_id, or the host callback as in set_shards).
