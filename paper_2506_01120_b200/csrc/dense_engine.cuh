@@ -872,7 +872,8 @@ private:
   // elements): a rank forms only its slice of every bracket -- the tile
   // columns and rows of P the slice touches (15 of 64 tiles at eight ranks) --
   // and the brackets' norms are summed over ranks (8 bytes per bracket).
-  // Alg. 4 only: Alg. 3 appends whole brackets to the commutator basis.
+  // Alg. 3 appends accepted brackets to the commutator basis: their slices are
+  // summed into whole operators like the accepted residuals'.
   // LIECL_B200_SHARD_COMM=0 keeps the whole-operator kernel on every rank.
   bool shard_commutator() const {
     static const bool enabled = [] {
@@ -880,7 +881,8 @@ private:
       return !(e && e[0] == '0');
     }();
     // tile_col_slices_ looks at every rank's bounds: all ranks take the same branch
-    return enabled && red_ && loop_shard_ && nranks_ > 1 && !keep_ && d_ == 64 && tile_col_slices_;
+    return enabled && red_ && loop_shard_ && nranks_ > 1 && d_ == 64 && tile_col_slices_ &&
+           field_ == Field::kAntiHerm;
   }
   void launch_comm_ah_cols(const double* basis, int64_t g0, int cnt) {
     using SA = CommAhShape<64, 2, 4>;
@@ -1106,6 +1108,7 @@ private:
       if (loop_shard_) {  // only this rank's slice of the residual is valid: rebuild the vector over ranks
         gather_slices(vp(V_, n_o_));
         if (field_ == Field::kAntiHerm) gather_slices(vp(Vw_, n_o_));
+        if (keep_ && shard_commutator()) gather_slices(vp(O_, n_b_));  // the bracket itself was formed in column slices
       }
       ++n_o_;
       if (keep_) ++n_b_;
@@ -1262,6 +1265,11 @@ private:
         dim3 gg(static_cast<unsigned>(std::min<int64_t>((W + 255) / 256, 64)), a);
         gather_words_kernel<<<gg, 256, 0, ctx_->stream>>>(C_.p, bc_idx_.p, W, O_.p + n_b_ * W);
         launched(ctx_); dbg_sync("block_chol 9");
+        if (shard_commutator()) {  // column-sharded brackets: rebuild the whole originals everywhere
+          bc_zero_outside_kernel<<<grid_for(a * W), 256, 0, ctx_->stream>>>(O_.p + n_b_ * W, a, W, lo * sc, hi * sc);
+          launched(ctx_);
+          red_->sum(O_.p + n_b_ * W, a * W, ctx_->stream);
+        }
       }
       if (nt > 0) {  // tentative rejects: explicit CGS2 against the accepts before each
         dim3 gg(static_cast<unsigned>(std::min<int64_t>((W + 255) / 256, 64)), nt);

@@ -247,19 +247,22 @@ def test_sharded_commutator_columns(P, monkeypatch):
 
 
 @pytest.mark.slow
-def test_sharded_commutator_columns_growth_phase(golden):
+@pytest.mark.parametrize("method", ["orthonorm-dimonly", "orthonorm"])
+def test_sharded_commutator_columns_growth_phase(golden, method):
     """Config 2's growth phase (all 4092 loop accepts) on P = 4 ranks with
-    column-sharded brackets: the reference's accept sequence, the basis of the
-    single-GPU run to 1e-12."""
-    meta, g = golden("c2_random_sums_n6_s0_orthonorm-dimonly_rows100")
+    column-sharded brackets, Alg. 4 and Alg. 3 (the accepted brackets' slices
+    are summed into whole originals): the reference's accept sequence, the
+    basis of the single-GPU run to 1e-11."""
+    meta, g = golden(f"c2_random_sums_n6_s0_{method}_rows100")
     cfg = w.config2()
+    keep = method == "orthonorm"
 
     def job(s):
         ind, rn, _ = s.check_candidates(cfg.generators)
         s.run_rows(1, meta["rows"])
         return ind, s.log(), s.size(), s.basis()
-    out, _ = run_threads(4, 64, job)
-    one = liecl.ClosureSession(64, config=liecl.ClosureConfig(tolerance=cfg.tol, record_log=True))
+    out, _ = run_threads(4, 64, job, keep=keep)
+    one = liecl.ClosureSession(64, keep_original=keep, config=liecl.ClosureConfig(tolerance=cfg.tol, record_log=True))
     one.check_candidates(cfg.generators)
     one.run_rows(1, meta["rows"])
     B1 = one.basis()
