@@ -30,6 +30,8 @@ public:
     // at d >= 2048 (D = 4M..16.7M elements) fewer than 64 candidates fit the budget
     bmax_ = cfg.batch_max > 0 ? cfg.batch_max
                               : std::clamp<int64_t>(budget / (3 * D_ * 16), D_ > (int64_t(1) << 20) ? 8 : 64, 8192);
+    explicit_batch_ = cfg.batch_max > 0;
+    bmax_default_ = bmax_;
     set_deadline(cfg);
     sqrt_d_ = std::sqrt(static_cast<double>(d));
     B_cur_ = std::min<int64_t>(bmax_, 512);
@@ -189,6 +191,26 @@ public:
     red_ = std::move(red);
     loop_shard_ = true;
     nranks_ = nranks;
+    // Saturated batches sized to the GPU (packed field): K2b's grid is (row
+    // tiles of the slice) x (column tiles of the chunk); a chunk of
+    // slots / gcd(slots, row tiles) column tiles fills whole waves of the
+    // resident CTA slots (148 SMs x 2: 37 column tiles at 2 or 4 ranks of
+    // d = 64, 74 at 8 ranks -- K2a's 32 x 37 grid is four exact waves too).
+    // Derived from the widest slice, so every rank takes the same batches.
+    wave_chunk_ = 0;
+    if (nranks > 1 && !explicit_batch_) {
+      int sms = 0, dev = 0;
+      CU(cudaGetDevice(&dev));
+      CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const int64_t slots = 2 * static_cast<int64_t>(sms);
+      const int64_t mtb = (max_slice_ + rg::BM - 1) / rg::BM;
+      const int64_t chunk = mtb > 0 ? slots / std::gcd(slots, mtb) * rg::BN : 0;
+      if (chunk >= 2048 && chunk <= 8192) {
+        wave_chunk_ = chunk;
+        wave_nch_ = static_cast<int>(std::clamp<int64_t>(8192 / chunk, 2, kMaxShardChunks));
+        bmax_ = std::max<int64_t>(bmax_, wave_nch_ * wave_chunk_);  // before any batch buffer exists
+      }
+    }
   }
   // Slice bounds: the multiple of `unit` nearest to D r / P. unit = 128 packed
   // elements (a row tile of the K2b GEMM, so no rank pays for a mostly empty
@@ -699,26 +721,19 @@ private:
   // 3.5 waves on 296 slots (measured 13 % slower at one rank), a 4,096 one
   // 6.9 waves. LIECL_B200_SHARD_CHUNKS forces a count (tests: one rank too).
   static constexpr int kMaxShardChunks = 4;
-  // Largest batch of the saturated phase. D-sharded packed loop with a narrow
-  // slice (8 ranks at d = 64: 520 elements = 5 row tiles of K2b): 64 column
-  // tiles make 320 CTAs, two waves on the 296 resident slots for 1.08 waves of
-  // work (measured: K2b no faster at 8 ranks than at 4). A chunk of
-  // floor(296 / row tiles) column tiles runs K2b in one wave, so the batch is
-  // two such chunks (7,552 candidates instead of 8,192).
+  // Largest batch of the saturated phase: whole waves of the projection GEMMs
+  // under D-sharding (set_loop_shards), else the batch buffers' size.
   int64_t batch_cap() const {
-    if (!red_ || !loop_shard_ || nranks_ < 2 || field_ != Field::kAntiHerm) return bmax_;
-    const int64_t mt = (max_slice_ + rg::BM - 1) / rg::BM;  // identical on every rank
-    constexpr int64_t kSlots = 2 * 148;  // two CTAs of the projection GEMMs per SM
-    if (mt < 1 || mt > 8 || mt * 64 <= kSlots) return bmax_;
-    const int64_t chunk = kSlots / mt * rg::BN;
-    return chunk >= 2048 ? std::min<int64_t>(bmax_, 2 * chunk) : bmax_;
+    if (wave_chunk_ > 0 && red_ && loop_shard_ && field_ == Field::kAntiHerm) return wave_nch_ * wave_chunk_;
+    return std::min<int64_t>(bmax_, bmax_default_);
   }
   int shard_chunks(int64_t n, int count, int64_t len, const int* before) const {
     if (!red_ || !loop_shard_ || n == 0 || len == 0 || before) return 1;
     const char* e = std::getenv("LIECL_B200_SHARD_CHUNKS");
     if (e) return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({std::atoi(e), kMaxShardChunks, count / 2048})));
     if (nranks_ < 2) return 1;
-    return count >= std::min<int64_t>(8192, batch_cap()) ? 2 : 1;
+    if (wave_chunk_ > 0 && field_ == Field::kAntiHerm) return count == batch_cap() ? wave_nch_ : 1;
+    return count >= 8192 ? 2 : 1;
   }
   void project_pipelined(const double* Vb, const double* Vwb, int64_t n, const double* X, int count, double* Rout,
                          double* rn, int64_t off, int64_t len, int64_t ldp, int nch) {
@@ -1404,6 +1419,9 @@ private:
   bool loop_shard_ = false;       // D-sharded closure loop: whole operators, GEMMs on [lo_, hi_)
   int64_t lo_ = 0, hi_ = 0, max_slice_ = 0;
   bool tile_col_slices_ = false;
+  int64_t wave_chunk_ = 0, bmax_default_ = 0;  // D-sharded wave-sized chunks; the cap without them
+  int wave_nch_ = 1;
+  bool explicit_batch_ = false;
   DevBuf<double> comm_sumsq_;  // D-sharded K1: per-bracket partial squared norms
   int nranks_ = 1;
   DevBuf<double> guard_;
