@@ -31,6 +31,23 @@ public:
     bmax_ = cfg.batch_max > 0 ? cfg.batch_max
                               : std::clamp<int64_t>(budget / (3 * D_ * 16), D_ > (int64_t(1) << 20) ? 8 : 64, 8192);
     explicit_batch_ = cfg.batch_max > 0;
+    if (!explicit_batch_ && bmax_ == 8192) {
+      // the saturated phase's GEMM grids are (row tiles) x (column tiles of the
+      // batch): a multiple of slots / gcd(slots, row tiles) column tiles runs
+      // whole waves on the resident CTA slots (148 SMs x 2 = 296: 37 column
+      // tiles; 4 x 37 x 64 = 9,472 candidates are sixteen exact waves of the
+      // 32 x 148 grid at d = 64, where 8,192 were 13.8). Measured on 8-row
+      // windows: 493.9k -> 505.2k brackets/s (tools/probe/batch_ab.py).
+      int sms = 0, dev = 0;
+      if (cudaGetDevice(&dev) == cudaSuccess &&
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0) {
+        const int64_t slots = 2 * static_cast<int64_t>(sms);
+        const int64_t mtb = (D_ + rg::BM - 1) / rg::BM;
+        const int64_t chunk = slots / std::gcd(slots, mtb) * rg::BN;
+        const int64_t k = (8192 + chunk - 1) / chunk;
+        if (k * chunk <= 10240 && k * chunk * 3 * D_ * 16 <= budget) bmax_ = k * chunk;
+      }
+    }
     bmax_default_ = bmax_;
     set_deadline(cfg);
     sqrt_d_ = std::sqrt(static_cast<double>(d));
@@ -207,7 +224,7 @@ public:
       const int64_t chunk = mtb > 0 ? slots / std::gcd(slots, mtb) * rg::BN : 0;
       if (chunk >= 2048 && chunk <= 8192) {
         wave_chunk_ = chunk;
-        wave_nch_ = static_cast<int>(std::clamp<int64_t>(8192 / chunk, 2, kMaxShardChunks));
+        wave_nch_ = static_cast<int>(std::clamp<int64_t>(bmax_ / chunk, 2, kMaxShardChunks));
         bmax_ = std::max<int64_t>(bmax_, wave_nch_ * wave_chunk_);  // before any batch buffer exists
       }
     }

@@ -97,7 +97,7 @@ def main():
     cfg = w.config2()
     brackets = sum((ROW0 + k * ROWS + i) for k in range(STEPS) for i in range(ROWS))
     base = None
-    for P in (1, 2, 4, 8):
+    for P in [int(x) for x in os.environ.get("SHARD_RANKS", "1,2,4,8").split(",")]:
         res = run(P, cfg)
         assert all(r[3] == 0 for r in res)
         per = []
