@@ -160,23 +160,30 @@ scatter_kernel(const u64* __restrict__ kin, const unsigned* __restrict__ vin, in
 constexpr unsigned kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValueMask = (1u << 30) - 1;
 constexpr int kMaxPasses = 8;
 
-// ghist[p * 256 + d] += keys whose digit p is d (zeroed by the caller)
+// ghist[p * 256 + d] += keys whose digit p is d (zeroed by the caller).
+// Shared-memory atomics on a block histogram; a warp whose 32 keys share the
+// digit (the usual case for the high digits: segment bits of keys that arrive
+// grouped by segment, or constant upper bits) adds once instead of serialising
+// 32 ways on one word.
 __global__ void __launch_bounds__(kThreads) digit_totals_kernel(const u64* __restrict__ key, int64_t n, int end_bit,
                                                                 int passes, unsigned* __restrict__ ghist) {
   __shared__ unsigned s_hist[kMaxPasses * kBins];
   for (int e = threadIdx.x; e < passes * kBins; e += kThreads) s_hist[e] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  // whole warps per trip; equal digits within a warp add once (skewed digits
-  // would otherwise serialise on one shared-memory word)
   for (int64_t b = blockIdx.x * static_cast<int64_t>(kThreads); b < n; b += static_cast<int64_t>(gridDim.x) * kThreads) {
     const int64_t i = b + threadIdx.x;
-    const bool live = i < n;
+    const bool live = i < n;  // whole warps per trip: only the last warp of the array is ragged
     const u64 k = live ? low_bits(key[i], end_bit) : 0ull;
+    const bool full = __all_sync(0xffffffffu, live);
     for (int p = 0; p < passes; ++p) {
-      const unsigned d = live ? (static_cast<unsigned>(k >> (8 * p)) & 255u) : 0xffffffffu;
-      const unsigned same = __match_any_sync(0xffffffffu, d);
-      if (live && lane == __ffs(same) - 1) atomicAdd(&s_hist[p * kBins + d], static_cast<unsigned>(__popc(same)));
+      const unsigned d = static_cast<unsigned>(k >> (8 * p)) & 255u;
+      const unsigned d0 = __shfl_sync(0xffffffffu, d, 0);
+      if (full && __all_sync(0xffffffffu, d == d0)) {
+        if (lane == 0) atomicAdd(&s_hist[p * kBins + d0], 32u);
+      } else if (live) {
+        atomicAdd(&s_hist[p * kBins + d], 1u);
+      }
     }
   }
   __syncthreads();
