@@ -196,13 +196,44 @@ __global__ void run_sum_kernel(const K* __restrict__ ks, const unsigned* __restr
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (!flag[i]) continue;
     const K k = ks[i];
+    const int sgi = seg[i];
     C2 acc = pauli::slot(val[is[i]]);
-    for (int j = i + 1; j < n && keq(ks[j], k) && seg[j] == seg[i]; ++j) acc = cadd(acc, val[is[j]]);
+    // the run's terms are added in input order (from_terms' order); the loads
+    // of the next kAhead entries are issued together so a long run costs one
+    // memory latency per kAhead terms, not two per term (entries past the
+    // run's end are loaded and dropped: they are inside the arrays)
+    constexpr int kAhead = 8;
+    int j = i + 1;
+    // most runs are one term long: look at the next entry alone first
+    if (j < n && keq(ks[j], k) && seg[j] == sgi) acc = cadd(acc, val[is[j]]), ++j;
+    else j = n;
+    for (; j < n;) {
+      const int m = n - j < kAhead ? n - j : kAhead;
+      K kk[kAhead];
+      int sg[kAhead];
+      C2 vv[kAhead];
+#pragma unroll
+      for (int u = 0; u < kAhead; ++u)
+        if (u < m) {
+          kk[u] = ks[j + u];
+          sg[u] = seg[j + u];
+          vv[u] = val[is[j + u]];
+        }
+      int u = 0;
+#pragma unroll
+      for (int q = 0; q < kAhead; ++q)
+        if (u == q && q < m && keq(kk[q], k) && sg[q] == sgi) {
+          acc = cadd(acc, vv[q]);
+          ++u;
+        }
+      if (u < m) break;
+      j += m;
+    }
     const int r = pos[i];
     rkey[r] = k;
     rval[r] = acc;
     rmag[r] = hypot(acc.re, acc.im);
-    rseg[r] = seg[i];
+    rseg[r] = sgi;
   }
 }
 
